@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py — Speculative HeTM GPU-side path on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], per GPU): 1 GiB STMR shard (2^27 words),
+one 2^20-transaction bank batch per round (4 reads / 2 writes, uniform, on the
+GPU half of the shard), and the round's host write log (2^20 entries of
+<addr,value,ts>, uniform over the host halves of ALL shards) validated against
+the GPU read-set bitmap (1 KiB granules) with the TS-guarded apply.
+
+One step = one synchronization round of the device side:
+    executeBatch (bank kernel) -> [G>1: route log by owner shard + NCCL
+    all-to-all] -> validateChunk(apply) -> round clear.
+`value` = committed GPU tx/s over all ranks, device-timed with CUDA events,
+inputs resident in HBM (rotating per-step buffers; 1 GiB STMR >> L2).
+`e2e` = the same rounds through the C-ABI host-buffer calls: H2D batch input,
+H2D log stream, verdict, D2H tickets, mergeCommit D2H of dirty chunks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "committed GPU tx/s (synthetic bank) 1 B200; validate+apply GB/s at 1/2/4/8 GPUs"
+UNIT = "tx/s"
+TX_BYTES = 224     # 24 B input + 8 B ticket + 4x32 B STMR sector reads + 2x32 B write-backs
+ENTRY_BYTES = 120  # 24 B log + 32 B TS read + 32 B TS write + 32 B STMR sector write
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--words-log2", type=int, default=27)
+    p.add_argument("--batch", type=int, default=1 << 20)
+    p.add_argument("--log-entries", type=int, default=1 << 20)
+    p.add_argument("--gran", type=int, default=1024)
+    p.add_argument("--lock-entries", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--cpu-seconds", type=float, default=8.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown", "sync_boost",
+           "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+                act = int(parts[2], 16)
+            except (ValueError, IndexError):
+                continue
+            for i, name in enumerate(REASONS):
+                if act & (1 << i) and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return world, rank, local, pg
+
+
+def host_log_slice(hetm, seed, n_entries, world, W, rank, ts_base):
+    """This rank's 1/G of the global host log: uniform over the host halves
+    [s*W + W/2, (s+1)*W) of every shard s; 2 writes per host tx."""
+    n_tx = n_entries // 2
+    log = hetm.gen_host_log(seed, n_tx, 2, 8, 0, world * (W // 2), ts_base=ts_base)
+    v = log["addr"]
+    shard = v // np.uint64(W // 2)
+    log["addr"] = shard * np.uint64(W) + np.uint64(W // 2) + (v % np.uint64(W // 2))
+    return log
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_1905_00661_b200 as hetm
+
+    world, rank, local, dist = dist_setup(args)
+    torch.cuda.set_device(local)
+    W = 1 << args.words_log2
+    base = rank * W
+    B, L = args.batch, args.log_entries
+    K, WU = args.steps, args.warmup
+    n_steps = K + WU
+
+    dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, lock_entries=args.lock_entries,
+                         device=local, log_capacity=max(L, 1 << 20))
+    dev.register_kernel(hetm.KERNEL_BANK)
+    init = np.full(W, 1000, np.uint64)
+    dev.upload(hetm.REPLICA_DEV, base, init)
+    host_replica = hetm.PinnedArray((W,), np.uint64)
+    host_replica.array[:] = init
+    dev.merge_commit(host_replica.array)  # shadow == round start, host replica aligned
+    dev.merge_wait()
+    dev.clear_round()
+
+    # ---- rotating per-step inputs, resident in HBM (total > L2)
+    t_gen = time.time()
+    n_bufs = min(n_steps, 16)
+    tx_d, log_d = [], []
+    for j in range(n_bufs):
+        txs = hetm.gen_bank_batch(1000 + 7919 * rank + j, B, base, W // 2)
+        tx_d.append(torch.from_numpy(txs.view(np.uint8)).cuda())
+    base_log = host_log_slice(hetm, 77 + rank, L, world, W, rank, ts_base=0)
+    base_log_t = torch.from_numpy(base_log.view(np.uint64).reshape(-1, 3).astype(np.int64)).cuda()
+    for j in range(n_steps):
+        t = base_log_t.clone()
+        t[:, 2] += (j * world + rank) * (L // 2) + 1  # unique, monotone ts across ranks and steps
+        log_d.append(t)
+    tickets = torch.empty(B, dtype=torch.int64, device="cuda")
+    recv = torch.empty((max(L * 2, 1), 3), dtype=torch.int64, device="cuda") if world > 1 else None
+    routed = torch.empty_like(base_log_t) if world > 1 else None
+    counts = torch.zeros(world, dtype=torch.int64, device="cuda")
+    gen_s = time.time() - t_gen
+
+    s_exec = dev.stream_handle(0)
+    s_val = dev.stream_handle(2)
+    ex = torch.cuda.ExternalStream(s_exec)
+    vs = torch.cuda.ExternalStream(s_val)
+    ev = {k: [torch.cuda.Event(enable_timing=True) for _ in range(K)] for k in ["b0", "b1", "v0", "v1"]}
+
+    def step(j, timed_idx=None):
+        tb = tx_d[j % n_bufs]
+        if timed_idx is not None:
+            ev["b0"][timed_idx].record(ex)
+        dev.execute_batch_dptr(hetm.KERNEL_BANK, tb.data_ptr(), B, tickets.data_ptr(), s_exec)
+        if timed_idx is not None:
+            ev["b1"][timed_idx].record(ex)
+        lg = log_d[j]
+        n_local = L
+        src = lg
+        if world > 1:
+            with torch.cuda.stream(vs):
+                dev.route_log_dptr(lg.data_ptr(), L, world, W, routed.data_ptr(), counts.data_ptr(), s_val)
+                in_splits = counts.clone()
+                out_splits = torch.empty_like(in_splits)
+                dist.all_to_all_single(out_splits, in_splits)
+                ins, outs = in_splits.tolist(), out_splits.tolist()
+                n_local = sum(outs)
+                dist.all_to_all_single(recv[:n_local], routed, outs, ins)
+                src = recv
+        if timed_idx is not None:
+            ev["v0"][timed_idx].record(vs)
+        dev.validate_dptr(src.data_ptr(), n_local, hetm.APPLY, s_val)
+        if timed_idx is not None:
+            ev["v1"][timed_idx].record(vs)
+        dev.clear_round(asynchronous=True)
+        return n_local
+
+    for j in range(WU):
+        step(j)
+    conflict, _ = dev.read_counters()
+    assert not conflict, "partitioned bank workload must not conflict"
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_val = 0
+    with ClockSampler(local) as clk:
+        start.record(ex)
+        for i in range(K):
+            n_val += step(WU + i, i)
+        # join every device stream back into s_exec before the stop event
+        for sidx in (1, 2, 3, 4):
+            other = torch.cuda.ExternalStream(dev.stream_handle(sidx))
+            e = torch.cuda.Event()
+            e.record(other)
+            ex.wait_event(e)
+        stop.record(ex)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = start.elapsed_time(stop)
+    conflict, st = dev.read_counters()
+    assert not conflict
+    batch_ms = statistics.mean(ev["b0"][i].elapsed_time(ev["b1"][i]) for i in range(K))
+    val_ms = statistics.mean(ev["v0"][i].elapsed_time(ev["v1"][i]) for i in range(K))
+    if dist:
+        t = torch.tensor([ms_total, batch_ms, val_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, batch_ms, val_ms = t.tolist()
+        nv = torch.tensor([n_val], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nv)
+        n_val = int(nv.item())
+
+    # correctness spot check after timing: bank sum preserved on the device
+    dev_words = dev.download(hetm.REPLICA_DEV, base + 0, W // 2)
+    bank_sum_ok = int(dev_words.sum(dtype=np.uint64)) == 1000 * (W // 2)
+
+    # ---- end-to-end through the host-buffer C-ABI (pinned host memory)
+    e2e = run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist)
+
+    ms_step = ms_total / K
+    value = world * B * K / (ms_total / 1e3)
+    peak, peak_kind = peaks()
+    achieved = TX_BYTES * B / (batch_ms / 1e-3) / 1e9
+    val_gbs = ENTRY_BYTES * (n_val / K / world) / (val_ms / 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": WU,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (seeded DetRng bank batches + host write logs)",
+        "config": {
+            "workload": "BASELINE configs[1]: bank, 1 GiB STMR per GPU, 2^20-tx GPU batch per round, 4R/2W "
+                        "uniform, RS/WS gran 1 KiB; round host log 2^20 entries on the host halves, "
+                        "validated+applied (routed by owner shard over NCCL when G>1)",
+            "stmr_words_per_gpu": W, "batch_tx": B, "log_entries_per_gpu": L, "rs_gran_bytes": args.gran,
+            "lock_entries": int(dev.info().lock_entries), "parallelism": f"shard{world}",
+            "l2": "inputs larger than L2: 1 GiB STMR per GPU, rotating per-step input buffers "
+                  f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
+        },
+        "roofline": {"bound": "hbm", "kernel": "bank_batch_kernel", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms},
+        "validate_apply": {"kernel": "validate_kernel<apply>", "gbs_algorithmic": val_gbs,
+                           "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
+                           "log_gbs_per_gpu": 24 * (n_val / K / world) / (val_ms / 1e-3) / 1e9,
+                           "frac": val_gbs / peak, "algorithmic_bytes_per_entry": ENTRY_BYTES,
+                           "kernel_ms": val_ms, "aggregate_gbs": val_gbs * world},
+        "batch": {"committed_last": int(st.committed), "aborts_last": int(st.aborts)},
+        "bank_sum_ok": bank_sum_ok,
+        "e2e": e2e,
+        "gpu_launches": K * (2 + (3 if world > 1 else 0)),
+        "clocks": clk.summary(),
+        "input_gen_s": gen_s,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dev.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
+    """Full synchronous rounds through the public C-ABI with HOST buffers."""
+    B, L = args.batch, args.log_entries
+    steps = args.e2e_steps
+    txs = [hetm.PinnedArray((B,), hetm.BANK_TX) for _ in range(2)]
+    for j, p in enumerate(txs):
+        hetm.gen_bank_batch(555 + j + 31 * rank, B, base, W // 2, out=p.array)
+    logs = [hetm.PinnedArray((L,), hetm.LOG_ENTRY) for _ in range(steps + 1)]
+    ts0 = 10_000_000_000
+    for j, p in enumerate(logs):  # produced by host txs before the round: not timed
+        hetm.gen_host_log(900 + j, L // 2, 2, 8, base + W // 2, W // 2, ts_base=ts0 + j * L, out=p.array)
+    info = dev.info()
+    dev.sync()
+    conflict, _ = dev.read_counters()
+    dev.clear_round()  # synchronous clear: refresh the TS floor after the pipelined rounds
+    tickets = hetm.PinnedArray((B,), np.uint64)
+    import ctypes as C
+    lib = hetm._lib.lib
+    h2d = d2h = 0
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for j in range(steps + 1):
+        if j == 1:  # first round is warm-up
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            h2d = d2h = 0
+        lg = logs[j].array
+        st = hetm._lib.BatchStats()
+        rc = lib.hetm_dev_execute_batch(dev.h, hetm.KERNEL_BANK, txs[j % 2].array.ctypes.data, 24, B,
+                                        tickets.array.ctypes.data, C.byref(st))
+        hetm.check(rc, dev.h)
+        for c in range(8):  # the round's log streamed in 8 chunks (one per host thread)
+            sl = lg[c * (L // 8):(c + 1) * (L // 8)]
+            dev.stream_chunk(sl, src_thread=c, seq=c)
+        conflict = dev.round_verdict()
+        if conflict:
+            raise RuntimeError("unexpected conflict in the partitioned e2e round")
+        ms = dev.merge_commit(host_replica.array)
+        dev.merge_wait()
+        dev.clear_round()
+        h2d += B * 24 + L * 24
+        d2h += B * 8 + ms.bytes_d2h
+    dt = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    for p in txs + logs + [tickets]:
+        p.free()
+    return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
+            "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
+            "timing": "host wall clock around full synchronous rounds (pinned buffers; verdict + merge D2H)",
+            "lock_entries": int(info.lock_entries)}
+
+
+# ---------------------------------------------------------- CPU baseline
+def cpu_baseline(args, seconds=8.0, rounds=None):
+    """The reference CPU path (oracle port, multi-threaded) on a bounded sample
+    of the same round: one bank batch (guest-stm-batch worker pool)
+    + validate/apply of the round's log on all host threads."""
+    import oracle as O
+
+    threads = os.cpu_count() or 1
+    W = 1 << args.words_log2
+    B = args.batch // 4
+    L = args.log_entries // 4
+    s = np.full(W, 1000, np.uint64)
+    ts = np.zeros(W, np.uint64)
+    gran = args.gran
+    rs = np.zeros(((W * 8 // gran) + 63) // 64, np.uint64)
+    done_tx, t_tot, r = 0, 0.0, 0
+    while (rounds is None and t_tot < seconds) or (rounds is not None and r < rounds):
+        txs = O.gen_bank_batch(3000 + r, B, 0, W // 2)
+        log = O.gen_host_log(4000 + r, L // 2, 2, 8, W // 2, W // 2, ts_base=r * L)
+        rs[:] = 0
+        t0 = time.perf_counter()
+        c, _, rsb, _, _ = O.mt_bank_batch(s, txs, threads, lock_entries=1 << 24, gran=gran, tickets=False)
+        O.mt_validate_apply(log, rsb, gran, ts, s, threads)
+        t_tot += time.perf_counter() - t0
+        done_tx += c
+        r += 1
+    return {"value": done_tx / t_tot, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{r} rounds x ({B} bank tx + {L} log entries) on the 2^{args.words_log2}-word STMR "
+                      f"(1/4 of a GPU round), oracle/hetm_oracle.c pthreads"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # warmup rounds untimed, then K timed rounds
+    import oracle  # noqa: F401  (builds the checker if needed)
+    cpu_baseline(args, rounds=max(1, args.warmup // 2))
+    t0 = time.perf_counter()
+    cb = cpu_baseline(args, rounds=args.steps)
+    dt = time.perf_counter() - t0
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "BASELINE configs[1] (bounded per-step sample, see cpu_baseline.sample)",
+                       "stmr_words": 1 << args.words_log2},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

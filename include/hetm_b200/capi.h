@@ -1,0 +1,316 @@
+/*
+ * hetm_b200 — C-ABI into the B200 (sm_100a) device side of Speculative HeTM.
+ *
+ * This header is the ONLY door from host code into CUDA.  Every entry point
+ * takes plain pointers and sizes (no C++ / torch types) and returns an `int`
+ * status (HETM_OK == 0).  There is no CPU fallback: without a usable CUDA
+ * device every call that needs one returns HETM_ERR_NO_DEVICE.
+ *
+ * Reference interfaces each group replaces (paths relative to the reference
+ * tree, /root/reference):
+ *
+ *   stmr module           SPEC.md:29-70   Stmr/create/rawWrite/rawRead/copyChunks
+ *   guest-stm-batch       SPEC.md:196-229 BatchSpec/executeBatch/clearRound/bitmapStats
+ *   bitmaps               proj/include/hetm/bitmap.hpp:15-158 (BitmapSnapshot word layout)
+ *   interconnect          proj/include/hetm/bus.hpp:43-91, SPEC.md:270-307 (streamChunk,
+ *                         copyDeviceToHost, copyDeviceToDevice, transferLog)
+ *   engine                SPEC.md:319-389 (TsArray, validateChunk, earlyValidate,
+ *                         mergeCommit, mergeAbortDevice, mergeAbortHost)
+ *   write log wire format proj/include/hetm/write_log.hpp:16-25 (24-byte <addr,value,ts>)
+ *   errors                proj/include/hetm/types.hpp:35-49 (one status per HetmError subclass)
+ *
+ * Threading: all hetm_dev_* calls come from one
+ * controller thread, except hetm_dev_stream_chunk which is safe to call from
+ * any host worker thread (chunks are serialised per device in call order,
+ * which preserves the per-source-thread FIFO of SPEC.md:300).
+ */
+#ifndef HETM_B200_CAPI_H
+#define HETM_B200_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HETM_B200_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- status --
+ * One code per hetm::HetmError subclass (types.hpp:38-48) plus device codes. */
+enum hetm_status {
+    HETM_OK = 0,
+    HETM_ERR_INVALID_SIZE = 1,          /* InvalidSizeError          types.hpp:38 */
+    HETM_ERR_OUT_OF_BOUNDS = 2,         /* OutOfBoundsError          types.hpp:39 */
+    HETM_ERR_ROUND_CLOSED = 3,          /* RoundClosedError          types.hpp:40 */
+    HETM_ERR_KERNEL_NOT_REGISTERED = 4, /* KernelNotRegisteredError  types.hpp:41 */
+    HETM_ERR_LIVELOCK = 5,              /* LivelockError             types.hpp:42 */
+    HETM_ERR_NO_IMPLEMENTATION = 6,     /* NoImplementationError     types.hpp:43 */
+    HETM_ERR_BAD_AFFINITY = 7,          /* BadAffinityError          types.hpp:44 */
+    HETM_ERR_INCOMPLETE_TRACE = 8,      /* IncompleteTraceError      types.hpp:45 */
+    HETM_ERR_NONDETERMINISTIC = 9,      /* NondeterministicInputError types.hpp:46 */
+    HETM_ERR_CONFIG = 10,               /* ConfigError               types.hpp:47 */
+    HETM_ERR_IO = 11,                   /* IoError                   types.hpp:48 */
+    HETM_ERR_INVALID_ARG = 100,         /* null handle / bad enum value */
+    HETM_ERR_CUDA = 101,                /* a CUDA runtime call failed */
+    HETM_ERR_NO_DEVICE = 102,           /* no CUDA device: there is no CPU fallback */
+    HETM_ERR_NONMONOTONE_TS = 103,      /* log ts not above the previous round's max (TS array not reset) */
+    HETM_ERR_STATE = 104                /* call not valid in the current round phase */
+};
+
+/* Buffers addressable by raw region ops — hetm::Replica (types.hpp:21). */
+enum hetm_replica {
+    HETM_REPLICA_HOST = 0,          /* host-owned; not addressable through this ABI */
+    HETM_REPLICA_DEV = 1,
+    HETM_REPLICA_DEV_SHADOW = 2,
+    HETM_REPLICA_HOST_SNAPSHOT = 3  /* host-owned; not addressable through this ABI */
+};
+
+/* Which device bitmap (bitmap.hpp:94-158). */
+enum hetm_bitmap_kind { HETM_BMP_RS = 0, HETM_BMP_WS = 1, HETM_BMP_CHUNK = 2 };
+
+/* validateChunk applyMode. */
+enum hetm_validate_mode { HETM_APPLY = 0, HETM_VALIDATE_ONLY = 1 };
+
+/* Built-in transactional kernels (kernels are registered by id). */
+enum hetm_kernel_id {
+    HETM_KERNEL_BANK = 1, /* hetm_bank_tx: read 4 accounts, move amount acct0 -> acct1 */
+    HETM_KERNEL_RW = 2    /* hetm_rw_tx: generic <=4 reads / <=2 read-modify-writes   */
+};
+
+/* hetm_dev_clear_round flags. */
+#define HETM_CLEAR_RESET_TS 1u /* also zero the TS array (SPEC.md:421 literal reset) */
+#define HETM_CLEAR_ASYNC 2u    /* enqueue the bitmap reset behind the round's work without a
+                                  host sync; the conflict flag keeps accumulating until the
+                                  next synchronous clear (pipelined benchmark rounds) */
+
+/* hetm_dev_config.flags */
+#define HETM_CFG_NO_SHADOW 1u /* do not allocate devShadow (validation-only sweeps) */
+
+/* ------------------------------------------------------------ wire types -- */
+
+/* One committed host write: layout-identical to hetm::WriteLogEntry
+ * (write_log.hpp:16-22), 24 bytes on the wire (write_log.hpp:25). `addr` is a
+ * GLOBAL word index; ts >= 1. */
+typedef struct hetm_log_entry {
+    uint64_t addr;
+    uint64_t value;
+    uint64_t ts;
+} hetm_log_entry;
+
+/* Bank transfer input record (24 B): read acct[0..3], then
+ * acct[0] -= amount, acct[1] += amount (uint64 wrap-around).  Accounts are
+ * GLOBAL word indices < 2^32. */
+typedef struct hetm_bank_tx {
+    uint32_t acct[4];
+    uint64_t amount;
+} hetm_bank_tx;
+
+/* Generic read/modify transaction (72 B): reads r_addr[0..nr), then for each
+ * j < nw: stmr[w_addr[j]] = stmr[w_addr[j]] + add[j] + sum(reads).  Writes
+ * imply reads (no blind writes). */
+typedef struct hetm_rw_tx {
+    uint32_t nr;
+    uint32_t nw;
+    uint64_t r_addr[4];
+    uint64_t w_addr[2];
+    uint64_t add[2];
+} hetm_rw_tx;
+
+typedef struct hetm_dev_config {
+    uint64_t size_words;    /* STMR words held by this device (its shard)           */
+    uint64_t shard_base;    /* first global word index held (0 on a single GPU)      */
+    uint64_t rs_gran_bytes; /* RS/WS granularity: pow2 multiple of 8 (default 1024)  */
+    uint64_t chunk_bytes;   /* ChunkMap granularity: pow2 multiple of 8 (16384)      */
+    uint64_t lock_entries;  /* batch-TM lock table entries, pow2; 0 = auto           */
+    uint64_t log_capacity;  /* initial round-log arena (entries); 0 = auto; grows    */
+    uint32_t max_attempts;  /* livelock budget per transaction; 0 = default (1<<20)  */
+    int32_t device;         /* CUDA device ordinal                                   */
+    uint32_t flags;         /* HETM_CFG_*                                            */
+    uint32_t reserved;
+} hetm_dev_config;
+
+typedef struct hetm_dev_info {
+    uint64_t size_words, shard_base, rs_gran_bytes, chunk_bytes, lock_entries;
+    uint64_t rs_bits, rs_words, chunk_bits, chunk_words;
+    uint64_t log_capacity;
+    uint64_t device_bytes; /* HBM allocated by this handle */
+    int32_t device, sm_count;
+    uint64_t l2_bytes;
+    uint64_t ticket_next;  /* next commit ticket to be handed out */
+} hetm_dev_info;
+
+typedef struct hetm_batch_stats {
+    uint64_t n_tx;
+    uint64_t committed;
+    uint64_t aborts;       /* intra-device aborted attempts (retried) */
+    uint64_t livelocked;   /* transactions that exhausted the budget */
+    uint64_t ticket_first; /* tickets of this batch lie in [ticket_first, ticket_end) */
+    uint64_t ticket_end;
+    double kernel_ms;      /* device time of the batch kernel (CUDA events) */
+} hetm_batch_stats;
+
+typedef struct hetm_merge_stats {
+    uint64_t dirty_chunks;
+    uint64_t transfers;      /* coalesced copy descriptors issued */
+    uint64_t bytes_d2h;
+    uint64_t bytes_h2d;
+    uint64_t bytes_d2d;
+    double ms;               /* host wall time of the call */
+} hetm_merge_stats;
+
+/* Interconnect transferLog record (bus.hpp:27-32, BusDir bus.hpp:16). */
+enum hetm_bus_dir { HETM_H2D = 0, HETM_D2H = 1, HETM_D2D = 2 };
+typedef struct hetm_transfer_record {
+    int32_t dir;
+    int32_t tag;   /* HETM_TAG_* */
+    uint64_t bytes;
+} hetm_transfer_record;
+enum hetm_transfer_tag {
+    HETM_TAG_LOG = 0, HETM_TAG_MERGE = 1, HETM_TAG_SHADOW = 2, HETM_TAG_ROLLBACK = 3,
+    HETM_TAG_INPUT = 4, HETM_TAG_OUTPUT = 5, HETM_TAG_RAW = 6
+};
+
+typedef struct hetm_dev hetm_dev;
+
+/* ------------------------------------------------------------ lifecycle -- */
+const char* hetm_strerror(int status);
+int hetm_abi_version(void);
+int hetm_device_count(int* n);
+void hetm_dev_config_default(hetm_dev_config* cfg);
+/* Stmr create: all device replicas zero-filled. */
+int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out);
+int hetm_dev_close(hetm_dev* dev);
+int hetm_dev_info_get(hetm_dev* dev, hetm_dev_info* out);
+/* Last CUDA error string seen by this handle (diagnostics). */
+const char* hetm_dev_last_error(hetm_dev* dev);
+
+/* ----------------------------------------------- raw region ops (stmr) --
+ * SPEC.md:53-61; caller-enforced quiescence.  Addresses are
+ * GLOBAL word indices; out-of-shard -> HETM_ERR_OUT_OF_BOUNDS. */
+int hetm_dev_raw_write(hetm_dev* dev, int replica, uint64_t addr, uint64_t value);
+int hetm_dev_raw_read(hetm_dev* dev, int replica, uint64_t addr, uint64_t* value);
+int hetm_dev_upload(hetm_dev* dev, int replica, uint64_t addr, const uint64_t* src, uint64_t n);
+int hetm_dev_download(hetm_dev* dev, int replica, uint64_t addr, uint64_t* dst, uint64_t n);
+
+/* --------------------------------------------- guest-stm-batch (device) -- */
+/* registerTxType's device half: unknown id -> NO_IMPLEMENTATION. */
+int hetm_dev_register_kernel(hetm_dev* dev, int kernel_id);
+/* executeBatch.  `inputs` is HOST memory (n_tx records of
+ * rec_bytes, which must equal the kernel's record size).  Every transaction
+ * eventually commits or the call fails with HETM_ERR_LIVELOCK.  tickets_out
+ * (nullable, n_tx entries) receives each transaction's commit ticket: replaying
+ * the batch in ascending ticket order reproduces devReplica.
+ * UINT64_MAX marks a transaction that exhausted the livelock budget. */
+int hetm_dev_execute_batch(hetm_dev* dev, int kernel_id, const void* inputs, uint64_t rec_bytes,
+                           uint64_t n_tx, uint64_t* tickets_out, hetm_batch_stats* stats);
+/* bitmapStats. */
+int hetm_dev_bitmap_stats(hetm_dev* dev, uint64_t* rs_bits, uint64_t* ws_bits, uint64_t* chunks);
+int hetm_dev_bitmap_words(hetm_dev* dev, int which, uint64_t* n_words);
+/* BitmapSnapshot::words (bitmap.hpp:15-23): bit b <-> words[b>>6] >> (b&63). */
+int hetm_dev_snapshot_bitmap(hetm_dev* dev, int which, uint64_t* out_words, uint64_t n_words);
+/* OR `words` into a device bitmap (seeding RS for validation sweeps, tests). */
+int hetm_dev_or_bitmap(hetm_dev* dev, int which, const uint64_t* words, uint64_t n_words);
+
+/* ------------------------------------------- interconnect + validation -- */
+/* Log intake (bus.hpp:72-76): open at round start; merge closes it. */
+int hetm_dev_open_intake(hetm_dev* dev);
+int hetm_dev_close_intake(hetm_dev* dev);
+/* streamChunk + validateChunk.  `entries` is a
+ * HOST buffer borrowed until the next hetm_dev_round_verdict / hetm_dev_sync
+ * (pinned memory gives an asynchronous DMA).  The chunk is appended to the
+ * round's device log arena.  APPLY: validate + TS-guarded apply, ordered after
+ * the device's in-flight batch.  VALIDATE_ONLY: early validation (SPEC.md:
+ * 354-362), runs concurrently with execution; its apply is deferred to
+ * hetm_dev_apply_log.  After close_intake -> HETM_ERR_ROUND_CLOSED. */
+int hetm_dev_stream_chunk(hetm_dev* dev, const hetm_log_entry* entries, uint64_t n,
+                          int src_thread, uint64_t seq, int mode);
+/* Apply every arena entry streamed VALIDATE_ONLY this round (final validation
+ * phase re-validates them). */
+int hetm_dev_apply_log(hetm_dev* dev);
+/* Non-blocking: conflict flag as of the last completed validation work. */
+int hetm_dev_poll_conflict(hetm_dev* dev, int* conflict);
+/* Blocking: waits for all streamed chunks; returns the round conflictFlag
+ * (monotone within a round). */
+int hetm_dev_round_verdict(hetm_dev* dev, int* conflict);
+/* Waits for all work on all device streams. */
+int hetm_dev_sync(hetm_dev* dev);
+
+/* ---------------------------------------------------------------- merge --
+ * host_replica: HOST array of size_words words (this shard's slice), ideally
+ * pinned (hetm_host_alloc / hetm_host_register). */
+/* mergeCommit: devShadow := devReplica; dirty chunks are
+ * copied shadow -> host_replica in coalesced transfers.  Asynchronous w.r.t.
+ * the next round's execution: call hetm_dev_merge_wait before touching
+ * host_replica. */
+int hetm_dev_merge_commit(hetm_dev* dev, uint64_t* host_replica, hetm_merge_stats* st);
+/* mergeAbortDevice.  optimized=0: host_replica copied over
+ * the device's dirty chunks.  optimized=1: round-start shadow + the round's
+ * host log in ts order, swapped in.  Both end with devReplica == host_replica. */
+int hetm_dev_merge_abort_device(hetm_dev* dev, int optimized, const uint64_t* host_replica,
+                                hetm_merge_stats* st);
+/* mergeAbortHost: host_replica := host_snapshot, then the
+ * device's dirty chunks are copied device -> host.  The round's log must not
+ * have been applied (validate-only rounds). */
+int hetm_dev_merge_abort_host(hetm_dev* dev, uint64_t* host_replica, const uint64_t* host_snapshot,
+                              hetm_merge_stats* st);
+int hetm_dev_merge_wait(hetm_dev* dev);
+/* clearRound: RS/WS/ChunkMap zeroed, arena emptied,
+ * conflict flag cleared, intake reopened.  The TS array is NOT reset unless
+ * HETM_CLEAR_RESET_TS is given: with a monotone GlobalClock
+ * stale TS values are always older than the next round's ts, so the apply
+ * outcome is identical; a log ts not above the previous round's maximum is
+ * reported as HETM_ERR_NONMONOTONE_TS by the next verdict. */
+int hetm_dev_clear_round(hetm_dev* dev, uint32_t flags);
+
+/* ------------------------------------------------ interconnect accounting --
+ * transferLog (bus.hpp:84-91). */
+int hetm_dev_transfer_count(hetm_dev* dev, uint64_t* n);
+int hetm_dev_transfer_log(hetm_dev* dev, hetm_transfer_record* out, uint64_t max, uint64_t* n);
+int hetm_dev_clear_transfer_log(hetm_dev* dev);
+
+/* ------------------------------------------------ device-resident entries --
+ * The same kernels on DEVICE pointers, enqueued on `stream` (a cudaStream_t;
+ * NULL = the handle's execution stream) without synchronising.  Used by the
+ * benchmark (inputs resident in HBM) and by the multi-GPU shard router. */
+int hetm_dev_execute_batch_dptr(hetm_dev* dev, int kernel_id, const void* d_inputs, uint64_t n_tx,
+                                uint64_t* d_tickets, void* stream);
+int hetm_dev_validate_dptr(hetm_dev* dev, const hetm_log_entry* d_entries, uint64_t n, int mode,
+                           void* stream);
+/* Read back (synchronously) the device conflict / stats counters. */
+int hetm_dev_read_counters(hetm_dev* dev, int* conflict, hetm_batch_stats* last_batch);
+/* Shard router for address-range sharding (G GPUs, shard s owns global words
+ * [s*shard_words, (s+1)*shard_words)).  Stable-partitions d_in into d_out by
+ * owner shard; d_counts[s] receives the bucket sizes (device array of
+ * n_shards uint64).  d_out must hold n entries. */
+int hetm_dev_route_log_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
+                            uint64_t shard_words, hetm_log_entry* d_out, uint64_t* d_counts,
+                            void* stream);
+/* Streams owned by the handle: 0 = execution, 1 = log copy, 2 = validation, 3 = merge. */
+int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
+/* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
+int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
+
+/* ------------------------------------------------------------ host side -- */
+int hetm_host_alloc(uint64_t bytes, void** p); /* pinned, portable */
+int hetm_host_free(void* p);
+int hetm_host_register(void* p, uint64_t bytes);
+int hetm_host_unregister(void* p);
+/* Seeded bank batch generator (DetRng, det_rng.hpp:19-42): for each tx, 4
+ * distinct accounts uniform in [lo, lo+span) drawn by below(span) with
+ * rejection on repeats, then amount = below(100)+1. */
+int hetm_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, hetm_bank_tx* out);
+/* Seeded host write log: n_tx host transactions, each writing `writes_per_tx`
+ * distinct words uniform in [lo, lo+span) with value = DetRng draw and one
+ * shared ts (ts_base+1, ts_base+2, ... in commit order).  The
+ * transactions are dealt round-robin to n_threads per-thread logs
+ * (ts-ordered within a thread, write_log.hpp:27-28) and concatenated in
+ * thread order like WriteLog::allEntries (write_log.hpp:74-82). */
+int hetm_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads,
+                      uint64_t lo, uint64_t span, uint64_t ts_base, hetm_log_entry* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETM_B200_CAPI_H */

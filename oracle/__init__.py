@@ -1,0 +1,176 @@
+"""oracle — CPU checker for the Speculative HeTM GPU-side path.
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` arm may import this package.  The product
+(paper_1905_00661_b200) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+REF_LIB_PATH = os.path.join(HERE, "_ref", "libhetm_ref.so")
+
+ENTRY = np.dtype([("addr", "<u8"), ("value", "<u8"), ("ts", "<u8")])
+BANK_TX = np.dtype([("acct", "<u4", (4,)), ("amount", "<u8")])
+RW_TX = np.dtype([("nr", "<u4"), ("nw", "<u4"), ("r_addr", "<u8", (4,)), ("w_addr", "<u8", (2,)),
+                  ("add", "<u8", (2,))])
+RANGE = np.dtype([("offset_bytes", "<u8"), ("bytes", "<u8")])
+
+
+def build():
+    import subprocess
+    subprocess.check_call(["make", "-s", "-C", HERE, "all"])
+
+
+if not os.path.exists(LIB_PATH):
+    build()
+
+lib = C.CDLL(LIB_PATH)
+_v, _u = C.c_void_p, C.c_uint64
+for name, res, args in [
+    ("orc_splitmix64", _u, [_u]),
+    ("orc_rng_fill_next", None, [_u, _u, _v]),
+    ("orc_rng_fill_below", None, [_u, _u, _u, _v]),
+    ("orc_rng_fill_uniform", None, [_u, _u, _v]),
+    ("orc_bits_for_region", _u, [_u, _u]),
+    ("orc_valid_gran", C.c_int, [_u]),
+    ("orc_bit_of_word", _u, [_u, _u]),
+    ("orc_popcount", _u, [_v, _u]),
+    ("orc_validate_chunk", C.c_int, [_v, _u, _v, _u, _u, _v, _v, C.c_int]),
+    ("orc_brute_force_intersect", C.c_int, [_v, _u, _v, _u, _u, _u]),
+    ("orc_bank_replay", None, [_v, _u, _v, _v, _u, _v, _v, _v, _u, _u]),
+    ("orc_rw_replay", None, [_v, _u, _v, _v, _u, _v, _v, _v, _u, _u]),
+    ("orc_order_by_ticket", _u, [_v, _u, _v]),
+    ("orc_coalesce_chunks", _u, [_v, _u, _u, _u, _v, _u]),
+    ("orc_apply_log_ts_order", None, [_v, _u, _v, _u]),
+    ("orc_gen_bank_batch", None, [_u, _u, _u, _u, _v]),
+    ("orc_gen_host_log", None, [_u, _u, C.c_uint32, C.c_uint32, _u, _u, _u, _v]),
+    ("orc_mt_bank_batch", _u, [_v, _u, _u, _v, _u, C.c_int, _u, _v, _v, _v, _v, _u, _u]),
+    ("orc_mt_validate_apply", C.c_int, [_v, _u, _v, _u, _u, _v, _v, C.c_int, C.c_int]),
+]:
+    f = getattr(lib, name)
+    f.restype, f.argtypes = res, args
+
+
+def P(a):
+    """Pointer of a contiguous numpy array (or None)."""
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def words_for_bits(nbits: int) -> int:
+    return (nbits + 63) // 64
+
+
+# --------------------------------------------------------------- high level
+def rng_next(seed, n):
+    o = np.empty(n, np.uint64); lib.orc_rng_fill_next(seed, n, P(o)); return o
+
+
+def rng_below(seed, bound, n):
+    o = np.empty(n, np.uint64); lib.orc_rng_fill_below(seed, bound, n, P(o)); return o
+
+
+def rng_uniform(seed, n):
+    o = np.empty(n, np.float64); lib.orc_rng_fill_uniform(seed, n, P(o)); return o
+
+
+def gen_bank_batch(seed, n, lo, span):
+    o = np.empty(n, BANK_TX); lib.orc_gen_bank_batch(seed, n, lo, span, P(o)); return o
+
+
+def gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base=0):
+    o = np.empty(n_tx * wpt, ENTRY); lib.orc_gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base, P(o)); return o
+
+
+def validate_chunk(entries, rs_words, gran, ts, dev, apply=True, base=0):
+    entries = np.ascontiguousarray(entries, ENTRY)
+    return bool(lib.orc_validate_chunk(P(entries), entries.size, P(rs_words), gran, base, P(ts), P(dev), int(apply)))
+
+
+def brute_force_intersect(entries, rs_words, rs_bits, gran, base=0):
+    entries = np.ascontiguousarray(entries, ENTRY)
+    return bool(lib.orc_brute_force_intersect(P(entries), entries.size, P(rs_words), rs_bits, gran, base))
+
+
+def order_by_ticket(tickets):
+    tickets = np.ascontiguousarray(tickets, np.uint64)
+    o = np.empty(tickets.size, np.uint64)
+    m = lib.orc_order_by_ticket(P(tickets), tickets.size, P(o))
+    return o[:m]
+
+
+def bank_replay(stmr, txs, order, gran, chunk, base=0):
+    """sequentialReplay of device txs; returns (rs, ws, chunk) bitmaps as word arrays."""
+    W = stmr.size
+    rs = np.zeros(words_for_bits((W * 8 + gran - 1) // gran), np.uint64)
+    ws = np.zeros_like(rs)
+    ch = np.zeros(words_for_bits((W * 8 + chunk - 1) // chunk), np.uint64)
+    order = np.ascontiguousarray(order, np.uint64)
+    lib.orc_bank_replay(P(stmr), base, P(txs), P(order), order.size, P(rs), P(ws), P(ch), gran, chunk)
+    return rs, ws, ch
+
+
+def rw_replay(stmr, txs, order, gran, chunk, base=0):
+    W = stmr.size
+    rs = np.zeros(words_for_bits((W * 8 + gran - 1) // gran), np.uint64)
+    ws = np.zeros_like(rs)
+    ch = np.zeros(words_for_bits((W * 8 + chunk - 1) // chunk), np.uint64)
+    order = np.ascontiguousarray(order, np.uint64)
+    lib.orc_rw_replay(P(stmr), base, P(txs), P(order), order.size, P(rs), P(ws), P(ch), gran, chunk)
+    return rs, ws, ch
+
+
+def coalesce_chunks(chunk_words, n_chunks, chunk_bytes, region_bytes):
+    out = np.empty(max(n_chunks, 1), RANGE)
+    m = lib.orc_coalesce_chunks(P(chunk_words), n_chunks, chunk_bytes, region_bytes, P(out), out.size)
+    return [(int(r["offset_bytes"]), int(r["bytes"])) for r in out[:m]]
+
+
+def apply_log_ts_order(region, entries, base=0):
+    entries = np.ascontiguousarray(entries, ENTRY)
+    lib.orc_apply_log_ts_order(P(region), base, P(entries), entries.size)
+
+
+def mt_bank_batch(stmr, txs, threads, lock_entries=1 << 22, gran=1024, chunk=16384, base=0, tickets=True):
+    W = stmr.size
+    tk = np.empty(txs.size, np.uint64) if tickets else None
+    rs = np.zeros(words_for_bits((W * 8 + gran - 1) // gran), np.uint64)
+    ws = np.zeros_like(rs)
+    ch = np.zeros(words_for_bits((W * 8 + chunk - 1) // chunk), np.uint64)
+    c = lib.orc_mt_bank_batch(P(stmr), base, W, P(txs), txs.size, threads, lock_entries, P(tk), P(rs), P(ws),
+                              P(ch), gran, chunk)
+    return c, tk, rs, ws, ch
+
+
+def mt_validate_apply(entries, rs_words, gran, ts, dev, threads, apply=True, base=0):
+    entries = np.ascontiguousarray(entries, ENTRY)
+    return bool(lib.orc_mt_validate_apply(P(entries), entries.size, P(rs_words), gran, base, P(ts), P(dev),
+                                          threads, int(apply)))
+
+
+def load_ref():
+    """The reference-header shim (oracle/_ref), present only where /root/reference was."""
+    if not os.path.exists(REF_LIB_PATH):
+        return None
+    r = C.CDLL(REF_LIB_PATH)
+    for name, res, args in [
+        ("ref_rng_next", None, [_u, _u, _v]),
+        ("ref_rng_below", None, [_u, _u, _u, _v]),
+        ("ref_rng_uniform", None, [_u, _u, _v]),
+        ("ref_splitmix64", _u, [_u]),
+        ("ref_access_bitmap", C.c_longlong, [_u, _u, _v, _u, _v]),
+        ("ref_chunk_map", C.c_longlong, [_u, _u, _v, _u, _v, _u]),
+        ("ref_write_log_all", None, [_v, _v, _u, C.c_int, _v]),
+        ("ref_log_entry_bytes", _u, []),
+    ]:
+        f = getattr(r, name)
+        f.restype, f.argtypes = res, args
+    return r

@@ -1,0 +1,364 @@
+"""Python mirror of the reference HeTM API for the GPU-side path.
+
+Names follow the reference (SPEC.md op names in the docstrings; error classes
+per proj/include/hetm/types.hpp:35-49).  Every call goes through the C-ABI in
+libhetm_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib
+
+# ------------------------------------------------------------------ constants
+REPLICA_HOST, REPLICA_DEV, REPLICA_DEV_SHADOW, REPLICA_HOST_SNAPSHOT = 0, 1, 2, 3  # types.hpp:21
+BMP_RS, BMP_WS, BMP_CHUNK = 0, 1, 2
+APPLY, VALIDATE_ONLY = 0, 1
+KERNEL_BANK, KERNEL_RW = 1, 2
+CLEAR_RESET_TS = 1
+CLEAR_ASYNC = 2
+CFG_NO_SHADOW = 1
+H2D, D2H, D2D = 0, 1, 2  # BusDir, bus.hpp:16
+TAG_LOG, TAG_MERGE, TAG_SHADOW, TAG_ROLLBACK, TAG_INPUT, TAG_OUTPUT, TAG_RAW = range(7)
+
+# 24-byte <addr,value,ts> (write_log.hpp:16-25)
+LOG_ENTRY = np.dtype([("addr", "<u8"), ("value", "<u8"), ("ts", "<u8")])
+BANK_TX = np.dtype([("acct", "<u4", (4,)), ("amount", "<u8")])
+RW_TX = np.dtype(
+    [("nr", "<u4"), ("nw", "<u4"), ("r_addr", "<u8", (4,)), ("w_addr", "<u8", (2,)), ("add", "<u8", (2,))]
+)
+assert LOG_ENTRY.itemsize == 24 and BANK_TX.itemsize == 24 and RW_TX.itemsize == 72
+
+
+# --------------------------------------------------------------------- errors
+class HetmError(RuntimeError):
+    """hetm::HetmError (types.hpp:35)."""
+
+    code = -1
+
+
+class InvalidSizeError(HetmError): code = 1
+class OutOfBoundsError(HetmError): code = 2
+class RoundClosedError(HetmError): code = 3
+class KernelNotRegisteredError(HetmError): code = 4
+class LivelockError(HetmError): code = 5
+class NoImplementationError(HetmError): code = 6
+class BadAffinityError(HetmError): code = 7
+class IncompleteTraceError(HetmError): code = 8
+class NondeterministicInputError(HetmError): code = 9
+class ConfigError(HetmError): code = 10
+class IoError(HetmError): code = 11
+class InvalidArgumentError(HetmError): code = 100
+class CudaError(HetmError): code = 101
+class NoDeviceError(HetmError): code = 102
+class NonMonotoneTsError(HetmError): code = 103
+class StateError(HetmError): code = 104
+
+
+_ERRORS = {c.code: c for c in HetmError.__subclasses__()}
+
+
+def check(rc: int, dev=None) -> None:
+    if rc == 0:
+        return
+    msg = lib.hetm_strerror(rc).decode()
+    if dev is not None and rc == CudaError.code:
+        msg += ": " + lib.hetm_dev_last_error(dev).decode()
+    raise _ERRORS.get(rc, HetmError)(msg)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    rc = lib.hetm_device_count(C.byref(n))
+    return n.value if rc == 0 else 0
+
+
+def _ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"], "arrays crossing the C-ABI must be contiguous"
+    return a.ctypes.data
+
+
+# -------------------------------------------------------------- host helpers
+class PinnedArray:
+    """Page-locked host buffer (cudaHostAlloc) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * dtype.itemsize
+        p = C.c_void_p()
+        check(lib.hetm_host_alloc(max(n, 8), C.byref(p)))
+        self._p = p
+        buf = (C.c_char * max(n, 8)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=np.uint8, count=n).view(dtype).reshape(shape)
+
+    def free(self):
+        if self._p is not None and self._p.value:
+            lib.hetm_host_free(self._p)
+        self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def gen_bank_batch(seed: int, n: int, lo: int, span: int, out: np.ndarray | None = None) -> np.ndarray:
+    """Seeded bank transfers (4 distinct accounts in [lo, lo+span), amount in [1,100])."""
+    out = np.empty(n, BANK_TX) if out is None else out
+    check(lib.hetm_gen_bank_batch(seed, n, lo, span, _ptr(out)))
+    return out
+
+
+def gen_host_log(seed: int, n_tx: int, writes_per_tx: int, n_threads: int, lo: int, span: int,
+                 ts_base: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """Seeded host write log in WriteLog::allEntries order (thread-major)."""
+    out = np.empty(n_tx * writes_per_tx, LOG_ENTRY) if out is None else out
+    check(lib.hetm_gen_host_log(seed, n_tx, writes_per_tx, n_threads, lo, span, ts_base, _ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------------ snapshots
+@dataclass
+class BitmapSnapshot:
+    """hetm::BitmapSnapshot (bitmap.hpp:15-23)."""
+
+    granBytes: int
+    nBits: int
+    words: np.ndarray = field(repr=False)
+
+    def test(self, bit: int) -> bool:
+        return bool((int(self.words[bit >> 6]) >> (bit & 63)) & 1)
+
+    def set_bits(self) -> np.ndarray:
+        bits = np.unpackbits(self.words.view(np.uint8), bitorder="little")
+        return np.flatnonzero(bits[: self.nBits])
+
+
+@dataclass
+class BatchResult:
+    tickets: np.ndarray
+    n_tx: int
+    committed: int
+    aborts: int
+    livelocked: int
+    ticket_first: int
+    ticket_end: int
+    kernel_ms: float
+
+
+# ------------------------------------------------------------- device guest
+class GpuDevice:
+    """One B200 holding one STMR shard: the device replica, shadow, TS array,
+    RS/WS/ChunkMap bitmaps and the batch-TM lock table (Stmr + guest-stm-batch
+    + engine device half)."""
+
+    def __init__(self, size_words: int, *, shard_base: int = 0, rs_gran_bytes: int = 1024,
+                 chunk_bytes: int = 16384, lock_entries: int = 0, log_capacity: int = 0,
+                 max_attempts: int = 0, device: int = 0, shadow: bool = True):
+        cfg = _lib.DevConfig()
+        lib.hetm_dev_config_default(C.byref(cfg))
+        cfg.size_words = size_words
+        cfg.shard_base = shard_base
+        cfg.rs_gran_bytes = rs_gran_bytes
+        cfg.chunk_bytes = chunk_bytes
+        cfg.lock_entries = lock_entries
+        cfg.log_capacity = log_capacity
+        cfg.max_attempts = max_attempts
+        cfg.device = device
+        cfg.flags = 0 if shadow else CFG_NO_SHADOW
+        h = C.c_void_p()
+        check(lib.hetm_dev_open(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.size_words = size_words
+        self.shard_base = shard_base
+        self.rs_gran_bytes = rs_gran_bytes
+        self.chunk_bytes = chunk_bytes
+
+    # lifecycle --------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib.hetm_dev_close(self.h)
+        self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        check(rc, self.h)
+
+    def info(self) -> _lib.DevInfo:
+        o = _lib.DevInfo()
+        self._chk(lib.hetm_dev_info_get(self.h, C.byref(o)))
+        return o
+
+    # stmr raw ops -------------------------------------------
+    def raw_write(self, replica: int, addr: int, value: int):
+        self._chk(lib.hetm_dev_raw_write(self.h, replica, addr, value))
+
+    def raw_read(self, replica: int, addr: int) -> int:
+        v = C.c_uint64()
+        self._chk(lib.hetm_dev_raw_read(self.h, replica, addr, C.byref(v)))
+        return v.value
+
+    def upload(self, replica: int, addr: int, words: np.ndarray):
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        self._chk(lib.hetm_dev_upload(self.h, replica, addr, _ptr(words), words.size))
+
+    def download(self, replica: int, addr: int = None, n: int = None) -> np.ndarray:
+        addr = self.shard_base if addr is None else addr
+        n = self.size_words - (addr - self.shard_base) if n is None else n
+        out = np.empty(n, np.uint64)
+        self._chk(lib.hetm_dev_download(self.h, replica, addr, _ptr(out), n))
+        return out
+
+    # guest-stm-batch --------------------------------------
+    def register_kernel(self, kernel_id: int):
+        self._chk(lib.hetm_dev_register_kernel(self.h, kernel_id))
+
+    def execute_batch(self, kernel_id: int, inputs: np.ndarray, want_tickets: bool = True) -> BatchResult:
+        """executeBatch: returns commit tickets (ascending ticket = serial order)."""
+        inputs = np.ascontiguousarray(inputs)
+        n = inputs.shape[0]
+        tickets = np.empty(n, np.uint64) if want_tickets else None
+        st = _lib.BatchStats()
+        self._chk(lib.hetm_dev_execute_batch(self.h, kernel_id, _ptr(inputs) if n else None,
+                                             inputs.dtype.itemsize, n,
+                                             _ptr(tickets) if (want_tickets and n) else None, C.byref(st)))
+        return BatchResult(tickets, st.n_tx, st.committed, st.aborts, st.livelocked, st.ticket_first,
+                           st.ticket_end, st.kernel_ms)
+
+    def bitmap_stats(self):
+        """bitmapStats -> (rsBitsSet, wsBitsSet, chunksDirty)."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._chk(lib.hetm_dev_bitmap_stats(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def snapshot(self, which: int) -> BitmapSnapshot:
+        n = C.c_uint64()
+        self._chk(lib.hetm_dev_bitmap_words(self.h, which, C.byref(n)))
+        out = np.zeros(n.value, np.uint64)
+        self._chk(lib.hetm_dev_snapshot_bitmap(self.h, which, _ptr(out), n.value))
+        gran = self.chunk_bytes if which == BMP_CHUNK else self.rs_gran_bytes
+        nbits = (self.size_words * 8 + gran - 1) // gran
+        return BitmapSnapshot(gran, nbits, out)
+
+    def or_bitmap(self, which: int, words: np.ndarray):
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        self._chk(lib.hetm_dev_or_bitmap(self.h, which, _ptr(words), words.size))
+
+    # interconnect + validation --------------------
+    def open_intake(self):
+        self._chk(lib.hetm_dev_open_intake(self.h))
+
+    def close_intake(self):
+        self._chk(lib.hetm_dev_close_intake(self.h))
+
+    def stream_chunk(self, entries: np.ndarray, src_thread: int = 0, seq: int = 0, mode: int = APPLY):
+        """streamChunk + validateChunk.  The buffer must stay alive until round_verdict."""
+        entries = np.ascontiguousarray(entries, dtype=LOG_ENTRY)
+        self._chk(lib.hetm_dev_stream_chunk(self.h, _ptr(entries) if entries.size else None, entries.size,
+                                            src_thread, seq, mode))
+        return entries
+
+    def apply_log(self):
+        self._chk(lib.hetm_dev_apply_log(self.h))
+
+    def poll_conflict(self) -> bool:
+        c = C.c_int()
+        self._chk(lib.hetm_dev_poll_conflict(self.h, C.byref(c)))
+        return bool(c.value)
+
+    def round_verdict(self) -> bool:
+        c = C.c_int()
+        self._chk(lib.hetm_dev_round_verdict(self.h, C.byref(c)))
+        return bool(c.value)
+
+    def sync(self):
+        self._chk(lib.hetm_dev_sync(self.h))
+
+    # merge -----------------------------------------------
+    def merge_commit(self, host_replica: np.ndarray) -> _lib.MergeStats:
+        st = _lib.MergeStats()
+        self._chk(lib.hetm_dev_merge_commit(self.h, _ptr(host_replica), C.byref(st)))
+        return st
+
+    def merge_abort_device(self, host_replica: np.ndarray | None, optimized: bool = True) -> _lib.MergeStats:
+        st = _lib.MergeStats()
+        self._chk(lib.hetm_dev_merge_abort_device(self.h, int(optimized),
+                                                  None if host_replica is None else _ptr(host_replica),
+                                                  C.byref(st)))
+        return st
+
+    def merge_abort_host(self, host_replica: np.ndarray, host_snapshot: np.ndarray) -> _lib.MergeStats:
+        st = _lib.MergeStats()
+        self._chk(lib.hetm_dev_merge_abort_host(self.h, _ptr(host_replica), _ptr(host_snapshot), C.byref(st)))
+        return st
+
+    def merge_wait(self):
+        self._chk(lib.hetm_dev_merge_wait(self.h))
+
+    def clear_round(self, reset_ts: bool = False, asynchronous: bool = False):
+        flags = (CLEAR_RESET_TS if reset_ts else 0) | (CLEAR_ASYNC if asynchronous else 0)
+        self._chk(lib.hetm_dev_clear_round(self.h, flags))
+
+    # transferLog (bus.hpp:84-91) ---------------------------------------------
+    def transfer_log(self) -> list[tuple[int, int, int]]:
+        n = C.c_uint64()
+        self._chk(lib.hetm_dev_transfer_count(self.h, C.byref(n)))
+        recs = (_lib.TransferRecord * max(n.value, 1))()
+        self._chk(lib.hetm_dev_transfer_log(self.h, recs, n.value, C.byref(n)))
+        return [(r.dir, r.tag, r.bytes) for r in recs[: n.value]]
+
+    def clear_transfer_log(self):
+        self._chk(lib.hetm_dev_clear_transfer_log(self.h))
+
+    # device-resident entries (benchmark / shard router) ---------------------
+    def execute_batch_dptr(self, kernel_id: int, d_inputs: int, n: int, d_tickets: int, stream: int = 0):
+        self._chk(lib.hetm_dev_execute_batch_dptr(self.h, kernel_id, d_inputs, n, d_tickets, stream or None))
+
+    def validate_dptr(self, d_entries: int, n: int, mode: int = APPLY, stream: int = 0):
+        self._chk(lib.hetm_dev_validate_dptr(self.h, d_entries, n, mode, stream or None))
+
+    def route_log_dptr(self, d_in: int, n: int, n_shards: int, shard_words: int, d_out: int, d_counts: int,
+                       stream: int = 0):
+        self._chk(lib.hetm_dev_route_log_dptr(self.h, d_in, n, n_shards, shard_words, d_out, d_counts,
+                                              stream or None))
+
+    def read_counters(self):
+        c = C.c_int()
+        st = _lib.BatchStats()
+        self._chk(lib.hetm_dev_read_counters(self.h, C.byref(c), C.byref(st)))
+        return bool(c.value), st
+
+    def stream_handle(self, which: int) -> int:
+        s = C.c_void_p()
+        self._chk(lib.hetm_dev_stream_handle(self.h, which, C.byref(s)))
+        return s.value or 0
+
+    def flush_l2(self, stream: int = 0):
+        self._chk(lib.hetm_dev_flush_l2(self.h, stream or None))
+
+    # reference op-name aliases -------------------------------------
+    rawWrite = raw_write
+    rawRead = raw_read
+    executeBatch = execute_batch
+    bitmapStats = bitmap_stats
+    streamChunk = stream_chunk
+    mergeCommit = merge_commit
+    mergeAbortDevice = merge_abort_device
+    mergeAbortHost = merge_abort_host
+    clearRound = clear_round

@@ -1,0 +1,1019 @@
+// capi.cu — the hetm_b200 C-ABI (include/hetm_b200/capi.h): device handle,
+// round state, streams, log arena, merge paths.
+//
+// Stream layout (one handle = one GPU = one STMR shard):
+//   s_exec   batch transaction kernels (execution phase)
+//   s_copy   H2D log chunk copies (interconnect streamChunk)
+//   s_val    validation kernels; APPLY kernels wait on the tail of s_exec
+//   s_merge  shadow update, rollback, round clear (round boundary)
+//   s_d2h    merge device->host chunk copies from devShadow, overlapping the
+//            next round's execution (double buffering)
+// Events carry every cross-stream dependency; nothing blocks the host except
+// the explicitly synchronous calls (verdict, merge_wait, snapshots, stats).
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "device_tm.cuh"
+#include "kernels.h"
+
+namespace hetm_b200 {
+int query_tx_occupancy(int* blocks);
+int query_val_occupancy(int* blocks);
+}  // namespace hetm_b200
+
+using namespace hetm_b200;
+
+struct hetm_dev {
+    hetm_dev_config cfg{};
+    int device = 0;
+    uint64_t W = 0, base = 0;
+    uint32_t gran_shift = 0, chunk_shift = 0;
+    uint64_t rs_bits = 0, rs_words = 0, chunk_bits = 0, chunk_words = 0;
+    uint64_t lock_entries = 0;
+    uint32_t lock_hash_shift = 0;
+    bool lock_identity = false;
+    uint32_t max_attempts = 1u << 20;
+
+    uint64_t* d_stmr = nullptr;
+    uint64_t* d_shadow = nullptr;
+    unsigned long long* d_ts = nullptr;
+    unsigned long long* d_rs = nullptr;
+    unsigned long long* d_ws = nullptr;
+    unsigned long long* d_chunk = nullptr;
+    unsigned long long* d_locks = nullptr;
+    DevCounters* d_ctr = nullptr;
+    DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
+    unsigned long long* d_pop = nullptr; // popcount scratch (3)
+    hetm_log_entry* d_arena = nullptr;   // this round's host log, in arrival order
+    uint64_t arena_cap = 0, arena_n = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> deferred;  // [lo,hi) streamed VALIDATE_ONLY, not applied
+    bool deferred_final = false;         // deferred ranges re-validated after execution ended
+    void* d_in = nullptr;
+    uint64_t in_cap = 0;
+    unsigned long long* d_tk = nullptr;
+    uint64_t tk_cap = 0;
+    void* d_route = nullptr;
+    size_t route_cap = 0;
+    void* d_flush = nullptr;
+    size_t flush_bytes = 0;
+    unsigned flush_gen = 0;
+
+    cudaStream_t s_exec = nullptr, s_copy = nullptr, s_val = nullptr, s_merge = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
+                ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    bool intake_open = true;
+    bool shadow_synced = true;   // devShadow == devReplica as of the round start
+    bool round_applied = false;  // some APPLY validation touched devReplica this round
+    bool d2h_pending = false;
+    uint64_t ts_floor = 0;
+    std::set<int> kernels;
+    std::vector<hetm_transfer_record> xfer;
+    std::mutex mu;
+    std::string last_err;
+    LaunchGeom geom{};
+    uint64_t bytes_alloc = 0;
+    uint64_t l2_bytes = 0;
+    hetm_batch_stats last_batch{};
+
+    ShardView view() const {
+        ShardView v;
+        v.stmr = d_stmr;
+        v.base = base;
+        v.size_words = W;
+        v.rs = d_rs;
+        v.ws = d_ws;
+        v.chunk = d_chunk;
+        v.gran_shift = gran_shift;
+        v.chunk_shift = chunk_shift;
+        return v;
+    }
+    LockTable locks() const {
+        LockTable lt;
+        lt.words = d_locks;
+        lt.hash_shift = 64u - (uint32_t)__builtin_ctzll(lock_entries);
+        lt.identity = lock_identity ? 1u : 0u;
+        return lt;
+    }
+    void record(int dir, int tag, uint64_t bytes) { xfer.push_back(hetm_transfer_record{dir, tag, bytes}); }
+};
+
+namespace {
+
+int fail(hetm_dev* d, cudaError_t e, const char* what) {
+    if (d) {
+        d->last_err = std::string(what) + ": " + cudaGetErrorString(e);
+    }
+    std::fprintf(stderr, "[hetm_b200] CUDA error in %s: %s\n", what, cudaGetErrorString(e));
+    return HETM_ERR_CUDA;
+}
+
+#define CK(dev, x)                                         \
+    do {                                                   \
+        cudaError_t e_ = (x);                              \
+        if (e_ != cudaSuccess) return fail(dev, e_, #x);   \
+    } while (0)
+
+bool pow2(uint64_t v) { return v && !(v & (v - 1)); }
+uint32_t log2u(uint64_t v) { return (uint32_t)__builtin_ctzll(v); }
+
+int dev_alloc(hetm_dev* d, void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e != cudaSuccess) return fail(d, e, "cudaMalloc");
+    d->bytes_alloc += bytes;
+    return HETM_OK;
+}
+
+uint64_t* replica_ptr(hetm_dev* d, int replica) {
+    if (replica == HETM_REPLICA_DEV) return d->d_stmr;
+    if (replica == HETM_REPLICA_DEV_SHADOW) return d->d_shadow;
+    return nullptr;
+}
+
+int check_range(hetm_dev* d, uint64_t addr, uint64_t n) {
+    if (addr < d->base) return HETM_ERR_OUT_OF_BOUNDS;
+    const uint64_t loc = addr - d->base;
+    if (loc >= d->W || n > d->W - loc) return HETM_ERR_OUT_OF_BOUNDS;
+    return HETM_OK;
+}
+
+int sync_all(hetm_dev* d) {
+    CK(d, cudaStreamSynchronize(d->s_exec));
+    CK(d, cudaStreamSynchronize(d->s_copy));
+    CK(d, cudaStreamSynchronize(d->s_val));
+    CK(d, cudaStreamSynchronize(d->s_merge));
+    CK(d, cudaStreamSynchronize(d->s_d2h));
+    return HETM_OK;
+}
+
+int read_counters(hetm_dev* d) {
+    CK(d, cudaMemcpy(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    return HETM_OK;
+}
+
+size_t record_bytes(int kernel_id) {
+    switch (kernel_id) {
+        case HETM_KERNEL_BANK: return sizeof(hetm_bank_tx);
+        case HETM_KERNEL_RW: return sizeof(hetm_rw_tx);
+        default: return 0;
+    }
+}
+
+// Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
+int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
+                  cudaStream_t s) {
+    CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
+    CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
+    CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
+    cudaError_t e = cudaSuccess;
+    if (kernel_id == HETM_KERNEL_BANK)
+        e = launch_bank_batch(d->view(), d->locks(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets,
+                              d->d_ctr, d->max_attempts, d->geom, s);
+    else
+        e = launch_rw_batch(d->view(), d->locks(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
+                            d->max_attempts, d->geom, s);
+    if (e != cudaSuccess) return fail(d, e, "batch kernel launch");
+    CK(d, cudaEventRecord(d->ev_exec, s));
+    return HETM_OK;
+}
+
+int ensure_arena(hetm_dev* d, uint64_t need) {
+    if (need <= d->arena_cap) return HETM_OK;
+    uint64_t cap = std::max<uint64_t>(need, d->arena_cap * 2);
+    int rc = sync_all(d);
+    if (rc) return rc;
+    void* p = nullptr;
+    if ((rc = dev_alloc(d, &p, cap * sizeof(hetm_log_entry)))) return rc;
+    if (d->arena_n) CK(d, cudaMemcpy(p, d->d_arena, d->arena_n * sizeof(hetm_log_entry), cudaMemcpyDeviceToDevice));
+    cudaFree(d->d_arena);
+    d->bytes_alloc -= d->arena_cap * sizeof(hetm_log_entry);
+    d->d_arena = static_cast<hetm_log_entry*>(p);
+    d->arena_cap = cap;
+    return HETM_OK;
+}
+
+// Dirty chunks of this round as coalesced [offset, bytes) word ranges
+// (adjacent dirty chunks form one transfer descriptor).
+int dirty_ranges(hetm_dev* d, std::vector<std::pair<uint64_t, uint64_t>>& out, uint64_t* n_dirty) {
+    std::vector<uint64_t> bits(d->chunk_words);
+    CK(d, cudaMemcpy(bits.data(), d->d_chunk, d->chunk_words * 8, cudaMemcpyDeviceToHost));
+    const uint64_t wpc = 1ull << d->chunk_shift;
+    uint64_t c = 0, nd = 0;
+    out.clear();
+    while (c < d->chunk_bits) {
+        if (!((bits[c >> 6] >> (c & 63)) & 1ull)) {
+            ++c;
+            continue;
+        }
+        const uint64_t first = c;
+        while (c < d->chunk_bits && ((bits[c >> 6] >> (c & 63)) & 1ull)) ++c;
+        nd += c - first;
+        const uint64_t lo = first * wpc, hi = std::min(c * wpc, d->W);
+        out.emplace_back(lo, hi - lo);
+    }
+    *n_dirty = nd;
+    return HETM_OK;
+}
+
+// devShadow := devReplica on s_merge.  Incremental when the shadow held the
+// round-start state: device-dirty chunks are copied and the round's host log
+// winners are patched in; otherwise a full D2D copy.
+int refresh_shadow(hetm_dev* d, bool host_log_applied, uint64_t dirty_bytes) {
+    if (!d->d_shadow) return HETM_OK;
+    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
+    if (d->shadow_synced) {
+        cudaError_t e = launch_copy_dirty_chunks(d->d_shadow, d->d_stmr, d->W, d->d_chunk, d->chunk_bits,
+                                                 d->chunk_shift, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "copy_dirty_chunks");
+        if (host_log_applied) {
+            e = launch_winner_apply(d->d_shadow, d->base, d->W, d->d_ts, d->d_arena, d->arena_n, d->geom, d->s_merge);
+            if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
+        }
+        d->record(HETM_D2D, HETM_TAG_SHADOW, dirty_bytes);
+    } else {
+        CK(d, cudaMemcpyAsync(d->d_shadow, d->d_stmr, d->W * 8, cudaMemcpyDeviceToDevice, d->s_merge));
+        d->record(HETM_D2D, HETM_TAG_SHADOW, d->W * 8);
+        d->shadow_synced = true;
+    }
+    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+    return HETM_OK;
+}
+
+int wait_round_work(hetm_dev* d, cudaStream_t s) {
+    CK(d, cudaEventRecord(d->ev_val, d->s_val));
+    CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
+    CK(d, cudaStreamWaitEvent(s, d->ev_val, 0));
+    return HETM_OK;
+}
+
+int enqueue_deferred_apply(hetm_dev* d) {
+    if (d->deferred.empty()) return HETM_OK;
+    CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
+    for (auto& r : d->deferred) {
+        cudaError_t e = launch_validate(d->view(), d->d_ts, d->d_arena + r.first, r.second - r.first, 1, d->ts_floor,
+                                        d->d_ctr, d->geom, d->s_val);
+        if (e != cudaSuccess) return fail(d, e, "validate(apply deferred)");
+    }
+    d->deferred.clear();
+    d->deferred_final = false;
+    d->round_applied = true;
+    return HETM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hetm_strerror(int s) {
+    switch (s) {
+        case HETM_OK: return "ok";
+        case HETM_ERR_INVALID_SIZE: return "invalid-size";
+        case HETM_ERR_OUT_OF_BOUNDS: return "out-of-bounds";
+        case HETM_ERR_ROUND_CLOSED: return "round-closed";
+        case HETM_ERR_KERNEL_NOT_REGISTERED: return "kernel-not-registered";
+        case HETM_ERR_LIVELOCK: return "livelock-budget-exceeded";
+        case HETM_ERR_NO_IMPLEMENTATION: return "no-implementation";
+        case HETM_ERR_BAD_AFFINITY: return "bad-affinity";
+        case HETM_ERR_INCOMPLETE_TRACE: return "incomplete-trace";
+        case HETM_ERR_NONDETERMINISTIC: return "nondeterministic-input";
+        case HETM_ERR_CONFIG: return "config-invalid";
+        case HETM_ERR_IO: return "io-error";
+        case HETM_ERR_INVALID_ARG: return "invalid-argument";
+        case HETM_ERR_CUDA: return "cuda-error";
+        case HETM_ERR_NO_DEVICE: return "no-cuda-device";
+        case HETM_ERR_NONMONOTONE_TS: return "non-monotone-timestamp";
+        case HETM_ERR_STATE: return "invalid-round-state";
+        default: return "unknown";
+    }
+}
+
+int hetm_abi_version(void) { return HETM_B200_ABI_VERSION; }
+
+int hetm_device_count(int* n) {
+    if (!n) return HETM_ERR_INVALID_ARG;
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        *n = 0;
+        return HETM_ERR_NO_DEVICE;
+    }
+    *n = c;
+    return c > 0 ? HETM_OK : HETM_ERR_NO_DEVICE;
+}
+
+void hetm_dev_config_default(hetm_dev_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->rs_gran_bytes = 1024;   // SPEC.md:239 default
+    c->chunk_bytes = 16384;    // bitmap.hpp:130
+}
+
+int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
+    if (!cfg || !out) return HETM_ERR_INVALID_ARG;
+    *out = nullptr;
+    // stmr.create pre-conditions, bitmap geometry (bitmap.hpp:99-100,134-135)
+    if (cfg->size_words == 0) return HETM_ERR_INVALID_SIZE;
+    if (!pow2(cfg->rs_gran_bytes) || cfg->rs_gran_bytes % 8) return HETM_ERR_INVALID_SIZE;
+    if (!pow2(cfg->chunk_bytes) || cfg->chunk_bytes % 8) return HETM_ERR_INVALID_SIZE;
+    if (cfg->lock_entries && (!pow2(cfg->lock_entries) || cfg->lock_entries > (1ull << 32)))
+        return HETM_ERR_CONFIG;
+    const uint64_t align_words = std::max(cfg->rs_gran_bytes, cfg->chunk_bytes) / 8;
+    if (cfg->shard_base % align_words) return HETM_ERR_CONFIG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return HETM_ERR_NO_DEVICE;
+    }
+    if (cfg->device < 0 || cfg->device >= ndev) return HETM_ERR_CONFIG;
+
+    hetm_dev* d = new hetm_dev();
+    d->cfg = *cfg;
+    d->device = cfg->device;
+    d->W = cfg->size_words;
+    d->base = cfg->shard_base;
+    d->gran_shift = log2u(cfg->rs_gran_bytes / 8);
+    d->chunk_shift = log2u(cfg->chunk_bytes / 8);
+    d->rs_bits = (d->W * 8 + cfg->rs_gran_bytes - 1) / cfg->rs_gran_bytes;  // bitmap.hpp:96-97 ceil
+    d->rs_words = (d->rs_bits + 63) / 64;
+    d->chunk_bits = (d->W * 8 + cfg->chunk_bytes - 1) / cfg->chunk_bytes;
+    d->chunk_words = (d->chunk_bits + 63) / 64;
+    uint64_t w2 = 1;
+    while (w2 < d->W) w2 <<= 1;
+    d->lock_entries = cfg->lock_entries ? cfg->lock_entries : std::min<uint64_t>(w2, 1ull << 24);
+    d->lock_identity = d->lock_entries >= d->W;
+    if (cfg->max_attempts) d->max_attempts = cfg->max_attempts;
+
+    auto bail = [&](int rc) {
+        hetm_dev_close(d);
+        return rc;
+    };
+    if (cudaSetDevice(d->device) != cudaSuccess) return bail(fail(d, cudaGetLastError(), "cudaSetDevice"));
+    int rc;
+    if ((rc = dev_alloc(d, (void**)&d->d_stmr, d->W * 8))) return bail(rc);
+    if (!(cfg->flags & HETM_CFG_NO_SHADOW))
+        if ((rc = dev_alloc(d, (void**)&d->d_shadow, d->W * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_ts, d->W * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_rs, d->rs_words * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_ws, d->rs_words * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_locks, d->lock_entries * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
+    d->arena_cap = cfg->log_capacity ? cfg->log_capacity : (1ull << 20);
+    if ((rc = dev_alloc(d, (void**)&d->d_arena, d->arena_cap * sizeof(hetm_log_entry)))) return bail(rc);
+    if (cudaHostAlloc((void**)&d->h_ctr, sizeof(DevCounters), cudaHostAllocPortable) != cudaSuccess)
+        return bail(fail(d, cudaGetLastError(), "cudaHostAlloc(counters)"));
+    std::memset(d->h_ctr, 0, sizeof(DevCounters));
+
+    // Stmr.create: all replicas zero-filled; TS/bitmaps/locks zero.
+    CK(d, cudaMemset(d->d_stmr, 0, d->W * 8));
+    if (d->d_shadow) CK(d, cudaMemset(d->d_shadow, 0, d->W * 8));
+    CK(d, cudaMemset(d->d_ts, 0, d->W * 8));
+    CK(d, cudaMemset(d->d_rs, 0, d->rs_words * 8));
+    CK(d, cudaMemset(d->d_ws, 0, d->rs_words * 8));
+    CK(d, cudaMemset(d->d_chunk, 0, d->chunk_words * 8));
+    CK(d, cudaMemset(d->d_locks, 0, d->lock_entries * 8));
+    CK(d, cudaMemset(d->d_ctr, 0, sizeof(DevCounters)));
+
+    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h})
+        CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h})
+        CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CK(d, cudaEventCreate(&d->ev_t0));
+    CK(d, cudaEventCreate(&d->ev_t1));
+    // Record the "round boundary" events once so the first waits are satisfied.
+    CK(d, cudaEventRecord(d->ev_round, d->s_merge));
+    CK(d, cudaEventRecord(d->ev_exec, d->s_exec));
+    CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
+
+    int sms = 0;
+    CK(d, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device));
+    int l2 = 0;
+    CK(d, cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, d->device));
+    d->l2_bytes = (uint64_t)l2;
+    d->geom.sm_count = sms;
+    int b = 0;
+    d->geom.max_blocks_tx = (query_tx_occupancy(&b) == 0 && b > 0) ? b : 4;
+    d->geom.max_blocks_val = (query_val_occupancy(&b) == 0 && b > 0) ? b : 4;
+    CK(d, cudaDeviceSynchronize());
+    *out = d;
+    return HETM_OK;
+}
+
+int hetm_dev_close(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    cudaSetDevice(d->device);
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
+        if (s) cudaStreamSynchronize(s);
+    for (void* p : {(void*)d->d_stmr, (void*)d->d_shadow, (void*)d->d_ts, (void*)d->d_rs, (void*)d->d_ws,
+                    (void*)d->d_chunk, (void*)d->d_locks, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_arena,
+                    d->d_in, (void*)d->d_tk, d->d_route, d->d_flush})
+        if (p) cudaFree(p);
+    if (d->h_ctr) cudaFreeHost(d->h_ctr);
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
+        if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1})
+        if (e) cudaEventDestroy(e);
+    delete d;
+    return HETM_OK;
+}
+
+int hetm_dev_info_get(hetm_dev* d, hetm_dev_info* o) {
+    if (!d || !o) return HETM_ERR_INVALID_ARG;
+    std::memset(o, 0, sizeof(*o));
+    o->size_words = d->W;
+    o->shard_base = d->base;
+    o->rs_gran_bytes = d->cfg.rs_gran_bytes;
+    o->chunk_bytes = d->cfg.chunk_bytes;
+    o->lock_entries = d->lock_entries;
+    o->rs_bits = d->rs_bits;
+    o->rs_words = d->rs_words;
+    o->chunk_bits = d->chunk_bits;
+    o->chunk_words = d->chunk_words;
+    o->log_capacity = d->arena_cap;
+    o->device_bytes = d->bytes_alloc;
+    o->device = d->device;
+    o->sm_count = d->geom.sm_count;
+    o->l2_bytes = d->l2_bytes;
+    int rc = sync_all(d);
+    if (rc) return rc;
+    if ((rc = read_counters(d))) return rc;
+    o->ticket_next = d->h_ctr->ticket;
+    return HETM_OK;
+}
+
+const char* hetm_dev_last_error(hetm_dev* d) { return d ? d->last_err.c_str() : "null handle"; }
+
+// ------------------------------------------------------------ raw region ops
+int hetm_dev_raw_write(hetm_dev* d, int replica, uint64_t addr, uint64_t value) {
+    return hetm_dev_upload(d, replica, addr, &value, 1);
+}
+
+int hetm_dev_raw_read(hetm_dev* d, int replica, uint64_t addr, uint64_t* value) {
+    if (!value) return HETM_ERR_INVALID_ARG;
+    return hetm_dev_download(d, replica, addr, value, 1);
+}
+
+int hetm_dev_upload(hetm_dev* d, int replica, uint64_t addr, const uint64_t* src, uint64_t n) {
+    if (!d || (!src && n)) return HETM_ERR_INVALID_ARG;
+    uint64_t* p = replica_ptr(d, replica);
+    if (!p) return replica == HETM_REPLICA_DEV_SHADOW ? HETM_ERR_CONFIG : HETM_ERR_INVALID_ARG;
+    int rc = check_range(d, addr, n);
+    if (rc) return rc;
+    if ((rc = sync_all(d))) return rc;  // raw ops require quiescence
+    CK(d, cudaMemcpy(p + (addr - d->base), src, n * 8, cudaMemcpyHostToDevice));
+    if (replica == HETM_REPLICA_DEV || replica == HETM_REPLICA_DEV_SHADOW) d->shadow_synced = false;
+    d->record(HETM_H2D, HETM_TAG_RAW, n * 8);
+    return HETM_OK;
+}
+
+int hetm_dev_download(hetm_dev* d, int replica, uint64_t addr, uint64_t* dst, uint64_t n) {
+    if (!d || (!dst && n)) return HETM_ERR_INVALID_ARG;
+    uint64_t* p = replica_ptr(d, replica);
+    if (!p) return replica == HETM_REPLICA_DEV_SHADOW ? HETM_ERR_CONFIG : HETM_ERR_INVALID_ARG;
+    int rc = check_range(d, addr, n);
+    if (rc) return rc;
+    if ((rc = sync_all(d))) return rc;
+    CK(d, cudaMemcpy(dst, p + (addr - d->base), n * 8, cudaMemcpyDeviceToHost));
+    d->record(HETM_D2H, HETM_TAG_RAW, n * 8);
+    return HETM_OK;
+}
+
+// ----------------------------------------------------------- batch execution
+int hetm_dev_register_kernel(hetm_dev* d, int kernel_id) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    if (record_bytes(kernel_id) == 0) return HETM_ERR_NO_IMPLEMENTATION;
+    d->kernels.insert(kernel_id);
+    return HETM_OK;
+}
+
+int hetm_dev_execute_batch(hetm_dev* d, int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx,
+                           uint64_t* tickets_out, hetm_batch_stats* stats) {
+    if (!d || (!inputs && n_tx)) return HETM_ERR_INVALID_ARG;
+    if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
+    if (rec_bytes != record_bytes(kernel_id)) return HETM_ERR_INVALID_SIZE;
+    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;  // priorities are 31-bit
+    int rc;
+    if (n_tx * rec_bytes > d->in_cap) {
+        if (d->d_in) { CK(d, cudaStreamSynchronize(d->s_exec)); cudaFree(d->d_in); d->bytes_alloc -= d->in_cap; }
+        d->in_cap = std::max<uint64_t>(n_tx * rec_bytes, 1 << 20);
+        if ((rc = dev_alloc(d, &d->d_in, d->in_cap))) return rc;
+    }
+    if (n_tx > d->tk_cap) {
+        if (d->d_tk) { CK(d, cudaStreamSynchronize(d->s_exec)); cudaFree(d->d_tk); d->bytes_alloc -= d->tk_cap * 8; }
+        d->tk_cap = std::max<uint64_t>(n_tx, 1 << 16);
+        if ((rc = dev_alloc(d, (void**)&d->d_tk, d->tk_cap * 8))) return rc;
+    }
+    cudaStream_t s = d->s_exec;
+    CK(d, cudaMemcpyAsync(&d->h_ctr->ticket, &d->d_ctr->ticket, 8, cudaMemcpyDeviceToHost, s));
+    CK(d, cudaStreamSynchronize(s));
+    const uint64_t first = d->h_ctr->ticket;
+    if (n_tx) {
+        CK(d, cudaMemcpyAsync(d->d_in, inputs, n_tx * rec_bytes, cudaMemcpyHostToDevice, s));
+        d->record(HETM_H2D, HETM_TAG_INPUT, n_tx * rec_bytes);
+    }
+    CK(d, cudaMemsetAsync(&d->d_ctr->oob, 0, sizeof(unsigned), s));
+    CK(d, cudaEventRecord(d->ev_t0, s));
+    if ((rc = enqueue_batch(d, kernel_id, d->d_in, n_tx, d->d_tk, s))) return rc;
+    CK(d, cudaEventRecord(d->ev_t1, s));
+    if (tickets_out && n_tx) {
+        CK(d, cudaMemcpyAsync(tickets_out, d->d_tk, n_tx * 8, cudaMemcpyDeviceToHost, s));
+        d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * 8);
+    }
+    CK(d, cudaMemcpyAsync(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CK(d, cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, d->ev_t0, d->ev_t1);
+    hetm_batch_stats st{};
+    st.n_tx = n_tx;
+    st.committed = d->h_ctr->committed;
+    st.aborts = d->h_ctr->aborts;
+    st.livelocked = d->h_ctr->livelocked;
+    st.ticket_first = first;
+    st.ticket_end = d->h_ctr->ticket;
+    st.kernel_ms = ms;
+    d->last_batch = st;
+    if (stats) *stats = st;
+    if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
+    if (st.livelocked) return HETM_ERR_LIVELOCK;
+    return HETM_OK;
+}
+
+int hetm_dev_bitmap_words(hetm_dev* d, int which, uint64_t* n) {
+    if (!d || !n) return HETM_ERR_INVALID_ARG;
+    if (which == HETM_BMP_RS || which == HETM_BMP_WS) *n = d->rs_words;
+    else if (which == HETM_BMP_CHUNK) *n = d->chunk_words;
+    else return HETM_ERR_INVALID_ARG;
+    return HETM_OK;
+}
+
+static unsigned long long* bitmap_ptr(hetm_dev* d, int which) {
+    return which == HETM_BMP_RS ? d->d_rs : which == HETM_BMP_WS ? d->d_ws : which == HETM_BMP_CHUNK ? d->d_chunk : nullptr;
+}
+
+int hetm_dev_bitmap_stats(hetm_dev* d, uint64_t* rs, uint64_t* ws, uint64_t* chunks) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    int rc = sync_all(d);
+    if (rc) return rc;
+    CK(d, cudaMemset(d->d_pop, 0, 3 * 8));
+    cudaError_t e;
+    if ((e = launch_popcount(d->d_rs, d->rs_words, d->d_pop + 0, 0)) != cudaSuccess) return fail(d, e, "popcount");
+    if ((e = launch_popcount(d->d_ws, d->rs_words, d->d_pop + 1, 0)) != cudaSuccess) return fail(d, e, "popcount");
+    if ((e = launch_popcount(d->d_chunk, d->chunk_words, d->d_pop + 2, 0)) != cudaSuccess) return fail(d, e, "popcount");
+    unsigned long long h[3];
+    CK(d, cudaMemcpy(h, d->d_pop, 24, cudaMemcpyDeviceToHost));
+    if (rs) *rs = h[0];
+    if (ws) *ws = h[1];
+    if (chunks) *chunks = h[2];
+    return HETM_OK;
+}
+
+int hetm_dev_snapshot_bitmap(hetm_dev* d, int which, uint64_t* out, uint64_t n_words) {
+    if (!d || !out) return HETM_ERR_INVALID_ARG;
+    unsigned long long* p = bitmap_ptr(d, which);
+    if (!p) return HETM_ERR_INVALID_ARG;
+    uint64_t want = which == HETM_BMP_CHUNK ? d->chunk_words : d->rs_words;
+    if (n_words != want) return HETM_ERR_INVALID_SIZE;
+    int rc = sync_all(d);
+    if (rc) return rc;
+    CK(d, cudaMemcpy(out, p, n_words * 8, cudaMemcpyDeviceToHost));
+    return HETM_OK;
+}
+
+int hetm_dev_or_bitmap(hetm_dev* d, int which, const uint64_t* words, uint64_t n_words) {
+    if (!d || (!words && n_words)) return HETM_ERR_INVALID_ARG;
+    unsigned long long* p = bitmap_ptr(d, which);
+    if (!p) return HETM_ERR_INVALID_ARG;
+    uint64_t want = which == HETM_BMP_CHUNK ? d->chunk_words : d->rs_words;
+    if (n_words != want) return HETM_ERR_INVALID_SIZE;
+    int rc = sync_all(d);
+    if (rc) return rc;
+    void* tmp = nullptr;
+    CK(d, cudaMalloc(&tmp, n_words * 8 + 8));
+    cudaError_t e = cudaMemcpy(tmp, words, n_words * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_or_words(p, static_cast<unsigned long long*>(tmp), n_words, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(d, e, "or_bitmap");
+    return HETM_OK;
+}
+
+// --------------------------------------------------- log streaming / validation
+int hetm_dev_open_intake(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->intake_open = true;
+    return HETM_OK;
+}
+
+int hetm_dev_close_intake(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->intake_open = false;
+    return HETM_OK;
+}
+
+int hetm_dev_stream_chunk(hetm_dev* d, const hetm_log_entry* entries, uint64_t n, int src_thread, uint64_t seq,
+                          int mode) {
+    (void)src_thread;
+    (void)seq;
+    if (!d || (!entries && n)) return HETM_ERR_INVALID_ARG;
+    if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (!d->intake_open) return HETM_ERR_ROUND_CLOSED;
+    d->record(HETM_H2D, HETM_TAG_LOG, n * sizeof(hetm_log_entry));
+    if (n == 0) return HETM_OK;
+    int rc = ensure_arena(d, d->arena_n + n);
+    if (rc) return rc;
+    hetm_log_entry* dst = d->d_arena + d->arena_n;
+    CK(d, cudaStreamWaitEvent(d->s_copy, d->ev_round, 0));
+    CK(d, cudaMemcpyAsync(dst, entries, n * sizeof(hetm_log_entry), cudaMemcpyHostToDevice, d->s_copy));
+    CK(d, cudaEventRecord(d->ev_copy, d->s_copy));
+    CK(d, cudaStreamWaitEvent(d->s_val, d->ev_copy, 0));
+    CK(d, cudaStreamWaitEvent(d->s_val, d->ev_round, 0));
+    const bool apply = mode == HETM_APPLY;
+    if (apply) CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));  // apply only after execution
+    cudaError_t e = launch_validate(d->view(), d->d_ts, dst, n, apply ? 1 : 0, d->ts_floor, d->d_ctr, d->geom, d->s_val);
+    if (e != cudaSuccess) return fail(d, e, "validate launch");
+    CK(d, cudaMemcpyAsync(&d->h_ctr->conflict, &d->d_ctr->conflict, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                          d->s_val));
+    if (apply) {
+        d->round_applied = true;
+    } else {
+        d->deferred.emplace_back(d->arena_n, d->arena_n + n);
+        d->deferred_final = false;
+    }
+    d->arena_n += n;
+    return HETM_OK;
+}
+
+int hetm_dev_apply_log(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    return enqueue_deferred_apply(d);
+}
+
+int hetm_dev_poll_conflict(hetm_dev* d, int* conflict) {
+    if (!d || !conflict) return HETM_ERR_INVALID_ARG;
+    *conflict = (int)*(volatile unsigned*)&d->h_ctr->conflict;
+    return HETM_OK;
+}
+
+int hetm_dev_round_verdict(hetm_dev* d, int* conflict) {
+    if (!d || !conflict) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    // Chunks validated only early (possibly before the batch finished setting
+    // its RS bits) are re-validated once execution has ended.
+    if (!d->deferred.empty() && !d->deferred_final) {
+        CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
+        for (auto& r : d->deferred) {
+            cudaError_t e = launch_validate(d->view(), d->d_ts, d->d_arena + r.first, r.second - r.first, 0,
+                                            d->ts_floor, d->d_ctr, d->geom, d->s_val);
+            if (e != cudaSuccess) return fail(d, e, "validate(final)");
+        }
+        d->deferred_final = true;
+    }
+    CK(d, cudaStreamSynchronize(d->s_copy));
+    CK(d, cudaStreamSynchronize(d->s_val));
+    int rc = read_counters(d);
+    if (rc) return rc;
+    *conflict = d->h_ctr->conflict ? 1 : 0;
+    if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
+    if (d->h_ctr->nonmonotone) return HETM_ERR_NONMONOTONE_TS;
+    return HETM_OK;
+}
+
+int hetm_dev_sync(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    return sync_all(d);
+}
+
+// ------------------------------------------------------------------- merge
+int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
+    if (!d || !host) return HETM_ERR_INVALID_ARG;
+    auto t0 = std::chrono::steady_clock::now();
+    std::lock_guard<std::mutex> g(d->mu);
+    d->intake_open = false;  // merge closes the log intake
+    if (!d->deferred.empty()) return HETM_ERR_STATE;  // all chunks must be applied
+    int rc = wait_round_work(d, d->s_merge);
+    if (rc) return rc;
+    CK(d, cudaStreamSynchronize(d->s_exec));
+    CK(d, cudaStreamSynchronize(d->s_val));
+    if ((rc = read_counters(d))) return rc;
+    if (d->h_ctr->conflict) return HETM_ERR_STATE;  // pre: conflictFlag = false
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    uint64_t nd = 0;
+    if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
+    uint64_t dirty_bytes = 0;
+    for (auto& r : ranges) dirty_bytes += r.second * 8;
+    const uint64_t* src = d->d_stmr;
+    if (d->d_shadow) {
+        if ((rc = refresh_shadow(d, true, dirty_bytes))) return rc;
+        src = d->d_shadow;
+        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
+    } else {
+        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_exec, 0));
+    }
+    for (auto& r : ranges) {
+        CK(d, cudaMemcpyAsync(host + r.first, src + r.first, r.second * 8, cudaMemcpyDeviceToHost, d->s_d2h));
+        d->record(HETM_D2H, HETM_TAG_MERGE, r.second * 8);
+    }
+    CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
+    d->d2h_pending = true;
+    if (!d->d_shadow) CK(d, cudaStreamSynchronize(d->s_d2h));  // no double buffer without a shadow
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->dirty_chunks = nd;
+        st->transfers = ranges.size();
+        st->bytes_d2h = dirty_bytes;
+        st->bytes_d2d = d->d_shadow ? dirty_bytes : 0;
+        st->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return HETM_OK;
+}
+
+int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host, hetm_merge_stats* st) {
+    if (!d || (!host && !optimized)) return HETM_ERR_INVALID_ARG;
+    auto t0 = std::chrono::steady_clock::now();
+    std::lock_guard<std::mutex> g(d->mu);
+    d->intake_open = false;
+    int rc = enqueue_deferred_apply(d);  // FavorHost: the host log always lands on the device
+    if (rc) return rc;
+    if ((rc = wait_round_work(d, d->s_merge))) return rc;
+    CK(d, cudaStreamSynchronize(d->s_exec));
+    CK(d, cudaStreamSynchronize(d->s_val));
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    uint64_t nd = 0;
+    if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
+    uint64_t dirty_bytes = 0;
+    for (auto& r : ranges) dirty_bytes += r.second * 8;
+    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
+    hetm_merge_stats s{};
+    if (optimized && d->d_shadow && d->shadow_synced) {
+        // Round-start shadow + the round's host log (freshest ts per word) -> swap
+        cudaError_t e = launch_winner_apply(d->d_shadow, d->base, d->W, d->d_ts, d->d_arena, d->arena_n, d->geom,
+                                            d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "winner_apply(rollback)");
+        std::swap(d->d_stmr, d->d_shadow);
+        // New shadow (old speculative replica) realigned on the device-dirty chunks.
+        e = launch_copy_dirty_chunks(d->d_shadow, d->d_stmr, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, d->geom,
+                                     d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "copy_dirty_chunks(realign)");
+        d->record(HETM_D2D, HETM_TAG_ROLLBACK, dirty_bytes);
+        s.bytes_d2d = dirty_bytes;
+        CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+    } else {
+        if (!host) return HETM_ERR_INVALID_ARG;
+        // Basic: host state copied over the device's dirty chunks
+        for (auto& r : ranges) {
+            CK(d, cudaMemcpyAsync(d->d_stmr + r.first, host + r.first, r.second * 8, cudaMemcpyHostToDevice,
+                                  d->s_merge));
+            d->record(HETM_H2D, HETM_TAG_ROLLBACK, r.second * 8);
+        }
+        s.bytes_h2d = dirty_bytes;
+        if ((rc = refresh_shadow(d, true, dirty_bytes))) return rc;
+    }
+    CK(d, cudaStreamSynchronize(d->s_merge));
+    s.dirty_chunks = nd;
+    s.transfers = ranges.size();
+    s.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = s;
+    return HETM_OK;
+}
+
+int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snapshot, hetm_merge_stats* st) {
+    if (!d || !host || !snapshot) return HETM_ERR_INVALID_ARG;
+    auto t0 = std::chrono::steady_clock::now();
+    std::lock_guard<std::mutex> g(d->mu);
+    d->intake_open = false;
+    if (d->round_applied) return HETM_ERR_STATE;  // FavorDevice validation is validate-only
+    int rc = wait_round_work(d, d->s_merge);
+    if (rc) return rc;
+    CK(d, cudaStreamSynchronize(d->s_exec));
+    CK(d, cudaStreamSynchronize(d->s_val));
+    if (d->d2h_pending) CK(d, cudaStreamSynchronize(d->s_d2h));
+    // hostReplica restored from the round-start snapshot
+    std::memcpy(host, snapshot, d->W * 8);
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    uint64_t nd = 0;
+    if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
+    uint64_t dirty_bytes = 0;
+    for (auto& r : ranges) dirty_bytes += r.second * 8;
+    const uint64_t* src = d->d_stmr;
+    if (d->d_shadow) {
+        if ((rc = refresh_shadow(d, false, dirty_bytes))) return rc;
+        src = d->d_shadow;
+        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
+    }
+    for (auto& r : ranges) {
+        CK(d, cudaMemcpyAsync(host + r.first, src + r.first, r.second * 8, cudaMemcpyDeviceToHost, d->s_d2h));
+        d->record(HETM_D2H, HETM_TAG_MERGE, r.second * 8);
+    }
+    CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
+    CK(d, cudaStreamSynchronize(d->s_d2h));
+    d->d2h_pending = false;
+    // The discarded host log is dropped from the arena: nothing to re-apply.
+    d->deferred.clear();
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->dirty_chunks = nd;
+        st->transfers = ranges.size();
+        st->bytes_d2h = dirty_bytes;
+        st->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return HETM_OK;
+}
+
+int hetm_dev_merge_wait(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    CK(d, cudaStreamSynchronize(d->s_merge));
+    CK(d, cudaStreamSynchronize(d->s_d2h));
+    d->d2h_pending = false;
+    return HETM_OK;
+}
+
+int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    int rc = wait_round_work(d, d->s_merge);
+    if (rc) return rc;
+    if (flags & HETM_CLEAR_ASYNC) {
+        cudaStream_t s = d->s_merge;
+        CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
+        CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
+        CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
+        CK(d, cudaEventRecord(d->ev_round, s));
+        d->arena_n = 0;
+        d->deferred.clear();
+        d->deferred_final = false;
+        d->round_applied = false;
+        d->intake_open = true;
+        return HETM_OK;
+    }
+    CK(d, cudaStreamSynchronize(d->s_val));
+    CK(d, cudaStreamSynchronize(d->s_exec));
+    if ((rc = read_counters(d))) return rc;
+    if (d->h_ctr->round_max_ts > d->ts_floor) d->ts_floor = d->h_ctr->round_max_ts;
+    cudaStream_t s = d->s_merge;
+    CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
+    CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
+    CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
+    CK(d, cudaMemsetAsync(&d->d_ctr->round_max_ts, 0, 8 + 3 * sizeof(unsigned), s));
+    if (flags & HETM_CLEAR_RESET_TS) {
+        CK(d, cudaMemsetAsync(d->d_ts, 0, d->W * 8, s));
+        d->ts_floor = 0;
+    }
+    CK(d, cudaEventRecord(d->ev_round, s));
+    d->h_ctr->conflict = 0;
+    d->arena_n = 0;
+    d->deferred.clear();
+    d->deferred_final = false;
+    d->round_applied = false;
+    d->intake_open = true;
+    return HETM_OK;
+}
+
+// --------------------------------------------------------- transfer log
+int hetm_dev_transfer_count(hetm_dev* d, uint64_t* n) {
+    if (!d || !n) return HETM_ERR_INVALID_ARG;
+    *n = d->xfer.size();
+    return HETM_OK;
+}
+
+int hetm_dev_transfer_log(hetm_dev* d, hetm_transfer_record* out, uint64_t max, uint64_t* n) {
+    if (!d || !n || (!out && max)) return HETM_ERR_INVALID_ARG;
+    const uint64_t k = std::min<uint64_t>(max, d->xfer.size());
+    std::copy(d->xfer.begin(), d->xfer.begin() + (ptrdiff_t)k, out);
+    *n = d->xfer.size();
+    return HETM_OK;
+}
+
+int hetm_dev_clear_transfer_log(hetm_dev* d) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    d->xfer.clear();
+    return HETM_OK;
+}
+
+// --------------------------------------------------- device-resident entries
+int hetm_dev_execute_batch_dptr(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n_tx, uint64_t* d_tickets,
+                                void* stream) {
+    if (!d || (n_tx && (!d_inputs || !d_tickets))) return HETM_ERR_INVALID_ARG;
+    if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
+    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
+    return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), s);
+}
+
+int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_t n, int mode, void* stream) {
+    if (!d || (n && !d_entries)) return HETM_ERR_INVALID_ARG;
+    if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
+    if (mode == HETM_APPLY) {
+        CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
+        d->round_applied = true;
+        d->shadow_synced = false;  // entries are not retained in the arena for the shadow patch
+    }
+    cudaError_t e = launch_validate(d->view(), d->d_ts, d_entries, n, mode == HETM_APPLY, d->ts_floor, d->d_ctr,
+                                    d->geom, s);
+    if (e != cudaSuccess) return fail(d, e, "validate_dptr");
+    if (stream) CK(d, cudaEventRecord(d->ev_val, s));
+    return HETM_OK;
+}
+
+int hetm_dev_read_counters(hetm_dev* d, int* conflict, hetm_batch_stats* last) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    CK(d, cudaDeviceSynchronize());
+    int rc = read_counters(d);
+    if (rc) return rc;
+    if (conflict) *conflict = d->h_ctr->conflict ? 1 : 0;
+    if (last) {
+        std::memset(last, 0, sizeof(*last));
+        last->committed = d->h_ctr->committed;
+        last->aborts = d->h_ctr->aborts;
+        last->livelocked = d->h_ctr->livelocked;
+        last->ticket_end = d->h_ctr->ticket;
+    }
+    if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
+    return HETM_OK;
+}
+
+int hetm_dev_route_log_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
+                            uint64_t shard_words, hetm_log_entry* d_out, uint64_t* d_counts, void* stream) {
+    if (!d || (n && (!d_in || !d_out)) || !d_counts) return HETM_ERR_INVALID_ARG;
+    if (n_shards == 0 || n_shards > 64 || shard_words == 0) return HETM_ERR_CONFIG;
+    const size_t need = route_log_scratch_bytes(n, n_shards);
+    if (need > d->route_cap) {
+        if (d->d_route) { CK(d, cudaDeviceSynchronize()); cudaFree(d->d_route); }
+        int rc = dev_alloc(d, &d->d_route, need);
+        if (rc) return rc;
+        d->route_cap = need;
+    }
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    cudaError_t e = launch_route_log(d_in, n, n_shards, shard_words, d_out,
+                                     reinterpret_cast<unsigned long long*>(d_counts), d->d_route, d->route_cap, s);
+    if (e != cudaSuccess) return fail(d, e, "route_log");
+    return HETM_OK;
+}
+
+int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
+    if (!d || !stream) return HETM_ERR_INVALID_ARG;
+    cudaStream_t s[5] = {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h};
+    if (which < 0 || which > 4) return HETM_ERR_INVALID_ARG;
+    *stream = s[which];
+    return HETM_OK;
+}
+
+int hetm_dev_flush_l2(hetm_dev* d, void* stream) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    if (!d->d_flush) {
+        d->flush_bytes = std::max<uint64_t>(2 * d->l2_bytes, 256ull << 20);
+        int rc = dev_alloc(d, &d->d_flush, d->flush_bytes);
+        if (rc) return rc;
+    }
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
+    CK(d, cudaMemsetAsync(d->d_flush, (int)(++d->flush_gen & 0xff), d->flush_bytes, s));
+    return HETM_OK;
+}
+
+// ------------------------------------------------------------------ host side
+int hetm_host_alloc(uint64_t bytes, void** p) {
+    if (!p) return HETM_ERR_INVALID_ARG;
+    cudaError_t e = cudaHostAlloc(p, bytes ? bytes : 8, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? HETM_ERR_NO_DEVICE : HETM_ERR_CUDA;
+    }
+    return HETM_OK;
+}
+
+int hetm_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+    return HETM_OK;
+}
+
+int hetm_host_register(void* p, uint64_t bytes) {
+    if (!p) return HETM_ERR_INVALID_ARG;
+    cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? HETM_ERR_NO_DEVICE : HETM_ERR_CUDA;
+    }
+    return HETM_OK;
+}
+
+int hetm_host_unregister(void* p) {
+    if (!p) return HETM_ERR_INVALID_ARG;
+    cudaHostUnregister(p);
+    return HETM_OK;
+}
+
+}  // extern "C"

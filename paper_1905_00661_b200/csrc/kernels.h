@@ -1,0 +1,51 @@
+// kernels.h — host-callable launchers for the sm_100a kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hetm_b200/capi.h"
+
+namespace hetm_b200 {
+
+struct DevCounters;
+struct ShardView;
+struct LockTable;
+
+struct LaunchGeom {
+    int sm_count;
+    int max_blocks_tx;    // resident blocks per SM for the batch kernels
+    int max_blocks_val;   // resident blocks per SM for the validation kernels
+};
+
+// guest-stm-batch: one launch executes a whole batch.
+cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const hetm_bank_tx* d_in, uint64_t n,
+                              unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
+                              const LaunchGeom& g, cudaStream_t s);
+cudaError_t launch_rw_batch(const ShardView& v, const LockTable& lt, const hetm_rw_tx* d_in, uint64_t n,
+                            unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
+                            const LaunchGeom& g, cudaStream_t s);
+
+// engine.validateChunk over n log entries.
+cudaError_t launch_validate(const ShardView& v, unsigned long long* d_ts, const hetm_log_entry* d_log, uint64_t n,
+                            int apply, uint64_t ts_floor, DevCounters* ctr, const LaunchGeom& g, cudaStream_t s);
+// Winner store: dst[addr] = value where TS[addr] == entry.ts (rollback /
+// shadow patch).
+cudaError_t launch_winner_apply(uint64_t* dst, uint64_t base, uint64_t size_words, const unsigned long long* d_ts,
+                                const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s);
+// Copy every dirty chunk src -> dst (device buffers of size_words words).
+cudaError_t launch_copy_dirty_chunks(uint64_t* dst, const uint64_t* src, uint64_t size_words,
+                                     const unsigned long long* chunk_bits, uint64_t n_chunks, uint32_t chunk_shift,
+                                     const LaunchGeom& g, cudaStream_t s);
+// Popcount of n words into *out (device counter, accumulated).
+cudaError_t launch_popcount(const unsigned long long* words, uint64_t n, unsigned long long* out, cudaStream_t s);
+// OR src words into dst words.
+cudaError_t launch_or_words(unsigned long long* dst, const unsigned long long* src, uint64_t n, cudaStream_t s);
+// Shard router: stable partition of entries by owner = addr / shard_words.
+cudaError_t launch_route_log(const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards, uint64_t shard_words,
+                             hetm_log_entry* d_out, unsigned long long* d_counts, void* d_scratch,
+                             size_t scratch_bytes, cudaStream_t s);
+size_t route_log_scratch_bytes(uint64_t n, uint32_t n_shards);
+
+int query_geom(LaunchGeom* g, int device);
+
+}  // namespace hetm_b200

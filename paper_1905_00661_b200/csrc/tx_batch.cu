@@ -1,0 +1,159 @@
+// tx_batch.cu — batch transaction kernels (guest-stm-batch).
+//
+// One launch executes a whole BatchSpec: thread i runs transaction i with
+// priority i+1 (PR-STM priority rule, device_tm.cuh), retrying aborted
+// attempts until commit or the livelock budget.  Commit
+// fuses the RS/WS/ChunkMap instrumentation as fire-and-forget
+// REDG.E.OR.64 and records the transaction's commit ticket.
+#include "common.cuh"
+#include "device_tm.cuh"
+#include "kernels.h"
+
+namespace hetm_b200 {
+
+constexpr int kTxThreads = 256;
+
+__device__ __forceinline__ void flush_batch_counters(unsigned long long commits, unsigned long long aborts,
+                                                     unsigned long long livelocks, unsigned oob, DevCounters* ctr) {
+    if (__any_sync(0xffffffffu, oob) && lane_id() == 0) atomicOr(&ctr->oob, 1u);
+    commits = warp_sum(commits);
+    aborts = warp_sum(aborts);
+    livelocks = warp_sum(livelocks);
+    if (lane_id() == 0) {
+        if (commits) atomicAdd(&ctr->committed, commits);
+        if (aborts) atomicAdd(&ctr->aborts, aborts);
+        if (livelocks) atomicAdd(&ctr->livelocked, livelocks);
+    }
+}
+
+// Bank transfer: read 4 accounts, acct0 -= amount, acct1 += amount.
+__global__ void __launch_bounds__(kTxThreads) bank_batch_kernel(ShardView v, LockTable lt, const hetm_bank_tx* __restrict__ in,
+                                                                uint64_t n, unsigned long long* __restrict__ tickets,
+                                                                DevCounters* ctr, uint32_t max_attempts) {
+    unsigned long long commits = 0, aborts = 0, livelocks = 0;
+    unsigned oob = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
+        const uint64_t w01 = __ldg(rec), w23 = __ldg(rec + 1), amount = __ldg(rec + 2);
+        const uint64_t loc[4] = {(w01 & 0xffffffffu) - v.base, (w01 >> 32) - v.base, (w23 & 0xffffffffu) - v.base,
+                                 (w23 >> 32) - v.base};
+        if (loc[0] >= v.size_words || loc[1] >= v.size_words || loc[2] >= v.size_words || loc[3] >= v.size_words) {
+            tickets[i] = ~0ull;  // outside this shard: rejected, reported as OutOfBounds
+            oob = 1;
+            continue;
+        }
+        DeviceTx<4, 2> tx;
+        uint32_t attempt = 0;
+        for (;;) {
+            ++attempt;
+            tx.begin((uint32_t)(i + 1));
+            uint64_t val[4];
+            unsigned long long t;
+            if (tm_read_n(tx, v, lt, loc, val)) {
+                tm_write(tx, v, lt, loc[0], val[0] - amount);
+                tm_write(tx, v, lt, loc[1], val[1] + amount);
+                if (tm_commit(tx, v, lt, &ctr->ticket, t)) {
+                    tickets[i] = t;
+                    tm_mark_bitmaps(tx, v);
+                    ++commits;
+                    break;
+                }
+            }
+            ++aborts;
+            if (attempt >= max_attempts) {
+                tickets[i] = ~0ull;
+                ++livelocks;
+                break;
+            }
+        }
+    }
+    flush_batch_counters(commits, aborts, livelocks, oob, ctr);
+}
+
+// Generic <=4 reads / <=2 read-modify-writes (hetm_rw_tx).
+__global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, LockTable lt, const hetm_rw_tx* __restrict__ in,
+                                                              uint64_t n, unsigned long long* __restrict__ tickets,
+                                                              DevCounters* ctr, uint32_t max_attempts) {
+    unsigned long long commits = 0, aborts = 0, livelocks = 0;
+    unsigned oob = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const hetm_rw_tx r = in[i];
+        const uint32_t nr = r.nr < 4 ? r.nr : 4, nw = r.nw < 2 ? r.nw : 2;
+        bool in_shard = true;
+        for (uint32_t j = 0; j < nr; ++j) in_shard &= (r.r_addr[j] - v.base) < v.size_words;
+        for (uint32_t j = 0; j < nw; ++j) in_shard &= (r.w_addr[j] - v.base) < v.size_words;
+        if (!in_shard) {
+            tickets[i] = ~0ull;
+            oob = 1;
+            continue;
+        }
+        DeviceTx<6, 2> tx;
+        uint32_t attempt = 0;
+        for (;;) {
+            ++attempt;
+            tx.begin((uint32_t)(i + 1));
+            bool ok = true;
+            uint64_t sum = 0;
+            for (uint32_t j = 0; j < nr && ok; ++j) {
+                uint64_t x;
+                ok = tm_read(tx, v, lt, r.r_addr[j] - v.base, x);
+                sum += x;
+            }
+            for (uint32_t j = 0; j < nw && ok; ++j) {
+                uint64_t cur;
+                const uint64_t loc = r.w_addr[j] - v.base;
+                ok = tm_read(tx, v, lt, loc, cur) && tm_write(tx, v, lt, loc, cur + r.add[j] + sum);
+            }
+            unsigned long long t;
+            if (ok && tm_commit(tx, v, lt, &ctr->ticket, t)) {
+                tickets[i] = t;
+                tm_mark_bitmaps(tx, v);
+                ++commits;
+                break;
+            }
+            ++aborts;
+            if (attempt >= max_attempts) {
+                tickets[i] = ~0ull;
+                ++livelocks;
+                break;
+            }
+        }
+    }
+    flush_batch_counters(commits, aborts, livelocks, oob, ctr);
+}
+
+static unsigned grid_for(uint64_t n, int threads, int blocks_per_sm, int sms) {
+    uint64_t want = (n + threads - 1) / threads;
+    uint64_t cap = (uint64_t)blocks_per_sm * (uint64_t)sms;
+    if (want > cap) want = cap;
+    return (unsigned)(want ? want : 1);
+}
+
+cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const hetm_bank_tx* d_in, uint64_t n,
+                              unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
+                              const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    bank_batch_kernel<<<grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count), kTxThreads, 0, s>>>(
+        v, lt, d_in, n, d_tickets, ctr, max_attempts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rw_batch(const ShardView& v, const LockTable& lt, const hetm_rw_tx* d_in, uint64_t n,
+                            unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
+                            const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    rw_batch_kernel<<<grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count), kTxThreads, 0, s>>>(
+        v, lt, d_in, n, d_tickets, ctr, max_attempts);
+    return cudaGetLastError();
+}
+
+int query_tx_occupancy(int* bank_blocks) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bank_batch_kernel, kTxThreads, 0) != cudaSuccess) return -1;
+    *bank_blocks = b;
+    return 0;
+}
+
+}  // namespace hetm_b200
