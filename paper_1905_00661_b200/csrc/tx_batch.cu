@@ -7,6 +7,7 @@
 // REDG.E.OR.64 and records the transaction's commit ticket.
 #include "common.cuh"
 #include "device_tm.cuh"
+#include "phased_tx.cuh"
 #include "kernels.h"
 
 namespace hetm_b200 {
@@ -27,46 +28,61 @@ __device__ __forceinline__ void flush_batch_counters(unsigned long long commits,
 }
 
 // Bank transfer: read 4 accounts, acct0 -= amount, acct1 += amount.
-__global__ void __launch_bounds__(kTxThreads) bank_batch_kernel(ShardView v, LockTable lt, const hetm_bank_tx* __restrict__ in,
-                                                                uint64_t n, unsigned long long* __restrict__ tickets,
-                                                                DevCounters* ctr, uint32_t max_attempts) {
+// Warp-phased commit (phased_tx.cuh); each lane keeps its transaction across
+// retries and moves to the next one (grid stride) once it commits.
+__global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, LockTable lt,
+                                                                   const hetm_bank_tx* __restrict__ in, uint64_t n,
+                                                                   unsigned long long* __restrict__ tickets,
+                                                                   DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
-        const uint64_t w01 = __ldg(rec), w23 = __ldg(rec + 1), amount = __ldg(rec + 2);
-        const uint64_t loc[4] = {(w01 & 0xffffffffu) - v.base, (w01 >> 32) - v.base, (w23 & 0xffffffffu) - v.base,
-                                 (w23 >> 32) - v.base};
-        if (loc[0] >= v.size_words || loc[1] >= v.size_words || loc[2] >= v.size_words || loc[3] >= v.size_words) {
-            tickets[i] = ~0ull;  // outside this shard: rejected, reported as OutOfBounds
-            oob = 1;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t attempts = 0;
+    bool loaded = false;
+    uint64_t amount = 0;
+    StaticTx<4, 2> tx;
+    while (__any_sync(0xffffffffu, i < n)) {
+        if (i < n && !loaded) {
+            const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
+            const uint64_t w01 = __ldg(rec), w23 = __ldg(rec + 1);
+            amount = __ldg(rec + 2);
+            tx.loc[0] = (w01 & 0xffffffffu) - v.base;
+            tx.loc[1] = (w01 >> 32) - v.base;
+            tx.loc[2] = (w23 & 0xffffffffu) - v.base;
+            tx.loc[3] = (w23 >> 32) - v.base;
+            if (tx.loc[0] >= v.size_words || tx.loc[1] >= v.size_words || tx.loc[2] >= v.size_words ||
+                tx.loc[3] >= v.size_words) {
+                tickets[i] = ~0ull;  // outside this shard: rejected, reported as OutOfBounds
+                oob = 1;
+                i += stride;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) tx.lk[k] = lt.index(tx.loc[k]);
+                loaded = true;
+            }
+        }
+        const bool active = i < n && loaded;
+        unsigned long long t = 0;
+        const bool committed = phased_attempt(tx, active, (uint32_t)(i + 1), v, lt, &ctr->ticket, t,
+                                              [&](StaticTx<4, 2>& x) {
+                                                  x.wval[0] = x.val[0] - amount;
+                                                  x.wval[1] = x.val[1] + amount;
+                                              });
+        if (committed) {
+            tickets[i] = t;
+            ++commits;
+        } else if (active) {
+            ++aborts;
+            if (++attempts < max_attempts) continue;
+            tickets[i] = ~0ull;
+            ++livelocks;
+        } else {
             continue;
         }
-        DeviceTx<4, 2> tx;
-        uint32_t attempt = 0;
-        for (;;) {
-            ++attempt;
-            tx.begin((uint32_t)(i + 1));
-            uint64_t val[4];
-            unsigned long long t;
-            if (tm_read_n(tx, v, lt, loc, val)) {
-                tm_write(tx, v, lt, loc[0], val[0] - amount);
-                tm_write(tx, v, lt, loc[1], val[1] + amount);
-                if (tm_commit(tx, v, lt, &ctr->ticket, t)) {
-                    tickets[i] = t;
-                    tm_mark_bitmaps(tx, v);
-                    ++commits;
-                    break;
-                }
-            }
-            ++aborts;
-            if (attempt >= max_attempts) {
-                tickets[i] = ~0ull;
-                ++livelocks;
-                break;
-            }
-        }
+        i += stride;
+        loaded = false;
+        attempts = 0;
     }
     flush_batch_counters(commits, aborts, livelocks, oob, ctr);
 }
