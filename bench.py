@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--log-entries", type=int, default=1 << 20)
     p.add_argument("--gran", type=int, default=1024)
     p.add_argument("--lock-entries", type=int, default=0)
+    p.add_argument("--l2-fetch32", action="store_true", help="cudaLimitMaxL2FetchGranularity = 32 B")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -164,7 +165,7 @@ def run_ours(args):
     n_steps = K + WU
 
     dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, lock_entries=args.lock_entries,
-                         device=local, log_capacity=max(L, 1 << 20))
+                         device=local, log_capacity=max(L, 1 << 20), l2_fetch_32=args.l2_fetch32)
     dev.register_kernel(hetm.KERNEL_BANK)
     init = np.full(W, 1000, np.uint64)
     dev.upload(hetm.REPLICA_DEV, base, init)
@@ -197,15 +198,10 @@ def run_ours(args):
     s_val = dev.stream_handle(2)
     ex = torch.cuda.ExternalStream(s_exec)
     vs = torch.cuda.ExternalStream(s_val)
-    ev = {k: [torch.cuda.Event(enable_timing=True) for _ in range(K)] for k in ["b0", "b1", "v0", "v1"]}
 
     def step(j, timed_idx=None):
         tb = tx_d[j % n_bufs]
-        if timed_idx is not None:
-            ev["b0"][timed_idx].record(ex)
         dev.execute_batch_dptr(hetm.KERNEL_BANK, tb.data_ptr(), B, tickets.data_ptr(), s_exec)
-        if timed_idx is not None:
-            ev["b1"][timed_idx].record(ex)
         lg = log_d[j]
         n_local = L
         src = lg
@@ -219,12 +215,7 @@ def run_ours(args):
                 n_local = sum(outs)
                 dist.all_to_all_single(recv[:n_local], routed, outs, ins)
                 src = recv
-        if timed_idx is not None:
-            vs.wait_event(ev["b1"][timed_idx])  # start the validation clock after the batch
-            ev["v0"][timed_idx].record(vs)
         dev.validate_dptr(src.data_ptr(), n_local, hetm.APPLY, s_val)
-        if timed_idx is not None:
-            ev["v1"][timed_idx].record(vs)
         dev.clear_round(asynchronous=True)
         return n_local
 
@@ -248,6 +239,8 @@ def run_ours(args):
             if j % 8 == 0:
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
+        dev.timing(0), dev.timing(1)
+        dev.set_timing(True)  # CUDA-event brackets around every batch / validation launch
         start.record(ex)
         for i in range(K):
             n_val += step(WU + i, i)
@@ -265,8 +258,10 @@ def run_ours(args):
     ms_total = start.elapsed_time(stop)
     conflict, st = dev.read_counters()
     assert not conflict
-    batch_ms = statistics.mean(ev["b0"][i].elapsed_time(ev["b1"][i]) for i in range(K))
-    val_ms = statistics.mean(ev["v0"][i].elapsed_time(ev["v1"][i]) for i in range(K))
+    bt, bc = dev.timing(0)
+    vt, vc = dev.timing(1)
+    dev.set_timing(False)
+    batch_ms, val_ms = bt / max(bc, 1), vt / max(vc, 1)
     if dist:
         t = torch.tensor([ms_total, batch_ms, val_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

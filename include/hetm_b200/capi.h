@@ -86,6 +86,7 @@ enum hetm_kernel_id {
 
 /* hetm_dev_config.flags */
 #define HETM_CFG_NO_SHADOW 1u /* do not allocate devShadow (validation-only sweeps) */
+#define HETM_CFG_L2_FETCH_32 2u /* cudaLimitMaxL2FetchGranularity = 32 B (random 8-B word access) */
 
 /* ------------------------------------------------------------ wire types -- */
 
@@ -288,6 +289,12 @@ int hetm_dev_route_log_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t 
                             void* stream);
 /* Streams owned by the handle: 0 = execution, 1 = log copy, 2 = validation, 3 = merge. */
 int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
+/* Per-kernel device timing (CUDA events around every batch / validation
+ * launch of this handle).  which: 0 = batch kernels, 1 = validation kernels.
+ * hetm_dev_timing waits for the recorded launches, returns their summed
+ * duration and count, and resets the accumulator. */
+int hetm_dev_set_timing(hetm_dev* dev, int on);
+int hetm_dev_timing(hetm_dev* dev, int which, double* total_ms, uint64_t* count);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
 

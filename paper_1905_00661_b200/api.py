@@ -22,6 +22,7 @@ KERNEL_BANK, KERNEL_RW = 1, 2
 CLEAR_RESET_TS = 1
 CLEAR_ASYNC = 2
 CFG_NO_SHADOW = 1
+CFG_L2_FETCH_32 = 2
 H2D, D2H, D2D = 0, 1, 2  # BusDir, bus.hpp:16
 TAG_LOG, TAG_MERGE, TAG_SHADOW, TAG_ROLLBACK, TAG_INPUT, TAG_OUTPUT, TAG_RAW = range(7)
 
@@ -159,7 +160,7 @@ class GpuDevice:
 
     def __init__(self, size_words: int, *, shard_base: int = 0, rs_gran_bytes: int = 1024,
                  chunk_bytes: int = 16384, lock_entries: int = 0, log_capacity: int = 0,
-                 max_attempts: int = 0, device: int = 0, shadow: bool = True):
+                 max_attempts: int = 0, device: int = 0, shadow: bool = True, l2_fetch_32: bool = False):
         cfg = _lib.DevConfig()
         lib.hetm_dev_config_default(C.byref(cfg))
         cfg.size_words = size_words
@@ -170,7 +171,7 @@ class GpuDevice:
         cfg.log_capacity = log_capacity
         cfg.max_attempts = max_attempts
         cfg.device = device
-        cfg.flags = 0 if shadow else CFG_NO_SHADOW
+        cfg.flags = (0 if shadow else CFG_NO_SHADOW) | (CFG_L2_FETCH_32 if l2_fetch_32 else 0)
         h = C.c_void_p()
         check(lib.hetm_dev_open(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -348,6 +349,15 @@ class GpuDevice:
         s = C.c_void_p()
         self._chk(lib.hetm_dev_stream_handle(self.h, which, C.byref(s)))
         return s.value or 0
+
+    def set_timing(self, on: bool = True):
+        self._chk(lib.hetm_dev_set_timing(self.h, int(on)))
+
+    def timing(self, which: int):
+        """(total_ms, launches) of batch (0) or validation (1) kernels since the last call."""
+        t, c = C.c_double(), C.c_uint64()
+        self._chk(lib.hetm_dev_timing(self.h, which, C.byref(t), C.byref(c)))
+        return t.value, c.value
 
     def flush_l2(self, stream: int = 0):
         self._chk(lib.hetm_dev_flush_l2(self.h, stream or None))

@@ -82,6 +82,20 @@ struct hetm_dev {
     uint64_t bytes_alloc = 0;
     uint64_t l2_bytes = 0;
     hetm_batch_stats last_batch{};
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tpairs[2];  // recorded launch brackets
+    std::vector<cudaEvent_t> tpool;
+
+    cudaEvent_t tev() {
+        if (!tpool.empty()) {
+            cudaEvent_t e = tpool.back();
+            tpool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
 
     ShardView view() const {
         ShardView v;
@@ -173,6 +187,12 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
     CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
     cudaError_t e = cudaSuccess;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (d->timing) {
+        t0 = d->tev();
+        t1 = d->tev();
+        CK(d, cudaEventRecord(t0, s));
+    }
     if (kernel_id == HETM_KERNEL_BANK)
         e = launch_bank_batch(d->view(), d->locks(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets,
                               d->d_ctr, d->max_attempts, d->geom, s);
@@ -180,8 +200,28 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
         e = launch_rw_batch(d->view(), d->locks(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                             d->max_attempts, d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "batch kernel launch");
+    if (d->timing) {
+        CK(d, cudaEventRecord(t1, s));
+        d->tpairs[0].emplace_back(t0, t1);
+    }
     CK(d, cudaEventRecord(d->ev_exec, s));
     return HETM_OK;
+}
+
+// Validation launch with optional timing brackets.
+cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, int apply, cudaStream_t s) {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (d->timing && n) {
+        t0 = d->tev();
+        t1 = d->tev();
+        cudaEventRecord(t0, s);
+    }
+    cudaError_t e = launch_validate(d->view(), d->d_ts, log, n, apply, d->ts_floor, d->d_ctr, d->geom, s);
+    if (d->timing && n) {
+        cudaEventRecord(t1, s);
+        d->tpairs[1].emplace_back(t0, t1);
+    }
+    return e;
 }
 
 int ensure_arena(hetm_dev* d, uint64_t need) {
@@ -257,8 +297,7 @@ int enqueue_deferred_apply(hetm_dev* d) {
     if (d->deferred.empty()) return HETM_OK;
     CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
     for (auto& r : d->deferred) {
-        cudaError_t e = launch_validate(d->view(), d->d_ts, d->d_arena + r.first, r.second - r.first, 1, d->ts_floor,
-                                        d->d_ctr, d->geom, d->s_val);
+        cudaError_t e = timed_validate(d, d->d_arena + r.first, r.second - r.first, 1, d->s_val);
         if (e != cudaSuccess) return fail(d, e, "validate(apply deferred)");
     }
     d->deferred.clear();
@@ -355,6 +394,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
         return rc;
     };
     if (cudaSetDevice(d->device) != cudaSuccess) return bail(fail(d, cudaGetLastError(), "cudaSetDevice"));
+    if (cfg->flags & HETM_CFG_L2_FETCH_32) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
     int rc;
     if ((rc = dev_alloc(d, (void**)&d->d_stmr, d->W * 8))) return bail(rc);
     if (!(cfg->flags & HETM_CFG_NO_SHADOW))
@@ -417,6 +457,12 @@ int hetm_dev_close(hetm_dev* d) {
                     d->d_in, (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
+    for (auto& v : d->tpairs)
+        for (auto& pr : v) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+    for (cudaEvent_t e : d->tpool) cudaEventDestroy(e);
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1})
@@ -640,7 +686,7 @@ int hetm_dev_stream_chunk(hetm_dev* d, const hetm_log_entry* entries, uint64_t n
     CK(d, cudaStreamWaitEvent(d->s_val, d->ev_round, 0));
     const bool apply = mode == HETM_APPLY;
     if (apply) CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));  // apply only after execution
-    cudaError_t e = launch_validate(d->view(), d->d_ts, dst, n, apply ? 1 : 0, d->ts_floor, d->d_ctr, d->geom, d->s_val);
+    cudaError_t e = timed_validate(d, dst, n, apply ? 1 : 0, d->s_val);
     if (e != cudaSuccess) return fail(d, e, "validate launch");
     CK(d, cudaMemcpyAsync(&d->h_ctr->conflict, &d->d_ctr->conflict, sizeof(unsigned), cudaMemcpyDeviceToHost,
                           d->s_val));
@@ -674,8 +720,7 @@ int hetm_dev_round_verdict(hetm_dev* d, int* conflict) {
     if (!d->deferred.empty() && !d->deferred_final) {
         CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
         for (auto& r : d->deferred) {
-            cudaError_t e = launch_validate(d->view(), d->d_ts, d->d_arena + r.first, r.second - r.first, 0,
-                                            d->ts_floor, d->d_ctr, d->geom, d->s_val);
+            cudaError_t e = timed_validate(d, d->d_arena + r.first, r.second - r.first, 0, d->s_val);
             if (e != cudaSuccess) return fail(d, e, "validate(final)");
         }
         d->deferred_final = true;
@@ -921,8 +966,7 @@ int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_
         d->round_applied = true;
         d->shadow_synced = false;  // entries are not retained in the arena for the shadow patch
     }
-    cudaError_t e = launch_validate(d->view(), d->d_ts, d_entries, n, mode == HETM_APPLY, d->ts_floor, d->d_ctr,
-                                    d->geom, s);
+    cudaError_t e = timed_validate(d, d_entries, n, mode == HETM_APPLY, s);
     if (e != cudaSuccess) return fail(d, e, "validate_dptr");
     if (stream) CK(d, cudaEventRecord(d->ev_val, s));
     return HETM_OK;
@@ -968,6 +1012,31 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
     cudaStream_t s[5] = {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h};
     if (which < 0 || which > 4) return HETM_ERR_INVALID_ARG;
     *stream = s[which];
+    return HETM_OK;
+}
+
+int hetm_dev_set_timing(hetm_dev* d, int on) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    d->timing = on != 0;
+    return HETM_OK;
+}
+
+int hetm_dev_timing(hetm_dev* d, int which, double* total_ms, uint64_t* count) {
+    if (!d || which < 0 || which > 1) return HETM_ERR_INVALID_ARG;
+    double tot = 0;
+    uint64_t c = 0;
+    for (auto& pr : d->tpairs[which]) {
+        CK(d, cudaEventSynchronize(pr.second));
+        float ms = 0.f;
+        CK(d, cudaEventElapsedTime(&ms, pr.first, pr.second));
+        tot += ms;
+        ++c;
+        d->tpool.push_back(pr.first);
+        d->tpool.push_back(pr.second);
+    }
+    d->tpairs[which].clear();
+    if (total_ms) *total_ms = tot;
+    if (count) *count = c;
     return HETM_OK;
 }
 

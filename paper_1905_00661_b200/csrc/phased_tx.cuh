@@ -166,12 +166,13 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     for (int k = NW; k < NR; ++k)
         if (stolen_mask & (1u << k))
             atomicCAS(&lt.words[tx.lk[k]], lk_make(me, lk_ver(tx.l[k])), lk_make(0, lk_ver(tx.l[k])));
+    // fire-and-forget REDs: they drain while the next attempt's loads are in flight
 #pragma unroll
-    for (int k = 0; k < NR; ++k) set_bit_probe(v.rs, tx.loc[k] >> v.gran_shift);
+    for (int k = 0; k < NR; ++k) set_bit(v.rs, tx.loc[k] >> v.gran_shift);
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
-        set_bit_probe(v.ws, tx.loc[j] >> v.gran_shift);
-        set_bit_probe(v.chunk, tx.loc[j] >> v.chunk_shift);
+        set_bit(v.ws, tx.loc[j] >> v.gran_shift);
+        set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
     }
     ticket = t;
     return true;
