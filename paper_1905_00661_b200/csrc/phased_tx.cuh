@@ -52,7 +52,11 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 
 // One phased attempt for every lane with `active`; returns true on commit and
 // sets `ticket`.  All 32 lanes of the warp must call it together.
-template <int NR, int NW, class Compute>
+// Knock-out bits for profiling experiments only (HETM_KNOCKOUT env var; 0 in
+// production): they remove protocol steps and break serializability.
+enum : int { KO_TICKET = 1, KO_FENCE = 2, KO_BITMAPS = 4, KO_FINALIZE = 8, KO_PRELOCK = 16, KO_LOCKLOAD = 32 };
+
+template <int NR, int NW, int KO = 0, class Compute>
 __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active, uint32_t me, const ShardView& v,
                                                const LockTable& lt, unsigned long long* ticket_ctr,
                                                unsigned long long& ticket, Compute compute) {
@@ -60,7 +64,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     // ---- P1: lock words
     if (ok) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) tx.l[k] = ld_relaxed(&lt.words[tx.lk[k]]);
+        for (int k = 0; k < NR; ++k) tx.l[k] = (KO & KO_LOCKLOAD) ? 0ull : ld_relaxed(&lt.words[tx.lk[k]]);
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             ok &= !(tx.l[k] & kLockFinal);
@@ -86,7 +90,9 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             bool dup = false;
 #pragma unroll
             for (int q = 0; q < j; ++q) dup |= (tx.lk[q] == tx.lk[j]);
-            prev[j] = dup ? tx.l[j] : atomicCAS(&lt.words[tx.lk[j]], tx.l[j], lk_make(me, lk_ver(tx.l[j])));
+            prev[j] = (dup || (KO & KO_PRELOCK)) ? tx.l[j]
+                                                 : atomicCAS(&lt.words[tx.lk[j]], tx.l[j], lk_make(me, lk_ver(tx.l[j])));
+            if (KO & KO_PRELOCK) dup = false;
             held[j] = !dup && prev[j] == tx.l[j];
             ok &= dup || held[j];
         }
@@ -97,7 +103,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
     }
     // ---- P3: ticket (after every surviving lane's claims are performed)
-    const unsigned long long t = warp_ticket(ok, ticket_ctr);
+    const unsigned long long t = (KO & KO_TICKET) ? (unsigned long long)me : warp_ticket(ok, ticket_ctr);
     // ---- P4: validate read-only entries || finalize write entries
     bool fin[NW];
 #pragma unroll
@@ -119,7 +125,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         for (int j = 0; j < NW; ++j) {
             const unsigned long long exp = lk_make(me, lk_ver(tx.l[j]));
             if (held[j]) {
-                fprev[j] = atomicCAS(&lt.words[tx.lk[j]], exp, exp | kLockFinal);
+                fprev[j] = (KO & KO_FINALIZE) ? exp : atomicCAS(&lt.words[tx.lk[j]], exp, exp | kLockFinal);
                 fin[j] = fprev[j] == exp;
                 ok &= fin[j];
             }
@@ -157,7 +163,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     compute(tx);
 #pragma unroll
     for (int j = 0; j < NW; ++j) st_relaxed(&v.stmr[tx.loc[j]], tx.wval[j]);
-    fence_acq_rel();
+    if (!(KO & KO_FENCE)) fence_acq_rel();
     const uint32_t nv = (uint32_t)(t + 1);
 #pragma unroll
     for (int j = 0; j < NW; ++j)
@@ -167,12 +173,14 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         if (stolen_mask & (1u << k))
             atomicCAS(&lt.words[tx.lk[k]], lk_make(me, lk_ver(tx.l[k])), lk_make(0, lk_ver(tx.l[k])));
     // fire-and-forget REDs: they drain while the next attempt's loads are in flight
+    if constexpr ((KO & KO_BITMAPS) == 0) {
 #pragma unroll
-    for (int k = 0; k < NR; ++k) set_bit(v.rs, tx.loc[k] >> v.gran_shift);
+        for (int k = 0; k < NR; ++k) set_bit(v.rs, tx.loc[k] >> v.gran_shift);
 #pragma unroll
-    for (int j = 0; j < NW; ++j) {
-        set_bit(v.ws, tx.loc[j] >> v.gran_shift);
-        set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
+        for (int j = 0; j < NW; ++j) {
+            set_bit(v.ws, tx.loc[j] >> v.gran_shift);
+            set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
+        }
     }
     ticket = t;
     return true;

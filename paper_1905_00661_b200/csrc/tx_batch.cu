@@ -5,6 +5,8 @@
 // attempts until commit or the livelock budget.  Commit
 // fuses the RS/WS/ChunkMap instrumentation as fire-and-forget
 // REDG.E.OR.64 and records the transaction's commit ticket.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "device_tm.cuh"
 #include "phased_tx.cuh"
@@ -30,6 +32,7 @@ __device__ __forceinline__ void flush_batch_counters(unsigned long long commits,
 // Bank transfer: read 4 accounts, acct0 -= amount, acct1 += amount.
 // Warp-phased commit (phased_tx.cuh); each lane keeps its transaction across
 // retries and moves to the next one (grid stride) once it commits.
+template <int KO>
 __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, LockTable lt,
                                                                    const hetm_bank_tx* __restrict__ in, uint64_t n,
                                                                    unsigned long long* __restrict__ tickets,
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
         }
         const bool active = i < n && loaded;
         unsigned long long t = 0;
-        const bool committed = phased_attempt(tx, active, (uint32_t)(i + 1), v, lt, &ctr->ticket, t,
+        const bool committed = phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, lt, &ctr->ticket, t,
                                               [&](StaticTx<4, 2>& x) {
                                                   x.wval[0] = x.val[0] - amount;
                                                   x.wval[1] = x.val[1] + amount;
@@ -151,8 +154,19 @@ cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const het
                               unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
                               const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    bank_batch_kernel<<<grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count), kTxThreads, 0, s>>>(
-        v, lt, d_in, n, d_tickets, ctr, max_attempts);
+    static const int ko = [] {
+        const char* e = std::getenv("HETM_KNOCKOUT");  // profiling experiments only
+        return e ? std::atoi(e) : 0;
+    }();
+    const unsigned grid = grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count);
+#define HETM_KO_CASE(K) \
+    case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, lt, d_in, n, d_tickets, ctr, max_attempts); break;
+    switch (ko) {
+        HETM_KO_CASE(1) HETM_KO_CASE(2) HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(32)
+        HETM_KO_CASE(7) HETM_KO_CASE(63)
+        default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, lt, d_in, n, d_tickets, ctr, max_attempts);
+    }
+#undef HETM_KO_CASE
     return cudaGetLastError();
 }
 
@@ -167,7 +181,8 @@ cudaError_t launch_rw_batch(const ShardView& v, const LockTable& lt, const hetm_
 
 int query_tx_occupancy(int* bank_blocks) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bank_batch_kernel, kTxThreads, 0) != cudaSuccess) return -1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bank_batch_kernel<0>, kTxThreads, 0) != cudaSuccess)
+        return -1;
     *bank_blocks = b;
     return 0;
 }

@@ -1,4 +1,6 @@
 // validate.cu — inter-device validation and TS-guarded apply (engine module).
+// (the TS lock bit of SPEC.md:320 is kept in the word layout but never set:
+//  the two-pass max/winner scheme below needs no lock.)
 //
 // validateChunk: for each host write-log
 // entry <addr,value,ts>:
@@ -17,23 +19,21 @@ namespace hetm_b200 {
 constexpr int kValThreads = 256;
 constexpr unsigned long long kTsLock = 1ull << 63;  // TsArray lockBit
 
-__device__ __forceinline__ void ts_guarded_apply(uint64_t* stmr, unsigned long long* ts_arr, uint64_t loc,
-                                                 uint64_t value, uint64_t ts) {
-    unsigned long long cur = ld_relaxed(&ts_arr[loc]);
-    for (;;) {
-        if (cur & kTsLock) {  // another entry for this word is mid-apply
-            cur = ld_relaxed(&ts_arr[loc]);
-            continue;
-        }
-        if (cur >= ts) return;  // not fresher than what is applied
-        unsigned long long prev = atomicCAS(&ts_arr[loc], cur, cur | kTsLock);
-        if (prev == cur) {
-            st_relaxed(&stmr[loc], value);
-            st_release(&ts_arr[loc], ts);  // value store ordered before unlock
-            return;
-        }
-        cur = prev;
-    }
+// Two lock-free passes per chunk replace the paper's per-entry TS lock bit
+// (PAPER.md:330): pass A raises TS[addr] to the freshest ts with a
+// fire-and-forget REDG.E.MAX.64; pass B stores the value of the entry whose ts
+// equals TS[addr] — the unique maximum, so the outcome equals SPEC.md:348's
+// "apply iff entry.ts > TS.ts" in any delivery order.  Apply-mode chunks are
+// serialised on one stream, so every pass B sees all earlier pass A's.
+constexpr int kUnroll = 4;
+
+struct EntryRegs {
+    uint64_t addr, value, ts;
+};
+
+__device__ __forceinline__ EntryRegs load_entry(const hetm_log_entry* log, uint64_t i) {
+    const uint64_t* e = reinterpret_cast<const uint64_t*>(log + i);
+    return EntryRegs{__ldg(e), __ldg(e + 1), __ldg(e + 2)};
 }
 
 template <bool kApply>
@@ -42,16 +42,25 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, unsi
                                                                uint64_t ts_floor, DevCounters* ctr) {
     unsigned conflict = 0, bad = 0, oob = 0;
     unsigned long long maxts = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint64_t* e = reinterpret_cast<const uint64_t*>(log + i);
-        const uint64_t addr = __ldg(e), value = __ldg(e + 1), ts = __ldg(e + 2);
-        const uint64_t loc = addr - v.base;
-        if (loc >= v.size_words) { oob = 1; continue; }
-        conflict |= (unsigned)((v.rs[loc >> v.gran_shift >> 6] >> ((loc >> v.gran_shift) & 63)) & 1ull);
-        bad |= (ts <= ts_floor);
-        maxts = ts > maxts ? ts : maxts;
-        if (kApply) ts_guarded_apply(v.stmr, ts_arr, loc, value, ts);
+    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
+        EntryRegs e[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base + v.size_words, 0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (i0 + (uint64_t)u * blockDim.x >= n) continue;
+            const uint64_t loc = e[u].addr - v.base;
+            if (loc >= v.size_words) { oob = 1; continue; }
+            const uint64_t bit = loc >> v.gran_shift;
+            conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
+            bad |= (e[u].ts <= ts_floor);
+            maxts = e[u].ts > maxts ? e[u].ts : maxts;
+            if (kApply) atomicMax(&ts_arr[loc], (unsigned long long)e[u].ts);  // (b) pass A
+        }
     }
     conflict = __any_sync(0xffffffffu, conflict);
     bad = __any_sync(0xffffffffu, bad);
@@ -69,16 +78,27 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, unsi
     }
 }
 
-// dst[addr] = value iff TS[addr] == ts: the unique freshest entry per word.
-__global__ void winner_apply_kernel(uint64_t* dst, uint64_t base, uint64_t size_words,
-                                    const unsigned long long* __restrict__ ts_arr,
-                                    const hetm_log_entry* __restrict__ log, uint64_t n) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint64_t* e = reinterpret_cast<const uint64_t*>(log + i);
-        const uint64_t loc = __ldg(e) - base;
-        if (loc >= size_words) continue;
-        if ((ts_arr[loc] & ~kTsLock) == __ldg(e + 2)) dst[loc] = __ldg(e + 1);
+// Pass B / rollback / shadow patch: dst[addr] = value iff TS[addr] == ts.
+__global__ void __launch_bounds__(kValThreads) winner_apply_kernel(uint64_t* dst, uint64_t base, uint64_t size_words,
+                                                                   const unsigned long long* __restrict__ ts_arr,
+                                                                   const hetm_log_entry* __restrict__ log, uint64_t n) {
+    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
+        EntryRegs e[kUnroll];
+        unsigned long long cur[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+            e[u] = i < n ? load_entry(log, i) : EntryRegs{base + size_words, 0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t loc = e[u].addr - base;
+            cur[u] = loc < size_words ? ld_relaxed(&ts_arr[loc]) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if ((cur[u] & ~kTsLock) == e[u].ts) dst[e[u].addr - base] = e[u].value;
     }
 }
 
@@ -123,18 +143,21 @@ static unsigned grid_cap(uint64_t n, int threads, const LaunchGeom& g, int per_s
 cudaError_t launch_validate(const ShardView& v, unsigned long long* d_ts, const hetm_log_entry* d_log, uint64_t n,
                             int apply, uint64_t ts_floor, DevCounters* ctr, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    unsigned grid = grid_cap(n, kValThreads, g, g.max_blocks_val);
-    if (apply)
+    const unsigned grid = grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
+    if (apply) {
         validate_kernel<true><<<grid, kValThreads, 0, s>>>(v, d_ts, d_log, n, ts_floor, ctr);
-    else
+        winner_apply_kernel<<<grid, kValThreads, 0, s>>>(v.stmr, v.base, v.size_words, d_ts, d_log, n);
+    } else {
         validate_kernel<false><<<grid, kValThreads, 0, s>>>(v, d_ts, d_log, n, ts_floor, ctr);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_winner_apply(uint64_t* dst, uint64_t base, uint64_t size_words, const unsigned long long* d_ts,
                                 const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    winner_apply_kernel<<<grid_cap(n, 256, g, 8), 256, 0, s>>>(dst, base, size_words, d_ts, d_log, n);
+    winner_apply_kernel<<<grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val), kValThreads, 0, s>>>(
+        dst, base, size_words, d_ts, d_log, n);
     return cudaGetLastError();
 }
 
