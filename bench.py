@@ -49,7 +49,6 @@ def parse():
     p.add_argument("--batch", type=int, default=1 << 20)
     p.add_argument("--log-entries", type=int, default=1 << 20)
     p.add_argument("--gran", type=int, default=1024)
-    p.add_argument("--lock-entries", type=int, default=0)
     p.add_argument("--l2-fetch32", action="store_true", help="cudaLimitMaxL2FetchGranularity = 32 B")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--cpu-seconds", type=float, default=8.0)
@@ -164,8 +163,7 @@ def run_ours(args):
     K, WU = args.steps, args.warmup
     n_steps = K + WU
 
-    dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, lock_entries=args.lock_entries,
-                         device=local, log_capacity=max(L, 1 << 20), l2_fetch_32=args.l2_fetch32)
+    dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, device=local, log_capacity=max(L, 1 << 20), l2_fetch_32=args.l2_fetch32)
     dev.register_kernel(hetm.KERNEL_BANK)
     init = np.full(W, 1000, np.uint64)
     dev.upload(hetm.REPLICA_DEV, base, init)
@@ -291,7 +289,7 @@ def run_ours(args):
                         "uniform, RS/WS gran 1 KiB; round host log 2^20 entries on the host halves, "
                         "validated+applied (routed by owner shard over NCCL when G>1)",
             "stmr_words_per_gpu": W, "batch_tx": B, "log_entries_per_gpu": L, "rs_gran_bytes": args.gran,
-            "lock_entries": int(dev.info().lock_entries), "parallelism": f"shard{world}",
+            "stmr_layout": "32-B word cells {value, lock, ts, spare}", "parallelism": f"shard{world}",
             "l2": "inputs larger than L2: 1 GiB STMR per GPU, rotating per-step input buffers "
                   f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
         },
@@ -374,8 +372,7 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
         p.free()
     return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
-            "timing": "host wall clock around full synchronous rounds (pinned buffers; verdict + merge D2H)",
-            "lock_entries": int(info.lock_entries)}
+            "timing": "host wall clock around full synchronous rounds (pinned buffers; verdict + merge D2H)"}
 
 
 # ---------------------------------------------------------- CPU baseline

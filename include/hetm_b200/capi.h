@@ -123,7 +123,6 @@ typedef struct hetm_dev_config {
     uint64_t shard_base;    /* first global word index held (0 on a single GPU)      */
     uint64_t rs_gran_bytes; /* RS/WS granularity: pow2 multiple of 8 (default 1024)  */
     uint64_t chunk_bytes;   /* ChunkMap granularity: pow2 multiple of 8 (16384)      */
-    uint64_t lock_entries;  /* batch-TM lock table entries, pow2; 0 = auto           */
     uint64_t log_capacity;  /* initial round-log arena (entries); 0 = auto; grows    */
     uint32_t max_attempts;  /* livelock budget per transaction; 0 = default (1<<20)  */
     int32_t device;         /* CUDA device ordinal                                   */
@@ -132,7 +131,7 @@ typedef struct hetm_dev_config {
 } hetm_dev_config;
 
 typedef struct hetm_dev_info {
-    uint64_t size_words, shard_base, rs_gran_bytes, chunk_bytes, lock_entries;
+    uint64_t size_words, shard_base, rs_gran_bytes, chunk_bytes, cell_bytes;
     uint64_t rs_bits, rs_words, chunk_bits, chunk_words;
     uint64_t log_capacity;
     uint64_t device_bytes; /* HBM allocated by this handle */

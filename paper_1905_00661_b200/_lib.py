@@ -29,7 +29,6 @@ class DevConfig(C.Structure):
         ("shard_base", C.c_uint64),
         ("rs_gran_bytes", C.c_uint64),
         ("chunk_bytes", C.c_uint64),
-        ("lock_entries", C.c_uint64),
         ("log_capacity", C.c_uint64),
         ("max_attempts", C.c_uint32),
         ("device", C.c_int32),
@@ -44,7 +43,7 @@ class DevInfo(C.Structure):
         ("shard_base", C.c_uint64),
         ("rs_gran_bytes", C.c_uint64),
         ("chunk_bytes", C.c_uint64),
-        ("lock_entries", C.c_uint64),
+        ("cell_bytes", C.c_uint64),
         ("rs_bits", C.c_uint64),
         ("rs_words", C.c_uint64),
         ("chunk_bits", C.c_uint64),

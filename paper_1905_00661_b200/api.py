@@ -155,11 +155,11 @@ class BatchResult:
 # ------------------------------------------------------------- device guest
 class GpuDevice:
     """One B200 holding one STMR shard: the device replica, shadow, TS array,
-    RS/WS/ChunkMap bitmaps and the batch-TM lock table (Stmr + guest-stm-batch
+    RS/WS/ChunkMap bitmaps and the batch-TM locks (Stmr + guest-stm-batch
     + engine device half)."""
 
     def __init__(self, size_words: int, *, shard_base: int = 0, rs_gran_bytes: int = 1024,
-                 chunk_bytes: int = 16384, lock_entries: int = 0, log_capacity: int = 0,
+                 chunk_bytes: int = 16384, log_capacity: int = 0,
                  max_attempts: int = 0, device: int = 0, shadow: bool = True, l2_fetch_32: bool = False):
         cfg = _lib.DevConfig()
         lib.hetm_dev_config_default(C.byref(cfg))
@@ -167,7 +167,6 @@ class GpuDevice:
         cfg.shard_base = shard_base
         cfg.rs_gran_bytes = rs_gran_bytes
         cfg.chunk_bytes = chunk_bytes
-        cfg.lock_entries = lock_entries
         cfg.log_capacity = log_capacity
         cfg.max_attempts = max_attempts
         cfg.device = device

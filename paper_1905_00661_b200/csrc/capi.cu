@@ -37,18 +37,15 @@ struct hetm_dev {
     uint64_t W = 0, base = 0;
     uint32_t gran_shift = 0, chunk_shift = 0;
     uint64_t rs_bits = 0, rs_words = 0, chunk_bits = 0, chunk_words = 0;
-    uint64_t lock_entries = 0;
-    uint32_t lock_hash_shift = 0;
-    bool lock_identity = false;
     uint32_t max_attempts = 1u << 20;
 
-    uint64_t* d_stmr = nullptr;
-    uint64_t* d_shadow = nullptr;
-    unsigned long long* d_ts = nullptr;
+    Cell* d_cells = nullptr;             // devReplica: {value, lock, ts, spare} per word
+    uint64_t* d_shadow = nullptr;        // devShadow: plain words
+    uint64_t* d_stage = nullptr;         // plain-word staging for raw ops / basic rollback
+    uint64_t stage_cap = 0;
     unsigned long long* d_rs = nullptr;
     unsigned long long* d_ws = nullptr;
     unsigned long long* d_chunk = nullptr;
-    unsigned long long* d_locks = nullptr;
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
@@ -99,7 +96,7 @@ struct hetm_dev {
 
     ShardView view() const {
         ShardView v;
-        v.stmr = d_stmr;
+        v.cells = d_cells;
         v.base = base;
         v.size_words = W;
         v.rs = d_rs;
@@ -108,13 +105,6 @@ struct hetm_dev {
         v.gran_shift = gran_shift;
         v.chunk_shift = chunk_shift;
         return v;
-    }
-    LockTable locks() const {
-        LockTable lt;
-        lt.words = d_locks;
-        lt.hash_shift = 64u - (uint32_t)__builtin_ctzll(lock_entries);
-        lt.identity = lock_identity ? 1u : 0u;
-        return lt;
     }
     void record(int dir, int tag, uint64_t bytes) { xfer.push_back(hetm_transfer_record{dir, tag, bytes}); }
 };
@@ -138,6 +128,8 @@ int fail(hetm_dev* d, cudaError_t e, const char* what) {
 bool pow2(uint64_t v) { return v && !(v & (v - 1)); }
 uint32_t log2u(uint64_t v) { return (uint32_t)__builtin_ctzll(v); }
 
+int sync_all(hetm_dev* d);
+
 int dev_alloc(hetm_dev* d, void** p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
     if (e != cudaSuccess) return fail(d, e, "cudaMalloc");
@@ -145,10 +137,16 @@ int dev_alloc(hetm_dev* d, void** p, size_t bytes) {
     return HETM_OK;
 }
 
-uint64_t* replica_ptr(hetm_dev* d, int replica) {
-    if (replica == HETM_REPLICA_DEV) return d->d_stmr;
-    if (replica == HETM_REPLICA_DEV_SHADOW) return d->d_shadow;
-    return nullptr;
+int ensure_stage(hetm_dev* d, uint64_t words) {
+    if (words <= d->stage_cap) return HETM_OK;
+    if (d->d_stage) {
+        int rc = sync_all(d);
+        if (rc) return rc;
+        cudaFree(d->d_stage);
+        d->bytes_alloc -= d->stage_cap * 8;
+    }
+    d->stage_cap = std::max<uint64_t>(words, 1 << 16);
+    return dev_alloc(d, (void**)&d->d_stage, d->stage_cap * 8);
 }
 
 int check_range(hetm_dev* d, uint64_t addr, uint64_t n) {
@@ -194,10 +192,10 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
         CK(d, cudaEventRecord(t0, s));
     }
     if (kernel_id == HETM_KERNEL_BANK)
-        e = launch_bank_batch(d->view(), d->locks(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets,
-                              d->d_ctr, d->max_attempts, d->geom, s);
+        e = launch_bank_batch(d->view(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
+                              d->max_attempts, d->geom, s);
     else
-        e = launch_rw_batch(d->view(), d->locks(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
+        e = launch_rw_batch(d->view(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                             d->max_attempts, d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "batch kernel launch");
     if (d->timing) {
@@ -216,7 +214,7 @@ cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, i
         t1 = d->tev();
         cudaEventRecord(t0, s);
     }
-    cudaError_t e = launch_validate(d->view(), d->d_ts, log, n, apply, d->ts_floor, d->d_ctr, d->geom, s);
+    cudaError_t e = launch_validate(d->view(), log, n, apply, d->ts_floor, d->d_ctr, d->geom, s);
     if (d->timing && n) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
@@ -269,16 +267,19 @@ int refresh_shadow(hetm_dev* d, bool host_log_applied, uint64_t dirty_bytes) {
     if (!d->d_shadow) return HETM_OK;
     if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
     if (d->shadow_synced) {
-        cudaError_t e = launch_copy_dirty_chunks(d->d_shadow, d->d_stmr, d->W, d->d_chunk, d->chunk_bits,
-                                                 d->chunk_shift, d->geom, d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "copy_dirty_chunks");
+        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
+                                            true, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(shadow)");
         if (host_log_applied) {
-            e = launch_winner_apply(d->d_shadow, d->base, d->W, d->d_ts, d->d_arena, d->arena_n, d->geom, d->s_merge);
+            e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
+                                    d->s_merge);
             if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
         }
         d->record(HETM_D2D, HETM_TAG_SHADOW, dirty_bytes);
     } else {
-        CK(d, cudaMemcpyAsync(d->d_shadow, d->d_stmr, d->W * 8, cudaMemcpyDeviceToDevice, d->s_merge));
+        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, nullptr, d->chunk_bits, d->chunk_shift, true,
+                                            d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(full shadow)");
         d->record(HETM_D2D, HETM_TAG_SHADOW, d->W * 8);
         d->shadow_synced = true;
     }
@@ -361,8 +362,6 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if (cfg->size_words == 0) return HETM_ERR_INVALID_SIZE;
     if (!pow2(cfg->rs_gran_bytes) || cfg->rs_gran_bytes % 8) return HETM_ERR_INVALID_SIZE;
     if (!pow2(cfg->chunk_bytes) || cfg->chunk_bytes % 8) return HETM_ERR_INVALID_SIZE;
-    if (cfg->lock_entries && (!pow2(cfg->lock_entries) || cfg->lock_entries > (1ull << 32)))
-        return HETM_ERR_CONFIG;
     const uint64_t align_words = std::max(cfg->rs_gran_bytes, cfg->chunk_bytes) / 8;
     if (cfg->shard_base % align_words) return HETM_ERR_CONFIG;
     int ndev = 0;
@@ -383,10 +382,6 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     d->rs_words = (d->rs_bits + 63) / 64;
     d->chunk_bits = (d->W * 8 + cfg->chunk_bytes - 1) / cfg->chunk_bytes;
     d->chunk_words = (d->chunk_bits + 63) / 64;
-    uint64_t w2 = 1;
-    while (w2 < d->W) w2 <<= 1;
-    d->lock_entries = cfg->lock_entries ? cfg->lock_entries : std::min<uint64_t>(w2, 1ull << 24);
-    d->lock_identity = d->lock_entries >= d->W;
     if (cfg->max_attempts) d->max_attempts = cfg->max_attempts;
 
     auto bail = [&](int rc) {
@@ -396,14 +391,12 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if (cudaSetDevice(d->device) != cudaSuccess) return bail(fail(d, cudaGetLastError(), "cudaSetDevice"));
     if (cfg->flags & HETM_CFG_L2_FETCH_32) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32);
     int rc;
-    if ((rc = dev_alloc(d, (void**)&d->d_stmr, d->W * 8))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_cells, d->W * sizeof(Cell)))) return bail(rc);
     if (!(cfg->flags & HETM_CFG_NO_SHADOW))
         if ((rc = dev_alloc(d, (void**)&d->d_shadow, d->W * 8))) return bail(rc);
-    if ((rc = dev_alloc(d, (void**)&d->d_ts, d->W * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_rs, d->rs_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ws, d->rs_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
-    if ((rc = dev_alloc(d, (void**)&d->d_locks, d->lock_entries * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
     d->arena_cap = cfg->log_capacity ? cfg->log_capacity : (1ull << 20);
@@ -412,14 +405,12 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
         return bail(fail(d, cudaGetLastError(), "cudaHostAlloc(counters)"));
     std::memset(d->h_ctr, 0, sizeof(DevCounters));
 
-    // Stmr.create: all replicas zero-filled; TS/bitmaps/locks zero.
-    CK(d, cudaMemset(d->d_stmr, 0, d->W * 8));
+    // Stmr.create: all replicas zero-filled; locks/TS/bitmaps zero.
+    CK(d, cudaMemset(d->d_cells, 0, d->W * sizeof(Cell)));
     if (d->d_shadow) CK(d, cudaMemset(d->d_shadow, 0, d->W * 8));
-    CK(d, cudaMemset(d->d_ts, 0, d->W * 8));
     CK(d, cudaMemset(d->d_rs, 0, d->rs_words * 8));
     CK(d, cudaMemset(d->d_ws, 0, d->rs_words * 8));
     CK(d, cudaMemset(d->d_chunk, 0, d->chunk_words * 8));
-    CK(d, cudaMemset(d->d_locks, 0, d->lock_entries * 8));
     CK(d, cudaMemset(d->d_ctr, 0, sizeof(DevCounters)));
 
     for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h})
@@ -452,9 +443,9 @@ int hetm_dev_close(hetm_dev* d) {
     cudaSetDevice(d->device);
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
         if (s) cudaStreamSynchronize(s);
-    for (void* p : {(void*)d->d_stmr, (void*)d->d_shadow, (void*)d->d_ts, (void*)d->d_rs, (void*)d->d_ws,
-                    (void*)d->d_chunk, (void*)d->d_locks, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_arena,
-                    d->d_in, (void*)d->d_tk, d->d_route, d->d_flush})
+    for (void* p : {(void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+                    (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_arena, d->d_in,
+                    (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     for (auto& v : d->tpairs)
@@ -478,7 +469,7 @@ int hetm_dev_info_get(hetm_dev* d, hetm_dev_info* o) {
     o->shard_base = d->base;
     o->rs_gran_bytes = d->cfg.rs_gran_bytes;
     o->chunk_bytes = d->cfg.chunk_bytes;
-    o->lock_entries = d->lock_entries;
+    o->cell_bytes = sizeof(Cell);
     o->rs_bits = d->rs_bits;
     o->rs_words = d->rs_words;
     o->chunk_bits = d->chunk_bits;
@@ -507,27 +498,49 @@ int hetm_dev_raw_read(hetm_dev* d, int replica, uint64_t addr, uint64_t* value) 
     return hetm_dev_download(d, replica, addr, value, 1);
 }
 
+static int check_replica(hetm_dev* d, int replica) {
+    if (replica == HETM_REPLICA_DEV) return HETM_OK;
+    if (replica == HETM_REPLICA_DEV_SHADOW) return d->d_shadow ? HETM_OK : HETM_ERR_CONFIG;
+    return HETM_ERR_INVALID_ARG;  // host-owned replicas are not addressable here
+}
+
 int hetm_dev_upload(hetm_dev* d, int replica, uint64_t addr, const uint64_t* src, uint64_t n) {
     if (!d || (!src && n)) return HETM_ERR_INVALID_ARG;
-    uint64_t* p = replica_ptr(d, replica);
-    if (!p) return replica == HETM_REPLICA_DEV_SHADOW ? HETM_ERR_CONFIG : HETM_ERR_INVALID_ARG;
-    int rc = check_range(d, addr, n);
+    int rc = check_replica(d, replica);
     if (rc) return rc;
+    if ((rc = check_range(d, addr, n))) return rc;
     if ((rc = sync_all(d))) return rc;  // raw ops require quiescence
-    CK(d, cudaMemcpy(p + (addr - d->base), src, n * 8, cudaMemcpyHostToDevice));
-    if (replica == HETM_REPLICA_DEV || replica == HETM_REPLICA_DEV_SHADOW) d->shadow_synced = false;
+    const uint64_t lo = addr - d->base;
+    if (replica == HETM_REPLICA_DEV_SHADOW) {
+        CK(d, cudaMemcpy(d->d_shadow + lo, src, n * 8, cudaMemcpyHostToDevice));
+    } else {
+        if ((rc = ensure_stage(d, n))) return rc;
+        CK(d, cudaMemcpy(d->d_stage, src, n * 8, cudaMemcpyHostToDevice));
+        cudaError_t e = launch_scatter_range(d->d_cells, d->d_stage, lo, n, d->geom, 0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return fail(d, e, "scatter_range");
+    }
+    d->shadow_synced = false;
     d->record(HETM_H2D, HETM_TAG_RAW, n * 8);
     return HETM_OK;
 }
 
 int hetm_dev_download(hetm_dev* d, int replica, uint64_t addr, uint64_t* dst, uint64_t n) {
     if (!d || (!dst && n)) return HETM_ERR_INVALID_ARG;
-    uint64_t* p = replica_ptr(d, replica);
-    if (!p) return replica == HETM_REPLICA_DEV_SHADOW ? HETM_ERR_CONFIG : HETM_ERR_INVALID_ARG;
-    int rc = check_range(d, addr, n);
+    int rc = check_replica(d, replica);
     if (rc) return rc;
+    if ((rc = check_range(d, addr, n))) return rc;
     if ((rc = sync_all(d))) return rc;
-    CK(d, cudaMemcpy(dst, p + (addr - d->base), n * 8, cudaMemcpyDeviceToHost));
+    const uint64_t lo = addr - d->base;
+    if (replica == HETM_REPLICA_DEV_SHADOW) {
+        CK(d, cudaMemcpy(dst, d->d_shadow + lo, n * 8, cudaMemcpyDeviceToHost));
+    } else {
+        if ((rc = ensure_stage(d, n))) return rc;
+        cudaError_t e = launch_gather_range(d->d_stage, d->d_cells, lo, n, d->geom, 0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return fail(d, e, "gather_range");
+        CK(d, cudaMemcpy(dst, d->d_stage, n * 8, cudaMemcpyDeviceToHost));
+    }
     d->record(HETM_D2H, HETM_TAG_RAW, n * 8);
     return HETM_OK;
 }
@@ -758,14 +771,18 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
     uint64_t dirty_bytes = 0;
     for (auto& r : ranges) dirty_bytes += r.second * 8;
-    const uint64_t* src = d->d_stmr;
+    const uint64_t* src = d->d_shadow;
     if (d->d_shadow) {
         if ((rc = refresh_shadow(d, true, dirty_bytes))) return rc;
-        src = d->d_shadow;
-        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
-    } else {
-        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_exec, 0));
+    } else {  // no shadow: pack the dirty chunks into the staging buffer instead
+        if ((rc = ensure_stage(d, d->W))) return rc;
+        cudaError_t e = launch_dirty_chunks(d->d_stage, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
+                                            true, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(stage)");
+        CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+        src = d->d_stage;
     }
+    CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
     for (auto& r : ranges) {
         CK(d, cudaMemcpyAsync(host + r.first, src + r.first, r.second * 8, cudaMemcpyDeviceToHost, d->s_d2h));
         d->record(HETM_D2H, HETM_TAG_MERGE, r.second * 8);
@@ -802,26 +819,32 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
     if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
     hetm_merge_stats s{};
     if (optimized && d->d_shadow && d->shadow_synced) {
-        // Round-start shadow + the round's host log (freshest ts per word) -> swap
-        cudaError_t e = launch_winner_apply(d->d_shadow, d->base, d->W, d->d_ts, d->d_arena, d->arena_n, d->geom,
-                                            d->s_merge);
+        // Round-start shadow + the round's host log in ts order: the
+        // device-dirty words are restored from devShadow, then the freshest log
+        // entry of every logged word is stored into both devReplica and devShadow.
+        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
+                                            false, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(restore)");
+        e = launch_winner_apply(d->d_cells, nullptr, d->base, d->W, d->d_arena, d->arena_n, d->geom, d->s_merge);
+        if (e == cudaSuccess)
+            e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
+                                    d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "winner_apply(rollback)");
-        std::swap(d->d_stmr, d->d_shadow);
-        // New shadow (old speculative replica) realigned on the device-dirty chunks.
-        e = launch_copy_dirty_chunks(d->d_shadow, d->d_stmr, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, d->geom,
-                                     d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "copy_dirty_chunks(realign)");
         d->record(HETM_D2D, HETM_TAG_ROLLBACK, dirty_bytes);
         s.bytes_d2d = dirty_bytes;
         CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
     } else {
         if (!host) return HETM_ERR_INVALID_ARG;
         // Basic: host state copied over the device's dirty chunks
+        if ((rc = ensure_stage(d, d->W))) return rc;
         for (auto& r : ranges) {
-            CK(d, cudaMemcpyAsync(d->d_stmr + r.first, host + r.first, r.second * 8, cudaMemcpyHostToDevice,
+            CK(d, cudaMemcpyAsync(d->d_stage + r.first, host + r.first, r.second * 8, cudaMemcpyHostToDevice,
                                   d->s_merge));
             d->record(HETM_H2D, HETM_TAG_ROLLBACK, r.second * 8);
         }
+        cudaError_t e = launch_dirty_chunks(d->d_stage, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
+                                            false, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(basic rollback)");
         s.bytes_h2d = dirty_bytes;
         if ((rc = refresh_shadow(d, true, dirty_bytes))) return rc;
     }
@@ -851,12 +874,18 @@ int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snaps
     if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
     uint64_t dirty_bytes = 0;
     for (auto& r : ranges) dirty_bytes += r.second * 8;
-    const uint64_t* src = d->d_stmr;
+    const uint64_t* src = d->d_shadow;
     if (d->d_shadow) {
         if ((rc = refresh_shadow(d, false, dirty_bytes))) return rc;
-        src = d->d_shadow;
-        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
+    } else {
+        if ((rc = ensure_stage(d, d->W))) return rc;
+        cudaError_t e = launch_dirty_chunks(d->d_stage, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
+                                            true, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(stage)");
+        CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+        src = d->d_stage;
     }
+    CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
     for (auto& r : ranges) {
         CK(d, cudaMemcpyAsync(host + r.first, src + r.first, r.second * 8, cudaMemcpyDeviceToHost, d->s_d2h));
         d->record(HETM_D2H, HETM_TAG_MERGE, r.second * 8);
@@ -912,7 +941,7 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
     CK(d, cudaMemsetAsync(&d->d_ctr->round_max_ts, 0, 8 + 3 * sizeof(unsigned), s));
     if (flags & HETM_CLEAR_RESET_TS) {
-        CK(d, cudaMemsetAsync(d->d_ts, 0, d->W * 8, s));
+        CK(d, cudaMemset2DAsync(&d->d_cells[0].ts, sizeof(Cell), 0, sizeof(unsigned long long), d->W, s));
         d->ts_floor = 0;
     }
     CK(d, cudaEventRecord(d->ev_round, s));

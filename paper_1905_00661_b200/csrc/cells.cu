@@ -1,0 +1,71 @@
+// cells.cu — conversions between the 32-B word-cell layout of devReplica
+// (common.cuh) and plain 64-bit word arrays (devShadow, raw-op staging).
+// Used at the edges only: raw ops, the shadow refresh of
+// mergeCommit and the rollback of mergeAbortDevice.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hetm_b200 {
+
+// dst[i] = cells[lo + i].value
+__global__ void gather_range_kernel(uint64_t* __restrict__ dst, const Cell* __restrict__ cells, uint64_t lo, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = cells[lo + i].value;
+}
+
+// cells[lo + i].value = src[i]
+__global__ void scatter_range_kernel(Cell* __restrict__ cells, const uint64_t* __restrict__ src, uint64_t lo, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        cells[lo + i].value = src[i];
+}
+
+// For every dirty chunk c: plain[w] <-> cells[w].value for w in chunk c.
+// One CTA walks one dirty chunk at a time (grid-stride over chunks).
+template <bool kToPlain>
+__global__ void dirty_chunks_kernel(uint64_t* __restrict__ plain, Cell* __restrict__ cells, uint64_t size_words,
+                                    const unsigned long long* __restrict__ bits, uint64_t n_chunks,
+                                    uint32_t chunk_shift) {
+    const uint64_t wpc = 1ull << chunk_shift;
+    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        if (bits && !((bits[c >> 6] >> (c & 63)) & 1ull)) continue;
+        const uint64_t lo = c * wpc;
+        const uint64_t hi = lo + wpc < size_words ? lo + wpc : size_words;
+        for (uint64_t w = lo + threadIdx.x; w < hi; w += blockDim.x) {
+            if (kToPlain) plain[w] = cells[w].value;
+            else cells[w].value = plain[w];
+        }
+    }
+}
+
+static unsigned grid_words(uint64_t n, const LaunchGeom& g) {
+    uint64_t want = (n + 255) / 256;
+    const uint64_t cap = (uint64_t)g.sm_count * 16;
+    return (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+cudaError_t launch_gather_range(uint64_t* dst, const Cell* cells, uint64_t lo, uint64_t n, const LaunchGeom& g,
+                                cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    gather_range_kernel<<<grid_words(n, g), 256, 0, s>>>(dst, cells, lo, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, uint64_t n, const LaunchGeom& g,
+                                 cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    scatter_range_kernel<<<grid_words(n, g), 256, 0, s>>>(cells, src, lo, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,
+                                uint64_t n_chunks, uint32_t chunk_shift, bool to_plain, const LaunchGeom& g,
+                                cudaStream_t s) {
+    if (n_chunks == 0) return cudaSuccess;
+    const uint64_t cap = (uint64_t)g.sm_count * 8;
+    const unsigned grid = (unsigned)(n_chunks < cap ? n_chunks : cap);
+    if (to_plain) dirty_chunks_kernel<true><<<grid, 256, 0, s>>>(plain, cells, size_words, bits, n_chunks, chunk_shift);
+    else dirty_chunks_kernel<false><<<grid, 256, 0, s>>>(plain, cells, size_words, bits, n_chunks, chunk_shift);
+    return cudaGetLastError();
+}
+
+}  // namespace hetm_b200

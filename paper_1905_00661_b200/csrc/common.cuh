@@ -1,4 +1,17 @@
-// common.cuh — sm_100a memory-model helpers shared by the HeTM device kernels.
+// common.cuh — HBM layout and sm_100a memory-model helpers for the HeTM kernels.
+//
+// Device replica layout: one 32-byte WORD CELL per STMR word,
+//     { value, lock, ts, spare }            (one 32-B L2/DRAM sector)
+// so every per-word operation of the hot path touches exactly one sector:
+//   * the batch TM reads {value, lock} with one 128-bit single-copy-atomic
+//     load and commits {new value, unlocked new version} with one 128-bit
+//     store (no separate lock table, no fence between write-back and release);
+//   * validation raises `ts` (the TsArray entry) with a
+//     fire-and-forget REDG.E.MAX.64 and stores the winning value in the same
+//     sector.
+// The raw-op / merge boundary still sees a plain array of 64-bit words
+// (SPEC.md:78): gather/scatter kernels convert at the edge, and devShadow is a
+// plain word array so dirty chunks DMA straight to the host replica.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -6,6 +19,14 @@
 #include "hetm_b200/capi.h"
 
 namespace hetm_b200 {
+
+struct alignas(32) Cell {
+    uint64_t value;           // the STMR word (devReplica)
+    unsigned long long lock;  // batch-TM versioned lock (device_tm.cuh)
+    unsigned long long ts;    // TsArray: freshest host ts applied (monotone, never reset)
+    uint64_t spare;
+};
+static_assert(sizeof(Cell) == 32, "one cell per 32-B sector");
 
 // Device-wide counters, one per handle (HBM, 128-B aligned).
 struct DevCounters {
@@ -23,8 +44,8 @@ struct DevCounters {
 
 // Kernel-wide view of one device's STMR shard and its metadata.
 struct ShardView {
-    uint64_t* stmr;            // devReplica (size_words)
-    uint64_t base;             // global index of stmr[0]
+    Cell* cells;               // devReplica + locks + TS (size_words cells)
+    uint64_t base;             // global index of cells[0]
     uint64_t size_words;
     unsigned long long* rs;    // RS bitmap words
     unsigned long long* ws;    // WS bitmap words
@@ -49,18 +70,20 @@ __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// Streaming (read-once) 128-bit load that does not allocate in L1.
-__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
+// {value, lock} of a cell as ONE single-copy-atomic 128-bit access
+// (LDG.E.128.STRONG.GPU / STG.E.128.STRONG.GPU; the same instructions
+// libcu++ uses for 16-byte cuda::atomic).
+__device__ __forceinline__ void ld_pair(const Cell* c, uint64_t& value, unsigned long long& lock) {
+    asm volatile("{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\tmov.b128 {%0, %1}, t;\n\t}"
+                 : "=l"(value), "=l"(lock)
+                 : "l"(c)
+                 : "memory");
+}
+__device__ __forceinline__ void st_pair(Cell* c, uint64_t value, unsigned long long lock) {
+    asm volatile("{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(c),
+                 "l"(value), "l"(lock)
+                 : "memory");
 }
 
 __device__ __forceinline__ void set_bit(unsigned long long* words, uint64_t bit) {

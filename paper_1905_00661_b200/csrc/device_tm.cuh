@@ -4,7 +4,7 @@
 // CUDA thread runs one transaction; every transaction eventually commits or
 // reports livelock.
 //
-// Lock table: 64-bit versioned locks, one per (hashed) STMR word:
+// Per-word versioned lock, stored in the word's cell (common.cuh):
 //     bit 63      FINAL  — write-back in progress, never stolen
 //     bits 62..32 owner  — priority of the pre-lock holder (0 = free)
 //     bits 31..0  version — low 32 bits of the last committing ticket + 1
@@ -16,16 +16,17 @@
 //
 // Commit (TL2 order, SURVEY.md §7 hard part 1):
 //     pre-lock write set -> take ticket -> validate read set -> finalize ->
-//     write back -> release (version = ticket + 1)
+//     write back + release in ONE 128-bit store {value, version = ticket+1}
 // The ticket is taken AFTER the write claims are visible and BEFORE the read
 // set is validated, so ascending ticket order is a valid serial order: it is
 // what hetm_dev_execute_batch reports and what the oracle replays.
 //
-// Ordering on sm_100a relies on value/control dependencies (the GPU issues a
-// warp's instructions in order and does not speculate loads):
-//   * lock words are loaded and tested before the dependent STMR loads issue;
-//   * the ticket is broadcast with a shuffle before validation loads issue;
-//   * write-back stores are fenced (fence.acq_rel.gpu) before the release.
+// Reads take a 128-bit snapshot {value, lock}: with no FINAL bit the value is
+// the one committed under that version (values only change under FINAL, and
+// the release store changes value and version atomically).
+// Ordering relies on value/control dependencies (a warp issues in order and
+// the GPU does not speculate loads): claims are checked before the ticket is
+// taken, and the ticket is broadcast with a shuffle before validation loads.
 #pragma once
 #include "common.cuh"
 
@@ -39,22 +40,12 @@ __device__ __forceinline__ unsigned long long lk_make(uint32_t owner, uint32_t v
     return ((unsigned long long)owner << 32) | ver;
 }
 
-struct LockTable {
-    unsigned long long* words;
-    uint32_t hash_shift;  // 64 - log2(entries)
-    uint32_t identity;    // 1: one lock per local word (entries >= size_words)
-    __device__ __forceinline__ uint32_t index(uint64_t local) const {
-        return identity ? (uint32_t)local : (uint32_t)((local * 0x9E3779B97F4A7C15ull) >> hash_shift);
-    }
-};
-
 template <int R, int W>
 struct DeviceTx {
     uint32_t prio;
     int nr, nw;
     uint64_t r_local[R];
     uint64_t r_val[R];
-    uint32_t r_lk[R];
     uint32_t r_ver[R];
     uint64_t w_local[W];
     uint64_t w_val[W];
@@ -66,61 +57,34 @@ struct DeviceTx {
     }
 };
 
-// Batched TM_read of n words (local indices).  Lock words of all n are loaded
-// first (in parallel); the STMR loads are control-dependent on them.  Returns
-// false (abort) if any is FINAL-locked.  No read-your-writes lookup: use
-// tm_read for words that may already be in the write buffer.
-template <int R, int W, int N>
-__device__ __forceinline__ bool tm_read_n(DeviceTx<R, W>& tx, const ShardView& v, const LockTable& lt,
-                                          const uint64_t (&loc)[N], uint64_t (&out)[N]) {
-    unsigned long long l[N];
-    uint32_t lk[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        lk[k] = lt.index(loc[k]);
-        l[k] = ld_relaxed(&lt.words[lk[k]]);
-    }
-    bool fin = false;
-#pragma unroll
-    for (int k = 0; k < N; ++k) fin |= (l[k] & kLockFinal) != 0;
-    if (fin) return false;
-#pragma unroll
-    for (int k = 0; k < N; ++k) out[k] = ld_relaxed(&v.stmr[loc[k]]);
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        tx.r_local[tx.nr] = loc[k];
-        tx.r_val[tx.nr] = out[k];
-        tx.r_lk[tx.nr] = lk[k];
-        tx.r_ver[tx.nr] = lk_ver(l[k]);
-        ++tx.nr;
-    }
-    return true;
-}
-
-// Single TM_read with read-your-writes (own buffered write, then own read set).
+// TM_read with read-your-writes (own buffered write, then own read set).
 template <int R, int W>
-__device__ __forceinline__ bool tm_read(DeviceTx<R, W>& tx, const ShardView& v, const LockTable& lt,
-                                        uint64_t loc, uint64_t& out) {
+__device__ __forceinline__ bool tm_read(DeviceTx<R, W>& tx, const ShardView& v, uint64_t loc, uint64_t& out) {
     for (int j = 0; j < tx.nw; ++j)
         if (tx.w_local[j] == loc) { out = tx.w_val[j]; return true; }
     for (int j = 0; j < tx.nr; ++j)
         if (tx.r_local[j] == loc) { out = tx.r_val[j]; return true; }
-    uint64_t a[1] = {loc}, o[1];
-    if (!tm_read_n(tx, v, lt, a, o)) return false;
-    out = o[0];
+    uint64_t val;
+    unsigned long long lock;
+    ld_pair(&v.cells[loc], val, lock);
+    if (lock & kLockFinal) return false;
+    tx.r_local[tx.nr] = loc;
+    tx.r_val[tx.nr] = val;
+    tx.r_ver[tx.nr] = lk_ver(lock);
+    ++tx.nr;
+    out = val;
     return true;
 }
 
-// TM_write: buffered; the word must be in the read set (no blind writes,
-// SPEC.md:108,144) — callers read first, tm_write enforces it.
+// TM_write: buffered; the word joins the read set first (no blind writes,
+// SPEC.md:108,144).
 template <int R, int W>
-__device__ __forceinline__ bool tm_write(DeviceTx<R, W>& tx, const ShardView& v, const LockTable& lt,
-                                         uint64_t loc, uint64_t val) {
+__device__ __forceinline__ bool tm_write(DeviceTx<R, W>& tx, const ShardView& v, uint64_t loc, uint64_t val) {
     bool in_rs = false;
     for (int j = 0; j < tx.nr; ++j) in_rs |= (tx.r_local[j] == loc);
     if (!in_rs) {
         uint64_t dummy;
-        if (!tm_read(tx, v, lt, loc, dummy)) return false;
+        if (!tm_read(tx, v, loc, dummy)) return false;
     }
     for (int j = 0; j < tx.nw; ++j)
         if (tx.w_local[j] == loc) { tx.w_val[j] = val; return true; }
@@ -144,67 +108,76 @@ __device__ __forceinline__ unsigned long long take_ticket(unsigned long long* ct
 }
 
 template <int R, int W>
-__device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v, const LockTable& lt,
-                                          unsigned long long* ticket_ctr, unsigned long long& ticket) {
+__device__ __forceinline__ uint32_t read_version(const DeviceTx<R, W>& tx, uint64_t loc) {
+    for (int k = 0; k < tx.nr; ++k)
+        if (tx.r_local[k] == loc) return tx.r_ver[k];
+    return 0;
+}
+
+template <int R, int W>
+__device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v, unsigned long long* ticket_ctr,
+                                          unsigned long long& ticket) {
     const uint32_t me = tx.prio;
-    // 0. words sharing a lock entry must have been read under one version
-    for (int k = 1; k < tx.nr; ++k)
-        for (int q = 0; q < k; ++q)
-            if (tx.r_lk[q] == tx.r_lk[k] && tx.r_ver[q] != tx.r_ver[k]) return false;
-    // 1. write lock set (distinct lock indices, ascending) with read versions
-    uint32_t wl[W], wv[W];
-    int nwl = 0;
-    for (int j = 0; j < tx.nw; ++j) {
-        uint32_t lk = lt.index(tx.w_local[j]);
-        uint32_t ver = 0;
-        for (int k = 0; k < tx.nr; ++k)
-            if (tx.r_lk[k] == lk) { ver = tx.r_ver[k]; break; }
-        bool dup = false;
-        for (int k = 0; k < nwl; ++k) dup |= (wl[k] == lk);
-        if (dup) continue;
-        int p = nwl++;
-        while (p > 0 && wl[p - 1] > lk) { wl[p] = wl[p - 1]; wv[p] = wv[p - 1]; --p; }
-        wl[p] = lk;
-        wv[p] = ver;
+    // 1. write set, ascending word order (tm_write deduplicates)
+    uint64_t wl[W];
+    uint64_t wv[W];
+    uint32_t wver[W];
+    const int nwl = tx.nw;
+    for (int j = 0; j < nwl; ++j) {
+        int p = j;
+        while (p > 0 && wl[p - 1] > tx.w_local[j]) {
+            wl[p] = wl[p - 1];
+            wv[p] = wv[p - 1];
+            wver[p] = wver[p - 1];
+            --p;
+        }
+        wl[p] = tx.w_local[j];
+        wv[p] = tx.w_val[j];
+        wver[p] = read_version(tx, tx.w_local[j]);
     }
     // 2. pre-lock under the priority rule
     int held = 0;
     bool ok = true;
     for (int k = 0; k < nwl && ok; ++k) {
-        unsigned long long want = lk_make(me, wv[k]);
-        unsigned long long cur = ld_relaxed(&lt.words[wl[k]]);
+        unsigned long long* lw = &v.cells[wl[k]].lock;
+        unsigned long long cur = ld_relaxed(lw);
         for (;;) {
-            if ((cur & kLockFinal) || lk_ver(cur) != wv[k]) { ok = false; break; }
-            uint32_t own = lk_owner(cur);
+            if ((cur & kLockFinal) || lk_ver(cur) != wver[k]) { ok = false; break; }
+            const uint32_t own = lk_owner(cur);
             if (own != 0 && own < me) { ok = false; break; }
-            unsigned long long prev = atomicCAS(&lt.words[wl[k]], cur, want);
+            const unsigned long long prev = atomicCAS(lw, cur, lk_make(me, wver[k]));
             if (prev == cur) { ++held; break; }
             cur = prev;
         }
     }
     if (!ok) {
-        for (int k = 0; k < held; ++k) atomicCAS(&lt.words[wl[k]], lk_make(me, wv[k]), lk_make(0, wv[k]));
+        for (int k = 0; k < held; ++k) atomicCAS(&v.cells[wl[k]].lock, lk_make(me, wver[k]), lk_make(0, wver[k]));
         return false;
     }
     // 3. commit ticket
     const unsigned long long t = take_ticket(ticket_ctr);
     // 4. validate the read-only part of the read set (steal lower-priority pre-locks)
-    uint32_t st_lk[R], st_ver[R];
+    uint64_t st_loc[R];
+    uint32_t st_ver[R];
     int ns = 0;
     for (int k = 0; k < tx.nr && ok; ++k) {
-        uint32_t lk = tx.r_lk[k];
-        bool skip = false;
-        for (int q = 0; q < nwl; ++q) skip |= (wl[q] == lk);
-        for (int q = 0; q < k; ++q) skip |= (tx.r_lk[q] == lk);
-        if (skip) continue;
-        unsigned long long cur = ld_relaxed(&lt.words[lk]);
+        bool written = false;
+        for (int q = 0; q < nwl; ++q) written |= (wl[q] == tx.r_local[k]);
+        if (written) continue;
+        unsigned long long* lw = &v.cells[tx.r_local[k]].lock;
+        unsigned long long cur = ld_relaxed(lw);
         for (;;) {
             if ((cur & kLockFinal) || lk_ver(cur) != tx.r_ver[k]) { ok = false; break; }
-            uint32_t own = lk_owner(cur);
+            const uint32_t own = lk_owner(cur);
             if (own == 0 || own == me) break;
             if (own < me) { ok = false; break; }
-            unsigned long long prev = atomicCAS(&lt.words[lk], cur, lk_make(me, tx.r_ver[k]));
-            if (prev == cur) { st_lk[ns] = lk; st_ver[ns] = tx.r_ver[k]; ++ns; break; }
+            const unsigned long long prev = atomicCAS(lw, cur, lk_make(me, tx.r_ver[k]));
+            if (prev == cur) {
+                st_loc[ns] = tx.r_local[k];
+                st_ver[ns] = tx.r_ver[k];
+                ++ns;
+                break;
+            }
             cur = prev;
         }
     }
@@ -212,24 +185,23 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
     int fin = 0;
     if (ok) {
         for (; fin < nwl; ++fin) {
-            unsigned long long exp = lk_make(me, wv[fin]);
-            if (atomicCAS(&lt.words[wl[fin]], exp, exp | kLockFinal) != exp) { ok = false; break; }
+            const unsigned long long exp = lk_make(me, wver[fin]);
+            if (atomicCAS(&v.cells[wl[fin]].lock, exp, exp | kLockFinal) != exp) { ok = false; break; }
         }
     }
     if (!ok) {
         for (int k = 0; k < nwl; ++k) {
-            if (k < fin) st_relaxed(&lt.words[wl[k]], lk_make(0, wv[k]));  // held FINAL, nothing written
-            else atomicCAS(&lt.words[wl[k]], lk_make(me, wv[k]), lk_make(0, wv[k]));
+            unsigned long long* lw = &v.cells[wl[k]].lock;
+            if (k < fin) st_relaxed(lw, lk_make(0, wver[k]));  // held FINAL, nothing written
+            else atomicCAS(lw, lk_make(me, wver[k]), lk_make(0, wver[k]));
         }
-        for (int s = 0; s < ns; ++s) atomicCAS(&lt.words[st_lk[s]], lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
+        for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].lock, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
         return false;
     }
-    // 6. write back, then release with the new version
-    for (int j = 0; j < tx.nw; ++j) st_relaxed(&v.stmr[tx.w_local[j]], tx.w_val[j]);
-    fence_acq_rel();
+    // 6. write back + release: one 128-bit store per written word
     const uint32_t nv = (uint32_t)(t + 1);
-    for (int k = 0; k < nwl; ++k) st_relaxed(&lt.words[wl[k]], lk_make(0, nv));
-    for (int s = 0; s < ns; ++s) atomicCAS(&lt.words[st_lk[s]], lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
+    for (int k = 0; k < nwl; ++k) st_pair(&v.cells[wl[k]], wv[k], lk_make(0, nv));
+    for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].lock, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
     ticket = t;
     return true;
 }

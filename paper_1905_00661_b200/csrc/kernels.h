@@ -9,7 +9,7 @@ namespace hetm_b200 {
 
 struct DevCounters;
 struct ShardView;
-struct LockTable;
+struct Cell;
 
 struct LaunchGeom {
     int sm_count;
@@ -18,24 +18,28 @@ struct LaunchGeom {
 };
 
 // guest-stm-batch: one launch executes a whole batch.
-cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const hetm_bank_tx* d_in, uint64_t n,
-                              unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
-                              const LaunchGeom& g, cudaStream_t s);
-cudaError_t launch_rw_batch(const ShardView& v, const LockTable& lt, const hetm_rw_tx* d_in, uint64_t n,
-                            unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
-                            const LaunchGeom& g, cudaStream_t s);
+cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
+                              DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
+cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t n, unsigned long long* d_tickets,
+                            DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
 
-// engine.validateChunk over n log entries.
-cudaError_t launch_validate(const ShardView& v, unsigned long long* d_ts, const hetm_log_entry* d_log, uint64_t n,
-                            int apply, uint64_t ts_floor, DevCounters* ctr, const LaunchGeom& g, cudaStream_t s);
-// Winner store: dst[addr] = value where TS[addr] == entry.ts (rollback /
-// shadow patch).
-cudaError_t launch_winner_apply(uint64_t* dst, uint64_t base, uint64_t size_words, const unsigned long long* d_ts,
+// engine.validateChunk over n log entries (apply: pass A + pass B).
+cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply, uint64_t ts_floor,
+                            DevCounters* ctr, const LaunchGeom& g, cudaStream_t s);
+// Winner store of the round's log: value of the entry whose ts equals the
+// cell's TS goes to dst[addr] (plain array) or, with dst == nullptr, to the
+// cell's value (rollback / shadow patch).
+cudaError_t launch_winner_apply(Cell* cells, uint64_t* dst, uint64_t base, uint64_t size_words,
                                 const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s);
-// Copy every dirty chunk src -> dst (device buffers of size_words words).
-cudaError_t launch_copy_dirty_chunks(uint64_t* dst, const uint64_t* src, uint64_t size_words,
-                                     const unsigned long long* chunk_bits, uint64_t n_chunks, uint32_t chunk_shift,
-                                     const LaunchGeom& g, cudaStream_t s);
+// Word-cell <-> plain word conversions (cells.cu).
+cudaError_t launch_gather_range(uint64_t* dst, const Cell* cells, uint64_t lo, uint64_t n, const LaunchGeom& g,
+                                cudaStream_t s);
+cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, uint64_t n, const LaunchGeom& g,
+                                 cudaStream_t s);
+// bits == nullptr: every chunk.  to_plain: plain[w] = cells[w].value, else the reverse.
+cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,
+                                uint64_t n_chunks, uint32_t chunk_shift, bool to_plain, const LaunchGeom& g,
+                                cudaStream_t s);
 // Popcount of n words into *out (device counter, accumulated).
 cudaError_t launch_popcount(const unsigned long long* words, uint64_t n, unsigned long long* out, cudaStream_t s);
 // OR src words into dst words.

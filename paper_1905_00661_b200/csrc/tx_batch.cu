@@ -9,8 +9,8 @@
 
 #include "common.cuh"
 #include "device_tm.cuh"
-#include "phased_tx.cuh"
 #include "kernels.h"
+#include "phased_tx.cuh"
 
 namespace hetm_b200 {
 
@@ -33,9 +33,8 @@ __device__ __forceinline__ void flush_batch_counters(unsigned long long commits,
 // Warp-phased commit (phased_tx.cuh); each lane keeps its transaction across
 // retries and moves to the next one (grid stride) once it commits.
 template <int KO>
-__global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, LockTable lt,
-                                                                   const hetm_bank_tx* __restrict__ in, uint64_t n,
-                                                                   unsigned long long* __restrict__ tickets,
+__global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, const hetm_bank_tx* __restrict__ in,
+                                                                   uint64_t n, unsigned long long* __restrict__ tickets,
                                                                    DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
@@ -60,18 +59,17 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
                 oob = 1;
                 i += stride;
             } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) tx.lk[k] = lt.index(tx.loc[k]);
+                tx.first = first_occurrences(tx.loc);
                 loaded = true;
             }
         }
         const bool active = i < n && loaded;
         unsigned long long t = 0;
-        const bool committed = phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, lt, &ctr->ticket, t,
-                                              [&](StaticTx<4, 2>& x) {
-                                                  x.wval[0] = x.val[0] - amount;
-                                                  x.wval[1] = x.val[1] + amount;
-                                              });
+        const bool committed =
+            phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, [&](StaticTx<4, 2>& x) {
+                x.wval[0] = x.val[0] - amount;
+                x.wval[1] = x.val[1] + amount;
+            });
         if (committed) {
             tickets[i] = t;
             ++commits;
@@ -90,9 +88,10 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
     flush_batch_counters(commits, aborts, livelocks, oob, ctr);
 }
 
-// Generic <=4 reads / <=2 read-modify-writes (hetm_rw_tx).
-__global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, LockTable lt, const hetm_rw_tx* __restrict__ in,
-                                                              uint64_t n, unsigned long long* __restrict__ tickets,
+// Generic <=4 reads / <=2 read-modify-writes (hetm_rw_tx) through the
+// TM_read / TM_write / TM_commit interface of device_tm.cuh.
+__global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const hetm_rw_tx* __restrict__ in, uint64_t n,
+                                                              unsigned long long* __restrict__ tickets,
                                                               DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
@@ -117,16 +116,16 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, LockT
             uint64_t sum = 0;
             for (uint32_t j = 0; j < nr && ok; ++j) {
                 uint64_t x;
-                ok = tm_read(tx, v, lt, r.r_addr[j] - v.base, x);
+                ok = tm_read(tx, v, r.r_addr[j] - v.base, x);
                 sum += x;
             }
             for (uint32_t j = 0; j < nw && ok; ++j) {
                 uint64_t cur;
                 const uint64_t loc = r.w_addr[j] - v.base;
-                ok = tm_read(tx, v, lt, loc, cur) && tm_write(tx, v, lt, loc, cur + r.add[j] + sum);
+                ok = tm_read(tx, v, loc, cur) && tm_write(tx, v, loc, cur + r.add[j] + sum);
             }
             unsigned long long t;
-            if (ok && tm_commit(tx, v, lt, &ctr->ticket, t)) {
+            if (ok && tm_commit(tx, v, &ctr->ticket, t)) {
                 tickets[i] = t;
                 tm_mark_bitmaps(tx, v);
                 ++commits;
@@ -150,9 +149,8 @@ static unsigned grid_for(uint64_t n, int threads, int blocks_per_sm, int sms) {
     return (unsigned)(want ? want : 1);
 }
 
-cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const hetm_bank_tx* d_in, uint64_t n,
-                              unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
-                              const LaunchGeom& g, cudaStream_t s) {
+cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
+                              DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     static const int ko = [] {
         const char* e = std::getenv("HETM_KNOCKOUT");  // profiling experiments only
@@ -160,22 +158,20 @@ cudaError_t launch_bank_batch(const ShardView& v, const LockTable& lt, const het
     }();
     const unsigned grid = grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count);
 #define HETM_KO_CASE(K) \
-    case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, lt, d_in, n, d_tickets, ctr, max_attempts); break;
+    case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
     switch (ko) {
-        HETM_KO_CASE(1) HETM_KO_CASE(2) HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(32)
-        HETM_KO_CASE(7) HETM_KO_CASE(63)
-        default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, lt, d_in, n, d_tickets, ctr, max_attempts);
+        HETM_KO_CASE(1) HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(13)
+        default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE
     return cudaGetLastError();
 }
 
-cudaError_t launch_rw_batch(const ShardView& v, const LockTable& lt, const hetm_rw_tx* d_in, uint64_t n,
-                            unsigned long long* d_tickets, DevCounters* ctr, uint32_t max_attempts,
-                            const LaunchGeom& g, cudaStream_t s) {
+cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t n, unsigned long long* d_tickets,
+                            DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    rw_batch_kernel<<<grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count), kTxThreads, 0, s>>>(
-        v, lt, d_in, n, d_tickets, ctr, max_attempts);
+    rw_batch_kernel<<<grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count), kTxThreads, 0, s>>>(v, d_in, n, d_tickets,
+                                                                                                ctr, max_attempts);
     return cudaGetLastError();
 }
 
