@@ -167,10 +167,14 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
         unsigned long long* lw = &v.cells[tx.r_local[k]].lock;
         unsigned long long cur = ld_relaxed(lw);
         for (;;) {
-            if ((cur & kLockFinal) || lk_ver(cur) != tx.r_ver[k]) { ok = false; break; }
+            if (lk_ver(cur) != tx.r_ver[k]) { ok = false; break; }
             const uint32_t own = lk_owner(cur);
+            if (own != 0 && own < me) { ok = false; break; }
+            if (cur & kLockFinal) {  // lower-priority holder mid-commit: wait (waits only go down in priority)
+                cur = ld_relaxed(lw);
+                continue;
+            }
             if (own == 0 || own == me) break;
-            if (own < me) { ok = false; break; }
             const unsigned long long prev = atomicCAS(lw, cur, lk_make(me, tx.r_ver[k]));
             if (prev == cur) {
                 st_loc[ns] = tx.r_local[k];

@@ -9,8 +9,16 @@
 //
 //   P1  128-bit {value, lock} snapshots of the NR words     (1 DRAM round trip)
 //   P2  pre-lock CAS of the NW write words                   (L2 hit)
+//       A CAS lost to a lower-priority claim is retried as a steal, so the
+//       highest-priority transaction never loses a lock race.
 //   P3  one ticket atomicAdd per warp for the surviving lanes
 //   P4  validation loads of read-only words || finalize CAS  (L2 hits)
+//       A read-only word held FINAL by a LOWER-priority transaction is waited
+//       for (its holder only ever waits on still lower priorities, so waits
+//       cannot cycle); a higher-priority claim aborts the attempt; a
+//       lower-priority pre-lock is stolen.  Aborting on every FINAL instead
+//       would let two transactions that read each other's write word abort
+//       each other forever.
 //   P5  128-bit {value, unlocked new version} stores + bitmap REDs (no wait)
 //
 // Writes are reads 0..NW-1 (no blind writes).  Duplicate words
@@ -95,11 +103,23 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             if (tx.first & (1u << j))
                 prev[j] = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], lk_make(me, lk_ver(tx.l[j])));
 #pragma unroll
-        for (int j = 0; j < NW; ++j)
-            if (tx.first & (1u << j)) {
-                held[j] = prev[j] == tx.l[j];
-                ok &= held[j];
+        for (int j = 0; j < NW; ++j) {
+            if (!(tx.first & (1u << j))) continue;
+            unsigned long long c = prev[j];
+            const unsigned long long mine = lk_make(me, lk_ver(tx.l[j]));
+            bool got = c == tx.l[j];
+            // Lost the race: steal from a lower-priority pre-lock holder (possibly a
+            // lane of this very warp), back off from a higher one (rare path).
+            while (!got) {
+                const uint32_t own = lk_owner(c);
+                if ((c & kLockFinal) || lk_ver(c) != lk_ver(tx.l[j]) || (own != 0 && own < me)) break;
+                const unsigned long long expect = c;
+                c = atomicCAS(&v.cells[tx.loc[j]].lock, expect, mine);
+                got = c == expect;
             }
+            held[j] = got;
+            ok &= got;
+        }
         if (!ok) {
 #pragma unroll
             for (int j = 0; j < NW; ++j)
@@ -142,11 +162,15 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         for (int k = NW; k < NR; ++k) {
             if (!check[k] || !ok) continue;
             unsigned long long c = cur[k];
-            for (;;) {  // rare loop: steal a lower-priority pre-lock on a read-only word
-                if ((c & kLockFinal) || lk_ver(c) != lk_ver(tx.l[k])) { ok = false; break; }
+            for (;;) {  // rare loop: priority rule on a claimed read-only word
+                if (lk_ver(c) != lk_ver(tx.l[k])) { ok = false; break; }  // someone committed it
                 const uint32_t own = lk_owner(c);
+                if (own != 0 && own < me) { ok = false; break; }          // higher priority claims it
+                if (c & kLockFinal) {  // lower-priority holder mid-commit: wait for its release
+                    c = ld_relaxed(&v.cells[tx.loc[k]].lock);
+                    continue;
+                }
                 if (own == 0 || own == me) break;
-                if (own < me) { ok = false; break; }
                 const unsigned long long p = atomicCAS(&v.cells[tx.loc[k]].lock, c, lk_make(me, lk_ver(tx.l[k])));
                 if (p == c) { stolen_mask |= 1u << k; break; }
                 c = p;
