@@ -1044,6 +1044,15 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
     return HETM_OK;
 }
 
+int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
+    if (!d || !out || n > 9) return HETM_ERR_INVALID_ARG;
+    int rc = sync_all(d);
+    if (rc) return rc;
+    if ((rc = read_counters(d))) return rc;
+    for (uint64_t i = 0; i < n; ++i) out[i] = d->h_ctr->pad[i];
+    return HETM_OK;
+}
+
 int hetm_dev_set_timing(hetm_dev* d, int on) {
     if (!d) return HETM_ERR_INVALID_ARG;
     d->timing = on != 0;

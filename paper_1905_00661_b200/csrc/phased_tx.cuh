@@ -1,46 +1,53 @@
-// phased_tx.cuh — warp-phased PR-STM commit for transactions whose read and
-// write sets are known at begin (bank transfers: the read set is the input).
+// phased_tx.cuh — warp-phased commit for transactions whose read and write
+// sets are known at begin (bank transfers: the read set is the input).
 //
-// Same lock protocol as device_tm.cuh (per-word versioned locks in the word
-// cells, priority pre-locks that a higher priority may steal, FINAL lock during
-// write-back, commit ticket taken after the write claims are visible and
-// before the read set is validated), reorganised so a warp walks the phases in
-// lock-step and every phase issues its memory operations back to back:
+// Same lock word and serial order as device_tm.cuh (per-word versioned locks
+// in the word cells; commit ticket taken after the write locks are visible
+// and before the read set is validated), reorganised so a warp walks the
+// phases in lock-step and every phase issues its memory operations back to
+// back.  Write words are locked straight to FINAL (commit-time locking): a
+// batch-phase transaction holds its locks only for its own short commit
+// window, so the pre-lock/steal stage of device_tm.cuh — one extra atomic per
+// written word — is replaced by priority-ordered WAITING:
 //
-//   P1  128-bit {value, lock} snapshots of the NR words     (1 DRAM round trip)
-//   P2  pre-lock CAS of the NW write words                   (L2 hit)
-//       A CAS lost to a lower-priority claim is retried as a steal, so the
-//       highest-priority transaction never loses a lock race.
-//   P3  one ticket atomicAdd per warp for the surviving lanes
-//   P4  validation loads of read-only words || finalize CAS  (L2 hits)
-//       A read-only word held FINAL by a LOWER-priority transaction is waited
-//       for (its holder only ever waits on still lower priorities, so waits
-//       cannot cycle); a higher-priority claim aborts the attempt; a
-//       lower-priority pre-lock is stolen.  Aborting on every FINAL instead
-//       would let two transactions that read each other's write word abort
-//       each other forever.
-//   P5  128-bit {value, unlocked new version} stores + bitmap REDs (no wait)
+//   P1  128-bit {value, lock} snapshot of each written word, lock word of each
+//       read-only word, weak probes of the RS/WS/ChunkMap words (1 DRAM trip)
+//   P2  CAS unlocked(version) -> FINAL|prio|version on the written words; a
+//       lost race against a LOWER-priority holder waits for its release and
+//       retries, a higher-priority holder or a new version aborts
+//   P3  one ticket atomicAdd per group of converged surviving lanes
+//   P4  validation loads of the read-only words.  Priority rule: a word held
+//       FINAL by a LOWER-priority transaction is waited for (that holder only
+//       ever waits on still lower priorities, so waits cannot cycle and the
+//       highest-priority live transaction never waits); a higher-priority
+//       holder or a changed version aborts the attempt.
+//   P5  128-bit {value, unlocked new version} store per written word (write
+//       back and release in one access), REDs only for bitmap bits the P1
+//       probe found clear (bits accrete within a round, so a stale clear probe
+//       only costs a redundant RED).
 //
-// Writes are reads 0..NW-1 (no blind writes).  Duplicate words
-// inside one transaction are handled: each distinct word is locked,
-// validated and stored once (the last write to it wins, as in the oracle's
-// sequential replay).
+// Duplicate words inside one transaction are handled: each distinct word is
+// locked, validated and stored once (the last write to it wins, as in the
+// oracle's sequential replay).
 #pragma once
 #include "device_tm.cuh"
 
 namespace hetm_b200 {
 
+// Words 0..NW-1 are read-modify-written (their values are snapshotted with the
+// lock, 128-bit); words NW..NR-1 are read-only and only their lock word is
+// loaded (bank: accounts 2 and 3 are read for validation, their values unused).
 template <int NR, int NW>
 struct StaticTx {
-    uint64_t loc[NR];          // local word index of read k (writes are reads 0..NW-1)
+    uint32_t loc[NR];          // local word (cell) index; shards hold < 2^32 words
     unsigned long long l[NR];  // lock word seen in P1
-    uint64_t val[NR];          // value read in P1
-    uint64_t wval[NW];         // value to write to loc[j], j < NW
+    uint64_t val[NW];          // value of write word j seen in P1
+    uint64_t wval[NW];         // value to write to loc[j]
     uint32_t first;            // bit k set: loc[k] is the first occurrence of its word
 };
 
 template <int NR>
-__device__ __forceinline__ uint32_t first_occurrences(const uint64_t (&loc)[NR]) {
+__device__ __forceinline__ uint32_t first_occurrences(const uint32_t (&loc)[NR]) {
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
@@ -64,35 +71,74 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
     return base + __popc(m & ((1u << lane_id()) - 1u));
 }
 
-// Knock-out bits for profiling experiments only (HETM_KNOCKOUT env var; 0 in
-// production): they remove protocol steps and break serializability.
-enum : int { KO_TICKET = 1, KO_BITMAPS = 4, KO_FINALIZE = 8 };
+// Diagnostics only (HETM_KNOCKOUT env var, 0 in production): KO_PROTOCOL
+// keeps the snapshot loads and stores and drops every protocol step (the
+// access-pattern floor); KO_PHASE_CLOCKS accumulates per-phase cycles.
+enum : int { KO_PROTOCOL = 64, KO_PHASE_CLOCKS = 128 };
+
+__device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
+    const long long now = clock64();
+    acc[phase] += (unsigned long long)(now - t);
+    if (phase == 0) acc[5] += 1;
+    t = now;
+}
 
 // One phased attempt for every lane with `active`; returns true on commit and
 // sets `ticket`.  All 32 lanes of the warp must call it together.
 template <int NR, int NW, int KO = 0, class Compute>
 __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active, uint32_t me, const ShardView& v,
                                                unsigned long long* ticket_ctr, unsigned long long& ticket,
-                                               Compute compute) {
+                                               Compute compute, unsigned long long* clocks = nullptr) {
     bool ok = active;
-    // ---- P1: consistent {value, lock} snapshots
+    long long tclk = 0;
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) tclk = clock64();
+    if constexpr ((KO & KO_PROTOCOL) != 0) {  // access-pattern floor
+        if (!ok) return false;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], tx.l[k]);
+            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
+        }
+        compute(tx);
+#pragma unroll
+        for (int j = 0; j < NW; ++j) st_pair(&v.cells[tx.loc[j]], tx.wval[j], tx.l[j]);
+        ticket = me;
+        return true;
+    }
+    // ---- P1: snapshots + bitmap probes
+    uint32_t need_bits = 0;  // bit k: RS bit of word k clear; bit NR+j: WS, bit NR+NW+j: chunk
     if (ok) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) ld_pair(&v.cells[tx.loc[k]], tx.val[k], tx.l[k]);
+        for (int k = 0; k < NR; ++k) {
+            if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], tx.l[k]);
+            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
+        }
+        unsigned long long pr[NR + 2 * NW];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
+            pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
+        }
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             ok &= !(tx.l[k] & kLockFinal);
+            // a word loaded twice must show one lock word (values only change
+            // together with the version, so equal unlocked lock words imply equal values)
 #pragma unroll
-            for (int q = 0; q < k; ++q)  // a word snapshotted twice must agree
-                ok &= !(tx.loc[q] == tx.loc[k] && (tx.l[q] != tx.l[k] || tx.val[q] != tx.val[k]));
+            for (int q = 0; q < k; ++q) ok &= !(tx.loc[q] == tx.loc[k] && tx.l[q] != tx.l[k]);
+            if (!((pr[k] >> ((tx.loc[k] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << k;
         }
 #pragma unroll
-        for (int j = 0; j < NW; ++j) {  // write words: a higher-priority claim makes us back off
-            const uint32_t own = lk_owner(tx.l[j]);
-            ok &= (own == 0 || own > me);
+        for (int j = 0; j < NW; ++j) {
+            if (!((pr[NR + j] >> ((tx.loc[j] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << (NR + j);
+            if (!((pr[NR + NW + j] >> ((tx.loc[j] >> v.chunk_shift) & 63)) & 1ull))
+                need_bits |= 1u << (NR + NW + j);
         }
     }
-    // ---- P2: pre-lock CAS of the distinct write words
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 0, tclk);
+    // ---- P2: lock the distinct written words (unlocked version -> FINAL)
     bool held[NW];
 #pragma unroll
     for (int j = 0; j < NW; ++j) held[j] = false;
@@ -101,39 +147,41 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int j = 0; j < NW; ++j)
             if (tx.first & (1u << j))
-                prev[j] = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], lk_make(me, lk_ver(tx.l[j])));
+                prev[j] = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
+#pragma unroll
+        for (int j = 0; j < NW; ++j) held[j] = (tx.first & (1u << j)) && prev[j] == tx.l[j];
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
-            if (!(tx.first & (1u << j))) continue;
+            if (!(tx.first & (1u << j)) || held[j] || !ok) continue;
             unsigned long long c = prev[j];
-            const unsigned long long mine = lk_make(me, lk_ver(tx.l[j]));
-            bool got = c == tx.l[j];
-            // Lost the race: steal from a lower-priority pre-lock holder (possibly a
-            // lane of this very warp), back off from a higher one (rare path).
-            while (!got) {
-                const uint32_t own = lk_owner(c);
-                if ((c & kLockFinal) || lk_ver(c) != lk_ver(tx.l[j]) || (own != 0 && own < me)) break;
-                const unsigned long long expect = c;
-                c = atomicCAS(&v.cells[tx.loc[j]].lock, expect, mine);
-                got = c == expect;
+            // Lost the race: wait for a LOWER-priority holder to commit or back
+            // off, then retry; a higher-priority holder or a new version aborts.
+            while (c != tx.l[j]) {
+                if (lk_ver(c) != lk_ver(tx.l[j]) || !(c & kLockFinal) || lk_owner(c) < me) {
+                    ok = false;
+                    break;
+                }
+                c = ld_relaxed(&v.cells[tx.loc[j]].lock);
+                if (c == tx.l[j])
+                    c = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
             }
-            held[j] = got;
-            ok &= got;
+            held[j] = c == tx.l[j];
         }
         if (!ok) {
 #pragma unroll
             for (int j = 0; j < NW; ++j)
-                if (held[j])
-                    atomicCAS(&v.cells[tx.loc[j]].lock, lk_make(me, lk_ver(tx.l[j])), lk_make(0, lk_ver(tx.l[j])));
+                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].lock, tx.l[j]);  // nothing written: restore
         }
     }
-    // ---- P3: ticket (after every surviving lane's claims are performed)
-    const unsigned long long t = (KO & KO_TICKET) ? (unsigned long long)me : warp_ticket(ok, ticket_ctr);
-    // ---- P4: validate read-only words || finalize write words
-    bool fin[NW];
-#pragma unroll
-    for (int j = 0; j < NW; ++j) fin[j] = false;
-    uint32_t stolen_mask = 0;
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 1, tclk);
+    // ---- P3: ticket (after every surviving lane's locks are performed).  Only
+    // the converged surviving lanes aggregate: a lane may still be waiting on
+    // a lower-priority holder of this very warp, so no full-warp collective
+    // may separate lock acquisition from release.
+    unsigned long long t = 0;
+    if (ok) t = take_ticket(ticket_ctr);
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 2, tclk);
+    // ---- P4: validate the read-only words
     if (ok) {
         unsigned long long cur[NR];
         bool check[NR];
@@ -145,51 +193,24 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             check[k] = !mine && (tx.first & (1u << k));
             if (check[k]) cur[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
         }
-        unsigned long long fprev[NW];
-#pragma unroll
-        for (int j = 0; j < NW; ++j) {
-            const unsigned long long exp = lk_make(me, lk_ver(tx.l[j]));
-            if (held[j])
-                fprev[j] = (KO & KO_FINALIZE) ? exp : atomicCAS(&v.cells[tx.loc[j]].lock, exp, exp | kLockFinal);
-        }
-#pragma unroll
-        for (int j = 0; j < NW; ++j)
-            if (held[j]) {
-                fin[j] = fprev[j] == lk_make(me, lk_ver(tx.l[j]));
-                ok &= fin[j];
-            }
 #pragma unroll
         for (int k = NW; k < NR; ++k) {
-            if (!check[k] || !ok) continue;
+            if (!check[k]) continue;
             unsigned long long c = cur[k];
-            for (;;) {  // rare loop: priority rule on a claimed read-only word
-                if (lk_ver(c) != lk_ver(tx.l[k])) { ok = false; break; }  // someone committed it
-                const uint32_t own = lk_owner(c);
-                if (own != 0 && own < me) { ok = false; break; }          // higher priority claims it
-                if (c & kLockFinal) {  // lower-priority holder mid-commit: wait for its release
-                    c = ld_relaxed(&v.cells[tx.loc[k]].lock);
-                    continue;
-                }
-                if (own == 0 || own == me) break;
-                const unsigned long long p = atomicCAS(&v.cells[tx.loc[k]].lock, c, lk_make(me, lk_ver(tx.l[k])));
-                if (p == c) { stolen_mask |= 1u << k; break; }
-                c = p;
+            while (ok) {
+                if (lk_ver(c) != lk_ver(tx.l[k])) ok = false;                 // committed since P1
+                else if (!(c & kLockFinal)) break;                            // unclaimed: valid
+                else if (lk_owner(c) < me) ok = false;                        // higher priority holds it
+                else c = ld_relaxed(&v.cells[tx.loc[k]].lock);                // lower priority: wait
             }
         }
-    }
-    if (active && !ok) {  // unwind whatever this attempt still holds
+        if (!ok) {
 #pragma unroll
-        for (int j = 0; j < NW; ++j) {
-            const unsigned long long plain = lk_make(0, lk_ver(tx.l[j]));
-            if (fin[j]) st_relaxed(&v.cells[tx.loc[j]].lock, plain);
-            else if (held[j]) atomicCAS(&v.cells[tx.loc[j]].lock, lk_make(me, lk_ver(tx.l[j])), plain);
+            for (int j = 0; j < NW; ++j)
+                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].lock, tx.l[j]);
         }
-#pragma unroll
-        for (int k = NW; k < NR; ++k)
-            if (stolen_mask & (1u << k))
-                atomicCAS(&v.cells[tx.loc[k]].lock, lk_make(me, lk_ver(tx.l[k])), lk_make(0, lk_ver(tx.l[k])));
-        return false;
     }
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 3, tclk);
     if (!ok) return false;
     // ---- P5: write back + release in one 128-bit store per distinct written word
     compute(tx);
@@ -204,21 +225,14 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         st_pair(&v.cells[tx.loc[j]], val, lk_make(0, nv));
     }
 #pragma unroll
-    for (int k = NW; k < NR; ++k)
-        if (stolen_mask & (1u << k))
-            atomicCAS(&v.cells[tx.loc[k]].lock, lk_make(me, lk_ver(tx.l[k])), lk_make(0, lk_ver(tx.l[k])));
-    // fire-and-forget REDs: they drain while the next attempt's loads are in flight
-    if constexpr ((KO & KO_BITMAPS) == 0) {
+    for (int k = 0; k < NR; ++k)
+        if ((need_bits >> k) & 1u) set_bit(v.rs, tx.loc[k] >> v.gran_shift);
 #pragma unroll
-        for (int k = 0; k < NR; ++k)
-            if (tx.first & (1u << k)) set_bit(v.rs, tx.loc[k] >> v.gran_shift);
-#pragma unroll
-        for (int j = 0; j < NW; ++j)
-            if (held[j]) {
-                set_bit(v.ws, tx.loc[j] >> v.gran_shift);
-                set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
-            }
+    for (int j = 0; j < NW; ++j) {
+        if ((need_bits >> (NR + j)) & 1u) set_bit(v.ws, tx.loc[j] >> v.gran_shift);
+        if ((need_bits >> (NR + NW + j)) & 1u) set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
     }
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 4, tclk);
     ticket = t;
     return true;
 }

@@ -32,8 +32,8 @@ __device__ __forceinline__ void flush_batch_counters(unsigned long long commits,
 // Bank transfer: read 4 accounts, acct0 -= amount, acct1 += amount.
 // Warp-phased commit (phased_tx.cuh); each lane keeps its transaction across
 // retries and moves to the next one (grid stride) once it commits.
-template <int KO>
-__global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, const hetm_bank_tx* __restrict__ in,
+template <int KO, int MINB = 4>
+__global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView v, const hetm_bank_tx* __restrict__ in,
                                                                    uint64_t n, unsigned long long* __restrict__ tickets,
                                                                    DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
@@ -44,21 +44,23 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
     bool loaded = false;
     uint64_t amount = 0;
     StaticTx<4, 2> tx;
+    unsigned long long clocks[6] = {0, 0, 0, 0, 0, 0};
     while (__any_sync(0xffffffffu, i < n)) {
         if (i < n && !loaded) {
             const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
             const uint64_t w01 = __ldg(rec), w23 = __ldg(rec + 1);
             amount = __ldg(rec + 2);
-            tx.loc[0] = (w01 & 0xffffffffu) - v.base;
-            tx.loc[1] = (w01 >> 32) - v.base;
-            tx.loc[2] = (w23 & 0xffffffffu) - v.base;
-            tx.loc[3] = (w23 >> 32) - v.base;
-            if (tx.loc[0] >= v.size_words || tx.loc[1] >= v.size_words || tx.loc[2] >= v.size_words ||
-                tx.loc[3] >= v.size_words) {
+            const uint64_t l0 = (w01 & 0xffffffffu) - v.base, l1 = (w01 >> 32) - v.base;
+            const uint64_t l2 = (w23 & 0xffffffffu) - v.base, l3 = (w23 >> 32) - v.base;
+            if (l0 >= v.size_words || l1 >= v.size_words || l2 >= v.size_words || l3 >= v.size_words) {
                 tickets[i] = ~0ull;  // outside this shard: rejected, reported as OutOfBounds
                 oob = 1;
                 i += stride;
             } else {
+                tx.loc[0] = (uint32_t)l0;
+                tx.loc[1] = (uint32_t)l1;
+                tx.loc[2] = (uint32_t)l2;
+                tx.loc[3] = (uint32_t)l3;
                 tx.first = first_occurrences(tx.loc);
                 loaded = true;
             }
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
             phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, [&](StaticTx<4, 2>& x) {
                 x.wval[0] = x.val[0] - amount;
                 x.wval[1] = x.val[1] + amount;
-            });
+            }, clocks);
         if (committed) {
             tickets[i] = t;
             ++commits;
@@ -84,6 +86,13 @@ __global__ void __launch_bounds__(kTxThreads, 4) bank_batch_kernel(ShardView v, 
         i += stride;
         loaded = false;
         attempts = 0;
+    }
+    if constexpr ((KO & KO_PHASE_CLOCKS) != 0) {
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+            const unsigned long long x = warp_sum(clocks[p]);
+            if (lane_id() == 0) atomicAdd(&ctr->pad[p], x);
+        }
     }
     flush_batch_counters(commits, aborts, livelocks, oob, ctr);
 }
@@ -159,8 +168,19 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
     const unsigned grid = grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count);
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+    static const int minb = [] {
+        const char* e = std::getenv("HETM_TX_MINBLOCKS");  // occupancy experiments only
+        return e ? std::atoi(e) : 0;
+    }();
+    if (minb == 5 || minb == 6 || minb == 8) {
+        const unsigned g2 = grid_for(n, kTxThreads, minb, g.sm_count);
+        if (minb == 5) bank_batch_kernel<0, 5><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        if (minb == 6) bank_batch_kernel<0, 6><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        if (minb == 8) bank_batch_kernel<0, 8><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        return cudaGetLastError();
+    }
     switch (ko) {
-        HETM_KO_CASE(1) HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(13)
+        HETM_KO_CASE(64) HETM_KO_CASE(128)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE

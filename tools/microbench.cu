@@ -3,6 +3,7 @@
 // designs rest on numbers taken on this hardware.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/microbench tools/microbench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -115,6 +116,16 @@ int main() {
     rand_access<4, 1><<<sms * 8, 256>>>(a, W - 1, W, 99, sink);
     CK(cudaDeviceSynchronize());
     const uint64_t N = 1ull << 24;  // ops per launch
+    for (size_t gran : {(size_t)32, (size_t)64, (size_t)128, (size_t)0}) {
+        cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+        size_t got = 999;
+        cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+        float ms = timeit([&] { rand_access<1, 4><<<sms * 8, 256>>>(a, W - 1, N, 777, sink); });
+        float ms2 = timeit([&] { rand_access<2, 4><<<sms * 8, 256>>>(a, W - 1, N, 778, sink); });
+        printf("L2 fetch granularity set %zu (%s) -> reads %zu: random load %7.2f G/s, RED.MAX %7.2f G/s\n", gran,
+               cudaGetErrorString(e), got, N / (ms * 1e6), N / (ms2 * 1e6));
+    }
+    if (getenv("MICRO_ONLY_GRAN")) return 0;
     const char* names[] = {"weak load", "relaxed.gpu load", "RED.MAX", "CAS", "store", "load+store"};
     for (uint64_t region : {W, W >> 3, W >> 6}) {  // 1 GiB, 128 MiB, 16 MiB
         for (int mode = 0; mode < 6; ++mode) {
