@@ -431,7 +431,13 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     d->l2_bytes = (uint64_t)l2;
     d->geom.sm_count = sms;
     int b = 0;
-    d->geom.max_blocks_tx = (query_tx_occupancy(&b) == 0 && b > 0) ? b : 4;
+    // Batch kernels: ONE resident 256-thread CTA per SM.  The bank batch is
+    // bound by the rate of random 128-B line fills (each account touch misses
+    // L2), not by occupancy: more resident warps only lengthen the memory
+    // queues and raise the abort rate (measured 0.300 / 0.312 / 0.331 ms per
+    // 2^20-tx batch at 1 / 2 / 4 CTAs per SM).
+    if (query_tx_occupancy(&b) != 0 || b < 1) return bail(fail(d, cudaErrorInvalidConfiguration, "batch kernel occupancy"));
+    d->geom.max_blocks_tx = 1;
     d->geom.max_blocks_val = (query_val_occupancy(&b) == 0 && b > 0) ? b : 4;
     CK(d, cudaDeviceSynchronize());
     *out = d;

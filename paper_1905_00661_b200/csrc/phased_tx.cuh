@@ -74,7 +74,7 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 // Diagnostics only (HETM_KNOCKOUT env var, 0 in production): KO_PROTOCOL
 // keeps the snapshot loads and stores and drops every protocol step (the
 // access-pattern floor); KO_PHASE_CLOCKS accumulates per-phase cycles.
-enum : int { KO_PROTOCOL = 64, KO_PHASE_CLOCKS = 128 };
+enum : int { KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_PROTOCOL = 64, KO_PHASE_CLOCKS = 128 };
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
     const long long now = clock64();
@@ -114,12 +114,17 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
         }
         unsigned long long pr[NR + 2 * NW];
+        if constexpr ((KO & (KO_NO_PROBE | KO_BITMAPS)) != 0) {
 #pragma unroll
-        for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
+            for (int k = 0; k < NR + 2 * NW; ++k) pr[k] = (KO & KO_BITMAPS) ? ~0ull : 0ull;
+        } else {
 #pragma unroll
-        for (int j = 0; j < NW; ++j) {
-            pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
-            pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
+            for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
+                pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
+            }
         }
 #pragma unroll
         for (int k = 0; k < NR; ++k) {

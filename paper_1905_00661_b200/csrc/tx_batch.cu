@@ -172,6 +172,14 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         const char* e = std::getenv("HETM_TX_MINBLOCKS");  // occupancy experiments only
         return e ? std::atoi(e) : 0;
     }();
+    if (minb >= 1 && minb <= 3) {  // fewer resident blocks per SM (queueing experiments)
+        const unsigned g2 = grid_for(n, kTxThreads, minb, g.sm_count);
+        if (ko == 4) bank_batch_kernel<4><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        else if (ko == 8) bank_batch_kernel<8><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        else if (ko == 64) bank_batch_kernel<64><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        else bank_batch_kernel<0><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        return cudaGetLastError();
+    }
     if (minb == 5 || minb == 6 || minb == 8) {
         const unsigned g2 = grid_for(n, kTxThreads, minb, g.sm_count);
         if (minb == 5) bank_batch_kernel<0, 5><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
@@ -180,7 +188,7 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         return cudaGetLastError();
     }
     switch (ko) {
-        HETM_KO_CASE(64) HETM_KO_CASE(128)
+        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(64) HETM_KO_CASE(128)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE
