@@ -115,6 +115,15 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the last committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[kernel]["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -294,12 +303,14 @@ def run_ours(args):
                   f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
         },
         "roofline": {"bound": "hbm", "kernel": "bank_batch_kernel", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic("bank_batch_kernel"),
+                     "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                      "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms},
         "validate_apply": {"kernel": "validate_kernel<apply>", "gbs_algorithmic": val_gbs,
                            "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
                            "log_gbs_per_gpu": 24 * (n_val / K / world) / (val_ms * 1e-3) / 1e9,
                            "frac": val_gbs / peak, "algorithmic_bytes_per_entry": ENTRY_BYTES,
+                           "traffic": measured_traffic("validate_apply"),
                            "kernel_ms": val_ms, "aggregate_gbs": val_gbs * world},
         "batch": {"committed_last": int(st.committed), "aborts_last": int(st.aborts)},
         "bank_sum_ok": bank_sum_ok,
