@@ -163,6 +163,7 @@ def run_ours(args):
     import torch
 
     import paper_1905_00661_b200 as hetm
+    from paper_1905_00661_b200.shard import ShardedValidator
 
     world, rank, local, dist = dist_setup(args)
     torch.cuda.set_device(local)
@@ -196,33 +197,20 @@ def run_ours(args):
         t[:, 2] += (j * world + rank) * (L // 2) + 1  # unique, monotone ts across ranks and steps
         log_d.append(t)
     tickets = torch.empty(B, dtype=torch.int64, device="cuda")
-    recv = torch.empty((max(L * 2, 1), 3), dtype=torch.int64, device="cuda") if world > 1 else None
-    routed = torch.empty_like(base_log_t) if world > 1 else None
-    counts = torch.zeros(world, dtype=torch.int64, device="cuda")
     gen_s = time.time() - t_gen
 
     s_exec = dev.stream_handle(0)
     s_val = dev.stream_handle(2)
     ex = torch.cuda.ExternalStream(s_exec)
     vs = torch.cuda.ExternalStream(s_val)
+    sv = ShardedValidator(dev, world, W, L, dist, s_val)
 
     def step(j, timed_idx=None):
         tb = tx_d[j % n_bufs]
         dev.execute_batch_dptr(hetm.KERNEL_BANK, tb.data_ptr(), B, tickets.data_ptr(), s_exec)
         lg = log_d[j]
-        n_local = L
-        src = lg
-        if world > 1:
-            with torch.cuda.stream(vs):
-                dev.route_log_dptr(lg.data_ptr(), L, world, W, routed.data_ptr(), counts.data_ptr(), s_val)
-                in_splits = counts.clone()
-                out_splits = torch.empty_like(in_splits)
-                dist.all_to_all_single(out_splits, in_splits)
-                ins, outs = in_splits.tolist(), out_splits.tolist()
-                n_local = sum(outs)
-                dist.all_to_all_single(recv[:n_local], routed, outs, ins)
-                src = recv
-        dev.validate_dptr(src.data_ptr(), n_local, hetm.APPLY, s_val)
+        with torch.cuda.stream(vs):  # router, NCCL exchange and validation share the validation stream
+            n_local = sv.validate(lg, hetm.APPLY)
         dev.clear_round(asynchronous=True)
         return n_local
 
