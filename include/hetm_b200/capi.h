@@ -294,7 +294,7 @@ int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
  * duration and count, and resets the accumulator. */
 int hetm_dev_set_timing(hetm_dev* dev, int on);
 int hetm_dev_timing(hetm_dev* dev, int which, double* total_ms, uint64_t* count);
-/* Diagnostic counter words (phase clocks of instrumented builds); n <= 9. */
+/* Diagnostic counter words (phase clocks of instrumented builds); n <= 6. */
 int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);

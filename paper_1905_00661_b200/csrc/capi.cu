@@ -49,6 +49,7 @@ struct hetm_dev {
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
+    unsigned long long* d_restore = nullptr; // apply-kernel restore queue (kRestoreCap entries)
     hetm_log_entry* d_arena = nullptr;   // this round's host log, in arrival order
     uint64_t arena_cap = 0, arena_n = 0;
     std::vector<std::pair<uint64_t, uint64_t>> deferred;  // [lo,hi) streamed VALIDATE_ONLY, not applied
@@ -70,7 +71,6 @@ struct hetm_dev {
     bool shadow_synced = true;   // devShadow == devReplica as of the round start
     bool round_applied = false;  // some APPLY validation touched devReplica this round
     bool d2h_pending = false;
-    uint64_t ts_floor = 0;
     std::set<int> kernels;
     std::vector<hetm_transfer_record> xfer;
     std::mutex mu;
@@ -214,7 +214,7 @@ cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, i
         t1 = d->tev();
         cudaEventRecord(t0, s);
     }
-    cudaError_t e = launch_validate(d->view(), log, n, apply, d->ts_floor, d->d_ctr, d->geom, s);
+    cudaError_t e = launch_validate(d->view(), log, n, apply, d->d_ctr, d->d_restore, d->geom, s);
     if (d->timing && n) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
@@ -399,6 +399,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
+    if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);
     d->arena_cap = cfg->log_capacity ? cfg->log_capacity : (1ull << 20);
     if ((rc = dev_alloc(d, (void**)&d->d_arena, d->arena_cap * sizeof(hetm_log_entry)))) return bail(rc);
     if (cudaHostAlloc((void**)&d->h_ctr, sizeof(DevCounters), cudaHostAllocPortable) != cudaSuccess)
@@ -450,7 +451,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
         if (s) cudaStreamSynchronize(s);
     for (void* p : {(void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
-                    (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_arena, d->d_in,
+                    (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
@@ -929,6 +930,10 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
         CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
         CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
         CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
+        cudaError_t e = launch_roll_round(d->d_ctr, (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, s);
+        if (e != cudaSuccess) return fail(d, e, "roll_round");
+        if (flags & HETM_CLEAR_RESET_TS)
+            CK(d, cudaMemset2DAsync(&d->d_cells[0].ts, sizeof(Cell), 0, sizeof(unsigned long long), d->W, s));
         CK(d, cudaEventRecord(d->ev_round, s));
         d->arena_n = 0;
         d->deferred.clear();
@@ -939,17 +944,17 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     }
     CK(d, cudaStreamSynchronize(d->s_val));
     CK(d, cudaStreamSynchronize(d->s_exec));
-    if ((rc = read_counters(d))) return rc;
-    if (d->h_ctr->round_max_ts > d->ts_floor) d->ts_floor = d->h_ctr->round_max_ts;
     cudaStream_t s = d->s_merge;
+    {
+        cudaError_t e = launch_roll_round(d->d_ctr, (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, s);
+        if (e != cudaSuccess) return fail(d, e, "roll_round");
+    }
     CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
     CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
     CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
-    CK(d, cudaMemsetAsync(&d->d_ctr->round_max_ts, 0, 8 + 3 * sizeof(unsigned), s));
-    if (flags & HETM_CLEAR_RESET_TS) {
+    CK(d, cudaMemsetAsync(&d->d_ctr->conflict, 0, 3 * sizeof(unsigned), s));
+    if (flags & HETM_CLEAR_RESET_TS)
         CK(d, cudaMemset2DAsync(&d->d_cells[0].ts, sizeof(Cell), 0, sizeof(unsigned long long), d->W, s));
-        d->ts_floor = 0;
-    }
     CK(d, cudaEventRecord(d->ev_round, s));
     d->h_ctr->conflict = 0;
     d->arena_n = 0;
@@ -1051,7 +1056,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 9) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 6) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

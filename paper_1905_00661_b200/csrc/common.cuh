@@ -28,6 +28,10 @@ struct alignas(32) Cell {
 };
 static_assert(sizeof(Cell) == 32, "one cell per 32-B sector");
 
+// Capacity of the apply kernel's restore queue (entries); overflow falls back
+// to a full winner pass over the launch.
+constexpr uint64_t kRestoreCap = 1ull << 20;
+
 // Device-wide counters, one per handle (HBM, 128-B aligned).
 struct DevCounters {
     unsigned long long ticket;      // next commit ticket (global serial order)
@@ -39,8 +43,13 @@ struct DevCounters {
     unsigned int nonmonotone;       // a log ts <= ts_floor was seen
     unsigned int oob;               // an address outside this shard was seen
     unsigned int pad0;
-    unsigned long long pad[9];
+    unsigned long long restore_n;    // apply: raced entries queued for restore_kernel
+    unsigned long long restore_done; // restore_kernel: finished blocks
+    unsigned long long ts_floor;     // max log ts of all previous rounds (device-maintained)
+    unsigned long long pad[6];       // diagnostics (phase clocks / ticket counts)
 };
+
+static_assert(sizeof(DevCounters) == 128, "one 128-B line");
 
 // Kernel-wide view of one device's STMR shard and its metadata.
 struct ShardView {

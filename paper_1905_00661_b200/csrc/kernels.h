@@ -24,8 +24,12 @@ cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t
                             DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
 
 // engine.validateChunk over n log entries (apply: pass A + pass B).
-cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply, uint64_t ts_floor,
-                            DevCounters* ctr, const LaunchGeom& g, cudaStream_t s);
+// Apply-mode launches of one handle must be stream-ordered (they share d_restore,
+// kRestoreCap entries, and rely on the previous launch's stores being complete).
+cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
+                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
+// Round boundary: ts_floor = max(ts_floor, round_max_ts) (0 with reset_ts), round_max_ts = 0.
+cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s);
 // Winner store of the round's log: value of the entry whose ts equals the
 // cell's TS goes to dst[addr] (plain array) or, with dst == nullptr, to the
 // cell's value (rollback / shadow patch).

@@ -74,7 +74,12 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 // Diagnostics only (HETM_KNOCKOUT env var, 0 in production): KO_PROTOCOL
 // keeps the snapshot loads and stores and drops every protocol step (the
 // access-pattern floor); KO_PHASE_CLOCKS accumulates per-phase cycles.
-enum : int { KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_PROTOCOL = 64, KO_PHASE_CLOCKS = 128 };
+// KO_COUNT_TICKETS counts ticket atomics (debug word 4); KO_STRIPED_TICKET
+// draws tickets from per-CTA counters (breaks the serial order: timing only).
+enum : int {
+    KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_STRIPED_TICKET = 32, KO_PROTOCOL = 64,
+    KO_PHASE_CLOCKS = 128
+};
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
     const long long now = clock64();
@@ -184,7 +189,14 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     // a lower-priority holder of this very warp, so no full-warp collective
     // may separate lock acquisition from release.
     unsigned long long t = 0;
-    if (ok) t = take_ticket(ticket_ctr);
+    if constexpr ((KO & KO_STRIPED_TICKET) != 0) {
+        if (ok) t = take_ticket(reinterpret_cast<unsigned long long*>(&v.cells[((uint64_t)blockIdx.x * 7919u) % v.size_words].spare));
+    } else {
+        if (ok) t = take_ticket(ticket_ctr);
+    }
+    if constexpr ((KO & KO_COUNT_TICKETS) != 0) {
+        if (ok && lane_id() == (unsigned)(__ffs(__activemask()) - 1)) clocks[0] += 1;
+    }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 2, tclk);
     // ---- P4: validate the read-only words
     if (ok) {

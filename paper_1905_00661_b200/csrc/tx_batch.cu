@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         loaded = false;
         attempts = 0;
     }
+    if constexpr ((KO & KO_COUNT_TICKETS) != 0) {
+        const unsigned long long x = warp_sum(clocks[0]);
+        if (lane_id() == 0) atomicAdd(&ctr->pad[4], x);
+    }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) {
 #pragma unroll
         for (int p = 0; p < 6; ++p) {
@@ -188,7 +192,7 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         return cudaGetLastError();
     }
     switch (ko) {
-        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(64) HETM_KO_CASE(128)
+        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(32) HETM_KO_CASE(64) HETM_KO_CASE(128)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE

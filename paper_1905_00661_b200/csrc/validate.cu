@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+
 namespace hetm_b200 {
 
 constexpr int kValThreads = 256;
@@ -33,37 +34,31 @@ __device__ __forceinline__ EntryRegs load_entry(const hetm_log_entry* log, uint6
     return EntryRegs{__ldg(e), __ldg(e + 1), __ldg(e + 2)};
 }
 
-template <bool kApply>
-__global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
-                                                               uint64_t n, uint64_t ts_floor, DevCounters* ctr) {
+// Pass A of one entry (RS test + TS raise); returns nothing, folds flags.
+struct PassAFlags {
     unsigned conflict = 0, bad = 0, oob = 0;
     unsigned long long maxts = 0;
-    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
-        EntryRegs e[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base, 0, ~0ull};
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            if (i0 + (uint64_t)u * blockDim.x >= n) continue;
-            const uint64_t loc = e[u].addr - v.base;
-            if (loc >= v.size_words) {
-                oob = 1;
-                continue;
-            }
-            const uint64_t bit = loc >> v.gran_shift;
-            conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
-            bad |= (e[u].ts <= ts_floor);
-            maxts = e[u].ts > maxts ? e[u].ts : maxts;
-            if (kApply) atomicMax(&v.cells[loc].ts, (unsigned long long)e[u].ts);  // (b) pass A
-        }
+};
+
+template <bool kApply>
+__device__ __forceinline__ void pass_a(const ShardView& v, const EntryRegs& e, uint64_t ts_floor, PassAFlags& f) {
+    const uint64_t loc = e.addr - v.base;
+    if (loc >= v.size_words) {
+        f.oob = 1;
+        return;
     }
-    conflict = __any_sync(0xffffffffu, conflict);
-    bad = __any_sync(0xffffffffu, bad);
-    oob = __any_sync(0xffffffffu, oob);
+    const uint64_t bit = loc >> v.gran_shift;
+    f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
+    f.bad |= (e.ts <= ts_floor);
+    f.maxts = e.ts > f.maxts ? e.ts : f.maxts;
+    if (kApply) atomicMax(&v.cells[loc].ts, (unsigned long long)e.ts);  // (b) pass A
+}
+
+__device__ __forceinline__ void flush_pass_a(PassAFlags f, DevCounters* ctr) {
+    const unsigned conflict = __any_sync(0xffffffffu, f.conflict);
+    const unsigned bad = __any_sync(0xffffffffu, f.bad);
+    const unsigned oob = __any_sync(0xffffffffu, f.oob);
+    unsigned long long maxts = f.maxts;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long x = __shfl_xor_sync(0xffffffffu, maxts, o);
@@ -74,6 +69,103 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, cons
         if (bad) atomicOr(&ctr->nonmonotone, 1u);
         if (oob) atomicOr(&ctr->oob, 1u);
         if (maxts) atomicMax(&ctr->round_max_ts, maxts);
+    }
+}
+
+template <bool kApply>
+__global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
+                                                               uint64_t n, DevCounters* ctr) {
+    const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
+    PassAFlags f;
+    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
+        EntryRegs e[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base, 0, ~0ull};
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (i0 + (uint64_t)u * blockDim.x < n) pass_a<kApply>(v, e[u], ts_floor, f);
+    }
+    flush_pass_a(f, ctr);
+}
+
+// Apply pass ("if entry.ts > TS.ts: dev[addr] = value; TS.ts = ts"):
+// one RETURNING atomicMax on the cell's TS; an entry that raised the TS
+// stores its value into the same (now L2-resident) sector right away.  Two
+// entries of one launch for the same word can race on that store; the larger
+// ts then saw a TS raised THIS round (old > ts_floor) and is queued for
+// restore_kernel, which re-stores it after this launch's stores completed.
+// An entry whose atomic saw a stale TS (old <= ts_floor) was first in the
+// atomic order, so every later entry for that word either loses (smaller ts)
+// or is queued itself.  Cost per entry: one random line RMW + one L2-hit
+// store; duplicates (rare under uniform access) cost one more L2 load+store.
+__global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
+                                                            uint64_t n, DevCounters* ctr,
+                                                            unsigned long long* __restrict__ restore) {
+    const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
+    PassAFlags f;
+    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
+        EntryRegs e[kUnroll];
+        unsigned long long old[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base + v.size_words, 0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t loc = e[u].addr - v.base;
+            old[u] = ~0ull;
+            if (i0 + (uint64_t)u * blockDim.x >= n) continue;
+            if (loc >= v.size_words) {
+                f.oob = 1;
+                continue;
+            }
+            const uint64_t bit = loc >> v.gran_shift;
+            f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
+            f.bad |= (e[u].ts <= ts_floor);
+            f.maxts = e[u].ts > f.maxts ? e[u].ts : f.maxts;
+            old[u] = atomicMax(&v.cells[loc].ts, (unsigned long long)e[u].ts);  // (b) TS raise
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (old[u] >= e[u].ts) continue;  // lost, out of shard, or past the end
+            v.cells[e[u].addr - v.base].value = e[u].value;
+            if (old[u] > ts_floor) {  // raced with another entry of this round: re-store later
+                const unsigned long long k = atomicAdd(&ctr->restore_n, 1ull);
+                if (k < kRestoreCap) restore[k] = i0 + (uint64_t)u * blockDim.x;
+            }
+        }
+    }
+    flush_pass_a(f, ctr);
+}
+
+// Re-store the queued entries whose ts is still the cell's TS (the unique
+// freshest one per word).  If the queue overflowed, every entry of the launch
+// is checked (pass B of the classic two-pass scheme).  The last block to
+// finish resets the queue for the next apply launch on this stream.
+__global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
+                                                              uint64_t n, DevCounters* ctr,
+                                                              const unsigned long long* __restrict__ restore) {
+    const unsigned long long m = ld_relaxed(&ctr->restore_n);
+    const bool full = m > kRestoreCap;
+    const uint64_t cnt = full ? n : m;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x) {
+        const EntryRegs e = load_entry(log, full ? j : restore[j]);
+        const uint64_t loc = e.addr - v.base;
+        if (loc < v.size_words && ld_relaxed(&v.cells[loc].ts) == e.ts) v.cells[loc].value = e.value;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->restore_done, 1ull) == gridDim.x - 1) {
+            ctr->restore_n = 0;
+            ctr->restore_done = 0;
+        }
     }
 }
 
@@ -127,16 +219,31 @@ static unsigned grid_cap(uint64_t items, int threads, const LaunchGeom& g, int p
     return (unsigned)(want ? want : 1);
 }
 
-cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply, uint64_t ts_floor,
-                            DevCounters* ctr, const LaunchGeom& g, cudaStream_t s) {
+// Round boundary on the device: ts_floor = max(ts_floor, round_max_ts) (or 0
+// for the literal SPEC.md:421 TS reset), round_max_ts = 0.  Enqueued by both
+// the synchronous and the asynchronous clear so pipelined rounds keep an exact
+// floor without a host round trip.
+__global__ void roll_round_kernel(DevCounters* ctr, int reset_ts) {
+    const unsigned long long m = ctr->round_max_ts;
+    ctr->ts_floor = reset_ts ? 0ull : (m > ctr->ts_floor ? m : ctr->ts_floor);
+    ctr->round_max_ts = 0;
+}
+
+cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s) {
+    roll_round_kernel<<<1, 1, 0, s>>>(ctr, reset_ts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
+                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const unsigned grid = grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
-    if (apply) {
-        validate_kernel<true><<<grid, kValThreads, 0, s>>>(v, d_log, n, ts_floor, ctr);
-        winner_kernel<<<grid, kValThreads, 0, s>>>(v.cells, nullptr, v.base, v.size_words, d_log, n);
-    } else {
-        validate_kernel<false><<<grid, kValThreads, 0, s>>>(v, d_log, n, ts_floor, ctr);
+    if (!apply) {
+        validate_kernel<false><<<grid, kValThreads, 0, s>>>(v, d_log, n, ctr);
+        return cudaGetLastError();
     }
+    apply_kernel<<<grid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
+    restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
     return cudaGetLastError();
 }
 

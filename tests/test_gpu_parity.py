@@ -220,6 +220,35 @@ def test_validate_apply_matches_oracle(hetm, orc, dev_factory, gran):
     assert (d.download(hetm.REPLICA_DEV) == dev).all()
 
 
+def test_validate_hot_words_one_chunk(hetm, orc, dev_factory):
+    """Many entries per word inside ONE apply launch, ts ascending with the
+    entry index (most TS raises race with an earlier entry of the launch): the
+    apply kernel's restore queue, and its overflow fallback (> 2^20 raced
+    entries), must still leave the freshest value in every word."""
+    W = 1 << 12
+    for n, tsorder in ((1 << 16, "random"), (3 << 20, "ascending")):
+        rng = np.random.default_rng(n)
+        log = np.zeros(n, dtype=hetm.LOG_ENTRY)
+        log["addr"] = rng.integers(0, W, n)
+        log["value"] = rng.integers(0, 2**63, n, dtype=np.uint64)
+        log["ts"] = (rng.permutation(n) if tsorder == "random" else np.arange(n)) + 1
+        d = dev_factory(W, rs_gran_bytes=8, log_capacity=n)
+        d.stream_chunk(log)
+        assert not d.round_verdict()
+        ts, want = np.zeros(W, np.uint64), np.zeros(W, np.uint64)
+        orc.validate_chunk(log, np.zeros(W // 64, np.uint64), 8, ts, want)
+        assert (d.download(hetm.REPLICA_DEV) == want).all(), tsorder
+        # the queue is reset for the next launch: a second round on the same handle
+        d.clear_round()
+        log2 = log.copy()
+        log2["ts"] += n
+        log2["value"] ^= np.uint64(0x5555)
+        d.stream_chunk(log2)
+        assert not d.round_verdict()
+        orc.validate_chunk(log2, np.zeros(W // 64, np.uint64), 8, ts, want)
+        assert (d.download(hetm.REPLICA_DEV) == want).all(), tsorder
+
+
 def test_validate_permuted_delivery_orders(hetm, orc, dev_factory):
     """Acceptance #5 on the device: 10 delivery orders, same max-ts result."""
     W = 256
