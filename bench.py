@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--gran", type=int, default=1024)
     p.add_argument("--l2-fetch32", action="store_true", help="cudaLimitMaxL2FetchGranularity = 32 B")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--chunk-merge", action="store_true", help="SPEC chunk-copy merge instead of the delta merge")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-preroll", action="store_true", help="skip the clock-sampling pre-roll (profiling runs)")
@@ -173,7 +174,8 @@ def run_ours(args):
     K, WU = args.steps, args.warmup
     n_steps = K + WU
 
-    dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, device=local, log_capacity=max(L, 1 << 20), l2_fetch_32=args.l2_fetch32)
+    dev = hetm.GpuDevice(W, shard_base=base, rs_gran_bytes=args.gran, device=local, log_capacity=max(L, 1 << 20),
+                         l2_fetch_32=args.l2_fetch32, merge_delta=not args.chunk_merge)
     dev.register_kernel(hetm.KERNEL_BANK)
     init = np.full(W, 1000, np.uint64)
     dev.upload(hetm.REPLICA_DEV, base, init)
@@ -341,15 +343,19 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
     t0 = time.perf_counter()
     for j in range(steps + 1):
         if j == 1:  # first round is warm-up
+            dev.merge_wait()
             if dist:
                 dist.barrier()
             t0 = time.perf_counter()
             h2d = d2h = 0
         lg = logs[j].array
         st = hetm._lib.BatchStats()
+        # the GPU resumes right away: this batch overlaps the
+        # previous round's merge landing in the host replica
         rc = lib.hetm_dev_execute_batch(dev.h, hetm.KERNEL_BANK, txs[j % 2].array.ctypes.data, 24, B,
                                         tickets.array.ctypes.data, C.byref(st))
         hetm.check(rc, dev.h)
+        dev.merge_wait()  # host transactions of this round see the merged replica
         for c in range(8):  # the round's log streamed in 8 chunks (one per host thread)
             sl = lg[c * (L // 8):(c + 1) * (L // 8)]
             dev.stream_chunk(sl, src_thread=c, seq=c)
@@ -357,10 +363,10 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
         if conflict:
             raise RuntimeError("unexpected conflict in the partitioned e2e round")
         ms = dev.merge_commit(host_replica.array)
-        dev.merge_wait()
         dev.clear_round()
         h2d += B * 24 + L * 24
         d2h += B * 8 + ms.bytes_d2h
+    dev.merge_wait()
     dt = time.perf_counter() - t0
     if dist:
         import torch
@@ -371,7 +377,9 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
         p.free()
     return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
-            "timing": "host wall clock around full synchronous rounds (pinned buffers; verdict + merge D2H)"}
+            "merge": "chunk copy (SPEC.md:363-371)" if args.chunk_merge else "delta (16-B {word,value} per device-written word)",
+            "timing": "host wall clock around full rounds (pinned buffers; verdict + merge D2H landed in the host "
+                      "replica before the next round's host log; the next GPU batch overlaps the merge, PAPER.md:355)"}
 
 
 # ---------------------------------------------------------- CPU baseline

@@ -87,6 +87,10 @@ enum hetm_kernel_id {
 /* hetm_dev_config.flags */
 #define HETM_CFG_NO_SHADOW 1u /* do not allocate devShadow (validation-only sweeps) */
 #define HETM_CFG_L2_FETCH_32 2u /* cudaLimitMaxL2FetchGranularity = 32 B (random 8-B word access) */
+#define HETM_CFG_MERGE_DELTA 4u /* mergeCommit ships the device write set as {word, value} records
+                                   (16 B per written word) when that is smaller than the dirty
+                                   chunks; recorded as HETM_TAG_MERGE_DELTA.  Off: the SPEC.md:
+                                   363-371 chunk copy (16 KiB per dirty chunk) */
 
 /* ------------------------------------------------------------ wire types -- */
 
@@ -168,7 +172,7 @@ typedef struct hetm_transfer_record {
 } hetm_transfer_record;
 enum hetm_transfer_tag {
     HETM_TAG_LOG = 0, HETM_TAG_MERGE = 1, HETM_TAG_SHADOW = 2, HETM_TAG_ROLLBACK = 3,
-    HETM_TAG_INPUT = 4, HETM_TAG_OUTPUT = 5, HETM_TAG_RAW = 6
+    HETM_TAG_INPUT = 4, HETM_TAG_OUTPUT = 5, HETM_TAG_RAW = 6, HETM_TAG_MERGE_DELTA = 7
 };
 
 typedef struct hetm_dev hetm_dev;
@@ -294,7 +298,7 @@ int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
  * duration and count, and resets the accumulator. */
 int hetm_dev_set_timing(hetm_dev* dev, int on);
 int hetm_dev_timing(hetm_dev* dev, int which, double* total_ms, uint64_t* count);
-/* Diagnostic counter words (phase clocks of instrumented builds); n <= 6. */
+/* Diagnostic counter words (phase clocks of instrumented builds); n <= 5. */
 int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);

@@ -12,9 +12,13 @@
 // the explicitly synchronous calls (verdict, merge_wait, snapshots, stats).
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <set>
 #include <string>
 #include <utility>
@@ -30,6 +34,63 @@ int query_val_occupancy(int* blocks);
 }  // namespace hetm_b200
 
 using namespace hetm_b200;
+
+namespace {
+// Persistent host workers for the delta merge: start(f) runs f(w, n) once on
+// every worker w in [0, n) and returns immediately; wait() joins that job.
+class WorkerPool {
+public:
+    explicit WorkerPool(int n) : n_(n) {
+        for (int w = 0; w < n; ++w) th_.emplace_back([this, w] { loop(w); });
+    }
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void start(std::function<void(int, int)> f) {
+        wait();
+        std::lock_guard<std::mutex> g(m_);
+        job_ = std::move(f);
+        pending_ = n_;
+        ++gen_;
+        cv_.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> g(m_);
+        done_.wait(g, [this] { return pending_ == 0; });
+    }
+
+private:
+    void loop(int w) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(int, int)> f;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                f = job_;
+            }
+            f(w, n_);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::function<void(int, int)> job_;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+}  // namespace
 
 struct hetm_dev {
     hetm_dev_config cfg{};
@@ -50,6 +111,17 @@ struct hetm_dev {
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
     unsigned long long* d_restore = nullptr; // apply-kernel restore queue (kRestoreCap entries)
+    uint32_t* d_wlog = nullptr;          // write-set log (2 slots per commit ticket of the round)
+    uint64_t wlog_slots = 0;
+    uint64_t round_tx = 0;               // transactions submitted this round (ticket upper bound)
+    uint32_t* d_wsorted = nullptr;       // write-set log sorted by word (delta merge)
+    void* d_sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    DeltaRec* d_delta = nullptr;         // merge delta (device) and its pinned host landing buffer
+    DeltaRec* h_delta = nullptr;
+    uint64_t delta_cap = 0;
+    std::vector<cudaEvent_t> piece_ev;   // per-piece D2H completion of the delta
+    std::unique_ptr<WorkerPool> pool;    // host scatter of the delta into host_replica
     hetm_log_entry* d_arena = nullptr;   // this round's host log, in arrival order
     uint64_t arena_cap = 0, arena_n = 0;
     std::vector<std::pair<uint64_t, uint64_t>> deferred;  // [lo,hi) streamed VALIDATE_ONLY, not applied
@@ -104,6 +176,8 @@ struct hetm_dev {
         v.chunk = d_chunk;
         v.gran_shift = gran_shift;
         v.chunk_shift = chunk_shift;
+        v.wlog = d_wlog;
+        v.wlog_slots = wlog_slots;
         return v;
     }
     void record(int dir, int tag, uint64_t bytes) { xfer.push_back(hetm_transfer_record{dir, tag, bytes}); }
@@ -178,9 +252,34 @@ size_t record_bytes(int kernel_id) {
     }
 }
 
+// Grow the write-set log to hold 2 slots per transaction submitted this round
+// (+ n more).  Shards of >= 2^32 words keep it disabled (chunk merge only).
+int ensure_wlog(hetm_dev* d, uint64_t n) {
+    if (d->W >= (1ull << 32)) return HETM_OK;
+    // tickets of attempts that aborted after taking one also own slots: +25% headroom
+    // (a round that outruns it merges by chunks; the log is only an accelerator)
+    const uint64_t need = 2 * (d->round_tx + n) + (d->round_tx + n) / 2 + 65536;
+    if (need <= d->wlog_slots) return HETM_OK;
+    const uint64_t cap = std::max<uint64_t>({need, 2 * d->wlog_slots, 1ull << 21});
+    int rc = sync_all(d);
+    if (rc) return rc;
+    void* p = nullptr;
+    if ((rc = dev_alloc(d, &p, cap * 4))) return rc;
+    if (d->d_wlog) {
+        const uint64_t used = std::min<uint64_t>(2 * d->round_tx, d->wlog_slots);
+        if (used) CK(d, cudaMemcpy(p, d->d_wlog, used * 4, cudaMemcpyDeviceToDevice));
+        cudaFree(d->d_wlog);
+        d->bytes_alloc -= d->wlog_slots * 4;
+    }
+    d->d_wlog = static_cast<uint32_t*>(p);
+    d->wlog_slots = cap;
+    return HETM_OK;
+}
+
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
                   cudaStream_t s) {
+    if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
     CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
@@ -203,6 +302,7 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
         d->tpairs[0].emplace_back(t0, t1);
     }
     CK(d, cudaEventRecord(d->ev_exec, s));
+    d->round_tx += n;
     return HETM_OK;
 }
 
@@ -450,7 +550,10 @@ int hetm_dev_close(hetm_dev* d) {
     cudaSetDevice(d->device);
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
         if (s) cudaStreamSynchronize(s);
-    for (void* p : {(void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    d->pool.reset();
+    if (d->h_delta) cudaFreeHost(d->h_delta);
+    for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
+    for (void* p : {(void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
@@ -761,6 +864,90 @@ int hetm_dev_sync(hetm_dev* d) {
 }
 
 // ------------------------------------------------------------------- merge
+namespace {
+constexpr uint64_t kDeltaPiece = 1ull << 17;  // delta records per D2H piece (2 MiB)
+
+// mergeCommit, delta form: the round's write-set log becomes a compact
+// {word, value} list (16 B per written word instead of 16 KiB per dirty
+// chunk), refreshed into devShadow on the device, DMA'd in pieces, and
+// scattered into host_replica by the worker pool as each piece lands.  The
+// host replica ends identical to the chunk copy: the words outside the device
+// write set inside a dirty chunk already hold the host's values (the round
+// committed, so no host entry touched a device-read word).
+int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots) {
+    if (d->pool) d->pool->wait();
+    if (n_slots > d->delta_cap) {
+        CK(d, cudaStreamSynchronize(d->s_d2h));
+        if (d->d_delta) { cudaFree(d->d_delta); d->bytes_alloc -= d->delta_cap * sizeof(DeltaRec); d->d_delta = nullptr; }
+        if (d->d_wsorted) { cudaFree(d->d_wsorted); d->bytes_alloc -= d->delta_cap * 4; d->d_wsorted = nullptr; }
+        if (d->d_sort_tmp) { cudaFree(d->d_sort_tmp); d->bytes_alloc -= d->sort_tmp_bytes; d->d_sort_tmp = nullptr; }
+        if (d->h_delta) { cudaFreeHost(d->h_delta); d->h_delta = nullptr; }
+        const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
+        if (int rc = dev_alloc(d, (void**)&d->d_delta, cap * sizeof(DeltaRec))) return rc;
+        if (int rc = dev_alloc(d, (void**)&d->d_wsorted, cap * 4)) return rc;
+        d->sort_tmp_bytes = wlog_sort_temp_bytes(cap, d->W);
+        if (int rc = dev_alloc(d, &d->d_sort_tmp, d->sort_tmp_bytes)) return rc;
+        if (cudaHostAlloc((void**)&d->h_delta, cap * sizeof(DeltaRec), cudaHostAllocPortable) != cudaSuccess)
+            return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
+        d->delta_cap = cap;
+    }
+    if (!d->pool) {
+        const unsigned hc = std::thread::hardware_concurrency();
+        d->pool.reset(new WorkerPool((int)std::max(1u, std::min(16u, hc ? hc : 4u))));
+    }
+    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
+    // shadow: incremental when it held the round-start state, else a full copy
+    uint64_t* shadow_inc = (d->d_shadow && d->shadow_synced) ? d->d_shadow : nullptr;
+    if (d->d_shadow && !d->shadow_synced) {
+        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, nullptr, d->chunk_bits, d->chunk_shift, true,
+                                            d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(full shadow)");
+        d->record(HETM_D2D, HETM_TAG_SHADOW, d->W * 8);
+        d->shadow_synced = true;
+    }
+    cudaError_t e = launch_wlog_sort(d->d_wlog, d->d_wsorted, n_slots, d->W, d->d_sort_tmp, d->sort_tmp_bytes,
+                                     d->s_merge);
+    if (e != cudaSuccess) return fail(d, e, "wlog_sort");
+    e = launch_wlog_gather(d->d_delta, shadow_inc, d->d_cells, d->d_wsorted, n_slots, d->W, d->geom, d->s_merge);
+    if (e != cudaSuccess) return fail(d, e, "wlog_gather");
+    if (shadow_inc) {
+        e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
+        d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
+    }
+    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+    CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
+    const uint64_t pieces = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
+    while (d->piece_ev.size() < pieces) {
+        cudaEvent_t ev = nullptr;
+        CK(d, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        d->piece_ev.push_back(ev);
+    }
+    for (uint64_t k = 0; k < pieces; ++k) {
+        const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
+        CK(d, cudaMemcpyAsync(d->h_delta + lo, d->d_delta + lo, m * sizeof(DeltaRec), cudaMemcpyDeviceToHost, d->s_d2h));
+        CK(d, cudaEventRecord(d->piece_ev[k], d->s_d2h));
+    }
+    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, n_slots * sizeof(DeltaRec));
+    CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
+    d->d2h_pending = true;
+    const DeltaRec* src = d->h_delta;
+    const std::vector<cudaEvent_t> evs(d->piece_ev.begin(), d->piece_ev.begin() + pieces);
+    const int dev = d->device;
+    d->pool->start([src, evs, host, n_slots, dev](int w, int nw) {
+        cudaSetDevice(dev);
+        for (uint64_t k = 0; k < evs.size(); ++k) {
+            cudaEventSynchronize(evs[k]);
+            const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
+            const uint64_t a = lo + m * w / nw, b = lo + m * (w + 1) / nw;
+            for (uint64_t i = a; i < b; ++i)
+                if (src[i].loc != ~0ull) host[src[i].loc] = src[i].value;
+        }
+    });
+    return HETM_OK;
+}
+}  // namespace
+
 int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     if (!d || !host) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
@@ -778,6 +965,23 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     if ((rc = dirty_ranges(d, ranges, &nd))) return rc;
     uint64_t dirty_bytes = 0;
     for (auto& r : ranges) dirty_bytes += r.second * 8;
+    // delta form when enabled, the write-set log is complete and it moves fewer bytes
+    const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
+    const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && n_slots <= d->wlog_slots &&
+                       n_slots * sizeof(DeltaRec) < dirty_bytes;
+    if (delta) {
+        if ((rc = merge_commit_delta(d, host, n_slots))) return rc;
+        if (st) {
+            std::memset(st, 0, sizeof(*st));
+            st->dirty_chunks = nd;
+            st->transfers = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
+            st->bytes_d2h = n_slots * sizeof(DeltaRec);
+            st->bytes_d2d = d->d_shadow ? n_slots * 8 : 0;
+            st->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+        return HETM_OK;
+    }
+    if (d->pool) d->pool->wait();  // a previous delta merge may still be landing in host_replica
     const uint64_t* src = d->d_shadow;
     if (d->d_shadow) {
         if ((rc = refresh_shadow(d, true, dirty_bytes))) return rc;
@@ -914,6 +1118,7 @@ int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snaps
 
 int hetm_dev_merge_wait(hetm_dev* d) {
     if (!d) return HETM_ERR_INVALID_ARG;
+    if (d->pool) d->pool->wait();
     CK(d, cudaStreamSynchronize(d->s_merge));
     CK(d, cudaStreamSynchronize(d->s_d2h));
     d->d2h_pending = false;
@@ -939,6 +1144,7 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
         d->deferred.clear();
         d->deferred_final = false;
         d->round_applied = false;
+        d->round_tx = 0;
         d->intake_open = true;
         return HETM_OK;
     }
@@ -961,6 +1167,7 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     d->deferred.clear();
     d->deferred_final = false;
     d->round_applied = false;
+    d->round_tx = 0;
     d->intake_open = true;
     return HETM_OK;
 }
@@ -1056,7 +1263,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 6) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 5) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

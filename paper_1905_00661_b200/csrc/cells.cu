@@ -2,6 +2,8 @@
 // (common.cuh) and plain 64-bit word arrays (devShadow, raw-op staging).
 // Used at the edges only: raw ops, the shadow refresh of
 // mergeCommit and the rollback of mergeAbortDevice.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -37,6 +39,24 @@ __global__ void dirty_chunks_kernel(uint64_t* __restrict__ plain, Cell* __restri
     }
 }
 
+// mergeCommit delta: out[i] = {word, devReplica value} for every write-set
+// log slot (duplicates carry the same final value; empty slots -> ~0 word),
+// and the same value into devShadow (the incremental shadow refresh).
+__global__ void wlog_gather_kernel(DeltaRec* __restrict__ out, uint64_t* __restrict__ shadow,
+                                   const Cell* __restrict__ cells, const uint32_t* __restrict__ wlog, uint64_t n,
+                                   uint64_t size_words) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t loc = wlog[i];
+        if (loc < size_words) {
+            const uint64_t val = cells[loc].value;
+            out[i] = DeltaRec{loc, val};
+            if (shadow) shadow[loc] = val;
+        } else {
+            out[i] = DeltaRec{~0ull, 0};
+        }
+    }
+}
+
 static unsigned grid_words(uint64_t n, const LaunchGeom& g) {
     uint64_t want = (n + 255) / 256;
     const uint64_t cap = (uint64_t)g.sm_count * 16;
@@ -55,6 +75,37 @@ cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, 
     if (n == 0) return cudaSuccess;
     scatter_range_kernel<<<grid_words(n, g), 256, 0, s>>>(cells, src, lo, n);
     return cudaGetLastError();
+}
+
+cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
+                               uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    wlog_gather_kernel<<<grid_words(n, g), 256, 0, s>>>(out, shadow, cells, wlog, n, size_words);
+    return cudaGetLastError();
+}
+
+// Sort the write-set log by word (CUB onesweep radix sort over the bits a
+// local word index needs): the delta then reaches the host in address order,
+// so each host worker scatters into one contiguous range of the replica.
+// Empty slots (~0u) have all low bits set and sort last (a tie with word
+// 2^bits-1 is harmless: the gather skips empty slots wherever they land).
+static int sort_bits(uint64_t size_words) {
+    int b = 1;
+    while (b < 32 && (1ull << b) < size_words) ++b;
+    return b;
+}
+
+size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
+                                   sort_bits(size_words));
+    return bytes;
+}
+
+cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
+                             size_t temp_bytes, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int64_t)n, 0, sort_bits(size_words), s);
 }
 
 cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,

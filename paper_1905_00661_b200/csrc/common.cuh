@@ -46,7 +46,8 @@ struct DevCounters {
     unsigned long long restore_n;    // apply: raced entries queued for restore_kernel
     unsigned long long restore_done; // restore_kernel: finished blocks
     unsigned long long ts_floor;     // max log ts of all previous rounds (device-maintained)
-    unsigned long long pad[6];       // diagnostics (phase clocks / ticket counts)
+    unsigned long long wlog_base;    // first commit ticket of the round (write-set log origin)
+    unsigned long long pad[5];       // diagnostics (phase clocks / ticket counts)
 };
 
 static_assert(sizeof(DevCounters) == 128, "one 128-B line");
@@ -61,7 +62,19 @@ struct ShardView {
     unsigned long long* chunk; // ChunkMap words
     uint32_t gran_shift;       // bit = local_word >> gran_shift   (gran = 8 << gran_shift)
     uint32_t chunk_shift;      // chunk = local_word >> chunk_shift
+    uint32_t* wlog;            // device write-set log (nullptr: disabled, shard >= 2^32 words)
+    uint64_t wlog_slots;       // its capacity in slots
 };
+
+// Device write-set log: slot 2*(ticket - round's first ticket) + j holds the
+// local index of the j-th written word of the committed transaction (~0u:
+// none).  Consecutive tickets of a warp store contiguously; the merge turns
+// the log into a compact {word, value} delta.
+__device__ __forceinline__ void wlog_put(const ShardView& v, unsigned long long wbase, unsigned long long t, int j,
+                                         uint32_t loc) {
+    const unsigned long long s = (t - wbase) * 2ull + (unsigned)j;
+    if (s < v.wlog_slots) v.wlog[s] = loc;
+}
 
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
     uint64_t v;

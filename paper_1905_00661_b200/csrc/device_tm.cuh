@@ -156,6 +156,7 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
     }
     // 3. commit ticket
     const unsigned long long t = take_ticket(ticket_ctr);
+    ticket = t;  // reported even if validation aborts below (write-set log slots)
     // 4. validate the read-only part of the read set (steal lower-priority pre-locks)
     uint64_t st_loc[R];
     uint32_t st_ver[R];

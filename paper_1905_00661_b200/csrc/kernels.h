@@ -11,6 +11,12 @@ struct DevCounters;
 struct ShardView;
 struct Cell;
 
+// One merge delta record: local word index + value (16 B, DMA'd to the host).
+struct DeltaRec {
+    uint64_t loc;
+    uint64_t value;
+};
+
 struct LaunchGeom {
     int sm_count;
     int max_blocks_tx;    // resident blocks per SM for the batch kernels
@@ -44,6 +50,13 @@ cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, 
 cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,
                                 uint64_t n_chunks, uint32_t chunk_shift, bool to_plain, const LaunchGeom& g,
                                 cudaStream_t s);
+// Write-set log -> compact delta (+ devShadow refresh when shadow != nullptr).
+cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
+                               uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
+// Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
+size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
+cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
+                             size_t temp_bytes, cudaStream_t s);
 // Popcount of n words into *out (device counter, accumulated).
 cudaError_t launch_popcount(const unsigned long long* words, uint64_t n, unsigned long long* out, cudaStream_t s);
 // OR src words into dst words.

@@ -89,7 +89,9 @@ __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, l
 }
 
 // One phased attempt for every lane with `active`; returns true on commit and
-// sets `ticket`.  All 32 lanes of the warp must call it together.
+// sets `ticket`.  An attempt that took a ticket and then aborted also reports
+// it (its write-set log slots must be cleared); otherwise ticket = ~0.  All
+// 32 lanes of the warp must call it together.
 template <int NR, int NW, int KO = 0, class Compute>
 __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active, uint32_t me, const ShardView& v,
                                                unsigned long long* ticket_ctr, unsigned long long& ticket,
@@ -188,7 +190,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     // the converged surviving lanes aggregate: a lane may still be waiting on
     // a lower-priority holder of this very warp, so no full-warp collective
     // may separate lock acquisition from release.
-    unsigned long long t = 0;
+    unsigned long long t = ~0ull;  // no ticket
     if constexpr ((KO & KO_STRIPED_TICKET) != 0) {
         if (ok) t = take_ticket(reinterpret_cast<unsigned long long*>(&v.cells[((uint64_t)blockIdx.x * 7919u) % v.size_words].spare));
     } else {
@@ -228,7 +230,10 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 3, tclk);
-    if (!ok) return false;
+    if (!ok) {
+        ticket = t;  // a ticket taken by an attempt that then aborted (0 = none taken)
+        return false;
+    }
     // ---- P5: write back + release in one 128-bit store per distinct written word
     compute(tx);
     const uint32_t nv = (uint32_t)(t + 1);

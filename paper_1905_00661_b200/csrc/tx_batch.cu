@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
     uint64_t amount = 0;
     StaticTx<4, 2> tx;
     unsigned long long clocks[6] = {0, 0, 0, 0, 0, 0};
+    const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
     while (__any_sync(0xffffffffu, i < n)) {
         if (i < n && !loaded) {
             const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             }
         }
         const bool active = i < n && loaded;
-        unsigned long long t = 0;
+        unsigned long long t = ~0ull;
         const bool committed =
             phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, [&](StaticTx<4, 2>& x) {
                 x.wval[0] = x.val[0] - amount;
@@ -74,8 +75,14 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             }, clocks);
         if (committed) {
             tickets[i] = t;
+            wlog_put(v, wbase, t, 0, tx.loc[0]);
+            wlog_put(v, wbase, t, 1, tx.loc[1]);
             ++commits;
         } else if (active) {
+            if (t != ~0ull) {  // aborted after taking a ticket: its log slots stay empty
+                wlog_put(v, wbase, t, 0, ~0u);
+                wlog_put(v, wbase, t, 1, ~0u);
+            }
             ++aborts;
             if (++attempts < max_attempts) continue;
             tickets[i] = ~0ull;
@@ -108,6 +115,7 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const
                                                               DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
+    const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const hetm_rw_tx r = in[i];
@@ -137,12 +145,18 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const
                 const uint64_t loc = r.w_addr[j] - v.base;
                 ok = tm_read(tx, v, loc, cur) && tm_write(tx, v, loc, cur + r.add[j] + sum);
             }
-            unsigned long long t;
+            unsigned long long t = ~0ull;
             if (ok && tm_commit(tx, v, &ctr->ticket, t)) {
                 tickets[i] = t;
                 tm_mark_bitmaps(tx, v);
+                wlog_put(v, wbase, t, 0, tx.nw > 0 ? (uint32_t)tx.w_local[0] : ~0u);
+                wlog_put(v, wbase, t, 1, tx.nw > 1 ? (uint32_t)tx.w_local[1] : ~0u);
                 ++commits;
                 break;
+            }
+            if (t != ~0ull) {  // aborted after taking a ticket: its log slots stay empty
+                wlog_put(v, wbase, t, 0, ~0u);
+                wlog_put(v, wbase, t, 1, ~0u);
             }
             ++aborts;
             if (attempt >= max_attempts) {

@@ -494,6 +494,78 @@ def test_rounds_match_sequential_replay(hetm, orc, dev_factory, optimized):
     assert any(outcomes) and not all(outcomes)
 
 
+@pytest.mark.parametrize("batches", [1, 3])
+def test_merge_delta_rounds_match_replay(hetm, orc, dev_factory, batches):
+    """mergeCommit in delta form (HETM_CFG_MERGE_DELTA): sparse device write
+    sets ship as 16-B {word, value} records; the host replica must end exactly
+    as with the SPEC chunk copy (replica equality after every round,
+    SPEC.md:640), across several batches per round and aborted rounds."""
+    W, gran = 1 << 20, 1024
+    d = dev_factory(W, rs_gran_bytes=gran, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_BANK)
+    host = np.full(W, 7, np.uint64)
+    d.upload(hetm.REPLICA_DEV, 0, host)
+    d.merge_commit(host)
+    d.merge_wait()
+    d.clear_round()
+    ref = host.copy()
+    ts0, outcomes = 0, []
+    for rnd in range(6):
+        overlap = rnd == 3
+        tks, all_txs, n_tickets = [], [], 0
+        for b in range(batches):
+            txs = orc.gen_bank_batch(100 * rnd + b + 1, 3000, 0, W // 2)
+            r = d.execute_batch(hetm.KERNEL_BANK, txs)
+            tks.append(r.tickets)
+            n_tickets += r.ticket_end - r.ticket_first  # includes tickets of aborted attempts
+            all_txs.append(txs)
+        txs = np.concatenate(all_txs)
+        tickets = np.concatenate(tks)
+        log = orc.gen_host_log(70 + rnd, 800, 2, 4, 0 if overlap else W // 2, W // 2, ts_base=ts0)
+        ts0 += 800
+        orc.apply_log_ts_order(host, log)
+        keep = [d.stream_chunk(c, src_thread=i) for i, c in enumerate(np.array_split(log, 4))]
+        conflict = d.round_verdict()
+        orc.apply_log_ts_order(ref, log)
+        d.clear_transfer_log()
+        if conflict:
+            d.merge_abort_device(host, optimized=True)
+        else:
+            orc.bank_replay(ref, txs, orc.order_by_ticket(tickets), gran, 16384)
+            st = d.merge_commit(host)
+            d.merge_wait()
+            n_slots = 2 * n_tickets
+            assert st.bytes_d2h == 16 * n_slots
+            assert (hetm.D2H, hetm.TAG_MERGE_DELTA, 16 * n_slots) in d.transfer_log()
+        d.clear_round()
+        outcomes.append(conflict)
+        assert (host == ref).all(), rnd
+        assert (d.download(hetm.REPLICA_DEV) == host).all(), rnd
+        assert (d.download(hetm.REPLICA_DEV_SHADOW) == host).all(), rnd
+        del keep
+    assert any(outcomes) and not all(outcomes)
+
+
+def test_merge_delta_falls_back_to_chunks_when_dense(hetm, orc, dev_factory):
+    """Dense write sets (more record bytes than dirty-chunk bytes) use the
+    SPEC chunk copy even with HETM_CFG_MERGE_DELTA."""
+    W = 1 << 14
+    d = dev_factory(W, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_BANK)
+    host = np.zeros(W, np.uint64)
+    txs = orc.gen_bank_batch(3, 6000, 0, W // 2)
+    r = d.execute_batch(hetm.KERNEL_BANK, txs)
+    assert not d.round_verdict()
+    d.clear_transfer_log()
+    st = d.merge_commit(host)
+    d.merge_wait()
+    assert st.bytes_d2h == st.dirty_chunks * 16384
+    assert all(t[1] == hetm.TAG_MERGE for t in d.transfer_log() if t[0] == hetm.D2H)
+    ref = np.zeros(W, np.uint64)
+    orc.bank_replay(ref, txs, orc.order_by_ticket(r.tickets), 1024, 16384)
+    assert (host == ref).all()
+
+
 # ------------------------------------------------------------ shard router
 def test_route_log_partitions_stably(hetm, dev_factory):
     torch = pytest.importorskip("torch")
