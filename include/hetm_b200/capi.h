@@ -128,7 +128,7 @@ typedef struct hetm_dev_config {
     uint64_t rs_gran_bytes; /* RS/WS granularity: pow2 multiple of 8 (default 1024)  */
     uint64_t chunk_bytes;   /* ChunkMap granularity: pow2 multiple of 8 (16384)      */
     uint64_t log_capacity;  /* initial round-log arena (entries); 0 = auto; grows    */
-    uint32_t max_attempts;  /* livelock budget per transaction; 0 = default (1<<20)  */
+    uint32_t max_attempts;  /* livelock budget per transaction; 0 = default (1<<24)  */
     int32_t device;         /* CUDA device ordinal                                   */
     uint32_t flags;         /* HETM_CFG_*                                            */
     uint32_t reserved;
@@ -298,7 +298,7 @@ int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
  * duration and count, and resets the accumulator. */
 int hetm_dev_set_timing(hetm_dev* dev, int on);
 int hetm_dev_timing(hetm_dev* dev, int which, double* total_ms, uint64_t* count);
-/* Diagnostic counter words (phase clocks of instrumented builds); n <= 5. */
+/* Diagnostic counter words (phase clocks of instrumented builds); n <= 21. */
 int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
@@ -320,6 +320,13 @@ int hetm_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, h
  * thread order like WriteLog::allEntries (write_log.hpp:74-82). */
 int hetm_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads,
                       uint64_t lo, uint64_t span, uint64_t ts_base, hetm_log_entry* out);
+/* Zipf-skewed variants (BASELINE configs[2]): every account /
+ * word is drawn as lo + rank - 1 with rank ~ Zipf(alpha) over [1, span] (rank 1
+ * hottest; rejection-inversion sampler over DetRng uniform(), det_rng.hpp:36).
+ * alpha == 0 is the uniform generator above. */
+int hetm_gen_bank_batch_zipf(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, double alpha, hetm_bank_tx* out);
+int hetm_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads, uint64_t lo,
+                           uint64_t span, uint64_t ts_base, double alpha, hetm_log_entry* out);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,9 @@ for name, res, args in [
     ("orc_apply_log_ts_order", None, [_v, _u, _v, _u]),
     ("orc_gen_bank_batch", None, [_u, _u, _u, _u, _v]),
     ("orc_gen_host_log", None, [_u, _u, C.c_uint32, C.c_uint32, _u, _u, _u, _v]),
+    ("orc_gen_bank_batch_zipf", None, [_u, _u, _u, _u, C.c_double, _v]),
+    ("orc_gen_host_log_zipf", None, [_u, _u, C.c_uint32, C.c_uint32, _u, _u, _u, C.c_double, _v]),
+    ("orc_zipf_fill", None, [_u, _u, _u, C.c_double, _v]),
     ("orc_mt_bank_batch", _u, [_v, _u, _u, _v, _u, C.c_int, _u, _v, _v, _v, _v, _u, _u]),
     ("orc_mt_validate_apply", C.c_int, [_v, _u, _v, _u, _u, _v, _v, C.c_int, C.c_int]),
 ]:
@@ -82,12 +85,18 @@ def rng_uniform(seed, n):
     o = np.empty(n, np.float64); lib.orc_rng_fill_uniform(seed, n, P(o)); return o
 
 
-def gen_bank_batch(seed, n, lo, span):
-    o = np.empty(n, BANK_TX); lib.orc_gen_bank_batch(seed, n, lo, span, P(o)); return o
+def gen_bank_batch(seed, n, lo, span, zipf=0.0):
+    o = np.empty(n, BANK_TX); lib.orc_gen_bank_batch_zipf(seed, n, lo, span, zipf, P(o)); return o
 
 
-def gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base=0):
-    o = np.empty(n_tx * wpt, ENTRY); lib.orc_gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base, P(o)); return o
+def gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base=0, zipf=0.0):
+    o = np.empty(n_tx * wpt, ENTRY)
+    lib.orc_gen_host_log_zipf(seed, n_tx, wpt, threads, lo, span, ts_base, zipf, P(o))
+    return o
+
+
+def zipf_ranks(seed, n, span, alpha):
+    o = np.empty(n, np.uint64); lib.orc_zipf_fill(seed, n, span, alpha, P(o)); return o
 
 
 def validate_chunk(entries, rs_words, gran, ts, dev, apply=True, base=0):

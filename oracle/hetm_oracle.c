@@ -10,6 +10,7 @@
 #define _GNU_SOURCE
 #include "hetm_oracle.h"
 
+#include <math.h>
 #include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
@@ -200,28 +201,80 @@ void orc_apply_log_ts_order(uint64_t* region, uint64_t base, const orc_entry* e,
 }
 
 /* ---------------------------------------------------------- generators -- */
-static uint64_t draw_distinct(orc_rng* r, uint64_t span, const uint64_t* prev, int nprev) {
+/* Zipf(alpha) ranks 1..n by rejection-inversion (W. Hormann, G. Derflinger,
+ * "Rejection-inversion to generate variates from monotone discrete
+ * distributions", ACM TOMACS 6(3), 1996), one DetRng uniform() per trial
+ * (det_rng.hpp:36).  The reference pins only the sampler's law (SPEC.md:620:
+ * top-10 rank frequencies within 5% of the analytic law at alpha 0.5). */
+typedef struct { double s, n, hx1, hxn, sdiv; } orc_zipf;
+static double zf_h1(double x) { return fabs(x) > 1e-8 ? log1p(x) / x : 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x)); }
+static double zf_h2(double x) { return fabs(x) > 1e-8 ? expm1(x) / x : 1.0 + x * 0.5 * (1.0 + x * (1.0 / 3.0) * (1.0 + 0.25 * x)); }
+static double zf_hint(const orc_zipf* z, double x) { const double lx = log(x); return zf_h2((1.0 - z->s) * lx) * lx; }
+static double zf_h(const orc_zipf* z, double x) { return exp(-z->s * log(x)); }
+static double zf_hinv(const orc_zipf* z, double x) {
+    double t = x * (1.0 - z->s);
+    if (t < -1.0) t = -1.0;
+    return exp(zf_h1(t) * x);
+}
+static void zf_init(orc_zipf* z, double alpha, uint64_t n) {
+    z->s = alpha;
+    z->n = (double)n;
+    z->hx1 = zf_hint(z, 1.5) - 1.0;
+    z->hxn = zf_hint(z, z->n + 0.5);
+    z->sdiv = 2.0 - zf_hinv(z, zf_hint(z, 2.5) - zf_h(z, 2.0));
+}
+static uint64_t zf_sample(const orc_zipf* z, orc_rng* r) {
     for (;;) {
-        uint64_t a = orc_rng_below(r, span);
+        const double u = z->hxn + orc_rng_uniform(r) * (z->hx1 - z->hxn);
+        const double x = zf_hinv(z, u);
+        double kd = floor(x + 0.5);
+        if (kd < 1.0) kd = 1.0;
+        else if (kd > z->n) kd = z->n;
+        if (kd - x <= z->sdiv || u >= zf_hint(z, kd + 0.5) - zf_h(z, kd)) return (uint64_t)kd;
+    }
+}
+
+void orc_zipf_fill(uint64_t seed, uint64_t n, uint64_t span, double alpha, uint64_t* out) {
+    orc_rng r; orc_rng_init(&r, seed);
+    orc_zipf z; zf_init(&z, alpha, span);
+    for (uint64_t i = 0; i < n; ++i) out[i] = zf_sample(&z, &r);
+}
+
+/* offset in [0, span): uniform below(span) (alpha == 0) or zipf rank - 1 */
+static uint64_t draw_offset(orc_rng* r, uint64_t span, const orc_zipf* z) {
+    return z ? zf_sample(z, r) - 1 : orc_rng_below(r, span);
+}
+
+static uint64_t draw_distinct(orc_rng* r, uint64_t span, const orc_zipf* z, const uint64_t* prev, int nprev) {
+    for (;;) {
+        uint64_t a = draw_offset(r, span, z);
         int dup = 0;
         for (int k = 0; k < nprev; ++k) dup |= (prev[k] == a);
         if (!dup) return a;
     }
 }
 
-void orc_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, orc_bank_tx* out) {
+void orc_gen_bank_batch_zipf(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, double alpha, orc_bank_tx* out) {
     orc_rng r; orc_rng_init(&r, seed);
+    orc_zipf z; zf_init(&z, alpha > 0 ? alpha : 1.0, span);
+    const orc_zipf* zp = alpha > 0 ? &z : NULL;
     for (uint64_t i = 0; i < n; ++i) {
         uint64_t a[4];
-        for (int k = 0; k < 4; ++k) a[k] = draw_distinct(&r, span, a, k);
+        for (int k = 0; k < 4; ++k) a[k] = draw_distinct(&r, span, zp, a, k);
         for (int k = 0; k < 4; ++k) out[i].acct[k] = (uint32_t)(lo + a[k]);
         out[i].amount = orc_rng_below(&r, 100) + 1;
     }
 }
 
-void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo,
-                      uint64_t span, uint64_t ts_base, orc_entry* out) {
+void orc_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, orc_bank_tx* out) {
+    orc_gen_bank_batch_zipf(seed, n, lo, span, 0.0, out);
+}
+
+void orc_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo, uint64_t span,
+                           uint64_t ts_base, double alpha, orc_entry* out) {
     orc_rng r; orc_rng_init(&r, seed);
+    orc_zipf z; zf_init(&z, alpha > 0 ? alpha : 1.0, span);
+    const orc_zipf* zp = alpha > 0 ? &z : NULL;
     /* thread t receives txs t, t+T, ...; its log starts after threads < t */
     uint64_t* off = (uint64_t*)calloc(T + 1, sizeof(uint64_t));
     for (uint32_t t = 0; t < T; ++t) {
@@ -233,7 +286,7 @@ void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, ui
         uint32_t t = (uint32_t)(i % T);
         uint64_t pos = off[t] + (i / T) * wpt;
         for (uint32_t k = 0; k < wpt; ++k) {
-            uint64_t a = draw_distinct(&r, span, prev, (int)(k < 16 ? k : 16));
+            uint64_t a = draw_distinct(&r, span, zp, prev, (int)(k < 16 ? k : 16));
             if (k < 16) prev[k] = a;
             out[pos + k].addr = lo + a;
             out[pos + k].value = orc_rng_next(&r);
@@ -241,6 +294,11 @@ void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, ui
         }
     }
     free(off);
+}
+
+void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo,
+                      uint64_t span, uint64_t ts_base, orc_entry* out) {
+    orc_gen_host_log_zipf(seed, n_tx, wpt, T, lo, span, ts_base, 0.0, out);
 }
 
 /* ------------------------------------------------------- CPU baselines -- */

@@ -85,6 +85,11 @@ void orc_apply_log_ts_order(uint64_t* region, uint64_t base, const orc_entry* e,
 
 /* ---- seeded inputs (generators must match libhetm_b200's) ---- */
 void orc_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, orc_bank_tx* out);
+/* alpha > 0: accounts / words drawn as lo + zipf(alpha) rank - 1 (rank 1 hottest) */
+void orc_gen_bank_batch_zipf(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, double alpha, orc_bank_tx* out);
+void orc_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo, uint64_t span,
+                           uint64_t ts_base, double alpha, orc_entry* out);
+void orc_zipf_fill(uint64_t seed, uint64_t n, uint64_t span, double alpha, uint64_t* out);
 void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads,
                       uint64_t lo, uint64_t span, uint64_t ts_base, orc_entry* out);
 

@@ -133,6 +133,9 @@ _sigs = {
     "hetm_host_register": (C.c_int, [_vp, C.c_uint64]),
     "hetm_host_unregister": (C.c_int, [_vp]),
     "hetm_gen_bank_batch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _vp]),
+    "hetm_gen_bank_batch_zipf": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, _vp]),
+    "hetm_gen_host_log_zipf": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                         C.c_uint64, C.c_double, _vp]),
     "hetm_gen_host_log": (
         C.c_int,
         [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, _vp],

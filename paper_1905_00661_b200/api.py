@@ -109,18 +109,22 @@ class PinnedArray:
             pass
 
 
-def gen_bank_batch(seed: int, n: int, lo: int, span: int, out: np.ndarray | None = None) -> np.ndarray:
-    """Seeded bank transfers (4 distinct accounts in [lo, lo+span), amount in [1,100])."""
+def gen_bank_batch(seed: int, n: int, lo: int, span: int, out: np.ndarray | None = None,
+                   zipf: float = 0.0) -> np.ndarray:
+    """Seeded bank transfers (4 distinct accounts in [lo, lo+span), amount in [1,100]);
+    zipf > 0 draws accounts as lo + Zipf(zipf) rank - 1."""
     out = np.empty(n, BANK_TX) if out is None else out
-    check(lib.hetm_gen_bank_batch(seed, n, lo, span, _ptr(out)))
+    check(lib.hetm_gen_bank_batch_zipf(seed, n, lo, span, float(zipf), _ptr(out)))
     return out
 
 
 def gen_host_log(seed: int, n_tx: int, writes_per_tx: int, n_threads: int, lo: int, span: int,
-                 ts_base: int = 0, out: np.ndarray | None = None) -> np.ndarray:
-    """Seeded host write log in WriteLog::allEntries order (thread-major)."""
+                 ts_base: int = 0, out: np.ndarray | None = None, zipf: float = 0.0) -> np.ndarray:
+    """Seeded host write log in WriteLog::allEntries order (thread-major); zipf > 0
+    draws the written words as lo + Zipf(zipf) rank - 1."""
     out = np.empty(n_tx * writes_per_tx, LOG_ENTRY) if out is None else out
-    check(lib.hetm_gen_host_log(seed, n_tx, writes_per_tx, n_threads, lo, span, ts_base, _ptr(out)))
+    check(lib.hetm_gen_host_log_zipf(seed, n_tx, writes_per_tx, n_threads, lo, span, ts_base, float(zipf),
+                                     _ptr(out)))
     return out
 
 

@@ -98,7 +98,7 @@ struct hetm_dev {
     uint64_t W = 0, base = 0;
     uint32_t gran_shift = 0, chunk_shift = 0;
     uint64_t rs_bits = 0, rs_words = 0, chunk_bits = 0, chunk_words = 0;
-    uint32_t max_attempts = 1u << 20;
+    uint32_t max_attempts = 1u << 24;
 
     Cell* d_cells = nullptr;             // devReplica: {value, lock, ts, spare} per word
     uint64_t* d_shadow = nullptr;        // devShadow: plain words
@@ -1263,7 +1263,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 5) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 21) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

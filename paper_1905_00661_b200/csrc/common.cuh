@@ -47,10 +47,10 @@ struct DevCounters {
     unsigned long long restore_done; // restore_kernel: finished blocks
     unsigned long long ts_floor;     // max log ts of all previous rounds (device-maintained)
     unsigned long long wlog_base;    // first commit ticket of the round (write-set log origin)
-    unsigned long long pad[5];       // diagnostics (phase clocks / ticket counts)
+    unsigned long long pad[21];      // diagnostics (phase clocks / ticket counts)
 };
 
-static_assert(sizeof(DevCounters) == 128, "one 128-B line");
+static_assert(sizeof(DevCounters) == 256, "two 128-B lines");
 
 // Kernel-wide view of one device's STMR shard and its metadata.
 struct ShardView {

@@ -44,6 +44,8 @@ struct StaticTx {
     uint64_t val[NW];          // value of write word j seen in P1
     uint64_t wval[NW];         // value to write to loc[j]
     uint32_t first;            // bit k set: loc[k] is the first occurrence of its word
+    uint32_t block_loc;        // abort cause: word held FINAL by another transaction ...
+    unsigned long long block_lk;  // ... with this lock word (0: no such blocker)
 };
 
 template <int NR>
@@ -97,6 +99,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
                                                unsigned long long* ticket_ctr, unsigned long long& ticket,
                                                Compute compute, unsigned long long* clocks = nullptr) {
     bool ok = active;
+    tx.block_lk = 0;
     long long tclk = 0;
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) tclk = clock64();
     if constexpr ((KO & KO_PROTOCOL) != 0) {  // access-pattern floor
@@ -135,7 +138,11 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            ok &= !(tx.l[k] & kLockFinal);
+            if (tx.l[k] & kLockFinal) {
+                ok = false;
+                tx.block_loc = tx.loc[k];
+                tx.block_lk = tx.l[k];
+            }
             // a word loaded twice must show one lock word (values only change
             // together with the version, so equal unlocked lock words imply equal values)
 #pragma unroll
@@ -170,6 +177,10 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             // off, then retry; a higher-priority holder or a new version aborts.
             while (c != tx.l[j]) {
                 if (lk_ver(c) != lk_ver(tx.l[j]) || !(c & kLockFinal) || lk_owner(c) < me) {
+                    if ((c & kLockFinal) && lk_ver(c) == lk_ver(tx.l[j])) {
+                        tx.block_loc = tx.loc[j];
+                        tx.block_lk = c;
+                    }
                     ok = false;
                     break;
                 }
@@ -219,7 +230,11 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             while (ok) {
                 if (lk_ver(c) != lk_ver(tx.l[k])) ok = false;                 // committed since P1
                 else if (!(c & kLockFinal)) break;                            // unclaimed: valid
-                else if (lk_owner(c) < me) ok = false;                        // higher priority holds it
+                else if (lk_owner(c) < me) {                                  // higher priority holds it
+                    ok = false;
+                    tx.block_loc = tx.loc[k];
+                    tx.block_lk = c;
+                }
                 else c = ld_relaxed(&v.cells[tx.loc[k]].lock);                // lower priority: wait
             }
         }

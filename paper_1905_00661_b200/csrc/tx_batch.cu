@@ -32,6 +32,12 @@ __device__ __forceinline__ void flush_batch_counters(unsigned long long commits,
 // Bank transfer: read 4 accounts, acct0 -= amount, acct1 += amount.
 // Warp-phased commit (phased_tx.cuh); each lane keeps its transaction across
 // retries and moves to the next one (grid stride) once it commits.
+//
+// Contention management (zipf hot spots, BASELINE configs[2]): an attempt
+// aborted by a FINAL holder re-reads only that word until its lock changes
+// (the holder released it) instead of re-running the whole commit and
+// flooding the hot word's L2 slice; other aborts back off after 8 attempts.
+
 template <int KO, int MINB = 4>
 __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView v, const hetm_bank_tx* __restrict__ in,
                                                                    uint64_t n, unsigned long long* __restrict__ tickets,
@@ -84,6 +90,15 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                 wlog_put(v, wbase, t, 1, ~0u);
             }
             ++aborts;
+            if (tx.block_lk) {  // wait for the FINAL holder to release, then retry
+                uint32_t ns = 32;
+                for (int p = 0; p < 256 && ld_relaxed(&v.cells[tx.block_loc].lock) == tx.block_lk; ++p) {
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? 2 * ns : ns;
+                }
+            } else if (attempts >= 8) {
+                __nanosleep(attempts < 64 ? 16u * attempts : 1024u);
+            }
             if (++attempts < max_attempts) continue;
             tickets[i] = ~0ull;
             ++livelocks;
@@ -159,6 +174,7 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const
                 wlog_put(v, wbase, t, 1, ~0u);
             }
             ++aborts;
+            if (attempt >= 4) __nanosleep(attempt < 64 ? 32u * attempt : 2048u);
             if (attempt >= max_attempts) {
                 tickets[i] = ~0ull;
                 ++livelocks;
@@ -186,25 +202,6 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
     const unsigned grid = grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count);
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
-    static const int minb = [] {
-        const char* e = std::getenv("HETM_TX_MINBLOCKS");  // occupancy experiments only
-        return e ? std::atoi(e) : 0;
-    }();
-    if (minb >= 1 && minb <= 3) {  // fewer resident blocks per SM (queueing experiments)
-        const unsigned g2 = grid_for(n, kTxThreads, minb, g.sm_count);
-        if (ko == 4) bank_batch_kernel<4><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        else if (ko == 8) bank_batch_kernel<8><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        else if (ko == 64) bank_batch_kernel<64><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        else bank_batch_kernel<0><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        return cudaGetLastError();
-    }
-    if (minb == 5 || minb == 6 || minb == 8) {
-        const unsigned g2 = grid_for(n, kTxThreads, minb, g.sm_count);
-        if (minb == 5) bank_batch_kernel<0, 5><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        if (minb == 6) bank_batch_kernel<0, 6><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        if (minb == 8) bank_batch_kernel<0, 8><<<g2, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
-        return cudaGetLastError();
-    }
     switch (ko) {
         HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(32) HETM_KO_CASE(64) HETM_KO_CASE(128)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);

@@ -84,6 +84,16 @@ def test_host_log_generator_matches_oracle(hetm, orc, args):
     assert a.tobytes() == b.tobytes()
 
 
+@pytest.mark.parametrize("alpha", [0.5, 0.99, 1.0, 1.5])
+def test_zipf_generators_match_oracle(hetm, orc, alpha):
+    a = hetm.gen_bank_batch(11, 4000, 1 << 20, 1 << 20, zipf=alpha)
+    b = orc.gen_bank_batch(11, 4000, 1 << 20, 1 << 20, zipf=alpha)
+    assert a.tobytes() == b.tobytes()
+    a = hetm.gen_host_log(12, 3000, 2, 8, 64, 1 << 16, ts_base=5, zipf=alpha)
+    b = orc.gen_host_log(12, 3000, 2, 8, 64, 1 << 16, ts_base=5, zipf=alpha)
+    assert a.tobytes() == b.tobytes()
+
+
 def test_wire_formats(hetm):
     assert hetm.LOG_ENTRY.itemsize == 24  # write_log.hpp:25
     assert hetm.BANK_TX.itemsize == 24

@@ -566,6 +566,80 @@ def test_merge_delta_falls_back_to_chunks_when_dense(hetm, orc, dev_factory):
     assert (host == ref).all()
 
 
+# ------------------------------------------- cfg3: zipf hot spot (abort path)
+@pytest.mark.parametrize("W,n,alpha", [(1 << 16, 1 << 14, 0.99), (1 << 20, 1 << 16, 0.99), (1 << 20, 1 << 15, 1.5)])
+def test_cfg3_zipf_batch_replays(hetm, orc, dev_factory, W, n, alpha):
+    """BASELINE configs[2] shape: zipf-skewed bank accounts (hot words contended
+    by thousands of transactions of one batch): every transaction commits and
+    the ticket-order replay reproduces the STMR and the bitmaps bit-exactly."""
+    d = dev_factory(W, rs_gran_bytes=1024)
+    d.register_kernel(hetm.KERNEL_BANK)
+    init = np.full(W, 1000, np.uint64)
+    d.upload(hetm.REPLICA_DEV, 0, init)
+    txs = orc.gen_bank_batch(31, n, 0, W, zipf=alpha)
+    r = d.execute_batch(hetm.KERNEL_BANK, txs)
+    assert r.committed == n
+    ref = check_replay(hetm, orc, d, txs, r.tickets, init, 1024, 16384)
+    assert int(ref.sum(dtype=np.uint64)) == (1000 * W) % (1 << 64)
+
+
+@pytest.mark.parametrize("optimized", [False, True])
+def test_cfg3_zipf_rounds_roll_back(hetm, orc, dev_factory, optimized):
+    """CPU and GPU draw from the same zipf hot set: the host log hits words the
+    device read, every round is DeviceAborted and rolled back (SPEC.md:372-380);
+    the device replica must equal the host-only replay after every round."""
+    W, gran = 1 << 20, 1024
+    d = dev_factory(W, rs_gran_bytes=gran, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_BANK)
+    host = np.full(W, 500, np.uint64)
+    d.upload(hetm.REPLICA_DEV, 0, host)
+    d.merge_commit(host)
+    d.merge_wait()
+    d.clear_round()
+    ts0 = 0
+    for rnd in range(4):
+        txs = orc.gen_bank_batch(200 + rnd, 1 << 14, 0, W, zipf=0.99)
+        r = d.execute_batch(hetm.KERNEL_BANK, txs)
+        assert r.committed == txs.size
+        log = orc.gen_host_log(300 + rnd, 4000, 2, 8, 0, W, ts_base=ts0, zipf=0.99)
+        ts0 += 4000
+        orc.apply_log_ts_order(host, log)
+        keep = [d.stream_chunk(c, src_thread=i) for i, c in enumerate(np.array_split(log, 8))]
+        assert d.round_verdict(), "zipf host log must hit the device read set"
+        d.merge_abort_device(host, optimized=optimized)
+        d.clear_round()
+        assert (d.download(hetm.REPLICA_DEV) == host).all(), rnd
+        del keep
+
+
+@pytest.mark.slow
+def test_cfg3_zipf_full_size(hetm, orc, dev_factory):
+    """BASELINE configs[2] at size: 1 GiB STMR, 2^20 zipf(0.99) bank transactions,
+    a 2^20-entry zipf host log on the same range -> conflict -> optimized
+    rollback; replay parity, bank sum, and replica equality after the abort."""
+    W, n = 1 << 27, 1 << 20
+    d = dev_factory(W, rs_gran_bytes=1024)
+    d.register_kernel(hetm.KERNEL_BANK)
+    init = np.full(W, 1000, np.uint64)
+    d.upload(hetm.REPLICA_DEV, 0, init)
+    d.merge_commit(init)
+    d.merge_wait()
+    d.clear_round()
+    txs = orc.gen_bank_batch(2025, n, 0, W, zipf=0.99)
+    r = d.execute_batch(hetm.KERNEL_BANK, txs)
+    assert r.committed == n
+    ref = check_replay(hetm, orc, d, txs, r.tickets, init, 1024, 16384)
+    assert int(ref.sum(dtype=np.uint64)) == (1000 * W) % (1 << 64)
+    log = orc.gen_host_log(77, n // 2, 2, 8, 0, W, ts_base=0, zipf=0.99)
+    host = init.copy()
+    orc.apply_log_ts_order(host, log)
+    keep = [d.stream_chunk(c, src_thread=i) for i, c in enumerate(np.array_split(log, 8))]
+    assert d.round_verdict()
+    d.merge_abort_device(host, optimized=True)
+    assert (d.download(hetm.REPLICA_DEV) == host).all()
+    del keep
+
+
 # ------------------------------------------------------------ shard router
 def test_route_log_partitions_stably(hetm, dev_factory):
     torch = pytest.importorskip("torch")

@@ -95,6 +95,37 @@ def test_bank_generator_distinct_accounts():
     assert (txs["amount"] >= 1).all() and (txs["amount"] <= 100).all()
 
 
+def test_zipf_sampler_law():
+    """10^6 samples at alpha 0.5 -- top-10 rank frequencies within
+    5% of the analytic law k^-a / H(N, a) (N = 1000 keeps the top ranks' counts
+    large enough that 5% is well above sampling noise)."""
+    N, n, a = 1000, 10**6, 0.5
+    ranks = O.zipf_ranks(3, n, N, a)
+    assert ranks.min() >= 1 and ranks.max() <= N
+    H = float(np.sum(np.arange(1, N + 1, dtype=np.float64) ** -a))
+    counts = np.bincount(ranks[ranks <= 10].astype(np.int64), minlength=11)[1:]
+    expect = n * np.arange(1, 11, dtype=np.float64) ** -a / H
+    assert (np.abs(counts - expect) / expect < 0.05).all(), (counts, expect)
+
+
+@pytest.mark.parametrize("alpha", [0.99, 1.2])
+def test_zipf_sampler_law_skewed(alpha):
+    N, n = 1 << 20, 10**6
+    ranks = O.zipf_ranks(9, n, N, alpha)
+    H = float(np.sum(np.arange(1, N + 1, dtype=np.float64) ** -alpha))
+    counts = np.bincount(ranks[ranks <= 10].astype(np.int64), minlength=11)[1:]
+    expect = n * np.arange(1, 11, dtype=np.float64) ** -alpha / H
+    assert (np.abs(counts - expect) / expect < 0.05).all(), (counts, expect)
+
+
+def test_zipf_bank_batch_distinct_and_hot():
+    txs = O.gen_bank_batch(5, 20000, 100, 1 << 20, zipf=0.99)
+    acct = txs["acct"].astype(np.int64)
+    assert (np.sort(acct, axis=1)[:, 1:] != np.sort(acct, axis=1)[:, :-1]).all()  # distinct per tx
+    assert acct.min() >= 100 and acct.max() < 100 + (1 << 20)
+    assert (acct == 100).any(axis=1).mean() > 0.1  # rank 1 is hot
+
+
 # --------------------------------------------------- SPEC.md examples (KATs)
 def _rs(nbits, bits):
     w = np.zeros(O.words_for_bits(nbits), np.uint64)

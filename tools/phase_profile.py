@@ -12,8 +12,8 @@ for rep in range(3):
     txs = hetm.gen_bank_batch(10 + rep, B, 0, W // 2)
     r = d.execute_batch(hetm.KERNEL_BANK, txs, want_tickets=False)
     d.clear_round()
-out = np.zeros(5, np.uint64)
-hetm.check(hetm._lib.lib.hetm_dev_debug_words(d.h, out.ctypes.data, 5))
+out = np.zeros(6, np.uint64)
+hetm.check(hetm._lib.lib.hetm_dev_debug_words(d.h, out.ctypes.data, 6))
 att = int(out[5])
 print(f"kernel {r.kernel_ms:.3f} ms, aborts {r.aborts}, thread attempts {att}")
 for i, name in enumerate(["P1 snapshot", "P2 prelock", "P3 ticket", "P4 validate+final", "P5 writeback"]):

@@ -29,8 +29,8 @@ def bank():
         if rep:
             ms.append(r.kernel_ms)
             ab.append(r.aborts)
-    out = np.zeros(5, np.uint64)
-    hetm.check(hetm._lib.lib.hetm_dev_debug_words(d.h, out.ctypes.data, 5))
+    out = np.zeros(6, np.uint64)
+    hetm.check(hetm._lib.lib.hetm_dev_debug_words(d.h, out.ctypes.data, 6))
     ko = os.environ.get("HETM_KNOCKOUT", "0")
     print(f"bank KO={ko} kernel_ms median {statistics.median(ms):.4f} min {min(ms):.4f} "
           f"aborts {statistics.median(ab):.0f} tx/s {B / statistics.median(ms) / 1e6:.2f} G "
