@@ -75,7 +75,8 @@ enum hetm_validate_mode { HETM_APPLY = 0, HETM_VALIDATE_ONLY = 1 };
 /* Built-in transactional kernels (kernels are registered by id). */
 enum hetm_kernel_id {
     HETM_KERNEL_BANK = 1, /* hetm_bank_tx: read 4 accounts, move amount acct0 -> acct1 */
-    HETM_KERNEL_RW = 2    /* hetm_rw_tx: generic <=4 reads / <=2 read-modify-writes   */
+    HETM_KERNEL_RW = 2,   /* hetm_rw_tx: generic <=4 reads / <=2 read-modify-writes   */
+    HETM_KERNEL_CACHE = 3 /* hetm_cache_tx: MemcachedGPU-style GET/SET (below)         */
 };
 
 /* hetm_dev_clear_round flags. */
@@ -121,6 +122,41 @@ typedef struct hetm_rw_tx {
     uint64_t w_addr[2];
     uint64_t add[2];
 } hetm_rw_tx;
+
+/* MemcachedGPU-style set-associative cache in the STMR (BASELINE configs[3];
+ * PAPER.md:480-508).  A set holds HETM_CACHE_WAYS ways of
+ * HETM_CACHE_WAY_WORDS words {key0, key1, value0..3, lru, flags}; set s
+ * occupies words [base + 64 s, base + 64 s + 64).  Keys route by their last
+ * bit: part p = key[0] & 1 owns sets [p n/2, (p+1) n/2), and
+ * set = p n/2 + (hetm_cache_hash(key) mod n/2), so the CPU (part 0) and GPU
+ * (part 1) halves of the cache never share a set or a 1 KiB RS granule.
+ *   GET: hit -> value, the way's lru := ticket+1 (LRU touch); miss -> nothing.
+ *   SET: hit -> value and lru rewritten; miss -> the first invalid way, else
+ *        the least-recently-used way (lowest index on ties) takes key, value,
+ *        lru := ticket+1, flags := 1.
+ * Every written word is read first (no blind writes). */
+#define HETM_CACHE_WAYS 8
+#define HETM_CACHE_WAY_WORDS 8
+#define HETM_CACHE_SET_WORDS 64
+enum hetm_cache_op { HETM_CACHE_GET = 0, HETM_CACHE_SET = 1 };
+typedef struct hetm_cache_tx {
+    uint32_t op; /* hetm_cache_op */
+    uint32_t reserved;
+    uint64_t key[2];
+    uint64_t value[4]; /* SET only */
+} hetm_cache_tx;
+enum hetm_cache_status {
+    HETM_CACHE_MISS = 0,     /* GET: key absent */
+    HETM_CACHE_HIT = 1,      /* GET: value returned */
+    HETM_CACHE_UPDATED = 2,  /* SET: key present, value replaced */
+    HETM_CACHE_INSERTED = 3, /* SET: stored in an invalid way */
+    HETM_CACHE_EVICTED = 4   /* SET: stored over the LRU way */
+};
+typedef struct hetm_cache_result {
+    uint64_t value[4]; /* GET hit: the value; SET: the value stored */
+    uint32_t status;   /* hetm_cache_status */
+    uint32_t way;      /* way used (HETM_CACHE_WAYS on a miss) */
+} hetm_cache_result;
 
 typedef struct hetm_dev_config {
     uint64_t size_words;    /* STMR words held by this device (its shard)           */
@@ -208,6 +244,18 @@ int hetm_dev_register_kernel(hetm_dev* dev, int kernel_id);
  * UINT64_MAX marks a transaction that exhausted the livelock budget. */
 int hetm_dev_execute_batch(hetm_dev* dev, int kernel_id, const void* inputs, uint64_t rec_bytes,
                            uint64_t n_tx, uint64_t* tickets_out, hetm_batch_stats* stats);
+/* executeBatch with per-transaction results (HETM_KERNEL_CACHE: one
+ * hetm_cache_result per transaction; res_bytes must equal its size). */
+int hetm_dev_execute_batch_ex(hetm_dev* dev, int kernel_id, const void* inputs, uint64_t rec_bytes,
+                              uint64_t n_tx, uint64_t* tickets_out, void* results_out, uint64_t res_bytes,
+                              hetm_batch_stats* stats);
+/* Cache region of HETM_KERNEL_CACHE: n_sets (power of two >= 2) sets from
+ * GLOBAL word base_word.  Default: the largest power-of-two set count that
+ * fits the shard, from its first word. */
+int hetm_dev_set_cache_geometry(hetm_dev* dev, uint64_t base_word, uint64_t n_sets);
+/* The key hash and set routing used by the device (for host-side tooling). */
+uint64_t hetm_cache_hash(uint64_t key0, uint64_t key1);
+uint64_t hetm_cache_set_of(uint64_t key0, uint64_t key1, uint64_t n_sets);
 /* bitmapStats. */
 int hetm_dev_bitmap_stats(hetm_dev* dev, uint64_t* rs_bits, uint64_t* ws_bits, uint64_t* chunks);
 int hetm_dev_bitmap_words(hetm_dev* dev, int which, uint64_t* n_words);
@@ -279,6 +327,9 @@ int hetm_dev_clear_transfer_log(hetm_dev* dev);
  * benchmark (inputs resident in HBM) and by the multi-GPU shard router. */
 int hetm_dev_execute_batch_dptr(hetm_dev* dev, int kernel_id, const void* d_inputs, uint64_t n_tx,
                                 uint64_t* d_tickets, void* stream);
+/* ... with a device results array (HETM_KERNEL_CACHE). */
+int hetm_dev_execute_batch_dptr_ex(hetm_dev* dev, int kernel_id, const void* d_inputs, uint64_t n_tx,
+                                   uint64_t* d_tickets, void* d_results, void* stream);
 int hetm_dev_validate_dptr(hetm_dev* dev, const hetm_log_entry* d_entries, uint64_t n, int mode,
                            void* stream);
 /* Read back (synchronously) the device conflict / stats counters. */
@@ -298,7 +349,7 @@ int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
  * duration and count, and resets the accumulator. */
 int hetm_dev_set_timing(hetm_dev* dev, int on);
 int hetm_dev_timing(hetm_dev* dev, int which, double* total_ms, uint64_t* count);
-/* Diagnostic counter words (phase clocks of instrumented builds); n <= 21. */
+/* Diagnostic counter words (phase clocks of instrumented builds); n <= 20. */
 int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
@@ -324,6 +375,13 @@ int hetm_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint
  * word is drawn as lo + rank - 1 with rank ~ Zipf(alpha) over [1, span] (rank 1
  * hottest; rejection-inversion sampler over DetRng uniform(), det_rng.hpp:36).
  * alpha == 0 is the uniform generator above. */
+/* Seeded cache transactions (BASELINE configs[3]): key rank ~ Zipf(alpha)
+ * over [1, key_space] (uniform when alpha == 0); key = {splitmix64(rank) with
+ * its last bit set to the part, rank}; part = `part` (0 or 1) or, when part <
+ * 0, part 1 except with probability steal_permille/1000 part 0; op GET with
+ * probability get_permille/1000, else SET of 4 DetRng value words. */
+int hetm_gen_cache_batch(uint64_t seed, uint64_t n, uint64_t key_space, double alpha, uint32_t get_permille,
+                         int32_t part, uint32_t steal_permille, hetm_cache_tx* out);
 int hetm_gen_bank_batch_zipf(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, double alpha, hetm_bank_tx* out);
 int hetm_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads, uint64_t lo,
                            uint64_t span, uint64_t ts_base, double alpha, hetm_log_entry* out);

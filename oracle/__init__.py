@@ -19,6 +19,8 @@ ENTRY = np.dtype([("addr", "<u8"), ("value", "<u8"), ("ts", "<u8")])
 BANK_TX = np.dtype([("acct", "<u4", (4,)), ("amount", "<u8")])
 RW_TX = np.dtype([("nr", "<u4"), ("nw", "<u4"), ("r_addr", "<u8", (4,)), ("w_addr", "<u8", (2,)),
                   ("add", "<u8", (2,))])
+CACHE_TX = np.dtype([("op", "<u4"), ("reserved", "<u4"), ("key", "<u8", (2,)), ("value", "<u8", (4,))])
+CACHE_RESULT = np.dtype([("value", "<u8", (4,)), ("status", "<u4"), ("way", "<u4")])
 RANGE = np.dtype([("offset_bytes", "<u8"), ("bytes", "<u8")])
 
 
@@ -53,6 +55,11 @@ for name, res, args in [
     ("orc_gen_bank_batch_zipf", None, [_u, _u, _u, _u, C.c_double, _v]),
     ("orc_gen_host_log_zipf", None, [_u, _u, C.c_uint32, C.c_uint32, _u, _u, _u, C.c_double, _v]),
     ("orc_zipf_fill", None, [_u, _u, _u, C.c_double, _v]),
+    ("orc_cache_hash", _u, [_u, _u]),
+    ("orc_cache_set_of", _u, [_u, _u, _u]),
+    ("orc_cache_replay", None, [_v, _u, _u, _u, _v, _v, _u, _v, _v, _v, _v, _v, _u, _u]),
+    ("orc_cache_host_run", _u, [_v, _u, _u, _u, _v, _u, _u, _v, _v]),
+    ("orc_gen_cache_batch", None, [_u, _u, _u, C.c_double, C.c_uint32, C.c_int32, C.c_uint32, _v]),
     ("orc_mt_bank_batch", _u, [_v, _u, _u, _v, _u, C.c_int, _u, _v, _v, _v, _v, _u, _u]),
     ("orc_mt_validate_apply", C.c_int, [_v, _u, _v, _u, _u, _v, _v, C.c_int, C.c_int]),
 ]:
@@ -93,6 +100,36 @@ def gen_host_log(seed, n_tx, wpt, threads, lo, span, ts_base=0, zipf=0.0):
     o = np.empty(n_tx * wpt, ENTRY)
     lib.orc_gen_host_log_zipf(seed, n_tx, wpt, threads, lo, span, ts_base, zipf, P(o))
     return o
+
+
+def gen_cache_batch(seed, n, key_space, alpha=0.5, get_permille=900, part=1, steal_permille=0):
+    o = np.empty(n, CACHE_TX)
+    lib.orc_gen_cache_batch(seed, n, key_space, alpha, get_permille, part, steal_permille, P(o))
+    return o
+
+
+def cache_replay(stmr, txs, tickets, n_sets, gran, chunk, base=0, cache_base=0):
+    """Device batch in ticket order on `stmr` (in place); returns (results, rs, ws, chunk) words."""
+    txs = np.ascontiguousarray(txs, CACHE_TX)
+    tickets = np.ascontiguousarray(tickets, np.uint64)
+    order = order_by_ticket(tickets)
+    res = np.zeros(txs.size, CACHE_RESULT)
+    W = stmr.size
+    rs = np.zeros(words_for_bits(W * 8 // gran), np.uint64)
+    ws = np.zeros_like(rs)
+    ch = np.zeros(words_for_bits((W * 8 + chunk - 1) // chunk), np.uint64)
+    lib.orc_cache_replay(P(stmr), base, cache_base, n_sets, P(txs), P(order), order.size, P(tickets), P(res),
+                         P(rs), P(ws), P(ch), gran, chunk)
+    return res, rs, ws, ch
+
+
+def cache_host_run(stmr, txs, n_sets, ts_base, base=0, cache_base=0):
+    """Host transactions in order (ts = ts_base+1+i) on `stmr`; returns (results, write log)."""
+    txs = np.ascontiguousarray(txs, CACHE_TX)
+    res = np.zeros(txs.size, CACHE_RESULT)
+    log = np.zeros(txs.size * 8, ENTRY)
+    m = lib.orc_cache_host_run(P(stmr), base, cache_base, n_sets, P(txs), txs.size, ts_base, P(res), P(log))
+    return res, log[:m].copy()
 
 
 def zipf_ranks(seed, n, span, alpha):

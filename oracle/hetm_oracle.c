@@ -146,6 +146,96 @@ void orc_rw_replay(uint64_t* s, uint64_t base, const orc_rw_tx* tx, const uint64
     }
 }
 
+/* ------------------------------------------------ cache (configs[3]) --
+ * MemcachedGPU-style set-associative cache (capi.h hetm_cache_*; PAPER.md:
+ * 480-508): 8 ways x 8 words {key0,key1,value0..3,lru,
+ * flags} per set; LRU stamp = serial position (device: ticket + 1). */
+enum { C_WAYS = 8, C_WAYW = 8, C_SETW = 64, C_VAL = 2, C_LRU = 6, C_FLAGS = 7 };
+
+uint64_t orc_cache_hash(uint64_t k0, uint64_t k1) {
+    uint64_t z = k0 ^ (k1 * 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+uint64_t orc_cache_set_of(uint64_t k0, uint64_t k1, uint64_t n_sets) {
+    uint64_t half = n_sets / 2;
+    return (k0 & 1) * half + (orc_cache_hash(k0, k1) & (half - 1));
+}
+
+static void cache_apply(uint64_t* s, uint64_t base, uint64_t cbase, uint64_t n_sets, const orc_cache_tx* t,
+                        uint64_t stamp, orc_cache_result* out, uint64_t* rs, uint64_t* ws, uint64_t* ch,
+                        uint64_t gran, uint64_t chunk, orc_entry* log, uint64_t* nlog, uint64_t ts) {
+    const uint64_t s0 = cbase + orc_cache_set_of(t->key[0], t->key[1], n_sets) * C_SETW;
+    int hit = C_WAYS, inv = C_WAYS, lru = 0;
+    for (int w = 0; w < C_WAYS; ++w) {
+        const uint64_t* way = s + s0 + (uint64_t)w * C_WAYW;
+        if (hit == C_WAYS && (way[C_FLAGS] & 1) && way[0] == t->key[0] && way[1] == t->key[1]) hit = w;
+        if (inv == C_WAYS && !(way[C_FLAGS] & 1)) inv = w;
+        if (way[C_LRU] < s[s0 + (uint64_t)lru * C_WAYW + C_LRU]) lru = w;
+        mark(rs, s0 + (uint64_t)w * C_WAYW + 0, gran);
+        mark(rs, s0 + (uint64_t)w * C_WAYW + 1, gran);
+        mark(rs, s0 + (uint64_t)w * C_WAYW + C_LRU, gran);
+        mark(rs, s0 + (uint64_t)w * C_WAYW + C_FLAGS, gran);
+    }
+    int target;
+    uint32_t status;
+    if (t->op == 0) { target = hit; status = hit < C_WAYS ? 1 : 0; }
+    else if (hit < C_WAYS) { target = hit; status = 2; }
+    else if (inv < C_WAYS) { target = inv; status = 3; }
+    else { target = lru; status = 4; }
+    out->status = status;
+    out->way = (uint32_t)target;
+    for (int q = 0; q < 4; ++q) out->value[q] = 0;
+    if (target == C_WAYS) return;
+    uint64_t* way = s + s0 + (uint64_t)target * C_WAYW;
+    const uint64_t wl = s0 + (uint64_t)target * C_WAYW;
+    for (int q = 0; q < 4; ++q) {
+        out->value[q] = t->op == 0 ? way[C_VAL + q] : t->value[q];
+        mark(rs, wl + C_VAL + q, gran);
+    }
+    unsigned wmask = t->op == 0 ? (1u << C_LRU) : (status == 2 ? (0xfu << C_VAL) | (1u << C_LRU) : 0xffu);
+    uint64_t nv[C_WAYW];
+    for (int q = 0; q < C_WAYW; ++q) nv[q] = way[q];
+    if (t->op == 1) {
+        nv[0] = t->key[0];
+        nv[1] = t->key[1];
+        for (int q = 0; q < 4; ++q) nv[C_VAL + q] = t->value[q];
+        nv[C_FLAGS] = 1;
+    }
+    nv[C_LRU] = stamp;
+    for (int q = 0; q < C_WAYW; ++q) {
+        if (!((wmask >> q) & 1u)) continue;
+        way[q] = nv[q];
+        mark(ws, wl + q, gran);
+        mark(ch, wl + q, chunk);
+        if (log) {
+            log[*nlog].addr = base + wl + q;
+            log[*nlog].value = nv[q];
+            log[*nlog].ts = ts;
+            ++*nlog;
+        }
+    }
+}
+
+void orc_cache_replay(uint64_t* s, uint64_t base, uint64_t cbase, uint64_t n_sets, const orc_cache_tx* tx,
+                      const uint64_t* order, uint64_t n_order, const uint64_t* tickets, orc_cache_result* results,
+                      uint64_t* rs, uint64_t* ws, uint64_t* ch, uint64_t gran, uint64_t chunk) {
+    for (uint64_t k = 0; k < n_order; ++k) {
+        const uint64_t i = order[k];
+        cache_apply(s, base, cbase, n_sets, &tx[i], tickets[i] + 1, &results[i], rs, ws, ch, gran, chunk, NULL, NULL, 0);
+    }
+}
+
+uint64_t orc_cache_host_run(uint64_t* s, uint64_t base, uint64_t cbase, uint64_t n_sets, const orc_cache_tx* tx,
+                            uint64_t n, uint64_t ts_base, orc_cache_result* results, orc_entry* log) {
+    uint64_t nlog = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        cache_apply(s, base, cbase, n_sets, &tx[i], ts_base + 1 + i, &results[i], NULL, NULL, NULL, 8, 8, log, &nlog,
+                    ts_base + 1 + i);
+    return nlog;
+}
+
 static const uint64_t* g_sort_keys;
 static int cmp_by_key(const void* x, const void* y) {
     uint64_t i = *(const uint64_t*)x, j = *(const uint64_t*)y;
@@ -299,6 +389,22 @@ void orc_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t 
 void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo,
                       uint64_t span, uint64_t ts_base, orc_entry* out) {
     orc_gen_host_log_zipf(seed, n_tx, wpt, T, lo, span, ts_base, 0.0, out);
+}
+
+void orc_gen_cache_batch(uint64_t seed, uint64_t n, uint64_t key_space, double alpha, uint32_t get_permille,
+                         int32_t part, uint32_t steal_permille, orc_cache_tx* out) {
+    orc_rng r; orc_rng_init(&r, seed);
+    orc_zipf z; zf_init(&z, alpha > 0 ? alpha : 1.0, key_space);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t rank = alpha > 0 ? zf_sample(&z, &r) : orc_rng_below(&r, key_space) + 1;
+        uint64_t p = (uint64_t)part;
+        if (part < 0) p = orc_rng_below(&r, 1000) < steal_permille ? 0 : 1;
+        out[i].op = orc_rng_below(&r, 1000) < get_permille ? 0 : 1;
+        out[i].reserved = 0;
+        out[i].key[0] = (orc_splitmix64(rank) & ~1ULL) | p;
+        out[i].key[1] = rank;
+        for (int q = 0; q < 4; ++q) out[i].value[q] = out[i].op == 1 ? orc_rng_next(&r) : 0;
+    }
 }
 
 /* ------------------------------------------------------- CPU baselines -- */

@@ -30,6 +30,8 @@ typedef struct {
     uint64_t r_addr[4], w_addr[2], add[2];
 } orc_rw_tx;                                                       /* capi.h hetm_rw_tx */
 typedef struct { uint64_t offset_bytes, bytes; } orc_range;
+typedef struct { uint32_t op, reserved; uint64_t key[2]; uint64_t value[4]; } orc_cache_tx; /* capi.h hetm_cache_tx */
+typedef struct { uint64_t value[4]; uint32_t status, way; } orc_cache_result;            /* hetm_cache_result */
 
 /* ---- det_rng.hpp:8-42 ---- */
 uint64_t orc_splitmix64(uint64_t x);
@@ -89,6 +91,18 @@ void orc_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, o
 void orc_gen_bank_batch_zipf(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, double alpha, orc_bank_tx* out);
 void orc_gen_host_log_zipf(uint64_t seed, uint64_t n_tx, uint32_t wpt, uint32_t T, uint64_t lo, uint64_t span,
                            uint64_t ts_base, double alpha, orc_entry* out);
+uint64_t orc_cache_hash(uint64_t k0, uint64_t k1);
+uint64_t orc_cache_set_of(uint64_t k0, uint64_t k1, uint64_t n_sets);
+/* device batch replayed in ticket order (LRU stamp = ticket + 1) */
+void orc_cache_replay(uint64_t* s, uint64_t base, uint64_t cbase, uint64_t n_sets, const orc_cache_tx* tx,
+                      const uint64_t* order, uint64_t n_order, const uint64_t* tickets, orc_cache_result* results,
+                      uint64_t* rs, uint64_t* ws, uint64_t* ch, uint64_t gran, uint64_t chunk);
+/* host transactions in order with ts = ts_base+1+i (LRU stamp = ts); their
+ * writes appended to `log` as <addr,value,ts>; returns the entry count */
+uint64_t orc_cache_host_run(uint64_t* s, uint64_t base, uint64_t cbase, uint64_t n_sets, const orc_cache_tx* tx,
+                            uint64_t n, uint64_t ts_base, orc_cache_result* results, orc_entry* log);
+void orc_gen_cache_batch(uint64_t seed, uint64_t n, uint64_t key_space, double alpha, uint32_t get_permille,
+                         int32_t part, uint32_t steal_permille, orc_cache_tx* out);
 void orc_zipf_fill(uint64_t seed, uint64_t n, uint64_t span, double alpha, uint64_t* out);
 void orc_gen_host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_threads,
                       uint64_t lo, uint64_t span, uint64_t ts_base, orc_entry* out);

@@ -120,6 +120,14 @@ _sigs = {
     "hetm_dev_transfer_log": (C.c_int, [_vp, C.POINTER(TransferRecord), C.c_uint64, u8p]),
     "hetm_dev_clear_transfer_log": (C.c_int, [_vp]),
     "hetm_dev_execute_batch_dptr": (C.c_int, [_vp, C.c_int, _vp, C.c_uint64, _vp, _vp]),
+    "hetm_dev_execute_batch_dptr_ex": (C.c_int, [_vp, C.c_int, _vp, C.c_uint64, _vp, _vp, _vp]),
+    "hetm_dev_execute_batch_ex": (C.c_int, [_vp, C.c_int, _vp, C.c_uint64, C.c_uint64, _vp, _vp, C.c_uint64,
+                                            C.POINTER(BatchStats)]),
+    "hetm_dev_set_cache_geometry": (C.c_int, [_vp, C.c_uint64, C.c_uint64]),
+    "hetm_cache_hash": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "hetm_cache_set_of": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
+    "hetm_gen_cache_batch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_uint32, C.c_int32,
+                                       C.c_uint32, _vp]),
     "hetm_dev_validate_dptr": (C.c_int, [_vp, _vp, C.c_uint64, C.c_int, _vp]),
     "hetm_dev_read_counters": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(BatchStats)]),
     "hetm_dev_route_log_dptr": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint64, _vp, _vp, _vp]),

@@ -18,7 +18,10 @@ from ._lib import lib
 REPLICA_HOST, REPLICA_DEV, REPLICA_DEV_SHADOW, REPLICA_HOST_SNAPSHOT = 0, 1, 2, 3  # types.hpp:21
 BMP_RS, BMP_WS, BMP_CHUNK = 0, 1, 2
 APPLY, VALIDATE_ONLY = 0, 1
-KERNEL_BANK, KERNEL_RW = 1, 2
+KERNEL_BANK, KERNEL_RW, KERNEL_CACHE = 1, 2, 3
+CACHE_GET, CACHE_SET = 0, 1
+CACHE_MISS, CACHE_HIT, CACHE_UPDATED, CACHE_INSERTED, CACHE_EVICTED = range(5)
+CACHE_WAYS, CACHE_WAY_WORDS, CACHE_SET_WORDS = 8, 8, 64
 CLEAR_RESET_TS = 1
 CLEAR_ASYNC = 2
 CFG_NO_SHADOW = 1
@@ -33,7 +36,10 @@ BANK_TX = np.dtype([("acct", "<u4", (4,)), ("amount", "<u8")])
 RW_TX = np.dtype(
     [("nr", "<u4"), ("nw", "<u4"), ("r_addr", "<u8", (4,)), ("w_addr", "<u8", (2,)), ("add", "<u8", (2,))]
 )
+CACHE_TX = np.dtype([("op", "<u4"), ("reserved", "<u4"), ("key", "<u8", (2,)), ("value", "<u8", (4,))])
+CACHE_RESULT = np.dtype([("value", "<u8", (4,)), ("status", "<u4"), ("way", "<u4")])
 assert LOG_ENTRY.itemsize == 24 and BANK_TX.itemsize == 24 and RW_TX.itemsize == 72
+assert CACHE_TX.itemsize == 56 and CACHE_RESULT.itemsize == 40
 
 
 # --------------------------------------------------------------------- errors
@@ -128,6 +134,20 @@ def gen_host_log(seed: int, n_tx: int, writes_per_tx: int, n_threads: int, lo: i
     return out
 
 
+def gen_cache_batch(seed: int, n: int, key_space: int, alpha: float = 0.5, get_permille: int = 900,
+                    part: int = 1, steal_permille: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """Seeded MemcachedGPU-style GET/SET transactions (BASELINE configs[3]): key
+    rank ~ Zipf(alpha), routed to `part` by the key's last bit (part < 0: part 1,
+    stealing part-0 keys with probability steal_permille/1000)."""
+    out = np.empty(n, CACHE_TX) if out is None else out
+    check(lib.hetm_gen_cache_batch(seed, n, key_space, float(alpha), get_permille, part, steal_permille, _ptr(out)))
+    return out
+
+
+def cache_set_of(key0: int, key1: int, n_sets: int) -> int:
+    return int(lib.hetm_cache_set_of(key0, key1, n_sets))
+
+
 # ------------------------------------------------------------------ snapshots
 @dataclass
 class BitmapSnapshot:
@@ -155,6 +175,7 @@ class BatchResult:
     ticket_first: int
     ticket_end: int
     kernel_ms: float
+    results: np.ndarray | None = None  # CACHE_RESULT per transaction (KERNEL_CACHE)
 
 
 # ------------------------------------------------------------- device guest
@@ -236,17 +257,28 @@ class GpuDevice:
     def register_kernel(self, kernel_id: int):
         self._chk(lib.hetm_dev_register_kernel(self.h, kernel_id))
 
-    def execute_batch(self, kernel_id: int, inputs: np.ndarray, want_tickets: bool = True) -> BatchResult:
-        """executeBatch: returns commit tickets (ascending ticket = serial order)."""
+    def execute_batch(self, kernel_id: int, inputs: np.ndarray, want_tickets: bool = True,
+                      results: bool = False) -> BatchResult:
+        """executeBatch: returns commit tickets (ascending ticket = serial order);
+        results=True also returns the per-transaction CACHE_RESULT records."""
         inputs = np.ascontiguousarray(inputs)
         n = inputs.shape[0]
         tickets = np.empty(n, np.uint64) if want_tickets else None
+        res = np.zeros(n, CACHE_RESULT) if results else None
         st = _lib.BatchStats()
-        self._chk(lib.hetm_dev_execute_batch(self.h, kernel_id, _ptr(inputs) if n else None,
-                                             inputs.dtype.itemsize, n,
-                                             _ptr(tickets) if (want_tickets and n) else None, C.byref(st)))
-        return BatchResult(tickets, st.n_tx, st.committed, st.aborts, st.livelocked, st.ticket_first,
-                           st.ticket_end, st.kernel_ms)
+        self._chk(lib.hetm_dev_execute_batch_ex(self.h, kernel_id, _ptr(inputs) if n else None,
+                                                inputs.dtype.itemsize, n,
+                                                _ptr(tickets) if (want_tickets and n) else None,
+                                                _ptr(res) if (results and n) else None,
+                                                CACHE_RESULT.itemsize if results else 0, C.byref(st)))
+        r = BatchResult(tickets, st.n_tx, st.committed, st.aborts, st.livelocked, st.ticket_first,
+                        st.ticket_end, st.kernel_ms)
+        r.results = res
+        return r
+
+    def set_cache_geometry(self, base_word: int, n_sets: int):
+        """Cache region of KERNEL_CACHE: n_sets (power of two) sets from base_word."""
+        self._chk(lib.hetm_dev_set_cache_geometry(self.h, base_word, n_sets))
 
     def bitmap_stats(self):
         """bitmapStats -> (rsBitsSet, wsBitsSet, chunksDirty)."""
@@ -334,8 +366,10 @@ class GpuDevice:
         self._chk(lib.hetm_dev_clear_transfer_log(self.h))
 
     # device-resident entries (benchmark / shard router) ---------------------
-    def execute_batch_dptr(self, kernel_id: int, d_inputs: int, n: int, d_tickets: int, stream: int = 0):
-        self._chk(lib.hetm_dev_execute_batch_dptr(self.h, kernel_id, d_inputs, n, d_tickets, stream or None))
+    def execute_batch_dptr(self, kernel_id: int, d_inputs: int, n: int, d_tickets: int, stream: int = 0,
+                           d_results: int = 0):
+        self._chk(lib.hetm_dev_execute_batch_dptr_ex(self.h, kernel_id, d_inputs, n, d_tickets, d_results or None,
+                                                     stream or None))
 
     def validate_dptr(self, d_entries: int, n: int, mode: int = APPLY, stream: int = 0):
         self._chk(lib.hetm_dev_validate_dptr(self.h, d_entries, n, mode, stream or None))

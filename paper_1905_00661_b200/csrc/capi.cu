@@ -111,6 +111,9 @@ struct hetm_dev {
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
     unsigned long long* d_restore = nullptr; // apply-kernel restore queue (kRestoreCap entries)
+    CacheGeom cache{};                   // HETM_KERNEL_CACHE region
+    hetm_cache_result* d_res = nullptr;  // per-transaction results (host-buffer path)
+    uint64_t res_cap = 0;
     uint32_t* d_wlog = nullptr;          // write-set log (2 slots per commit ticket of the round)
     uint64_t wlog_slots = 0;
     uint64_t round_tx = 0;               // transactions submitted this round (ticket upper bound)
@@ -248,6 +251,7 @@ size_t record_bytes(int kernel_id) {
     switch (kernel_id) {
         case HETM_KERNEL_BANK: return sizeof(hetm_bank_tx);
         case HETM_KERNEL_RW: return sizeof(hetm_rw_tx);
+        case HETM_KERNEL_CACHE: return sizeof(hetm_cache_tx);
         default: return 0;
     }
 }
@@ -278,7 +282,7 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
-                  cudaStream_t s) {
+                  void* d_results, cudaStream_t s) {
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
@@ -293,6 +297,9 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     if (kernel_id == HETM_KERNEL_BANK)
         e = launch_bank_batch(d->view(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                               d->max_attempts, d->geom, s);
+    else if (kernel_id == HETM_KERNEL_CACHE)
+        e = launch_cache_batch(d->view(), d->cache, static_cast<const hetm_cache_tx*>(d_inputs), n, d_tickets,
+                               static_cast<hetm_cache_result*>(d_results), d->d_ctr, d->max_attempts, d->geom, s);
     else
         e = launch_rw_batch(d->view(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                             d->max_attempts, d->geom, s);
@@ -476,6 +483,9 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     d->device = cfg->device;
     d->W = cfg->size_words;
     d->base = cfg->shard_base;
+    d->cache.base_local = 0;  // default cache region: the largest power-of-two set count that fits
+    d->cache.n_sets = 2;
+    while (d->cache.n_sets * 2 * HETM_CACHE_SET_WORDS <= d->W) d->cache.n_sets *= 2;
     d->gran_shift = log2u(cfg->rs_gran_bytes / 8);
     d->chunk_shift = log2u(cfg->chunk_bytes / 8);
     d->rs_bits = (d->W * 8 + cfg->rs_gran_bytes - 1) / cfg->rs_gran_bytes;  // bitmap.hpp:96-97 ceil
@@ -553,7 +563,7 @@ int hetm_dev_close(hetm_dev* d) {
     d->pool.reset();
     if (d->h_delta) cudaFreeHost(d->h_delta);
     for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
@@ -665,11 +675,24 @@ int hetm_dev_register_kernel(hetm_dev* d, int kernel_id) {
 
 int hetm_dev_execute_batch(hetm_dev* d, int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx,
                            uint64_t* tickets_out, hetm_batch_stats* stats) {
+    return hetm_dev_execute_batch_ex(d, kernel_id, inputs, rec_bytes, n_tx, tickets_out, nullptr, 0, stats);
+}
+
+int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx,
+                              uint64_t* tickets_out, void* results_out, uint64_t res_bytes,
+                              hetm_batch_stats* stats) {
     if (!d || (!inputs && n_tx)) return HETM_ERR_INVALID_ARG;
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
     if (rec_bytes != record_bytes(kernel_id)) return HETM_ERR_INVALID_SIZE;
     if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;  // priorities are 31-bit
+    if (results_out && (kernel_id != HETM_KERNEL_CACHE || res_bytes != sizeof(hetm_cache_result)))
+        return HETM_ERR_INVALID_SIZE;
     int rc;
+    if (results_out && n_tx > d->res_cap) {
+        if (d->d_res) { CK(d, cudaStreamSynchronize(d->s_exec)); cudaFree(d->d_res); d->bytes_alloc -= d->res_cap * sizeof(hetm_cache_result); }
+        d->res_cap = std::max<uint64_t>(n_tx, 1 << 16);
+        if ((rc = dev_alloc(d, (void**)&d->d_res, d->res_cap * sizeof(hetm_cache_result)))) return rc;
+    }
     if (n_tx * rec_bytes > d->in_cap) {
         if (d->d_in) { CK(d, cudaStreamSynchronize(d->s_exec)); cudaFree(d->d_in); d->bytes_alloc -= d->in_cap; }
         d->in_cap = std::max<uint64_t>(n_tx * rec_bytes, 1 << 20);
@@ -690,11 +713,15 @@ int hetm_dev_execute_batch(hetm_dev* d, int kernel_id, const void* inputs, uint6
     }
     CK(d, cudaMemsetAsync(&d->d_ctr->oob, 0, sizeof(unsigned), s));
     CK(d, cudaEventRecord(d->ev_t0, s));
-    if ((rc = enqueue_batch(d, kernel_id, d->d_in, n_tx, d->d_tk, s))) return rc;
+    if ((rc = enqueue_batch(d, kernel_id, d->d_in, n_tx, d->d_tk, results_out ? d->d_res : nullptr, s))) return rc;
     CK(d, cudaEventRecord(d->ev_t1, s));
     if (tickets_out && n_tx) {
         CK(d, cudaMemcpyAsync(tickets_out, d->d_tk, n_tx * 8, cudaMemcpyDeviceToHost, s));
         d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * 8);
+    }
+    if (results_out && n_tx) {
+        CK(d, cudaMemcpyAsync(results_out, d->d_res, n_tx * res_bytes, cudaMemcpyDeviceToHost, s));
+        d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * res_bytes);
     }
     CK(d, cudaMemcpyAsync(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(d, cudaStreamSynchronize(s));
@@ -967,8 +994,8 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     for (auto& r : ranges) dirty_bytes += r.second * 8;
     // delta form when enabled, the write-set log is complete and it moves fewer bytes
     const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
-    const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && n_slots <= d->wlog_slots &&
-                       n_slots * sizeof(DeltaRec) < dirty_bytes;
+    const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && !d->h_ctr->wlog_overflow &&
+                       n_slots <= d->wlog_slots && n_slots * sizeof(DeltaRec) < dirty_bytes;
     if (delta) {
         if ((rc = merge_commit_delta(d, host, n_slots))) return rc;
         if (st) {
@@ -1031,11 +1058,19 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
     hetm_merge_stats s{};
     if (optimized && d->d_shadow && d->shadow_synced) {
         // Round-start shadow + the round's host log in ts order: the
-        // device-dirty words are restored from devShadow, then the freshest log
-        // entry of every logged word is stored into both devReplica and devShadow.
-        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift,
-                                            false, d->geom, d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(restore)");
+        // device-dirty words are restored from devShadow (just the device write
+        // set when the write-set log holds it, else whole dirty chunks), then the
+        // freshest log entry of every logged word is stored into both devReplica
+        // and devShadow.
+        if ((rc = read_counters(d))) return rc;
+        const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
+        cudaError_t e;
+        if (d->d_wlog && !d->h_ctr->wlog_overflow && n_slots <= d->wlog_slots && n_slots * 8 < dirty_bytes)
+            e = launch_wlog_restore(d->d_cells, d->d_shadow, d->d_wlog, n_slots, d->W, d->geom, d->s_merge);
+        else
+            e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, false,
+                                    d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "restore(rollback)");
         e = launch_winner_apply(d->d_cells, nullptr, d->base, d->W, d->d_arena, d->arena_n, d->geom, d->s_merge);
         if (e == cudaSuccess)
             e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
@@ -1200,7 +1235,33 @@ int hetm_dev_execute_batch_dptr(hetm_dev* d, int kernel_id, const void* d_inputs
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
     if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
-    return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), s);
+    return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), nullptr, s);
+}
+
+int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n_tx,
+                                   uint64_t* d_tickets, void* d_results, void* stream) {
+    if (!d || (n_tx && (!d_inputs || !d_tickets))) return HETM_ERR_INVALID_ARG;
+    if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
+    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;
+    if (d_results && kernel_id != HETM_KERNEL_CACHE) return HETM_ERR_INVALID_SIZE;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
+    return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), d_results,
+                         s);
+}
+
+int hetm_dev_set_cache_geometry(hetm_dev* d, uint64_t base_word, uint64_t n_sets) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    if (n_sets < 2 || (n_sets & (n_sets - 1))) return HETM_ERR_INVALID_SIZE;
+    if (base_word < d->base || base_word - d->base + n_sets * HETM_CACHE_SET_WORDS > d->W)
+        return HETM_ERR_OUT_OF_BOUNDS;
+    d->cache.base_local = base_word - d->base;
+    d->cache.n_sets = n_sets;
+    return HETM_OK;
+}
+
+uint64_t hetm_cache_hash(uint64_t key0, uint64_t key1) { return cache_hash(key0, key1); }
+uint64_t hetm_cache_set_of(uint64_t key0, uint64_t key1, uint64_t n_sets) {
+    return n_sets >= 2 ? cache_set_of(key0, key1, n_sets) : 0;
 }
 
 int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_t n, int mode, void* stream) {
@@ -1263,7 +1324,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 21) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 20) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

@@ -57,6 +57,15 @@ __global__ void wlog_gather_kernel(DeltaRec* __restrict__ out, uint64_t* __restr
     }
 }
 
+// Rollback: cells[loc].value = shadow[loc] for every write-set log slot.
+__global__ void wlog_restore_kernel(Cell* __restrict__ cells, const uint64_t* __restrict__ shadow,
+                                    const uint32_t* __restrict__ wlog, uint64_t n, uint64_t size_words) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t loc = wlog[i];
+        if (loc < size_words) cells[loc].value = shadow[loc];
+    }
+}
+
 static unsigned grid_words(uint64_t n, const LaunchGeom& g) {
     uint64_t want = (n + 255) / 256;
     const uint64_t cap = (uint64_t)g.sm_count * 16;
@@ -106,6 +115,13 @@ cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint
                              size_t temp_bytes, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int64_t)n, 0, sort_bits(size_words), s);
+}
+
+cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
+                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    wlog_restore_kernel<<<grid_words(n, g), 256, 0, s>>>(cells, shadow, wlog, n, size_words);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,

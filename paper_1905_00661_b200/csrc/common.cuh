@@ -47,7 +47,8 @@ struct DevCounters {
     unsigned long long restore_done; // restore_kernel: finished blocks
     unsigned long long ts_floor;     // max log ts of all previous rounds (device-maintained)
     unsigned long long wlog_base;    // first commit ticket of the round (write-set log origin)
-    unsigned long long pad[21];      // diagnostics (phase clocks / ticket counts)
+    unsigned long long wlog_overflow;// a committed write set did not fit the write-set log
+    unsigned long long pad[20];      // diagnostics (phase clocks / ticket counts)
 };
 
 static_assert(sizeof(DevCounters) == 256, "two 128-B lines");
@@ -65,6 +66,26 @@ struct ShardView {
     uint32_t* wlog;            // device write-set log (nullptr: disabled, shard >= 2^32 words)
     uint64_t wlog_slots;       // its capacity in slots
 };
+
+// Cache region of HETM_KERNEL_CACHE (capi.h hetm_cache_*): n_sets sets of
+// HETM_CACHE_SET_WORDS words from local word base_local.
+struct CacheGeom {
+    uint64_t base_local;
+    uint64_t n_sets;  // power of two >= 2
+};
+
+// Key hash (splitmix64 finalizer over the two key words) and last-bit routing
+// (PAPER.md:489): part = key0 & 1 owns the half [part*n/2, (part+1)*n/2).
+__host__ __device__ __forceinline__ uint64_t cache_hash(uint64_t k0, uint64_t k1) {
+    uint64_t z = k0 ^ (k1 * 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t cache_set_of(uint64_t k0, uint64_t k1, uint64_t n_sets) {
+    const uint64_t half = n_sets >> 1;
+    return (k0 & 1ull) * half + (cache_hash(k0, k1) & (half - 1));
+}
 
 // Device write-set log: slot 2*(ticket - round's first ticket) + j holds the
 // local index of the j-th written word of the committed transaction (~0u:

@@ -119,7 +119,35 @@ int host_log(uint64_t seed, uint64_t n_tx, uint32_t writes_per_tx, uint32_t n_th
     return HETM_OK;
 }
 
+uint64_t mix64(uint64_t x) {  // splitmix64 output function (det_rng.hpp:8-13)
+    uint64_t z = x + 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
 }  // namespace
+
+extern "C" int hetm_gen_cache_batch(uint64_t seed, uint64_t n, uint64_t key_space, double alpha, uint32_t get_permille,
+                                    int32_t part, uint32_t steal_permille, hetm_cache_tx* out) {
+    if (!out && n) return HETM_ERR_INVALID_ARG;
+    if (key_space < 1 || get_permille > 1000 || steal_permille > 1000 || part > 1 || !(alpha >= 0.0))
+        return HETM_ERR_INVALID_SIZE;
+    const Zipf z(alpha > 0 ? alpha : 1.0, key_space);
+    SeqRng r(seed);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t rank = alpha > 0 ? z.rank(r) : r.below(key_space) + 1;
+        uint64_t p = (uint64_t)part;
+        if (part < 0) p = r.below(1000) < steal_permille ? 0 : 1;
+        hetm_cache_tx& t = out[i];
+        t.op = r.below(1000) < get_permille ? HETM_CACHE_GET : HETM_CACHE_SET;
+        t.reserved = 0;
+        t.key[0] = (mix64(rank) & ~1ull) | p;
+        t.key[1] = rank;
+        for (int q = 0; q < 4; ++q) t.value[q] = t.op == HETM_CACHE_SET ? r.next() : 0;
+    }
+    return HETM_OK;
+}
 
 extern "C" int hetm_gen_bank_batch(uint64_t seed, uint64_t n, uint64_t lo, uint64_t span, hetm_bank_tx* out) {
     return bank_batch(seed, n, lo, span, 0.0, out);

@@ -10,6 +10,7 @@ namespace hetm_b200 {
 struct DevCounters;
 struct ShardView;
 struct Cell;
+struct CacheGeom;
 
 // One merge delta record: local word index + value (16 B, DMA'd to the host).
 struct DeltaRec {
@@ -26,6 +27,9 @@ struct LaunchGeom {
 // guest-stm-batch: one launch executes a whole batch.
 cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                               DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
+cudaError_t launch_cache_batch(const ShardView& v, const CacheGeom& cg, const hetm_cache_tx* d_in, uint64_t n,
+                               unsigned long long* d_tickets, hetm_cache_result* d_res, DevCounters* ctr,
+                               uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
 cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                             DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
 
@@ -53,6 +57,9 @@ cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_word
 // Write-set log -> compact delta (+ devShadow refresh when shadow != nullptr).
 cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
+// Rollback of the device write set: cells[loc].value = shadow[loc] per log slot.
+cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
+                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

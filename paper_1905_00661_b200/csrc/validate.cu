@@ -228,6 +228,7 @@ __global__ void roll_round_kernel(DevCounters* ctr, int reset_ts) {
     ctr->ts_floor = reset_ts ? 0ull : (m > ctr->ts_floor ? m : ctr->ts_floor);
     ctr->round_max_ts = 0;
     ctr->wlog_base = ctr->ticket;  // the next round's write-set log starts here
+    ctr->wlog_overflow = 0;
 }
 
 cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s) {

@@ -94,7 +94,20 @@ def test_zipf_generators_match_oracle(hetm, orc, alpha):
     assert a.tobytes() == b.tobytes()
 
 
+@pytest.mark.parametrize("args", [(1, 5000, 1 << 20, 0.5, 900, 1, 0), (2, 3000, 1000, 0.0, 999, -1, 200),
+                                  (3, 2000, 1 << 16, 0.99, 500, 0, 0)])
+def test_cache_generator_matches_oracle(hetm, orc, args):
+    a = hetm.gen_cache_batch(*args)
+    b = orc.gen_cache_batch(*args)
+    assert a.tobytes() == b.tobytes()
+    for t in a[:200]:
+        for n_sets in (2, 1024, 1 << 20):
+            assert hetm.cache_set_of(int(t["key"][0]), int(t["key"][1]), n_sets) == \
+                orc.lib.orc_cache_set_of(int(t["key"][0]), int(t["key"][1]), n_sets)
+
+
 def test_wire_formats(hetm):
     assert hetm.LOG_ENTRY.itemsize == 24  # write_log.hpp:25
     assert hetm.BANK_TX.itemsize == 24
     assert hetm.RW_TX.itemsize == 72
+    assert hetm.CACHE_TX.itemsize == 56 and hetm.CACHE_RESULT.itemsize == 40

@@ -640,6 +640,97 @@ def test_cfg3_zipf_full_size(hetm, orc, dev_factory):
     del keep
 
 
+# ------------------------------------ cfg4: MemcachedGPU-style cache GET/SET
+def check_cache_replay(hetm, orc, d, txs, r, init, n_sets, gran=1024, chunk=16384):
+    order = orc.order_by_ticket(r.tickets)
+    assert order.size == txs.size
+    ref = init.copy()
+    res, rs, ws, ch = orc.cache_replay(ref, txs, r.tickets, n_sets, gran, chunk)
+    got = d.download(hetm.REPLICA_DEV)
+    assert (got == ref).all(), f"{int((got != ref).sum())} words differ from ticket-order replay"
+    assert (r.results == res).all(), "GET/SET results differ"
+    assert (d.snapshot(hetm.BMP_RS).words == rs).all()
+    assert (d.snapshot(hetm.BMP_WS).words == ws).all()
+    assert (d.snapshot(hetm.BMP_CHUNK).words == ch).all()
+    assert ((ws & ~rs) == 0).all()
+    return ref
+
+
+@pytest.mark.parametrize("gran", GRANS)
+@pytest.mark.parametrize("n_sets,n,alpha", [(64, 1 << 12, 0.5), (1024, 1 << 14, 0.5), (1 << 14, 1 << 16, 0.99)])
+def test_cache_batch_replays(hetm, orc, dev_factory, gran, n_sets, n, alpha):
+    """GET/SET 90/10 (BASELINE configs[3]) after a warm-up SET batch: STMR,
+    per-transaction results and bitmaps equal the ticket-order replay."""
+    W = n_sets * 64
+    d = dev_factory(W, rs_gran_bytes=gran)
+    d.register_kernel(hetm.KERNEL_CACHE)
+    init = np.zeros(W, np.uint64)
+    warm = orc.gen_cache_batch(1, n, n_sets * 4, alpha, get_permille=0, part=-1, steal_permille=500)
+    r = d.execute_batch(hetm.KERNEL_CACHE, warm, results=True)
+    ref = check_cache_replay(hetm, orc, d, warm, r, init, n_sets, gran)
+    d.clear_round()
+    txs = orc.gen_cache_batch(2, n, n_sets * 4, alpha, get_permille=900, part=-1, steal_permille=500)
+    r = d.execute_batch(hetm.KERNEL_CACHE, txs, results=True)
+    check_cache_replay(hetm, orc, d, txs, r, ref, n_sets, gran)
+    st = r.results["status"]
+    assert (st == hetm.CACHE_HIT).any() and (st == hetm.CACHE_MISS).any()
+
+
+@pytest.mark.parametrize("steal", [0, 1000])
+def test_cache_rounds_against_host(hetm, orc, dev_factory, steal):
+    """routing by the key's last bit -> no inter-device
+    conflict (steal 0); the GPU taking the CPU's keys (steal 1000) conflicts
+    and rolls back.  Replicas equal after every round."""
+    n_sets = 1 << 12
+    W = n_sets * 64
+    d = dev_factory(W, rs_gran_bytes=1024, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_CACHE)
+    host = np.zeros(W, np.uint64)
+    outcomes = []
+    ts = 0
+    for rnd in range(4):
+        gpu = orc.gen_cache_batch(10 + rnd, 1 << 13, 1 << 14, 0.5, 900 if rnd else 0, part=-1,
+                                  steal_permille=steal)
+        r = d.execute_batch(hetm.KERNEL_CACHE, gpu, results=True)
+        cpu = orc.gen_cache_batch(20 + rnd, 1 << 11, 1 << 14, 0.5, 900 if rnd else 0, part=0)
+        _, log = orc.cache_host_run(host, cpu, n_sets, ts_base=ts)
+        ts += cpu.size
+        keep = [d.stream_chunk(c, src_thread=i) for i, c in enumerate(np.array_split(log, 4))]
+        conflict = d.round_verdict()
+        if conflict:
+            d.merge_abort_device(host, optimized=True)
+        else:
+            orc.cache_replay(host, gpu, r.tickets, n_sets, 1024, 16384)
+            d.merge_commit(host)
+            d.merge_wait()
+        d.clear_round()
+        outcomes.append(conflict)
+        assert (d.download(hetm.REPLICA_DEV) == host).all(), rnd
+        del keep
+    if steal == 0:
+        assert not any(outcomes)
+    else:
+        assert all(outcomes)
+
+
+@pytest.mark.slow
+def test_cfg4_cache_full_size(hetm, orc, dev_factory):
+    """BASELINE configs[3] geometry: 2^20 sets x 8 ways (512 MiB of words),
+    a 2^20-transaction SET warm-up then a 2^20 GET/SET 90/10 batch (zipf 0.5)."""
+    n_sets, n = 1 << 20, 1 << 20
+    W = n_sets * 64
+    d = dev_factory(W, rs_gran_bytes=1024)
+    d.register_kernel(hetm.KERNEL_CACHE)
+    init = np.zeros(W, np.uint64)
+    warm = orc.gen_cache_batch(7, n, 1 << 22, 0.5, get_permille=0, part=1)
+    r = d.execute_batch(hetm.KERNEL_CACHE, warm, results=True)
+    ref = check_cache_replay(hetm, orc, d, warm, r, init, n_sets)
+    d.clear_round()
+    txs = orc.gen_cache_batch(8, n, 1 << 22, 0.5, get_permille=900, part=1)
+    r = d.execute_batch(hetm.KERNEL_CACHE, txs, results=True)
+    check_cache_replay(hetm, orc, d, txs, r, ref, n_sets)
+
+
 # ------------------------------------------------------------ shard router
 def test_route_log_partitions_stably(hetm, dev_factory):
     torch = pytest.importorskip("torch")

@@ -126,6 +126,43 @@ def test_zipf_bank_batch_distinct_and_hot():
     assert (acct == 100).any(axis=1).mean() > 0.1  # rank 1 is hot
 
 
+def test_cache_lru_matches_independent_model():
+    """within one set the evicted way is always the least recently
+    touched -- the oracle's stamp-based LRU vs a recency-list model."""
+    n_sets, n = 4, 3000
+    txs = O.gen_cache_batch(5, n, 200, alpha=0.3, get_permille=600, part=1)
+    stmr = np.zeros(n_sets * 64, np.uint64)
+    res, log = O.cache_host_run(stmr, txs, n_sets, ts_base=0)
+    sets = {}  # set -> list of (key, value) with most recent last, <= 8 entries
+    for i, t in enumerate(txs):
+        key = (int(t["key"][0]), int(t["key"][1]))
+        s = int(O.lib.orc_cache_set_of(key[0], key[1], n_sets))
+        lst = sets.setdefault(s, [])
+        idx = next((j for j, (k, _) in enumerate(lst) if k == key), None)
+        if t["op"] == 0:
+            if idx is None:
+                assert res[i]["status"] == 0
+            else:
+                assert res[i]["status"] == 1 and tuple(res[i]["value"]) == lst[idx][1]
+                lst.append(lst.pop(idx))
+        else:
+            val = tuple(int(x) for x in t["value"])
+            if idx is not None:
+                assert res[i]["status"] == 2
+                lst.pop(idx)
+            elif len(lst) < 8:
+                assert res[i]["status"] == 3
+            else:
+                assert res[i]["status"] == 4
+                lst.pop(0)  # least recently touched
+            lst.append((key, val))
+    assert (res["status"] == 4).sum() > 100  # evictions exercised
+    # the host write log replays to the same region
+    again = np.zeros_like(stmr)
+    O.apply_log_ts_order(again, log)
+    assert (again == stmr).all()
+
+
 # --------------------------------------------------- SPEC.md examples (KATs)
 def _rs(nbits, bits):
     w = np.zeros(O.words_for_bits(nbits), np.uint64)
