@@ -1,0 +1,170 @@
+// engine.hpp — the SHeTM round controller on the host (SPEC.md:314-433,
+// engine.runRound), header-only C++20 over the C-ABI.
+//
+// One synchronization round (call stack SURVEY.md §3 (1)):
+//   EXECUTION   the GPU-controller thread runs one device batch
+//               (hetm_dev_execute_batch) while host worker threads run
+//               transactions on the host replica through HostStm; their
+//               commit callbacks append to the per-thread WriteLog.  The
+//               streamer (the calling thread) ships every full chunk of a
+//               thread's log over PCIe as it fills (hetm_dev_stream_chunk,
+//               VALIDATE_ONLY = early validation) and stops
+//               the host early when the device reports a conflict.
+//   VALIDATION  host cut-off, the log tail streamed in APPLY mode, the early
+//               chunks re-validated and applied (hetm_dev_apply_log), verdict.
+//   MERGE       no conflict: mergeCommit (device write set -> host replica);
+//               conflict: FavorHost mergeAbortDevice.
+// Chunk buffers are pinned (hetm_host_alloc) and stay valid until the verdict.
+#pragma once
+
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hetm_b200/capi.h"
+#include "hetm_b200/host_tm.hpp"
+
+namespace hetm::b200 {
+
+struct EngineConfig {
+    uint64_t chunk_entries = 1u << 16;  // entries per streamed LogChunk
+    bool early_validation = true;       // stream chunks VALIDATE_ONLY during execution
+    bool optimized_abort = true;        // mergeAbortDevice: shadow + log (true) or chunk copy (false)
+    bool keep_round_log = false;        // keep a copy of the last round's host log (checkers)
+};
+
+struct RoundReport {
+    bool conflict = false;
+    bool cut_short = false;         // early validation ended the execution phase
+    uint64_t host_commits = 0;
+    uint64_t dev_committed = 0;
+    uint64_t log_entries = 0;
+    uint64_t chunks = 0;
+    double exec_ms = 0, validate_ms = 0, merge_ms = 0;
+    hetm_batch_stats batch{};
+};
+
+inline void check_rc(int rc, const char* what) {
+    if (rc != HETM_OK) throw std::runtime_error(std::string(what) + ": " + hetm_strerror(rc));
+}
+
+class Engine {
+public:
+    Engine(hetm_dev* dev, HostStm& stm, WriteLog& log, uint64_t* host_replica, EngineConfig cfg = {})
+        : dev_(dev), stm_(stm), log_(log), host_(host_replica), cfg_(cfg), shipped_(log.threads(), 0) {}
+    ~Engine() {
+        for (void* p : pool_) hetm_host_free(p);
+    }
+
+    /// Host worker: run transactions until `stop` is set or its work ends;
+    /// returns the number it committed.
+    using HostWorker = std::function<uint64_t(int thread, const std::atomic<bool>& stop)>;
+
+    RoundReport runRound(int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx, uint64_t* tickets_out,
+                         const HostWorker& worker) {
+        RoundReport rep;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::atomic<bool> stop{false}, gpu_done{false};
+        int gpu_rc = HETM_OK;
+        // ---- EXECUTION
+        std::thread gpu([&] {  // GPU-controller
+            gpu_rc = hetm_dev_execute_batch(dev_, kernel_id, inputs, rec_bytes, n_tx, tickets_out, &rep.batch);
+            gpu_done.store(true, std::memory_order_release);
+        });
+        std::vector<std::thread> hosts;
+        std::vector<uint64_t> commits(log_.threads(), 0);
+        for (int t = 0; t < log_.threads(); ++t)
+            hosts.emplace_back([&, t] { commits[t] = worker(t, stop); });
+        while (!gpu_done.load(std::memory_order_acquire)) {
+            stream_full_chunks(cfg_.early_validation ? HETM_VALIDATE_ONLY : HETM_APPLY, rep);
+            int c = 0;
+            if (cfg_.early_validation && hetm_dev_poll_conflict(dev_, &c) == HETM_OK && c) {
+                rep.cut_short = true;  // a conflict already dooms the device's round
+                break;
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+        stop.store(true, std::memory_order_release);  // host cut-off
+        for (auto& h : hosts) h.join();
+        gpu.join();
+        check_rc(gpu_rc, "executeBatch");
+        for (uint64_t c : commits) rep.host_commits += c;
+        rep.dev_committed = rep.batch.committed;
+        const auto t1 = std::chrono::steady_clock::now();
+        // ---- VALIDATION: the log tail in APPLY mode, early chunks re-validated + applied
+        stream_full_chunks(HETM_APPLY, rep);
+        stream_tail(rep);
+        check_rc(hetm_dev_apply_log(dev_), "apply_log");
+        int conflict = 0;
+        check_rc(hetm_dev_round_verdict(dev_, &conflict), "round_verdict");
+        rep.conflict = conflict != 0;
+        const auto t2 = std::chrono::steady_clock::now();
+        // ---- MERGE (FavorHost)
+        if (rep.conflict) {
+            check_rc(hetm_dev_merge_abort_device(dev_, cfg_.optimized_abort ? 1 : 0, host_, nullptr),
+                     "merge_abort_device");
+        } else {
+            check_rc(hetm_dev_merge_commit(dev_, host_, nullptr), "merge_commit");
+            check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
+        }
+        check_rc(hetm_dev_clear_round(dev_, 0), "clear_round");
+        if (cfg_.keep_round_log) last_log_ = log_.allEntries();
+        log_.clearRound();
+        std::fill(shipped_.begin(), shipped_.end(), 0);
+        used_ = 0;
+        const auto t3 = std::chrono::steady_clock::now();
+        rep.exec_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        rep.validate_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+        rep.merge_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
+        return rep;
+    }
+
+    /// The last round's host log in WriteLog::allEntries order (keep_round_log).
+    const std::vector<hetm_log_entry>& lastRoundLog() const { return last_log_; }
+
+private:
+    hetm_log_entry* chunk_buffer() {
+        if (used_ == pool_.size()) {
+            void* p = nullptr;
+            check_rc(hetm_host_alloc(cfg_.chunk_entries * sizeof(hetm_log_entry), &p), "host_alloc");
+            pool_.push_back(p);
+        }
+        return static_cast<hetm_log_entry*>(pool_[used_++]);
+    }
+    void ship(int t, uint64_t n, int mode, RoundReport& rep) {
+        hetm_log_entry* buf = chunk_buffer();
+        const uint64_t got = log_.slice(t, shipped_[t], shipped_[t] + n, buf);
+        check_rc(hetm_dev_stream_chunk(dev_, buf, got, t, seq_++, mode), "stream_chunk");
+        shipped_[t] += got;
+        rep.log_entries += got;
+        ++rep.chunks;
+    }
+    void stream_full_chunks(int mode, RoundReport& rep) {
+        for (int t = 0; t < log_.threads(); ++t)
+            while (log_.entryCount(t) - shipped_[t] >= cfg_.chunk_entries) ship(t, cfg_.chunk_entries, mode, rep);
+    }
+    void stream_tail(RoundReport& rep) {
+        for (int t = 0; t < log_.threads(); ++t) {
+            const uint64_t left = log_.entryCount(t) - shipped_[t];
+            if (left) ship(t, left, HETM_APPLY, rep);
+        }
+    }
+
+    hetm_dev* dev_;
+    HostStm& stm_;
+    WriteLog& log_;
+    uint64_t* host_;
+    EngineConfig cfg_;
+    std::vector<uint64_t> shipped_;
+    std::vector<void*> pool_;
+    std::size_t used_ = 0;
+    uint64_t seq_ = 0;
+    std::vector<hetm_log_entry> last_log_;
+};
+
+}  // namespace hetm::b200

@@ -183,7 +183,11 @@ struct hetm_dev {
         v.wlog_slots = wlog_slots;
         return v;
     }
-    void record(int dir, int tag, uint64_t bytes) { xfer.push_back(hetm_transfer_record{dir, tag, bytes}); }
+    std::mutex xfer_mu;  // record() is reached from the GPU-controller and the log streamer threads
+    void record(int dir, int tag, uint64_t bytes) {
+        std::lock_guard<std::mutex> g(xfer_mu);
+        xfer.push_back(hetm_transfer_record{dir, tag, bytes});
+    }
 };
 
 namespace {
