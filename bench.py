@@ -296,7 +296,7 @@ def run_ours(args):
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic("bank_batch_kernel"),
                      "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                      "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms},
-        "validate_apply": {"kernel": "validate_kernel<apply>", "gbs_algorithmic": val_gbs,
+        "validate_apply": {"kernel": "apply_kernel", "gbs_algorithmic": val_gbs,
                            "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
                            "log_gbs_per_gpu": 24 * (n_val / K / world) / (val_ms * 1e-3) / 1e9,
                            "frac": val_gbs / peak, "algorithmic_bytes_per_entry": ENTRY_BYTES,
