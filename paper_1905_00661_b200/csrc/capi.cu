@@ -1305,7 +1305,7 @@ int hetm_dev_route_log_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n,
                             uint64_t shard_words, hetm_log_entry* d_out, uint64_t* d_counts, void* stream) {
     if (!d || (n && (!d_in || !d_out)) || !d_counts) return HETM_ERR_INVALID_ARG;
     if (n_shards == 0 || n_shards > 64 || shard_words == 0) return HETM_ERR_CONFIG;
-    const size_t need = route_log_scratch_bytes(n, n_shards);
+    const size_t need = route_log_scratch_bytes(n, n_shards, d->geom);
     if (need > d->route_cap) {
         if (d->d_route) { CK(d, cudaDeviceSynchronize()); cudaFree(d->d_route); }
         int rc = dev_alloc(d, &d->d_route, need);
@@ -1314,7 +1314,8 @@ int hetm_dev_route_log_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n,
     }
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
     cudaError_t e = launch_route_log(d_in, n, n_shards, shard_words, d_out,
-                                     reinterpret_cast<unsigned long long*>(d_counts), d->d_route, d->route_cap, s);
+                                     reinterpret_cast<unsigned long long*>(d_counts), d->d_route, d->route_cap,
+                                     d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "route_log");
     return HETM_OK;
 }

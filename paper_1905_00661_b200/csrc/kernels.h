@@ -71,8 +71,8 @@ cudaError_t launch_or_words(unsigned long long* dst, const unsigned long long* s
 // Shard router: stable partition of entries by owner = addr / shard_words.
 cudaError_t launch_route_log(const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards, uint64_t shard_words,
                              hetm_log_entry* d_out, unsigned long long* d_counts, void* d_scratch,
-                             size_t scratch_bytes, cudaStream_t s);
-size_t route_log_scratch_bytes(uint64_t n, uint32_t n_shards);
+                             size_t scratch_bytes, const LaunchGeom& g, cudaStream_t s);
+size_t route_log_scratch_bytes(uint64_t n, uint32_t n_shards, const LaunchGeom& g);
 
 int query_geom(LaunchGeom* g, int device);
 

@@ -3,63 +3,109 @@
 // Shard s owns global words [s*shard_words, (s+1)*shard_words).  The router
 // stable-partitions a log buffer by owner shard so the buckets can be sent
 // all-to-all (NCCL over NVLink) and validated/applied locally by the owner.
-// Three launches: per-CTA counts -> one-CTA scan -> in-order ballot scatter.
+//
+// Warp-granular counting sort, no block-level barriers on the data path:
+//   1. count   — every warp owns a contiguous slice of the log and counts its
+//                entries per shard (one ballot per shard per 32 entries);
+//                counts are stored shard-major: [shard][warp]
+//   2. scan    — ONE exclusive prefix sum over that flattened array is the
+//                output offset of every (shard, warp) run (single CTA)
+//   3. scatter — each warp re-reads its slice and writes every entry to
+//                base[shard] + its rank among the warp's entries of that
+//                shard; lane s keeps the running base of shard s (s < 64)
+// Stable (input order within a shard is kept), streaming: 24 B read twice,
+// 24 B written once per entry.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace hetm_b200 {
 
 constexpr int kRouteThreads = 256;
-constexpr int kRouteGrid = 592;  // 4 CTAs per SM on 148 SMs; each CTA owns one contiguous range
+constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxShards = 64;
+constexpr int kScanThreads = 1024;
 
 __device__ __forceinline__ uint32_t owner_of(uint64_t addr, uint64_t shard_words, uint32_t n_shards) {
     uint64_t s = addr / shard_words;
     return (uint32_t)(s < n_shards ? s : n_shards - 1);
 }
 
-__global__ void route_count_kernel(const hetm_log_entry* __restrict__ in, uint64_t n, uint32_t nsh,
-                                   uint64_t shard_words, unsigned long long* counts) {
-    __shared__ unsigned long long c[kMaxShards];
-    for (uint32_t s = threadIdx.x; s < nsh; s += blockDim.x) c[s] = 0;
-    __syncthreads();
-    const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
-        atomicAdd(&c[owner_of(__ldg(&in[i].addr), shard_words, nsh)], 1ull);
-    __syncthreads();
-    for (uint32_t s = threadIdx.x; s < nsh; s += blockDim.x) counts[(uint64_t)blockIdx.x * nsh + s] = c[s];
+__device__ __forceinline__ void warp_slice(uint64_t n, uint64_t n_warps, uint64_t w, uint64_t& lo, uint64_t& hi) {
+    lo = n * w / n_warps;
+    hi = n * (w + 1) / n_warps;
 }
 
-// offsets[b*nsh+s] = sum_{s'<s} total[s'] + sum_{b'<b} counts[b'][s]
-__global__ void route_scan_kernel(const unsigned long long* counts, uint32_t grid, uint32_t nsh,
-                                  unsigned long long* offsets, unsigned long long* totals) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    unsigned long long run = 0;
-    for (uint32_t s = 0; s < nsh; ++s) {
-        unsigned long long start = run;
-        for (uint32_t b = 0; b < grid; ++b) {
-            offsets[(uint64_t)b * nsh + s] = run;
-            run += counts[(uint64_t)b * nsh + s];
+__global__ void __launch_bounds__(kRouteThreads) route_count_kernel(const hetm_log_entry* __restrict__ in, uint64_t n,
+                                                                    uint32_t nsh, uint64_t shard_words,
+                                                                    unsigned long long* __restrict__ counts) {
+    const uint64_t n_warps = (uint64_t)gridDim.x * kRouteWarps;
+    const uint64_t w = (uint64_t)blockIdx.x * kRouteWarps + (threadIdx.x >> 5);
+    const unsigned lane = lane_id();
+    uint64_t lo, hi;
+    warp_slice(n, n_warps, w, lo, hi);
+    unsigned long long c0 = 0, c1 = 0;  // lane L counts shard L and shard L+32
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t s = i < hi ? owner_of(__ldg(&in[i].addr), shard_words, nsh) : 0xffffffffu;
+        for (uint32_t sh = 0; sh < nsh; ++sh) {
+            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
+            if (lane == (sh & 31)) {
+                if (sh < 32) c0 += __popc(m);
+                else c1 += __popc(m);
+            }
         }
-        totals[s] = run - start;
+    }
+    if (lane < nsh) counts[(uint64_t)lane * n_warps + w] = c0;
+    if (lane + 32 < nsh) counts[(uint64_t)(lane + 32) * n_warps + w] = c1;
+}
+
+// Exclusive prefix sum of m values (one CTA): offsets[k] = sum_{j<k} counts[j];
+// totals[s] = sum of shard s's segment [s*n_warps, (s+1)*n_warps).
+__global__ void __launch_bounds__(kScanThreads) route_scan_kernel(const unsigned long long* __restrict__ counts,
+                                                                  uint64_t n_warps, uint32_t nsh,
+                                                                  unsigned long long* __restrict__ offsets,
+                                                                  unsigned long long* __restrict__ totals) {
+    __shared__ unsigned long long part[kScanThreads];
+    const uint64_t m = n_warps * nsh;
+    const uint64_t lo = m * threadIdx.x / kScanThreads, hi = m * (threadIdx.x + 1) / kScanThreads;
+    unsigned long long sum = 0;
+    for (uint64_t k = lo; k < hi; ++k) sum += counts[k];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int d = 1; d < kScanThreads; d <<= 1) {  // Hillis-Steele inclusive scan of the partial sums
+        const unsigned long long x = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0ull;
+        __syncthreads();
+        part[threadIdx.x] += x;
+        __syncthreads();
+    }
+    unsigned long long run = part[threadIdx.x] - sum;
+    for (uint64_t k = lo; k < hi; ++k) {
+        offsets[k] = run;
+        run += counts[k];
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < nsh; s += kScanThreads) {
+        const unsigned long long start = offsets[(uint64_t)s * n_warps];
+        const unsigned long long end =
+            s + 1 < nsh ? offsets[(uint64_t)(s + 1) * n_warps] : offsets[m - 1] + counts[m - 1];
+        totals[s] = end - start;
     }
 }
 
 __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm_log_entry* __restrict__ in, uint64_t n,
                                                                       uint32_t nsh, uint64_t shard_words,
-                                                                      const unsigned long long* offsets,
+                                                                      const unsigned long long* __restrict__ offsets,
                                                                       hetm_log_entry* __restrict__ out) {
-    constexpr int kWarps = kRouteThreads / 32;
-    __shared__ unsigned long long base[kMaxShards];
-    __shared__ unsigned warp_cnt[kWarps][kMaxShards];
-    __shared__ unsigned warp_pre[kWarps][kMaxShards];
-    __shared__ unsigned tile_tot[kMaxShards];
-    for (uint32_t s = threadIdx.x; s < nsh; s += blockDim.x) base[s] = offsets[(uint64_t)blockIdx.x * nsh + s];
-    __syncthreads();
-    const uint64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
-    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-    for (uint64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
-        const uint64_t i = t0 + threadIdx.x;
+    const uint64_t n_warps = (uint64_t)gridDim.x * kRouteWarps;
+    const uint64_t w = (uint64_t)blockIdx.x * kRouteWarps + (threadIdx.x >> 5);
+    const unsigned lane = lane_id();
+    uint64_t lo, hi;
+    warp_slice(n, n_warps, w, lo, hi);
+    unsigned long long b0 = lane < nsh ? offsets[(uint64_t)lane * n_warps + w] : 0;
+    unsigned long long b1 = lane + 32 < nsh ? offsets[(uint64_t)(lane + 32) * n_warps + w] : 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+        const uint64_t i = i0 + lane;
         const bool valid = i < hi;
         hetm_log_entry e{};
         uint32_t s = 0xffffffffu;
@@ -67,43 +113,45 @@ __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm
             e = in[i];
             s = owner_of(e.addr, shard_words, nsh);
         }
-        unsigned my_rank = 0;
+        unsigned rank = 0;
+        const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
+        const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
         for (uint32_t sh = 0; sh < nsh; ++sh) {
-            unsigned m = __ballot_sync(0xffffffffu, s == sh);
-            if (s == sh) my_rank = __popc(m & ((1u << lane) - 1u));
-            if (lane == 0) warp_cnt[warp][sh] = __popc(m);
-        }
-        __syncthreads();
-        for (uint32_t sh = threadIdx.x; sh < nsh; sh += blockDim.x) {
-            unsigned run = 0;
-            for (int w = 0; w < kWarps; ++w) {
-                warp_pre[w][sh] = run;
-                run += warp_cnt[w][sh];
+            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
+            if (s == sh) rank = __popc(m & lt);
+            if (lane == (sh & 31)) {
+                if (sh < 32) b0 += __popc(m);
+                else b1 += __popc(m);
             }
-            tile_tot[sh] = run;
         }
-        __syncthreads();
-        if (valid) out[base[s] + warp_pre[warp][s] + my_rank] = e;
-        __syncthreads();
-        for (uint32_t sh = threadIdx.x; sh < nsh; sh += blockDim.x) base[sh] += tile_tot[sh];
-        __syncthreads();
+        if (valid) out[(s < 32 ? my0 : my1) + rank] = e;
     }
 }
 
-size_t route_log_scratch_bytes(uint64_t, uint32_t n_shards) {
-    return 2ull * kRouteGrid * n_shards * sizeof(unsigned long long);
+// Up to 8 CTAs per SM; small logs get fewer warps (>= 512 entries per warp) so
+// the single-CTA scan over [shard][warp] stays short.
+static unsigned route_grid(uint64_t n, const LaunchGeom& g) {
+    const uint64_t want = (n + kRouteThreads * 16 - 1) / (kRouteThreads * 16);
+    const uint64_t cap = (uint64_t)g.sm_count * 8u;
+    return (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+size_t route_log_scratch_bytes(uint64_t n, uint32_t n_shards, const LaunchGeom& g) {
+    return 2ull * route_grid(n, g) * kRouteWarps * n_shards * sizeof(unsigned long long);
 }
 
 cudaError_t launch_route_log(const hetm_log_entry* d_in, uint64_t n, uint32_t nsh, uint64_t shard_words,
                              hetm_log_entry* d_out, unsigned long long* d_counts, void* d_scratch, size_t scratch_bytes,
-                             cudaStream_t s) {
+                             const LaunchGeom& g, cudaStream_t s) {
     if (nsh == 0 || nsh > kMaxShards || shard_words == 0) return cudaErrorInvalidValue;
-    if (scratch_bytes < route_log_scratch_bytes(n, nsh)) return cudaErrorInvalidValue;
+    if (scratch_bytes < route_log_scratch_bytes(n, nsh, g)) return cudaErrorInvalidValue;
+    const unsigned grid = route_grid(n, g);
+    const uint64_t n_warps = (uint64_t)grid * kRouteWarps;
     auto* counts = static_cast<unsigned long long*>(d_scratch);
-    auto* offsets = counts + (size_t)kRouteGrid * nsh;
-    route_count_kernel<<<kRouteGrid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, counts);
-    route_scan_kernel<<<1, 32, 0, s>>>(counts, kRouteGrid, nsh, offsets, d_counts);
-    route_scatter_kernel<<<kRouteGrid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, offsets, d_out);
+    auto* offsets = counts + n_warps * nsh;
+    route_count_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, counts);
+    route_scan_kernel<<<1, kScanThreads, 0, s>>>(counts, n_warps, nsh, offsets, d_counts);
+    route_scatter_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, offsets, d_out);
     return cudaGetLastError();
 }
 

@@ -732,11 +732,12 @@ def test_cfg4_cache_full_size(hetm, orc, dev_factory):
 
 
 # ------------------------------------------------------------ shard router
-def test_route_log_partitions_stably(hetm, dev_factory):
+@pytest.mark.parametrize("n,G", [(100003, 8), (5, 3), (70001, 40), (1 << 20, 64), (4097, 1)])
+def test_route_log_partitions_stably(hetm, dev_factory, n, G):
     torch = pytest.importorskip("torch")
     d = dev_factory(1024)
-    rng = np.random.default_rng(4)
-    n, G, sw = 100003, 8, 1 << 20
+    rng = np.random.default_rng(n + G)
+    sw = 1 << 20
     log = random_log(rng, n, G * sw)
     src = torch.from_numpy(log.view(np.uint64).reshape(-1).astype(np.int64)).cuda()
     dst = torch.empty_like(src)
