@@ -288,7 +288,7 @@ def run_ours(args):
                         "uniform, RS/WS gran 1 KiB; round host log 2^20 entries on the host halves, "
                         "validated+applied (routed by owner shard over NCCL when G>1)",
             "stmr_words_per_gpu": W, "batch_tx": B, "log_entries_per_gpu": L, "rs_gran_bytes": args.gran,
-            "stmr_layout": "32-B word cells {value, lock, ts, spare}", "parallelism": f"shard{world}",
+            "stmr_layout": "16-B word cells {value, lock-or-TS}", "parallelism": f"shard{world}",
             "l2": "inputs larger than L2: 1 GiB STMR per GPU, rotating per-step input buffers "
                   f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
         },

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
             continue;
         }
         Cell* set = v.cells + s0;
-        unsigned long long* lockp = &set[0].lock;
+        unsigned long long* lockp = &set[0].meta;
         const bool is_get = r.op == HETM_CACHE_GET;
         for (uint32_t attempt = 1;; ++attempt) {
             // ---- P1
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
                         for (int q = 0; q < 4; ++q) st_relaxed(&way[kVal + q].value, r.value[q]);
                     }
                     st_relaxed(&way[kLru].value, t + 1);
-                    st_release(lockp, lk_make(0, (uint32_t)(t + 1)));
+                    st_release(lockp, lk_commit(t));
                 }
             } else if (ok) {  // read-only GET miss: ticket, then validate the set lock
                 t = take_ticket(&ctr->ticket);

@@ -688,7 +688,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     if (!d || (!inputs && n_tx)) return HETM_ERR_INVALID_ARG;
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
     if (rec_bytes != record_bytes(kernel_id)) return HETM_ERR_INVALID_SIZE;
-    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;  // priorities are 31-bit
+    if (n_tx >= (1ull << 30)) return HETM_ERR_INVALID_SIZE;  // priorities are 30-bit
     if (results_out && (kernel_id != HETM_KERNEL_CACHE || res_bytes != sizeof(hetm_cache_result)))
         return HETM_ERR_INVALID_SIZE;
     int rc;
@@ -1075,11 +1075,9 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
             e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, false,
                                     d->geom, d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "restore(rollback)");
-        e = launch_winner_apply(d->d_cells, nullptr, d->base, d->W, d->d_arena, d->arena_n, d->geom, d->s_merge);
-        if (e == cudaSuccess)
-            e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
+        e = launch_rollback_reapply(d->view(), d->d_shadow, d->d_arena, d->arena_n, d->d_ctr, d->d_restore, d->geom,
                                     d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "winner_apply(rollback)");
+        if (e != cudaSuccess) return fail(d, e, "rollback_reapply");
         d->record(HETM_D2D, HETM_TAG_ROLLBACK, dirty_bytes);
         s.bytes_d2d = dirty_bytes;
         CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
@@ -1176,8 +1174,10 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
         CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
         cudaError_t e = launch_roll_round(d->d_ctr, (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, s);
         if (e != cudaSuccess) return fail(d, e, "roll_round");
-        if (flags & HETM_CLEAR_RESET_TS)
-            CK(d, cudaMemset2DAsync(&d->d_cells[0].ts, sizeof(Cell), 0, sizeof(unsigned long long), d->W, s));
+        if (flags & HETM_CLEAR_RESET_TS) {
+            cudaError_t er = launch_reset_ts(d->d_cells, d->W, d->geom, s);
+            if (er != cudaSuccess) return fail(d, er, "reset_ts");
+        }
         CK(d, cudaEventRecord(d->ev_round, s));
         d->arena_n = 0;
         d->deferred.clear();
@@ -1198,8 +1198,10 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
     CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
     CK(d, cudaMemsetAsync(&d->d_ctr->conflict, 0, 3 * sizeof(unsigned), s));
-    if (flags & HETM_CLEAR_RESET_TS)
-        CK(d, cudaMemset2DAsync(&d->d_cells[0].ts, sizeof(Cell), 0, sizeof(unsigned long long), d->W, s));
+    if (flags & HETM_CLEAR_RESET_TS) {
+        cudaError_t er = launch_reset_ts(d->d_cells, d->W, d->geom, s);
+        if (er != cudaSuccess) return fail(d, er, "reset_ts");
+    }
     CK(d, cudaEventRecord(d->ev_round, s));
     d->h_ctr->conflict = 0;
     d->arena_n = 0;
@@ -1237,7 +1239,7 @@ int hetm_dev_execute_batch_dptr(hetm_dev* d, int kernel_id, const void* d_inputs
                                 void* stream) {
     if (!d || (n_tx && (!d_inputs || !d_tickets))) return HETM_ERR_INVALID_ARG;
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
-    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;
+    if (n_tx >= (1ull << 30)) return HETM_ERR_INVALID_SIZE;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
     return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), nullptr, s);
 }
@@ -1246,7 +1248,7 @@ int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inp
                                    uint64_t* d_tickets, void* d_results, void* stream) {
     if (!d || (n_tx && (!d_inputs || !d_tickets))) return HETM_ERR_INVALID_ARG;
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
-    if (n_tx >= (1ull << 31)) return HETM_ERR_INVALID_SIZE;
+    if (n_tx >= (1ull << 30)) return HETM_ERR_INVALID_SIZE;
     if (d_results && kernel_id != HETM_KERNEL_CACHE) return HETM_ERR_INVALID_SIZE;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
     return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), d_results,

@@ -1,14 +1,19 @@
 // common.cuh — HBM layout and sm_100a memory-model helpers for the HeTM kernels.
 //
-// Device replica layout: one 32-byte WORD CELL per STMR word,
-//     { value, lock, ts, spare }            (one 32-B L2/DRAM sector)
+// Device replica layout: one 16-byte WORD CELL per STMR word,
+//     { value, meta }                       (two cells per 32-B sector)
 // so every per-word operation of the hot path touches exactly one sector:
-//   * the batch TM reads {value, lock} with one 128-bit single-copy-atomic
+//   * the batch TM reads {value, meta} with one 128-bit single-copy-atomic
 //     load and commits {new value, unlocked new version} with one 128-bit
 //     store (no separate lock table, no fence between write-back and release);
-//   * validation raises `ts` (the TsArray entry) with a
-//     fire-and-forget REDG.E.MAX.64 and stores the winning value in the same
-//     sector.
+//   * validation raises the TsArray entry held in `meta`
+//     and stores the winning value in the same sector.
+// `meta` is the batch TM's versioned lock word between validation phases and
+// the word's TS after a host write was applied to it (device_tm.cuh):
+//     FINAL(63) | 0 | owner(61..32) | version(31..0)    lock / version word
+//     0 | TS-tag(62) | host ts(61..0)                    TS word (unlocked)
+// The two never coexist in time: validation/apply never overlaps a batch,
+// and a batch treats a TS word as an unlocked word of one reserved version.
 // The raw-op / merge boundary still sees a plain array of 64-bit words
 // (SPEC.md:78): gather/scatter kernels convert at the edge, and devShadow is a
 // plain word array so dirty chunks DMA straight to the host replica.
@@ -20,13 +25,15 @@
 
 namespace hetm_b200 {
 
-struct alignas(32) Cell {
+struct alignas(16) Cell {
     uint64_t value;           // the STMR word (devReplica)
-    unsigned long long lock;  // batch-TM versioned lock (device_tm.cuh)
-    unsigned long long ts;    // TsArray: freshest host ts applied (monotone, never reset)
-    uint64_t spare;
+    unsigned long long meta;  // versioned lock word, or TS-tag | ts
 };
-static_assert(sizeof(Cell) == 32, "one cell per 32-B sector");
+static_assert(sizeof(Cell) == 16, "two cells per 32-B sector");
+
+constexpr unsigned long long kTsTag = 1ull << 62;
+// meta of a word whose freshest applied host write has timestamp ts
+__host__ __device__ __forceinline__ unsigned long long ts_meta(uint64_t ts) { return kTsTag | ts; }
 
 // Capacity of the apply kernel's restore queue (entries); overflow falls back
 // to a full winner pass over the launch.

@@ -4,10 +4,13 @@
 // CUDA thread runs one transaction; every transaction eventually commits or
 // reports livelock.
 //
-// Per-word versioned lock, stored in the word's cell (common.cuh):
+// Per-word versioned lock, the `meta` word of the word's cell (common.cuh):
 //     bit 63      FINAL  — write-back in progress, never stolen
-//     bits 62..32 owner  — priority of the pre-lock holder (0 = free)
-//     bits 31..0  version — low 32 bits of the last committing ticket + 1
+//     bits 61..32 owner  — priority of the pre-lock holder (0 = free)
+//     bits 31..0  version — low 31 bits of the last committing ticket + 1
+// A TS word (bit 62, left by validation) reads as an unlocked word of the
+// reserved version 0xffffffff, which no commit produces (commit versions are
+// 31-bit), so a value change is always a version change (no ABA).
 // Priority rule (PR-STM): priority = batch index + 1, smaller wins.  A
 // transaction may steal a lower-priority PRE-lock; the robbed transaction
 // fails its finalize step and retries.  The highest-priority live transaction
@@ -34,10 +37,18 @@ namespace hetm_b200 {
 
 constexpr unsigned long long kLockFinal = 1ull << 63;
 
-__device__ __forceinline__ uint32_t lk_owner(unsigned long long l) { return (uint32_t)(l >> 32) & 0x7fffffffu; }
-__device__ __forceinline__ uint32_t lk_ver(unsigned long long l) { return (uint32_t)l; }
+constexpr uint32_t kTsVersion = 0xffffffffu;  // version a TS word reads as
+
+__device__ __forceinline__ uint32_t lk_owner(unsigned long long l) {
+    return (l & kTsTag) ? 0u : (uint32_t)(l >> 32) & 0x3fffffffu;
+}
+__device__ __forceinline__ uint32_t lk_ver(unsigned long long l) { return (l & kTsTag) ? kTsVersion : (uint32_t)l; }
 __device__ __forceinline__ unsigned long long lk_make(uint32_t owner, uint32_t ver) {
     return ((unsigned long long)owner << 32) | ver;
+}
+// unlocked word published by the commit holding ticket t
+__device__ __forceinline__ unsigned long long lk_commit(unsigned long long t) {
+    return lk_make(0, (uint32_t)((t + 1) & 0x7fffffffull));
 }
 
 template <int R, int W>
@@ -139,7 +150,7 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
     int held = 0;
     bool ok = true;
     for (int k = 0; k < nwl && ok; ++k) {
-        unsigned long long* lw = &v.cells[wl[k]].lock;
+        unsigned long long* lw = &v.cells[wl[k]].meta;
         unsigned long long cur = ld_relaxed(lw);
         for (;;) {
             if ((cur & kLockFinal) || lk_ver(cur) != wver[k]) { ok = false; break; }
@@ -151,7 +162,7 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
         }
     }
     if (!ok) {
-        for (int k = 0; k < held; ++k) atomicCAS(&v.cells[wl[k]].lock, lk_make(me, wver[k]), lk_make(0, wver[k]));
+        for (int k = 0; k < held; ++k) atomicCAS(&v.cells[wl[k]].meta, lk_make(me, wver[k]), lk_make(0, wver[k]));
         return false;
     }
     // 3. commit ticket
@@ -165,7 +176,7 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
         bool written = false;
         for (int q = 0; q < nwl; ++q) written |= (wl[q] == tx.r_local[k]);
         if (written) continue;
-        unsigned long long* lw = &v.cells[tx.r_local[k]].lock;
+        unsigned long long* lw = &v.cells[tx.r_local[k]].meta;
         unsigned long long cur = ld_relaxed(lw);
         for (;;) {
             if (lk_ver(cur) != tx.r_ver[k]) { ok = false; break; }
@@ -191,22 +202,21 @@ __device__ __forceinline__ bool tm_commit(DeviceTx<R, W>& tx, const ShardView& v
     if (ok) {
         for (; fin < nwl; ++fin) {
             const unsigned long long exp = lk_make(me, wver[fin]);
-            if (atomicCAS(&v.cells[wl[fin]].lock, exp, exp | kLockFinal) != exp) { ok = false; break; }
+            if (atomicCAS(&v.cells[wl[fin]].meta, exp, exp | kLockFinal) != exp) { ok = false; break; }
         }
     }
     if (!ok) {
         for (int k = 0; k < nwl; ++k) {
-            unsigned long long* lw = &v.cells[wl[k]].lock;
+            unsigned long long* lw = &v.cells[wl[k]].meta;
             if (k < fin) st_relaxed(lw, lk_make(0, wver[k]));  // held FINAL, nothing written
             else atomicCAS(lw, lk_make(me, wver[k]), lk_make(0, wver[k]));
         }
-        for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].lock, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
+        for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].meta, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
         return false;
     }
     // 6. write back + release: one 128-bit store per written word
-    const uint32_t nv = (uint32_t)(t + 1);
-    for (int k = 0; k < nwl; ++k) st_pair(&v.cells[wl[k]], wv[k], lk_make(0, nv));
-    for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].lock, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
+    for (int k = 0; k < nwl; ++k) st_pair(&v.cells[wl[k]], wv[k], lk_commit(t));
+    for (int s = 0; s < ns; ++s) atomicCAS(&v.cells[st_loc[s]].meta, lk_make(me, st_ver[s]), lk_make(0, st_ver[s]));
     ticket = t;
     return true;
 }

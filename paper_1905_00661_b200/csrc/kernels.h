@@ -38,6 +38,12 @@ cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t
 // kRestoreCap entries, and rely on the previous launch's stores being complete).
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
                             DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
+// Optimized rollback: untag the logged words, re-apply the round log, copy them to shadow.
+cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
+                                    DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g,
+                                    cudaStream_t s);
+// Literal TS reset: every TS word becomes an unlocked word.
+cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Round boundary: ts_floor = max(ts_floor, round_max_ts) (0 with reset_ts), round_max_ts = 0.
 cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s);
 // Winner store of the round's log: value of the entry whose ts equals the

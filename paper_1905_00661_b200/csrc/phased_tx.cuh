@@ -76,10 +76,9 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 // Diagnostics only (HETM_KNOCKOUT env var, 0 in production): KO_PROTOCOL
 // keeps the snapshot loads and stores and drops every protocol step (the
 // access-pattern floor); KO_PHASE_CLOCKS accumulates per-phase cycles.
-// KO_COUNT_TICKETS counts ticket atomics (debug word 4); KO_STRIPED_TICKET
-// draws tickets from per-CTA counters (breaks the serial order: timing only).
+// KO_COUNT_TICKETS counts ticket atomics (debug word 4).
 enum : int {
-    KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_STRIPED_TICKET = 32, KO_PROTOCOL = 64,
+    KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_PROTOCOL = 64,
     KO_PHASE_CLOCKS = 128
 };
 
@@ -107,7 +106,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], tx.l[k]);
-            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
+            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].meta);
         }
         compute(tx);
 #pragma unroll
@@ -121,7 +120,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], tx.l[k]);
-            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
+            else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].meta);
         }
         unsigned long long pr[NR + 2 * NW];
         if constexpr ((KO & (KO_NO_PROBE | KO_BITMAPS)) != 0) {
@@ -166,7 +165,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int j = 0; j < NW; ++j)
             if (tx.first & (1u << j))
-                prev[j] = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
+                prev[j] = atomicCAS(&v.cells[tx.loc[j]].meta, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
 #pragma unroll
         for (int j = 0; j < NW; ++j) held[j] = (tx.first & (1u << j)) && prev[j] == tx.l[j];
 #pragma unroll
@@ -184,16 +183,16 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
                     ok = false;
                     break;
                 }
-                c = ld_relaxed(&v.cells[tx.loc[j]].lock);
+                c = ld_relaxed(&v.cells[tx.loc[j]].meta);
                 if (c == tx.l[j])
-                    c = atomicCAS(&v.cells[tx.loc[j]].lock, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
+                    c = atomicCAS(&v.cells[tx.loc[j]].meta, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
             }
             held[j] = c == tx.l[j];
         }
         if (!ok) {
 #pragma unroll
             for (int j = 0; j < NW; ++j)
-                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].lock, tx.l[j]);  // nothing written: restore
+                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].meta, tx.l[j]);  // nothing written: restore
         }
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 1, tclk);
@@ -202,11 +201,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     // a lower-priority holder of this very warp, so no full-warp collective
     // may separate lock acquisition from release.
     unsigned long long t = ~0ull;  // no ticket
-    if constexpr ((KO & KO_STRIPED_TICKET) != 0) {
-        if (ok) t = take_ticket(reinterpret_cast<unsigned long long*>(&v.cells[((uint64_t)blockIdx.x * 7919u) % v.size_words].spare));
-    } else {
-        if (ok) t = take_ticket(ticket_ctr);
-    }
+    if (ok) t = take_ticket(ticket_ctr);
     if constexpr ((KO & KO_COUNT_TICKETS) != 0) {
         if (ok && lane_id() == (unsigned)(__ffs(__activemask()) - 1)) clocks[0] += 1;
     }
@@ -221,7 +216,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
             for (int q = 0; q < NW; ++q) mine |= (tx.loc[q] == tx.loc[k]);
             check[k] = !mine && (tx.first & (1u << k));
-            if (check[k]) cur[k] = ld_relaxed(&v.cells[tx.loc[k]].lock);
+            if (check[k]) cur[k] = ld_relaxed(&v.cells[tx.loc[k]].meta);
         }
 #pragma unroll
         for (int k = NW; k < NR; ++k) {
@@ -235,13 +230,13 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
                     tx.block_loc = tx.loc[k];
                     tx.block_lk = c;
                 }
-                else c = ld_relaxed(&v.cells[tx.loc[k]].lock);                // lower priority: wait
+                else c = ld_relaxed(&v.cells[tx.loc[k]].meta);                // lower priority: wait
             }
         }
         if (!ok) {
 #pragma unroll
             for (int j = 0; j < NW; ++j)
-                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].lock, tx.l[j]);
+                if (held[j]) st_relaxed(&v.cells[tx.loc[j]].meta, tx.l[j]);
         }
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 3, tclk);
@@ -251,7 +246,6 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     }
     // ---- P5: write back + release in one 128-bit store per distinct written word
     compute(tx);
-    const uint32_t nv = (uint32_t)(t + 1);
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
         if (!held[j]) continue;
@@ -259,7 +253,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int q = j + 1; q < NW; ++q)
             if (tx.loc[q] == tx.loc[j]) val = tx.wval[q];  // the last write to a word wins
-        st_pair(&v.cells[tx.loc[j]], val, lk_make(0, nv));
+        st_pair(&v.cells[tx.loc[j]], val, lk_commit(t));
     }
 #pragma unroll
     for (int k = 0; k < NR; ++k)

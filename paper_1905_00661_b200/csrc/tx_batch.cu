@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             ++aborts;
             if (tx.block_lk) {  // wait for the FINAL holder to release, then retry
                 uint32_t ns = 32;
-                for (int p = 0; p < 256 && ld_relaxed(&v.cells[tx.block_loc].lock) == tx.block_lk; ++p) {
+                for (int p = 0; p < 256 && ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk; ++p) {
                     __nanosleep(ns);
                     ns = ns < 1024 ? 2 * ns : ns;
                 }
@@ -203,7 +203,7 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
     switch (ko) {
-        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(32) HETM_KO_CASE(64) HETM_KO_CASE(128)
+        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(64) HETM_KO_CASE(128)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE

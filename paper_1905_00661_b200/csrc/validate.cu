@@ -42,7 +42,7 @@ struct PassAFlags {
     unsigned long long maxts = 0;
 };
 
-template <bool kApply>
+// RS test of one entry (validate-only pass; the apply pass inlines it).
 __device__ __forceinline__ void pass_a(const ShardView& v, const EntryRegs& e, uint64_t ts_floor, PassAFlags& f) {
     const uint64_t loc = e.addr - v.base;
     if (loc >= v.size_words) {
@@ -53,7 +53,6 @@ __device__ __forceinline__ void pass_a(const ShardView& v, const EntryRegs& e, u
     f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
     f.bad |= (e.ts <= ts_floor);
     f.maxts = e.ts > f.maxts ? e.ts : f.maxts;
-    if (kApply) atomicMax(&v.cells[loc].ts, (unsigned long long)e.ts);  // (b) pass A
 }
 
 __device__ __forceinline__ void flush_pass_a(PassAFlags f, DevCounters* ctr) {
@@ -74,7 +73,6 @@ __device__ __forceinline__ void flush_pass_a(PassAFlags f, DevCounters* ctr) {
     }
 }
 
-template <bool kApply>
 __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
                                                                uint64_t n, DevCounters* ctr) {
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
@@ -89,7 +87,7 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, cons
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-            if (i0 + (uint64_t)u * blockDim.x < n) pass_a<kApply>(v, e[u], ts_floor, f);
+            if (i0 + (uint64_t)u * blockDim.x < n) pass_a(v, e[u], ts_floor, f);
     }
     flush_pass_a(f, ctr);
 }
@@ -132,13 +130,13 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, const h
             f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
             f.bad |= (e[u].ts <= ts_floor);
             f.maxts = e[u].ts > f.maxts ? e[u].ts : f.maxts;
-            old[u] = atomicMax(&v.cells[loc].ts, (unsigned long long)e[u].ts);  // (b) TS raise
+            old[u] = atomicMax(&v.cells[loc].meta, ts_meta(e[u].ts));  // (b) TS raise (a lock word < any TS word)
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (old[u] >= e[u].ts) continue;  // lost, out of shard, or past the end
+            if (old[u] >= ts_meta(e[u].ts)) continue;  // lost, out of shard, or past the end
             v.cells[e[u].addr - v.base].value = e[u].value;
-            if (old[u] > ts_floor) {  // raced with another entry of this round: re-store later
+            if ((old[u] & kTsTag) && (old[u] & ~kTsTag) > ts_floor) {  // raced with an entry of this round
                 const unsigned long long k = atomicAdd(&ctr->restore_n, 1ull);
                 if (k < kRestoreCap) restore[k] = i0 + (uint64_t)u * blockDim.x;
             }
@@ -160,7 +158,7 @@ __global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, const
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x) {
         const EntryRegs e = load_entry(log, full ? j : restore[j]);
         const uint64_t loc = e.addr - v.base;
-        if (loc < v.size_words && ld_relaxed(&v.cells[loc].ts) == e.ts) v.cells[loc].value = e.value;
+        if (loc < v.size_words && ld_relaxed(&v.cells[loc].meta) == ts_meta(e.ts)) v.cells[loc].value = e.value;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -190,11 +188,11 @@ __global__ void __launch_bounds__(kValThreads) winner_kernel(Cell* cells, uint64
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t loc = e[u].addr - base;
-            cur[u] = loc < size_words ? ld_relaxed(&cells[loc].ts) : ~0ull;
+            cur[u] = loc < size_words ? ld_relaxed(&cells[loc].meta) : ~0ull;
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            if (cur[u] != e[u].ts) continue;
+            if (cur[u] != ts_meta(e[u].ts)) continue;
             const uint64_t loc = e[u].addr - base;
             if (dst) dst[loc] = e[u].value;
             else cells[loc].value = e[u].value;
@@ -222,6 +220,38 @@ static unsigned grid_cap(uint64_t items, int threads, const LaunchGeom& g, int p
     return (unsigned)(want ? want : 1);
 }
 
+// Rollback helpers (optimized mergeAbortDevice) and the literal
+// TS reset.  0x00000000ffffffff is the unlocked reserved-version
+// word a TS word reads as (device_tm.cuh), so the batch TM sees no change.
+constexpr unsigned long long kUntagged = 0xffffffffull;
+
+__global__ void untag_log_kernel(Cell* cells, uint64_t base, uint64_t size_words,
+                                 const hetm_log_entry* __restrict__ log, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t loc = __ldg(&log[i].addr) - base;
+        if (loc < size_words) cells[loc].meta = kUntagged;
+    }
+}
+
+__global__ void log_to_shadow_kernel(uint64_t* shadow, const Cell* __restrict__ cells, uint64_t base,
+                                     uint64_t size_words, const hetm_log_entry* __restrict__ log, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t loc = __ldg(&log[i].addr) - base;
+        if (loc < size_words) shadow[loc] = cells[loc].value;
+    }
+}
+
+__global__ void reset_ts_kernel(Cell* cells, uint64_t size_words) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size_words;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (cells[i].meta & kTsTag) cells[i].meta = kUntagged;
+}
+
+cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
+    reset_ts_kernel<<<(unsigned)g.sm_count * 8u, kValThreads, 0, s>>>(cells, size_words);
+    return cudaGetLastError();
+}
+
 // Round boundary on the device: ts_floor = max(ts_floor, round_max_ts) (or 0
 // for the literal SPEC.md:421 TS reset), round_max_ts = 0.  Enqueued by both
 // the synchronous and the asynchronous clear so pipelined rounds keep an exact
@@ -244,7 +274,7 @@ cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uin
     if (n == 0) return cudaSuccess;
     const unsigned grid = grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
     if (!apply) {
-        validate_kernel<false><<<grid, kValThreads, 0, s>>>(v, d_log, n, ctr);
+        validate_kernel<<<grid, kValThreads, 0, s>>>(v, d_log, n, ctr);
         return cudaGetLastError();
     }
     static const int apply_bps = [] {  // tuning experiments only: resident blocks per SM for apply
@@ -264,6 +294,22 @@ cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uin
     else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
     else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
     restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
+    return cudaGetLastError();
+}
+
+// Clean re-apply of the round log onto the device replica whose device write
+// set was restored from devShadow: forget this round's TS words (a batch that
+// ran after an earlier apply may have replaced some), apply the whole log
+// again (apply + restore kernels), copy the logged words to devShadow.
+cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
+                                    DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g,
+                                    cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = grid_cap(n, kValThreads, g, 8);
+    untag_log_kernel<<<grid, kValThreads, 0, s>>>(v.cells, v.base, v.size_words, d_log, n);
+    cudaError_t e = launch_validate(v, d_log, n, 1, ctr, d_restore, g, s);
+    if (e != cudaSuccess) return e;
+    if (shadow) log_to_shadow_kernel<<<grid, kValThreads, 0, s>>>(shadow, v.cells, v.base, v.size_words, d_log, n);
     return cudaGetLastError();
 }
 
@@ -293,7 +339,7 @@ cudaError_t launch_or_words(unsigned long long* dst, const unsigned long long* s
 
 int query_val_occupancy(int* blocks) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, validate_kernel<true>, kValThreads, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, validate_kernel, kValThreads, 0) != cudaSuccess)
         return -1;
     *blocks = b;
     return 0;
