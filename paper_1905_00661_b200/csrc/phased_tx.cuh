@@ -79,7 +79,7 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 // KO_COUNT_TICKETS counts ticket atomics (debug word 4).
 enum : int {
     KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_PROTOCOL = 64,
-    KO_PHASE_CLOCKS = 128
+    KO_PHASE_CLOCKS = 128, KO_LOCK_READS = 256, KO_SKIP_VALIDATE = 512, KO_NO_TICKET = 1024
 };
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
@@ -156,20 +156,23 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 0, tclk);
-    // ---- P2: lock the distinct written words (unlocked version -> FINAL)
-    bool held[NW];
+    // ---- P2: lock the distinct written words (unlocked version -> FINAL);
+    // with kLockReads the read-only words too (2PL: no validation phase)
+    constexpr bool kLockReads = (KO & KO_LOCK_READS) != 0;
+    constexpr int NL = kLockReads ? NR : NW;  // words locked in P2
+    bool held[NL];
 #pragma unroll
-    for (int j = 0; j < NW; ++j) held[j] = false;
+    for (int j = 0; j < NL; ++j) held[j] = false;
     if (ok) {
-        unsigned long long prev[NW];
+        unsigned long long prev[NL];
 #pragma unroll
-        for (int j = 0; j < NW; ++j)
+        for (int j = 0; j < NL; ++j)
             if (tx.first & (1u << j))
                 prev[j] = atomicCAS(&v.cells[tx.loc[j]].meta, tx.l[j], kLockFinal | lk_make(me, lk_ver(tx.l[j])));
 #pragma unroll
-        for (int j = 0; j < NW; ++j) held[j] = (tx.first & (1u << j)) && prev[j] == tx.l[j];
+        for (int j = 0; j < NL; ++j) held[j] = (tx.first & (1u << j)) && prev[j] == tx.l[j];
 #pragma unroll
-        for (int j = 0; j < NW; ++j) {
+        for (int j = 0; j < NL; ++j) {
             if (!(tx.first & (1u << j)) || held[j] || !ok) continue;
             unsigned long long c = prev[j];
             // Lost the race: wait for a LOWER-priority holder to commit or back
@@ -191,7 +194,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
         if (!ok) {
 #pragma unroll
-            for (int j = 0; j < NW; ++j)
+            for (int j = 0; j < NL; ++j)
                 if (held[j]) st_relaxed(&v.cells[tx.loc[j]].meta, tx.l[j]);  // nothing written: restore
         }
     }
@@ -201,13 +204,17 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
     // a lower-priority holder of this very warp, so no full-warp collective
     // may separate lock acquisition from release.
     unsigned long long t = ~0ull;  // no ticket
-    if (ok) t = take_ticket(ticket_ctr);
+    if constexpr ((KO & KO_NO_TICKET) != 0) {
+        if (ok) t = me;
+    } else {
+        if (ok) t = take_ticket(ticket_ctr);
+    }
     if constexpr ((KO & KO_COUNT_TICKETS) != 0) {
         if (ok && lane_id() == (unsigned)(__ffs(__activemask()) - 1)) clocks[0] += 1;
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 2, tclk);
-    // ---- P4: validate the read-only words
-    if (ok) {
+    // ---- P4: validate the read-only words (not needed when they are locked)
+    if (!kLockReads && (KO & KO_SKIP_VALIDATE) == 0 && ok) {
         unsigned long long cur[NR];
         bool check[NR];
 #pragma unroll
@@ -235,7 +242,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         }
         if (!ok) {
 #pragma unroll
-            for (int j = 0; j < NW; ++j)
+            for (int j = 0; j < NL; ++j)
                 if (held[j]) st_relaxed(&v.cells[tx.loc[j]].meta, tx.l[j]);
         }
     }
@@ -255,6 +262,9 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
             if (tx.loc[q] == tx.loc[j]) val = tx.wval[q];  // the last write to a word wins
         st_pair(&v.cells[tx.loc[j]], val, lk_commit(t));
     }
+#pragma unroll
+    for (int j = NW; j < NL; ++j)  // read-only words locked in P2: release, version unchanged
+        if (held[j]) st_relaxed(&v.cells[tx.loc[j]].meta, tx.l[j]);
 #pragma unroll
     for (int k = 0; k < NR; ++k)
         if ((need_bits >> k) & 1u) set_bit(v.rs, tx.loc[k] >> v.gran_shift);

@@ -199,11 +199,15 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         const char* e = std::getenv("HETM_KNOCKOUT");  // profiling experiments only
         return e ? std::atoi(e) : 0;
     }();
-    const unsigned grid = grid_for(n, kTxThreads, g.max_blocks_tx, g.sm_count);
+    static const int bps = [] {  // occupancy experiments only
+        const char* e = std::getenv("HETM_TX_BLOCKS_PER_SM");
+        return e ? std::atoi(e) : 0;
+    }();
+    const unsigned grid = grid_for(n, kTxThreads, bps > 0 ? bps : g.max_blocks_tx, g.sm_count);
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
     switch (ko) {
-        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(64) HETM_KO_CASE(128)
+        HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(64) HETM_KO_CASE(128) HETM_KO_CASE(256) HETM_KO_CASE(512) HETM_KO_CASE(1024) HETM_KO_CASE(1536)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
 #undef HETM_KO_CASE

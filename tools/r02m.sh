@@ -1,0 +1,2 @@
+for ko in 0 256 0 256; do HETM_KNOCKOUT=$ko timeout 120 python tools/probe_r02.py bank; done
+HETM_KNOCKOUT=256 timeout 600 python -m pytest tests -m gpu -x -q -k "bank or cfg2 or cfg3 or rounds or merge" 2>&1 | tail -3
