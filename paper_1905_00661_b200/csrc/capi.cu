@@ -14,8 +14,10 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -23,6 +25,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "common.cuh"
 #include "device_tm.cuh"
@@ -139,9 +143,10 @@ struct hetm_dev {
     size_t flush_bytes = 0;
     unsigned flush_gen = 0;
 
-    cudaStream_t s_exec = nullptr, s_copy = nullptr, s_val = nullptr, s_merge = nullptr, s_d2h = nullptr;
+    cudaStream_t s_exec = nullptr, s_copy = nullptr, s_val = nullptr, s_merge = nullptr, s_d2h = nullptr,
+                 s_zc = nullptr;  // s_zc: zero-copy delta stores into the host replica
     cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
-                ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+                ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_copy_zc = nullptr;
     bool intake_open = true;
     bool shadow_synced = true;   // devShadow == devReplica as of the round start
     bool round_applied = false;  // some APPLY validation touched devReplica this round
@@ -528,9 +533,9 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     CK(d, cudaMemset(d->d_chunk, 0, d->chunk_words * 8));
     CK(d, cudaMemset(d->d_ctr, 0, sizeof(DevCounters)));
 
-    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h})
+    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc})
         CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h})
+    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc})
         CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CK(d, cudaEventCreate(&d->ev_t0));
     CK(d, cudaEventCreate(&d->ev_t1));
@@ -562,7 +567,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
 int hetm_dev_close(hetm_dev* d) {
     if (!d) return HETM_ERR_INVALID_ARG;
     cudaSetDevice(d->device);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc})
         if (s) cudaStreamSynchronize(s);
     d->pool.reset();
     if (d->h_delta) cudaFreeHost(d->h_delta);
@@ -578,9 +583,10 @@ int hetm_dev_close(hetm_dev* d) {
             cudaEventDestroy(pr.second);
         }
     for (cudaEvent_t e : d->tpool) cudaEventDestroy(e);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc})
         if (s) cudaStreamDestroy(s);
-    for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1})
+    for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1,
+                          d->ev_copy_zc})
         if (e) cudaEventDestroy(e);
     delete d;
     return HETM_OK;
@@ -905,7 +911,7 @@ constexpr uint64_t kDeltaPiece = 1ull << 17;  // delta records per D2H piece (2 
 // host replica ends identical to the chunk copy: the words outside the device
 // write set inside a dirty chunk already hold the host's values (the round
 // committed, so no host entry touched a device-read word).
-int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots) {
+int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* bytes_d2h) {
     if (d->pool) d->pool->wait();
     if (n_slots > d->delta_cap) {
         CK(d, cudaStreamSynchronize(d->s_d2h));
@@ -948,26 +954,54 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots) {
     }
     CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
     CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
+    // Split: the first n_zc sorted records are stored into the host replica by
+    // the GPU itself (zero-copy PCIe writes, s_merge) while the copy engine and
+    // the host workers deliver the rest — two independent paths into host DRAM.
+    static const double zc_frac = [] {
+        const char* e = std::getenv("HETM_ZC_FRACTION");
+        return e ? std::atof(e) : 0.5;  // measured best split (profiles/r01_e2e_zc_split.txt)
+    }();
+    uint64_t n_zc = 0;
+    cudaPointerAttributes pa{};
+    if (zc_frac > 0 && cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer) {
+        n_zc = std::min<uint64_t>(n_slots, (uint64_t)(zc_frac * (double)n_slots)) / kDeltaPiece * kDeltaPiece;
+        if (n_zc) {
+            CK(d, cudaStreamWaitEvent(d->s_zc, d->ev_shadow, 0));
+            cudaError_t ez = launch_delta_zc_scatter(static_cast<uint64_t*>(pa.devicePointer), d->d_delta, n_zc,
+                                                     d->geom, d->s_zc);
+            if (ez != cudaSuccess) return fail(d, ez, "delta_zc_scatter");
+            d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, n_zc * 8);
+        }
+    } else {
+        cudaGetLastError();
+    }
     const uint64_t pieces = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
     while (d->piece_ev.size() < pieces) {
         cudaEvent_t ev = nullptr;
         CK(d, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         d->piece_ev.push_back(ev);
     }
-    for (uint64_t k = 0; k < pieces; ++k) {
+    const uint64_t k0 = n_zc / kDeltaPiece;  // pieces already delivered by the zero-copy kernel
+    for (uint64_t k = k0; k < pieces; ++k) {
         const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
         CK(d, cudaMemcpyAsync(d->h_delta + lo, d->d_delta + lo, m * sizeof(DeltaRec), cudaMemcpyDeviceToHost, d->s_d2h));
         CK(d, cudaEventRecord(d->piece_ev[k], d->s_d2h));
     }
-    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, n_slots * sizeof(DeltaRec));
+    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_slots - n_zc) * sizeof(DeltaRec));
+    *bytes_d2h = n_zc * 8 + (n_slots - n_zc) * sizeof(DeltaRec);
+    if (n_zc) {  // the merge is complete when both paths are
+        CK(d, cudaEventRecord(d->ev_copy_zc, d->s_zc));
+        CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_copy_zc, 0));
+    }
     CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
     d->d2h_pending = true;
     const DeltaRec* src = d->h_delta;
     const std::vector<cudaEvent_t> evs(d->piece_ev.begin(), d->piece_ev.begin() + pieces);
     const int dev = d->device;
-    d->pool->start([src, evs, host, n_slots, dev](int w, int nw) {
+    d->pool->start([src, evs, host, n_slots, dev, k0](int w, int nw) {
         cudaSetDevice(dev);
-        for (uint64_t k = 0; k < evs.size(); ++k) {
+        for (uint64_t k = k0; k < evs.size(); ++k) {
             cudaEventSynchronize(evs[k]);
             const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
             const uint64_t a = lo + m * w / nw, b = lo + m * (w + 1) / nw;
@@ -1001,12 +1035,13 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && !d->h_ctr->wlog_overflow &&
                        n_slots <= d->wlog_slots && n_slots * sizeof(DeltaRec) < dirty_bytes;
     if (delta) {
-        if ((rc = merge_commit_delta(d, host, n_slots))) return rc;
+        uint64_t moved = 0;
+        if ((rc = merge_commit_delta(d, host, n_slots, &moved))) return rc;
         if (st) {
             std::memset(st, 0, sizeof(*st));
             st->dirty_chunks = nd;
             st->transfers = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
-            st->bytes_d2h = n_slots * sizeof(DeltaRec);
+            st->bytes_d2h = moved;
             st->bytes_d2d = d->d_shadow ? n_slots * 8 : 0;
             st->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         }
@@ -1377,8 +1412,37 @@ int hetm_dev_flush_l2(hetm_dev* d, void* stream) {
 }
 
 // ------------------------------------------------------------------ host side
+// Large pinned host buffers (host replica, delta landing zones) are backed by
+// 2 MiB transparent huge pages when the kernel allows it (madvise mode): the
+// delta merge scatters ~10^6 words per round into the host replica, and 4 KiB
+// pages make every write a TLB miss.
+namespace {
+std::mutex g_host_mu;
+std::map<void*, std::pair<void*, size_t>> g_host_maps;  // aligned ptr -> (mmap base, mmap length)
+constexpr size_t kHuge = 2ull << 20;
+}  // namespace
+
 int hetm_host_alloc(uint64_t bytes, void** p) {
     if (!p) return HETM_ERR_INVALID_ARG;
+    *p = nullptr;
+    if (bytes >= 2 * kHuge) {
+        const size_t len = (bytes + kHuge - 1) / kHuge * kHuge + kHuge;
+        void* base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (base != MAP_FAILED) {
+            void* al = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(base) + kHuge - 1) & ~(uintptr_t)(kHuge - 1));
+            madvise(al, len - kHuge, MADV_HUGEPAGE);
+            const cudaError_t e = cudaHostRegister(al, len - kHuge, cudaHostRegisterPortable);
+            if (e == cudaSuccess) {
+                std::lock_guard<std::mutex> g(g_host_mu);
+                g_host_maps[al] = {base, len};
+                *p = al;
+                return HETM_OK;
+            }
+            cudaGetLastError();
+            munmap(base, len);
+            if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return HETM_ERR_NO_DEVICE;
+        }
+    }
     cudaError_t e = cudaHostAlloc(p, bytes ? bytes : 8, cudaHostAllocPortable);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1389,7 +1453,18 @@ int hetm_host_alloc(uint64_t bytes, void** p) {
 }
 
 int hetm_host_free(void* p) {
-    if (p) cudaFreeHost(p);
+    if (!p) return HETM_OK;
+    {
+        std::lock_guard<std::mutex> g(g_host_mu);
+        auto it = g_host_maps.find(p);
+        if (it != g_host_maps.end()) {
+            cudaHostUnregister(p);
+            munmap(it->second.first, it->second.second);
+            g_host_maps.erase(it);
+            return HETM_OK;
+        }
+    }
+    cudaFreeHost(p);
     return HETM_OK;
 }
 

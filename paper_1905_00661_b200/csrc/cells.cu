@@ -66,6 +66,16 @@ __global__ void wlog_restore_kernel(Cell* __restrict__ cells, const uint64_t* __
     }
 }
 
+// The first part of the sorted delta goes straight into the (mapped, pinned)
+// host replica as zero-copy PCIe stores, concurrently with the DMA + host
+// scatter of the rest.
+__global__ void delta_zc_scatter_kernel(uint64_t* host, const DeltaRec* __restrict__ d, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const DeltaRec r = d[i];
+        if (r.loc != ~0ull) host[r.loc] = r.value;
+    }
+}
+
 static unsigned grid_words(uint64_t n, const LaunchGeom& g) {
     uint64_t want = (n + 255) / 256;
     const uint64_t cap = (uint64_t)g.sm_count * 16;
@@ -121,6 +131,13 @@ cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint3
                                 uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     wlog_restore_kernel<<<grid_words(n, g), 256, 0, s>>>(cells, shadow, wlog, n, size_words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
+                                    cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    delta_zc_scatter_kernel<<<(unsigned)g.sm_count * 4u, 256, 0, s>>>(host_dev, d, n);
     return cudaGetLastError();
 }
 

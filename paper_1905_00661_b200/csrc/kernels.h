@@ -66,6 +66,9 @@ cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cell
 // Rollback of the device write set: cells[loc].value = shadow[loc] per log slot.
 cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
                                 uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
+// Zero-copy scatter of delta records into a device-accessible host buffer.
+cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
+                                    cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
