@@ -13,13 +13,21 @@
 //   VALIDATION  host cut-off, the log tail streamed in APPLY mode, the early
 //               chunks re-validated and applied (hetm_dev_apply_log), verdict.
 //   MERGE       no conflict: mergeCommit (device write set -> host replica);
-//               conflict: FavorHost mergeAbortDevice.
+//               conflict: FavorHost mergeAbortDevice, or
+//               FavorDevice mergeAbortHost: every chunk is
+//               validate-only until the verdict, the host replica is restored
+//               from the round-start snapshot and takes the device's chunks.
+// Starvation guard: under FavorHost, after starvation_k
+// consecutive DeviceAborted rounds the next round admits only read-only host
+// transactions (RoundContext::updates_allowed), so the device commits.
 // Chunk buffers are pinned (hetm_host_alloc) and stay valid until the verdict.
 #pragma once
 
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -31,7 +39,12 @@
 
 namespace hetm::b200 {
 
+enum class Policy { FavorHost, FavorDevice };  // PolicyConfig.mode
+enum class Outcome { Commit, DeviceAborted, HostAborted };
+
 struct EngineConfig {
+    Policy policy = Policy::FavorHost;
+    uint32_t starvation_k = 3;          // PolicyConfig.starvationK (>= 1)
     uint64_t chunk_entries = 1u << 16;  // entries per streamed LogChunk
     bool early_validation = true;       // stream chunks VALIDATE_ONLY during execution
     bool optimized_abort = true;        // mergeAbortDevice: shadow + log (true) or chunk copy (false)
@@ -39,6 +52,9 @@ struct EngineConfig {
 };
 
 struct RoundReport {
+    uint64_t round_id = 0;
+    Outcome outcome = Outcome::Commit;
+    bool updates_allowed = true;    // false: starvation-guard round (read-only host)
     bool conflict = false;
     bool cut_short = false;         // early validation ended the execution phase
     uint64_t host_commits = 0;
@@ -47,6 +63,29 @@ struct RoundReport {
     uint64_t chunks = 0;
     double exec_ms = 0, validate_ms = 0, merge_ms = 0;
     hetm_batch_stats batch{};
+
+    /// Round stats in a fixed field order (External Interfaces).
+    std::string json() const {
+        static const char* names[] = {"Commit", "DeviceAborted", "HostAborted"};
+        char buf[512];
+        std::snprintf(buf, sizeof buf,
+                      "{\"roundId\": %llu, \"outcome\": \"%s\", \"txCommittedHost\": %llu, "
+                      "\"txCommittedDev\": %llu, \"txWastedDev\": %llu, \"bytesLogs\": %llu, \"readOnlyHost\": %d, "
+                      "\"cutShort\": %d, \"execMs\": %.3f, \"validateMs\": %.3f, \"mergeMs\": %.3f}",
+                      (unsigned long long)round_id, names[(int)outcome],
+                      (unsigned long long)(outcome == Outcome::HostAborted ? 0 : host_commits),
+                      (unsigned long long)(outcome == Outcome::DeviceAborted ? 0 : dev_committed),
+                      (unsigned long long)(outcome == Outcome::DeviceAborted ? dev_committed : 0),
+                      (unsigned long long)(log_entries * sizeof(hetm_log_entry)), (int)!updates_allowed,
+                      (int)cut_short, exec_ms, validate_ms, merge_ms);
+        return buf;
+    }
+};
+
+/// What a host worker sees of the round.
+struct RoundContext {
+    const std::atomic<bool>& stop;  // host cut-off / early-validation stop
+    bool updates_allowed;           // false under the starvation guard: read-only transactions only
 };
 
 inline void check_rc(int rc, const char* what) {
@@ -56,20 +95,32 @@ inline void check_rc(int rc, const char* what) {
 class Engine {
 public:
     Engine(hetm_dev* dev, HostStm& stm, WriteLog& log, uint64_t* host_replica, EngineConfig cfg = {})
-        : dev_(dev), stm_(stm), log_(log), host_(host_replica), cfg_(cfg), shipped_(log.threads(), 0) {}
+        : dev_(dev), stm_(stm), log_(log), host_(host_replica), cfg_(cfg), shipped_(log.threads(), 0) {
+        if (cfg_.starvation_k < 1) throw std::invalid_argument("starvationK >= 1 (SPEC.md:332)");
+        if (cfg_.policy == Policy::FavorDevice) snapshot_.resize(stm.sizeWords());
+    }
     ~Engine() {
         for (void* p : pool_) hetm_host_free(p);
     }
 
-    /// Host worker: run transactions until `stop` is set or its work ends;
-    /// returns the number it committed.
-    using HostWorker = std::function<uint64_t(int thread, const std::atomic<bool>& stop)>;
+    /// Host worker: run transactions until ctx.stop is set or its work ends
+    /// (read-only ones when !ctx.updates_allowed); returns how many committed.
+    using HostWorker = std::function<uint64_t(int thread, const RoundContext& ctx)>;
+    uint32_t consecutiveDeviceAborts() const { return dev_aborts_; }
 
     RoundReport runRound(int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx, uint64_t* tickets_out,
                          const HostWorker& worker) {
         RoundReport rep;
+        rep.round_id = round_id_++;
+        const bool favor_device = cfg_.policy == Policy::FavorDevice;
+        // starvation guard (FavorHost): a read-only host round after K device aborts
+        rep.updates_allowed = favor_device || dev_aborts_ < cfg_.starvation_k;
+        // FavorDevice: explicit host snapshot at round start
+        if (favor_device) std::memcpy(snapshot_.data(), host_, snapshot_.size() * sizeof(uint64_t));
+        const int stream_mode = (favor_device || cfg_.early_validation) ? HETM_VALIDATE_ONLY : HETM_APPLY;
         const auto t0 = std::chrono::steady_clock::now();
         std::atomic<bool> stop{false}, gpu_done{false};
+        const RoundContext ctx{stop, rep.updates_allowed};
         int gpu_rc = HETM_OK;
         // ---- EXECUTION
         std::thread gpu([&] {  // GPU-controller
@@ -79,9 +130,9 @@ public:
         std::vector<std::thread> hosts;
         std::vector<uint64_t> commits(log_.threads(), 0);
         for (int t = 0; t < log_.threads(); ++t)
-            hosts.emplace_back([&, t] { commits[t] = worker(t, stop); });
+            hosts.emplace_back([&, t] { commits[t] = worker(t, ctx); });
         while (!gpu_done.load(std::memory_order_acquire)) {
-            stream_full_chunks(cfg_.early_validation ? HETM_VALIDATE_ONLY : HETM_APPLY, rep);
+            stream_full_chunks(stream_mode, rep);
             int c = 0;
             if (cfg_.early_validation && hetm_dev_poll_conflict(dev_, &c) == HETM_OK && c) {
                 rep.cut_short = true;  // a conflict already dooms the device's round
@@ -96,20 +147,34 @@ public:
         for (uint64_t c : commits) rep.host_commits += c;
         rep.dev_committed = rep.batch.committed;
         const auto t1 = std::chrono::steady_clock::now();
-        // ---- VALIDATION: the log tail in APPLY mode, early chunks re-validated + applied
-        stream_full_chunks(HETM_APPLY, rep);
-        stream_tail(rep);
-        check_rc(hetm_dev_apply_log(dev_), "apply_log");
+        // ---- VALIDATION: the log tail (APPLY, or validate-only under FavorDevice),
+        // early chunks re-validated + applied (FavorDevice: only on success)
+        const int tail_mode = favor_device ? HETM_VALIDATE_ONLY : HETM_APPLY;
+        stream_full_chunks(tail_mode, rep);
+        stream_tail(rep, tail_mode);
         int conflict = 0;
+        if (!favor_device) check_rc(hetm_dev_apply_log(dev_), "apply_log");
         check_rc(hetm_dev_round_verdict(dev_, &conflict), "round_verdict");
         rep.conflict = conflict != 0;
+        if (favor_device && !rep.conflict) {
+            check_rc(hetm_dev_apply_log(dev_), "apply_log");
+            check_rc(hetm_dev_round_verdict(dev_, &conflict), "round_verdict");
+        }
         const auto t2 = std::chrono::steady_clock::now();
-        // ---- MERGE (FavorHost)
-        if (rep.conflict) {
+        // ---- MERGE
+        if (!rep.conflict) {
+            rep.outcome = Outcome::Commit;
+            check_rc(hetm_dev_merge_commit(dev_, host_, nullptr), "merge_commit");
+            check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
+            dev_aborts_ = 0;
+        } else if (!favor_device) {
+            rep.outcome = Outcome::DeviceAborted;
             check_rc(hetm_dev_merge_abort_device(dev_, cfg_.optimized_abort ? 1 : 0, host_, nullptr),
                      "merge_abort_device");
+            ++dev_aborts_;
         } else {
-            check_rc(hetm_dev_merge_commit(dev_, host_, nullptr), "merge_commit");
+            rep.outcome = Outcome::HostAborted;
+            check_rc(hetm_dev_merge_abort_host(dev_, host_, snapshot_.data(), nullptr), "merge_abort_host");
             check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
         }
         check_rc(hetm_dev_clear_round(dev_, 0), "clear_round");
@@ -148,10 +213,10 @@ private:
         for (int t = 0; t < log_.threads(); ++t)
             while (log_.entryCount(t) - shipped_[t] >= cfg_.chunk_entries) ship(t, cfg_.chunk_entries, mode, rep);
     }
-    void stream_tail(RoundReport& rep) {
+    void stream_tail(RoundReport& rep, int mode) {
         for (int t = 0; t < log_.threads(); ++t) {
             const uint64_t left = log_.entryCount(t) - shipped_[t];
-            if (left) ship(t, left, HETM_APPLY, rep);
+            if (left) ship(t, left, mode, rep);
         }
     }
 
@@ -165,6 +230,9 @@ private:
     std::size_t used_ = 0;
     uint64_t seq_ = 0;
     std::vector<hetm_log_entry> last_log_;
+    std::vector<uint64_t> snapshot_;  // FavorDevice round-start host snapshot
+    uint64_t round_id_ = 0;
+    uint32_t dev_aborts_ = 0;         // consecutiveDeviceAborts
 };
 
 }  // namespace hetm::b200

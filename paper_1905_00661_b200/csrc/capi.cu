@@ -1149,6 +1149,7 @@ int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snaps
     if (rc) return rc;
     CK(d, cudaStreamSynchronize(d->s_exec));
     CK(d, cudaStreamSynchronize(d->s_val));
+    if (d->pool) d->pool->wait();  // a previous delta merge may still be landing in host_replica
     if (d->d2h_pending) CK(d, cudaStreamSynchronize(d->s_d2h));
     // hostReplica restored from the round-start snapshot
     std::memcpy(host, snapshot, d->W * 8);

@@ -9,8 +9,12 @@
 //   aborted round:   S' = apply_log_ts_order(S, host log)
 // plus host replica == device replica and the bank sum.
 //
-//   round_test [rounds] [log2 words] [batch] [host threads] [conflict every k]
-// Exit 0 = all rounds bit-exact; prints one JSON line with the totals.
+//   round_test [rounds] [log2 words] [batch] [host threads] [conflict every k] [host|device] [starvation k]
+// policy host (FavorHost, default) or device (FavorDevice: a conflicting round
+// is HostAborted, S' = device batch replay on S, host effects discarded).
+// conflict every k = 1 makes every round conflict (starvation-guard test).
+// Exit 0 = all rounds bit-exact; prints one JSON line per round + the totals.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -40,6 +44,8 @@ int main(int argc, char** argv) {
     const uint64_t B = argc > 3 ? std::strtoull(argv[3], nullptr, 10) : (1u << 14);
     const int T = argc > 4 ? std::atoi(argv[4]) : 4;
     const int conflict_every = argc > 5 ? std::atoi(argv[5]) : 3;
+    const bool favor_device = argc > 6 && std::strcmp(argv[6], "device") == 0;
+    const uint32_t starvation_k = argc > 7 ? (uint32_t)std::atoi(argv[7]) : 3;
     const uint64_t W = 1ull << log2w, half = W / 2;
 
     hetm_dev_config cfg;
@@ -68,19 +74,23 @@ int main(int argc, char** argv) {
     EngineConfig ec;
     ec.chunk_entries = 1u << 12;
     ec.keep_round_log = true;
+    ec.policy = favor_device ? Policy::FavorDevice : Policy::FavorHost;
+    ec.starvation_k = starvation_k;
     Engine eng(dev, stm, log, host, ec);
 
     std::vector<uint64_t> ref(host, host + W), dev_words(W), tickets(B), order(B);
     std::vector<orc_bank_tx> txs(B);
-    uint64_t host_total = 0, dev_total = 0, n_conflict = 0, n_cut = 0;
+    uint64_t host_total = 0, dev_total = 0, n_conflict = 0, n_cut = 0, n_guard = 0;
+    uint32_t run_aborts = 0, max_run_aborts = 0;
     bool ok = true;
+    std::vector<uint64_t> start(W);
     for (int r = 0; r < rounds && ok; ++r) {
         const bool steal = conflict_every > 0 && r % conflict_every == conflict_every - 1;
         orc_gen_bank_batch(1000 + r, B, 0, half, txs.data());  // device partition [0, W/2)
         const uint64_t per_thread = 1500;
-        auto worker = [&](int t, const std::atomic<bool>& stop) -> uint64_t {
+        auto worker = [&](int t, const RoundContext& ctx) -> uint64_t {
             uint64_t s = orc_splitmix64(7919u * r + t + 1), done = 0;
-            for (uint64_t k = 0; k < per_thread && !stop.load(std::memory_order_relaxed); ++k) {
+            for (uint64_t k = 0; k < per_thread && !ctx.stop.load(std::memory_order_relaxed); ++k) {
                 uint64_t a[4];
                 for (int j = 0; j < 4; ++j) {
                     s = orc_splitmix64(s);
@@ -95,6 +105,7 @@ int main(int argc, char** argv) {
                     const uint64_t y = TM_read(stm, tx, a[1]);
                     (void)TM_read(stm, tx, a[2]);
                     (void)TM_read(stm, tx, a[3]);
+                    if (!ctx.updates_allowed) return;  // starvation guard: read-only transaction
                     TM_write(stm, tx, a[0], x - amt);
                     TM_write(stm, tx, a[1], y + amt);
                 });
@@ -103,23 +114,25 @@ int main(int argc, char** argv) {
             return done;
         };
         RoundReport rep = eng.runRound(HETM_KERNEL_BANK, txs.data(), sizeof(hetm_bank_tx), B, tickets.data(), worker);
-        host_total += rep.host_commits;
         n_conflict += rep.conflict;
         n_cut += rep.cut_short;
-        if (steal != rep.conflict) {
-            std::printf("round %d: conflict=%d but steal=%d\n", r, (int)rep.conflict, (int)steal);
+        n_guard += !rep.updates_allowed;
+        const bool host_updates = steal && rep.updates_allowed;
+        if (host_updates != rep.conflict) {
+            std::printf("round %d: conflict=%d but steal=%d updates=%d\n", r, (int)rep.conflict, (int)steal,
+                        (int)rep.updates_allowed);
             ok = false;
         }
-        std::printf("{\"round\": %d, \"conflict\": %d, \"cut_short\": %d, \"host_commits\": %llu, \"dev_committed\": %llu, "
-                    "\"log_entries\": %llu, \"chunks\": %llu, \"exec_ms\": %.3f, \"validate_ms\": %.3f, \"merge_ms\": %.3f}\n",
-                    r, (int)rep.conflict, (int)rep.cut_short, (unsigned long long)rep.host_commits,
-                    (unsigned long long)rep.dev_committed, (unsigned long long)rep.log_entries,
-                    (unsigned long long)rep.chunks, rep.exec_ms, rep.validate_ms, rep.merge_ms);
-        if (!rep.conflict) dev_total += rep.dev_committed;
+        std::printf("%s\n", rep.json().c_str());
+        if (rep.outcome != Outcome::HostAborted) host_total += rep.host_commits;
+        if (rep.outcome != Outcome::DeviceAborted) dev_total += rep.dev_committed;
+        run_aborts = rep.outcome == Outcome::DeviceAborted ? run_aborts + 1 : 0;
+        max_run_aborts = std::max(max_run_aborts, run_aborts);
         // exact oracle replay of the round
         const auto& hl = eng.lastRoundLog();
-        orc_apply_log_ts_order(ref.data(), 0, reinterpret_cast<const orc_entry*>(hl.data()), hl.size());
-        if (!rep.conflict) {
+        if (rep.outcome != Outcome::HostAborted)
+            orc_apply_log_ts_order(ref.data(), 0, reinterpret_cast<const orc_entry*>(hl.data()), hl.size());
+        if (rep.outcome != Outcome::DeviceAborted) {
             const uint64_t m = orc_order_by_ticket(tickets.data(), B, order.data());
             orc_bank_replay(ref.data(), 0, txs.data(), order.data(), m, nullptr, nullptr, nullptr, 1024, 16384);
         }
@@ -139,10 +152,16 @@ int main(int argc, char** argv) {
             ok = false;
         }
     }
-    std::printf("{\"rounds\": %d, \"ok\": %d, \"host_commits\": %llu, \"dev_commits\": %llu, \"conflict_rounds\": %llu, "
-                "\"cut_short\": %llu, \"host_aborts\": %llu}\n",
-                rounds, (int)ok, (unsigned long long)host_total, (unsigned long long)dev_total,
-                (unsigned long long)n_conflict, (unsigned long long)n_cut, (unsigned long long)stm.aborts());
+    if (!favor_device && max_run_aborts > starvation_k) {  // device commits within K+1 rounds
+        std::printf("starvation guard failed: %u consecutive device aborts\n", max_run_aborts);
+        ok = false;
+    }
+    std::printf("{\"rounds\": %d, \"ok\": %d, \"policy\": \"%s\", \"host_commits\": %llu, \"dev_commits\": %llu, "
+                "\"conflict_rounds\": %llu, \"cut_short\": %llu, \"guard_rounds\": %llu, \"max_consecutive_device_aborts\": %u, "
+                "\"host_aborts\": %llu}\n",
+                rounds, (int)ok, favor_device ? "FavorDevice" : "FavorHost", (unsigned long long)host_total,
+                (unsigned long long)dev_total, (unsigned long long)n_conflict, (unsigned long long)n_cut,
+                (unsigned long long)n_guard, max_run_aborts, (unsigned long long)stm.aborts());
     hetm_host_free(host);
     hetm_dev_close(dev);
     return ok ? 0 : 1;

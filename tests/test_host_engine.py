@@ -34,7 +34,8 @@ def test_round_controller_refuses_without_device(hetm):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("args", [["6", "20", "16384", "4", "3"], ["4", "22", "65536", "8", "2"]])
+@pytest.mark.parametrize("args", [["6", "20", "16384", "4", "3"], ["4", "22", "65536", "8", "2"],
+                                  ["6", "20", "16384", "4", "2", "device"]])
 def test_live_rounds_match_oracle(args):
     """Host workers commit bank transfers through the host TM while the GPU
     runs a bank batch; the engine streams the log with early validation and
@@ -46,3 +47,15 @@ def test_live_rounds_match_oracle(args):
     summary = json.loads(r.stdout.strip().splitlines()[-1])
     assert summary["ok"] == 1 and summary["conflict_rounds"] >= 1
     assert summary["host_commits"] > 0 and summary["dev_commits"] > 0
+
+
+@pytest.mark.gpu
+def test_starvation_guard_lets_the_device_commit():
+    """an adversarial host that conflicts every round; with
+    starvationK = 3 the device commits at least once in every 4 rounds."""
+    r = subprocess.run([_exe("round_test"), "12", "20", "16384", "4", "1", "host", "3"], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    summary = json.loads(r.stdout.strip().splitlines()[-1])
+    assert summary["ok"] == 1 and summary["guard_rounds"] >= 2
+    assert summary["max_consecutive_device_aborts"] <= 3
