@@ -2,6 +2,8 @@
 // (common.cuh) and plain 64-bit word arrays (devShadow, raw-op staging).
 // Used at the edges only: raw ops, the shadow refresh of
 // mergeCommit and the rollback of mergeAbortDevice.
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -137,7 +139,11 @@ cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint3
 cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
                                     cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    delta_zc_scatter_kernel<<<(unsigned)g.sm_count * 4u, 256, 0, s>>>(host_dev, d, n);
+    static const int zc_blocks = [] {  // tuning experiments only: CTAs of 128 threads per SM
+        const char* e = std::getenv("HETM_ZC_BLOCKS_PER_SM");
+        return e ? std::atoi(e) : 1;
+    }();
+    delta_zc_scatter_kernel<<<(unsigned)(g.sm_count * (zc_blocks > 0 ? zc_blocks : 1)), 128, 0, s>>>(host_dev, d, n);
     return cudaGetLastError();
 }
 
