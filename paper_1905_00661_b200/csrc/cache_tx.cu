@@ -35,6 +35,15 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Two adjacent word cells {value, meta, value, meta} in one 256-bit access
+// (LDG.E.ENL2.256.STRONG.GPU on sm_100a).
+__device__ __forceinline__ void ld_cells2(const Cell* c, uint64_t& v0, uint64_t& v1) {
+    asm volatile("{\n\t.reg .b64 m0, m1;\n\tld.relaxed.gpu.global.v4.u64 {%0, m0, %1, m1}, [%2];\n\t}"
+                 : "=l"(v0), "=l"(v1)
+                 : "l"(c)
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -76,11 +85,9 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
             unsigned long long block = ok ? 0ull : L;
             uint64_t k0[kWays], k1[kWays], lru[kWays], fl[kWays];
 #pragma unroll
-            for (int w = 0; w < kWays; ++w) {
-                k0[w] = ld_relaxed(&set[w * kWayWords + kKey0].value);
-                k1[w] = ld_relaxed(&set[w * kWayWords + kKey1].value);
-                lru[w] = ld_relaxed(&set[w * kWayWords + kLru].value);
-                fl[w] = ld_relaxed(&set[w * kWayWords + kFlags].value);
+            for (int w = 0; w < kWays; ++w) {  // {key0, key1} and {lru, flags}: two 256-bit loads per way
+                ld_cells2(&set[w * kWayWords + kKey0], k0[w], k1[w]);
+                ld_cells2(&set[w * kWayWords + kLru], lru[w], fl[w]);
             }
             int hit = kWays, invalid = kWays, lru_way = 0;
 #pragma unroll
@@ -108,8 +115,8 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
             }
             uint64_t val[4] = {0, 0, 0, 0};
             if (target < kWays) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) val[q] = ld_relaxed(&set[target * kWayWords + kVal + q].value);
+                ld_cells2(&set[target * kWayWords + kVal], val[0], val[1]);
+                ld_cells2(&set[target * kWayWords + kVal + 2], val[2], val[3]);
             }
             // ---- P2 .. P5
             unsigned long long t = ~0ull;
