@@ -135,17 +135,38 @@ def peaks():
 
 # ----------------------------------------------------------- distributed
 def dist_setup(args):
+    """One process per GPU over NCCL.  HETM_BENCH_BACKEND=gloo with
+    HETM_BENCH_ONE_GPU=1 runs the N-rank protocol with every rank on GPU 0
+    (a functional test of the multi-rank path on a single-GPU box)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("HETM_BENCH_ONE_GPU") == "1":
+        local = 0
     pg = None
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HETM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         pg = dist
     return world, rank, local, pg
+
+
+def all_reduce(dist, t, op=None):
+    """all_reduce that also works for a CPU-only backend (gloo test mode)."""
+    import torch
+
+    if os.environ.get("HETM_BENCH_BACKEND", "nccl") == "nccl":
+        dist.all_reduce(t, op=op) if op is not None else dist.all_reduce(t)
+        return t
+    c = t.cpu()
+    dist.all_reduce(c, op=op) if op is not None else dist.all_reduce(c)
+    return c.to(t.device)
 
 
 def host_log_slice(hetm, seed, n_entries, world, W, rank, ts_base):
@@ -164,7 +185,7 @@ def run_ours(args):
     import torch
 
     import paper_1905_00661_b200 as hetm
-    from paper_1905_00661_b200.shard import ShardedValidator
+    from paper_1905_00661_b200.shard import PeerValidator, ShardedValidator
 
     world, rank, local, dist = dist_setup(args)
     torch.cuda.set_device(local)
@@ -205,7 +226,19 @@ def run_ours(args):
     s_val = dev.stream_handle(2)
     ex = torch.cuda.ExternalStream(s_exec)
     vs = torch.cuda.ExternalStream(s_val)
-    sv = ShardedValidator(dev, world, W, L, dist, s_val)
+    exchange = "none (1 shard)"
+    sv = None
+    if world > 1:  # fused router + NVLink delivery into the owners' arenas; NCCL all_to_all as the fallback
+        try:
+            sv = PeerValidator(dev, world, rank, W, L, dist, s_val)
+            exchange = "fused router -> NVLink peer stores (CUDA IPC arenas)"
+        except RuntimeError:
+            sv = None
+    if sv is None:
+        sv = ShardedValidator(dev, world, W, L, dist, s_val)
+        if world > 1:
+            exchange = "router -> NCCL all_to_all"
+
 
     def step(j, timed_idx=None):
         tb = tx_d[j % n_bufs]
@@ -258,13 +291,13 @@ def run_ours(args):
     bt, bc = dev.timing(0)
     vt, vc = dev.timing(1)
     dev.set_timing(False)
-    batch_ms, val_ms = bt / max(bc, 1), vt / max(vc, 1)
+    batch_ms, val_ms = bt / max(bc, 1), vt / K  # validation: all launches of a step (G regions with the peer exchange)
     if dist:
         t = torch.tensor([ms_total, batch_ms, val_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = all_reduce(dist, t, op=dist.ReduceOp.MAX)
         ms_total, batch_ms, val_ms = t.tolist()
         nv = torch.tensor([n_val], dtype=torch.int64, device="cuda")
-        dist.all_reduce(nv)
+        nv = all_reduce(dist, nv)
         n_val = int(nv.item())
 
     # correctness spot check after timing: bank sum preserved on the device
@@ -289,6 +322,7 @@ def run_ours(args):
                         "validated+applied (routed by owner shard over NCCL when G>1)",
             "stmr_words_per_gpu": W, "batch_tx": B, "log_entries_per_gpu": L, "rs_gran_bytes": args.gran,
             "stmr_layout": "16-B word cells {value, lock-or-TS}", "parallelism": f"shard{world}",
+            "log_exchange": exchange,
             "l2": "inputs larger than L2: 1 GiB STMR per GPU, rotating per-step input buffers "
                   f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
         },
@@ -371,7 +405,7 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
     if dist:
         import torch
         t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = all_reduce(dist, t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     for p in txs + logs + [tickets]:
         p.free()

@@ -341,6 +341,28 @@ int hetm_dev_read_counters(hetm_dev* dev, int* conflict, hetm_batch_stats* last_
 int hetm_dev_route_log_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
                             uint64_t shard_words, hetm_log_entry* d_out, uint64_t* d_counts,
                             void* stream);
+/* Fused route + delivery over NVLink (no NCCL on the data path).
+ * Every shard exposes two receive arenas (round parity) of n_shards regions of
+ * `cap` entries and two bucket-count blocks of 64 (hetm_dev_recv_arena returns
+ * their bases); the sender's router writes its bucket for owner s straight
+ * into s's arena[parity] region [my_shard] and the bucket size into s's
+ * counts[parity][my_shard] — peer pointers (hetm_enable_peer_access, one
+ * process) or IPC-opened pointers (hetm_ipc_*, one process per GPU).  Every
+ * sender writes every owner's count (0 included) every round.  After all
+ * senders of a round have completed (stream sync + a barrier among ranks),
+ * hetm_dev_apply_received validates/applies arena[parity] (mode as in
+ * stream_chunk); *n_out = entries applied.  Alternating the parity per round
+ * lets a sender route round r+1 while an owner still applies round r. */
+int hetm_dev_recv_arena(hetm_dev* dev, uint32_t n_shards, uint64_t cap, void** d_entries, void** d_counts);
+int hetm_dev_route_to_peers_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
+                                 uint64_t shard_words, uint32_t my_shard, uint64_t cap, uint32_t parity,
+                                 void* const* peer_entries, void* const* peer_counts, void* stream);
+int hetm_dev_apply_received(hetm_dev* dev, uint32_t parity, int mode, uint64_t* n_out, void* stream);
+/* CUDA IPC of device buffers between the ranks of one node (64-byte handles). */
+int hetm_ipc_get_handle(void* dptr, void* handle64);
+int hetm_ipc_open_handle(const void* handle64, void** dptr);
+int hetm_ipc_close(void* dptr);
+int hetm_enable_peer_access(int device, int peer_device);
 /* Streams owned by the handle: 0 = execution, 1 = log copy, 2 = validation, 3 = merge. */
 int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
 /* Per-kernel device timing (CUDA events around every batch / validation

@@ -130,6 +130,14 @@ _sigs = {
                                        C.c_uint32, _vp]),
     "hetm_dev_validate_dptr": (C.c_int, [_vp, _vp, C.c_uint64, C.c_int, _vp]),
     "hetm_dev_read_counters": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(BatchStats)]),
+    "hetm_dev_recv_arena": (C.c_int, [_vp, C.c_uint32, C.c_uint64, C.POINTER(_vp), C.POINTER(_vp)]),
+    "hetm_dev_route_to_peers_dptr": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
+                                               C.c_uint32, _vp, _vp, _vp]),
+    "hetm_dev_apply_received": (C.c_int, [_vp, C.c_uint32, C.c_int, u8p, _vp]),
+    "hetm_ipc_get_handle": (C.c_int, [_vp, _vp]),
+    "hetm_ipc_open_handle": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "hetm_ipc_close": (C.c_int, [_vp]),
+    "hetm_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "hetm_dev_route_log_dptr": (C.c_int, [_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint64, _vp, _vp, _vp]),
     "hetm_dev_stream_handle": (C.c_int, [_vp, C.c_int, C.POINTER(_vp)]),
     "hetm_dev_flush_l2": (C.c_int, [_vp, _vp]),

@@ -144,6 +144,27 @@ def gen_cache_batch(seed: int, n: int, key_space: int, alpha: float = 0.5, get_p
     return out
 
 
+def ipc_get_handle(dptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (cross-process peer access)."""
+    buf = (C.c_char * 64)()
+    check(lib.hetm_ipc_get_handle(dptr, buf))
+    return bytes(buf)
+
+
+def ipc_open_handle(handle: bytes) -> int:
+    p = C.c_void_p()
+    check(lib.hetm_ipc_open_handle(C.create_string_buffer(handle, 64), C.byref(p)))
+    return p.value
+
+
+def ipc_close(dptr: int):
+    check(lib.hetm_ipc_close(dptr))
+
+
+def enable_peer_access(device: int, peer: int):
+    check(lib.hetm_enable_peer_access(device, peer))
+
+
 def cache_set_of(key0: int, key1: int, n_sets: int) -> int:
     return int(lib.hetm_cache_set_of(key0, key1, n_sets))
 
@@ -378,6 +399,25 @@ class GpuDevice:
                        stream: int = 0):
         self._chk(lib.hetm_dev_route_log_dptr(self.h, d_in, n, n_shards, shard_words, d_out, d_counts,
                                               stream or None))
+
+    # fused route + delivery over peer memory ----------------
+    def recv_arena(self, n_shards: int, cap: int):
+        """(entries, counts) device pointers of this shard's double receive arena."""
+        e, c = C.c_void_p(), C.c_void_p()
+        self._chk(lib.hetm_dev_recv_arena(self.h, n_shards, cap, C.byref(e), C.byref(c)))
+        return e.value, c.value
+
+    def route_to_peers_dptr(self, d_in: int, n: int, n_shards: int, shard_words: int, my_shard: int, cap: int,
+                            parity: int, peer_entries, peer_counts, stream: int = 0):
+        pe = (C.c_void_p * n_shards)(*peer_entries)
+        pc = (C.c_void_p * n_shards)(*peer_counts)
+        self._chk(lib.hetm_dev_route_to_peers_dptr(self.h, d_in, n, n_shards, shard_words, my_shard, cap, parity,
+                                                   pe, pc, stream or None))
+
+    def apply_received(self, parity: int, mode: int = APPLY, stream: int = 0) -> int:
+        n = C.c_uint64()
+        self._chk(lib.hetm_dev_apply_received(self.h, parity, mode, C.byref(n), stream or None))
+        return n.value
 
     def read_counters(self):
         c = C.c_int()

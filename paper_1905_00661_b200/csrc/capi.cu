@@ -139,6 +139,13 @@ struct hetm_dev {
     uint64_t tk_cap = 0;
     void* d_route = nullptr;
     size_t route_cap = 0;
+    // peer delivery (route_to_peers): this shard's receive arena + bucket counts
+    hetm_log_entry* d_recv = nullptr;
+    unsigned long long* d_recv_counts = nullptr;
+    uint32_t recv_shards = 0;
+    uint64_t recv_cap = 0;
+    void** d_peer_ptrs = nullptr;  // device copy of {entries[64], counts[64]} peer pointer tables
+    unsigned long long* d_peer_totals = nullptr;
     void* d_flush = nullptr;
     size_t flush_bytes = 0;
     unsigned flush_gen = 0;
@@ -572,7 +579,7 @@ int hetm_dev_close(hetm_dev* d) {
     d->pool.reset();
     if (d->h_delta) cudaFreeHost(d->h_delta);
     for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush})
         if (p) cudaFree(p);
@@ -1355,6 +1362,132 @@ int hetm_dev_route_log_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n,
                                      reinterpret_cast<unsigned long long*>(d_counts), d->d_route, d->route_cap,
                                      d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "route_log");
+    return HETM_OK;
+}
+
+int hetm_dev_recv_arena(hetm_dev* d, uint32_t n_shards, uint64_t cap, void** d_entries, void** d_counts) {
+    if (!d || !d_entries || !d_counts || n_shards == 0 || n_shards > 64 || cap == 0) return HETM_ERR_INVALID_ARG;
+    if (n_shards != d->recv_shards || cap != d->recv_cap) {
+        int rc = sync_all(d);
+        if (rc) return rc;
+        if (d->d_recv) { cudaFree(d->d_recv); d->bytes_alloc -= 2 * d->recv_shards * d->recv_cap * sizeof(hetm_log_entry); }
+        if (d->d_recv_counts) { cudaFree(d->d_recv_counts); d->bytes_alloc -= 128 * 8; }
+        d->d_recv = nullptr;
+        d->d_recv_counts = nullptr;
+        // two arenas (round parity): a sender may route round r+1 while this owner still applies round r
+        if ((rc = dev_alloc(d, (void**)&d->d_recv, 2 * (size_t)n_shards * cap * sizeof(hetm_log_entry)))) return rc;
+        if ((rc = dev_alloc(d, (void**)&d->d_recv_counts, 128 * 8))) return rc;
+        CK(d, cudaMemset(d->d_recv_counts, 0, 128 * 8));
+        d->recv_shards = n_shards;
+        d->recv_cap = cap;
+    }
+    *d_entries = d->d_recv;
+    *d_counts = d->d_recv_counts;
+    return HETM_OK;
+}
+
+int hetm_dev_route_to_peers_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
+                                 uint64_t shard_words, uint32_t my_shard, uint64_t cap, uint32_t parity,
+                                 void* const* peer_entries, void* const* peer_counts, void* stream) {
+    if (!d || (n && !d_in) || !peer_entries || !peer_counts) return HETM_ERR_INVALID_ARG;
+    if (n_shards == 0 || n_shards > 64 || shard_words == 0 || my_shard >= n_shards) return HETM_ERR_CONFIG;
+    if (n > cap) return HETM_ERR_INVALID_SIZE;
+    int rc;
+    const size_t need = route_log_scratch_bytes(n, n_shards, d->geom);
+    if (need > d->route_cap) {
+        if (d->d_route) { CK(d, cudaDeviceSynchronize()); cudaFree(d->d_route); }
+        if ((rc = dev_alloc(d, &d->d_route, need))) return rc;
+        d->route_cap = need;
+    }
+    if (!d->d_peer_ptrs) {
+        if ((rc = dev_alloc(d, (void**)&d->d_peer_ptrs, 128 * sizeof(void*)))) return rc;
+        if ((rc = dev_alloc(d, (void**)&d->d_peer_totals, 64 * 8))) return rc;
+    }
+    void* table[128] = {};
+    for (uint32_t s = 0; s < n_shards; ++s) {  // this round's arena / count block of every owner
+        table[s] = static_cast<hetm_log_entry*>(peer_entries[s]) + (uint64_t)(parity & 1) * n_shards * cap;
+        table[64 + s] = static_cast<unsigned long long*>(peer_counts[s]) + (parity & 1) * 64;
+    }
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    CK(d, cudaMemcpyAsync(d->d_peer_ptrs, table, sizeof(table), cudaMemcpyHostToDevice, s));
+    CK(d, cudaStreamSynchronize(s));  // `table` is a stack buffer
+    cudaError_t e = launch_route_to_peers(d_in, n, n_shards, shard_words, my_shard, cap,
+                                          reinterpret_cast<hetm_log_entry* const*>(d->d_peer_ptrs),
+                                          reinterpret_cast<unsigned long long* const*>(d->d_peer_ptrs + 64),
+                                          d->d_peer_totals, d->d_route, d->route_cap, d->geom, s);
+    if (e != cudaSuccess) return fail(d, e, "route_to_peers");
+    return HETM_OK;
+}
+
+int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_out, void* stream) {
+    if (!d || !d->d_recv) return HETM_ERR_INVALID_ARG;
+    if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    unsigned long long counts[64] = {};
+    const uint64_t p = parity & 1;
+    CK(d, cudaMemcpyAsync(counts, d->d_recv_counts + p * 64, d->recv_shards * 8, cudaMemcpyDeviceToHost, s));
+    CK(d, cudaStreamSynchronize(s));
+    uint64_t total = 0;
+    hetm_log_entry* arena = d->d_recv + p * d->recv_shards * d->recv_cap;
+    for (uint32_t src = 0; src < d->recv_shards; ++src) {  // every sender rewrites its count every round
+        if (counts[src] > d->recv_cap) return HETM_ERR_INVALID_SIZE;
+        if (!counts[src]) continue;
+        const int rc = hetm_dev_validate_dptr(d, arena + (uint64_t)src * d->recv_cap, counts[src], mode, s);
+        if (rc) return rc;
+        total += counts[src];
+    }
+    if (n_out) *n_out = total;
+    return HETM_OK;
+}
+
+int hetm_ipc_get_handle(void* dptr, void* handle64) {
+    if (!dptr || !handle64) return HETM_ERR_INVALID_ARG;
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, dptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return HETM_ERR_CUDA;
+    }
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    return HETM_OK;
+}
+
+int hetm_ipc_open_handle(const void* handle64, void** dptr) {
+    if (!handle64 || !dptr) return HETM_ERR_INVALID_ARG;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    const cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *dptr = nullptr;
+        return HETM_ERR_CUDA;
+    }
+    return HETM_OK;
+}
+
+int hetm_ipc_close(void* dptr) {
+    if (!dptr) return HETM_ERR_INVALID_ARG;
+    cudaIpcCloseMemHandle(dptr);
+    return HETM_OK;
+}
+
+int hetm_enable_peer_access(int device, int peer) {
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, device, peer) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return HETM_ERR_CUDA;
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    cudaSetDevice(cur);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return HETM_ERR_CUDA;
+    }
+    cudaGetLastError();
     return HETM_OK;
 }
 

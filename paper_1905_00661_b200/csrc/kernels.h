@@ -82,6 +82,12 @@ cudaError_t launch_route_log(const hetm_log_entry* d_in, uint64_t n, uint32_t n_
                              hetm_log_entry* d_out, unsigned long long* d_counts, void* d_scratch,
                              size_t scratch_bytes, const LaunchGeom& g, cudaStream_t s);
 size_t route_log_scratch_bytes(uint64_t n, uint32_t n_shards, const LaunchGeom& g);
+// Route + deliver: entries of shard s land in d_peer_out[s][my*cap ...], bucket sizes in
+// d_peer_counts[s][my] (device arrays of n_shards pointers, peer/IPC pointers allowed).
+cudaError_t launch_route_to_peers(const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards, uint64_t shard_words,
+                                  uint32_t my, uint64_t cap, hetm_log_entry* const* d_peer_out,
+                                  unsigned long long* const* d_peer_counts, unsigned long long* d_totals,
+                                  void* d_scratch, size_t scratch_bytes, const LaunchGeom& g, cudaStream_t s);
 
 int query_geom(LaunchGeom* g, int device);
 

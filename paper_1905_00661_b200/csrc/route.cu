@@ -15,6 +15,12 @@
 //                shard; lane s keeps the running base of shard s (s < 64)
 // Stable (input order within a shard is kept), streaming: 24 B read twice,
 // 24 B written once per entry.
+//
+// Peer delivery (route_to_peers): the same count/scan, but the scatter writes
+// each entry straight into its OWNER's receive arena — region [my_shard] of
+// the owner's arena, over NVLink when the owner is another GPU (peer / IPC
+// pointers) — and the scan publishes the bucket sizes into the owners' count
+// arrays.  Route and all-to-all are one pass; no local bucket buffer, no NCCL.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -92,6 +98,18 @@ __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(const unsigned
     }
 }
 
+// Peer variant of the scan epilogue: bucket sizes go to owner s's counts[my]
+// and every offset becomes relative to its shard's bucket start.
+__global__ void route_peer_publish_kernel(unsigned long long* offsets, const unsigned long long* totals,
+                                          uint64_t n_warps, uint32_t nsh, uint32_t my,
+                                          unsigned long long* const* peer_counts) {
+    const uint32_t s = blockIdx.x;
+    const unsigned long long start = offsets[(uint64_t)s * n_warps];
+    __syncthreads();
+    for (uint64_t w = threadIdx.x; w < n_warps; w += blockDim.x) offsets[(uint64_t)s * n_warps + w] -= start;
+    if (threadIdx.x == 0) peer_counts[s][my] = totals[s];
+}
+
 __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm_log_entry* __restrict__ in, uint64_t n,
                                                                       uint32_t nsh, uint64_t shard_words,
                                                                       const unsigned long long* __restrict__ offsets,
@@ -130,6 +148,48 @@ __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm
 
 // Up to 8 CTAs per SM; small logs get fewer warps (>= 512 entries per warp) so
 // the single-CTA scan over [shard][warp] stays short.
+// Scatter into the owners' receive arenas: entry of shard s -> peer_out[s][my*cap + bucket offset].
+__global__ void __launch_bounds__(kRouteThreads) route_peer_scatter_kernel(
+    const hetm_log_entry* __restrict__ in, uint64_t n, uint32_t nsh, uint64_t shard_words,
+    const unsigned long long* __restrict__ offsets, hetm_log_entry* const* peer_out, uint64_t region) {
+    const uint64_t n_warps = (uint64_t)gridDim.x * kRouteWarps;
+    const uint64_t w = (uint64_t)blockIdx.x * kRouteWarps + (threadIdx.x >> 5);
+    const unsigned lane = lane_id();
+    uint64_t lo, hi;
+    warp_slice(n, n_warps, w, lo, hi);
+    unsigned long long b0 = lane < nsh ? offsets[(uint64_t)lane * n_warps + w] : 0;
+    unsigned long long b1 = lane + 32 < nsh ? offsets[(uint64_t)(lane + 32) * n_warps + w] : 0;
+    hetm_log_entry* d0 = lane < nsh ? peer_out[lane] + region : nullptr;
+    hetm_log_entry* d1 = lane + 32 < nsh ? peer_out[lane + 32] + region : nullptr;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const bool valid = i < hi;
+        hetm_log_entry e{};
+        uint32_t s = 0xffffffffu;
+        if (valid) {
+            e = in[i];
+            s = owner_of(e.addr, shard_words, nsh);
+        }
+        unsigned rank = 0;
+        const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
+        const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
+        hetm_log_entry* const p0 = reinterpret_cast<hetm_log_entry*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), s & 31));
+        hetm_log_entry* const p1 = reinterpret_cast<hetm_log_entry*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), s & 31));
+        for (uint32_t sh = 0; sh < nsh; ++sh) {
+            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
+            if (s == sh) rank = __popc(m & lt);
+            if (lane == (sh & 31)) {
+                if (sh < 32) b0 += __popc(m);
+                else b1 += __popc(m);
+            }
+        }
+        if (valid) (s < 32 ? p0 + my0 : p1 + my1)[rank] = e;
+    }
+}
+
 static unsigned route_grid(uint64_t n, const LaunchGeom& g) {
     const uint64_t want = (n + kRouteThreads * 16 - 1) / (kRouteThreads * 16);
     const uint64_t cap = (uint64_t)g.sm_count * 8u;
@@ -152,6 +212,24 @@ cudaError_t launch_route_log(const hetm_log_entry* d_in, uint64_t n, uint32_t ns
     route_count_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, counts);
     route_scan_kernel<<<1, kScanThreads, 0, s>>>(counts, n_warps, nsh, offsets, d_counts);
     route_scatter_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, offsets, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_route_to_peers(const hetm_log_entry* d_in, uint64_t n, uint32_t nsh, uint64_t shard_words,
+                                  uint32_t my, uint64_t cap, hetm_log_entry* const* d_peer_out,
+                                  unsigned long long* const* d_peer_counts, unsigned long long* d_totals,
+                                  void* d_scratch, size_t scratch_bytes, const LaunchGeom& g, cudaStream_t s) {
+    if (nsh == 0 || nsh > kMaxShards || shard_words == 0 || my >= nsh || n > cap) return cudaErrorInvalidValue;
+    if (scratch_bytes < route_log_scratch_bytes(n, nsh, g)) return cudaErrorInvalidValue;
+    const unsigned grid = route_grid(n, g);
+    const uint64_t n_warps = (uint64_t)grid * kRouteWarps;
+    auto* counts = static_cast<unsigned long long*>(d_scratch);
+    auto* offsets = counts + n_warps * nsh;
+    route_count_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, counts);
+    route_scan_kernel<<<1, kScanThreads, 0, s>>>(counts, n_warps, nsh, offsets, d_totals);
+    route_peer_publish_kernel<<<nsh, 256, 0, s>>>(offsets, d_totals, n_warps, nsh, my, d_peer_counts);
+    route_peer_scatter_kernel<<<grid, kRouteThreads, 0, s>>>(d_in, n, nsh, shard_words, offsets, d_peer_out,
+                                                             (uint64_t)my * cap);
     return cudaGetLastError();
 }
 

@@ -1,5 +1,12 @@
 """Address-range sharding of the validation path across the GPUs of one node.
 
+Two exchange paths:
+  * PeerValidator (default product path): ONE fused router pass writes every
+    entry straight into its owner GPU's receive arena over NVLink (CUDA IPC
+    pointers of the peers' arenas, hetm_dev_route_to_peers_dptr), then one
+    barrier, then each owner applies what it received — no NCCL on the data path;
+  * ShardedValidator (fallback): local router -> NCCL all_to_all -> apply.
+
 SURVEY.md §8(e): shard s owns global STMR words [s*W, (s+1)*W).  Every rank
 ingests 1/G of the round's host write log over its own PCIe link, the CUDA
 router (hetm_dev_route_log_dptr) stable-partitions it by owner shard, the
@@ -74,3 +81,73 @@ class ShardedValidator:
         self.dev.validate_dptr(recv.data_ptr(), int(recv.shape[0]), mode, self.stream)
         self._keep = recv  # alive until the validation kernel has consumed it
         return int(recv.shape[0])
+
+
+class PeerValidator:
+    """Fused route + NVLink delivery of one rank.
+
+    Each rank exposes a double receive arena (world regions x `cap` entries,
+    two round parities) and its bucket counts; their CUDA IPC handles are
+    all-gathered once.  validate() = one router launch that scatters each
+    entry into its owner's arena (peer stores), a stream sync + barrier so
+    every rank's deliveries of this round are complete, and the owner's
+    validate/apply of its received regions.  Round parity alternates, so a
+    fast rank can route round r+1 while a slow one still applies round r."""
+
+    def __init__(self, dev, world: int, rank: int, shard_words: int, cap: int, dist, stream: int = 0):
+        """Collective over all ranks; raises RuntimeError on EVERY rank if any rank
+        cannot export or open the arenas (the caller then falls back to NCCL)."""
+        from . import api
+
+        self.dev, self.world, self.rank, self.shard_words, self.cap = dev, world, rank, shard_words, cap
+        self.dist, self.stream, self.parity = dist, stream, 0
+        self._opened = []
+        try:
+            ent, cnt = dev.recv_arena(world, cap)
+            mine = (api.ipc_get_handle(ent), api.ipc_get_handle(cnt))
+        except Exception:
+            ent = cnt = mine = None
+        handles = [None] * world
+        dist.all_gather_object(handles, mine)
+        ok = all(h is not None for h in handles)
+        self.entries, self.counts = [], []
+        if ok:
+            try:
+                for r in range(world):
+                    if r == rank:
+                        self.entries.append(ent)
+                        self.counts.append(cnt)
+                    else:
+                        e = api.ipc_open_handle(handles[r][0])
+                        self._opened.append(e)
+                        c = api.ipc_open_handle(handles[r][1])
+                        self._opened.append(c)
+                        self.entries.append(e)
+                        self.counts.append(c)
+            except Exception:
+                ok = False
+        flags = [None] * world
+        dist.all_gather_object(flags, ok)
+        if not all(flags):
+            self.close()
+            raise RuntimeError("peer arenas unavailable on some rank")
+
+    def validate(self, log, mode: int):
+        """Route + deliver + validate `log` ((n, 3) int64 CUDA tensor); returns the entries applied here."""
+        import torch
+
+        n = int(log.shape[0])
+        self.dev.route_to_peers_dptr(log.data_ptr(), n, self.world, self.shard_words, self.rank, self.cap,
+                                     self.parity, self.entries, self.counts, self.stream)
+        torch.cuda.ExternalStream(self.stream).synchronize() if self.stream else torch.cuda.synchronize()
+        self.dist.barrier()  # every rank's deliveries for this parity are complete
+        m = self.dev.apply_received(self.parity, mode, self.stream)
+        self.parity ^= 1
+        return m
+
+    def close(self):
+        from . import api
+
+        for p in self._opened:
+            api.ipc_close(p)
+        self._opened = []
