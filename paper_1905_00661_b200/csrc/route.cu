@@ -30,6 +30,7 @@ constexpr int kRouteThreads = 256;
 constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxShards = 64;
 constexpr int kScanThreads = 1024;
+constexpr int kRouteUnroll = 4;  // 32-entry groups a warp loads before ranking them
 
 __device__ __forceinline__ uint32_t owner_of(uint64_t addr, uint64_t shard_words, uint32_t n_shards) {
     uint64_t s = addr / shard_words;
@@ -50,14 +51,21 @@ __global__ void __launch_bounds__(kRouteThreads) route_count_kernel(const hetm_l
     uint64_t lo, hi;
     warp_slice(n, n_warps, w, lo, hi);
     unsigned long long c0 = 0, c1 = 0;  // lane L counts shard L and shard L+32
-    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const uint32_t s = i < hi ? owner_of(__ldg(&in[i].addr), shard_words, nsh) : 0xffffffffu;
-        for (uint32_t sh = 0; sh < nsh; ++sh) {
-            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
-            if (lane == (sh & 31)) {
-                if (sh < 32) c0 += __popc(m);
-                else c1 += __popc(m);
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32 * kRouteUnroll) {
+        uint32_t sv[kRouteUnroll];
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {  // kRouteUnroll independent loads in flight per lane
+            const uint64_t i = i0 + 32 * u + lane;
+            sv[u] = i < hi ? owner_of(__ldg(&in[i].addr), shard_words, nsh) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {
+            for (uint32_t sh = 0; sh < nsh; ++sh) {
+                const unsigned m = __ballot_sync(0xffffffffu, sv[u] == sh);
+                if (lane == (sh & 31)) {
+                    if (sh < 32) c0 += __popc(m);
+                    else c1 += __popc(m);
+                }
             }
         }
     }
@@ -122,27 +130,34 @@ __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm
     unsigned long long b0 = lane < nsh ? offsets[(uint64_t)lane * n_warps + w] : 0;
     unsigned long long b1 = lane + 32 < nsh ? offsets[(uint64_t)(lane + 32) * n_warps + w] : 0;
     const unsigned lt = (1u << lane) - 1u;
-    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const bool valid = i < hi;
-        hetm_log_entry e{};
-        uint32_t s = 0xffffffffu;
-        if (valid) {
-            e = in[i];
-            s = owner_of(e.addr, shard_words, nsh);
-        }
-        unsigned rank = 0;
-        const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
-        const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
-        for (uint32_t sh = 0; sh < nsh; ++sh) {
-            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
-            if (s == sh) rank = __popc(m & lt);
-            if (lane == (sh & 31)) {
-                if (sh < 32) b0 += __popc(m);
-                else b1 += __popc(m);
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32 * kRouteUnroll) {
+        hetm_log_entry ev[kRouteUnroll];
+        uint32_t sv[kRouteUnroll];
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {
+            const uint64_t i = i0 + 32 * u + lane;
+            sv[u] = 0xffffffffu;
+            if (i < hi) {
+                ev[u] = in[i];
+                sv[u] = owner_of(ev[u].addr, shard_words, nsh);
             }
         }
-        if (valid) out[(s < 32 ? my0 : my1) + rank] = e;
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {
+            const uint32_t s = sv[u];
+            unsigned rank = 0;
+            const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
+            const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
+            for (uint32_t sh = 0; sh < nsh; ++sh) {
+                const unsigned m = __ballot_sync(0xffffffffu, s == sh);
+                if (s == sh) rank = __popc(m & lt);
+                if (lane == (sh & 31)) {
+                    if (sh < 32) b0 += __popc(m);
+                    else b1 += __popc(m);
+                }
+            }
+            if (s != 0xffffffffu) out[(s < 32 ? my0 : my1) + rank] = ev[u];
+        }
     }
 }
 
@@ -162,37 +177,44 @@ __global__ void __launch_bounds__(kRouteThreads) route_peer_scatter_kernel(
     hetm_log_entry* d0 = lane < nsh ? peer_out[lane] + region : nullptr;
     hetm_log_entry* d1 = lane + 32 < nsh ? peer_out[lane + 32] + region : nullptr;
     const unsigned lt = (1u << lane) - 1u;
-    for (uint64_t i0 = lo; i0 < hi; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const bool valid = i < hi;
-        hetm_log_entry e{};
-        uint32_t s = 0xffffffffu;
-        if (valid) {
-            e = in[i];
-            s = owner_of(e.addr, shard_words, nsh);
-        }
-        unsigned rank = 0;
-        const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
-        const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
-        hetm_log_entry* const p0 = reinterpret_cast<hetm_log_entry*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), s & 31));
-        hetm_log_entry* const p1 = reinterpret_cast<hetm_log_entry*>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), s & 31));
-        for (uint32_t sh = 0; sh < nsh; ++sh) {
-            const unsigned m = __ballot_sync(0xffffffffu, s == sh);
-            if (s == sh) rank = __popc(m & lt);
-            if (lane == (sh & 31)) {
-                if (sh < 32) b0 += __popc(m);
-                else b1 += __popc(m);
+    for (uint64_t i0 = lo; i0 < hi; i0 += 32 * kRouteUnroll) {
+        hetm_log_entry ev[kRouteUnroll];
+        uint32_t sv[kRouteUnroll];
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {
+            const uint64_t i = i0 + 32 * u + lane;
+            sv[u] = 0xffffffffu;
+            if (i < hi) {
+                ev[u] = in[i];
+                sv[u] = owner_of(ev[u].addr, shard_words, nsh);
             }
         }
-        if (valid) (s < 32 ? p0 + my0 : p1 + my1)[rank] = e;
+#pragma unroll
+        for (int u = 0; u < kRouteUnroll; ++u) {
+            const uint32_t s = sv[u];
+            unsigned rank = 0;
+            const unsigned long long my0 = __shfl_sync(0xffffffffu, b0, s & 31);
+            const unsigned long long my1 = __shfl_sync(0xffffffffu, b1, s & 31);
+            hetm_log_entry* const p0 = reinterpret_cast<hetm_log_entry*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), s & 31));
+            hetm_log_entry* const p1 = reinterpret_cast<hetm_log_entry*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), s & 31));
+            for (uint32_t sh = 0; sh < nsh; ++sh) {
+                const unsigned m = __ballot_sync(0xffffffffu, s == sh);
+                if (s == sh) rank = __popc(m & lt);
+                if (lane == (sh & 31)) {
+                    if (sh < 32) b0 += __popc(m);
+                    else b1 += __popc(m);
+                }
+            }
+            if (s != 0xffffffffu) (s < 32 ? p0 + my0 : p1 + my1)[rank] = ev[u];
+        }
     }
 }
 
 static unsigned route_grid(uint64_t n, const LaunchGeom& g) {
     const uint64_t want = (n + kRouteThreads * 16 - 1) / (kRouteThreads * 16);
-    const uint64_t cap = (uint64_t)g.sm_count * 8u;
+    const uint64_t cap = (uint64_t)g.sm_count * 2u;  // each warp streams a long slice, 4 loads in flight
     return (unsigned)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 

@@ -110,6 +110,19 @@ def main():
                 if r:
                     rt.append(ev0.elapsed_time(ev1))
             ms_route = statistics.median(rt)
+            # fused route + delivery kernel with every owner's arena local (kernel cost;
+            # across GPUs the stores go over NVLink, estimated below)
+            ent, cnt = dev.recv_arena(G, n)
+            pt = []
+            for r in range(a.reps + 1):
+                ev0.record(rstream)
+                dev.route_to_peers_dptr(ingest.data_ptr(), n, G, W, 0, n, r & 1, [ent] * G, [cnt] * G,
+                                        rstream.cuda_stream)
+                ev1.record(rstream)
+                torch.cuda.synchronize()
+                if r:
+                    pt.append(ev0.elapsed_time(ev1))
+            ms_peer = statistics.median(pt)
             xchg_bytes = n * ENTRY * (G - 1) / G  # entries leaving this rank
             row = {
                 "G": G, "shard_gib_words": W * 8 / 2**30, "log_mib_global": mib, "entries_per_shard": n,
@@ -119,6 +132,7 @@ def main():
                 "log_gbs_aggregate": G * ENTRY * n / ms_apply / 1e6,
                 "validate_only_ms": ms_vonly, "validate_only_log_gbs_per_gpu": ENTRY * n / ms_vonly / 1e6,
                 "route_ms": ms_route, "route_gbs_per_gpu": 2 * ENTRY * n / ms_route / 1e6,
+                "route_to_peers_ms_local": ms_peer,
                 "exchange_ms_estimate_nvlink": xchg_bytes / (NVLINK_GBS * 1e6),
                 "conflict": bool(conflict),
             }
