@@ -244,8 +244,10 @@ def run_ours(args):
         tb = tx_d[j % n_bufs]
         dev.execute_batch_dptr(hetm.KERNEL_BANK, tb.data_ptr(), B, tickets.data_ptr(), s_exec)
         lg = log_d[j]
-        with torch.cuda.stream(vs):  # router, NCCL exchange and validation share the validation stream
+        with torch.cuda.stream(vs):  # router, exchange and validation share the validation stream
             n_local = sv.validate(lg, hetm.APPLY)
+        if n_local is None:  # fused peer exchange on NCCL: counts stay on the device; every entry has one owner
+            n_local = L
         dev.clear_round(asynchronous=True)
         return n_local
 

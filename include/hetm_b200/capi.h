@@ -351,8 +351,11 @@ int hetm_dev_route_log_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t 
  * sender writes every owner's count (0 included) every round.  After all
  * senders of a round have completed (stream sync + a barrier among ranks),
  * hetm_dev_apply_received validates/applies arena[parity] (mode as in
- * stream_chunk); *n_out = entries applied.  Alternating the parity per round
- * lets a sender route round r+1 while an owner still applies round r. */
+ * stream_chunk) in ONE launch that reads the counts on the device — no host
+ * round trip, so the ranks can order it behind a device-side barrier (e.g. a
+ * 1-element NCCL all-reduce on the same stream).  n_out (nullable) costs a
+ * sync: entries applied.  Alternating the parity per round lets a sender
+ * route round r+1 while an owner still applies round r. */
 int hetm_dev_recv_arena(hetm_dev* dev, uint32_t n_shards, uint64_t cap, void** d_entries, void** d_counts);
 int hetm_dev_route_to_peers_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
                                  uint64_t shard_words, uint32_t my_shard, uint64_t cap, uint32_t parity,

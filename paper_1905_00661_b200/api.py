@@ -414,7 +414,11 @@ class GpuDevice:
         self._chk(lib.hetm_dev_route_to_peers_dptr(self.h, d_in, n, n_shards, shard_words, my_shard, cap, parity,
                                                    pe, pc, stream or None))
 
-    def apply_received(self, parity: int, mode: int = APPLY, stream: int = 0) -> int:
+    def apply_received(self, parity: int, mode: int = APPLY, stream: int = 0, count: bool = True):
+        """Validate/apply arena[parity]; count=False keeps it asynchronous (returns None)."""
+        if not count:
+            self._chk(lib.hetm_dev_apply_received(self.h, parity, mode, None, stream or None))
+            return None
         n = C.c_uint64()
         self._chk(lib.hetm_dev_apply_received(self.h, parity, mode, C.byref(n), stream or None))
         return n.value

@@ -1423,20 +1423,38 @@ int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_
     if (!d || !d->d_recv) return HETM_ERR_INVALID_ARG;
     if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
-    unsigned long long counts[64] = {};
     const uint64_t p = parity & 1;
-    CK(d, cudaMemcpyAsync(counts, d->d_recv_counts + p * 64, d->recv_shards * 8, cudaMemcpyDeviceToHost, s));
-    CK(d, cudaStreamSynchronize(s));
-    uint64_t total = 0;
-    hetm_log_entry* arena = d->d_recv + p * d->recv_shards * d->recv_cap;
-    for (uint32_t src = 0; src < d->recv_shards; ++src) {  // every sender rewrites its count every round
-        if (counts[src] > d->recv_cap) return HETM_ERR_INVALID_SIZE;
-        if (!counts[src]) continue;
-        const int rc = hetm_dev_validate_dptr(d, arena + (uint64_t)src * d->recv_cap, counts[src], mode, s);
-        if (rc) return rc;
-        total += counts[src];
+    const hetm_log_entry* arena = d->d_recv + p * d->recv_shards * d->recv_cap;
+    const unsigned long long* counts = d->d_recv_counts + p * 64;
+    CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
+    if (mode == HETM_APPLY) {
+        CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
+        d->round_applied = true;
+        d->shadow_synced = false;  // entries are not retained in the arena for the shadow patch
     }
-    if (n_out) *n_out = total;
+    // one launch over every received region; the counts stay on the device
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (d->timing) {
+        t0 = d->tev();
+        t1 = d->tev();
+        cudaEventRecord(t0, s);
+    }
+    const cudaError_t e = launch_validate_regions(d->view(), arena, counts, d->recv_shards, d->recv_cap,
+                                                  mode == HETM_APPLY ? 1 : 0, d->d_ctr, d->d_restore, d->geom, s);
+    if (d->timing) {
+        cudaEventRecord(t1, s);
+        d->tpairs[1].emplace_back(t0, t1);
+    }
+    if (e != cudaSuccess) return fail(d, e, "validate_regions");
+    if (stream) CK(d, cudaEventRecord(d->ev_val, s));
+    if (n_out) {  // optional: the entry count needs a host round trip
+        unsigned long long c[64] = {};
+        CK(d, cudaMemcpyAsync(c, counts, d->recv_shards * 8, cudaMemcpyDeviceToHost, s));
+        CK(d, cudaStreamSynchronize(s));
+        uint64_t total = 0;
+        for (uint32_t r = 0; r < d->recv_shards; ++r) total += std::min<uint64_t>(c[r], d->recv_cap);
+        *n_out = total;
+    }
     return HETM_OK;
 }
 

@@ -44,6 +44,10 @@ cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const 
                                     cudaStream_t s);
 // Literal TS reset: every TS word becomes an unlocked word.
 cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
+// Validate/apply the received regions of a peer arena (counts on the device; no host sync).
+cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_base, const unsigned long long* d_counts,
+                                    uint32_t n_regions, uint64_t cap, int apply, DevCounters* ctr,
+                                    unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
 // Round boundary: ts_floor = max(ts_floor, round_max_ts) (0 with reset_ts), round_max_ts = 0.
 cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s);
 // Winner store of the round's log: value of the entry whose ts equals the

@@ -36,6 +36,44 @@ __device__ __forceinline__ EntryRegs load_entry(const hetm_log_entry* log, uint6
     return EntryRegs{__ldg(e), __ldg(e + 1), __ldg(e + 2)};
 }
 
+// The entries a validation launch covers: a flat array of n entries, or the
+// received regions of a peer arena (region r = base[r*cap .. r*cap + counts[r]),
+// counts read on the device, so the launch needs no host round trip).
+// Logical index g runs over [0, total) across the regions in order.
+struct LogView {
+    const hetm_log_entry* base;
+    uint64_t n;                             // flat entry count (segments == nullptr)
+    const unsigned long long* segments;     // device counts of the regions, or nullptr
+    uint32_t n_seg;                         // <= 64
+    uint64_t cap;                           // entries per region
+};
+
+struct SegPrefix {  // per-block copy of the region prefix sums
+    unsigned long long pre[65];
+};
+
+__device__ __forceinline__ uint64_t view_total(const LogView& lv, SegPrefix& sp) {
+    if (!lv.segments) return lv.n;
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (uint32_t r = 0; r < lv.n_seg; ++r) {
+            sp.pre[r] = run;
+            const unsigned long long c = ld_relaxed(&lv.segments[r]);
+            run += c < lv.cap ? c : lv.cap;
+        }
+        sp.pre[lv.n_seg] = run;
+    }
+    __syncthreads();
+    return sp.pre[lv.n_seg];
+}
+
+__device__ __forceinline__ EntryRegs view_entry(const LogView& lv, const SegPrefix& sp, uint64_t g) {
+    if (!lv.segments) return load_entry(lv.base, g);
+    uint32_t r = 0;
+    while (r + 1 < lv.n_seg && sp.pre[r + 1] <= g) ++r;
+    return load_entry(lv.base, (uint64_t)r * lv.cap + (g - sp.pre[r]));
+}
+
 // Pass A of one entry (RS test + TS raise); returns nothing, folds flags.
 struct PassAFlags {
     unsigned conflict = 0, bad = 0, oob = 0;
@@ -73,8 +111,9 @@ __device__ __forceinline__ void flush_pass_a(PassAFlags f, DevCounters* ctr) {
     }
 }
 
-__global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
-                                                               uint64_t n, DevCounters* ctr) {
+__global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, LogView lv, DevCounters* ctr) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
     PassAFlags f;
     const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
@@ -83,7 +122,7 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, cons
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base, 0, ~0ull};
+            e[u] = i < n ? view_entry(lv, sp, i) : EntryRegs{v.base, 0, ~0ull};
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
@@ -103,9 +142,10 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, cons
 // or is queued itself.  Cost per entry: one random line RMW + one L2-hit
 // store; duplicates (rare under uniform access) cost one more L2 load+store.
 template <int U>
-__global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
-                                                            uint64_t n, DevCounters* ctr,
+__global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView lv, DevCounters* ctr,
                                                             unsigned long long* __restrict__ restore) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
     PassAFlags f;
     const uint64_t span = (uint64_t)gridDim.x * blockDim.x * U;
@@ -115,7 +155,7 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, const h
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-            e[u] = i < n ? load_entry(log, i) : EntryRegs{v.base + v.size_words, 0, 0};
+            e[u] = i < n ? view_entry(lv, sp, i) : EntryRegs{v.base + v.size_words, 0, 0};
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -149,14 +189,15 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, const h
 // freshest one per word).  If the queue overflowed, every entry of the launch
 // is checked (pass B of the classic two-pass scheme).  The last block to
 // finish resets the queue for the next apply launch on this stream.
-__global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
-                                                              uint64_t n, DevCounters* ctr,
+__global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, LogView lv, DevCounters* ctr,
                                                               const unsigned long long* __restrict__ restore) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
     const unsigned long long m = ld_relaxed(&ctr->restore_n);
     const bool full = m > kRestoreCap;
     const uint64_t cnt = full ? n : m;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x) {
-        const EntryRegs e = load_entry(log, full ? j : restore[j]);
+        const EntryRegs e = view_entry(lv, sp, full ? j : restore[j]);
         const uint64_t loc = e.addr - v.base;
         if (loc < v.size_words && ld_relaxed(&v.cells[loc].meta) == ts_meta(e.ts)) v.cells[loc].value = e.value;
     }
@@ -269,12 +310,14 @@ cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
-                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const unsigned grid = grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
+// Core launcher over a LogView; n_hint sizes the grid (the flat count, or the
+// segmented view's capacity when the counts live on the device).
+static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n_hint, int apply, DevCounters* ctr,
+                               unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
+    if (n_hint == 0) return cudaSuccess;
+    const unsigned grid = grid_cap((n_hint + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
     if (!apply) {
-        validate_kernel<<<grid, kValThreads, 0, s>>>(v, d_log, n, ctr);
+        validate_kernel<<<grid, kValThreads, 0, s>>>(v, lv, ctr);
         return cudaGetLastError();
     }
     static const int apply_bps = [] {  // tuning experiments only: resident blocks per SM for apply
@@ -289,12 +332,25 @@ cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uin
     // 0.081 vs 0.111 ms per 2^20 entries at full occupancy)
     const int bps = apply_bps > 0 ? apply_bps : 1;
     const int u = apply_unroll == 2 || apply_unroll == 8 ? apply_unroll : 4;
-    const unsigned agrid = grid_cap((n + u - 1) / u, kValThreads, g, bps);
-    if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
-    else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
-    else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
-    restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, d_log, n, ctr, d_restore);
+    const unsigned agrid = grid_cap((n_hint + u - 1) / u, kValThreads, g, bps);
+    if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+    else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+    else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+    restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
     return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
+                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
+    return launch_view(v, LogView{d_log, n, nullptr, 0, 0}, n, apply, ctr, d_restore, g, s);
+}
+
+cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_base, const unsigned long long* d_counts,
+                                    uint32_t n_regions, uint64_t cap, int apply, DevCounters* ctr,
+                                    unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
+    if (n_regions == 0 || n_regions > 64) return cudaErrorInvalidValue;
+    // the grid is sized for one region's worth (the expected share); the kernels grid-stride over the total
+    return launch_view(v, LogView{d_base, 0, d_counts, n_regions, cap}, cap, apply, ctr, d_restore, g, s);
 }
 
 // Clean re-apply of the round log onto the device replica whose device write

@@ -102,6 +102,7 @@ class PeerValidator:
         self.dev, self.world, self.rank, self.shard_words, self.cap = dev, world, rank, shard_words, cap
         self.dist, self.stream, self.parity = dist, stream, 0
         self._opened = []
+        self._flag = None
         try:
             ent, cnt = dev.recv_arena(world, cap)
             mine = (api.ipc_get_handle(ent), api.ipc_get_handle(cnt))
@@ -133,15 +134,29 @@ class PeerValidator:
             raise RuntimeError("peer arenas unavailable on some rank")
 
     def validate(self, log, mode: int):
-        """Route + deliver + validate `log` ((n, 3) int64 CUDA tensor); returns the entries applied here."""
+        """Route + deliver + validate `log` ((n, 3) int64 CUDA tensor).  With NCCL
+        the round barrier is a 1-element all-reduce ordered on the validation
+        stream, so nothing waits on the host; returns None then (the number of
+        entries applied here is known only on the device).  With a CPU backend
+        (gloo test mode) the stream is synchronized around a host barrier and
+        the count is returned."""
         import torch
 
         n = int(log.shape[0])
         self.dev.route_to_peers_dptr(log.data_ptr(), n, self.world, self.shard_words, self.rank, self.cap,
                                      self.parity, self.entries, self.counts, self.stream)
-        torch.cuda.ExternalStream(self.stream).synchronize() if self.stream else torch.cuda.synchronize()
-        self.dist.barrier()  # every rank's deliveries for this parity are complete
-        m = self.dev.apply_received(self.parity, mode, self.stream)
+        device_barrier = self.dist.get_backend() == "nccl"
+        if device_barrier:
+            st = torch.cuda.ExternalStream(self.stream) if self.stream else torch.cuda.current_stream()
+            with torch.cuda.stream(st):
+                if self._flag is None:
+                    self._flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+                self.dist.all_reduce(self._flag)  # completes only after every rank's delivery kernel
+            m = self.dev.apply_received(self.parity, mode, self.stream, count=False)
+        else:
+            torch.cuda.ExternalStream(self.stream).synchronize() if self.stream else torch.cuda.synchronize()
+            self.dist.barrier()  # every rank's deliveries for this parity are complete
+            m = self.dev.apply_received(self.parity, mode, self.stream)
         self.parity ^= 1
         return m
 
