@@ -22,3 +22,12 @@ d.register_kernel(hetm.KERNEL_CACHE)
 for k in range(3):
     d.execute_batch(hetm.KERNEL_CACHE, hetm.gen_cache_batch(30 + k, B, 1 << 22, 0.5, 0 if k == 0 else 900, part=1))
     d.clear_round()
+# fused router (one launch set) for the capture
+import torch
+d2 = hetm.GpuDevice(1 << 20, rs_gran_bytes=1024)
+n = 1 << 20
+log = torch.randint(0, 8 << 20, (n, 3), dtype=torch.int64, device="cuda")
+ent, cnt = d2.recv_arena(8, n)
+for r in range(2):
+    d2.route_to_peers_dptr(log.data_ptr(), n, 8, 1 << 20, 0, n, r & 1, [ent] * 8, [cnt] * 8)
+    d2.sync()
