@@ -310,6 +310,15 @@ def run_ours(args):
     e2e = run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist)
 
     ms_step = ms_total / K
+    # our kernels per step (the ncu launch list in profiles/ shows the same set):
+    # bank_batch_kernel, apply_kernel + restore_kernel, roll_round_kernel (async clear)
+    launches_detail = {"bank_batch_kernel": 1, "apply_kernel": 1, "restore_kernel": 1, "roll_round_kernel": 1}
+    if world > 1 and isinstance(sv, PeerValidator):
+        launches_detail.update({"route_count_kernel": 1, "route_scan_kernel": 1, "route_peer_publish_kernel": 1,
+                                "route_peer_scatter_kernel": 1})
+    elif world > 1:
+        launches_detail.update({"route_count_kernel": 1, "route_scan_kernel": 1, "route_scatter_kernel": 1})
+    launches_per_step = sum(launches_detail.values())
     value = world * B * K / (ms_total / 1e3)
     peak, peak_kind = peaks()
     achieved = TX_BYTES * B / (batch_ms * 1e-3) / 1e9
@@ -341,7 +350,8 @@ def run_ours(args):
         "batch": {"committed_last": int(st.committed), "aborts_last": int(st.aborts)},
         "bank_sum_ok": bank_sum_ok,
         "e2e": e2e,
-        "gpu_launches": K * (2 + (3 if world > 1 else 0)),
+        "gpu_launches": K * launches_per_step,
+        "gpu_launches_per_step": launches_detail,
         "clocks": clk.summary(),
         "input_gen_s": gen_s,
     }
