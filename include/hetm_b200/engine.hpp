@@ -61,6 +61,7 @@ struct RoundReport {
     uint64_t dev_committed = 0;
     uint64_t log_entries = 0;
     uint64_t chunks = 0;
+    uint32_t dev_batches = 0;       // device batches executed in the execution phase
     double exec_ms = 0, validate_ms = 0, merge_ms = 0;
     hetm_batch_stats batch{};
 
@@ -71,13 +72,13 @@ struct RoundReport {
         std::snprintf(buf, sizeof buf,
                       "{\"roundId\": %llu, \"outcome\": \"%s\", \"txCommittedHost\": %llu, "
                       "\"txCommittedDev\": %llu, \"txWastedDev\": %llu, \"bytesLogs\": %llu, \"readOnlyHost\": %d, "
-                      "\"cutShort\": %d, \"execMs\": %.3f, \"validateMs\": %.3f, \"mergeMs\": %.3f}",
+                      "\"cutShort\": %d, \"devBatches\": %u, \"execMs\": %.3f, \"validateMs\": %.3f, \"mergeMs\": %.3f}",
                       (unsigned long long)round_id, names[(int)outcome],
                       (unsigned long long)(outcome == Outcome::HostAborted ? 0 : host_commits),
                       (unsigned long long)(outcome == Outcome::DeviceAborted ? 0 : dev_committed),
                       (unsigned long long)(outcome == Outcome::DeviceAborted ? dev_committed : 0),
                       (unsigned long long)(log_entries * sizeof(hetm_log_entry)), (int)!updates_allowed,
-                      (int)cut_short, exec_ms, validate_ms, merge_ms);
+                      (int)cut_short, dev_batches, exec_ms, validate_ms, merge_ms);
         return buf;
     }
 };
@@ -108,8 +109,30 @@ public:
     using HostWorker = std::function<uint64_t(int thread, const RoundContext& ctx)>;
     uint32_t consecutiveDeviceAborts() const { return dev_aborts_; }
 
+    /// Next device batch of the round: fill inputs/n_tx/tickets_out and return
+    /// true, or return false when the execution budget is spent.
+    struct Batch {
+        const void* inputs = nullptr;
+        uint64_t n_tx = 0;
+        uint64_t* tickets_out = nullptr;
+    };
+    using BatchSource = std::function<bool(uint32_t k, Batch& b)>;
+
+    /// One round with a single device batch.
     RoundReport runRound(int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx, uint64_t* tickets_out,
                          const HostWorker& worker) {
+        return runRoundBatches(kernel_id, rec_bytes, [&](uint32_t k, Batch& b) {
+            if (k) return false;
+            b = Batch{inputs, n_tx, tickets_out};
+            return true;
+        }, worker);
+    }
+
+    /// One round whose execution phase runs device batches back to back until
+    /// `next` ends the budget — or until early validation finds a conflict, which
+    /// ends the phase before the next batch is launched.
+    RoundReport runRoundBatches(int kernel_id, uint64_t rec_bytes, const BatchSource& next,
+                                const HostWorker& worker) {
         RoundReport rep;
         rep.round_id = round_id_++;
         const bool favor_device = cfg_.policy == Policy::FavorDevice;
@@ -123,8 +146,17 @@ public:
         const RoundContext ctx{stop, rep.updates_allowed};
         int gpu_rc = HETM_OK;
         // ---- EXECUTION
-        std::thread gpu([&] {  // GPU-controller
-            gpu_rc = hetm_dev_execute_batch(dev_, kernel_id, inputs, rec_bytes, n_tx, tickets_out, &rep.batch);
+        std::atomic<bool> cut{false};
+        std::thread gpu([&] {  // GPU-controller: batches until the budget ends or a conflict shows
+            Batch b;
+            for (uint32_t k = 0; !cut.load(std::memory_order_acquire) && next(k, b); ++k) {
+                hetm_batch_stats st{};
+                gpu_rc = hetm_dev_execute_batch(dev_, kernel_id, b.inputs, rec_bytes, b.n_tx, b.tickets_out, &st);
+                if (gpu_rc != HETM_OK) break;
+                rep.batch = st;
+                rep.dev_committed += st.committed;
+                ++rep.dev_batches;
+            }
             gpu_done.store(true, std::memory_order_release);
         });
         std::vector<std::thread> hosts;
@@ -134,9 +166,12 @@ public:
         while (!gpu_done.load(std::memory_order_acquire)) {
             stream_full_chunks(stream_mode, rep);
             int c = 0;
-            if (cfg_.early_validation && hetm_dev_poll_conflict(dev_, &c) == HETM_OK && c) {
-                rep.cut_short = true;  // a conflict already dooms the device's round
-                break;
+            if (cfg_.early_validation && !rep.cut_short && hetm_dev_poll_conflict(dev_, &c) == HETM_OK && c) {
+                // a conflict already decides the round: FavorHost dooms the device's
+                // batches (launch no more), FavorDevice dooms the host's transactions (stop them)
+                rep.cut_short = true;
+                if (favor_device) stop.store(true, std::memory_order_release);
+                else cut.store(true, std::memory_order_release);
             }
             std::this_thread::sleep_for(std::chrono::microseconds(50));
         }
@@ -145,7 +180,6 @@ public:
         gpu.join();
         check_rc(gpu_rc, "executeBatch");
         for (uint64_t c : commits) rep.host_commits += c;
-        rep.dev_committed = rep.batch.committed;
         const auto t1 = std::chrono::steady_clock::now();
         // ---- VALIDATION: the log tail (APPLY, or validate-only under FavorDevice),
         // early chunks re-validated + applied (FavorDevice: only on success)

@@ -10,6 +10,7 @@
 // plus host replica == device replica and the bank sum.
 //
 //   round_test [rounds] [log2 words] [batch] [host threads] [conflict every k] [host|device] [starvation k]
+//              [batches per round] [early validation 1|0]
 // policy host (FavorHost, default) or device (FavorDevice: a conflicting round
 // is HostAborted, S' = device batch replay on S, host effects discarded).
 // conflict every k = 1 makes every round conflict (starvation-guard test).
@@ -46,6 +47,8 @@ int main(int argc, char** argv) {
     const int conflict_every = argc > 5 ? std::atoi(argv[5]) : 3;
     const bool favor_device = argc > 6 && std::strcmp(argv[6], "device") == 0;
     const uint32_t starvation_k = argc > 7 ? (uint32_t)std::atoi(argv[7]) : 3;
+    const uint32_t n_batches = argc > 8 ? (uint32_t)std::atoi(argv[8]) : 1;
+    const bool early = argc > 9 ? std::atoi(argv[9]) != 0 : true;
     const uint64_t W = 1ull << log2w, half = W / 2;
 
     hetm_dev_config cfg;
@@ -72,21 +75,25 @@ int main(int argc, char** argv) {
     WriteLog log(T);
     stm.setCommitCallback([&](int t, std::span<const hetm_log_entry> es) { log.append(t, es); });
     EngineConfig ec;
-    ec.chunk_entries = 1u << 12;
+    ec.chunk_entries = n_batches > 1 ? 256 : (1u << 12);  // small chunks: early validation during execution
+    ec.early_validation = early;
     ec.keep_round_log = true;
     ec.policy = favor_device ? Policy::FavorDevice : Policy::FavorHost;
     ec.starvation_k = starvation_k;
     Engine eng(dev, stm, log, host, ec);
 
-    std::vector<uint64_t> ref(host, host + W), dev_words(W), tickets(B), order(B);
-    std::vector<orc_bank_tx> txs(B);
+    std::vector<uint64_t> ref(host, host + W), dev_words(W), tickets((uint64_t)B * n_batches), order((uint64_t)B * n_batches);
+    std::vector<orc_bank_tx> txs((uint64_t)B * n_batches);
+    uint64_t batches_total = 0, wasted = 0;
     uint64_t host_total = 0, dev_total = 0, n_conflict = 0, n_cut = 0, n_guard = 0;
     uint32_t run_aborts = 0, max_run_aborts = 0;
     bool ok = true;
     std::vector<uint64_t> start(W);
     for (int r = 0; r < rounds && ok; ++r) {
         const bool steal = conflict_every > 0 && r % conflict_every == conflict_every - 1;
-        orc_gen_bank_batch(1000 + r, B, 0, half, txs.data());  // device partition [0, W/2)
+        for (uint32_t k = 0; k < n_batches; ++k)  // device partition [0, W/2)
+            orc_gen_bank_batch(1000 + 64 * r + k, B, 0, half, txs.data() + (uint64_t)k * B);
+        std::fill(tickets.begin(), tickets.end(), ~0ull);
         const uint64_t per_thread = 1500;
         auto worker = [&](int t, const RoundContext& ctx) -> uint64_t {
             uint64_t s = orc_splitmix64(7919u * r + t + 1), done = 0;
@@ -113,7 +120,13 @@ int main(int argc, char** argv) {
             }
             return done;
         };
-        RoundReport rep = eng.runRound(HETM_KERNEL_BANK, txs.data(), sizeof(hetm_bank_tx), B, tickets.data(), worker);
+        RoundReport rep = eng.runRoundBatches(HETM_KERNEL_BANK, sizeof(hetm_bank_tx), [&](uint32_t k, Engine::Batch& b) {
+            if (k >= n_batches) return false;
+            b = Engine::Batch{txs.data() + (uint64_t)k * B, B, tickets.data() + (uint64_t)k * B};
+            return true;
+        }, worker);
+        batches_total += rep.dev_batches;
+        if (rep.outcome == Outcome::DeviceAborted) wasted += rep.dev_committed;
         n_conflict += rep.conflict;
         n_cut += rep.cut_short;
         n_guard += !rep.updates_allowed;
@@ -133,7 +146,7 @@ int main(int argc, char** argv) {
         if (rep.outcome != Outcome::HostAborted)
             orc_apply_log_ts_order(ref.data(), 0, reinterpret_cast<const orc_entry*>(hl.data()), hl.size());
         if (rep.outcome != Outcome::DeviceAborted) {
-            const uint64_t m = orc_order_by_ticket(tickets.data(), B, order.data());
+            const uint64_t m = orc_order_by_ticket(tickets.data(), tickets.size(), order.data());
             orc_bank_replay(ref.data(), 0, txs.data(), order.data(), m, nullptr, nullptr, nullptr, 1024, 16384);
         }
         if (std::memcmp(ref.data(), host, W * 8) != 0) {
@@ -158,10 +171,11 @@ int main(int argc, char** argv) {
     }
     std::printf("{\"rounds\": %d, \"ok\": %d, \"policy\": \"%s\", \"host_commits\": %llu, \"dev_commits\": %llu, "
                 "\"conflict_rounds\": %llu, \"cut_short\": %llu, \"guard_rounds\": %llu, \"max_consecutive_device_aborts\": %u, "
-                "\"host_aborts\": %llu}\n",
+                "\"host_aborts\": %llu, \"device_batches\": %llu, \"wasted_device_tx\": %llu}\n",
                 rounds, (int)ok, favor_device ? "FavorDevice" : "FavorHost", (unsigned long long)host_total,
                 (unsigned long long)dev_total, (unsigned long long)n_conflict, (unsigned long long)n_cut,
-                (unsigned long long)n_guard, max_run_aborts, (unsigned long long)stm.aborts());
+                (unsigned long long)n_guard, max_run_aborts, (unsigned long long)stm.aborts(),
+                (unsigned long long)batches_total, (unsigned long long)wasted);
     hetm_host_free(host);
     hetm_dev_close(dev);
     return ok ? 0 : 1;

@@ -59,3 +59,23 @@ def test_starvation_guard_lets_the_device_commit():
     summary = json.loads(r.stdout.strip().splitlines()[-1])
     assert summary["ok"] == 1 and summary["guard_rounds"] >= 2
     assert summary["max_consecutive_device_aborts"] <= 3
+
+
+@pytest.mark.gpu
+def test_early_validation_cuts_the_execution_phase():
+    """SPEC.md:354-362 / acceptance #9: with several device
+    batches per round and a host that conflicts every round, early validation
+    stops launching device batches once a streamed chunk hits the read set, so
+    the device wastes less work than the same seeds without early validation."""
+    def run(early):
+        r = subprocess.run([_exe("round_test"), "6", "20", "4096", "4", "1", "host", "1000", "16", early],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    on, off = run("1"), run("0")
+    assert on["ok"] == 1 and off["ok"] == 1
+    assert on["conflict_rounds"] == off["conflict_rounds"] == 6
+    assert on["cut_short"] >= 1 and off["cut_short"] == 0
+    assert off["device_batches"] == 6 * 16
+    assert on["device_batches"] < off["device_batches"]
+    assert on["wasted_device_tx"] < off["wasted_device_tx"]
