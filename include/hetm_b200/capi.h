@@ -88,6 +88,9 @@ enum hetm_kernel_id {
 /* hetm_dev_config.flags */
 #define HETM_CFG_NO_SHADOW 1u /* do not allocate devShadow (validation-only sweeps) */
 #define HETM_CFG_L2_FETCH_32 2u /* cudaLimitMaxL2FetchGranularity = 32 B (random 8-B word access) */
+#define HETM_CFG_DETERMINISTIC 8u /* deterministic single-worker batches: transactions
+                                     commit one at a time in input order, ticket i = first + i
+                                     (reproducible runs; orders of magnitude slower) */
 #define HETM_CFG_MERGE_DELTA 4u /* mergeCommit ships the device write set as {word, value} records
                                    (16 B per written word) when that is smaller than the dirty
                                    chunks; recorded as HETM_TAG_MERGE_DELTA.  Off: the SPEC.md:

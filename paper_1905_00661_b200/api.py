@@ -27,6 +27,7 @@ CLEAR_ASYNC = 2
 CFG_NO_SHADOW = 1
 CFG_L2_FETCH_32 = 2
 CFG_MERGE_DELTA = 4
+CFG_DETERMINISTIC = 8
 H2D, D2H, D2D = 0, 1, 2  # BusDir, bus.hpp:16
 TAG_LOG, TAG_MERGE, TAG_SHADOW, TAG_ROLLBACK, TAG_INPUT, TAG_OUTPUT, TAG_RAW, TAG_MERGE_DELTA = range(8)
 
@@ -208,7 +209,7 @@ class GpuDevice:
     def __init__(self, size_words: int, *, shard_base: int = 0, rs_gran_bytes: int = 1024,
                  chunk_bytes: int = 16384, log_capacity: int = 0,
                  max_attempts: int = 0, device: int = 0, shadow: bool = True, l2_fetch_32: bool = False,
-                 merge_delta: bool = False):
+                 merge_delta: bool = False, deterministic: bool = False):
         cfg = _lib.DevConfig()
         lib.hetm_dev_config_default(C.byref(cfg))
         cfg.size_words = size_words
@@ -219,7 +220,7 @@ class GpuDevice:
         cfg.max_attempts = max_attempts
         cfg.device = device
         cfg.flags = ((0 if shadow else CFG_NO_SHADOW) | (CFG_L2_FETCH_32 if l2_fetch_32 else 0)
-                     | (CFG_MERGE_DELTA if merge_delta else 0))
+                     | (CFG_MERGE_DELTA if merge_delta else 0) | (CFG_DETERMINISTIC if deterministic else 0))
         h = C.c_void_p()
         check(lib.hetm_dev_open(C.byref(cfg), C.byref(h)))
         self.h = h

@@ -66,8 +66,9 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0, wlog_full = 0;
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t i0, stride;
+    tx_range(v, n, i0, stride);
+    for (uint64_t i = i0; i < n; i += stride) {
         const hetm_cache_tx r = in[i];
         const uint64_t s0 = cg.base_local + cache_set_of(r.key[0], r.key[1], cg.n_sets) * kSetWords;
         if (s0 + kSetWords > v.size_words) {

@@ -193,6 +193,7 @@ struct hetm_dev {
         v.chunk_shift = chunk_shift;
         v.wlog = d_wlog;
         v.wlog_slots = wlog_slots;
+        v.serial = (cfg.flags & HETM_CFG_DETERMINISTIC) ? 1u : 0u;
         return v;
     }
     std::mutex xfer_mu;  // record() is reached from the GPU-controller and the log streamer threads

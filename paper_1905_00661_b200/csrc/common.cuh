@@ -72,7 +72,22 @@ struct ShardView {
     uint32_t chunk_shift;      // chunk = local_word >> chunk_shift
     uint32_t* wlog;            // device write-set log (nullptr: disabled, shard >= 2^32 words)
     uint64_t wlog_slots;       // its capacity in slots
+    uint32_t serial;           // deterministic single-worker mode (HETM_CFG_DETERMINISTIC)
 };
+
+// First transaction and stride of the calling thread in a batch kernel.  In the
+// deterministic single-worker mode global thread 0 runs every
+// transaction in input order, so ticket i = first ticket + i.
+__device__ __forceinline__ void tx_range(const ShardView& v, uint64_t n, uint64_t& i, uint64_t& stride) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v.serial) {
+        i = tid == 0 ? 0 : n;
+        stride = 1;
+    } else {
+        i = tid;
+        stride = (uint64_t)gridDim.x * blockDim.x;
+    }
+}
 
 // Cache region of HETM_KERNEL_CACHE (capi.h hetm_cache_*): n_sets sets of
 // HETM_CACHE_SET_WORDS words from local word base_local.

@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                                                                    DevCounters* ctr, uint32_t max_attempts) {
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t i, stride;
+    tx_range(v, n, i, stride);
     uint32_t attempts = 0;
     bool loaded = false;
     uint64_t amount = 0;
@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0;
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t i0, stride;
+    tx_range(v, n, i0, stride);
+    for (uint64_t i = i0; i < n; i += stride) {
         const hetm_rw_tx r = in[i];
         const uint32_t nr = r.nr < 4 ? r.nr : 4, nw = r.nw < 2 ? r.nw : 2;
         bool in_shard = true;
