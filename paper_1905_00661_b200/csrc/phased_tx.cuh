@@ -98,7 +98,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
                                                unsigned long long* ticket_ctr, unsigned long long& ticket,
                                                Compute compute, unsigned long long* clocks = nullptr) {
     bool ok = active;
-    tx.block_lk = 0;
+    if (active) tx.block_lk = 0;  // a sitting-out lane keeps its blocker
     long long tclk = 0;
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) tclk = clock64();
     if constexpr ((KO & KO_PROTOCOL) != 0) {  // access-pattern floor

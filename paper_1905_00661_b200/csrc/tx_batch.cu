@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
     bool loaded = false;
     uint64_t amount = 0;
     StaticTx<4, 2> tx;
+    tx.block_lk = 0;
+    uint32_t backoff = 0;
+    unsigned long long rng = 0x9e3779b97f4a7c15ull * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1);
     unsigned long long clocks[6] = {0, 0, 0, 0, 0, 0};
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
     while (__any_sync(0xffffffffu, i < n)) {
@@ -72,7 +75,20 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                 loaded = true;
             }
         }
-        const bool active = i < n && loaded;
+        // A lane whose last attempt was stopped by a FINAL holder sits out (one
+        // poll of that word per warp iteration) until the holder releases it,
+        // so the other lanes of the warp keep committing meanwhile.
+        bool blocked = false;
+        if (i < n && loaded && tx.block_lk) {
+            blocked = ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk;
+            if (!blocked) tx.block_lk = 0;
+        }
+        if (i < n && loaded && backoff) {  // randomized sit-out after repeated version-change aborts
+            --backoff;
+            blocked = true;
+        }
+        if (__all_sync(0xffffffffu, blocked || !(i < n && loaded))) __nanosleep(256);  // whole warp waits
+        const bool active = i < n && loaded && !blocked;
         unsigned long long t = ~0ull;
         const bool committed =
             phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, [&](StaticTx<4, 2>& x) {
@@ -90,14 +106,17 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                 wlog_put(v, wbase, t, 1, ~0u);
             }
             ++aborts;
-            if (tx.block_lk) {  // wait for the FINAL holder to release, then retry
+            if (tx.block_lk && attempts < 4) {  // mild contention: the holder is mid-commit, wait in place briefly
                 uint32_t ns = 32;
-                for (int p = 0; p < 256 && ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk; ++p) {
+                for (int p = 0; p < 16 && ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk; ++p) {
                     __nanosleep(ns);
-                    ns = ns < 1024 ? 2 * ns : ns;
+                    ns = ns < 512 ? 2 * ns : ns;
                 }
-            } else if (attempts >= 8) {
-                __nanosleep(attempts < 64 ? 16u * attempts : 1024u);
+                tx.block_lk = 0;
+            }
+            if (!tx.block_lk && attempts >= 4) {  // hot word: spread the retries over 2^min(attempts-1, 6 / 10 from 32) iterations
+                rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                backoff = (uint32_t)(rng >> 40) & ((1u << (attempts < 7 ? attempts - 1 : (attempts < 32 ? 6 : 10))) - 1u);
             }
             if (++attempts < max_attempts) continue;
             tickets[i] = ~0ull;
@@ -108,6 +127,8 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         i += stride;
         loaded = false;
         attempts = 0;
+        tx.block_lk = 0;
+        backoff = 0;
     }
     if constexpr ((KO & KO_COUNT_TICKETS) != 0) {
         const unsigned long long x = warp_sum(clocks[0]);
