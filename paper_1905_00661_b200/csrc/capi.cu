@@ -28,6 +28,8 @@
 
 #include <sys/mman.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "device_tm.cuh"
 #include "kernels.h"
@@ -40,6 +42,13 @@ int query_val_occupancy(int* blocks);
 using namespace hetm_b200;
 
 namespace {
+// NVTX range per round phase (execute / stream / verdict / merge / clear /
+// exchange) for nsys timelines; header-only nvtx3, no-ops without a tool.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Persistent host workers for the delta merge: start(f) runs f(w, n) once on
 // every worker w in [0, n) and returns immediately; wait() joins that job.
 class WorkerPool {
@@ -699,6 +708,7 @@ int hetm_dev_execute_batch(hetm_dev* d, int kernel_id, const void* inputs, uint6
 int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx,
                               uint64_t* tickets_out, void* results_out, uint64_t res_bytes,
                               hetm_batch_stats* stats) {
+    NvtxRange nvtx_range("hetm.executeBatch");
     if (!d || (!inputs && n_tx)) return HETM_ERR_INVALID_ARG;
     if (!d->kernels.count(kernel_id)) return HETM_ERR_KERNEL_NOT_REGISTERED;
     if (rec_bytes != record_bytes(kernel_id)) return HETM_ERR_INVALID_SIZE;
@@ -836,6 +846,7 @@ int hetm_dev_close_intake(hetm_dev* d) {
 
 int hetm_dev_stream_chunk(hetm_dev* d, const hetm_log_entry* entries, uint64_t n, int src_thread, uint64_t seq,
                           int mode) {
+    NvtxRange nvtx_range("hetm.streamChunk");
     (void)src_thread;
     (void)seq;
     if (!d || (!entries && n)) return HETM_ERR_INVALID_ARG;
@@ -881,6 +892,7 @@ int hetm_dev_poll_conflict(hetm_dev* d, int* conflict) {
 }
 
 int hetm_dev_round_verdict(hetm_dev* d, int* conflict) {
+    NvtxRange nvtx_range("hetm.roundVerdict");
     if (!d || !conflict) return HETM_ERR_INVALID_ARG;
     std::lock_guard<std::mutex> g(d->mu);
     // Chunks validated only early (possibly before the batch finished setting
@@ -1022,6 +1034,7 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
 }  // namespace
 
 int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
+    NvtxRange nvtx_range("hetm.mergeCommit");
     if (!d || !host) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> g(d->mu);
@@ -1087,6 +1100,7 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
 }
 
 int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host, hetm_merge_stats* st) {
+    NvtxRange nvtx_range("hetm.mergeAbortDevice");
     if (!d || (!host && !optimized)) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> g(d->mu);
@@ -1148,6 +1162,7 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
 }
 
 int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snapshot, hetm_merge_stats* st) {
+    NvtxRange nvtx_range("hetm.mergeAbortHost");
     if (!d || !host || !snapshot) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> g(d->mu);
@@ -1207,6 +1222,7 @@ int hetm_dev_merge_wait(hetm_dev* d) {
 }
 
 int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
+    NvtxRange nvtx_range("hetm.clearRound");
     if (!d) return HETM_ERR_INVALID_ARG;
     std::lock_guard<std::mutex> g(d->mu);
     int rc = wait_round_work(d, d->s_merge);
@@ -1390,6 +1406,7 @@ int hetm_dev_recv_arena(hetm_dev* d, uint32_t n_shards, uint64_t cap, void** d_e
 int hetm_dev_route_to_peers_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64_t n, uint32_t n_shards,
                                  uint64_t shard_words, uint32_t my_shard, uint64_t cap, uint32_t parity,
                                  void* const* peer_entries, void* const* peer_counts, void* stream) {
+    NvtxRange nvtx_range("hetm.routeToPeers");
     if (!d || (n && !d_in) || !peer_entries || !peer_counts) return HETM_ERR_INVALID_ARG;
     if (n_shards == 0 || n_shards > 64 || shard_words == 0 || my_shard >= n_shards) return HETM_ERR_CONFIG;
     if (n > cap) return HETM_ERR_INVALID_SIZE;
@@ -1421,6 +1438,7 @@ int hetm_dev_route_to_peers_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64
 }
 
 int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_out, void* stream) {
+    NvtxRange nvtx_range("hetm.applyReceived");
     if (!d || !d->d_recv) return HETM_ERR_INVALID_ARG;
     if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
