@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
     unsigned long long commits = 0, aborts = 0, livelocks = 0;
     unsigned oob = 0, wlog_full = 0;
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
+    unsigned long long rng = 0x9e3779b97f4a7c15ull * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1);
     uint64_t i0, stride;
     tx_range(v, n, i0, stride);
     for (uint64_t i = i0; i < n; i += stride) {
@@ -203,6 +204,10 @@ __global__ void __launch_bounds__(kCacheThreads) cache_batch_kernel(ShardView v,
                     __nanosleep(ns);
                     ns = ns < 1024 ? 2 * ns : ns;
                 }
+            } else if (attempt >= 3) {  // hot set: jittered exponential backoff before re-reading it
+                rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                const uint32_t cap = 64u << (attempt < 8 ? attempt : 8);
+                __nanosleep((uint32_t)(rng >> 40) % cap);
             }
             if (attempt >= max_attempts) {
                 tickets[i] = ~0ull;
