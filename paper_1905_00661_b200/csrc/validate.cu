@@ -185,6 +185,127 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView
     flush_pass_a(f, ctr);
 }
 
+// ---- TMA-staged apply (flat, 16-B aligned logs): one persistent CTA per SM
+// walks tiles of kTile log entries; the tile after next is fetched into
+// shared memory by the bulk-copy engine (cp.async.bulk + mbarrier, SASS
+// UBLKCP) while the threads run the random TS RMWs of the current tile, so
+// the streaming log read never sits in front of the atomics.  Same per-entry
+// logic (and restore queue) as apply_kernel.
+constexpr int kTile = 1024;                                   // entries per stage (24 KiB)
+constexpr unsigned kTileBytes = kTile * sizeof(hetm_log_entry);
+static_assert(kTileBytes % 16 == 0, "bulk copies move multiples of 16 B");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(phase)
+                     : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(kValThreads) apply_tma_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
+                                                                uint64_t n, DevCounters* ctr,
+                                                                unsigned long long* __restrict__ restore) {
+    extern __shared__ __align__(128) unsigned char apply_smem[];
+    auto buf = reinterpret_cast<hetm_log_entry(*)[kTile]>(apply_smem);  // two stages
+    __shared__ alignas(8) uint64_t bar[2];
+    const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
+    const uint64_t full_tiles = n / kTile;  // the partial tail tile is read straight from global memory
+    const uint64_t tiles = (n + kTile - 1) / kTile;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // prologue: this CTA's first two full tiles
+    for (int st = 0; st < 2; ++st) {
+        const uint64_t t = blockIdx.x + (uint64_t)st * gridDim.x;
+        if (threadIdx.x == 0 && t < full_tiles) {
+            mbar_expect_tx(&bar[st], kTileBytes);
+            bulk_g2s(buf[st], log + t * kTile, kTileBytes, &bar[st]);
+        }
+    }
+    PassAFlags f;
+    uint32_t phase[2] = {0, 0};
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int st = it & 1;
+        const bool staged = t < full_tiles;
+        if (staged) {
+            mbar_wait(&bar[st], phase[st]);
+            phase[st] ^= 1;
+        }
+        constexpr int U = kTile / kValThreads;
+        EntryRegs e[U];
+        unsigned long long old[U];
+        const uint64_t base_i = t * kTile;
+        const uint64_t m = staged ? kTile : n - base_i;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t j = threadIdx.x + u * kValThreads;
+            if (j < m) {
+                if (staged) {
+                    const hetm_log_entry& x = buf[st][j];
+                    e[u] = EntryRegs{x.addr, x.value, x.ts};
+                } else {
+                    e[u] = load_entry(log, base_i + j);
+                }
+            } else {
+                e[u] = EntryRegs{v.base + v.size_words, 0, 0};
+            }
+        }
+        __syncthreads();  // every thread has its entries: the stage can be refilled
+        if (threadIdx.x == 0) {
+            const uint64_t nt = t + 2 * (uint64_t)gridDim.x;
+            if (nt < full_tiles) {
+                mbar_expect_tx(&bar[st], kTileBytes);
+                bulk_g2s(buf[st], log + nt * kTile, kTileBytes, &bar[st]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t loc = e[u].addr - v.base;
+            old[u] = ~0ull;
+            if (threadIdx.x + u * kValThreads >= m) continue;
+            if (loc >= v.size_words) {
+                f.oob = 1;
+                continue;
+            }
+            const uint64_t bit = loc >> v.gran_shift;
+            f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
+            f.bad |= (e[u].ts <= ts_floor);
+            f.maxts = e[u].ts > f.maxts ? e[u].ts : f.maxts;
+            old[u] = atomicMax(&v.cells[loc].meta, ts_meta(e[u].ts));  // (b) TS raise
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (old[u] >= ts_meta(e[u].ts)) continue;
+            v.cells[e[u].addr - v.base].value = e[u].value;
+            if ((old[u] & kTsTag) && (old[u] & ~kTsTag) > ts_floor) {
+                const unsigned long long k = atomicAdd(&ctr->restore_n, 1ull);
+                if (k < kRestoreCap) restore[k] = base_i + threadIdx.x + u * kValThreads;
+            }
+        }
+    }
+    flush_pass_a(f, ctr);
+}
+
 // Re-store the queued entries whose ts is still the cell's TS (the unique
 // freshest one per word).  If the queue overflowed, every entry of the launch
 // is checked (pass B of the classic two-pass scheme).  The last block to
@@ -333,6 +454,20 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
     const int bps = apply_bps > 0 ? apply_bps : 1;
     const int u = apply_unroll == 2 || apply_unroll == 8 ? apply_unroll : 4;
     const unsigned agrid = grid_cap((n_hint + u - 1) / u, kValThreads, g, bps);
+    static const bool tma = [] {  // experiment only (HETM_APPLY_TMA=1): measured no faster, profiles/r01_apply_tma.txt
+        const char* e = std::getenv("HETM_APPLY_TMA");
+        return e && std::atoi(e) != 0;
+    }();
+    if (tma && !lv.segments && (reinterpret_cast<uintptr_t>(lv.base) & 15) == 0 && n_hint >= (uint64_t)kTile) {
+        const uint64_t tiles = (n_hint + kTile - 1) / kTile;
+        const unsigned tgrid = (unsigned)(tiles < (uint64_t)g.sm_count ? tiles : (uint64_t)g.sm_count);
+        static const cudaError_t attr =
+            cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileBytes);
+        if (attr != cudaSuccess) return attr;
+        apply_tma_kernel<<<tgrid, kValThreads, 2 * kTileBytes, s>>>(v, lv.base, n_hint, ctr, d_restore);
+        restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+        return cudaGetLastError();
+    }
     if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
     else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
     else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
