@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--log-entries", type=int, default=1 << 20)
     p.add_argument("--gran", type=int, default=1024)
     p.add_argument("--l2-fetch32", action="store_true", help="cudaLimitMaxL2FetchGranularity = 32 B")
-    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--chunk-merge", action="store_true", help="SPEC chunk-copy merge instead of the delta merge")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--no-cpu-baseline", action="store_true")

@@ -11,6 +11,7 @@
 // Events carry every cross-stream dependency; nothing blocks the host except
 // the explicitly synchronous calls (verdict, merge_wait, snapshots, stats).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
@@ -160,7 +161,10 @@ struct hetm_dev {
     unsigned flush_gen = 0;
 
     cudaStream_t s_exec = nullptr, s_copy = nullptr, s_val = nullptr, s_merge = nullptr, s_d2h = nullptr,
-                 s_zc = nullptr;  // s_zc: zero-copy delta stores into the host replica
+                 s_zc = nullptr,  // s_zc: zero-copy delta stores into the host replica
+        s_in = nullptr, s_out = nullptr;  // pipelined host-input batches: input pieces in, tickets/results out
+    std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
+    std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
     cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
                 ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_copy_zc = nullptr;
     bool intake_open = true;
@@ -308,11 +312,11 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
-                  void* d_results, cudaStream_t s) {
+                  void* d_results, cudaStream_t s, bool reset_counters = true) {
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
-    CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
+    if (reset_counters) CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
     cudaError_t e = cudaSuccess;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (d->timing) {
@@ -550,7 +554,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     CK(d, cudaMemset(d->d_chunk, 0, d->chunk_words * 8));
     CK(d, cudaMemset(d->d_ctr, 0, sizeof(DevCounters)));
 
-    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc})
+    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc, &d->s_in, &d->s_out})
         CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc})
         CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -584,11 +588,13 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
 int hetm_dev_close(hetm_dev* d) {
     if (!d) return HETM_ERR_INVALID_ARG;
     cudaSetDevice(d->device);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamSynchronize(s);
     d->pool.reset();
     if (d->h_delta) cudaFreeHost(d->h_delta);
     for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush})
@@ -600,7 +606,7 @@ int hetm_dev_close(hetm_dev* d) {
             cudaEventDestroy(pr.second);
         }
     for (cudaEvent_t e : d->tpool) cudaEventDestroy(e);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1,
                           d->ev_copy_zc})
@@ -705,6 +711,17 @@ int hetm_dev_execute_batch(hetm_dev* d, int kernel_id, const void* inputs, uint6
     return hetm_dev_execute_batch_ex(d, kernel_id, inputs, rec_bytes, n_tx, tickets_out, nullptr, 0, stats);
 }
 
+// Pieces of a host-input batch: one per 2^17 transactions, at most 8
+// (HETM_EXEC_PIECES overrides, for experiments; 1 = unpipelined).
+static uint64_t exec_pieces(uint64_t n_tx) {
+    static const long want = [] {
+        const char* e = std::getenv("HETM_EXEC_PIECES");
+        return e ? std::atol(e) : 0L;
+    }();
+    uint64_t p = want > 0 ? (uint64_t)want : std::min<uint64_t>(8, n_tx >> 17);
+    return std::max<uint64_t>(1, std::min<uint64_t>(p, std::max<uint64_t>(n_tx, 1)));
+}
+
 int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, uint64_t rec_bytes, uint64_t n_tx,
                               uint64_t* tickets_out, void* results_out, uint64_t res_bytes,
                               hetm_batch_stats* stats) {
@@ -735,26 +752,58 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     CK(d, cudaMemcpyAsync(&d->h_ctr->ticket, &d->d_ctr->ticket, 8, cudaMemcpyDeviceToHost, s));
     CK(d, cudaStreamSynchronize(s));
     const uint64_t first = d->h_ctr->ticket;
-    if (n_tx) {
-        CK(d, cudaMemcpyAsync(d->d_in, inputs, n_tx * rec_bytes, cudaMemcpyHostToDevice, s));
-        d->record(HETM_H2D, HETM_TAG_INPUT, n_tx * rec_bytes);
-    }
     CK(d, cudaMemsetAsync(&d->d_ctr->oob, 0, sizeof(unsigned), s));
-    CK(d, cudaEventRecord(d->ev_t0, s));
-    if ((rc = enqueue_batch(d, kernel_id, d->d_in, n_tx, d->d_tk, results_out ? d->d_res : nullptr, s))) return rc;
-    CK(d, cudaEventRecord(d->ev_t1, s));
-    if (tickets_out && n_tx) {
-        CK(d, cudaMemcpyAsync(tickets_out, d->d_tk, n_tx * 8, cudaMemcpyDeviceToHost, s));
-        d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * 8);
+    // Pipelined pieces: the H2D of piece k+1 (s_in) overlaps the kernel on
+    // piece k (s_exec), whose tickets/results return on s_out while later
+    // pieces run.  The pieces run back to back on s_exec, so the batch is
+    // still one serializable execution (and input order in deterministic mode).
+    const uint64_t P = exec_pieces(n_tx);
+    while (d->in_ev.size() < P) {
+        cudaEvent_t e = nullptr;
+        CK(d, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        d->in_ev.push_back(e);
     }
-    if (results_out && n_tx) {
-        CK(d, cudaMemcpyAsync(results_out, d->d_res, n_tx * res_bytes, cudaMemcpyDeviceToHost, s));
-        d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * res_bytes);
+    while (d->kp_ev.size() < 2 * P) {
+        cudaEvent_t e = nullptr;
+        CK(d, cudaEventCreate(&e));
+        d->kp_ev.push_back(e);
     }
+    const char* in_h = static_cast<const char*>(inputs);
+    char* in_d = static_cast<char*>(d->d_in);
+    for (uint64_t k = 0; k < P; ++k) {
+        const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
+        if (m) {
+            CK(d, cudaMemcpyAsync(in_d + lo * rec_bytes, in_h + lo * rec_bytes, m * rec_bytes, cudaMemcpyHostToDevice,
+                                  d->s_in));
+            CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
+            CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
+        }
+        CK(d, cudaEventRecord(d->kp_ev[2 * k], s));
+        if ((rc = enqueue_batch(d, kernel_id, in_d + lo * rec_bytes, m, d->d_tk + lo,
+                                results_out ? d->d_res + lo : nullptr, s, k == 0)))
+            return rc;
+        CK(d, cudaEventRecord(d->kp_ev[2 * k + 1], s));
+        if (m && (tickets_out || results_out)) {
+            CK(d, cudaStreamWaitEvent(d->s_out, d->kp_ev[2 * k + 1], 0));
+            if (tickets_out)
+                CK(d, cudaMemcpyAsync(tickets_out + lo, d->d_tk + lo, m * 8, cudaMemcpyDeviceToHost, d->s_out));
+            if (results_out)
+                CK(d, cudaMemcpyAsync(static_cast<char*>(results_out) + lo * res_bytes, d->d_res + lo, m * res_bytes,
+                                      cudaMemcpyDeviceToHost, d->s_out));
+        }
+    }
+    if (n_tx) d->record(HETM_H2D, HETM_TAG_INPUT, n_tx * rec_bytes);
+    if (tickets_out && n_tx) d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * 8);
+    if (results_out && n_tx) d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * res_bytes);
     CK(d, cudaMemcpyAsync(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(d, cudaStreamSynchronize(s));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, d->ev_t0, d->ev_t1);
+    CK(d, cudaStreamSynchronize(d->s_out));
+    float ms = 0.f;  // kernel time only: the sum over pieces
+    for (uint64_t k = 0; k < P; ++k) {
+        float mk = 0.f;
+        cudaEventElapsedTime(&mk, d->kp_ev[2 * k], d->kp_ev[2 * k + 1]);
+        ms += mk;
+    }
     hetm_batch_stats st{};
     st.n_tx = n_tx;
     st.committed = d->h_ctr->committed;
@@ -923,6 +972,7 @@ int hetm_dev_sync(hetm_dev* d) {
 // ------------------------------------------------------------------- merge
 namespace {
 constexpr uint64_t kDeltaPiece = 1ull << 17;  // delta records per D2H piece (2 MiB)
+static_assert(kDeltaPiece % 8192 == 0, "host scatter blocks must not straddle pieces");
 
 // mergeCommit, delta form: the round's write-set log becomes a compact
 // {word, value} list (16 B per written word instead of 16 KiB per dirty
@@ -949,8 +999,14 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
         d->delta_cap = cap;
     }
     if (!d->pool) {
+        // one core is left to the controller thread (it spin-waits on CUDA)
         const unsigned hc = std::thread::hardware_concurrency();
-        d->pool.reset(new WorkerPool((int)std::max(1u, std::min(16u, hc ? hc : 4u))));
+        static const unsigned want = [] {
+            const char* e = std::getenv("HETM_MERGE_THREADS");
+            return e ? (unsigned)std::atoi(e) : 0u;
+        }();
+        const unsigned n = want ? want : std::min(32u, hc > 1 ? hc - 1 : 4u);
+        d->pool.reset(new WorkerPool((int)std::max(1u, n)));
     }
     if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
     // shadow: incremental when it held the round-start state, else a full copy
@@ -979,7 +1035,9 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
     // the host workers deliver the rest — two independent paths into host DRAM.
     static const double zc_frac = [] {
         const char* e = std::getenv("HETM_ZC_FRACTION");
-        return e ? std::atof(e) : 0.5;  // measured best split (profiles/r01_e2e_zc_split.txt)
+        // 0 since the host scatter prefetches: the zero-copy stores then only
+        // slow the next batch's input H2D (profiles/r01_e2e_timeline.txt)
+        return e ? std::atof(e) : 0.0;
     }();
     uint64_t n_zc = 0;
     cudaPointerAttributes pa{};
@@ -1019,14 +1077,43 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
     const DeltaRec* src = d->h_delta;
     const std::vector<cudaEvent_t> evs(d->piece_ev.begin(), d->piece_ev.begin() + pieces);
     const int dev = d->device;
-    d->pool->start([src, evs, host, n_slots, dev, k0](int w, int nw) {
+    // Dynamic blocks in sorted order: a worker that the OS deschedules delays
+    // only the block it holds, not a static 1/nw share of every piece.  Piece
+    // arrival is polled by one worker at a time (cudaEventQuery under a
+    // try-lock) and published through `landed`.
+    struct ScatterState {
+        std::atomic<uint64_t> cursor{0};  // next record to claim
+        std::atomic<uint64_t> landed{0};  // pieces known to be in h_delta
+        std::mutex waiter;                // one worker at a time polls the driver
+    };
+    auto st = std::make_shared<ScatterState>();
+    st->cursor = k0 * kDeltaPiece;
+    st->landed = k0;
+    d->pool->start([src, evs, host, n_slots, dev, st](int, int) {
         cudaSetDevice(dev);
-        for (uint64_t k = k0; k < evs.size(); ++k) {
-            cudaEventSynchronize(evs[k]);
-            const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
-            const uint64_t a = lo + m * w / nw, b = lo + m * (w + 1) / nw;
-            for (uint64_t i = a; i < b; ++i)
+        constexpr uint64_t kBlock = 8192;   // records per claim (divides kDeltaPiece)
+        constexpr uint64_t kPrefetch = 64;  // prefetch-for-write distance, see below
+        for (;;) {
+            const uint64_t a = st->cursor.fetch_add(kBlock, std::memory_order_relaxed);
+            if (a >= n_slots) return;
+            const uint64_t b = std::min(a + kBlock, n_slots), k = a / kDeltaPiece;
+            while (st->landed.load(std::memory_order_acquire) <= k) {
+                if (st->waiter.try_lock()) {  // the others spin on `landed`, not in the driver
+                    uint64_t l = st->landed.load(std::memory_order_relaxed);
+                    while (l <= k && cudaEventQuery(evs[l]) == cudaSuccess) ++l;
+                    st->landed.store(l, std::memory_order_release);
+                    st->waiter.unlock();
+                }
+                std::this_thread::yield();
+            }
+            // x86 drains stores in order, so without the prefetch the random RFO
+            // misses serialise (3.3 vs 1.8 G words/s on the box's 16 cores,
+            // profiles/r01_host_scatter_probe.txt)
+            for (uint64_t i = a; i < b; ++i) {
+                if (i + kPrefetch < b && src[i + kPrefetch].loc != ~0ull)
+                    __builtin_prefetch(&host[src[i + kPrefetch].loc], 1, 0);
                 if (src[i].loc != ~0ull) host[src[i].loc] = src[i].value;
+            }
         }
     });
     return HETM_OK;
