@@ -27,6 +27,7 @@
 #include <utility>
 #include <vector>
 
+#include <sched.h>
 #include <sys/mman.h>
 
 #include <nvtx3/nvToolsExt.h>
@@ -999,13 +1000,20 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
         d->delta_cap = cap;
     }
     if (!d->pool) {
-        // one core is left to the controller thread (it spin-waits on CUDA)
-        const unsigned hc = std::thread::hardware_concurrency();
+        // this process's share of the usable cores (torchrun runs one process
+        // per GPU: LOCAL_WORLD_SIZE), one core left to the controller thread
+        // (it spin-waits on CUDA)
         static const unsigned want = [] {
             const char* e = std::getenv("HETM_MERGE_THREADS");
             return e ? (unsigned)std::atoi(e) : 0u;
         }();
-        const unsigned n = want ? want : std::min(32u, hc > 1 ? hc - 1 : 4u);
+        unsigned cores = std::thread::hardware_concurrency();
+        cpu_set_t cs;
+        if (sched_getaffinity(0, sizeof(cs), &cs) == 0) cores = (unsigned)CPU_COUNT(&cs);
+        const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+        const unsigned procs = lws ? std::max(1, std::atoi(lws)) : 1u;
+        const unsigned share = std::max(1u, (cores ? cores : 4u) / procs);
+        const unsigned n = want ? want : std::min(32u, share > 1 ? share - 1 : 1u);
         d->pool.reset(new WorkerPool((int)std::max(1u, n)));
     }
     if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));

@@ -115,7 +115,10 @@ __global__ void route_peer_publish_kernel(unsigned long long* offsets, const uns
     const unsigned long long start = offsets[(uint64_t)s * n_warps];
     __syncthreads();
     for (uint64_t w = threadIdx.x; w < n_warps; w += blockDim.x) offsets[(uint64_t)s * n_warps + w] -= start;
-    if (threadIdx.x == 0) peer_counts[s][my] = totals[s];
+    if (threadIdx.x == 0) {
+        peer_counts[s][my] = totals[s];
+        __threadfence_system();  // the owner reads it after the round barrier
+    }
 }
 
 __global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(const hetm_log_entry* __restrict__ in, uint64_t n,
@@ -210,6 +213,11 @@ __global__ void __launch_bounds__(kRouteThreads) route_peer_scatter_kernel(
             if (s != 0xffffffffu) (s < 32 ? p0 + my0 : p1 + my1)[rank] = ev[u];
         }
     }
+    // Peer stores over NVLink: make them visible system-wide before this kernel
+    // completes, so the round barrier that follows on the stream (an NCCL
+    // all-reduce, or a host barrier after a stream sync) orders them before
+    // the owner's apply.
+    __threadfence_system();
 }
 
 static unsigned route_grid(uint64_t n, const LaunchGeom& g) {
