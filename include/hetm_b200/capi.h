@@ -382,6 +382,59 @@ int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
 
+/* ---------------------------------------------------- checker support -- *
+ * Traces for the P1 / P2-dagger consistency checker (the
+ * `checker` module).  Recording is toggleable and lossless:
+ * events carry values, not just addresses.
+ *
+ * hetm_dev_trace_next_batch arms the NEXT hetm_dev_execute_batch /
+ * hetm_dev_execute_batch_ex call of the handle (host-buffer form, bank and rw
+ * kernels): out_records must hold n_tx * HETM_TRACE_TX_WORDS words and
+ * receives, per input transaction i, {ticket, the values it read in program
+ * order (bank: acct0..3; rw: r_addr[0..nr)), the values its read-modify-writes
+ * read (rw: w_addr[0..nw); bank: acct0, acct1), the values it wrote, and 3
+ * reserved words};
+ * ticket = ~0 when it did not commit.  The batch runs the traced kernel
+ * instantiation; untraced batches are unaffected. */
+#define HETM_TRACE_TX_WORDS 12
+int hetm_dev_trace_next_batch(hetm_dev* dev, uint64_t* out_records);
+
+/* Fault injection for the checker's mutation suite ("rejects
+ * every seeded mutation"): each flag disables one step of the protocol so the
+ * tests can show the checker catches it.  Never set outside tests. */
+#define HETM_FAULT_SKIP_RS 1u       /* validation never tests the RS bitmap (no conflicts) */
+#define HETM_FAULT_SKIP_TS 2u       /* APPLY stores entries in arrival order, no TS freshness */
+#define HETM_FAULT_SKIP_ROLLBACK 4u /* mergeAbortDevice leaves 1/8 of the write set un-restored */
+#define HETM_FAULT_ALL 7u
+int hetm_dev_set_fault(hetm_dev* dev, uint32_t flags);
+
+/* One recorded event (40 B).  device: 0 host, 1 device.  kind: HETM_EV_*.
+ * tx: host (thread << 40 | per-thread attempt number), device
+ * (1 << 63 | batch number << 32 | input index).  value: read/write value,
+ * SPEC_COMMIT ts (host) or commit ticket (device), FINAL_COMMIT round id,
+ * ABORT reason.  seq: global append order (the real-time order key of host
+ * events; device events are appended when the batch returns). */
+enum {
+    HETM_EV_BEGIN = 0,
+    HETM_EV_READ = 1,
+    HETM_EV_WRITE = 2,
+    HETM_EV_SPEC_COMMIT = 3,
+    HETM_EV_FINAL_COMMIT = 4,
+    HETM_EV_ABORT = 5,
+    HETM_EV_ROUND = 6 /* round boundary marker: value = round id */
+};
+enum { HETM_ABORT_CONFLICT = 1, HETM_ABORT_ROUND = 2 };
+typedef struct hetm_trace_event {
+    uint64_t seq;
+    uint64_t tx;
+    uint64_t addr;
+    uint64_t value;
+    uint32_t round;
+    uint8_t device;
+    uint8_t kind;
+    uint16_t pad;
+} hetm_trace_event;
+
 /* ------------------------------------------------------------ host side -- */
 int hetm_host_alloc(uint64_t bytes, void** p); /* pinned, portable */
 int hetm_host_free(void* p);

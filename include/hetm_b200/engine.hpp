@@ -23,6 +23,7 @@
 // Chunk buffers are pinned (hetm_host_alloc) and stay valid until the verdict.
 #pragma once
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -36,6 +37,7 @@
 
 #include "hetm_b200/capi.h"
 #include "hetm_b200/host_tm.hpp"
+#include "hetm_b200/trace.hpp"
 
 namespace hetm::b200 {
 
@@ -49,7 +51,13 @@ struct EngineConfig {
     bool early_validation = true;       // stream chunks VALIDATE_ONLY during execution
     bool optimized_abort = true;        // mergeAbortDevice: shadow + log (true) or chunk copy (false)
     bool keep_round_log = false;        // keep a copy of the last round's host log (checkers)
+    uint32_t fault = 0;                 // ENGINE_FAULT_* (checker mutation suite only)
 };
+
+// Engine-level mutations for the checker's mutation suite; the
+// device-level ones are hetm_dev_set_fault.  Never set outside tests.
+constexpr uint32_t ENGINE_FAULT_EARLY_DEVICE_COMMIT = 1;  // report device commits final before validation
+constexpr uint32_t ENGINE_FAULT_DROP_CHUNK = 2;           // drop the round's first streamed log chunk
 
 struct RoundReport {
     uint64_t round_id = 0;
@@ -109,6 +117,15 @@ public:
     using HostWorker = std::function<uint64_t(int thread, const RoundContext& ctx)>;
     uint32_t consecutiveDeviceAborts() const { return dev_aborts_; }
 
+    /// Checker traces: host transactions through HostStm,
+    /// device batches through hetm_dev_trace_next_batch (bank and rw kernels),
+    /// round markers and the final-commit / abort verdict of every speculative
+    /// commit.  nullptr turns recording off.
+    void setTrace(Trace* t) {
+        trace_ = t;
+        stm_.setTrace(t);
+    }
+
     /// Next device batch of the round: fill inputs/n_tx/tickets_out and return
     /// true, or return false when the execution budget is spent.
     struct Batch {
@@ -135,6 +152,8 @@ public:
                                 const HostWorker& worker) {
         RoundReport rep;
         rep.round_id = round_id_++;
+        if (trace_) trace_->beginRound((uint32_t)rep.round_id);
+        dropped_ = false;
         const bool favor_device = cfg_.policy == Policy::FavorDevice;
         // starvation guard (FavorHost): a read-only host round after K device aborts
         rep.updates_allowed = favor_device || dev_aborts_ < cfg_.starvation_k;
@@ -151,8 +170,14 @@ public:
             Batch b;
             for (uint32_t k = 0; !cut.load(std::memory_order_acquire) && next(k, b); ++k) {
                 hetm_batch_stats st{};
+                if (trace_) {
+                    trace_rec_.assign(b.n_tx * HETM_TRACE_TX_WORDS, ~0ull);
+                    gpu_rc = hetm_dev_trace_next_batch(dev_, trace_rec_.data());
+                    if (gpu_rc != HETM_OK) break;
+                }
                 gpu_rc = hetm_dev_execute_batch(dev_, kernel_id, b.inputs, rec_bytes, b.n_tx, b.tickets_out, &st);
                 if (gpu_rc != HETM_OK) break;
+                if (trace_) trace_batch(kernel_id, b);
                 rep.batch = st;
                 rep.dev_committed += st.committed;
                 ++rep.dev_batches;
@@ -195,7 +220,11 @@ public:
             check_rc(hetm_dev_round_verdict(dev_, &conflict), "round_verdict");
         }
         const auto t2 = std::chrono::steady_clock::now();
-        // ---- MERGE
+        // ---- MERGE (the trace records the verdict of every speculative commit)
+        if (trace_) {
+            const bool early = (cfg_.fault & ENGINE_FAULT_EARLY_DEVICE_COMMIT) != 0;
+            trace_->finalizeRound(!rep.conflict || !favor_device, !rep.conflict || favor_device || early);
+        }
         if (!rep.conflict) {
             rep.outcome = Outcome::Commit;
             check_rc(hetm_dev_merge_commit(dev_, host_, nullptr), "merge_commit");
@@ -235,9 +264,38 @@ private:
         }
         return static_cast<hetm_log_entry*>(pool_[used_++]);
     }
+    // Device events of one traced batch, in program order per transaction.
+    void trace_batch(int kernel_id, const Batch& b) {
+        const uint64_t batch = trace_batches_++;
+        for (uint64_t i = 0; i < b.n_tx; ++i) {
+            const uint64_t* r = trace_rec_.data() + i * HETM_TRACE_TX_WORDS;
+            if (r[0] == ~0ull) continue;  // did not commit
+            const uint64_t id = 1ull << 63 | batch << 32 | i;
+            trace_->append(1, HETM_EV_BEGIN, id, 0, 0);
+            if (kernel_id == HETM_KERNEL_BANK) {
+                const hetm_bank_tx& t = static_cast<const hetm_bank_tx*>(b.inputs)[i];
+                for (int k = 0; k < 4; ++k) trace_->append(1, HETM_EV_READ, id, t.acct[k], r[1 + k]);
+                for (int k = 0; k < 2; ++k) trace_->append(1, HETM_EV_WRITE, id, t.acct[k], r[7 + k]);
+            } else if (kernel_id == HETM_KERNEL_RW) {
+                const hetm_rw_tx& t = static_cast<const hetm_rw_tx*>(b.inputs)[i];
+                for (uint32_t k = 0; k < std::min<uint32_t>(t.nr, 4); ++k)
+                    trace_->append(1, HETM_EV_READ, id, t.r_addr[k], r[1 + k]);
+                for (uint32_t k = 0; k < std::min<uint32_t>(t.nw, 2); ++k) {
+                    trace_->append(1, HETM_EV_READ, id, t.w_addr[k], r[5 + k]);
+                    trace_->append(1, HETM_EV_WRITE, id, t.w_addr[k], r[7 + k]);
+                }
+            }
+            trace_->append(1, HETM_EV_SPEC_COMMIT, id, 0, r[0]);
+        }
+    }
     void ship(int t, uint64_t n, int mode, RoundReport& rep) {
         hetm_log_entry* buf = chunk_buffer();
         const uint64_t got = log_.slice(t, shipped_[t], shipped_[t] + n, buf);
+        if ((cfg_.fault & ENGINE_FAULT_DROP_CHUNK) && !dropped_ && got) {  // mutation: the chunk never reaches the GPU
+            dropped_ = true;
+            shipped_[t] += got;
+            return;
+        }
         check_rc(hetm_dev_stream_chunk(dev_, buf, got, t, seq_++, mode), "stream_chunk");
         shipped_[t] += got;
         rep.log_entries += got;
@@ -267,6 +325,10 @@ private:
     std::vector<uint64_t> snapshot_;  // FavorDevice round-start host snapshot
     uint64_t round_id_ = 0;
     uint32_t dev_aborts_ = 0;         // consecutiveDeviceAborts
+    Trace* trace_ = nullptr;
+    std::vector<uint64_t> trace_rec_;  // per-batch device trace records
+    uint64_t trace_batches_ = 0;
+    bool dropped_ = false;             // ENGINE_FAULT_DROP_CHUNK: this round's chunk is gone
 };
 
 }  // namespace hetm::b200

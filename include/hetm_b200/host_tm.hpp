@@ -25,6 +25,7 @@
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -33,6 +34,7 @@
 #include <vector>
 
 #include "hetm_b200/capi.h"
+#include "hetm_b200/trace.hpp"
 
 namespace hetm::b200 {
 
@@ -105,6 +107,7 @@ public:
     struct Tx {
         uint64_t rv = 0;    // startTs
         int thread = 0;
+        uint64_t id = 0;    // trace txId: thread << 40 | attempt serial number (trace on)
         std::vector<uint64_t> reads;                               // lock indices read
         std::vector<std::pair<uint64_t, uint64_t>> writes;         // addr -> pending value (insertion order)
         std::vector<std::pair<uint64_t, uint64_t>> held;           // (lock index, pre-lock word) during commit
@@ -117,6 +120,9 @@ public:
     }
 
     void setCommitCallback(Callback cb) { cb_ = std::move(cb); }
+    /// Checker traces: record every begin / read / write /
+    /// speculative commit / abort with its value; nullptr turns recording off.
+    void setTrace(Trace* t) { trace_ = t; }
     uint64_t clock() const { return clock_.load(std::memory_order_acquire); }
     /// GlobalClock floor after a device round (the device's ts space is separate; kept for completeness)
     void advanceClockTo(uint64_t v) {
@@ -132,21 +138,37 @@ public:
         tx.thread = thread;
         tx.reads.clear();
         tx.writes.clear();
+        if (trace_) {  // ids unique over the STM's lifetime (worker threads are re-created every round)
+            tx.id = (uint64_t)thread << 40 | (trace_ids_.fetch_add(1, std::memory_order_relaxed) & ((1ull << 40) - 1));
+            trace_->append(0, HETM_EV_BEGIN, tx.id, 0, tx.rv);
+        }
     }
     uint64_t read(Tx& tx, uint64_t addr) const {
         if (addr >= words_) throw HostOutOfBounds("host TM read out of bounds");
         for (auto it = tx.writes.rbegin(); it != tx.writes.rend(); ++it)
-            if (it->first == addr) return it->second;  // read-your-writes
+            if (it->first == addr) {  // read-your-writes
+                if (trace_) trace_->append(0, HETM_EV_READ, tx.id, addr, it->second);
+                return it->second;
+            }
         const uint64_t li = lock_index(addr);
         const uint64_t l1 = locks_[li].load(std::memory_order_acquire);
         const uint64_t v = std::atomic_ref<uint64_t>(mem_[addr]).load(std::memory_order_acquire);
         const uint64_t l2 = locks_[li].load(std::memory_order_acquire);
-        if ((l1 & 1) || l1 != l2 || (l1 >> 1) > tx.rv) throw TxAbort{};  // opacity: abort on stale
+        if ((l1 & 1) || l1 != l2 || (l1 >> 1) > tx.rv) abort_tx(tx);  // opacity: abort on stale
         tx.reads.push_back(li);
+        if (trace_) trace_->append(0, HETM_EV_READ, tx.id, addr, v);
         return v;
     }
     void write(Tx& tx, uint64_t addr, uint64_t value) const {
         if (addr >= words_) throw HostOutOfBounds("host TM write out of bounds");
+        struct Record {  // the WRITE event follows the implicit read in program order
+            const HostStm& s;
+            Tx& tx;
+            uint64_t addr, value;
+            ~Record() {
+                if (s.trace_ && std::uncaught_exceptions() == 0) s.trace_->append(0, HETM_EV_WRITE, tx.id, addr, value);
+            }
+        } rec{*this, tx, addr, value};
         bool seen = false;
         for (auto& w : tx.writes)
             if (w.first == addr) {
@@ -160,7 +182,10 @@ public:
     }
     /// Returns the commit ts (read-only: rv, no clock advance, no callback).
     uint64_t commit(Tx& tx) {
-        if (tx.writes.empty()) return tx.rv;
+        if (tx.writes.empty()) {  // read-only: serializes at rv
+            if (trace_) trace_->append(0, HETM_EV_SPEC_COMMIT, tx.id, 0, tx.rv);
+            return tx.rv;
+        }
         // 1. lock the write set in canonical order
         tx.held.clear();
         for (auto& w : tx.writes) tx.held.emplace_back(lock_index(w.first), 0);
@@ -182,7 +207,7 @@ public:
         }
         if (got < tx.held.size()) {
             release(tx, got, false, 0);
-            throw TxAbort{};
+            abort_tx(tx);
         }
         // 2. ts = ++clock (unique; the write locks are held)
         const uint64_t ts = clock_.fetch_add(1, std::memory_order_acq_rel) + 1;
@@ -195,13 +220,13 @@ public:
                     auto h = std::lower_bound(tx.held.begin(), tx.held.end(), std::make_pair(li, uint64_t(0)));
                     if (h == tx.held.end() || h->first != li) {
                         release(tx, tx.held.size(), false, 0);
-                        throw TxAbort{};
+                        abort_tx(tx);
                     }
                     ver = h->second >> 1;
                 }
                 if (ver > tx.rv) {
                     release(tx, tx.held.size(), false, 0);
-                    throw TxAbort{};
+                    abort_tx(tx);
                 }
             }
         }
@@ -212,6 +237,7 @@ public:
             tx.out.push_back(hetm_log_entry{w.first, w.second, ts});
         }
         release(tx, tx.held.size(), true, ts);
+        if (trace_) trace_->append(0, HETM_EV_SPEC_COMMIT, tx.id, 0, ts);
         if (cb_) cb_(tx.thread, tx.out);
         return ts;
     }
@@ -233,6 +259,10 @@ public:
     uint64_t aborts() const { return aborts_.load(); }
 
 private:
+    [[noreturn]] void abort_tx(Tx& tx) const {
+        if (trace_) trace_->append(0, HETM_EV_ABORT, tx.id, 0, HETM_ABORT_CONFLICT);
+        throw TxAbort{};
+    }
     uint64_t lock_index(uint64_t addr) const { return (addr * 0x9e3779b97f4a7c15ull >> 20) & mask_; }
     void release(Tx& tx, std::size_t n, bool committed, uint64_t ts) const {
         for (std::size_t k = 0; k < n; ++k)
@@ -250,6 +280,8 @@ private:
     std::atomic<uint64_t> clock_{0};
     std::atomic<uint64_t> aborts_{0};
     Callback cb_;
+    Trace* trace_ = nullptr;
+    mutable std::atomic<uint64_t> trace_ids_{0};
 };
 
 // ---- the HeTM host API names (north_star: TM_begin / TM_read / TM_write / TM_commit)

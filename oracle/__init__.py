@@ -62,6 +62,8 @@ for name, res, args in [
     ("orc_gen_cache_batch", None, [_u, _u, _u, C.c_double, C.c_uint32, C.c_int32, C.c_uint32, _v]),
     ("orc_mt_bank_batch", _u, [_v, _u, _u, _v, _u, C.c_int, _u, _v, _v, _v, _v, _u, _u]),
     ("orc_mt_validate_apply", C.c_int, [_v, _u, _v, _u, _u, _v, _v, C.c_int, C.c_int]),
+    ("orc_check_p1", C.c_int, [_v, _u, _v, _u, _v]),
+    ("orc_check_p2dagger", C.c_int, [_v, _u, _v, _u, _v]),
 ]:
     f = getattr(lib, name)
     f.restype, f.argtypes = res, args
@@ -200,6 +202,58 @@ def mt_validate_apply(entries, rs_words, gran, ts, dev, threads, apply=True, bas
     entries = np.ascontiguousarray(entries, ENTRY)
     return bool(lib.orc_mt_validate_apply(P(entries), entries.size, P(rs_words), gran, base, P(ts), P(dev),
                                           threads, int(apply)))
+
+
+# ---- checker (checker.c) ------------------------------------
+TRACE_EVENT = np.dtype([("seq", "<u8"), ("tx", "<u8"), ("addr", "<u8"), ("value", "<u8"), ("round", "<u4"),
+                        ("device", "u1"), ("kind", "u1"), ("pad", "<u2")])
+assert TRACE_EVENT.itemsize == 40
+EV_BEGIN, EV_READ, EV_WRITE, EV_SPEC_COMMIT, EV_FINAL_COMMIT, EV_ABORT, EV_ROUND = range(7)
+ABORT_CONFLICT, ABORT_ROUND = 1, 2
+CHECK_PASS, CHECK_FAIL, CHECK_INCOMPLETE = 0, 1, 2
+REASON_NONE, REASON_READ, REASON_REALTIME, REASON_INCOMPLETE, REASON_BAD_ADDR = range(5)
+
+
+class CheckResult(C.Structure):
+    _fields_ = [("verdict", C.c_int), ("reason", C.c_int), ("tx", _u), ("addr", _u), ("expected", _u), ("got", _u),
+                ("round", C.c_uint32), ("checked_txs", _u), ("checked_reads", _u)]
+
+
+def _check(fn, events, init):
+    ev = np.ascontiguousarray(events, dtype=TRACE_EVENT)
+    st = np.ascontiguousarray(init, dtype=np.uint64)
+    r = CheckResult()
+    fn(P(ev) if len(ev) else None, len(ev), P(st), len(st), C.byref(r))
+    return r
+
+
+def check_p1(events, init):
+    """checkP1: the finally committed transactions explained by the claimed serial order."""
+    return _check(lib.orc_check_p1, events, init)
+
+
+def check_p2dagger(events, init):
+    """checkP2dagger: speculative commits of aborted sides explained by their own device's order."""
+    return _check(lib.orc_check_p2dagger, events, init)
+
+
+def load_trace(path):
+    """Parses a HETMTRC1 dump (include/hetm_b200/trace.hpp): (header dict, events)."""
+    import json
+    import struct
+    raw = open(path, "rb").read()
+    if raw[:8] != b"HETMTRC1":
+        raise ValueError("not a HETMTRC1 trace")
+    (hl,) = struct.unpack_from("<I", raw, 8)
+    header = json.loads(raw[12:12 + hl].decode())
+    body = raw[12 + hl:]
+    rec = 4 + TRACE_EVENT.itemsize
+    if len(body) % rec:
+        raise ValueError("truncated trace record")
+    recs = np.frombuffer(body, dtype=np.uint8).reshape(-1, rec)
+    if len(recs) and not (recs[:, :4].copy().view("<u4") == TRACE_EVENT.itemsize).all():
+        raise ValueError("bad record length")
+    return header, recs[:, 4:].copy().view(TRACE_EVENT).reshape(-1)
 
 
 def load_ref():

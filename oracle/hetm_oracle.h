@@ -119,6 +119,31 @@ uint64_t orc_mt_bank_batch(uint64_t* stmr, uint64_t base, uint64_t size_words, c
 int orc_mt_validate_apply(const orc_entry* e, uint64_t n, const uint64_t* rs_words, uint64_t gran_bytes,
                           uint64_t base, uint64_t* ts, uint64_t* dev, int threads, int apply);
 
+/* ---- checker: P1 / P2-dagger over execution traces,
+ * checker.c.  orc_trace_event mirrors capi.h hetm_trace_event (40 B). */
+typedef struct {
+    uint64_t seq, tx, addr, value;
+    uint32_t round;
+    uint8_t device, kind;
+    uint16_t pad;
+} orc_trace_event;
+enum { ORC_CHECK_PASS = 0, ORC_CHECK_FAIL = 1, ORC_CHECK_INCOMPLETE = 2 };
+enum { ORC_REASON_NONE = 0, ORC_REASON_READ = 1, ORC_REASON_REALTIME = 2, ORC_REASON_INCOMPLETE = 3,
+       ORC_REASON_BAD_ADDR = 4 };
+typedef struct {
+    int verdict, reason;
+    uint64_t tx, addr, expected, got; /* witness: first inconsistent read (or real-time pair bound / ts) */
+    uint32_t round;
+    uint64_t checked_txs, checked_reads;
+} orc_check_result;
+/* P1: the finally committed transactions explained by the claimed serial order
+ * (per round: host by commit ts, then device by ticket) from `init`. */
+int orc_check_p1(const orc_trace_event* ev, uint64_t n, const uint64_t* init, uint64_t words, orc_check_result* res);
+/* P2-dagger: every speculatively committed transaction of an aborted side
+ * explained by the committed state plus its own device's speculative set. */
+int orc_check_p2dagger(const orc_trace_event* ev, uint64_t n, const uint64_t* init, uint64_t words,
+                       orc_check_result* res);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,8 @@ REPLICA_HOST, REPLICA_DEV, REPLICA_DEV_SHADOW, REPLICA_HOST_SNAPSHOT = 0, 1, 2, 
 BMP_RS, BMP_WS, BMP_CHUNK = 0, 1, 2
 APPLY, VALIDATE_ONLY = 0, 1
 KERNEL_BANK, KERNEL_RW, KERNEL_CACHE = 1, 2, 3
+TRACE_TX_WORDS = 12  # capi.h HETM_TRACE_TX_WORDS
+FAULT_SKIP_RS, FAULT_SKIP_TS, FAULT_SKIP_ROLLBACK = 1, 2, 4  # capi.h HETM_FAULT_* (checker mutation suite)
 CACHE_GET, CACHE_SET = 0, 1
 CACHE_MISS, CACHE_HIT, CACHE_UPDATED, CACHE_INSERTED, CACHE_EVICTED = range(5)
 CACHE_WAYS, CACHE_WAY_WORDS, CACHE_SET_WORDS = 8, 8, 64
@@ -434,6 +436,18 @@ class GpuDevice:
         s = C.c_void_p()
         self._chk(lib.hetm_dev_stream_handle(self.h, which, C.byref(s)))
         return s.value or 0
+
+    def trace_next_batch(self, out: np.ndarray):
+        """Arm a checker trace of the next execute_batch (bank / rw): `out` (uint64,
+        n_tx * TRACE_TX_WORDS, kept alive by the caller) receives per transaction
+        {ticket, read values, rmw read values, written values, 3 reserved}."""
+        assert out.dtype == np.uint64 and out.flags["C_CONTIGUOUS"]
+        self._trace_keep = out
+        self._chk(lib.hetm_dev_trace_next_batch(self.h, out.ctypes.data))
+
+    def set_fault(self, flags: int):
+        """Checker mutation suite only: FAULT_SKIP_RS | FAULT_SKIP_TS | FAULT_SKIP_ROLLBACK."""
+        self._chk(lib.hetm_dev_set_fault(self.h, flags))
 
     def set_timing(self, on: bool = True):
         self._chk(lib.hetm_dev_set_timing(self.h, int(on)))

@@ -164,6 +164,11 @@ struct hetm_dev {
     cudaStream_t s_exec = nullptr, s_copy = nullptr, s_val = nullptr, s_merge = nullptr, s_d2h = nullptr,
                  s_zc = nullptr,  // s_zc: zero-copy delta stores into the host replica
         s_in = nullptr, s_out = nullptr;  // pipelined host-input batches: input pieces in, tickets/results out
+    unsigned long long* d_trace = nullptr;  // checker trace of the armed batch (kTraceWords per tx)
+    uint64_t trace_cap = 0;                 // in transactions
+    uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
+    uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
+    unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
     cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
@@ -208,6 +213,7 @@ struct hetm_dev {
         v.wlog = d_wlog;
         v.wlog_slots = wlog_slots;
         v.serial = (cfg.flags & HETM_CFG_DETERMINISTIC) ? 1u : 0u;
+        v.trace = nullptr;
         return v;
     }
     std::mutex xfer_mu;  // record() is reached from the GPU-controller and the log streamer threads
@@ -313,7 +319,7 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
-                  void* d_results, cudaStream_t s, bool reset_counters = true) {
+                  void* d_results, cudaStream_t s, bool reset_counters = true, unsigned long long* trace = nullptr) {
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
@@ -325,14 +331,16 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
         t1 = d->tev();
         CK(d, cudaEventRecord(t0, s));
     }
+    ShardView v = d->view();
+    v.trace = trace;
     if (kernel_id == HETM_KERNEL_BANK)
-        e = launch_bank_batch(d->view(), static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
+        e = launch_bank_batch(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                               d->max_attempts, d->geom, s);
     else if (kernel_id == HETM_KERNEL_CACHE)
         e = launch_cache_batch(d->view(), d->cache, static_cast<const hetm_cache_tx*>(d_inputs), n, d_tickets,
                                static_cast<hetm_cache_result*>(d_results), d->d_ctr, d->max_attempts, d->geom, s);
     else
-        e = launch_rw_batch(d->view(), static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
+        e = launch_rw_batch(v, static_cast<const hetm_rw_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                             d->max_attempts, d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "batch kernel launch");
     if (d->timing) {
@@ -352,7 +360,11 @@ cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, i
         t1 = d->tev();
         cudaEventRecord(t0, s);
     }
-    cudaError_t e = launch_validate(d->view(), log, n, apply, d->d_ctr, d->d_restore, d->geom, s);
+    ShardView v = d->view();
+    if (d->fault & HETM_FAULT_SKIP_RS) v.rs = d->d_rs_zero;  // mutation: the RS test never fires
+    cudaError_t e = (apply && (d->fault & HETM_FAULT_SKIP_TS))
+                        ? launch_blind_apply(v, log, n, d->d_ctr, d->geom, s)  // mutation: no TS freshness
+                        : launch_validate(v, log, n, apply, d->d_ctr, d->d_restore, d->geom, s);
     if (d->timing && n) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
@@ -598,7 +610,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
-                    (void*)d->d_tk, d->d_route, d->d_flush})
+                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     for (auto& v : d->tpairs)
@@ -769,6 +781,16 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         CK(d, cudaEventCreate(&e));
         d->kp_ev.push_back(e);
     }
+    unsigned long long* trace = nullptr;  // armed checker trace (hetm_dev_trace_next_batch)
+    if (d->trace_out && n_tx) {
+        if (n_tx > d->trace_cap) {
+            if (d->d_trace) { cudaFree(d->d_trace); d->bytes_alloc -= d->trace_cap * kTraceWords * 8; d->d_trace = nullptr; }
+            if ((rc = dev_alloc(d, (void**)&d->d_trace, n_tx * kTraceWords * 8))) return rc;
+            d->trace_cap = n_tx;
+        }
+        CK(d, cudaMemsetAsync(d->d_trace, 0xff, n_tx * kTraceWords * 8, s));  // ~0: did not commit
+        trace = d->d_trace;
+    }
     const char* in_h = static_cast<const char*>(inputs);
     char* in_d = static_cast<char*>(d->d_in);
     for (uint64_t k = 0; k < P; ++k) {
@@ -781,7 +803,8 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         }
         CK(d, cudaEventRecord(d->kp_ev[2 * k], s));
         if ((rc = enqueue_batch(d, kernel_id, in_d + lo * rec_bytes, m, d->d_tk + lo,
-                                results_out ? d->d_res + lo : nullptr, s, k == 0)))
+                                results_out ? d->d_res + lo : nullptr, s, k == 0,
+                                trace ? trace + lo * kTraceWords : nullptr)))
             return rc;
         CK(d, cudaEventRecord(d->kp_ev[2 * k + 1], s));
         if (m && (tickets_out || results_out)) {
@@ -796,6 +819,10 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     if (n_tx) d->record(HETM_H2D, HETM_TAG_INPUT, n_tx * rec_bytes);
     if (tickets_out && n_tx) d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * 8);
     if (results_out && n_tx) d->record(HETM_D2H, HETM_TAG_OUTPUT, n_tx * res_bytes);
+    if (trace) {
+        CK(d, cudaMemcpyAsync(d->trace_out, trace, n_tx * kTraceWords * 8, cudaMemcpyDeviceToHost, s));
+        d->trace_out = nullptr;
+    }
     CK(d, cudaMemcpyAsync(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(d, cudaStreamSynchronize(s));
     CK(d, cudaStreamSynchronize(d->s_out));
@@ -1221,8 +1248,13 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
         if ((rc = read_counters(d))) return rc;
         const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
         cudaError_t e;
-        if (d->d_wlog && !d->h_ctr->wlog_overflow && n_slots <= d->wlog_slots && n_slots * 8 < dirty_bytes)
-            e = launch_wlog_restore(d->d_cells, d->d_shadow, d->d_wlog, n_slots, d->W, d->geom, d->s_merge);
+        if (d->d_wlog && !d->h_ctr->wlog_overflow && n_slots <= d->wlog_slots && n_slots * 8 < dirty_bytes) {
+            // mutation HETM_FAULT_SKIP_ROLLBACK: the first 1/8 of the write set (a chunk's worth of
+            // state, "skip rollback of one chunk") is not rolled back
+            const uint64_t skip = (d->fault & HETM_FAULT_SKIP_ROLLBACK) ? (n_slots / 8) & ~1ull : 0;
+            e = launch_wlog_restore(d->d_cells, d->d_shadow, d->d_wlog + skip, n_slots - skip, d->W, d->geom,
+                                    d->s_merge);
+        }
         else
             e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, false,
                                     d->geom, d->s_merge);
@@ -1620,6 +1652,24 @@ int hetm_enable_peer_access(int device, int peer) {
         return HETM_ERR_CUDA;
     }
     cudaGetLastError();
+    return HETM_OK;
+}
+
+int hetm_dev_trace_next_batch(hetm_dev* d, uint64_t* out_records) {
+    if (!d || !out_records) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->trace_out = out_records;
+    return HETM_OK;
+}
+
+int hetm_dev_set_fault(hetm_dev* d, uint32_t flags) {
+    if (!d || (flags & ~(uint32_t)HETM_FAULT_ALL)) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    if ((flags & HETM_FAULT_SKIP_RS) && !d->d_rs_zero) {
+        if (int rc = dev_alloc(d, (void**)&d->d_rs_zero, d->rs_words * 8)) return rc;
+        CK(d, cudaMemset(d->d_rs_zero, 0, d->rs_words * 8));
+    }
+    d->fault = flags;
     return HETM_OK;
 }
 

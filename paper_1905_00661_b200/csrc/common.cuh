@@ -73,7 +73,14 @@ struct ShardView {
     uint32_t* wlog;            // device write-set log (nullptr: disabled, shard >= 2^32 words)
     uint64_t wlog_slots;       // its capacity in slots
     uint32_t serial;           // deterministic single-worker mode (HETM_CFG_DETERMINISTIC)
+    unsigned long long* trace; // checker trace of the batch (nullptr: off): HETM_TRACE_TX_WORDS per tx index
 };
+
+// Checker trace record of one committed batch transaction (capi.h
+// hetm_dev_trace_next_batch): [0] ticket, [1..4] values of the read words in
+// program order, [5..6] values read by the read-modify-writes, [7..8] values
+// written, [9..11] reserved.  Transactions that did not commit keep ~0 in [0].
+constexpr int kTraceWords = 12;
 
 // First transaction and stride of the calling thread in a batch kernel.  In the
 // deterministic single-worker mode global thread 0 runs every

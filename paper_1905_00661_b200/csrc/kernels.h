@@ -36,6 +36,8 @@ cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t
 // engine.validateChunk over n log entries (apply: pass A + pass B).
 // Apply-mode launches of one handle must be stream-ordered (they share d_restore,
 // kRestoreCap entries, and rely on the previous launch's stores being complete).
+cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, DevCounters* ctr,
+                               const LaunchGeom& g, cudaStream_t s);  // fault injection only
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
                             DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
 // Optimized rollback: untag the logged words, re-apply the round log, copy them to shadow.

@@ -43,6 +43,7 @@ struct StaticTx {
     unsigned long long l[NR];  // lock word seen in P1
     uint64_t val[NW];          // value of write word j seen in P1
     uint64_t wval[NW];         // value to write to loc[j]
+    uint64_t rv[NR > NW ? NR - NW : 1];  // KO_TRACE only: value of read-only word NW+k seen in P1
     uint32_t first;            // bit k set: loc[k] is the first occurrence of its word
     uint32_t block_loc;        // abort cause: word held FINAL by another transaction ...
     unsigned long long block_lk;  // ... with this lock word (0: no such blocker)
@@ -79,7 +80,8 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 // KO_COUNT_TICKETS counts ticket atomics (debug word 4).
 enum : int {
     KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_PROTOCOL = 64,
-    KO_PHASE_CLOCKS = 128, KO_LOCK_READS = 256, KO_SKIP_VALIDATE = 512, KO_NO_TICKET = 1024
+    KO_PHASE_CLOCKS = 128, KO_LOCK_READS = 256, KO_SKIP_VALIDATE = 512, KO_NO_TICKET = 1024,
+    KO_TRACE = 2048  // checker traces: also load the VALUES of the read-only words (tx.rv)
 };
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
@@ -120,6 +122,7 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
             if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], tx.l[k]);
+            else if constexpr ((KO & KO_TRACE) != 0) ld_pair(&v.cells[tx.loc[k]], tx.rv[k >= NW ? k - NW : 0], tx.l[k]);
             else tx.l[k] = ld_relaxed(&v.cells[tx.loc[k]].meta);
         }
         unsigned long long pr[NR + 2 * NW];

@@ -104,6 +104,18 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             }, clocks);
         if (committed) {
             tickets[i] = t;
+            if constexpr ((KO & KO_TRACE) != 0) {  // reads acct0..3 in order, then writes acct0, acct1
+                unsigned long long* r = v.trace + i * kTraceWords;
+                r[0] = t;
+                r[1] = tx.val[0];
+                r[2] = tx.val[1];
+                r[3] = tx.rv[0];
+                r[4] = tx.rv[1];
+                r[5] = tx.val[0];
+                r[6] = tx.val[1];
+                r[7] = tx.wval[0];
+                r[8] = tx.wval[1];
+            }
             wlog_put(v, wbase, t, 0, tx.loc[0]);
             wlog_put(v, wbase, t, 1, tx.loc[1]);
             ++commits;
@@ -179,19 +191,32 @@ __global__ void __launch_bounds__(kTxThreads) rw_batch_kernel(ShardView v, const
             tx.begin((uint32_t)(i + 1));
             bool ok = true;
             uint64_t sum = 0;
+            uint64_t rx[4] = {0, 0, 0, 0}, cx[2] = {0, 0}, wx[2] = {0, 0};  // trace: values in program order
             for (uint32_t j = 0; j < nr && ok; ++j) {
                 uint64_t x;
                 ok = tm_read(tx, v, r.r_addr[j] - v.base, x);
+                rx[j] = x;
                 sum += x;
             }
             for (uint32_t j = 0; j < nw && ok; ++j) {
                 uint64_t cur;
                 const uint64_t loc = r.w_addr[j] - v.base;
                 ok = tm_read(tx, v, loc, cur) && tm_write(tx, v, loc, cur + r.add[j] + sum);
+                cx[j] = cur;
+                wx[j] = cur + r.add[j] + sum;
             }
             unsigned long long t = ~0ull;
             if (ok && tm_commit(tx, v, &ctr->ticket, t)) {
                 tickets[i] = t;
+                if (v.trace) {
+                    unsigned long long* tr = v.trace + i * kTraceWords;
+                    tr[0] = t;
+                    for (int j = 0; j < 4; ++j) tr[1 + j] = rx[j];
+                    for (int j = 0; j < 2; ++j) {
+                        tr[5 + j] = cx[j];
+                        tr[7 + j] = wx[j];
+                    }
+                }
                 tm_mark_bitmaps(tx, v);
                 wlog_put(v, wbase, t, 0, tx.nw > 0 ? (uint32_t)tx.w_local[0] : ~0u);
                 wlog_put(v, wbase, t, 1, tx.nw > 1 ? (uint32_t)tx.w_local[1] : ~0u);
@@ -235,6 +260,10 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
     const unsigned grid = grid_for(n, kTxThreads, bps > 0 ? bps : g.max_blocks_tx, g.sm_count);
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+    if (v.trace) {  // checker traces: the KO_TRACE instantiation (the product one is untouched)
+        bank_batch_kernel<KO_TRACE><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        return cudaGetLastError();
+    }
     switch (ko) {
         HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(64) HETM_KO_CASE(128) HETM_KO_CASE(256) HETM_KO_CASE(512) HETM_KO_CASE(1024) HETM_KO_CASE(1536)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);

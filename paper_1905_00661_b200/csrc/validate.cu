@@ -475,6 +475,31 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
     return cudaGetLastError();
 }
 
+// Fault injection only (HETM_FAULT_SKIP_TS, the checker's mutation suite,
+// SPEC.md:569): every entry is stored in arrival order, with no TS freshness
+// test, so an older host write can overwrite a newer one.
+__global__ void blind_apply_kernel(ShardView v, const hetm_log_entry* __restrict__ log, uint64_t n, DevCounters* ctr) {
+    const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
+    PassAFlags f;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const EntryRegs e = load_entry(log, i);
+        pass_a(v, e, ts_floor, f);
+        const uint64_t loc = e.addr - v.base;
+        if (loc < v.size_words) {
+            v.cells[loc].value = e.value;
+            v.cells[loc].meta = ts_meta(e.ts);
+        }
+    }
+    flush_pass_a(f, ctr);
+}
+
+cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, DevCounters* ctr,
+                               const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    blind_apply_kernel<<<grid_cap(n, kValThreads, g, 4), kValThreads, 0, s>>>(v, d_log, n, ctr);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
                             DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
     return launch_view(v, LogView{d_log, n, nullptr, 0, 0}, n, apply, ctr, d_restore, g, s);
