@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -33,6 +34,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "hetm_b200/capi.h"
@@ -69,27 +71,105 @@ struct RoundReport {
     uint64_t dev_committed = 0;
     uint64_t log_entries = 0;
     uint64_t chunks = 0;
+    uint64_t bytes_merge = 0;       // merge / rollback transfer bytes (D2H + H2D + D2D)
     uint32_t dev_batches = 0;       // device batches executed in the execution phase
     double exec_ms = 0, validate_ms = 0, merge_ms = 0;
     hetm_batch_stats batch{};
 
-    /// Round stats in a fixed field order (External Interfaces).
-    std::string json() const {
+    /// (name, value, is_string) in the fixed SPEC.md:427 field order; json()
+    /// and csvRow() print the same strings.
+    std::vector<std::tuple<const char*, std::string, bool>> fields() const {
         static const char* names[] = {"Commit", "DeviceAborted", "HostAborted"};
-        char buf[512];
-        std::snprintf(buf, sizeof buf,
-                      "{\"roundId\": %llu, \"outcome\": \"%s\", \"txCommittedHost\": %llu, "
-                      "\"txCommittedDev\": %llu, \"txWastedDev\": %llu, \"bytesLogs\": %llu, \"readOnlyHost\": %d, "
-                      "\"cutShort\": %d, \"devBatches\": %u, \"execMs\": %.3f, \"validateMs\": %.3f, \"mergeMs\": %.3f}",
-                      (unsigned long long)round_id, names[(int)outcome],
-                      (unsigned long long)(outcome == Outcome::HostAborted ? 0 : host_commits),
-                      (unsigned long long)(outcome == Outcome::DeviceAborted ? 0 : dev_committed),
-                      (unsigned long long)(outcome == Outcome::DeviceAborted ? dev_committed : 0),
-                      (unsigned long long)(log_entries * sizeof(hetm_log_entry)), (int)!updates_allowed,
-                      (int)cut_short, dev_batches, exec_ms, validate_ms, merge_ms);
-        return buf;
+        const auto u = [](uint64_t v) { return std::to_string(v); };
+        const auto ms = [](double v) {
+            char b[32];
+            std::snprintf(b, sizeof b, "%.3f", v);
+            return std::string(b);
+        };
+        return {{"roundId", u(round_id), false},
+                {"outcome", names[(int)outcome], true},
+                {"txCommittedHost", u(outcome == Outcome::HostAborted ? 0 : host_commits), false},
+                {"txCommittedDev", u(outcome == Outcome::DeviceAborted ? 0 : dev_committed), false},
+                {"txWastedDev", u(outcome == Outcome::DeviceAborted ? dev_committed : 0), false},
+                {"bytesLogs", u(log_entries * sizeof(hetm_log_entry)), false},
+                {"bytesMerge", u(bytes_merge), false},
+                {"readOnlyHost", u(!updates_allowed), false},
+                {"cutShort", u(cut_short), false},
+                {"devBatches", u(dev_batches), false},
+                {"execMs", ms(exec_ms), false},
+                {"validateMs", ms(validate_ms), false},
+                {"mergeMs", ms(merge_ms), false}};
+    }
+    std::string json() const { return json_object(fields()); }
+    std::string csvRow() const { return csv_line(fields(), false); }
+    static std::string csvHeader() { return csv_line(RoundReport{}.fields(), true); }
+
+    template <class F>
+    static std::string json_object(const F& fs) {
+        std::string o = "{";
+        for (const auto& [k, v, str] : fs) {
+            if (o.size() > 1) o += ", ";
+            o += std::string("\"") + k + "\": " + (str ? "\"" + v + "\"" : v);
+        }
+        return o + "}";
+    }
+    template <class F>
+    static std::string csv_line(const F& fs, bool header) {
+        std::string o;
+        for (const auto& [k, v, str] : fs) o += (o.empty() ? "" : ",") + (header ? std::string(k) : v);
+        return o;
     }
 };
+
+/// Run summary over the rounds (throughput = sum committed / sum time).
+struct RunSummary {
+    uint64_t rounds = 0, tx_host = 0, tx_dev = 0, tx_wasted_dev = 0, bytes_logs = 0, bytes_merge = 0;
+    double time_ms = 0;
+    explicit RunSummary(const std::vector<RoundReport>& rs) {
+        for (const auto& r : rs) {
+            ++rounds;
+            tx_host += r.outcome == Outcome::HostAborted ? 0 : r.host_commits;
+            tx_dev += r.outcome == Outcome::DeviceAborted ? 0 : r.dev_committed;
+            tx_wasted_dev += r.outcome == Outcome::DeviceAborted ? r.dev_committed : 0;
+            bytes_logs += r.log_entries * sizeof(hetm_log_entry);
+            bytes_merge += r.bytes_merge;
+            // each phase rounded like the per-round rows, so the summary recomputes from them exactly
+            for (double m : {r.exec_ms, r.validate_ms, r.merge_ms}) time_ms += std::round(m * 1000.0) / 1000.0;
+        }
+    }
+    std::vector<std::tuple<const char*, std::string, bool>> fields() const {
+        const auto u = [](uint64_t v) { return std::to_string(v); };
+        char t[32], thr[48];
+        std::snprintf(t, sizeof t, "%.3f", time_ms);
+        std::snprintf(thr, sizeof thr, "%.1f", time_ms > 0 ? (tx_host + tx_dev) / (time_ms * 1e-3) : 0.0);
+        return {{"rounds", u(rounds), false},           {"txCommittedHost", u(tx_host), false},
+                {"txCommittedDev", u(tx_dev), false},     {"txWastedDev", u(tx_wasted_dev), false},
+                {"bytesLogs", u(bytes_logs), false},      {"bytesMerge", u(bytes_merge), false},
+                {"timeMs", t, false},                     {"throughputTxPerS", thr, false}};
+    }
+};
+
+/// emitReport: one row per round in a deterministic field
+/// order plus a summary block; "csv" or "json"; throws on an I/O error.
+inline void emitReport(const std::vector<RoundReport>& rounds, const std::string& format, const std::string& path) {
+    std::string out;
+    const RunSummary sum(rounds);
+    if (format == "csv") {
+        out = RoundReport::csvHeader() + "\n";
+        for (const auto& r : rounds) out += r.csvRow() + "\n";
+        out += "\n" + RoundReport::csv_line(sum.fields(), true) + "\n" + RoundReport::csv_line(sum.fields(), false) + "\n";
+    } else if (format == "json") {
+        out = "{\"rounds\": [";
+        for (std::size_t i = 0; i < rounds.size(); ++i) out += (i ? ", " : "") + rounds[i].json();
+        out += "], \"summary\": " + RoundReport::json_object(sum.fields()) + "}\n";
+    } else {
+        throw std::invalid_argument("emitReport: format is csv or json");
+    }
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("emitReport: io-error opening " + path);
+    const bool ok = std::fwrite(out.data(), 1, out.size(), f) == out.size();
+    if (std::fclose(f) != 0 || !ok) throw std::runtime_error("emitReport: io-error writing " + path);
+}
 
 /// What a host worker sees of the round.
 struct RoundContext {
@@ -227,17 +307,23 @@ public:
         }
         if (!rep.conflict) {
             rep.outcome = Outcome::Commit;
-            check_rc(hetm_dev_merge_commit(dev_, host_, nullptr), "merge_commit");
+            hetm_merge_stats ms{};
+            check_rc(hetm_dev_merge_commit(dev_, host_, &ms), "merge_commit");
+            rep.bytes_merge = ms.bytes_d2h + ms.bytes_h2d + ms.bytes_d2d;
             check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
             dev_aborts_ = 0;
         } else if (!favor_device) {
             rep.outcome = Outcome::DeviceAborted;
-            check_rc(hetm_dev_merge_abort_device(dev_, cfg_.optimized_abort ? 1 : 0, host_, nullptr),
+            hetm_merge_stats ms{};
+            check_rc(hetm_dev_merge_abort_device(dev_, cfg_.optimized_abort ? 1 : 0, host_, &ms),
                      "merge_abort_device");
+            rep.bytes_merge = ms.bytes_d2h + ms.bytes_h2d + ms.bytes_d2d;
             ++dev_aborts_;
         } else {
             rep.outcome = Outcome::HostAborted;
-            check_rc(hetm_dev_merge_abort_host(dev_, host_, snapshot_.data(), nullptr), "merge_abort_host");
+            hetm_merge_stats ms{};
+            check_rc(hetm_dev_merge_abort_host(dev_, host_, snapshot_.data(), &ms), "merge_abort_host");
+            rep.bytes_merge = ms.bytes_d2h + ms.bytes_h2d + ms.bytes_d2d;
             check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
         }
         check_rc(hetm_dev_clear_round(dev_, 0), "clear_round");
