@@ -382,6 +382,22 @@ int hetm_dev_debug_words(hetm_dev* dev, uint64_t* out, uint64_t n);
 /* Flush L2 (writes a buffer larger than L2) on `stream` — benchmark hygiene. */
 int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
 
+/* Bank batch schedule.  OPTIMISTIC: the PR-STM-style
+ * phased kernel (lock / ticket / validate / write-back, retries on conflict).
+ * SCAN: an abort-free execution of the batch in input order (ticket = first +
+ * input index): a radix sort of the accesses by account + a segmented scan
+ * of the transfers' deltas; its cost does not grow with skew, while the
+ * optimistic kernel serializes every commit on a hot account.  AUTO (default):
+ * host-buffer batches take SCAN when a sample of the inputs predicts a chain
+ * of >= 1024 conflicting commits on one account (HETM_SCHED_CHAIN), device-
+ * pointer batches stay OPTIMISTIC (their inputs are not visible to the host
+ * without a sync).  The deterministic mode (HETM_CFG_DETERMINISTIC) always
+ * runs bank batches as SCAN: the same input-order serialization, in parallel.
+ * Both schedules give serializable batches whose replay in ticket order is
+ * bit-exact (RS/WS/ChunkMap, write-set log and tickets included). */
+enum { HETM_SCHED_OPTIMISTIC = 0, HETM_SCHED_SCAN = 1, HETM_SCHED_AUTO = 2 };
+int hetm_dev_set_schedule(hetm_dev* dev, int mode);
+
 /* ---------------------------------------------------- checker support -- *
  * Traces for the P1 / P2-dagger consistency checker (the
  * `checker` module).  Recording is toggleable and lossless:

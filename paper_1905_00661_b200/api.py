@@ -20,6 +20,7 @@ BMP_RS, BMP_WS, BMP_CHUNK = 0, 1, 2
 APPLY, VALIDATE_ONLY = 0, 1
 KERNEL_BANK, KERNEL_RW, KERNEL_CACHE = 1, 2, 3
 TRACE_TX_WORDS = 12  # capi.h HETM_TRACE_TX_WORDS
+SCHED_OPTIMISTIC, SCHED_SCAN, SCHED_AUTO = 0, 1, 2  # capi.h HETM_SCHED_* (bank batch schedule)
 FAULT_SKIP_RS, FAULT_SKIP_TS, FAULT_SKIP_ROLLBACK = 1, 2, 4  # capi.h HETM_FAULT_* (checker mutation suite)
 CACHE_GET, CACHE_SET = 0, 1
 CACHE_MISS, CACHE_HIT, CACHE_UPDATED, CACHE_INSERTED, CACHE_EVICTED = range(5)
@@ -444,6 +445,10 @@ class GpuDevice:
         assert out.dtype == np.uint64 and out.flags["C_CONTIGUOUS"]
         self._trace_keep = out
         self._chk(lib.hetm_dev_trace_next_batch(self.h, out.ctypes.data))
+
+    def set_schedule(self, mode: int):
+        """Bank batch schedule: SCHED_OPTIMISTIC | SCHED_SCAN | SCHED_AUTO (default)."""
+        self._chk(lib.hetm_dev_set_schedule(self.h, mode))
 
     def set_fault(self, flags: int):
         """Checker mutation suite only: FAULT_SKIP_RS | FAULT_SKIP_TS | FAULT_SKIP_ROLLBACK."""

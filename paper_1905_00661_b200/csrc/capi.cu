@@ -168,6 +168,9 @@ struct hetm_dev {
     uint64_t trace_cap = 0;                 // in transactions
     uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
+    int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
+    void* d_sched = nullptr;                // SCAN schedule scratch (bank_sched_temp_bytes)
+    size_t sched_bytes = 0;
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
@@ -318,8 +321,49 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 }
 
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
+// Hot-spot estimate of a host-resident bank batch (HETM_SCHED_AUTO): the
+// access count of the hottest account among S sampled transactions, scaled to
+// the batch, estimates the longest chain of conflicting commits the
+// optimistic kernel would serialize (~1.4 us per link on B200,
+// profiles/r01_sched_crossover.txt); above kSchedChain the SCAN schedule wins.
+bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
+    static const uint64_t chain = [] {
+        const char* e = std::getenv("HETM_SCHED_CHAIN");
+        return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+    }();
+    constexpr uint64_t kS = 4096, kSlots = 1 << 15;
+    if (n * 4 < chain) return false;
+    const uint64_t S = std::min(n, kS), stride = n / S;
+    std::vector<uint32_t> key(kSlots, ~0u), cnt(kSlots, 0);
+    uint32_t best = 0;
+    for (uint64_t q = 0; q < S; ++q)
+        for (uint32_t a : in[q * stride].acct) {
+            uint64_t h = (a * 0x9e3779b97f4a7c15ull) >> 49;  // 15 bits
+            while (key[h] != ~0u && key[h] != a) h = (h + 1) & (kSlots - 1);
+            key[h] = a;
+            best = std::max(best, ++cnt[h]);
+        }
+    return (uint64_t)best * n / S >= chain;
+}
+
+int ensure_sched(hetm_dev* d, uint64_t n) {
+    const size_t need = bank_sched_temp_bytes(n, d->W);
+    if (need <= d->sched_bytes) return HETM_OK;
+    if (d->d_sched) {
+        CK(d, cudaDeviceSynchronize());
+        cudaFree(d->d_sched);
+        d->bytes_alloc -= d->sched_bytes;
+        d->d_sched = nullptr;
+        d->sched_bytes = 0;
+    }
+    if (int rc = dev_alloc(d, &d->d_sched, need)) return rc;
+    d->sched_bytes = need;
+    return HETM_OK;
+}
+
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
-                  void* d_results, cudaStream_t s, bool reset_counters = true, unsigned long long* trace = nullptr) {
+                  void* d_results, cudaStream_t s, bool reset_counters = true, unsigned long long* trace = nullptr,
+                  bool hot = false) {
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
@@ -333,7 +377,15 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     }
     ShardView v = d->view();
     v.trace = trace;
-    if (kernel_id == HETM_KERNEL_BANK)
+    // bank: SCAN schedule in the deterministic mode (same input order, no
+    // single worker), when requested, or under AUTO for a hot batch
+    const bool scan = kernel_id == HETM_KERNEL_BANK &&
+                      (v.serial || d->schedule == HETM_SCHED_SCAN || (d->schedule == HETM_SCHED_AUTO && hot));
+    if (scan) {
+        if (int rc = ensure_sched(d, n)) return rc;
+        e = launch_bank_sched(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr, d->d_sched,
+                              d->sched_bytes, d->geom, s);
+    } else if (kernel_id == HETM_KERNEL_BANK)
         e = launch_bank_batch(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                               d->max_attempts, d->geom, s);
     else if (kernel_id == HETM_KERNEL_CACHE)
@@ -610,7 +662,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
-                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero})
+                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     for (auto& v : d->tpairs)
@@ -791,6 +843,8 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         CK(d, cudaMemsetAsync(d->d_trace, 0xff, n_tx * kTraceWords * 8, s));  // ~0: did not commit
         trace = d->d_trace;
     }
+    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
+                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
     const char* in_h = static_cast<const char*>(inputs);
     char* in_d = static_cast<char*>(d->d_in);
     for (uint64_t k = 0; k < P; ++k) {
@@ -804,7 +858,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         CK(d, cudaEventRecord(d->kp_ev[2 * k], s));
         if ((rc = enqueue_batch(d, kernel_id, in_d + lo * rec_bytes, m, d->d_tk + lo,
                                 results_out ? d->d_res + lo : nullptr, s, k == 0,
-                                trace ? trace + lo * kTraceWords : nullptr)))
+                                trace ? trace + lo * kTraceWords : nullptr, hot)))
             return rc;
         CK(d, cudaEventRecord(d->kp_ev[2 * k + 1], s));
         if (m && (tickets_out || results_out)) {
@@ -1659,6 +1713,13 @@ int hetm_dev_trace_next_batch(hetm_dev* d, uint64_t* out_records) {
     if (!d || !out_records) return HETM_ERR_INVALID_ARG;
     std::lock_guard<std::mutex> g(d->mu);
     d->trace_out = out_records;
+    return HETM_OK;
+}
+
+int hetm_dev_set_schedule(hetm_dev* d, int mode) {
+    if (!d || mode < HETM_SCHED_OPTIMISTIC || mode > HETM_SCHED_AUTO) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->schedule = mode;
     return HETM_OK;
 }
 

@@ -75,6 +75,11 @@ cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint3
 // Zero-copy scatter of delta records into a device-accessible host buffer.
 cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
                                     cudaStream_t s);
+// SCAN schedule of a bank batch (bank_sched.cu): sort + segmented scan, input
+// order, no aborts; temp from bank_sched_temp_bytes.
+size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words);
+cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
+                              DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

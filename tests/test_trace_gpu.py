@@ -92,14 +92,17 @@ def _replay_records(state, txs, rec, kernel):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("sched", ["optimistic", "scan"])
 @pytest.mark.parametrize("hot", [False, True])
-def test_device_trace_records_match_ticket_replay(hot):
-    """hetm_dev_trace_next_batch: the traced bank kernel's per-transaction read / write values are
-    exactly what the ticket-order serial replay reads and writes (hot = contended 256-account span)."""
+def test_device_trace_records_match_ticket_replay(hot, sched):
+    """hetm_dev_trace_next_batch: the traced bank batch's per-transaction read / write values are
+    exactly what the ticket-order serial replay reads and writes (hot = contended 256-account span),
+    for both schedules."""
     import paper_1905_00661_b200 as hetm
     W, B = 1 << 16, 1 << 13
     d = hetm.GpuDevice(W, rs_gran_bytes=1024)
     d.register_kernel(hetm.KERNEL_BANK)
+    d.set_schedule(hetm.SCHED_SCAN if sched == "scan" else hetm.SCHED_OPTIMISTIC)
     init = (np.arange(W, dtype=np.uint64) * np.uint64(7919)) % np.uint64(100000)
     d.upload(hetm.REPLICA_DEV, 0, init)
     txs = hetm.gen_bank_batch(11, B, 0, 256 if hot else W)
