@@ -389,9 +389,11 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
  * of the transfers' deltas; its cost does not grow with skew, while the
  * optimistic kernel serializes every commit on a hot account.  AUTO (default):
  * host-buffer batches take SCAN when a sample of the inputs predicts a chain
- * of >= 1024 conflicting commits on one account (HETM_SCHED_CHAIN), device-
- * pointer batches stay OPTIMISTIC (their inputs are not visible to the host
- * without a sync).  The deterministic mode (HETM_CFG_DETERMINISTIC) always
+ * of >= 1024 conflicting commits on one account (HETM_SCHED_CHAIN); device-
+ * pointer batches follow the same estimate of an EARLIER device batch of the
+ * handle (a one-CTA kernel samples each batch on a side stream into mapped
+ * host memory, read by the next call without a sync), so a steady hot
+ * workload switches after its first batch.  The deterministic mode (HETM_CFG_DETERMINISTIC) always
  * runs bank batches as SCAN: the same input-order serialization, in parallel.
  * Both schedules give serializable batches whose replay in ticket order is
  * bit-exact (RS/WS/ChunkMap, write-set log and tickets included). */

@@ -181,6 +181,59 @@ uint32_t bits_for(uint64_t x) {  // bits to hold values < x
 
 }  // namespace
 
+// Hot-spot estimate of a device-resident bank batch (AUTO on the device-
+// pointer path): one CTA inserts the accounts of kEstTx sampled transactions
+// into a shared-memory hash table of {account, count} and stores the largest
+// count to *out (mapped host memory: the next batch reads it without a sync).
+constexpr unsigned kEstThreads = 1024, kEstTx = 2048, kEstSlots = 1u << 14;  // 8 K keys, load 0.5
+constexpr size_t kEstSmem = kEstSlots * sizeof(unsigned long long);           // 128 KiB
+
+__global__ void __launch_bounds__(kEstThreads) hot_estimate_kernel(const hetm_bank_tx* __restrict__ in, uint64_t n,
+                                                                   uint32_t* out) {
+    extern __shared__ unsigned long long slot[];  // account << 32 | count; ~0 = empty
+    for (unsigned q = threadIdx.x; q < kEstSlots; q += blockDim.x) slot[q] = ~0ull;
+    __syncthreads();
+    const uint64_t S = n < kEstTx ? n : kEstTx, stride = n / S;
+    unsigned best = 0;
+    for (uint64_t q = threadIdx.x; q < 4 * S; q += blockDim.x) {
+        const uint32_t a = in[(q >> 2) * stride].acct[q & 3];
+        uint32_t h = (uint32_t)((a * 0x9e3779b97f4a7c15ull) >> 50);  // 14 bits
+        for (;;) {
+            unsigned long long cur = slot[h];
+            if (cur == ~0ull) {
+                cur = atomicCAS(&slot[h], ~0ull, (unsigned long long)a << 32 | 1u);
+                if (cur == ~0ull) {
+                    best = best > 1u ? best : 1u;
+                    break;
+                }
+            }
+            if ((uint32_t)(cur >> 32) == a) {
+                const unsigned c = (unsigned)(atomicAdd(&slot[h], 1ull) & 0xffffffffu) + 1u;
+                best = best > c ? best : c;
+                break;
+            }
+            h = (h + 1) & (kEstSlots - 1);
+        }
+    }
+    __shared__ unsigned block_best;
+    if (threadIdx.x == 0) block_best = 0;
+    __syncthreads();
+    atomicMax(&block_best, best);
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(out) = block_best;
+}
+
+cudaError_t launch_bank_hot_estimate(const hetm_bank_tx* d_in, uint64_t n, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(hot_estimate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEstSmem);
+    if (attr != cudaSuccess) return attr;
+    hot_estimate_kernel<<<1, kEstThreads, kEstSmem, s>>>(d_in, n, out);
+    return cudaGetLastError();
+}
+
+uint64_t bank_hot_estimate_sample(uint64_t n) { return n < kEstTx ? n : kEstTx; }
+
 size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words) {
     const uint64_t n4 = 4 * n;
     const uint32_t sh = bits_for(n4), end_bit = std::min<uint32_t>(64, sh + bits_for(size_words) + 1);

@@ -169,6 +169,10 @@ struct hetm_dev {
     uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
     int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
+    uint32_t* h_hot = nullptr;              // device-side hot-spot estimate (mapped host word)
+    uint32_t* d_hot = nullptr;
+    cudaStream_t s_est = nullptr;           // the estimator runs off the batch's critical path
+    cudaEvent_t ev_est = nullptr;
     void* d_sched = nullptr;                // SCAN schedule scratch (bank_sched_temp_bytes)
     size_t sched_bytes = 0;
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
@@ -326,11 +330,19 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 // the batch, estimates the longest chain of conflicting commits the
 // optimistic kernel would serialize (~1.4 us per link on B200,
 // profiles/r01_sched_crossover.txt); above kSchedChain the SCAN schedule wins.
-bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
+uint64_t sched_chain() {
     static const uint64_t chain = [] {
         const char* e = std::getenv("HETM_SCHED_CHAIN");
         return e ? std::strtoull(e, nullptr, 10) : 1024ull;
     }();
+    return chain;
+}
+// A count of >= 3 in the sample is required: chance pairs are common under
+// uniform access (8 K sampled accounts over 2^26 meet ~0.5 times).
+bool hot_chain(uint64_t best, uint64_t n, uint64_t S, uint64_t chain) { return best >= 3 && best * n / S >= chain; }
+
+bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
+    const uint64_t chain = sched_chain();
     constexpr uint64_t kS = 4096, kSlots = 1 << 15;
     if (n * 4 < chain) return false;
     const uint64_t S = std::min(n, kS), stride = n / S;
@@ -343,7 +355,7 @@ bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
             key[h] = a;
             best = std::max(best, ++cnt[h]);
         }
-    return (uint64_t)best * n / S >= chain;
+    return hot_chain(best, n, S, chain);
 }
 
 int ensure_sched(hetm_dev* d, uint64_t n) {
@@ -659,6 +671,12 @@ int hetm_dev_close(hetm_dev* d) {
     if (d->h_delta) cudaFreeHost(d->h_delta);
     for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
+    if (d->s_est) {
+        cudaStreamSynchronize(d->s_est);
+        cudaStreamDestroy(d->s_est);
+        cudaEventDestroy(d->ev_est);
+        cudaFreeHost(d->h_hot);
+    }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
@@ -1492,8 +1510,27 @@ int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inp
     if (n_tx >= (1ull << 30)) return HETM_ERR_INVALID_SIZE;
     if (d_results && kernel_id != HETM_KERNEL_CACHE) return HETM_ERR_INVALID_SIZE;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_exec;
+    bool hot = false;
+    if (kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx) {
+        // AUTO without a host view of the inputs: follow the estimate of an earlier
+        // device batch (written to mapped host memory, read without a sync) and
+        // estimate this one on a side stream for the next.
+        if (!d->h_hot) {
+            CK(d, cudaHostAlloc((void**)&d->h_hot, 64, cudaHostAllocMapped));
+            *d->h_hot = 0;
+            CK(d, cudaHostGetDevicePointer((void**)&d->d_hot, d->h_hot, 0));
+            CK(d, cudaStreamCreateWithFlags(&d->s_est, cudaStreamNonBlocking));
+            CK(d, cudaEventCreateWithFlags(&d->ev_est, cudaEventDisableTiming));
+        }
+        const uint32_t last = *reinterpret_cast<volatile uint32_t*>(d->h_hot);
+        hot = hot_chain(last, n_tx, bank_hot_estimate_sample(n_tx), sched_chain());
+        CK(d, cudaEventRecord(d->ev_est, s));
+        CK(d, cudaStreamWaitEvent(d->s_est, d->ev_est, 0));
+        cudaError_t e = launch_bank_hot_estimate(static_cast<const hetm_bank_tx*>(d_inputs), n_tx, d->d_hot, d->s_est);
+        if (e != cudaSuccess) return fail(d, e, "hot_estimate");
+    }
     return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), d_results,
-                         s);
+                         s, true, nullptr, hot);
 }
 
 int hetm_dev_set_cache_geometry(hetm_dev* d, uint64_t base_word, uint64_t n_sets) {

@@ -78,6 +78,10 @@ cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint6
 // SCAN schedule of a bank batch (bank_sched.cu): sort + segmented scan, input
 // order, no aborts; temp from bank_sched_temp_bytes.
 size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words);
+// Device-side hot-spot estimate: largest account count among
+// bank_hot_estimate_sample(n) sampled transactions -> *out (mapped host word).
+cudaError_t launch_bank_hot_estimate(const hetm_bank_tx* d_in, uint64_t n, uint32_t* out, cudaStream_t s);
+uint64_t bank_hot_estimate_sample(uint64_t n);
 cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                               DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.

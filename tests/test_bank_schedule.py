@@ -109,3 +109,40 @@ def test_deterministic_mode_runs_scan_in_input_order(hetm, orc, dev_factory):
     r = d.execute_batch(hetm.KERNEL_BANK, txs)
     assert (r.tickets == r.ticket_first + np.arange(n, dtype=np.uint64)).all() and r.aborts == 0
     check_replay(hetm, orc, d, txs, r.tickets, init, 8, 16384)
+
+
+def test_auto_device_batches_follow_the_previous_estimate(hetm, orc, dev_factory):
+    """Device-pointer batches under AUTO: the first hot batch runs optimistic, later ones switch to
+    SCAN from the side-stream estimate of an earlier batch; uniform batches never switch."""
+    import torch
+    W, n = 1 << 16, 1 << 14
+    d = dev_factory(W, rs_gran_bytes=1024)
+    d.register_kernel(hetm.KERNEL_BANK)
+    init = np.full(W, 1000, np.uint64)
+    d.upload(hetm.REPLICA_DEV, 0, init)
+    tk = torch.empty(n, dtype=torch.int64, device="cuda")
+
+    def run(txs):
+        b = torch.from_numpy(txs.view(np.uint8)).cuda()
+        d.execute_batch_dptr(hetm.KERNEL_BANK, b.data_ptr(), n, tk.data_ptr())
+        d.sync()
+        _, st = d.read_counters()
+        t = tk.cpu().numpy().view(np.uint64)
+        d.clear_round()
+        return st, t
+
+    ref = init.copy()
+    sts = []
+    for k in range(4):
+        txs = orc.gen_bank_batch(60 + k, n, 0, W, zipf=0.99)
+        st, t = run(txs)
+        orc.bank_replay(ref, txs, orc.order_by_ticket(t), 1024, 16384)
+        sts.append((st.aborts, bool((np.diff(t.astype(np.int64)) == 1).all())))
+    assert (d.download(hetm.REPLICA_DEV) == ref).all()
+    assert sts[0][0] > 0                              # first hot batch: optimistic (no estimate yet)
+    assert sts[-1] == (0, True)                       # later: SCAN in input order
+    for k in range(3):
+        st, t = run(orc.gen_bank_batch(90 + k, n, 0, W))
+        orc.bank_replay(ref, orc.gen_bank_batch(90 + k, n, 0, W), orc.order_by_ticket(t), 1024, 16384)
+    assert (d.download(hetm.REPLICA_DEV) == ref).all()
+    assert not (np.diff(t.astype(np.int64)) == 1).all()  # back to optimistic on uniform input
