@@ -4,16 +4,18 @@
 // A bank transaction's writes are read-modify-writes with known deltas
 // (acct0 -= amount, acct1 += amount; acct2/acct3 only read), so the serial
 // execution of the batch in input order is a segmented prefix sum:
-//   1. keys: one 64-bit key per access, loc << sh | i << 2 | k (sh = bits of
-//      4n), so sorting groups each account's accesses in input order;
-//   2. CUB radix sort of the 4n keys;
+//   1. per transaction (coalesced): one 32-bit key per access (the account)
+//      with the payload (4 i + k) << 1 | writer and the access's delta; the
+//      ticket and write-set log slots are written here too;
+//   2. CUB radix sort of the 4n (account, payload) pairs on the account bits
+//      only — the sort is stable, so each account's accesses stay in input
+//      order;
 //   3. CUB inclusive scan-by-account of {delta, last writer}: the delta of an
 //      access is the transaction's net effect on that account (last write wins
 //      when acct0 == acct1), carried by the first slot naming the account;
 //   4. one pass over the sorted accesses: at the end of each account's segment
 //      the final value and version (lk_commit of the last writer's ticket) are
-//      stored and the WS / chunk bits set, at its start the RS bit; every
-//      access of slot 0/1 writes its ticket and write-set log slot.  With a
+//      stored and the WS / chunk bits set, at its start the RS bit.  With a
 //      trace armed, a read-only pass first records each access's pre-value.
 // Cost is independent of skew (no locks, no retries): at zipf 0.99 the
 // optimistic PR-STM kernel serializes ~10^5 commits on the hottest account.
@@ -27,6 +29,8 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 namespace hetm_b200 {
 
@@ -34,6 +38,7 @@ namespace {
 
 constexpr unsigned kSchedThreads = 256;
 constexpr unsigned long long kNone = ~0ull;
+constexpr uint32_t kNoLoc = 0xffffffffu;  // sort sentinel: accesses of rejected transactions
 
 struct DeltaW {  // scan value: summed delta, last writing transaction (input index) or kNone
     unsigned long long d, w;
@@ -44,10 +49,17 @@ struct DeltaWOp {
     }
 };
 
-struct LocOf {  // segment key: the account (sentinels form their own segment)
-    using result_type = unsigned long long;
-    uint32_t sh;
-    __host__ __device__ unsigned long long operator()(unsigned long long key) const { return key >> sh; }
+// Sort payload: access index a = 4 i + k (input order) << 1 | writer, where
+// writer marks the transaction's first slot naming an account it writes.
+__device__ __forceinline__ uint32_t acc_of(uint32_t p) { return p >> 1; }
+__device__ __forceinline__ uint64_t tx_of(uint32_t p) { return p >> 3; }
+
+struct DeltaOf {  // scan value of a sorted access: its precomputed delta + writer
+    using result_type = DeltaW;
+    const unsigned long long* delta;
+    __device__ DeltaW operator()(uint32_t p) const {
+        return DeltaW{delta[acc_of(p)], (p & 1u) ? tx_of(p) : kNone};
+    }
 };
 
 __device__ __forceinline__ void load_accts(const hetm_bank_tx* in, uint64_t i, uint64_t base, uint64_t (&a)[4],
@@ -61,70 +73,67 @@ __device__ __forceinline__ void load_accts(const hetm_bank_tx* in, uint64_t i, u
     a[3] = (w23 >> 32) - base;
 }
 
-struct DeltaOf {  // the access's scan value
-    using result_type = DeltaW;
-    const hetm_bank_tx* in;
-    uint64_t base;
-    uint32_t sh;
-    __device__ DeltaW operator()(unsigned long long key) const {
-        if (key == kNone) return DeltaW{0, kNone};
-        const uint64_t i = (key & ((1ull << sh) - 1)) >> 2;
-        const int k = (int)(key & 3);
-        uint64_t a[4], amount;
-        load_accts(in, i, base, a, amount);
-        for (int q = 0; q < k; ++q)
-            if (a[q] == a[k]) return DeltaW{0, kNone};  // not the first slot naming this account
-        if (a[k] == a[1]) return DeltaW{amount, i};   // the last write wins (acct1 after acct0)
-        if (a[k] == a[0]) return DeltaW{0ull - amount, i};
-        return DeltaW{0, kNone};
-    }
-};
-
-__global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ in, uint64_t n, uint32_t sh,
-                                  unsigned long long* __restrict__ keys, unsigned long long* __restrict__ tickets,
+// Per transaction (coalesced): the 4 sort keys + payloads, the per-access
+// deltas (the tx's net effect on an account — the last write wins, acct1
+// after acct0 — on the first slot naming it), its ticket and write-set log
+// slots; a rejected (out-of-shard) transaction gets sentinel keys, no ticket
+// and empty log slots.
+__global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ in, uint64_t n,
+                                  uint32_t* __restrict__ locs, uint32_t* __restrict__ pay,
+                                  unsigned long long* __restrict__ delta, unsigned long long* __restrict__ tickets,
                                   const unsigned long long* first, DevCounters* ctr) {
-    const uint64_t base = v.base, size_words = v.size_words;
     const unsigned long long t0 = *first, wbase = ld_relaxed(&ctr->wlog_base);
     unsigned oob = 0;
+    unsigned long long commits = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t a[4], amount;
-        load_accts(in, i, base, a, amount);
-        const bool ok = a[0] < size_words && a[1] < size_words && a[2] < size_words && a[3] < size_words;
+        load_accts(in, i, v.base, a, amount);
+        const bool ok = a[0] < v.size_words && a[1] < v.size_words && a[2] < v.size_words && a[3] < v.size_words;
+        const unsigned long long t = t0 + i;
         oob |= !ok;
-        if (!ok) {  // rejected (outside this shard): no ticket, its log slots empty
-            tickets[i] = kNone;
-            wlog_put(v, wbase, t0 + i, 0, ~0u);
-            wlog_put(v, wbase, t0 + i, 1, ~0u);
-        }
+        commits += ok;
+        tickets[i] = ok ? t : kNone;
+        wlog_put(v, wbase, t, 0, ok ? (uint32_t)a[0] : ~0u);
+        wlog_put(v, wbase, t, 1, ok ? (uint32_t)a[1] : ~0u);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) keys[4 * i + k] = ok ? (a[k] << sh | i << 2 | (uint64_t)k) : kNone;
+        for (int k = 0; k < 4; ++k) {
+            bool first_slot = true;
+#pragma unroll
+            for (int q = 0; q < k; ++q) first_slot &= a[q] != a[k];
+            const unsigned long long d = !first_slot ? 0ull : a[k] == a[1] ? amount : a[k] == a[0] ? 0ull - amount : 0ull;
+            const bool writer = first_slot && (a[k] == a[0] || a[k] == a[1]);
+            locs[4 * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
+            pay[4 * i + k] = (uint32_t)(4 * i + k) << 1 | (uint32_t)writer;
+            delta[4 * i + k] = d;
+        }
     }
     if (__any_sync(0xffffffffu, oob) && lane_id() == 0) atomicOr(&ctr->oob, 1u);
+    const unsigned long long c = warp_sum(commits);
+    if (lane_id() == 0 && c) atomicAdd(&ctr->committed, c);
 }
 
-// First ticket of the batch; tickets of rejected (out-of-shard) transactions
-// stay unused, their write-set log slots empty.
+// First ticket of the batch (ticket = first + input index).
 __global__ void sched_ticket_kernel(DevCounters* ctr, uint64_t n, unsigned long long* first) {
     *first = atomicAdd(&ctr->ticket, (unsigned long long)n);
 }
 
 // Read-only pass (traced batches): the value every access reads = the account's
 // batch-start value + the deltas of the earlier transactions.
-__global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__ in, uint64_t n4, uint32_t sh,
-                                   const unsigned long long* __restrict__ keys, const DeltaW* __restrict__ incl,
+__global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__ in, uint64_t n4,
+                                   const uint32_t* __restrict__ locs, const uint32_t* __restrict__ pay,
+                                   const unsigned long long* __restrict__ delta, const DeltaW* __restrict__ incl,
                                    const unsigned long long* first) {
     const unsigned long long t0 = *first;
-    const DeltaOf dof{in, v.base, sh};
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long key = keys[j];
-        if (key == kNone) continue;
-        const uint64_t loc = key >> sh, i = (key & ((1ull << sh) - 1)) >> 2;
-        const int k = (int)(key & 3);
+        const uint32_t loc = locs[j];
+        if (loc == kNoLoc) continue;
+        const uint64_t i = tx_of(pay[j]);
+        const int k = (int)(acc_of(pay[j]) & 3);
         // pre-value: exclusive of this transaction's own delta, which sits on its
-        // first slot naming the account (the entry itself or an earlier one of i)
+        // first slot naming the account (this entry or an earlier one of tx i)
         uint64_t jj = j;
-        while (jj > 0 && (keys[jj - 1] >> 2) == (key >> 2)) --jj;  // first entry of (loc, i)
-        const unsigned long long pre = v.cells[loc].value + incl[jj].d - dof(keys[jj]).d;
+        while (jj > 0 && locs[jj - 1] == loc && tx_of(pay[jj - 1]) == i) --jj;
+        const unsigned long long pre = v.cells[loc].value + incl[jj].d - delta[acc_of(pay[jj])];
         unsigned long long* r = v.trace + i * kTraceWords;
         if (k == 0) r[0] = t0 + i;
         r[1 + k] = pre;
@@ -137,35 +146,32 @@ __global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__
     }
 }
 
-__global__ void sched_commit_kernel(ShardView v, uint64_t n4, uint32_t sh, const unsigned long long* __restrict__ keys,
-                                    const DeltaW* __restrict__ incl, const unsigned long long* first,
-                                    unsigned long long* __restrict__ tickets, DevCounters* ctr) {
+// Per sorted access: RS at each account's first access, the final value and
+// version + WS / ChunkMap at the last one if the account was written.  The
+// bitmap words are probed first (most are set already: RS/WS/ChunkMap are
+// L2-resident), so only first-time bits cost an atomic.
+__global__ void sched_commit_kernel(ShardView v, uint64_t n4, const uint32_t* __restrict__ locs,
+                                    const DeltaW* __restrict__ incl, const unsigned long long* first) {
     const unsigned long long t0 = *first;
-    const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
-    unsigned long long commits = 0;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long key = keys[j];
-        if (key == kNone) continue;
-        const uint64_t loc = key >> sh, i = (key & ((1ull << sh) - 1)) >> 2;
-        const int k = (int)(key & 3);
-        const unsigned long long t = t0 + i;
-        if (k == 0) {
-            tickets[i] = t;
-            ++commits;
+        const uint32_t loc = locs[j];
+        if (loc == kNoLoc) continue;
+        const bool seg_first = j == 0 || locs[j - 1] != loc;
+        const bool seg_last = j + 1 == n4 || locs[j + 1] != loc;
+        if (seg_first) {  // every access reads (RS = reads U writes)
+            const uint64_t b = loc >> v.gran_shift;
+            if (!test_bit(v.rs, b)) set_bit(v.rs, b);
         }
-        if (k < 2) wlog_put(v, wbase, t, k, (uint32_t)loc);
-        const bool seg_first = j == 0 || (keys[j - 1] >> sh) != loc;
-        const bool seg_last = j + 1 == n4 || (keys[j + 1] >> sh) != loc;
-        if (seg_first) set_bit(v.rs, loc >> v.gran_shift);  // every access reads (RS = reads U writes)
-        if (seg_last && incl[j].w != kNone) {
-            const Cell c{v.cells[loc].value + incl[j].d, lk_commit(t0 + incl[j].w)};
-            st_pair(&v.cells[loc], c.value, c.meta);
-            set_bit(v.ws, loc >> v.gran_shift);
-            set_bit(v.chunk, loc >> v.chunk_shift);
+        if (seg_last) {
+            const DeltaW x = incl[j];
+            if (x.w != kNone) {
+                st_pair(&v.cells[loc], v.cells[loc].value + x.d, lk_commit(t0 + x.w));
+                const uint64_t b = loc >> v.gran_shift, c = loc >> v.chunk_shift;
+                if (!test_bit(v.ws, b)) set_bit(v.ws, b);
+                if (!test_bit(v.chunk, c)) set_bit(v.chunk, c);
+            }
         }
     }
-    const unsigned long long c = warp_sum(commits);
-    if (lane_id() == 0 && c) atomicAdd(&ctr->committed, c);
 }
 
 unsigned grid_for(uint64_t n, unsigned threads, unsigned blocks_per_sm, int sms) {
@@ -236,44 +242,119 @@ uint64_t bank_hot_estimate_sample(uint64_t n) { return n < kEstTx ? n : kEstTx; 
 
 size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words) {
     const uint64_t n4 = 4 * n;
-    const uint32_t sh = bits_for(n4), end_bit = std::min<uint32_t>(64, sh + bits_for(size_words) + 1);
+    const int end_bit = (int)std::min<uint32_t>(32, bits_for(size_words) + 1);  // + the sentinel
     size_t a = 0, b = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                   (int64_t)n4, 0, (int)end_bit);
-    auto ki = thrust::make_transform_iterator((const unsigned long long*)nullptr, LocOf{sh});
-    auto vi = thrust::make_transform_iterator((const unsigned long long*)nullptr, DeltaOf{nullptr, 0, sh});
-    cub::DeviceScan::InclusiveScanByKey(nullptr, b, ki, vi, (DeltaW*)nullptr, DeltaWOp{}, (int64_t)n4);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n4, 0, end_bit);
+    auto vi = thrust::make_transform_iterator((const uint32_t*)nullptr, DeltaOf{nullptr});
+    cub::DeviceScan::InclusiveScanByKey(nullptr, b, (const uint32_t*)nullptr, vi, (DeltaW*)nullptr, DeltaWOp{},
+                                        (int64_t)n4);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    // [keys | sorted keys | scan | first ticket | cub temp]
-    return al(n4 * 8) * 2 + al(n4 * sizeof(DeltaW)) + 256 + al(std::max(a, b));
+    // [locs in/out | payload in/out | delta | scan | first ticket | cub temp]
+    return 4 * al(n4 * 4) + al(n4 * 8) + al(n4 * sizeof(DeltaW)) + 256 + al(std::max(a, b));
 }
 
 cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
-                              DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s) {
+                              DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s,
+                              SchedGraph* graph) {
     if (n == 0) return cudaSuccess;
+    if (graph && !v.trace) {
+        // Replay the captured sequence: ~10 dependent launches (4 sort passes, the
+        // scan, CUB's bookkeeping) cost more host time than GPU time when issued
+        // one by one.  Only the keys kernel's inputs / tickets change per batch.
+        const bool same = graph->exec && graph->n == n && graph->temp == temp && graph->wlog == v.wlog &&
+                          graph->wlog_slots == v.wlog_slots && graph->cells == v.cells && graph->ctr == ctr;
+        if (!same) {
+            if (graph->exec) cudaGraphExecDestroy(graph->exec);
+            if (graph->graph) cudaGraphDestroy(graph->graph);
+            graph->exec = nullptr;
+            graph->graph = nullptr;
+            if (!graph->cap) {
+                cudaError_t e = cudaStreamCreateWithFlags(&graph->cap, cudaStreamNonBlocking);
+                if (e != cudaSuccess) return e;
+            }
+            cudaError_t e = cudaStreamBeginCapture(graph->cap, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return e;
+            e = launch_bank_sched(v, d_in, n, d_tickets, ctr, temp, temp_bytes, g, graph->cap, nullptr);
+            cudaGraph_t gr = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(graph->cap, &gr);
+            if (e != cudaSuccess || e2 != cudaSuccess) {
+                if (gr) cudaGraphDestroy(gr);
+                return e != cudaSuccess ? e : e2;
+            }
+            size_t nn = 0;
+            cudaGraphGetNodes(gr, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            cudaGraphGetNodes(gr, nodes.data(), &nn);
+            graph->keys_node = nullptr;
+            for (auto nd : nodes) {
+                cudaGraphNodeType t;
+                cudaKernelNodeParams kp{};
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel &&
+                    cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+                    kp.func == reinterpret_cast<void*>(sched_keys_kernel)) {
+                    graph->keys_node = nd;
+                    auto& a = graph->keys_args;
+                    void* dst[9] = {&a.v, &a.in, &a.n, &a.locs, &a.pay, &a.delta, &a.tickets, &a.first, &a.ctr};
+                    const size_t sz[9] = {sizeof a.v, 8, 8, 8, 8, 8, 8, 8, 8};
+                    for (int q = 0; q < 9; ++q) {
+                        std::memcpy(dst[q], kp.kernelParams[q], sz[q]);
+                        graph->keys_ptrs[q] = dst[q];
+                    }
+                    graph->keys_params = kp;
+                    graph->keys_params.kernelParams = graph->keys_ptrs;
+                    graph->keys_params.extra = nullptr;
+                }
+            }
+            e = graph->keys_node ? cudaGraphInstantiate(&graph->exec, gr, 0) : cudaErrorUnknown;
+            if (e != cudaSuccess) {
+                cudaGraphDestroy(gr);
+                graph->exec = nullptr;
+                return e;
+            }
+            graph->graph = gr;
+            graph->n = n;
+            graph->temp = temp;
+            graph->wlog = v.wlog;
+            graph->wlog_slots = v.wlog_slots;
+            graph->cells = v.cells;
+            graph->ctr = ctr;
+        }
+        // sched_keys_kernel(v, in, n, locs, pay, delta, tickets, first, ctr): patch in + tickets
+        graph->keys_args.in = d_in;
+        graph->keys_args.tickets = d_tickets;
+        cudaError_t e = cudaGraphExecKernelNodeSetParams(graph->exec, graph->keys_node, &graph->keys_params);
+        if (e != cudaSuccess) return e;
+        return cudaGraphLaunch(graph->exec, s);
+    }
+    if (n >= (1ull << 29)) return cudaErrorInvalidValue;  // 4n << 1 payloads fit 32 bits
     const uint64_t n4 = 4 * n;
-    const uint32_t sh = bits_for(n4), end_bit = std::min<uint32_t>(64, sh + bits_for(v.size_words) + 1);
+    const int end_bit = (int)std::min<uint32_t>(32, bits_for(v.size_words) + 1);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     char* p = static_cast<char*>(temp);
-    auto* keys = reinterpret_cast<unsigned long long*>(p);
-    auto* sorted = reinterpret_cast<unsigned long long*>(p + al(n4 * 8));
-    auto* incl = reinterpret_cast<DeltaW*>(p + 2 * al(n4 * 8));
-    auto* first = reinterpret_cast<unsigned long long*>(p + 2 * al(n4 * 8) + al(n4 * sizeof(DeltaW)));
-    void* cub_tmp = p + 2 * al(n4 * 8) + al(n4 * sizeof(DeltaW)) + 256;
-    size_t cub_bytes = temp_bytes - (2 * al(n4 * 8) + al(n4 * sizeof(DeltaW)) + 256);
+    uint32_t* locs = reinterpret_cast<uint32_t*>(p);
+    uint32_t* locs_s = reinterpret_cast<uint32_t*>(p + al(n4 * 4));
+    uint32_t* pay = reinterpret_cast<uint32_t*>(p + 2 * al(n4 * 4));
+    uint32_t* pay_s = reinterpret_cast<uint32_t*>(p + 3 * al(n4 * 4));
+    auto* delta = reinterpret_cast<unsigned long long*>(p + 4 * al(n4 * 4));
+    auto* incl = reinterpret_cast<DeltaW*>(p + 4 * al(n4 * 4) + al(n4 * 8));
+    const size_t off = 4 * al(n4 * 4) + al(n4 * 8) + al(n4 * sizeof(DeltaW));
+    auto* first = reinterpret_cast<unsigned long long*>(p + off);
+    void* cub_tmp = p + off + 256;
+    size_t cub_bytes = temp_bytes - (off + 256);
     const unsigned grid_tx = grid_for(n, kSchedThreads, 8, g.sm_count);
     const unsigned grid_acc = grid_for(n4, kSchedThreads, 8, g.sm_count);
     sched_ticket_kernel<<<1, 1, 0, s>>>(ctr, n, first);
-    sched_keys_kernel<<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, sh, keys, d_tickets, first, ctr);
-    cudaError_t e = cub::DeviceRadixSort::SortKeys(cub_tmp, cub_bytes, keys, sorted, (int64_t)n4, 0, (int)end_bit, s);
+    sched_keys_kernel<<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, locs, locs_s, pay, pay_s, (int64_t)n4, 0,
+                                                    end_bit, s);
     if (e != cudaSuccess) return e;
-    auto ki = thrust::make_transform_iterator((const unsigned long long*)sorted, LocOf{sh});
-    auto vi = thrust::make_transform_iterator((const unsigned long long*)sorted, DeltaOf{d_in, v.base, sh});
-    e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, ki, vi, incl, DeltaWOp{}, (int64_t)n4,
-                                             cub::Equality(), s);
+    auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf{delta});
+    e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
+                                             (int64_t)n4, cub::Equality(), s);
     if (e != cudaSuccess) return e;
-    if (v.trace) sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, sh, sorted, incl, first);
-    sched_commit_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, n4, sh, sorted, incl, first, d_tickets, ctr);
+    if (v.trace) sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, locs_s, pay_s, delta, incl, first);
+    sched_commit_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
     return cudaGetLastError();
 }
 

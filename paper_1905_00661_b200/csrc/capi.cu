@@ -175,6 +175,7 @@ struct hetm_dev {
     cudaEvent_t ev_est = nullptr;
     void* d_sched = nullptr;                // SCAN schedule scratch (bank_sched_temp_bytes)
     size_t sched_bytes = 0;
+    SchedGraph sched_graph;                 // its captured launch sequence
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
@@ -395,8 +396,12 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
                       (v.serial || d->schedule == HETM_SCHED_SCAN || (d->schedule == HETM_SCHED_AUTO && hot));
     if (scan) {
         if (int rc = ensure_sched(d, n)) return rc;
+        static const bool use_graph = [] {  // HETM_SCHED_GRAPH=0: launch kernel by kernel (experiments)
+            const char* e = std::getenv("HETM_SCHED_GRAPH");
+            return !e || std::atoi(e) != 0;
+        }();
         e = launch_bank_sched(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr, d->d_sched,
-                              d->sched_bytes, d->geom, s);
+                              d->sched_bytes, d->geom, s, use_graph ? &d->sched_graph : nullptr);
     } else if (kernel_id == HETM_KERNEL_BANK)
         e = launch_bank_batch(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                               d->max_attempts, d->geom, s);
@@ -671,6 +676,9 @@ int hetm_dev_close(hetm_dev* d) {
     if (d->h_delta) cudaFreeHost(d->h_delta);
     for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
+    if (d->sched_graph.exec) cudaGraphExecDestroy(d->sched_graph.exec);
+    if (d->sched_graph.graph) cudaGraphDestroy(d->sched_graph.graph);
+    if (d->sched_graph.cap) cudaStreamDestroy(d->sched_graph.cap);
     if (d->s_est) {
         cudaStreamSynchronize(d->s_est);
         cudaStreamDestroy(d->s_est);

@@ -82,8 +82,34 @@ size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words);
 // bank_hot_estimate_sample(n) sampled transactions -> *out (mapped host word).
 cudaError_t launch_bank_hot_estimate(const hetm_bank_tx* d_in, uint64_t n, uint32_t* out, cudaStream_t s);
 uint64_t bank_hot_estimate_sample(uint64_t n);
+// Captured CUDA graph of the untraced SCAN sequence (one per handle), rebuilt
+// when the batch size or a buffer changes; nullptr launches kernel by kernel.
+struct SchedGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;  // kept: the exec's node handles refer to it
+    cudaStream_t cap = nullptr;   // private capture stream
+    cudaGraphNode_t keys_node = nullptr;
+    cudaKernelNodeParams keys_params{};
+    // owned copies of the keys kernel's arguments (the captured node's own
+    // storage dies with the graph): its signature in bank_sched.cu
+    struct KeysArgs {
+        ShardView v;
+        const void* in;
+        uint64_t n;
+        void *locs, *pay, *delta, *tickets;
+        const void* first;
+        void* ctr;
+    } keys_args{};
+    void* keys_ptrs[9] = {};
+    uint64_t n = 0, wlog_slots = 0;
+    void* temp = nullptr;
+    const void* wlog = nullptr;
+    const void* cells = nullptr;
+    const void* ctr = nullptr;
+};
 cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
-                              DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
+                              DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s,
+                              SchedGraph* graph = nullptr);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
