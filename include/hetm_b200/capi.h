@@ -395,8 +395,11 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
  * host memory, read by the next call without a sync), so a steady hot
  * workload switches after its first batch.  The deterministic mode (HETM_CFG_DETERMINISTIC) always
  * runs bank batches as SCAN: the same input-order serialization, in parallel.
+ * Cache batches have a SCAN schedule too (a stable sort by set, then one
+ * thread per set runs that set's transactions in input order with the set in
+ * registers); AUTO uses it for batches of >= 8192 transactions.
  * Both schedules give serializable batches whose replay in ticket order is
- * bit-exact (RS/WS/ChunkMap, write-set log and tickets included). */
+ * bit-exact (RS/WS/ChunkMap, write-set log, results and tickets included). */
 enum { HETM_SCHED_OPTIMISTIC = 0, HETM_SCHED_SCAN = 1, HETM_SCHED_AUTO = 2 };
 int hetm_dev_set_schedule(hetm_dev* dev, int mode);
 

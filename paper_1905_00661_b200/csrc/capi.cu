@@ -359,8 +359,15 @@ bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
     return hot_chain(best, n, S, chain);
 }
 
-int ensure_sched(hetm_dev* d, uint64_t n) {
-    const size_t need = bank_sched_temp_bytes(n, d->W);
+// AUTO runs cache batches of at least this size as SCAN: it is faster at any
+// skew (one set per thread, no set-lock handoffs; 0.48 vs 0.97 ms per 2^20
+// GET/SET 90/10, profiles/r01_configs_probe.json), while tiny batches do not
+// amortize its sort.
+constexpr uint64_t kCacheScanMin = 1u << 13;
+
+int ensure_sched(hetm_dev* d, uint64_t n, int kernel_id = HETM_KERNEL_BANK) {
+    const size_t need = kernel_id == HETM_KERNEL_CACHE ? cache_sched_temp_bytes(n, d->cache.n_sets)
+                                                       : bank_sched_temp_bytes(n, d->W);
     if (need <= d->sched_bytes) return HETM_OK;
     if (d->d_sched) {
         CK(d, cudaDeviceSynchronize());
@@ -402,6 +409,12 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
         }();
         e = launch_bank_sched(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr, d->d_sched,
                               d->sched_bytes, d->geom, s, use_graph ? &d->sched_graph : nullptr);
+    } else if (kernel_id == HETM_KERNEL_CACHE &&
+               (v.serial || d->schedule == HETM_SCHED_SCAN || (d->schedule == HETM_SCHED_AUTO && n >= kCacheScanMin))) {
+        if (int rc = ensure_sched(d, n, kernel_id)) return rc;
+        e = launch_cache_sched(v, d->cache, static_cast<const hetm_cache_tx*>(d_inputs), n, d_tickets,
+                               static_cast<hetm_cache_result*>(d_results), d->d_ctr, d->d_sched, d->sched_bytes,
+                               d->geom, s);
     } else if (kernel_id == HETM_KERNEL_BANK)
         e = launch_bank_batch(v, static_cast<const hetm_bank_tx*>(d_inputs), n, d_tickets, d->d_ctr,
                               d->max_attempts, d->geom, s);

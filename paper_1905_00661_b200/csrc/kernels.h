@@ -110,6 +110,12 @@ struct SchedGraph {
 cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                               DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s,
                               SchedGraph* graph = nullptr);
+// SCAN schedule of a cache batch (cache_sched.cu): stable sort by set, one
+// thread per set runs its transactions in input order; no locks, no aborts.
+size_t cache_sched_temp_bytes(uint64_t n, uint64_t n_sets);
+cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const hetm_cache_tx* d_in, uint64_t n,
+                               unsigned long long* d_tickets, hetm_cache_result* d_res, DevCounters* ctr, void* temp,
+                               size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

@@ -656,14 +656,17 @@ def check_cache_replay(hetm, orc, d, txs, r, init, n_sets, gran=1024, chunk=1638
     return ref
 
 
+@pytest.mark.parametrize("sched", ["optimistic", "scan"])
 @pytest.mark.parametrize("gran", GRANS)
 @pytest.mark.parametrize("n_sets,n,alpha", [(64, 1 << 12, 0.5), (1024, 1 << 14, 0.5), (1 << 14, 1 << 16, 0.99)])
-def test_cache_batch_replays(hetm, orc, dev_factory, gran, n_sets, n, alpha):
+def test_cache_batch_replays(hetm, orc, dev_factory, gran, n_sets, n, alpha, sched):
     """GET/SET 90/10 (BASELINE configs[3]) after a warm-up SET batch: STMR,
-    per-transaction results and bitmaps equal the ticket-order replay."""
+    per-transaction results and bitmaps equal the ticket-order replay, for the
+    optimistic kernel and the set-sequential SCAN schedule (input order)."""
     W = n_sets * 64
     d = dev_factory(W, rs_gran_bytes=gran)
     d.register_kernel(hetm.KERNEL_CACHE)
+    d.set_schedule(hetm.SCHED_SCAN if sched == "scan" else hetm.SCHED_OPTIMISTIC)
     init = np.zeros(W, np.uint64)
     warm = orc.gen_cache_batch(1, n, n_sets * 4, alpha, get_permille=0, part=-1, steal_permille=500)
     r = d.execute_batch(hetm.KERNEL_CACHE, warm, results=True)
@@ -674,10 +677,13 @@ def test_cache_batch_replays(hetm, orc, dev_factory, gran, n_sets, n, alpha):
     check_cache_replay(hetm, orc, d, txs, r, ref, n_sets, gran)
     st = r.results["status"]
     assert (st == hetm.CACHE_HIT).any() and (st == hetm.CACHE_MISS).any()
+    if sched == "scan":
+        assert r.aborts == 0 and (r.tickets == r.ticket_first + np.arange(n, dtype=np.uint64)).all()
 
 
+@pytest.mark.parametrize("sched", ["optimistic", "scan"])
 @pytest.mark.parametrize("steal", [0, 1000])
-def test_cache_rounds_against_host(hetm, orc, dev_factory, steal):
+def test_cache_rounds_against_host(hetm, orc, dev_factory, steal, sched):
     """routing by the key's last bit -> no inter-device
     conflict (steal 0); the GPU taking the CPU's keys (steal 1000) conflicts
     and rolls back.  Replicas equal after every round."""
@@ -685,6 +691,7 @@ def test_cache_rounds_against_host(hetm, orc, dev_factory, steal):
     W = n_sets * 64
     d = dev_factory(W, rs_gran_bytes=1024, merge_delta=True)
     d.register_kernel(hetm.KERNEL_CACHE)
+    d.set_schedule(hetm.SCHED_SCAN if sched == "scan" else hetm.SCHED_OPTIMISTIC)
     host = np.zeros(W, np.uint64)
     outcomes = []
     ts = 0

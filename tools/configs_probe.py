@@ -77,10 +77,14 @@ d.register_kernel(hetm.KERNEL_CACHE)
 res = torch.empty(B * 40, dtype=torch.uint8, device="cuda")
 warm = torch.from_numpy(hetm.gen_cache_batch(1, B, 1 << 22, 0.5, get_permille=0, part=1).view(np.uint8)).cuda()
 timed_batches(d, hetm.KERNEL_CACHE, [warm], tickets, res, reps=0)
-for gp in [900, 999]:
-    bs = [torch.from_numpy(hetm.gen_cache_batch(10 + k, B, 1 << 22, 0.5, get_permille=gp, part=1).view(np.uint8)).cuda()
-          for k in range(2)]
-    ms, ab = timed_batches(d, hetm.KERNEL_CACHE, bs, tickets, res)
-    out[f"cfg4_cache_get{gp / 10:.1f}"] = {"batch_ms": ms, "tx_per_s": B / ms * 1e3, "aborts_per_batch": ab}
-    print(f"cfg4 cache GET {gp / 10:.1f}%: {ms:.3f} ms/batch, {B / ms / 1e6:.3f} G tx/s, aborts {ab}", flush=True)
+sched_names = {hetm.SCHED_AUTO: "", hetm.SCHED_OPTIMISTIC: "_optimistic", hetm.SCHED_SCAN: "_scan"}
+for sched in [hetm.SCHED_AUTO, hetm.SCHED_OPTIMISTIC, hetm.SCHED_SCAN]:
+    d.set_schedule(sched)
+    for gp in [900, 999]:
+        bs = [torch.from_numpy(hetm.gen_cache_batch(10 + k, B, 1 << 22, 0.5, get_permille=gp, part=1).view(np.uint8)).cuda()
+              for k in range(2)]
+        ms, ab = timed_batches(d, hetm.KERNEL_CACHE, bs, tickets, res)
+        key = f"cfg4_cache_get{gp / 10:.1f}{sched_names[sched]}"
+        out[key] = {"batch_ms": ms, "tx_per_s": B / ms * 1e3, "aborts_per_batch": ab}
+        print(f"{key}: {ms:.3f} ms/batch, {B / ms / 1e6:.3f} G tx/s, aborts {ab}", flush=True)
 print(json.dumps(out))
