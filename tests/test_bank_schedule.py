@@ -146,3 +146,36 @@ def test_auto_device_batches_follow_the_previous_estimate(hetm, orc, dev_factory
         orc.bank_replay(ref, orc.gen_bank_batch(90 + k, n, 0, W), orc.order_by_ticket(t), 1024, 16384)
     assert (d.download(hetm.REPLICA_DEV) == ref).all()
     assert not (np.diff(t.astype(np.int64)) == 1).all()  # back to optimistic on uniform input
+
+
+@pytest.mark.parametrize("W,n", [(1000, 1), (1000, 3), (12345, 777), (1 << 10, 0)])
+def test_scan_edge_sizes(hetm, orc, dev_factory, W, n):
+    """Non-power-of-two shards, single transactions and empty batches under SCAN."""
+    d = dev_factory(W, rs_gran_bytes=8)
+    d.register_kernel(hetm.KERNEL_BANK)
+    d.set_schedule(hetm.SCHED_SCAN)
+    init = np.arange(W, dtype=np.uint64) + np.uint64(5000)
+    d.upload(hetm.REPLICA_DEV, 0, init)
+    txs = orc.gen_bank_batch(W + n, n, 0, W) if n else np.zeros(0, orc.BANK_TX)
+    r = d.execute_batch(hetm.KERNEL_BANK, txs)
+    assert r.committed == n and r.aborts == 0
+    if n:
+        check_replay(hetm, orc, d, txs, r.tickets, init, 8, 16384)
+    else:
+        assert (d.download(hetm.REPLICA_DEV) == init).all() and d.bitmap_stats() == (0, 0, 0)
+
+
+@pytest.mark.parametrize("n", [(1 << 13) - 1, 1 << 13])
+def test_cache_auto_threshold_both_sides(hetm, orc, dev_factory, n):
+    """AUTO runs cache batches below 8192 optimistic and from 8192 as SCAN; both replay bit-exactly."""
+    from test_gpu_parity import check_cache_replay
+    n_sets = 1 << 10
+    W = n_sets * 64
+    d = dev_factory(W, rs_gran_bytes=1024)
+    d.register_kernel(hetm.KERNEL_CACHE)
+    init = np.zeros(W, np.uint64)
+    txs = orc.gen_cache_batch(3, n, n_sets * 4, 0.5, get_permille=500, part=-1, steal_permille=500)
+    r = d.execute_batch(hetm.KERNEL_CACHE, txs, results=True)
+    check_cache_replay(hetm, orc, d, txs, r, init, n_sets)
+    in_order = bool((r.tickets == r.ticket_first + np.arange(n, dtype=np.uint64)).all())
+    assert in_order == (n >= 1 << 13) or r.aborts == 0
