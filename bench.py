@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--gran", type=int, default=1024)
     p.add_argument("--l2-fetch32", action="store_true", help="cudaLimitMaxL2FetchGranularity = 32 B")
     p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--no-early-merge", dest="early_merge", action="store_false",
+                   help="e2e: merge only after the verdict (no hetm_dev_merge_prepare)")
     p.add_argument("--chunk-merge", action="store_true", help="SPEC chunk-copy merge instead of the delta merge")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -403,7 +405,14 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
         rc = lib.hetm_dev_execute_batch(dev.h, hetm.KERNEL_BANK, txs[j % 2].array.ctypes.data, 24, B,
                                         tickets.array.ctypes.data, C.byref(st))
         hetm.check(rc, dev.h)
-        dev.merge_wait()  # host transactions of this round see the merged replica
+        # execution phase over: stage this round's delta merge now and apply it to
+        # the host replica speculatively (undone on abort); this waits for the
+        # previous round's merge to have landed, so host transactions of this
+        # round saw the merged replica
+        if args.early_merge:
+            dev.merge_prepare(host_replica.array)
+        else:
+            dev.merge_wait()
         for c in range(8):  # the round's log streamed in 8 chunks (one per host thread)
             sl = lg[c * (L // 8):(c + 1) * (L // 8)]
             dev.stream_chunk(sl, src_thread=c, seq=c)
@@ -425,7 +434,10 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
         p.free()
     return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
-            "merge": "chunk copy (SPEC.md:363-371)" if args.chunk_merge else "delta (16-B {word,value} per device-written word)",
+            "merge": ("chunk copy (SPEC.md:363-371)" if args.chunk_merge else
+                      "delta (16-B {word,value} per device-written word)" +
+                      (", staged + speculatively applied right after the execution phase (hetm_dev_merge_prepare)"
+                       if args.early_merge else "")),
             "timing": "host wall clock around full rounds (pinned buffers; verdict + merge D2H landed in the host "
                       "replica before the next round's host log; the next GPU batch overlaps the merge, PAPER.md:355)"}
 

@@ -403,6 +403,19 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
 enum { HETM_SCHED_OPTIMISTIC = 0, HETM_SCHED_SCAN = 1, HETM_SCHED_AUTO = 2 };
 int hetm_dev_set_schedule(hetm_dev* dev, int mode);
 
+/* Early merge (PAPER.md:355 double buffering, pushed one phase earlier): the
+ * execution phase of the round is over (no executeBatch until its merge), so
+ * the device write set is sorted, gathered and copied to the host now —
+ * overlapping the log streaming and validation — instead of after the
+ * verdict.  With host_replica != NULL the worker pool also writes it into the
+ * host replica speculatively, each record keeping the value it replaced; the
+ * round's mergeCommit then only refreshes devShadow, while mergeAbortDevice /
+ * mergeAbortHost (or a new batch, or clearRound) first put the host replica
+ * back.  Between this call and the round's merge call no host transaction may
+ * touch host_replica (the host cut-off precedes validation).
+ * A no-op without HETM_CFG_MERGE_DELTA or when the write-set log overflowed. */
+int hetm_dev_merge_prepare(hetm_dev* dev, uint64_t* host_replica);
+
 /* ---------------------------------------------------- checker support -- *
  * Traces for the P1 / P2-dagger consistency checker (the
  * `checker` module).  Recording is toggleable and lossless:

@@ -446,6 +446,14 @@ class GpuDevice:
         self._trace_keep = out
         self._chk(lib.hetm_dev_trace_next_batch(self.h, out.ctypes.data))
 
+    def merge_prepare(self, host_replica: np.ndarray | None = None):
+        """Stage the round's delta merge right after the execution phase; with the host
+        replica also apply it speculatively (undone by an abort).  See capi.h."""
+        if host_replica is not None:
+            assert host_replica.dtype == np.uint64 and host_replica.flags["C_CONTIGUOUS"]
+            self._prep_keep = host_replica
+        self._chk(lib.hetm_dev_merge_prepare(self.h, host_replica.ctypes.data if host_replica is not None else None))
+
     def set_schedule(self, mode: int):
         """Bank batch schedule: SCHED_OPTIMISTIC | SCHED_SCAN | SCHED_AUTO (default)."""
         self._chk(lib.hetm_dev_set_schedule(self.h, mode))

@@ -107,6 +107,16 @@ private:
 };
 }  // namespace
 
+// Delta merge staged by hetm_dev_merge_prepare before the round's verdict.
+struct PreparedMerge {
+    bool active = false;
+    bool speculative = false;  // the records were swapped into `host` already
+    uint64_t n_slots = 0, k0 = 0, pieces = 0;
+    uint64_t round_tx = 0;     // the round's submitted transactions when staged
+    uint64_t* host = nullptr;
+    int buf = 0;               // delta buffer holding it
+};
+
 struct hetm_dev {
     hetm_dev_config cfg{};
     int device = 0;
@@ -135,10 +145,14 @@ struct hetm_dev {
     uint32_t* d_wsorted = nullptr;       // write-set log sorted by word (delta merge)
     void* d_sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
-    DeltaRec* d_delta = nullptr;         // merge delta (device) and its pinned host landing buffer
-    DeltaRec* h_delta = nullptr;
+    // merge delta (device) and its pinned host landing buffer, double-buffered:
+    // a round's delta is staged while the worker pool still scatters the
+    // previous round's (hetm_dev_merge_prepare)
+    DeltaRec* d_delta[2] = {nullptr, nullptr};
+    DeltaRec* h_delta[2] = {nullptr, nullptr};
     uint64_t delta_cap = 0;
-    std::vector<cudaEvent_t> piece_ev;   // per-piece D2H completion of the delta
+    std::vector<cudaEvent_t> piece_ev[2];  // per-piece D2H completion of each buffer
+    int dbuf = 0;                          // the buffer the next delta is staged into
     std::unique_ptr<WorkerPool> pool;    // host scatter of the delta into host_replica
     hetm_log_entry* d_arena = nullptr;   // this round's host log, in arrival order
     uint64_t arena_cap = 0, arena_n = 0;
@@ -176,6 +190,8 @@ struct hetm_dev {
     void* d_sched = nullptr;                // SCAN schedule scratch (bank_sched_temp_bytes)
     size_t sched_bytes = 0;
     SchedGraph sched_graph;                 // its captured launch sequence
+    PreparedMerge prep;                     // hetm_dev_merge_prepare state
+    cudaEvent_t ev_stage = nullptr;         // delta records gathered (s_merge)
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
@@ -381,9 +397,12 @@ int ensure_sched(hetm_dev* d, uint64_t n, int kernel_id = HETM_KERNEL_BANK) {
     return HETM_OK;
 }
 
+extern "C" void cancel_prepare(hetm_dev* d);  // defined with the merge code (C linkage block)
+
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
                   void* d_results, cudaStream_t s, bool reset_counters = true, unsigned long long* trace = nullptr,
                   bool hot = false) {
+    cancel_prepare(d);  // a new batch of the round: a staged merge would miss it
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
@@ -651,7 +670,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
 
     for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc, &d->s_in, &d->s_out})
         CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc})
+    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc, &d->ev_stage})
         CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CK(d, cudaEventCreate(&d->ev_t0));
     CK(d, cudaEventCreate(&d->ev_t1));
@@ -686,9 +705,15 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamSynchronize(s);
     d->pool.reset();
-    if (d->h_delta) cudaFreeHost(d->h_delta);
-    for (cudaEvent_t e : d->piece_ev) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b) {
+        if (d->h_delta[b]) cudaFreeHost(d->h_delta[b]);
+        for (cudaEvent_t e : d->piece_ev[b]) cudaEventDestroy(e);
+    }
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
+    if (d->prep.active) {  // never merged: leave the host replica as it was
+        std::lock_guard<std::mutex> g(d->mu);
+        cancel_prepare(d);
+    }
     if (d->sched_graph.exec) cudaGraphExecDestroy(d->sched_graph.exec);
     if (d->sched_graph.graph) cudaGraphDestroy(d->sched_graph.graph);
     if (d->sched_graph.cap) cudaStreamDestroy(d->sched_graph.cap);
@@ -699,7 +724,7 @@ int hetm_dev_close(hetm_dev* d) {
         cudaFreeHost(d->h_hot);
     }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0], (void*)d->d_delta[1], (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched})
         if (p) cudaFree(p);
@@ -713,7 +738,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1,
-                          d->ev_copy_zc})
+                          d->ev_copy_zc, d->ev_stage})
         if (e) cudaEventDestroy(e);
     delete d;
     return HETM_OK;
@@ -1102,23 +1127,41 @@ static_assert(kDeltaPiece % 8192 == 0, "host scatter blocks must not straddle pi
 // host replica ends identical to the chunk copy: the words outside the device
 // write set inside a dirty chunk already hold the host's values (the round
 // committed, so no host entry touched a device-read word).
-int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* bytes_d2h) {
-    if (d->pool) d->pool->wait();
+// Enqueue the delta of the round's device write set: radix sort of the
+// write-set log by word, gather of {word, value} records (refreshing devShadow
+// too when shadow != nullptr), an optional zero-copy head stored by the GPU
+// into the mapped host replica (zc_host), and the DMA of the rest in pieces,
+// each with a completion event.  Returns the first DMA'd piece and the count.
+int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_host, uint64_t* k0_out,
+                uint64_t* pieces_out, uint64_t* bytes_d2h, int* buf_out) {
     if (n_slots > d->delta_cap) {
+        if (d->pool) d->pool->wait();  // nothing may still read the old buffers
+        CK(d, cudaStreamSynchronize(d->s_merge));
         CK(d, cudaStreamSynchronize(d->s_d2h));
-        if (d->d_delta) { cudaFree(d->d_delta); d->bytes_alloc -= d->delta_cap * sizeof(DeltaRec); d->d_delta = nullptr; }
+        for (int b = 0; b < 2; ++b) {
+            if (d->d_delta[b]) { cudaFree(d->d_delta[b]); d->bytes_alloc -= d->delta_cap * sizeof(DeltaRec); d->d_delta[b] = nullptr; }
+            if (d->h_delta[b]) { cudaFreeHost(d->h_delta[b]); d->h_delta[b] = nullptr; }
+        }
         if (d->d_wsorted) { cudaFree(d->d_wsorted); d->bytes_alloc -= d->delta_cap * 4; d->d_wsorted = nullptr; }
         if (d->d_sort_tmp) { cudaFree(d->d_sort_tmp); d->bytes_alloc -= d->sort_tmp_bytes; d->d_sort_tmp = nullptr; }
-        if (d->h_delta) { cudaFreeHost(d->h_delta); d->h_delta = nullptr; }
         const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
-        if (int rc = dev_alloc(d, (void**)&d->d_delta, cap * sizeof(DeltaRec))) return rc;
+        for (int b = 0; b < 2; ++b) {
+            if (int rc = dev_alloc(d, (void**)&d->d_delta[b], cap * sizeof(DeltaRec))) return rc;
+            if (cudaHostAlloc((void**)&d->h_delta[b], cap * sizeof(DeltaRec), cudaHostAllocPortable) != cudaSuccess)
+                return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
+        }
         if (int rc = dev_alloc(d, (void**)&d->d_wsorted, cap * 4)) return rc;
         d->sort_tmp_bytes = wlog_sort_temp_bytes(cap, d->W);
         if (int rc = dev_alloc(d, &d->d_sort_tmp, d->sort_tmp_bytes)) return rc;
-        if (cudaHostAlloc((void**)&d->h_delta, cap * sizeof(DeltaRec), cudaHostAllocPortable) != cudaSuccess)
-            return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
         d->delta_cap = cap;
     }
+    // the other buffer may still feed the worker pool; this one's last job ended
+    // before the pool accepted that one
+    const int b = d->dbuf;
+    d->dbuf ^= 1;
+    DeltaRec* dd = d->d_delta[b];
+    DeltaRec* hd = d->h_delta[b];
+    std::vector<cudaEvent_t>& pev = d->piece_ev[b];
     if (!d->pool) {
         // this process's share of the usable cores (torchrun runs one process
         // per GPU: LOCAL_WORLD_SIZE), one core left to the controller thread
@@ -1136,63 +1179,50 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
         const unsigned n = want ? want : std::min(32u, share > 1 ? share - 1 : 1u);
         d->pool.reset(new WorkerPool((int)std::max(1u, n)));
     }
-    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));
-    // shadow: incremental when it held the round-start state, else a full copy
-    uint64_t* shadow_inc = (d->d_shadow && d->shadow_synced) ? d->d_shadow : nullptr;
-    if (d->d_shadow && !d->shadow_synced) {
-        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, nullptr, d->chunk_bits, d->chunk_shift, true,
-                                            d->geom, d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(full shadow)");
-        d->record(HETM_D2D, HETM_TAG_SHADOW, d->W * 8);
-        d->shadow_synced = true;
-    }
     cudaError_t e = launch_wlog_sort(d->d_wlog, d->d_wsorted, n_slots, d->W, d->d_sort_tmp, d->sort_tmp_bytes,
                                      d->s_merge);
     if (e != cudaSuccess) return fail(d, e, "wlog_sort");
-    e = launch_wlog_gather(d->d_delta, shadow_inc, d->d_cells, d->d_wsorted, n_slots, d->W, d->geom, d->s_merge);
+    e = launch_wlog_gather(dd, shadow, d->d_cells, d->d_wsorted, n_slots, d->W, d->geom, d->s_merge);
     if (e != cudaSuccess) return fail(d, e, "wlog_gather");
-    if (shadow_inc) {
-        e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom, d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
-        d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
-    }
-    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
-    CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_shadow, 0));
-    // Split: the first n_zc sorted records are stored into the host replica by
-    // the GPU itself (zero-copy PCIe writes, s_merge) while the copy engine and
-    // the host workers deliver the rest — two independent paths into host DRAM.
-    static const double zc_frac = [] {
-        const char* e = std::getenv("HETM_ZC_FRACTION");
-        // 0 since the host scatter prefetches: the zero-copy stores then only
-        // slow the next batch's input H2D (profiles/r01_e2e_timeline.txt)
-        return e ? std::atof(e) : 0.0;
-    }();
+    CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
+    CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_stage, 0));
     uint64_t n_zc = 0;
-    cudaPointerAttributes pa{};
-    if (zc_frac > 0 && cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
-        pa.devicePointer) {
-        n_zc = std::min<uint64_t>(n_slots, (uint64_t)(zc_frac * (double)n_slots)) / kDeltaPiece * kDeltaPiece;
-        if (n_zc) {
-            CK(d, cudaStreamWaitEvent(d->s_zc, d->ev_shadow, 0));
-            cudaError_t ez = launch_delta_zc_scatter(static_cast<uint64_t*>(pa.devicePointer), d->d_delta, n_zc,
-                                                     d->geom, d->s_zc);
-            if (ez != cudaSuccess) return fail(d, ez, "delta_zc_scatter");
-            d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, n_zc * 8);
+    if (zc_host) {
+        // Split: the first n_zc sorted records are stored into the host replica
+        // by the GPU itself (zero-copy PCIe writes, s_zc) while the copy engine
+        // and the host workers deliver the rest — two independent paths.
+        static const double zc_frac = [] {
+            const char* e = std::getenv("HETM_ZC_FRACTION");
+            // 0 since the host scatter prefetches: the zero-copy stores then only
+            // slow the next batch's input H2D (profiles/r01_e2e_timeline.txt)
+            return e ? std::atof(e) : 0.0;
+        }();
+        cudaPointerAttributes pa{};
+        if (zc_frac > 0 && cudaPointerGetAttributes(&pa, zc_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer) {
+            n_zc = std::min<uint64_t>(n_slots, (uint64_t)(zc_frac * (double)n_slots)) / kDeltaPiece * kDeltaPiece;
+            if (n_zc) {
+                CK(d, cudaStreamWaitEvent(d->s_zc, d->ev_stage, 0));
+                cudaError_t ez = launch_delta_zc_scatter(static_cast<uint64_t*>(pa.devicePointer), dd, n_zc,
+                                                         d->geom, d->s_zc);
+                if (ez != cudaSuccess) return fail(d, ez, "delta_zc_scatter");
+                d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, n_zc * 8);
+            }
+        } else {
+            cudaGetLastError();
         }
-    } else {
-        cudaGetLastError();
     }
     const uint64_t pieces = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
-    while (d->piece_ev.size() < pieces) {
+    while (pev.size() < pieces) {
         cudaEvent_t ev = nullptr;
         CK(d, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        d->piece_ev.push_back(ev);
+        pev.push_back(ev);
     }
     const uint64_t k0 = n_zc / kDeltaPiece;  // pieces already delivered by the zero-copy kernel
     for (uint64_t k = k0; k < pieces; ++k) {
         const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
-        CK(d, cudaMemcpyAsync(d->h_delta + lo, d->d_delta + lo, m * sizeof(DeltaRec), cudaMemcpyDeviceToHost, d->s_d2h));
-        CK(d, cudaEventRecord(d->piece_ev[k], d->s_d2h));
+        CK(d, cudaMemcpyAsync(hd + lo, dd + lo, m * sizeof(DeltaRec), cudaMemcpyDeviceToHost, d->s_d2h));
+        CK(d, cudaEventRecord(pev[k], d->s_d2h));
     }
     d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_slots - n_zc) * sizeof(DeltaRec));
     *bytes_d2h = n_zc * 8 + (n_slots - n_zc) * sizeof(DeltaRec);
@@ -1202,8 +1232,22 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
     }
     CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
     d->d2h_pending = true;
-    const DeltaRec* src = d->h_delta;
-    const std::vector<cudaEvent_t> evs(d->piece_ev.begin(), d->piece_ev.begin() + pieces);
+    *k0_out = k0;
+    *pieces_out = pieces;
+    *buf_out = b;
+    return HETM_OK;
+}
+
+// Host side of the delta: the worker pool writes the records into the host
+// replica as each DMA piece lands.  PLAIN stores them; SWAP (speculative, before
+// the round's verdict) stores them and keeps the replaced value in the record,
+// so UNDO can put the replica back (records are unique per word).
+enum ScatterMode { kScatterPlain, kScatterSwap, kScatterUndo };
+
+void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_slots, uint64_t k0, uint64_t pieces,
+                   ScatterMode mode) {
+    DeltaRec* src = d->h_delta[buf];
+    const std::vector<cudaEvent_t> evs(d->piece_ev[buf].begin(), d->piece_ev[buf].begin() + pieces);
     const int dev = d->device;
     // Dynamic blocks in sorted order: a worker that the OS deschedules delays
     // only the block it holds, not a static 1/nw share of every piece.  Piece
@@ -1216,8 +1260,8 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
     };
     auto st = std::make_shared<ScatterState>();
     st->cursor = k0 * kDeltaPiece;
-    st->landed = k0;
-    d->pool->start([src, evs, host, n_slots, dev, st](int, int) {
+    st->landed = mode == kScatterUndo ? pieces : k0;  // undo runs on records already in place
+    d->pool->start([src, evs, host, n_slots, dev, st, mode](int, int) {
         cudaSetDevice(dev);
         constexpr uint64_t kBlock = 8192;   // records per claim (divides kDeltaPiece)
         constexpr uint64_t kPrefetch = 64;  // prefetch-for-write distance, see below
@@ -1227,8 +1271,14 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
             const uint64_t b = std::min(a + kBlock, n_slots), k = a / kDeltaPiece;
             while (st->landed.load(std::memory_order_acquire) <= k) {
                 if (st->waiter.try_lock()) {  // the others spin on `landed`, not in the driver
+                    // block on the next missing piece: a tight cudaEventQuery loop
+                    // would contend with the controller thread's CUDA calls
                     uint64_t l = st->landed.load(std::memory_order_relaxed);
-                    while (l <= k && cudaEventQuery(evs[l]) == cudaSuccess) ++l;
+                    if (l <= k) {
+                        cudaEventSynchronize(evs[l]);
+                        ++l;
+                        while (l <= k && cudaEventQuery(evs[l]) == cudaSuccess) ++l;
+                    }
                     st->landed.store(l, std::memory_order_release);
                     st->waiter.unlock();
                 }
@@ -1240,10 +1290,94 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
             for (uint64_t i = a; i < b; ++i) {
                 if (i + kPrefetch < b && src[i + kPrefetch].loc != ~0ull)
                     __builtin_prefetch(&host[src[i + kPrefetch].loc], 1, 0);
-                if (src[i].loc != ~0ull) host[src[i].loc] = src[i].value;
+                const uint64_t loc = src[i].loc;
+                if (loc == ~0ull) continue;
+                if (mode == kScatterSwap) {
+                    const uint64_t old = host[loc];
+                    host[loc] = src[i].value;
+                    src[i].value = old;
+                } else {
+                    host[loc] = src[i].value;
+                }
             }
         }
     });
+}
+
+// A prepared merge that will not be committed (a conflict, a new batch, a
+// clear): wait for its host side and undo a speculative scatter.
+void cancel_prepare(hetm_dev* d) {
+    if (!d->prep.active) return;
+    d->pool->wait();
+    if (d->prep.speculative) {
+        start_scatter(d, d->prep.buf, d->prep.host, d->prep.n_slots, d->prep.k0, d->prep.pieces, kScatterUndo);
+        d->pool->wait();
+    }
+    d->prep = PreparedMerge{};
+}
+
+// Delta mergeCommit: the batch kernels logged the word index of every
+// committed write into the slot of its commit ticket; the log is sorted and
+// gathered into {word, value} records (devShadow refreshed with them), DMA'd
+// in 2 MiB pieces and scattered into host_replica by the worker pool as each
+// piece lands.  The host replica ends identical to the chunk copy: the words
+// outside the device write set inside a dirty chunk already hold the host's
+// values (the round committed, so no host entry touched a device-read word).
+// After hetm_dev_merge_prepare the records are already staged (and, when it
+// got the host replica, already in it): only the shadow is refreshed here.
+int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* bytes_d2h) {
+    const bool prepared = d->prep.active && d->prep.round_tx == d->round_tx && d->prep.n_slots == n_slots;
+    if (!prepared && d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));  // the previous delta
+    // shadow: incremental when it held the round-start state, else a full copy
+    uint64_t* shadow_inc = (d->d_shadow && d->shadow_synced) ? d->d_shadow : nullptr;
+    if (d->d_shadow && !d->shadow_synced) {
+        cudaError_t e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, nullptr, d->chunk_bits, d->chunk_shift, true,
+                                            d->geom, d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "dirty_chunks(full shadow)");
+        d->record(HETM_D2D, HETM_TAG_SHADOW, d->W * 8);
+        d->shadow_synced = true;
+    }
+    if (prepared) {
+        const PreparedMerge p = d->prep;
+        d->prep = PreparedMerge{};
+        if (shadow_inc) {
+            cudaError_t e = launch_delta_to_shadow(shadow_inc, d->d_delta[p.buf], n_slots, d->geom, d->s_merge);
+            if (e == cudaSuccess)
+                e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
+                                        d->s_merge);
+            if (e != cudaSuccess) return fail(d, e, "shadow(prepared merge)");
+            d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
+        }
+        CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+        if (!p.speculative || p.host != host) {
+            if (p.speculative) {  // prepared for another replica: put that one back first
+                d->pool->wait();
+                start_scatter(d, p.buf, p.host, p.n_slots, p.k0, p.pieces, kScatterUndo);
+                d->pool->wait();
+                for (uint64_t k = 0; k < p.pieces; ++k) {  // the records hold old values now: restage
+                    const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
+                    CK(d, cudaMemcpyAsync(d->h_delta[p.buf] + lo, d->d_delta[p.buf] + lo, m * sizeof(DeltaRec),
+                                          cudaMemcpyDeviceToHost, d->s_d2h));
+                    CK(d, cudaEventRecord(d->piece_ev[p.buf][k], d->s_d2h));
+                }
+            }
+            start_scatter(d, p.buf, host, n_slots, p.k0, p.pieces, kScatterPlain);
+        }
+        *bytes_d2h = n_slots * sizeof(DeltaRec);
+        return HETM_OK;
+    }
+    cancel_prepare(d);
+    uint64_t k0 = 0, pieces = 0;
+    int buf = 0;
+    if (int rc = stage_delta(d, n_slots, shadow_inc, host, &k0, &pieces, bytes_d2h, &buf)) return rc;
+    if (shadow_inc) {
+        cudaError_t e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
+                                            d->s_merge);
+        if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
+        d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
+    }
+    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+    start_scatter(d, buf, host, n_slots, k0, pieces, kScatterPlain);
     return HETM_OK;
 }
 }  // namespace
@@ -1314,11 +1448,43 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     return HETM_OK;
 }
 
+int hetm_dev_merge_prepare(hetm_dev* d, uint64_t* host) {
+    NvtxRange nvtx_range("hetm.mergePrepare");
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    cancel_prepare(d);
+    if (!(d->cfg.flags & HETM_CFG_MERGE_DELTA) || !d->d_wlog) return HETM_OK;  // chunk merge: nothing to stage
+    CK(d, cudaStreamSynchronize(d->s_exec));  // the execution phase is over
+    int rc = read_counters(d);
+    if (rc) return rc;
+    const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
+    if (d->h_ctr->wlog_overflow || n_slots == 0 || n_slots > d->wlog_slots) return HETM_OK;
+    // staged into the other delta buffer while the pool may still scatter the
+    // previous round's; starting this round's job below waits for that one, so
+    // host transactions after this call see the previous merge landed
+    CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_exec, 0));
+    uint64_t k0 = 0, pieces = 0, moved = 0;
+    int buf = 0;
+    if ((rc = stage_delta(d, n_slots, nullptr, nullptr, &k0, &pieces, &moved, &buf))) return rc;
+    d->prep.active = true;
+    d->prep.speculative = host != nullptr;
+    d->prep.n_slots = n_slots;
+    d->prep.k0 = k0;
+    d->prep.pieces = pieces;
+    d->prep.round_tx = d->round_tx;
+    d->prep.host = host;
+    d->prep.buf = buf;
+    if (host) start_scatter(d, buf, host, n_slots, k0, pieces, kScatterSwap);
+    else if (d->pool) d->pool->wait();  // still: the previous merge has landed when this returns
+    return HETM_OK;
+}
+
 int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host, hetm_merge_stats* st) {
     NvtxRange nvtx_range("hetm.mergeAbortDevice");
     if (!d || (!host && !optimized)) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> g(d->mu);
+    cancel_prepare(d);  // undo a speculative delta first: the device side of the round is void
     d->intake_open = false;
     int rc = enqueue_deferred_apply(d);  // FavorHost: the host log always lands on the device
     if (rc) return rc;
@@ -1386,6 +1552,7 @@ int hetm_dev_merge_abort_host(hetm_dev* d, uint64_t* host, const uint64_t* snaps
     if (!d || !host || !snapshot) return HETM_ERR_INVALID_ARG;
     auto t0 = std::chrono::steady_clock::now();
     std::lock_guard<std::mutex> g(d->mu);
+    cancel_prepare(d);
     d->intake_open = false;
     if (d->round_applied) return HETM_ERR_STATE;  // FavorDevice validation is validate-only
     int rc = wait_round_work(d, d->s_merge);
@@ -1445,6 +1612,7 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     NvtxRange nvtx_range("hetm.clearRound");
     if (!d) return HETM_ERR_INVALID_ARG;
     std::lock_guard<std::mutex> g(d->mu);
+    cancel_prepare(d);  // staged but never merged: not part of the replica
     int rc = wait_round_work(d, d->s_merge);
     if (rc) return rc;
     if (flags & HETM_CLEAR_ASYNC) {

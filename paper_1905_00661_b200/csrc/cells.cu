@@ -49,13 +49,21 @@ __global__ void wlog_gather_kernel(DeltaRec* __restrict__ out, uint64_t* __restr
                                    uint64_t size_words) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t loc = wlog[i];
-        if (loc < size_words) {
+        if (loc < size_words && (i == 0 || wlog[i - 1] != loc)) {  // one record per word (the log is sorted)
             const uint64_t val = cells[loc].value;
             out[i] = DeltaRec{loc, val};
             if (shadow) shadow[loc] = val;
         } else {
             out[i] = DeltaRec{~0ull, 0};
         }
+    }
+}
+
+// devShadow refresh from staged delta records (a prepared merge).
+__global__ void delta_to_shadow_kernel(uint64_t* __restrict__ shadow, const DeltaRec* __restrict__ d, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const DeltaRec r = d[i];
+        if (r.loc != ~0ull) shadow[r.loc] = r.value;
     }
 }
 
@@ -102,6 +110,12 @@ cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cell
                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     wlog_gather_kernel<<<grid_words(n, g), 256, 0, s>>>(out, shadow, cells, wlog, n, size_words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_delta_to_shadow(uint64_t* shadow, const DeltaRec* d, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    delta_to_shadow_kernel<<<grid_words(n, g), 256, 0, s>>>(shadow, d, n);
     return cudaGetLastError();
 }
 

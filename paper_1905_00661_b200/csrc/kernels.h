@@ -116,6 +116,8 @@ size_t cache_sched_temp_bytes(uint64_t n, uint64_t n_sets);
 cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const hetm_cache_tx* d_in, uint64_t n,
                                unsigned long long* d_tickets, hetm_cache_result* d_res, DevCounters* ctr, void* temp,
                                size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
+// devShadow[loc] = value for staged delta records (prepared merge).
+cudaError_t launch_delta_to_shadow(uint64_t* shadow, const DeltaRec* d, uint64_t n, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

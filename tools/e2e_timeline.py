@@ -24,6 +24,7 @@ import paper_1905_00661_b200 as hetm
 
 W, B, L = 1 << 27, 1 << 20, 1 << 20
 out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else "gpurun_out/e2e_trace.json"
+EARLY = "--early" in sys.argv
 dev = hetm.GpuDevice(W, rs_gran_bytes=1024, log_capacity=L, merge_delta=True)
 dev.register_kernel(hetm.KERNEL_BANK)
 init = np.full(W, 1000, np.uint64)
@@ -49,8 +50,12 @@ def round_(j):
     with record_function("H execute_batch"):
         hetm.check(lib.hetm_dev_execute_batch(dev.h, hetm.KERNEL_BANK, txs[j % 2].array.ctypes.data, 24, B,
                                               tickets.array.ctypes.data, C.byref(st)), dev.h)
-    with record_function("H merge_wait"):
-        dev.merge_wait()
+    if EARLY:
+        with record_function("H merge_prepare"):
+            dev.merge_prepare(host.array)
+    else:
+        with record_function("H merge_wait"):
+            dev.merge_wait()
     lg = logs[j].array
     with record_function("H stream_chunks"):
         for c in range(8):
