@@ -389,7 +389,7 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
  * of the transfers' deltas; its cost does not grow with skew, while the
  * optimistic kernel serializes every commit on a hot account.  AUTO (default):
  * host-buffer batches take SCAN when a sample of the inputs predicts a chain
- * of >= 1024 conflicting commits on one account (HETM_SCHED_CHAIN); device-
+ * of >= 768 conflicting commits on one account (HETM_SCHED_CHAIN); device-
  * pointer batches follow the same estimate of an EARLIER device batch of the
  * handle (a one-CTA kernel samples each batch on a side stream into mapped
  * host memory, read by the next call without a sync), so a steady hot

@@ -343,14 +343,15 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
 
 // Enqueue one batch kernel on `s` (inputs and tickets are device pointers).
 // Hot-spot estimate of a host-resident bank batch (HETM_SCHED_AUTO): the
-// access count of the hottest account among S sampled transactions, scaled to
-// the batch, estimates the longest chain of conflicting commits the
+// access count of the hottest account among 4096 sampled transactions, scaled
+// to the batch, estimates the longest chain of conflicting commits the
 // optimistic kernel would serialize (~1.4 us per link on B200,
-// profiles/r01_sched_crossover.txt); above kSchedChain the SCAN schedule wins.
+// profiles/r01_sched_crossover.txt); from 768 (HETM_SCHED_CHAIN) the SCAN
+// schedule wins.
 uint64_t sched_chain() {
     static const uint64_t chain = [] {
         const char* e = std::getenv("HETM_SCHED_CHAIN");
-        return e ? std::strtoull(e, nullptr, 10) : 1024ull;
+        return e ? std::strtoull(e, nullptr, 10) : 768ull;
     }();
     return chain;
 }
@@ -360,18 +361,35 @@ bool hot_chain(uint64_t best, uint64_t n, uint64_t S, uint64_t chain) { return b
 
 bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
     const uint64_t chain = sched_chain();
-    constexpr uint64_t kS = 4096, kSlots = 1 << 15;
+    constexpr uint64_t kBlocks = 32, kPerBlock = 128, kSlots = 1 << 15;
     if (n * 4 < chain) return false;
-    const uint64_t S = std::min(n, kS), stride = n / S;
-    std::vector<uint32_t> key(kSlots, ~0u), cnt(kSlots, 0);
+    // 32 evenly spaced blocks of 128 consecutive transactions: the reads stream
+    // (the worker pool may be saturating host DRAM with the previous merge —
+    // 4096 scattered cache misses cost ~0.4 ms then, 32 cost nothing); the
+    // per-thread table is reused across batches (a generation tag replaces the clear)
+    const uint64_t per = std::min<uint64_t>(kPerBlock, n / kBlocks ? n / kBlocks : 1);
+    const uint64_t nb = n < kBlocks ? n : kBlocks, S = nb * per;
+    thread_local std::vector<uint32_t> key(kSlots), cnt(kSlots), tag(kSlots);
+    thread_local uint32_t gen = 0;
+    if (++gen == 0) {
+        std::fill(tag.begin(), tag.end(), 0u);
+        gen = 1;
+    }
     uint32_t best = 0;
-    for (uint64_t q = 0; q < S; ++q)
-        for (uint32_t a : in[q * stride].acct) {
-            uint64_t h = (a * 0x9e3779b97f4a7c15ull) >> 49;  // 15 bits
-            while (key[h] != ~0u && key[h] != a) h = (h + 1) & (kSlots - 1);
-            key[h] = a;
-            best = std::max(best, ++cnt[h]);
-        }
+    for (uint64_t blk = 0; blk < nb; ++blk) {
+        const hetm_bank_tx* b = in + blk * (n / nb);
+        for (uint64_t q = 0; q < per; ++q)
+            for (uint32_t a : b[q].acct) {
+                uint64_t h = (a * 0x9e3779b97f4a7c15ull) >> 49;  // 15 bits
+                while (tag[h] == gen && key[h] != a) h = (h + 1) & (kSlots - 1);
+                if (tag[h] != gen) {
+                    tag[h] = gen;
+                    key[h] = a;
+                    cnt[h] = 0;
+                }
+                best = std::max(best, ++cnt[h]);
+            }
+    }
     return hot_chain(best, n, S, chain);
 }
 

@@ -27,6 +27,8 @@ out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else "gpurun_
 EARLY = "--early" in sys.argv
 dev = hetm.GpuDevice(W, rs_gran_bytes=1024, log_capacity=L, merge_delta=True)
 dev.register_kernel(hetm.KERNEL_BANK)
+if "--optimistic" in sys.argv:
+    dev.set_schedule(hetm.SCHED_OPTIMISTIC)
 init = np.full(W, 1000, np.uint64)
 dev.upload(hetm.REPLICA_DEV, 0, init)
 host = hetm.PinnedArray((W,), np.uint64)

@@ -24,11 +24,11 @@ d.upload(hetm.REPLICA_DEV, 0, np.full(W, 1000, np.uint64))
 tickets = torch.empty(n, dtype=torch.int64, device="cuda")
 
 
-def est_chain(txs):
-    S = min(n, 4096)
-    acc = txs["acct"][:: n // S][:S].reshape(-1)
+def est_chain(txs):  # capi.cu bank_batch_hot: 32 evenly spaced blocks of 128 transactions
+    per = min(128, n // 32)
+    acc = np.concatenate([txs["acct"][b * (n // 32): b * (n // 32) + per] for b in range(32)]).reshape(-1)
     _, c = np.unique(acc, return_counts=True)
-    return int(c.max()) * n // S
+    return int(c.max()) * n // (32 * per)
 
 
 def timed(sched, batch, reps):
@@ -54,6 +54,6 @@ for alpha in [0.0, 0.5, 0.6, 0.7, 0.75, 0.8, 0.9, 0.99]:
     scan_ms, _ = timed(hetm.SCHED_SCAN, b, 3)
     opt_ms, ab = timed(hetm.SCHED_OPTIMISTIC, b, 1 if alpha >= 0.8 else 3)
     row = {"alpha": alpha, "n": n, "est_chain": est_chain(txs), "optimistic_ms": opt_ms, "optimistic_aborts": ab,
-           "scan_ms": scan_ms, "scan_tx_per_s": n / scan_ms * 1e3, "auto_picks_scan": est_chain(txs) >= 1024}
+           "scan_ms": scan_ms, "scan_tx_per_s": n / scan_ms * 1e3, "auto_picks_scan": est_chain(txs) >= 768}
     out.append(row)
     print(json.dumps(row), flush=True)
