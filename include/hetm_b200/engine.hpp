@@ -53,6 +53,8 @@ struct EngineConfig {
     bool early_validation = true;       // stream chunks VALIDATE_ONLY during execution
     bool optimized_abort = true;        // mergeAbortDevice: shadow + log (true) or chunk copy (false)
     bool keep_round_log = false;        // keep a copy of the last round's host log (checkers)
+    bool early_merge = true;            // stage + speculatively apply the delta merge after execution
+                                        // (hetm_dev_merge_prepare; a no-op without HETM_CFG_MERGE_DELTA)
     uint32_t fault = 0;                 // ENGINE_FAULT_* (checker mutation suite only)
 };
 
@@ -285,6 +287,10 @@ public:
         gpu.join();
         check_rc(gpu_rc, "executeBatch");
         for (uint64_t c : commits) rep.host_commits += c;
+        // the host is cut off and the device batches are done: the device write
+        // set can travel to the host replica now, under the validation phase
+        // (undone by the abort paths if the round does not commit)
+        if (cfg_.early_merge) check_rc(hetm_dev_merge_prepare(dev_, host_), "merge_prepare");
         const auto t1 = std::chrono::steady_clock::now();
         // ---- VALIDATION: the log tail (APPLY, or validate-only under FavorDevice),
         // early chunks re-validated + applied (FavorDevice: only on success)
