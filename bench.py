@@ -435,7 +435,7 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
     return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
             "merge": ("chunk copy (SPEC.md:363-371)" if args.chunk_merge else
-                      "delta (16-B {word,value} per device-written word)" +
+                      "delta (12-B {word,value} per device-written word)" +
                       (", staged + speculatively applied right after the execution phase (hetm_dev_merge_prepare)"
                        if args.early_merge else "")),
             "timing": "host wall clock around full rounds (pinned buffers; verdict + merge D2H landed in the host "

@@ -148,8 +148,8 @@ struct hetm_dev {
     // merge delta (device) and its pinned host landing buffer, double-buffered:
     // a round's delta is staged while the worker pool still scatters the
     // previous round's (hetm_dev_merge_prepare)
-    DeltaRec* d_delta[2] = {nullptr, nullptr};
-    DeltaRec* h_delta[2] = {nullptr, nullptr};
+    DeltaBuf d_delta[2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    DeltaBuf h_delta[2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     uint64_t delta_cap = 0;
     std::vector<cudaEvent_t> piece_ev[2];  // per-piece D2H completion of each buffer
     int dbuf = 0;                          // the buffer the next delta is staged into
@@ -724,7 +724,8 @@ int hetm_dev_close(hetm_dev* d) {
         if (s) cudaStreamSynchronize(s);
     d->pool.reset();
     for (int b = 0; b < 2; ++b) {
-        if (d->h_delta[b]) cudaFreeHost(d->h_delta[b]);
+        if (d->h_delta[b].loc) cudaFreeHost(d->h_delta[b].loc);
+        if (d->h_delta[b].val) cudaFreeHost(d->h_delta[b].val);
         for (cudaEvent_t e : d->piece_ev[b]) cudaEventDestroy(e);
     }
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
@@ -742,7 +743,7 @@ int hetm_dev_close(hetm_dev* d) {
         cudaFreeHost(d->h_hot);
     }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0], (void*)d->d_delta[1], (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched})
         if (p) cudaFree(p);
@@ -1157,15 +1158,19 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
         CK(d, cudaStreamSynchronize(d->s_merge));
         CK(d, cudaStreamSynchronize(d->s_d2h));
         for (int b = 0; b < 2; ++b) {
-            if (d->d_delta[b]) { cudaFree(d->d_delta[b]); d->bytes_alloc -= d->delta_cap * sizeof(DeltaRec); d->d_delta[b] = nullptr; }
-            if (d->h_delta[b]) { cudaFreeHost(d->h_delta[b]); d->h_delta[b] = nullptr; }
+            if (d->d_delta[b].loc) { cudaFree(d->d_delta[b].loc); cudaFree(d->d_delta[b].val); d->bytes_alloc -= d->delta_cap * 12; }
+            if (d->h_delta[b].loc) { cudaFreeHost(d->h_delta[b].loc); cudaFreeHost(d->h_delta[b].val); }
+            d->d_delta[b] = DeltaBuf{nullptr, nullptr};
+            d->h_delta[b] = DeltaBuf{nullptr, nullptr};
         }
         if (d->d_wsorted) { cudaFree(d->d_wsorted); d->bytes_alloc -= d->delta_cap * 4; d->d_wsorted = nullptr; }
         if (d->d_sort_tmp) { cudaFree(d->d_sort_tmp); d->bytes_alloc -= d->sort_tmp_bytes; d->d_sort_tmp = nullptr; }
         const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
         for (int b = 0; b < 2; ++b) {
-            if (int rc = dev_alloc(d, (void**)&d->d_delta[b], cap * sizeof(DeltaRec))) return rc;
-            if (cudaHostAlloc((void**)&d->h_delta[b], cap * sizeof(DeltaRec), cudaHostAllocPortable) != cudaSuccess)
+            if (int rc = dev_alloc(d, (void**)&d->d_delta[b].loc, cap * 4)) return rc;
+            if (int rc = dev_alloc(d, (void**)&d->d_delta[b].val, cap * 8)) return rc;
+            if (cudaHostAlloc((void**)&d->h_delta[b].loc, cap * 4, cudaHostAllocPortable) != cudaSuccess ||
+                cudaHostAlloc((void**)&d->h_delta[b].val, cap * 8, cudaHostAllocPortable) != cudaSuccess)
                 return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
         }
         if (int rc = dev_alloc(d, (void**)&d->d_wsorted, cap * 4)) return rc;
@@ -1177,8 +1182,8 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
     // before the pool accepted that one
     const int b = d->dbuf;
     d->dbuf ^= 1;
-    DeltaRec* dd = d->d_delta[b];
-    DeltaRec* hd = d->h_delta[b];
+    const DeltaBuf dd = d->d_delta[b];
+    const DeltaBuf hd = d->h_delta[b];
     std::vector<cudaEvent_t>& pev = d->piece_ev[b];
     if (!d->pool) {
         // this process's share of the usable cores (torchrun runs one process
@@ -1239,11 +1244,12 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
     const uint64_t k0 = n_zc / kDeltaPiece;  // pieces already delivered by the zero-copy kernel
     for (uint64_t k = k0; k < pieces; ++k) {
         const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
-        CK(d, cudaMemcpyAsync(hd + lo, dd + lo, m * sizeof(DeltaRec), cudaMemcpyDeviceToHost, d->s_d2h));
+        CK(d, cudaMemcpyAsync(hd.loc + lo, dd.loc + lo, m * 4, cudaMemcpyDeviceToHost, d->s_d2h));
+        CK(d, cudaMemcpyAsync(hd.val + lo, dd.val + lo, m * 8, cudaMemcpyDeviceToHost, d->s_d2h));
         CK(d, cudaEventRecord(pev[k], d->s_d2h));
     }
-    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_slots - n_zc) * sizeof(DeltaRec));
-    *bytes_d2h = n_zc * 8 + (n_slots - n_zc) * sizeof(DeltaRec);
+    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_slots - n_zc) * 12);
+    *bytes_d2h = n_zc * 8 + (n_slots - n_zc) * 12;
     if (n_zc) {  // the merge is complete when both paths are
         CK(d, cudaEventRecord(d->ev_copy_zc, d->s_zc));
         CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_copy_zc, 0));
@@ -1264,7 +1270,7 @@ enum ScatterMode { kScatterPlain, kScatterSwap, kScatterUndo };
 
 void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_slots, uint64_t k0, uint64_t pieces,
                    ScatterMode mode) {
-    DeltaRec* src = d->h_delta[buf];
+    const DeltaBuf src = d->h_delta[buf];
     const std::vector<cudaEvent_t> evs(d->piece_ev[buf].begin(), d->piece_ev[buf].begin() + pieces);
     const int dev = d->device;
     // Dynamic blocks in sorted order: a worker that the OS deschedules delays
@@ -1306,16 +1312,16 @@ void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_slots, uint6
             // misses serialise (3.3 vs 1.8 G words/s on the box's 16 cores,
             // profiles/r01_host_scatter_probe.txt)
             for (uint64_t i = a; i < b; ++i) {
-                if (i + kPrefetch < b && src[i + kPrefetch].loc != ~0ull)
-                    __builtin_prefetch(&host[src[i + kPrefetch].loc], 1, 0);
-                const uint64_t loc = src[i].loc;
-                if (loc == ~0ull) continue;
+                if (i + kPrefetch < b && src.loc[i + kPrefetch] != ~0u)
+                    __builtin_prefetch(&host[src.loc[i + kPrefetch]], 1, 0);
+                const uint32_t loc = src.loc[i];
+                if (loc == ~0u) continue;
                 if (mode == kScatterSwap) {
                     const uint64_t old = host[loc];
-                    host[loc] = src[i].value;
-                    src[i].value = old;
+                    host[loc] = src.val[i];
+                    src.val[i] = old;
                 } else {
-                    host[loc] = src[i].value;
+                    host[loc] = src.val[i];
                 }
             }
         }
@@ -1374,14 +1380,14 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
                 d->pool->wait();
                 for (uint64_t k = 0; k < p.pieces; ++k) {  // the records hold old values now: restage
                     const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
-                    CK(d, cudaMemcpyAsync(d->h_delta[p.buf] + lo, d->d_delta[p.buf] + lo, m * sizeof(DeltaRec),
+                    CK(d, cudaMemcpyAsync(d->h_delta[p.buf].val + lo, d->d_delta[p.buf].val + lo, m * 8,
                                           cudaMemcpyDeviceToHost, d->s_d2h));
                     CK(d, cudaEventRecord(d->piece_ev[p.buf][k], d->s_d2h));
                 }
             }
             start_scatter(d, p.buf, host, n_slots, p.k0, p.pieces, kScatterPlain);
         }
-        *bytes_d2h = n_slots * sizeof(DeltaRec);
+        *bytes_d2h = n_slots * 12;
         return HETM_OK;
     }
     cancel_prepare(d);
@@ -1421,7 +1427,7 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     // delta form when enabled, the write-set log is complete and it moves fewer bytes
     const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
     const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && !d->h_ctr->wlog_overflow &&
-                       n_slots <= d->wlog_slots && n_slots * sizeof(DeltaRec) < dirty_bytes;
+                       n_slots <= d->wlog_slots && n_slots * 12 < dirty_bytes;
     if (delta) {
         uint64_t moved = 0;
         if ((rc = merge_commit_delta(d, host, n_slots, &moved))) return rc;

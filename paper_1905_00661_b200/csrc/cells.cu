@@ -44,26 +44,28 @@ __global__ void dirty_chunks_kernel(uint64_t* __restrict__ plain, Cell* __restri
 // mergeCommit delta: out[i] = {word, devReplica value} for every write-set
 // log slot (duplicates carry the same final value; empty slots -> ~0 word),
 // and the same value into devShadow (the incremental shadow refresh).
-__global__ void wlog_gather_kernel(DeltaRec* __restrict__ out, uint64_t* __restrict__ shadow,
+__global__ void wlog_gather_kernel(DeltaBuf out, uint64_t* __restrict__ shadow,
                                    const Cell* __restrict__ cells, const uint32_t* __restrict__ wlog, uint64_t n,
                                    uint64_t size_words) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t loc = wlog[i];
         if (loc < size_words && (i == 0 || wlog[i - 1] != loc)) {  // one record per word (the log is sorted)
             const uint64_t val = cells[loc].value;
-            out[i] = DeltaRec{loc, val};
+            out.loc[i] = (uint32_t)loc;
+            out.val[i] = val;
             if (shadow) shadow[loc] = val;
         } else {
-            out[i] = DeltaRec{~0ull, 0};
+            out.loc[i] = ~0u;
+            out.val[i] = 0;
         }
     }
 }
 
 // devShadow refresh from staged delta records (a prepared merge).
-__global__ void delta_to_shadow_kernel(uint64_t* __restrict__ shadow, const DeltaRec* __restrict__ d, uint64_t n) {
+__global__ void delta_to_shadow_kernel(uint64_t* __restrict__ shadow, DeltaBuf d, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const DeltaRec r = d[i];
-        if (r.loc != ~0ull) shadow[r.loc] = r.value;
+        const uint32_t loc = d.loc[i];
+        if (loc != ~0u) shadow[loc] = d.val[i];
     }
 }
 
@@ -79,10 +81,10 @@ __global__ void wlog_restore_kernel(Cell* __restrict__ cells, const uint64_t* __
 // The first part of the sorted delta goes straight into the (mapped, pinned)
 // host replica as zero-copy PCIe stores, concurrently with the DMA + host
 // scatter of the rest.
-__global__ void delta_zc_scatter_kernel(uint64_t* host, const DeltaRec* __restrict__ d, uint64_t n) {
+__global__ void delta_zc_scatter_kernel(uint64_t* host, DeltaBuf d, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const DeltaRec r = d[i];
-        if (r.loc != ~0ull) host[r.loc] = r.value;
+        const uint32_t loc = d.loc[i];
+        if (loc != ~0u) host[loc] = d.val[i];
     }
 }
 
@@ -106,14 +108,14 @@ cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
+cudaError_t launch_wlog_gather(DeltaBuf out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     wlog_gather_kernel<<<grid_words(n, g), 256, 0, s>>>(out, shadow, cells, wlog, n, size_words);
     return cudaGetLastError();
 }
 
-cudaError_t launch_delta_to_shadow(uint64_t* shadow, const DeltaRec* d, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
+cudaError_t launch_delta_to_shadow(uint64_t* shadow, DeltaBuf d, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     delta_to_shadow_kernel<<<grid_words(n, g), 256, 0, s>>>(shadow, d, n);
     return cudaGetLastError();
@@ -150,7 +152,7 @@ cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint3
     return cudaGetLastError();
 }
 
-cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
+cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, DeltaBuf d, uint64_t n, const LaunchGeom& g,
                                     cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     static const int zc_blocks = [] {  // tuning experiments only: CTAs of 128 threads per SM

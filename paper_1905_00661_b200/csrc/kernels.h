@@ -13,9 +13,11 @@ struct Cell;
 struct CacheGeom;
 
 // One merge delta record: local word index + value (16 B, DMA'd to the host).
-struct DeltaRec {
-    uint64_t loc;
-    uint64_t value;
+// Merge delta records, struct of arrays (12 B per record on the wire): the
+// shard-local word (< 2^32; ~0u = empty slot) and its value.
+struct DeltaBuf {
+    uint32_t* loc;
+    uint64_t* val;
 };
 
 struct LaunchGeom {
@@ -67,13 +69,13 @@ cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_word
                                 uint64_t n_chunks, uint32_t chunk_shift, bool to_plain, const LaunchGeom& g,
                                 cudaStream_t s);
 // Write-set log -> compact delta (+ devShadow refresh when shadow != nullptr).
-cudaError_t launch_wlog_gather(DeltaRec* out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
+cudaError_t launch_wlog_gather(DeltaBuf out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
                                uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Rollback of the device write set: cells[loc].value = shadow[loc] per log slot.
 cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
                                 uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Zero-copy scatter of delta records into a device-accessible host buffer.
-cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, const DeltaRec* d, uint64_t n, const LaunchGeom& g,
+cudaError_t launch_delta_zc_scatter(uint64_t* host_dev, DeltaBuf d, uint64_t n, const LaunchGeom& g,
                                     cudaStream_t s);
 // SCAN schedule of a bank batch (bank_sched.cu): sort + segmented scan, input
 // order, no aborts; temp from bank_sched_temp_bytes.
@@ -117,7 +119,7 @@ cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const he
                                unsigned long long* d_tickets, hetm_cache_result* d_res, DevCounters* ctr, void* temp,
                                size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
 // devShadow[loc] = value for staged delta records (prepared merge).
-cudaError_t launch_delta_to_shadow(uint64_t* shadow, const DeltaRec* d, uint64_t n, const LaunchGeom& g, cudaStream_t s);
+cudaError_t launch_delta_to_shadow(uint64_t* shadow, DeltaBuf d, uint64_t n, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

@@ -497,7 +497,7 @@ def test_rounds_match_sequential_replay(hetm, orc, dev_factory, optimized):
 @pytest.mark.parametrize("batches", [1, 3])
 def test_merge_delta_rounds_match_replay(hetm, orc, dev_factory, batches):
     """mergeCommit in delta form (HETM_CFG_MERGE_DELTA): sparse device write
-    sets ship as 16-B {word, value} records; the host replica must end exactly
+    sets ship as 12-B {word, value} records; the host replica must end exactly
     as with the SPEC chunk copy (replica equality after every round,
     SPEC.md:640), across several batches per round and aborted rounds."""
     W, gran = 1 << 20, 1024
@@ -534,9 +534,9 @@ def test_merge_delta_rounds_match_replay(hetm, orc, dev_factory, batches):
             orc.bank_replay(ref, txs, orc.order_by_ticket(tickets), gran, 16384)
             st = d.merge_commit(host)
             d.merge_wait()
-            n_slots = 2 * n_tickets  # records: 8 B each by zero-copy stores, 16 B each by DMA
+            n_slots = 2 * n_tickets  # records: 8 B each by zero-copy stores, 12 B each by DMA
             recs = [t[2] for t in d.transfer_log() if t[:2] == (hetm.D2H, hetm.TAG_MERGE_DELTA)]
-            assert st.bytes_d2h == sum(recs) and 8 * n_slots <= st.bytes_d2h <= 16 * n_slots
+            assert st.bytes_d2h == sum(recs) and 8 * n_slots <= st.bytes_d2h <= 12 * n_slots
         d.clear_round()
         outcomes.append(conflict)
         assert (host == ref).all(), rnd
