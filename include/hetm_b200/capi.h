@@ -364,6 +364,18 @@ int hetm_dev_route_to_peers_dptr(hetm_dev* dev, const hetm_log_entry* d_in, uint
                                  uint64_t shard_words, uint32_t my_shard, uint64_t cap, uint32_t parity,
                                  void* const* peer_entries, void* const* peer_counts, void* stream);
 int hetm_dev_apply_received(hetm_dev* dev, uint32_t parity, int mode, uint64_t* n_out, void* stream);
+/* Bitmap OR-reduce over NVLink (NCCL has no bitwise OR):
+ * hetm_dev_bitmap_dptr exposes a bitmap (HETM_BMP_RS / WS / CHUNK) for CUDA IPC
+ * export; hetm_dev_bitmap_or_peers ORs words [word_lo, word_hi) (word_hi == 0:
+ * all) of n_peers peer bitmaps of the same geometry — device pointers usable
+ * from this GPU (IPC-opened, or other handles in the process) — into this
+ * handle's bitmap, ordered after its batches, on `stream` (NULL: the handle's
+ * validation stream).  Every rank ORing all words is the all-reduce; each
+ * rank ORing only its own slice [lo, hi) is the reduce-scatter.  The caller
+ * orders the peers' bitmaps before the call (a barrier). */
+int hetm_dev_bitmap_dptr(hetm_dev* dev, int which, void** dptr, uint64_t* n_words);
+int hetm_dev_bitmap_or_peers(hetm_dev* dev, int which, const void* const* peer_words, uint32_t n_peers,
+                             uint64_t word_lo, uint64_t word_hi, void* stream);
 /* CUDA IPC of device buffers between the ranks of one node (64-byte handles). */
 int hetm_ipc_get_handle(void* dptr, void* handle64);
 int hetm_ipc_open_handle(const void* handle64, void** dptr);

@@ -454,6 +454,17 @@ class GpuDevice:
             self._prep_keep = host_replica
         self._chk(lib.hetm_dev_merge_prepare(self.h, host_replica.ctypes.data if host_replica is not None else None))
 
+    def bitmap_dptr(self, which: int):
+        """(device pointer, n_words) of bitmap `which` (for CUDA IPC export)."""
+        p, n = C.c_void_p(), C.c_uint64()
+        self._chk(lib.hetm_dev_bitmap_dptr(self.h, which, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def bitmap_or_peers(self, which: int, peer_ptrs, word_lo: int = 0, word_hi: int = 0, stream: int = 0):
+        """OR words [word_lo, word_hi) (0: all) of the peers' bitmaps into this one (NVLink peer loads)."""
+        arr = (C.c_void_p * max(len(peer_ptrs), 1))(*[C.c_void_p(p) for p in peer_ptrs])
+        self._chk(lib.hetm_dev_bitmap_or_peers(self.h, which, arr, len(peer_ptrs), word_lo, word_hi, stream or None))
+
     def set_schedule(self, mode: int):
         """Bank batch schedule: SCHED_OPTIMISTIC | SCHED_SCAN | SCHED_AUTO (default)."""
         self._chk(lib.hetm_dev_set_schedule(self.h, mode))

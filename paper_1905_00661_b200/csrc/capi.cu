@@ -1025,6 +1025,33 @@ int hetm_dev_snapshot_bitmap(hetm_dev* d, int which, uint64_t* out, uint64_t n_w
     return HETM_OK;
 }
 
+int hetm_dev_bitmap_dptr(hetm_dev* d, int which, void** dptr, uint64_t* n_words) {
+    if (!d || !dptr) return HETM_ERR_INVALID_ARG;
+    unsigned long long* p = bitmap_ptr(d, which);
+    if (!p) return HETM_ERR_INVALID_ARG;
+    *dptr = p;
+    if (n_words) *n_words = which == HETM_BMP_CHUNK ? d->chunk_words : d->rs_words;
+    return HETM_OK;
+}
+
+int hetm_dev_bitmap_or_peers(hetm_dev* d, int which, const void* const* peer_words, uint32_t n_peers,
+                             uint64_t word_lo, uint64_t word_hi, void* stream) {
+    if (!d || (n_peers && !peer_words)) return HETM_ERR_INVALID_ARG;
+    unsigned long long* p = bitmap_ptr(d, which);
+    if (!p) return HETM_ERR_INVALID_ARG;
+    const uint64_t n = which == HETM_BMP_CHUNK ? d->chunk_words : d->rs_words;
+    if (word_hi == 0) word_hi = n;  // 0: the whole bitmap
+    if (word_lo > word_hi || word_hi > n) return HETM_ERR_INVALID_SIZE;
+    for (uint32_t k = 0; k < n_peers; ++k)
+        if (!peer_words[k]) return HETM_ERR_INVALID_ARG;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));  // the local batches' bits are final
+    cudaError_t e = launch_or_peers(p, reinterpret_cast<const unsigned long long* const*>(peer_words), n_peers,
+                                    word_lo, word_hi, d->geom, s);
+    if (e != cudaSuccess) return fail(d, e, "bitmap_or_peers");
+    return HETM_OK;
+}
+
 int hetm_dev_or_bitmap(hetm_dev* d, int which, const uint64_t* words, uint64_t n_words) {
     if (!d || (!words && n_words)) return HETM_ERR_INVALID_ARG;
     unsigned long long* p = bitmap_ptr(d, which);

@@ -120,6 +120,9 @@ cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const he
                                size_t temp_bytes, const LaunchGeom& g, cudaStream_t s);
 // devShadow[loc] = value for staged delta records (prepared merge).
 cudaError_t launch_delta_to_shadow(uint64_t* shadow, DeltaBuf d, uint64_t n, const LaunchGeom& g, cudaStream_t s);
+// dst[lo, hi) |= peers[k][lo, hi) for every peer bitmap (NVLink peer loads).
+cudaError_t launch_or_peers(unsigned long long* dst, const unsigned long long* const* peers, uint32_t n_peers,
+                            uint64_t lo, uint64_t hi, const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

@@ -375,6 +375,21 @@ __global__ void or_words_kernel(unsigned long long* dst, const unsigned long lon
         if (src[i]) atomicOr(&dst[i], src[i]);
 }
 
+// Bitwise-OR reduction of bitmaps over NVLink (NCCL has no
+// bitwise OR): words [lo, hi) of dst |= the same words of every peer bitmap,
+// read through peer pointers (CUDA IPC / same-process handles of other GPUs).
+// Coalesced peer loads, one plain store per word; up to 16 peers per launch.
+struct PeerWords {
+    const unsigned long long* p[16];
+};
+__global__ void or_peers_kernel(unsigned long long* dst, PeerWords peers, uint32_t n_peers, uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long acc = dst[i];
+        for (uint32_t k = 0; k < n_peers; ++k) acc |= peers.p[k][i];
+        dst[i] = acc;
+    }
+}
+
 static unsigned grid_cap(uint64_t items, int threads, const LaunchGeom& g, int per_sm) {
     uint64_t want = (items + threads - 1) / threads;
     const uint64_t cap = (uint64_t)per_sm * (uint64_t)g.sm_count;
@@ -550,6 +565,18 @@ cudaError_t launch_or_words(unsigned long long* dst, const unsigned long long* s
     uint64_t grid = (n + 255) / 256;
     if (grid > 1184) grid = 1184;
     or_words_kernel<<<(unsigned)grid, 256, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_or_peers(unsigned long long* dst, const unsigned long long* const* peers, uint32_t n_peers,
+                            uint64_t lo, uint64_t hi, const LaunchGeom& g, cudaStream_t s) {
+    if (hi <= lo || n_peers == 0) return cudaSuccess;
+    for (uint32_t base = 0; base < n_peers; base += 16) {
+        PeerWords pw{};
+        const uint32_t m = n_peers - base < 16 ? n_peers - base : 16;
+        for (uint32_t k = 0; k < m; ++k) pw.p[k] = peers[base + k];
+        or_peers_kernel<<<grid_cap(hi - lo, 256, g, 8), 256, 0, s>>>(dst, pw, m, lo, hi);
+    }
     return cudaGetLastError();
 }
 
