@@ -438,6 +438,8 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
                       "delta (12-B {word,value} per device-written word)" +
                       (", staged + speculatively applied right after the execution phase (hetm_dev_merge_prepare)"
                        if args.early_merge else "")),
+            "bound": "host DRAM: the merge scatter of ~2^21 random words into the host replica per round plus "
+                     "the DMAs (profiles/r01_e2e_bounds.txt)",
             "timing": "host wall clock around full rounds (pinned buffers; verdict + merge D2H landed in the host "
                       "replica before the next round's host log; the next GPU batch overlaps the merge, PAPER.md:355)"}
 
