@@ -18,6 +18,8 @@
 // No lock is taken and nothing retries: hot sets cost one thread a loop over
 // their transactions instead of a chain of lock handoffs.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 
@@ -96,9 +98,13 @@ __device__ __noinline__ void mark_mask(unsigned long long* bm, uint64_t s0, uint
 // segment's records are contiguous: the serial walk of a hot set then reads
 // lines already in L1/L2 instead of one random DRAM record per step.
 __global__ void cs_gather_kernel(const hetm_cache_tx* __restrict__ in, uint64_t n, const uint32_t* __restrict__ pay,
-                                 hetm_cache_tx* __restrict__ recs) {
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+                                 const uint32_t* __restrict__ sets, hetm_cache_tx* __restrict__ recs,
+                                 uint8_t* __restrict__ start) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
         recs[j] = in[pay[j]];
+        const uint32_t set = sets[j];
+        start[j] = set != kNoSet && (j == 0 || sets[j - 1] != set);  // a set segment begins here
+    }
 }
 
 // One 256-bit load: the value words of two adjacent cells {v0, m0, v1, m1}.
@@ -109,36 +115,51 @@ __device__ __forceinline__ void ld_vals2(const Cell* c, uint64_t& v0, uint64_t& 
                  : "memory");
 }
 
-// One thread per set segment.  The whole set (8 ways x 8 words) lives in
-// registers for the segment — every way is touched through unrolled,
-// predicated loops (a runtime index would spill the arrays to local memory)
-// — and the next transaction record is loaded while the current one runs, so
-// a hot set's serial chain costs register work, not dependent memory round
-// trips.  Dirty words are stored once, at the segment's end.
+// One thread per set segment (the segment starts compacted first, so no lane
+// idles on a non-start position).  The 32 tag words {key0, key1, lru, flags}
+// of the 8 ways live in registers (predicated updates); the 32 value words in
+// shared memory, column-major per thread (conflict-free), indexed by way —
+// a runtime index into registers would spill, and selecting over all 32
+// value registers per transaction cost most of the instructions.  The next
+// record is loaded while the current one runs; dirty words are stored once,
+// at the segment's end.
+
 __global__ void __launch_bounds__(kCsThreads) cs_run_kernel(ShardView v, CacheGeom cg,
                                                             const hetm_cache_tx* __restrict__ recs, uint64_t n,
                                                             const uint32_t* __restrict__ sets,
                                                             const uint32_t* __restrict__ pay,
+                                                            const uint32_t* __restrict__ starts,
+                                                            const uint32_t* __restrict__ n_starts,
                                                             hetm_cache_result* __restrict__ res,
                                                             const unsigned long long* first, DevCounters* ctr) {
+    __shared__ uint64_t sval[4 * kWays][kCsThreads];  // [way * 4 + q][thread]
+    uint64_t* val = &sval[0][threadIdx.x];             // val[(way * 4 + q) * kCsThreads]
     const unsigned long long t0 = *first, wbase = ld_relaxed(&ctr->wlog_base);
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = *n_starts;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = starts[k];
         const uint32_t set = sets[j];
-        if (set == kNoSet || (j > 0 && sets[j - 1] == set)) continue;  // not a segment start
         const uint64_t s0 = cg.base_local + (uint64_t)set * kSetWords;
         Cell* cs = v.cells + s0;
-        uint64_t w[kWays][kWayWords];  // the set's words
+        uint64_t k0[kWays], k1[kWays], lru[kWays], fl[kWays];
 #pragma unroll
-        for (int a = 0; a < kWays; ++a)
-#pragma unroll
-            for (int q = 0; q < kWayWords; q += 2) ld_vals2(&cs[a * kWayWords + q], w[a][q], w[a][q + 1]);
+        for (int a = 0; a < kWays; ++a) {
+            ld_vals2(&cs[a * kWayWords + kKey0], k0[a], k1[a]);
+            ld_vals2(&cs[a * kWayWords + kLru], lru[a], fl[a]);
+            uint64_t x0, x1, x2, x3;
+            ld_vals2(&cs[a * kWayWords + kVal], x0, x1);
+            ld_vals2(&cs[a * kWayWords + kVal + 2], x2, x3);
+            val[(a * 4 + 0) * kCsThreads] = x0;
+            val[(a * 4 + 1) * kCsThreads] = x1;
+            val[(a * 4 + 2) * kCsThreads] = x2;
+            val[(a * 4 + 3) * kCsThreads] = x3;
+        }
         uint64_t rs_mask = 0, ws_mask = 0;  // words of the set read / written by the segment
         unsigned long long last_update = ~0ull;
         uint64_t i = pay[j];
         hetm_cache_tx r = recs[j];
         for (uint64_t jj = j;;) {
-            // load the next transaction of this set ahead (contiguous records)
-            const bool more = jj + 1 < n && sets[jj + 1] == set;
+            const bool more = jj + 1 < n && sets[jj + 1] == set;  // load the next transaction ahead
             uint64_t i_next = 0;
             hetm_cache_tx r_next;
             if (more) {
@@ -150,14 +171,14 @@ __global__ void __launch_bounds__(kCsThreads) cs_run_kernel(ShardView v, CacheGe
             int hit = kWays, invalid = kWays, lru_way = 0;
 #pragma unroll
             for (int a = kWays - 1; a >= 0; --a) {  // lowest index wins every tie
-                if ((w[a][kFlags] & 1) && w[a][kKey0] == r.key[0] && w[a][kKey1] == r.key[1]) hit = a;
-                if (!(w[a][kFlags] & 1)) invalid = a;
+                if ((fl[a] & 1) && k0[a] == r.key[0] && k1[a] == r.key[1]) hit = a;
+                if (!(fl[a] & 1)) invalid = a;
             }
-            uint64_t lru_min = w[0][kLru];
+            uint64_t lru_min = lru[0];
 #pragma unroll
             for (int a = 1; a < kWays; ++a)
-                if (w[a][kLru] < lru_min) {
-                    lru_min = w[a][kLru];
+                if (lru[a] < lru_min) {
+                    lru_min = lru[a];
                     lru_way = a;
                 }
             int target;
@@ -178,31 +199,33 @@ __global__ void __launch_bounds__(kCsThreads) cs_run_kernel(ShardView v, CacheGe
             hetm_cache_result out;
             out.status = status;
             out.way = (uint32_t)target;
-            // branch-free update of the target way (target == kWays: no way)
-            const bool fill = !is_get && status != HETM_CACHE_UPDATED;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) out.value[q] = 0;
-#pragma unroll
-            for (int a = 0; a < kWays; ++a) {
-                const bool m = a == target;
+            if (target < kWays) {
+                uint64_t* tv = val + (uint64_t)target * 4 * kCsThreads;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    out.value[q] = m ? (is_get ? w[a][kVal + q] : r.value[q]) : out.value[q];
-                    w[a][kVal + q] = (m && !is_get) ? r.value[q] : w[a][kVal + q];
+                    out.value[q] = is_get ? tv[q * kCsThreads] : r.value[q];
+                    if (!is_get) tv[q * kCsThreads] = r.value[q];
                 }
-                w[a][kKey0] = (m && fill) ? r.key[0] : w[a][kKey0];
-                w[a][kKey1] = (m && fill) ? r.key[1] : w[a][kKey1];
-                w[a][kFlags] = (m && fill) ? 1ull : w[a][kFlags];
-                w[a][kLru] = m ? t + 1 : w[a][kLru];
-            }
-            if (target < kWays) {
+                const bool fill = !is_get && status != HETM_CACHE_UPDATED;
+#pragma unroll
+                for (int a = 0; a < kWays; ++a) {
+                    const bool mt = a == target;
+                    k0[a] = (mt && fill) ? r.key[0] : k0[a];
+                    k1[a] = (mt && fill) ? r.key[1] : k1[a];
+                    fl[a] = (mt && fill) ? 1ull : fl[a];
+                    lru[a] = mt ? t + 1 : lru[a];
+                }
                 const uint32_t wl = (uint32_t)(target * kWayWords);
                 rs_mask |= 0xfull << (wl + kVal);
                 ws_mask |= (is_get ? (1ull << kLru)
                                    : (status == HETM_CACHE_UPDATED ? (0x1full << kVal) : 0xffull)) << wl;
                 last_update = t;
+                wlog_put(v, wbase, t, 0, is_get ? (uint32_t)(s0 + wl + kLru) : ~0u);  // the LRU touch
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) out.value[q] = 0;
+                wlog_put(v, wbase, t, 0, ~0u);
             }
-            wlog_put(v, wbase, t, 0, (target < kWays && is_get) ? (uint32_t)(s0 + target * kWayWords + kLru) : ~0u);
             wlog_put(v, wbase, t, 1, ~0u);
             if (res) res[i] = out;
             if (!more) break;
@@ -215,10 +238,18 @@ __global__ void __launch_bounds__(kCsThreads) cs_run_kernel(ShardView v, CacheGe
         for (int a = 0; a < kWays; ++a)
             rs_mask |= ((1ull << kKey0) | (1ull << kKey1) | (1ull << kLru) | (1ull << kFlags)) << (a * kWayWords);
 #pragma unroll
-        for (int a = 0; a < kWays; ++a)
+        for (int a = 0; a < kWays; ++a) {
+            const uint64_t wm = ws_mask >> (a * kWayWords);
+            if (!(wm & 0xffull)) continue;
+            Cell* way = cs + a * kWayWords;
+            if (wm & (1ull << kKey0)) way[kKey0].value = k0[a];
+            if (wm & (1ull << kKey1)) way[kKey1].value = k1[a];
 #pragma unroll
-            for (int q = 0; q < kWayWords; ++q)
-                if ((ws_mask >> (a * kWayWords + q)) & 1ull) cs[a * kWayWords + q].value = w[a][q];
+            for (int q = 0; q < 4; ++q)
+                if (wm & (1ull << (kVal + q))) way[kVal + q].value = val[(a * 4 + q) * kCsThreads];
+            if (wm & (1ull << kLru)) way[kLru].value = lru[a];
+            if (wm & (1ull << kFlags)) way[kFlags].value = fl[a];
+        }
         mark_mask(v.rs, s0, rs_mask, v.gran_shift);
         mark_mask(v.ws, s0, ws_mask, v.gran_shift);
         mark_mask(v.chunk, s0, ws_mask, v.chunk_shift);
@@ -233,8 +264,12 @@ size_t cache_sched_temp_bytes(uint64_t n, uint64_t n_sets) {
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
                                     (int)std::min<uint32_t>(32, bits_of(n_sets) + 1));
+    size_t b = 0;
+    cub::DeviceSelect::Flagged(nullptr, b, thrust::counting_iterator<uint32_t>(0), (const uint8_t*)nullptr,
+                               (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    return 4 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + 256 + al(a);
+    // [sets in/out | payload in/out | starts | records | start flags | first | n_starts | cub temp]
+    return 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + al(n) + 512 + al(std::max(a, b));
 }
 
 cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const hetm_cache_tx* d_in, uint64_t n,
@@ -248,20 +283,26 @@ cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const he
     uint32_t* sets_s = reinterpret_cast<uint32_t*>(p + al(n * 4));
     uint32_t* pay = reinterpret_cast<uint32_t*>(p + 2 * al(n * 4));
     uint32_t* pay_s = reinterpret_cast<uint32_t*>(p + 3 * al(n * 4));
-    auto* recs = reinterpret_cast<hetm_cache_tx*>(p + 4 * al(n * 4));
-    const size_t off = 4 * al(n * 4) + al(n * sizeof(hetm_cache_tx));
+    uint32_t* starts = reinterpret_cast<uint32_t*>(p + 4 * al(n * 4));
+    auto* recs = reinterpret_cast<hetm_cache_tx*>(p + 5 * al(n * 4));
+    auto* start = reinterpret_cast<uint8_t*>(p + 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)));
+    const size_t off = 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + al(n);
     auto* first = reinterpret_cast<unsigned long long*>(p + off);
-    void* cub_tmp = p + off + 256;
-    size_t cub_bytes = temp_bytes - (off + 256);
+    auto* n_starts = reinterpret_cast<uint32_t*>(p + off + 256);
+    void* cub_tmp = p + off + 512;
+    size_t cub_bytes = temp_bytes - (off + 512);
     const int end_bit = (int)std::min<uint32_t>(32, bits_of(cg.n_sets) + 1);
     cs_ticket_kernel<<<1, 1, 0, s>>>(ctr, n, first);
     cs_keys_kernel<<<grid_of(n, 256, 8, g.sm_count), 256, 0, s>>>(v, cg, d_in, n, sets, pay, d_tickets, first, ctr);
     cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, sets, sets_s, pay, pay_s, (int64_t)n, 0,
                                                     end_bit, s);
     if (e != cudaSuccess) return e;
-    cs_gather_kernel<<<grid_of(n, 256, 8, g.sm_count), 256, 0, s>>>(d_in, n, pay_s, recs);
-    cs_run_kernel<<<grid_of(n, kCsThreads, 16, g.sm_count), kCsThreads, 0, s>>>(v, cg, recs, n, sets_s, pay_s, d_res,
-                                                                              first, ctr);
+    cs_gather_kernel<<<grid_of(n, 256, 8, g.sm_count), 256, 0, s>>>(d_in, n, pay_s, sets_s, recs, start);
+    e = cub::DeviceSelect::Flagged(cub_tmp, cub_bytes, thrust::counting_iterator<uint32_t>(0), start, starts, n_starts,
+                                   (int64_t)n, s);
+    if (e != cudaSuccess) return e;
+    cs_run_kernel<<<grid_of(n, kCsThreads, 16, g.sm_count), kCsThreads, 0, s>>>(v, cg, recs, n, sets_s, pay_s, starts,
+                                                                              n_starts, d_res, first, ctr);
     return cudaGetLastError();
 }
 
