@@ -138,3 +138,20 @@ def test_prepare_is_a_noop_without_delta_merge(hetm, orc, dev_factory):
     d.merge_commit(host)
     d.merge_wait()
     assert (host == d.download(hetm.REPLICA_DEV)).all()
+
+
+def test_prepared_for_another_replica(hetm, orc, dev_factory):
+    """merge_prepare(A) speculatively, then merge_commit(B): A is put back, B gets the merge."""
+    d, host_a = fresh(hetm, dev_factory)
+    host_b = host_a.copy()
+    ref = host_a.copy()
+    txs = orc.gen_bank_batch(95, 1 << 13, 0, W)
+    r = d.execute_batch(hetm.KERNEL_BANK, txs)
+    orc.bank_replay(ref, txs, orc.order_by_ticket(r.tickets), 1024, 16384)
+    before_a = host_a.copy()
+    d.merge_prepare(host_a)
+    assert not d.round_verdict()
+    d.merge_commit(host_b)
+    d.merge_wait()
+    assert (host_a == before_a).all()
+    assert (host_b == ref).all() and (d.download(hetm.REPLICA_DEV) == ref).all()
