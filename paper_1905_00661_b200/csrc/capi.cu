@@ -5,11 +5,18 @@
 //   s_exec   batch transaction kernels (execution phase)
 //   s_copy   H2D log chunk copies (interconnect streamChunk)
 //   s_val    validation kernels; APPLY kernels wait on the tail of s_exec
-//   s_merge  shadow update, rollback, round clear (round boundary)
-//   s_d2h    merge device->host chunk copies from devShadow, overlapping the
-//            next round's execution (double buffering)
-// Events carry every cross-stream dependency; nothing blocks the host except
-// the explicitly synchronous calls (verdict, merge_wait, snapshots, stats).
+//   s_merge  shadow update, delta sort/gather, rollback, round clear
+//   s_d2h    merge device->host copies (chunks from devShadow, or the delta
+//            records), overlapping the next round's execution (double
+//            buffering)
+//   s_zc     zero-copy delta stores into the mapped host replica (optional)
+//   s_in     input pieces H2D of a host-buffer batch, under the kernel on the
+//            previous piece; s_out its tickets / results D2H
+//   s_est    the AUTO schedule's hot-spot estimate of device-pointer batches
+// plus the worker pool that scatters the merge delta into the host replica as
+// its pieces land.  Events carry every cross-stream dependency; nothing blocks
+// the host except the explicitly synchronous calls (verdict, merge_wait,
+// snapshots, stats) and the pool hand-off of merge_prepare.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
