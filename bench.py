@@ -472,7 +472,29 @@ def cpu_baseline(args, seconds=8.0, rounds=None):
         r += 1
     return {"value": done_tx / t_tot, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{r} rounds x ({B} bank tx + {L} log entries) on the 2^{args.words_log2}-word STMR "
-                      f"(1/4 of a GPU round), oracle/hetm_oracle.c pthreads"}
+                      f"(1/4 of a GPU round), oracle/hetm_oracle.c pthreads",
+            "host": host_info()}
+
+
+def host_info():
+    """the CPU the baseline ran on (hardware_concurrency, model, MemTotal)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        info["affinity_cpus"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["mem_total_gb"] = round(int(line.split()[1]) / (1 << 20), 1)
+                break
+    except OSError:
+        pass
+    return info
 
 
 def run_reference(args):
