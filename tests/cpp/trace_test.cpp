@@ -8,7 +8,9 @@
 // wrote in the previous one; every 3rd round the host also writes into the
 // device half (a conflict: DeviceAborted under FavorHost).
 //
-//   trace_test [rounds] [device faults HETM_FAULT_*] [engine faults ENGINE_FAULT_*] [dump path]
+//   trace_test [rounds] [device faults HETM_FAULT_*] [engine faults ENGINE_FAULT_*] [dump path] [host|device]
+// (policy: FavorHost, or FavorDevice — conflicting rounds are then HostAborted
+// and P2-dagger checks the host's speculative set)
 // Exit 0 iff the verdicts are as expected: both checks pass with no fault, and
 // at least one fails (the mutation is caught) with any fault.  One JSON line.
 #include <cstdio>
@@ -43,6 +45,7 @@ int main(int argc, char** argv) {
     const uint32_t dev_fault = argc > 2 ? (uint32_t)std::strtoul(argv[2], nullptr, 0) : 0;
     const uint32_t eng_fault = argc > 3 ? (uint32_t)std::strtoul(argv[3], nullptr, 0) : 0;
     const std::string dump = argc > 4 ? argv[4] : "";
+    const bool favor_device = argc > 5 && std::strcmp(argv[5], "device") == 0;
     const uint64_t W = 1ull << 18, half = W / 2, B = 1u << 12;
     const int T = 4;
 
@@ -74,6 +77,7 @@ int main(int argc, char** argv) {
     EngineConfig ec;
     ec.chunk_entries = 256;
     ec.fault = eng_fault;
+    ec.policy = favor_device ? Policy::FavorDevice : Policy::FavorHost;
     Engine eng(dev, stm, log, host, ec);
     Trace trace(W, "{\"kernel\": \"bank\", \"batch\": " + std::to_string(B) + ", \"host_threads\": " +
                        std::to_string(T) + ", \"dev_fault\": " + std::to_string(dev_fault) +
@@ -122,12 +126,12 @@ int main(int argc, char** argv) {
     const bool faulty = dev_fault || eng_fault;
     const bool caught = p1.verdict != 0 || p2.verdict != 0;
     const bool ok = faulty ? caught : (p1.verdict == 0 && p2.verdict == 0);
-    std::printf("{\"rounds\": %d, \"dev_fault\": %u, \"engine_fault\": %u, \"events\": %zu, \"conflict_rounds\": %d, "
+    std::printf("{\"rounds\": %d, \"policy\": \"%s\", \"dev_fault\": %u, \"engine_fault\": %u, \"events\": %zu, \"conflict_rounds\": %d, "
                 "\"p1\": {\"verdict\": %d, \"reason\": %d, \"tx\": %llu, \"addr\": %llu, \"expected\": %llu, "
                 "\"got\": %llu, \"round\": %u, \"txs\": %llu, \"reads\": %llu}, "
                 "\"p2dagger\": {\"verdict\": %d, \"reason\": %d, \"round\": %u, \"txs\": %llu, \"reads\": %llu}, "
                 "\"ok\": %d}\n",
-                rounds, dev_fault, eng_fault, ev.size(), n_conflict, p1.verdict, p1.reason,
+                rounds, favor_device ? "FavorDevice" : "FavorHost", dev_fault, eng_fault, ev.size(), n_conflict, p1.verdict, p1.reason,
                 (unsigned long long)p1.tx, (unsigned long long)p1.addr, (unsigned long long)p1.expected,
                 (unsigned long long)p1.got, p1.round, (unsigned long long)p1.checked_txs,
                 (unsigned long long)p1.checked_reads, p2.verdict, p2.reason, p2.round,

@@ -23,11 +23,11 @@ FAULT_SKIP_RS, FAULT_SKIP_TS, FAULT_SKIP_ROLLBACK = 1, 2, 4          # capi.h HE
 ENGINE_EARLY_DEVICE_COMMIT, ENGINE_DROP_CHUNK = 1, 2                  # engine.hpp ENGINE_FAULT_*
 
 
-def run(rounds, dev_fault=0, eng_fault=0, dump=""):
+def run(rounds, dev_fault=0, eng_fault=0, dump="", policy="host"):
     if not os.path.exists(EXE):
         pytest.skip("build/trace_test not built")
-    out = subprocess.run([EXE, str(rounds), str(dev_fault), str(eng_fault), dump], capture_output=True, text=True,
-                         timeout=600)
+    out = subprocess.run([EXE, str(rounds), str(dev_fault), str(eng_fault), dump or "", policy], capture_output=True,
+                         text=True, timeout=600)
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert lines, out.stdout + out.stderr
     return out.returncode, json.loads(lines[-1])
@@ -48,6 +48,15 @@ def test_live_rounds_pass_p1_and_p2dagger(tmp_path):
     p1 = O.check_p1(ev, init)
     assert p1.verdict == O.CHECK_PASS and p1.checked_reads == r["p1"]["reads"]
     assert O.check_p2dagger(ev, init).verdict == O.CHECK_PASS
+
+
+@pytest.mark.gpu
+def test_live_rounds_favor_device_pass():
+    """FavorDevice: the conflicting rounds are HostAborted — P2-dagger then checks the
+    host transactions' speculative set (on the round-start state), P1 the rest."""
+    rc, r = run(9, policy="device")
+    assert rc == 0 and r["ok"] == 1 and r["policy"] == "FavorDevice", r
+    assert r["conflict_rounds"] == 3 and r["p2dagger"]["txs"] > 0
 
 
 @pytest.mark.gpu
