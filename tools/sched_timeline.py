@@ -26,6 +26,11 @@ for alpha in (0.0, 0.99):
         d.sync()
     d.clear_round()
     print(f"== alpha {alpha}")
+    ks = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    if ks:
+        t0 = min(e.time_range.start for e in ks)
+        t1 = max(e.time_range.end for e in ks)
+        print(f"  span first start -> last end: {t1 - t0:.1f} us over {len(ks)} GPU ops")
     tot = 0.0
     for e in prof.events():
         if e.device_type == torch.autograd.DeviceType.CUDA:
