@@ -113,6 +113,9 @@ public:
     void closeLogIntake() { check(hetm_dev_close_intake(d_)); }
 
     // merge; hostReplica spans this shard's words
+    /// After the host cut-off: stage the delta merge under validation and apply
+    /// it speculatively (undone by the abort paths); needs HETM_CFG_MERGE_DELTA.
+    void mergePrepare(std::span<Word> hostReplica) { check(hetm_dev_merge_prepare(d_, hostReplica.data())); }
     void mergeCommit(std::span<Word> hostReplica) { check(hetm_dev_merge_commit(d_, hostReplica.data(), nullptr)); }
     void mergeAbortDevice(std::span<const Word> hostReplica, bool optimized = true) {
         check(hetm_dev_merge_abort_device(d_, optimized ? 1 : 0, hostReplica.data(), nullptr));
@@ -121,6 +124,9 @@ public:
         check(hetm_dev_merge_abort_host(d_, hostReplica.data(), hostSnapshot.data(), nullptr));
     }
     void mergeWait() { check(hetm_dev_merge_wait(d_)); }
+
+    /// Batch schedule: HETM_SCHED_OPTIMISTIC | HETM_SCHED_SCAN | HETM_SCHED_AUTO (default).
+    void setSchedule(int mode) { check(hetm_dev_set_schedule(d_, mode)); }
 
     hetm_dev* handle() { return d_; }
 
