@@ -317,9 +317,9 @@ def run_ours(args):
     ms_step = ms_total / K
     # our kernels per step (the ncu launch list in profiles/ shows the same set):
     # bank_batch_kernel (+ the AUTO schedule's side-stream hot_estimate_kernel), apply_kernel +
-    # restore_kernel, roll_round_kernel (async clear)
+    # restore_kernel, clear_round_kernel (async clear: bitmaps zeroed + round counters rolled)
     launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_kernel": 1, "restore_kernel": 1,
-                       "roll_round_kernel": 1}
+                       "clear_round_kernel": 1}
     if world > 1 and isinstance(sv, PeerValidator):
         launches_detail.update({"route_count_kernel": 1, "route_scan_kernel": 1, "route_peer_publish_kernel": 1,
                                 "route_peer_scatter_kernel": 1})

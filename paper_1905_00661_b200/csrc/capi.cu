@@ -1675,11 +1675,9 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     if (rc) return rc;
     if (flags & HETM_CLEAR_ASYNC) {
         cudaStream_t s = d->s_merge;
-        CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
-        CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
-        CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
-        cudaError_t e = launch_roll_round(d->d_ctr, (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, s);
-        if (e != cudaSuccess) return fail(d, e, "roll_round");
+        cudaError_t e = launch_clear_round(d->d_rs, d->d_ws, d->rs_words, d->d_chunk, d->chunk_words, d->d_ctr,
+                                           (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, d->geom, s);
+        if (e != cudaSuccess) return fail(d, e, "clear_round");
         if (flags & HETM_CLEAR_RESET_TS) {
             cudaError_t er = launch_reset_ts(d->d_cells, d->W, d->geom, s);
             if (er != cudaSuccess) return fail(d, er, "reset_ts");

@@ -123,6 +123,10 @@ cudaError_t launch_delta_to_shadow(uint64_t* shadow, DeltaBuf d, uint64_t n, con
 // dst[lo, hi) |= peers[k][lo, hi) for every peer bitmap (NVLink peer loads).
 cudaError_t launch_or_peers(unsigned long long* dst, const unsigned long long* const* peers, uint32_t n_peers,
                             uint64_t lo, uint64_t hi, const LaunchGeom& g, cudaStream_t s);
+// Asynchronous clearRound in one launch (bitmaps zeroed + round counters rolled).
+cudaError_t launch_clear_round(unsigned long long* rs, unsigned long long* ws, uint64_t rs_words,
+                               unsigned long long* chunk, uint64_t chunk_words, DevCounters* ctr, int reset_ts,
+                               const LaunchGeom& g, cudaStream_t s);
 // Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
 size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
 cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,

@@ -446,6 +446,35 @@ cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Asynchronous clearRound in one launch: zero RS, WS and ChunkMap and roll the
+// round counters (roll_round_kernel's rule, by block 0) — one kernel instead of
+// three memsets + a roll on the round boundary of the pipelined bench step.
+__global__ void clear_round_kernel(unsigned long long* rs, unsigned long long* ws, uint64_t rs_words,
+                                   unsigned long long* chunk, uint64_t chunk_words, DevCounters* ctr, int reset_ts) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long m = ctr->round_max_ts;
+        ctr->ts_floor = reset_ts ? 0ull : (m > ctr->ts_floor ? m : ctr->ts_floor);
+        ctr->round_max_ts = 0;
+        ctr->wlog_base = ctr->ticket;
+        ctr->wlog_overflow = 0;
+    }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rs_words; i += stride) {
+        rs[i] = 0;
+        ws[i] = 0;
+    }
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < chunk_words; i += stride) chunk[i] = 0;
+}
+
+cudaError_t launch_clear_round(unsigned long long* rs, unsigned long long* ws, uint64_t rs_words,
+                               unsigned long long* chunk, uint64_t chunk_words, DevCounters* ctr, int reset_ts,
+                               const LaunchGeom& g, cudaStream_t s) {
+    const uint64_t n = rs_words > chunk_words ? rs_words : chunk_words;
+    clear_round_kernel<<<grid_cap(n ? n : 1, 256, g, 2), 256, 0, s>>>(rs, ws, rs_words, chunk, chunk_words, ctr,
+                                                                      reset_ts);
+    return cudaGetLastError();
+}
+
 // Core launcher over a LogView; n_hint sizes the grid (the flat count, or the
 // segmented view's capacity when the counts live on the device).
 static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n_hint, int apply, DevCounters* ctr,
