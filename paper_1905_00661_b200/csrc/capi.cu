@@ -141,6 +141,7 @@ struct hetm_dev {
     unsigned long long* d_chunk = nullptr;
     DevCounters* d_ctr = nullptr;
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
+    uint64_t* h_first = nullptr;         // pinned: first ticket of the current host-buffer batch
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
     unsigned long long* d_restore = nullptr; // apply-kernel restore queue (kRestoreCap entries)
     CacheGeom cache{};                   // HETM_KERNEL_CACHE region
@@ -681,6 +682,8 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);
     d->arena_cap = cfg->log_capacity ? cfg->log_capacity : (1ull << 20);
     if ((rc = dev_alloc(d, (void**)&d->d_arena, d->arena_cap * sizeof(hetm_log_entry)))) return bail(rc);
+    if (cudaHostAlloc((void**)&d->h_first, 64, cudaHostAllocPortable) != cudaSuccess)
+        return bail(fail(d, cudaGetLastError(), "cudaHostAlloc(first ticket)"));
     if (cudaHostAlloc((void**)&d->h_ctr, sizeof(DevCounters), cudaHostAllocPortable) != cudaSuccess)
         return bail(fail(d, cudaGetLastError(), "cudaHostAlloc(counters)"));
     std::memset(d->h_ctr, 0, sizeof(DevCounters));
@@ -755,6 +758,7 @@ int hetm_dev_close(hetm_dev* d) {
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
+    if (d->h_first) cudaFreeHost(d->h_first);
     for (auto& v : d->tpairs)
         for (auto& pr : v) {
             cudaEventDestroy(pr.first);
@@ -904,9 +908,8 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         if ((rc = dev_alloc(d, (void**)&d->d_tk, d->tk_cap * 8))) return rc;
     }
     cudaStream_t s = d->s_exec;
-    CK(d, cudaMemcpyAsync(&d->h_ctr->ticket, &d->d_ctr->ticket, 8, cudaMemcpyDeviceToHost, s));
-    CK(d, cudaStreamSynchronize(s));
-    const uint64_t first = d->h_ctr->ticket;
+    // first ticket of the batch, read after the batch's final sync (no extra host sync here)
+    CK(d, cudaMemcpyAsync(d->h_first, &d->d_ctr->ticket, 8, cudaMemcpyDeviceToHost, s));
     CK(d, cudaMemsetAsync(&d->d_ctr->oob, 0, sizeof(unsigned), s));
     // Pipelined pieces: the H2D of piece k+1 (s_in) overlaps the kernel on
     // piece k (s_exec), whose tickets/results return on s_out while later
@@ -976,6 +979,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         cudaEventElapsedTime(&mk, d->kp_ev[2 * k], d->kp_ev[2 * k + 1]);
         ms += mk;
     }
+    const uint64_t first = *d->h_first;
     hetm_batch_stats st{};
     st.n_tx = n_tx;
     st.committed = d->h_ctr->committed;
