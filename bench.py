@@ -118,6 +118,27 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# Random 16-B accesses on a 1 GiB footprint, measured on B200 (tools/microbench.cu,
+# profiles/r01_microbench_random_access.txt): L2-missing loads and read-modify-writes per second.
+RANDOM_LOAD_PER_S, RANDOM_RMW_PER_S = 42.6e9, 22.6e9
+
+
+def access_ceiling(tx_per_s, traffic, kernel_ms, peak):
+    """The bank kernel's access-pattern bound beside the copy roofline: a transfer
+    needs 4 random cell loads (P1) and 2 random RMWs of written cells (lock CAS,
+    then the 128-bit commit store hitting the same line) — no schedule of the
+    protocol issues fewer line fills.  Model time per tx = 4/load rate + 2/RMW rate."""
+    ceil = 1.0 / (4 / RANDOM_LOAD_PER_S + 2 / RANDOM_RMW_PER_S)
+    out = {"model": "4 random loads + 2 random RMWs per tx at the measured random-access rates",
+           "load_per_s": RANDOM_LOAD_PER_S, "rmw_per_s": RANDOM_RMW_PER_S,
+           "source": "profiles/r01_microbench_random_access.txt", "tx_per_s_ceiling": ceil,
+           "kernel_tx_per_s": tx_per_s, "frac": tx_per_s / ceil}
+    if traffic:
+        dram_gbs = traffic / (kernel_ms * 1e-3) / 1e9
+        out.update({"dram_gbs": dram_gbs, "dram_frac_of_peak": dram_gbs / peak})
+    return out
+
+
 NOMINAL_HBM_GBS = 8000.0  # north_star's nominal B200 HBM3e bandwidth (SURVEY.md §8d: report both fractions)
 
 
@@ -349,7 +370,9 @@ def run_ours(args):
                      "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": achieved / NOMINAL_HBM_GBS,
                      "traffic": measured_traffic("bank_batch_kernel"),
                      "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
-                     "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms},
+                     "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms,
+                     "access_pattern_ceiling": access_ceiling(B / (batch_ms * 1e-3), measured_traffic("bank_batch_kernel"),
+                                                              batch_ms, peak)},
         "validate_apply": {"kernel": "apply_kernel", "gbs_algorithmic": val_gbs,
                            "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
                            "log_gbs_per_gpu": 24 * (n_val / K / world) / (val_ms * 1e-3) / 1e9,

@@ -81,9 +81,9 @@ enum hetm_kernel_id {
 
 /* hetm_dev_clear_round flags. */
 #define HETM_CLEAR_RESET_TS 1u /* also zero the TS array (SPEC.md:421 literal reset) */
-#define HETM_CLEAR_ASYNC 2u    /* enqueue the bitmap reset behind the round's work without a
-                                  host sync; the conflict flag keeps accumulating until the
-                                  next synchronous clear (pipelined benchmark rounds) */
+#define HETM_CLEAR_ASYNC 2u    /* enqueue the reset (bitmaps, round flags, counter roll) behind
+                                  the round's work without a host sync (pipelined rounds); the
+                                  device state after it equals the synchronous clear's */
 
 /* hetm_dev_config.flags */
 #define HETM_CFG_NO_SHADOW 1u /* do not allocate devShadow (validation-only sweeps) */

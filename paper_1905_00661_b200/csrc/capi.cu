@@ -1677,41 +1677,24 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     cancel_prepare(d);  // staged but never merged: not part of the replica
     int rc = wait_round_work(d, d->s_merge);
     if (rc) return rc;
-    if (flags & HETM_CLEAR_ASYNC) {
-        cudaStream_t s = d->s_merge;
+    if (!(flags & HETM_CLEAR_ASYNC)) {
+        CK(d, cudaStreamSynchronize(d->s_val));
+        CK(d, cudaStreamSynchronize(d->s_exec));
+    }
+    // one kernel behind the round's work on s_merge (wait_round_work above);
+    // the next round's work waits for ev_round
+    cudaStream_t s = d->s_merge;
+    {
         cudaError_t e = launch_clear_round(d->d_rs, d->d_ws, d->rs_words, d->d_chunk, d->chunk_words, d->d_ctr,
                                            (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, d->geom, s);
         if (e != cudaSuccess) return fail(d, e, "clear_round");
-        if (flags & HETM_CLEAR_RESET_TS) {
-            cudaError_t er = launch_reset_ts(d->d_cells, d->W, d->geom, s);
-            if (er != cudaSuccess) return fail(d, er, "reset_ts");
-        }
-        CK(d, cudaEventRecord(d->ev_round, s));
-        d->arena_n = 0;
-        d->deferred.clear();
-        d->deferred_final = false;
-        d->round_applied = false;
-        d->round_tx = 0;
-        d->intake_open = true;
-        return HETM_OK;
     }
-    CK(d, cudaStreamSynchronize(d->s_val));
-    CK(d, cudaStreamSynchronize(d->s_exec));
-    cudaStream_t s = d->s_merge;
-    {
-        cudaError_t e = launch_roll_round(d->d_ctr, (flags & HETM_CLEAR_RESET_TS) ? 1 : 0, s);
-        if (e != cudaSuccess) return fail(d, e, "roll_round");
-    }
-    CK(d, cudaMemsetAsync(d->d_rs, 0, d->rs_words * 8, s));
-    CK(d, cudaMemsetAsync(d->d_ws, 0, d->rs_words * 8, s));
-    CK(d, cudaMemsetAsync(d->d_chunk, 0, d->chunk_words * 8, s));
-    CK(d, cudaMemsetAsync(&d->d_ctr->conflict, 0, 3 * sizeof(unsigned), s));
     if (flags & HETM_CLEAR_RESET_TS) {
         cudaError_t er = launch_reset_ts(d->d_cells, d->W, d->geom, s);
         if (er != cudaSuccess) return fail(d, er, "reset_ts");
     }
     CK(d, cudaEventRecord(d->ev_round, s));
-    d->h_ctr->conflict = 0;
+    if (!(flags & HETM_CLEAR_ASYNC)) d->h_ctr->conflict = 0;
     d->arena_n = 0;
     d->deferred.clear();
     d->deferred_final = false;

@@ -53,7 +53,6 @@ cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_
                                     uint32_t n_regions, uint64_t cap, int apply, DevCounters* ctr,
                                     unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
 // Round boundary: ts_floor = max(ts_floor, round_max_ts) (0 with reset_ts), round_max_ts = 0.
-cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s);
 // Winner store of the round's log: value of the entry whose ts equals the
 // cell's TS goes to dst[addr] (plain array) or, with dst == nullptr, to the
 // cell's value (rollback / shadow patch).

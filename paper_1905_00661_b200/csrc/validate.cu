@@ -433,22 +433,10 @@ cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& 
 // for the literal SPEC.md:421 TS reset), round_max_ts = 0.  Enqueued by both
 // the synchronous and the asynchronous clear so pipelined rounds keep an exact
 // floor without a host round trip.
-__global__ void roll_round_kernel(DevCounters* ctr, int reset_ts) {
-    const unsigned long long m = ctr->round_max_ts;
-    ctr->ts_floor = reset_ts ? 0ull : (m > ctr->ts_floor ? m : ctr->ts_floor);
-    ctr->round_max_ts = 0;
-    ctr->wlog_base = ctr->ticket;  // the next round's write-set log starts here
-    ctr->wlog_overflow = 0;
-}
-
-cudaError_t launch_roll_round(DevCounters* ctr, int reset_ts, cudaStream_t s) {
-    roll_round_kernel<<<1, 1, 0, s>>>(ctr, reset_ts);
-    return cudaGetLastError();
-}
-
-// Asynchronous clearRound in one launch: zero RS, WS and ChunkMap and roll the
-// round counters (roll_round_kernel's rule, by block 0) — one kernel instead of
-// three memsets + a roll on the round boundary of the pipelined bench step.
+// clearRound in one launch, stream-ordered behind the round's
+// work: zero RS, WS and ChunkMap, clear the round's conflict / nonmonotone /
+// out-of-shard flags and roll the round counters (block 0): TS floor = max ts
+// seen so far, the next round's write-set log starts at the current ticket.
 __global__ void clear_round_kernel(unsigned long long* rs, unsigned long long* ws, uint64_t rs_words,
                                    unsigned long long* chunk, uint64_t chunk_words, DevCounters* ctr, int reset_ts) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -457,6 +445,9 @@ __global__ void clear_round_kernel(unsigned long long* rs, unsigned long long* w
         ctr->round_max_ts = 0;
         ctr->wlog_base = ctr->ticket;
         ctr->wlog_overflow = 0;
+        ctr->conflict = 0;
+        ctr->nonmonotone = 0;
+        ctr->oob = 0;
     }
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rs_words; i += stride) {

@@ -266,15 +266,19 @@ def test_validate_permuted_delivery_orders(hetm, orc, dev_factory):
         d.close()
 
 
-def test_false_positive_1k(hetm, orc, dev_factory):
-    """device read word 0, host wrote word 127 -> conflict at 1 KiB."""
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_false_positive_1k(hetm, orc, dev_factory, asynchronous):
+    """SPEC.md:641: device read word 0, host wrote word 127 -> conflict at 1 KiB;
+    the clear (sync, or enqueued without a host sync) resets bitmaps and verdict."""
     d = dev_factory(1 << 17, rs_gran_bytes=1024)
     d.register_kernel(hetm.KERNEL_RW)
     d.execute_batch(hetm.KERNEL_RW, rw_txs(orc, [([0], [], [])]))
     log = np.array([(127, 1, 1)], dtype=hetm.LOG_ENTRY)
     d.stream_chunk(log)
     assert d.round_verdict()
-    d.clear_round()
+    d.clear_round(asynchronous=asynchronous)
+    d.sync()
+    assert d.bitmap_stats() == (0, 0, 0)
     d.execute_batch(hetm.KERNEL_RW, rw_txs(orc, [([0], [], [])]))
     log2 = np.array([(128, 1, 2)], dtype=hetm.LOG_ENTRY)
     d.stream_chunk(log2)
@@ -313,15 +317,16 @@ def test_empty_chunk_recorded(hetm, dev_factory):
     assert (hetm.H2D, hetm.TAG_LOG, 0) in d.transfer_log()
 
 
-def test_nonmonotone_ts_detected(hetm, dev_factory):
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_nonmonotone_ts_detected(hetm, dev_factory, asynchronous):
     d = dev_factory(64, rs_gran_bytes=8)
     d.stream_chunk(np.array([(1, 5, 100)], dtype=hetm.LOG_ENTRY))
     d.round_verdict()
-    d.clear_round()
+    d.clear_round(asynchronous=asynchronous)  # the TS floor rolls to 100 either way
     d.stream_chunk(np.array([(2, 6, 50)], dtype=hetm.LOG_ENTRY))
     with pytest.raises(hetm.NonMonotoneTsError):
         d.round_verdict()
-    d.clear_round(reset_ts=True)  # SPEC.md:421 literal reset
+    d.clear_round(reset_ts=True, asynchronous=asynchronous)  # SPEC.md:421 literal reset; the flag clears
     d.stream_chunk(np.array([(2, 6, 50)], dtype=hetm.LOG_ENTRY))
     d.round_verdict()
     assert d.raw_read(hetm.REPLICA_DEV, 2) == 6
