@@ -4,19 +4,23 @@
 // A bank transaction's writes are read-modify-writes with known deltas
 // (acct0 -= amount, acct1 += amount; acct2/acct3 only read), so the serial
 // execution of the batch in input order is a segmented prefix sum:
-//   1. per transaction (coalesced): one 32-bit key per access (the account)
-//      with the payload (4 i + k) << 1 | writer and the access's delta; the
-//      ticket and write-set log slots are written here too;
-//   2. CUB radix sort of the 4n (account, payload) pairs on the account bits
-//      only — the sort is stable, so each account's accesses stay in input
-//      order;
+//   1. per transaction (coalesced): one 32-bit key per written account with
+//      the payload (2 i + k) << 1 | writer and the access's delta, and the RS
+//      bits of the read-only accounts (probe-gated); the ticket and write-set log
+//      slots are written here too.  A traced batch keys all four accesses
+//      ((4 i + k) << 1 | writer): the trace records every read's pre-value;
+//   2. CUB radix sort of the 2n (4n) (account, payload) pairs on the account
+//      bits only — the sort is stable, so each account's accesses stay in
+//      input order;
 //   3. CUB inclusive scan-by-account of {delta, last writer}: the delta of an
 //      access is the transaction's net effect on that account (last write wins
 //      when acct0 == acct1), carried by the first slot naming the account;
 //   4. one pass over the sorted accesses: at the end of each account's segment
 //      the final value and version (lk_commit of the last writer's ticket) are
-//      stored and the WS / chunk bits set, at its start the RS bit.  With a
-//      trace armed, a read-only pass first records each access's pre-value.
+//      stored and the WS / chunk bits set, at its start the RS bit (bits
+//      warp-aggregated: the stream is sorted).
+//      With a trace armed, a read-only pass first records each access's
+//      pre-value.
 // Cost is independent of skew (no locks, no retries): at zipf 0.99 the
 // optimistic PR-STM kernel serializes ~10^5 commits on the hottest account.
 // The result is exactly the deterministic single-worker mode.
@@ -39,6 +43,7 @@ namespace {
 constexpr unsigned kSchedThreads = 256;
 constexpr unsigned long long kNone = ~0ull;
 constexpr uint32_t kNoLoc = 0xffffffffu;  // sort sentinel: accesses of rejected transactions
+constexpr unsigned kSeenLog = 11, kSeenSlots = 1u << kSeenLog;  // keys kernel: per-CTA RS filter (16 KiB)
 
 struct DeltaW {  // scan value: summed delta, last writing transaction (input index) or kNone
     unsigned long long d, w;
@@ -49,16 +54,19 @@ struct DeltaWOp {
     }
 };
 
-// Sort payload: access index a = 4 i + k (input order) << 1 | writer, where
-// writer marks the transaction's first slot naming an account it writes.
+// Sort payload: access index a = S i + k (input order) << 1 | writer, where
+// writer marks the transaction's first slot naming an account it writes and S
+// is the slots keyed per transaction (2: the written accounts; 4: all, traced).
 __device__ __forceinline__ uint32_t acc_of(uint32_t p) { return p >> 1; }
-__device__ __forceinline__ uint64_t tx_of(uint32_t p) { return p >> 3; }
+template <int S>
+__device__ __forceinline__ uint64_t tx_of(uint32_t p) { return p >> (S == 4 ? 3 : 2); }
 
+template <int S>
 struct DeltaOf {  // scan value of a sorted access: its precomputed delta + writer
     using result_type = DeltaW;
     const unsigned long long* delta;
     __device__ DeltaW operator()(uint32_t p) const {
-        return DeltaW{delta[acc_of(p)], (p & 1u) ? tx_of(p) : kNone};
+        return DeltaW{delta[acc_of(p)], (p & 1u) ? tx_of<S>(p) : kNone};
     }
 };
 
@@ -73,15 +81,25 @@ __device__ __forceinline__ void load_accts(const hetm_bank_tx* in, uint64_t i, u
     a[3] = (w23 >> 32) - base;
 }
 
-// Per transaction (coalesced): the 4 sort keys + payloads, the per-access
+// Per transaction (coalesced): the S sort keys + payloads, the per-access
 // deltas (the tx's net effect on an account — the last write wins, acct1
 // after acct0 — on the first slot naming it), its ticket and write-set log
-// slots; a rejected (out-of-shard) transaction gets sentinel keys, no ticket
-// and empty log slots.
+// slots, and (S = 2) the RS bits of its read-only accounts; a rejected
+// (out-of-shard) transaction gets sentinel keys, no ticket, no bits and empty
+// log slots.
+template <int S>
 __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ in, uint64_t n,
                                   uint32_t* __restrict__ locs, uint32_t* __restrict__ pay,
                                   unsigned long long* __restrict__ delta, unsigned long long* __restrict__ tickets,
                                   const unsigned long long* first, DevCounters* ctr) {
+    // RS bits this CTA already set (hashed by bit, the full bit index stored:
+    // a hit is exact): hot read-only accounts of a skewed batch then cost one
+    // atomic per CTA instead of a queue of them on cleared bitmaps.
+    __shared__ unsigned long long seen[kSeenSlots];
+    if (S == 2) {
+        for (unsigned q = threadIdx.x; q < kSeenSlots; q += blockDim.x) seen[q] = ~0ull;
+        __syncthreads();
+    }
     const unsigned long long t0 = *first, wbase = ld_relaxed(&ctr->wlog_base);
     unsigned oob = 0;
     unsigned long long commits = 0;
@@ -89,6 +107,17 @@ __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ 
         uint64_t a[4], amount;
         load_accts(in, i, v.base, a, amount);
         const bool ok = a[0] < v.size_words && a[1] < v.size_words && a[2] < v.size_words && a[3] < v.size_words;
+        if (S == 2 && ok) {  // RS of the read-only accounts (the sorted written ones: commit kernel)
+#pragma unroll
+            for (int k = 2; k < 4; ++k) {
+                const uint64_t b = a[k] >> v.gran_shift;
+                unsigned long long& slot = seen[(b * 0x9e3779b97f4a7c15ull) >> (64 - kSeenLog)];
+                if (a[k] != a[0] && a[k] != a[1] && slot != b) {
+                    if (!test_bit(v.rs, b)) set_bit(v.rs, b);
+                    slot = b;
+                }
+            }
+        }
         const unsigned long long t = t0 + i;
         oob |= !ok;
         commits += ok;
@@ -96,15 +125,15 @@ __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ 
         wlog_put(v, wbase, t, 0, ok ? (uint32_t)a[0] : ~0u);
         wlog_put(v, wbase, t, 1, ok ? (uint32_t)a[1] : ~0u);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < S; ++k) {
             bool first_slot = true;
 #pragma unroll
             for (int q = 0; q < k; ++q) first_slot &= a[q] != a[k];
             const unsigned long long d = !first_slot ? 0ull : a[k] == a[1] ? amount : a[k] == a[0] ? 0ull - amount : 0ull;
             const bool writer = first_slot && (a[k] == a[0] || a[k] == a[1]);
-            locs[4 * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
-            pay[4 * i + k] = (uint32_t)(4 * i + k) << 1 | (uint32_t)writer;
-            delta[4 * i + k] = d;
+            locs[S * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
+            pay[S * i + k] = (uint32_t)(S * i + k) << 1 | (uint32_t)writer;
+            delta[S * i + k] = d;
         }
     }
     if (__any_sync(0xffffffffu, oob) && lane_id() == 0) atomicOr(&ctr->oob, 1u);
@@ -127,12 +156,12 @@ __global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t loc = locs[j];
         if (loc == kNoLoc) continue;
-        const uint64_t i = tx_of(pay[j]);
+        const uint64_t i = tx_of<4>(pay[j]);
         const int k = (int)(acc_of(pay[j]) & 3);
         // pre-value: exclusive of this transaction's own delta, which sits on its
         // first slot naming the account (this entry or an earlier one of tx i)
         uint64_t jj = j;
-        while (jj > 0 && locs[jj - 1] == loc && tx_of(pay[jj - 1]) == i) --jj;
+        while (jj > 0 && locs[jj - 1] == loc && tx_of<4>(pay[jj - 1]) == i) --jj;
         const unsigned long long pre = v.cells[loc].value + incl[jj].d - delta[acc_of(pay[jj])];
         unsigned long long* r = v.trace + i * kTraceWords;
         if (k == 0) r[0] = t0 + i;
@@ -147,30 +176,33 @@ __global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__
 }
 
 // Per sorted access: RS at each account's first access, the final value and
-// version + WS / ChunkMap at the last one if the account was written.  The
-// bitmap words are probed first (most are set already: RS/WS/ChunkMap are
-// L2-resident), so only first-time bits cost an atomic.
+// version + WS / ChunkMap at its last one if the account was written.  A warp
+// walks 32 consecutive sorted accesses, so its bitmap bits arrive in word
+// order: each run of lanes on one bitmap word issues a single probe-gated
+// atomic (the first batch of a round, on cleared bitmaps, otherwise queues
+// thousands of atomics on the words of hot accounts).
+template <int S>
 __global__ void sched_commit_kernel(ShardView v, uint64_t n4, const uint32_t* __restrict__ locs,
                                     const DeltaW* __restrict__ incl, const unsigned long long* first) {
     const unsigned long long t0 = *first;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t loc = locs[j];
-        if (loc == kNoLoc) continue;
-        const bool seg_first = j == 0 || locs[j - 1] != loc;
-        const bool seg_last = j + 1 == n4 || locs[j + 1] != loc;
-        if (seg_first) {  // every access reads (RS = reads U writes)
-            const uint64_t b = loc >> v.gran_shift;
-            if (!test_bit(v.rs, b)) set_bit(v.rs, b);
-        }
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n4; base += stride) {
+        const uint64_t j = base + lane_id();  // warp-uniform loop: the bitmap sets are warp-collective
+        const uint32_t loc = j < n4 ? locs[j] : kNoLoc;
+        const bool live = loc != kNoLoc;
+        const bool seg_first = live && (j == 0 || locs[j - 1] != loc);
+        const bool seg_last = live && (j + 1 == n4 || locs[j + 1] != loc);
+        bool wrote = false;
         if (seg_last) {
             const DeltaW x = incl[j];
             if (x.w != kNone) {
                 st_pair(&v.cells[loc], v.cells[loc].value + x.d, lk_commit(t0 + x.w));
-                const uint64_t b = loc >> v.gran_shift, c = loc >> v.chunk_shift;
-                if (!test_bit(v.ws, b)) set_bit(v.ws, b);
-                if (!test_bit(v.chunk, c)) set_bit(v.chunk, c);
+                wrote = true;
             }
         }
+        warp_set_bits_sorted(v.rs, (uint64_t)loc >> v.gran_shift, seg_first);  // every access reads
+        warp_set_bits_sorted(v.ws, (uint64_t)loc >> v.gran_shift, wrote);
+        warp_set_bits_sorted(v.chunk, (uint64_t)loc >> v.chunk_shift, wrote);
     }
 }
 
@@ -246,7 +278,7 @@ size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words) {
     size_t a = 0, b = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n4, 0, end_bit);
-    auto vi = thrust::make_transform_iterator((const uint32_t*)nullptr, DeltaOf{nullptr});
+    auto vi = thrust::make_transform_iterator((const uint32_t*)nullptr, DeltaOf<4>{nullptr});
     cub::DeviceScan::InclusiveScanByKey(nullptr, b, (const uint32_t*)nullptr, vi, (DeltaW*)nullptr, DeltaWOp{},
                                         (int64_t)n4);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -292,7 +324,7 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
                 cudaKernelNodeParams kp{};
                 if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel &&
                     cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
-                    kp.func == reinterpret_cast<void*>(sched_keys_kernel)) {
+                    kp.func == reinterpret_cast<void*>(sched_keys_kernel<2>)) {
                     graph->keys_node = nd;
                     auto& a = graph->keys_args;
                     void* dst[9] = {&a.v, &a.in, &a.n, &a.locs, &a.pay, &a.delta, &a.tickets, &a.first, &a.ctr};
@@ -321,14 +353,18 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
             graph->ctr = ctr;
         }
         // sched_keys_kernel(v, in, n, locs, pay, delta, tickets, first, ctr): patch in + tickets
-        graph->keys_args.in = d_in;
-        graph->keys_args.tickets = d_tickets;
-        cudaError_t e = cudaGraphExecKernelNodeSetParams(graph->exec, graph->keys_node, &graph->keys_params);
-        if (e != cudaSuccess) return e;
+        if (graph->keys_args.in != d_in || graph->keys_args.tickets != d_tickets) {
+            graph->keys_args.in = d_in;
+            graph->keys_args.tickets = d_tickets;
+            cudaError_t e = cudaGraphExecKernelNodeSetParams(graph->exec, graph->keys_node, &graph->keys_params);
+            if (e != cudaSuccess) return e;
+        }
         return cudaGraphLaunch(graph->exec, s);
     }
     if (n >= (1ull << 29)) return cudaErrorInvalidValue;  // 4n << 1 payloads fit 32 bits
-    const uint64_t n4 = 4 * n;
+    // keyed slots: the two written accounts, or all four accesses for a trace
+    const int S = v.trace ? 4 : 2;
+    const uint64_t n4 = (uint64_t)S * n;
     const int end_bit = (int)std::min<uint32_t>(32, bits_for(v.size_words) + 1);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     char* p = static_cast<char*>(temp);
@@ -345,16 +381,25 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
     const unsigned grid_tx = grid_for(n, kSchedThreads, 8, g.sm_count);
     const unsigned grid_acc = grid_for(n4, kSchedThreads, 8, g.sm_count);
     sched_ticket_kernel<<<1, 1, 0, s>>>(ctr, n, first);
-    sched_keys_kernel<<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
+    if (S == 4) sched_keys_kernel<4><<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
+    else sched_keys_kernel<2><<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
     cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, locs, locs_s, pay, pay_s, (int64_t)n4, 0,
                                                     end_bit, s);
     if (e != cudaSuccess) return e;
-    auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf{delta});
-    e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
-                                             (int64_t)n4, cub::Equality(), s);
-    if (e != cudaSuccess) return e;
-    if (v.trace) sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, locs_s, pay_s, delta, incl, first);
-    sched_commit_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
+    if (S == 4) {
+        auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf<4>{delta});
+        e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
+                                                 (int64_t)n4, cub::Equality(), s);
+        if (e != cudaSuccess) return e;
+        sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, locs_s, pay_s, delta, incl, first);
+        sched_commit_kernel<4><<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
+    } else {
+        auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf<2>{delta});
+        e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
+                                                 (int64_t)n4, cub::Equality(), s);
+        if (e != cudaSuccess) return e;
+        sched_commit_kernel<2><<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
+    }
     return cudaGetLastError();
 }
 

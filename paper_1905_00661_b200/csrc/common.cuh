@@ -167,6 +167,26 @@ __device__ __forceinline__ bool test_bit(const unsigned long long* words, uint64
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Warp-collective (all 32 lanes): set bit `bit` of `words` where `pred`, for
+// lanes whose bits arrive in NONDECREASING word order across the warp (a
+// sorted stream): each contiguous run of lanes naming the same word ORs its
+// masks together and its first lane issues one probe-gated atomic.  Lanes with
+// pred false split runs but stay correct.
+__device__ __forceinline__ void warp_set_bits_sorted(unsigned long long* words, uint64_t bit, bool pred) {
+    const unsigned lane = lane_id();
+    const uint64_t w = pred ? bit >> 6 : ~0ull;
+    unsigned long long m = pred ? 1ull << (bit & 63) : 0ull;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // suffix OR within the run
+        const uint64_t wd = __shfl_down_sync(0xffffffffu, w, d);
+        const unsigned long long md = __shfl_down_sync(0xffffffffu, m, d);
+        if (lane + d < 32 && wd == w) m |= md;
+    }
+    const uint64_t wprev = __shfl_up_sync(0xffffffffu, w, 1);
+    if (pred && (lane == 0 || wprev != w) && (words[w] & m) != m) atomicOr(&words[w], m);
+}
+
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

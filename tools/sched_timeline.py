@@ -16,16 +16,19 @@ d.register_kernel(hetm.KERNEL_BANK)
 d.set_schedule(hetm.SCHED_SCAN)
 d.upload(hetm.REPLICA_DEV, 0, np.full(W, 1000, np.uint64))
 tk = torch.empty(n, dtype=torch.int64, device="cuda")
-for alpha in (0.0, 0.99):
+cases = [(0.0, False), (0.99, False)] + ([(0.0, True), (0.99, True)] if "--first" in sys.argv else [])
+for alpha, first in cases:
     b = torch.from_numpy(hetm.gen_bank_batch(5, n, 0, W, zipf=alpha).view(np.uint8)).cuda()
     for _ in range(3):
         d.execute_batch_dptr(hetm.KERNEL_BANK, b.data_ptr(), n, tk.data_ptr())
     d.sync()
+    if first:  # the first batch of a round (bitmaps just cleared)
+        d.clear_round()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         d.execute_batch_dptr(hetm.KERNEL_BANK, b.data_ptr(), n, tk.data_ptr())
         d.sync()
     d.clear_round()
-    print(f"== alpha {alpha}")
+    print(f"== alpha {alpha}{' (first batch of the round)' if first else ''}")
     ks = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     if ks:
         t0 = min(e.time_range.start for e in ks)
