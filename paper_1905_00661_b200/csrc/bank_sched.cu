@@ -111,10 +111,10 @@ __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ 
 #pragma unroll
             for (int k = 2; k < 4; ++k) {
                 const uint64_t b = a[k] >> v.gran_shift;
-                unsigned long long& slot = seen[(b * 0x9e3779b97f4a7c15ull) >> (64 - kSeenLog)];
-                if (a[k] != a[0] && a[k] != a[1] && slot != b) {
+                unsigned long long* slot = &seen[(b * 0x9e3779b97f4a7c15ull) >> (64 - kSeenLog)];
+                if (a[k] != a[0] && a[k] != a[1] && atomicAdd(slot, 0ull) != b) {  // one 64-bit word: exact
                     if (!test_bit(v.rs, b)) set_bit(v.rs, b);
-                    slot = b;
+                    atomicExch(slot, b);
                 }
             }
         }
