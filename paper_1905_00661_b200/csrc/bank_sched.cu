@@ -44,6 +44,8 @@ constexpr unsigned kSchedThreads = 256;
 constexpr unsigned long long kNone = ~0ull;
 constexpr uint32_t kNoLoc = 0xffffffffu;  // sort sentinel: accesses of rejected transactions
 constexpr unsigned kSeenLog = 11, kSeenSlots = 1u << kSeenLog;  // keys kernel: per-CTA RS filter (16 KiB)
+constexpr int kCommitU = 4;                                      // commit kernel: 32-access runs per warp sweep
+constexpr int kKeysU = 2;                                        // keys kernel: transactions per thread per sweep
 
 struct DeltaW {  // scan value: summed delta, last writing transaction (input index) or kNone
     unsigned long long d, w;
@@ -103,37 +105,48 @@ __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ 
     const unsigned long long t0 = *first, wbase = ld_relaxed(&ctr->wlog_base);
     unsigned oob = 0;
     unsigned long long commits = 0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t a[4], amount;
-        load_accts(in, i, v.base, a, amount);
-        const bool ok = a[0] < v.size_words && a[1] < v.size_words && a[2] < v.size_words && a[3] < v.size_words;
-        if (S == 2 && ok) {  // RS of the read-only accounts (the sorted written ones: commit kernel)
+    // kKeysU transactions per thread per sweep, their records loaded up front
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * kKeysU) {
+        uint64_t aa[kKeysU][4], am[kKeysU];
 #pragma unroll
-            for (int k = 2; k < 4; ++k) {
-                const uint64_t b = a[k] >> v.gran_shift;
-                unsigned long long* slot = &seen[(b * 0x9e3779b97f4a7c15ull) >> (64 - kSeenLog)];
-                if (a[k] != a[0] && a[k] != a[1] && atomicAdd(slot, 0ull) != b) {  // one 64-bit word: exact
-                    if (!test_bit(v.rs, b)) set_bit(v.rs, b);
-                    atomicExch(slot, b);
+        for (int u = 0; u < kKeysU; ++u)
+            if (i0 + u * stride < n) load_accts(in, i0 + u * stride, v.base, aa[u], am[u]);
+#pragma unroll
+        for (int u = 0; u < kKeysU; ++u) {
+            const uint64_t i = i0 + u * stride;
+            if (i >= n) break;
+            const uint64_t(&a)[4] = aa[u];
+            const uint64_t amount = am[u];
+            const bool ok = a[0] < v.size_words && a[1] < v.size_words && a[2] < v.size_words && a[3] < v.size_words;
+            if (S == 2 && ok) {  // RS of the read-only accounts (the sorted written ones: commit kernel)
+#pragma unroll
+                for (int k = 2; k < 4; ++k) {
+                    const uint64_t b = a[k] >> v.gran_shift;
+                    unsigned long long* slot = &seen[(b * 0x9e3779b97f4a7c15ull) >> (64 - kSeenLog)];
+                    if (a[k] != a[0] && a[k] != a[1] && atomicAdd(slot, 0ull) != b) {  // one 64-bit word: exact
+                        if (!test_bit(v.rs, b)) set_bit(v.rs, b);
+                        atomicExch(slot, b);
+                    }
                 }
             }
-        }
-        const unsigned long long t = t0 + i;
-        oob |= !ok;
-        commits += ok;
-        tickets[i] = ok ? t : kNone;
-        wlog_put(v, wbase, t, 0, ok ? (uint32_t)a[0] : ~0u);
-        wlog_put(v, wbase, t, 1, ok ? (uint32_t)a[1] : ~0u);
+            const unsigned long long t = t0 + i;
+            oob |= !ok;
+            commits += ok;
+            tickets[i] = ok ? t : kNone;
+            wlog_put(v, wbase, t, 0, ok ? (uint32_t)a[0] : ~0u);
+            wlog_put(v, wbase, t, 1, ok ? (uint32_t)a[1] : ~0u);
 #pragma unroll
-        for (int k = 0; k < S; ++k) {
-            bool first_slot = true;
+            for (int k = 0; k < S; ++k) {
+                bool first_slot = true;
 #pragma unroll
-            for (int q = 0; q < k; ++q) first_slot &= a[q] != a[k];
-            const unsigned long long d = !first_slot ? 0ull : a[k] == a[1] ? amount : a[k] == a[0] ? 0ull - amount : 0ull;
-            const bool writer = first_slot && (a[k] == a[0] || a[k] == a[1]);
-            locs[S * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
-            pay[S * i + k] = (uint32_t)(S * i + k) << 1 | (uint32_t)writer;
-            delta[S * i + k] = d;
+                for (int q = 0; q < k; ++q) first_slot &= a[q] != a[k];
+                const unsigned long long d = !first_slot ? 0ull : a[k] == a[1] ? amount : a[k] == a[0] ? 0ull - amount : 0ull;
+                const bool writer = first_slot && (a[k] == a[0] || a[k] == a[1]);
+                locs[S * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
+                pay[S * i + k] = (uint32_t)(S * i + k) << 1 | (uint32_t)writer;
+                delta[S * i + k] = d;
+            }
         }
     }
     if (__any_sync(0xffffffffu, oob) && lane_id() == 0) atomicOr(&ctr->oob, 1u);
@@ -184,25 +197,41 @@ __global__ void sched_trace_kernel(ShardView v, const hetm_bank_tx* __restrict__
 template <int S>
 __global__ void sched_commit_kernel(ShardView v, uint64_t n4, const uint32_t* __restrict__ locs,
                                     const DeltaW* __restrict__ incl, const unsigned long long* first) {
+    // A warp takes kCommitU consecutive 32-access runs per sweep and issues each
+    // stage's loads for all of them before using any (memory-level parallelism:
+    // the stages are dependent — account, then scan value, then cell).
+    constexpr int U = kCommitU;
     const unsigned long long t0 = *first;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n4; base += stride) {
-        const uint64_t j = base + lane_id();  // warp-uniform loop: the bitmap sets are warp-collective
-        const uint32_t loc = j < n4 ? locs[j] : kNoLoc;
-        const bool live = loc != kNoLoc;
-        const bool seg_first = live && (j == 0 || locs[j - 1] != loc);
-        const bool seg_last = live && (j + 1 == n4 || locs[j + 1] != loc);
-        bool wrote = false;
-        if (seg_last) {
-            const DeltaW x = incl[j];
-            if (x.w != kNone) {
-                st_pair(&v.cells[loc], v.cells[loc].value + x.d, lk_commit(t0 + x.w));
-                wrote = true;
-            }
+    const unsigned lane = lane_id();
+    const uint64_t sweep = (uint64_t)gridDim.x * blockDim.x * U;
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n4; base += sweep) {
+        uint32_t loc[U];
+        bool seg_first[U], seg_last[U], wrote[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = base + (uint64_t)u * 32 + lane;
+            loc[u] = j < n4 ? locs[j] : kNoLoc;
+            const uint32_t prev = j > 0 && j - 1 < n4 ? locs[j - 1] : kNoLoc;
+            const uint32_t next = j + 1 < n4 ? locs[j + 1] : kNoLoc;
+            seg_first[u] = loc[u] != kNoLoc && (j == 0 || prev != loc[u]);
+            seg_last[u] = loc[u] != kNoLoc && next != loc[u];
         }
-        warp_set_bits_sorted(v.rs, (uint64_t)loc >> v.gran_shift, seg_first);  // every access reads
-        warp_set_bits_sorted(v.ws, (uint64_t)loc >> v.gran_shift, wrote);
-        warp_set_bits_sorted(v.chunk, (uint64_t)loc >> v.chunk_shift, wrote);
+        DeltaW x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = seg_last[u] ? incl[base + (uint64_t)u * 32 + lane] : DeltaW{0, kNone};
+        uint64_t val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            wrote[u] = x[u].w != kNone;
+            val[u] = wrote[u] ? v.cells[loc[u]].value : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (wrote[u]) st_pair(&v.cells[loc[u]], val[u] + x[u].d, lk_commit(t0 + x[u].w));
+            warp_set_bits_sorted(v.rs, (uint64_t)loc[u] >> v.gran_shift, seg_first[u]);  // every access reads
+            warp_set_bits_sorted(v.ws, (uint64_t)loc[u] >> v.gran_shift, wrote[u]);
+            warp_set_bits_sorted(v.chunk, (uint64_t)loc[u] >> v.chunk_shift, wrote[u]);
+        }
     }
 }
 
