@@ -143,7 +143,9 @@ __global__ void sched_keys_kernel(ShardView v, const hetm_bank_tx* __restrict__ 
                 for (int q = 0; q < k; ++q) first_slot &= a[q] != a[k];
                 const unsigned long long d = !first_slot ? 0ull : a[k] == a[1] ? amount : a[k] == a[0] ? 0ull - amount : 0ull;
                 const bool writer = first_slot && (a[k] == a[0] || a[k] == a[1]);
-                locs[S * i + k] = ok ? (uint32_t)a[k] : kNoLoc;
+                // S = 2: slot 1 of a transfer onto its own account is dropped, so every
+                // live sorted access is a writer (the reduction commit relies on it)
+                locs[S * i + k] = ok && (S == 4 || first_slot) ? (uint32_t)a[k] : kNoLoc;
                 pay[S * i + k] = (uint32_t)(S * i + k) << 1 | (uint32_t)writer;
                 delta[S * i + k] = d;
             }
@@ -231,6 +233,61 @@ __global__ void sched_commit_kernel(ShardView v, uint64_t n4, const uint32_t* __
             warp_set_bits_sorted(v.rs, (uint64_t)loc[u] >> v.gran_shift, seg_first[u]);  // every access reads
             warp_set_bits_sorted(v.ws, (uint64_t)loc[u] >> v.gran_shift, wrote[u]);
             warp_set_bits_sorted(v.chunk, (uint64_t)loc[u] >> v.chunk_shift, wrote[u]);
+        }
+    }
+}
+
+// The untraced commit (S = 2, every live access a writer): no scan.  A
+// warp takes 32 consecutive sorted accesses (kCommitU runs per sweep); a
+// segmented prefix sum over the run's lanes (runs of one account are
+// contiguous: the stream is sorted) leaves each run's delta total on its last
+// lane, which adds it to the cell's value with one fire-and-forget RED.ADD —
+// addition commutes, so an account split over several runs (a hot account of
+// a skewed batch) needs no ordering between them — and, if the run ends the
+// account's segment, stores the version of the last writer (the stable sort
+// keeps input order, so that is the segment's last access).  No load of the
+// cell: the serial input-order result is value + sum of deltas.
+__global__ void sched_commit_red_kernel(ShardView v, uint64_t n2, const uint32_t* __restrict__ locs,
+                                        const uint32_t* __restrict__ pay, const unsigned long long* __restrict__ delta,
+                                        const unsigned long long* first) {
+    constexpr int U = kCommitU;
+    const unsigned long long t0 = *first;
+    const unsigned lane = lane_id();
+    const uint64_t sweep = (uint64_t)gridDim.x * blockDim.x * U;
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n2; base += sweep) {
+        uint32_t loc[U], p[U];
+        bool seg_first[U], seg_last[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t j = base + (uint64_t)u * 32 + lane;
+            loc[u] = j < n2 ? locs[j] : kNoLoc;
+            p[u] = j < n2 ? pay[j] : 0u;
+            const uint32_t prev = j > 0 && j - 1 < n2 ? locs[j - 1] : kNoLoc;
+            const uint32_t next = j + 1 < n2 ? locs[j + 1] : kNoLoc;
+            seg_first[u] = loc[u] != kNoLoc && (j == 0 || prev != loc[u]);
+            seg_last[u] = loc[u] != kNoLoc && next != loc[u];
+        }
+        unsigned long long d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[u] = loc[u] != kNoLoc ? delta[acc_of(p[u])] : 0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive prefix sum within the run
+                const uint32_t lo = __shfl_up_sync(0xffffffffu, loc[u], o);
+                const unsigned long long dd = __shfl_up_sync(0xffffffffu, d[u], o);
+                if (lane >= (unsigned)o && lo == loc[u]) d[u] += dd;
+            }
+            const uint32_t nxt = __shfl_down_sync(0xffffffffu, loc[u], 1);
+            const bool run_last = loc[u] != kNoLoc && (lane == 31 || nxt != loc[u]);
+            if (run_last) {
+                Cell* c = &v.cells[loc[u]];
+                if (d[u]) atomicAdd(reinterpret_cast<unsigned long long*>(&c->value), d[u]);  // RED.E.ADD.64
+                if (seg_last[u]) st_relaxed(&c->meta, lk_commit(t0 + tx_of<2>(p[u])));
+            }
+            warp_set_bits_sorted(v.rs, (uint64_t)loc[u] >> v.gran_shift, seg_first[u]);  // every access reads
+            warp_set_bits_sorted(v.ws, (uint64_t)loc[u] >> v.gran_shift, seg_last[u]);
+            warp_set_bits_sorted(v.chunk, (uint64_t)loc[u] >> v.chunk_shift, seg_last[u]);
         }
     }
 }
@@ -423,11 +480,7 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
         sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, locs_s, pay_s, delta, incl, first);
         sched_commit_kernel<4><<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
     } else {
-        auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf<2>{delta});
-        e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
-                                                 (int64_t)n4, cub::Equality(), s);
-        if (e != cudaSuccess) return e;
-        sched_commit_kernel<2><<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);
+        sched_commit_red_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, pay_s, delta, first);
     }
     return cudaGetLastError();
 }
