@@ -10,11 +10,13 @@ d = hetm.GpuDevice(W, rs_gran_bytes=1024)
 d.register_kernel(hetm.KERNEL_BANK)
 d.upload(hetm.REPLICA_DEV, 0, np.full(W, 1000, np.uint64))
 tk = torch.empty(n, dtype=torch.int64, device="cuda")
-txs = hetm.gen_bank_batch(70, n, 0, W, zipf=0.99)
+ZIPF = float(sys.argv[sys.argv.index("--zipf") + 1]) if "--zipf" in sys.argv else 0.99
+txs = hetm.gen_bank_batch(70, n, 0, W, zipf=ZIPF)
 bs = [torch.from_numpy(txs.view(np.uint8)).cuda() for _ in range(2)]
 ex = torch.cuda.ExternalStream(d.stream_handle(0))
-d.set_schedule(hetm.SCHED_SCAN)
-for mode in ["same", "alternate", "same", "alternate"]:
+for sched, mode in [(hetm.SCHED_SCAN, "same"), (hetm.SCHED_SCAN, "alternate"), (hetm.SCHED_OPTIMISTIC, "same"),
+                    (hetm.SCHED_SCAN, "same")]:
+    d.set_schedule(sched)
     ms = []
     for rep in range(6):
         b = bs[rep % 2] if mode == "alternate" else bs[0]
@@ -26,4 +28,4 @@ for mode in ["same", "alternate", "same", "alternate"]:
         d.sync()
         d.clear_round()
         ms.append(e0.elapsed_time(e1))
-    print(mode, ["%.3f" % m for m in ms])
+    print("scan" if sched == hetm.SCHED_SCAN else "optimistic", mode, ["%.3f" % m for m in ms])
