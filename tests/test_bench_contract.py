@@ -32,6 +32,8 @@ def test_bench_line_has_the_contract_keys():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and r["traffic"]
+    ac = r["access_pattern_ceiling"]  # the random-access bound beside the copy roofline
+    assert 0 < ac["frac"] < 1.5 and ac["tx_per_s_ceiling"] > 0 and 0 < ac["dram_frac_of_peak"] < 1
     c = d["cpu_baseline"]
     assert c["kind"] in ("port", "reference") and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
     e = d["e2e"]
