@@ -397,9 +397,11 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
 /* Bank batch schedule.  OPTIMISTIC: the PR-STM-style
  * phased kernel (lock / ticket / validate / write-back, retries on conflict).
  * SCAN: an abort-free execution of the batch in input order (ticket = first +
- * input index): a radix sort of the accesses by account + a segmented scan
- * of the transfers' deltas; its cost does not grow with skew, while the
- * optimistic kernel serializes every commit on a hot account.  AUTO (default):
+ * input index): a radix sort of the written accounts + a segmented sum of
+ * the transfers' deltas per account (applied with commutative adds; a traced
+ * batch runs a segmented scan for every access's pre-value); its cost does not
+ * grow with skew, while the optimistic kernel serializes every commit on a hot
+ * account.  AUTO (default):
  * host-buffer batches take SCAN when a sample of the inputs predicts a chain
  * of >= 768 conflicting commits on one account (HETM_SCHED_CHAIN); device-
  * pointer batches follow the same estimate of an EARLIER device batch of the
