@@ -936,18 +936,23 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         CK(d, cudaMemsetAsync(d->d_trace, 0xff, n_tx * kTraceWords * 8, s));  // ~0: did not commit
         trace = d->d_trace;
     }
-    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
-                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
     const char* in_h = static_cast<const char*>(inputs);
     char* in_d = static_cast<char*>(d->d_in);
+    // every piece's H2D is queued first: the copies do not depend on the
+    // schedule, so AUTO's host-side sample below runs while they stream (d_in
+    // is free: the previous batch of this handle ended with a stream sync)
     for (uint64_t k = 0; k < P; ++k) {
         const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
-        if (m) {
-            CK(d, cudaMemcpyAsync(in_d + lo * rec_bytes, in_h + lo * rec_bytes, m * rec_bytes, cudaMemcpyHostToDevice,
-                                  d->s_in));
-            CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
-            CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
-        }
+        if (!m) continue;
+        CK(d, cudaMemcpyAsync(in_d + lo * rec_bytes, in_h + lo * rec_bytes, m * rec_bytes, cudaMemcpyHostToDevice,
+                              d->s_in));
+        CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
+    }
+    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
+                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
+    for (uint64_t k = 0; k < P; ++k) {
+        const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
+        if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
         CK(d, cudaEventRecord(d->kp_ev[2 * k], s));
         if ((rc = enqueue_batch(d, kernel_id, in_d + lo * rec_bytes, m, d->d_tk + lo,
                                 results_out ? d->d_res + lo : nullptr, s, k == 0,
