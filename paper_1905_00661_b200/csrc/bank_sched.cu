@@ -3,24 +3,25 @@
 //
 // A bank transaction's writes are read-modify-writes with known deltas
 // (acct0 -= amount, acct1 += amount; acct2/acct3 only read), so the serial
-// execution of the batch in input order is a segmented prefix sum:
+// execution of the batch in input order is a per-account sum of deltas:
 //   1. per transaction (coalesced): one 32-bit key per written account with
-//      the payload (2 i + k) << 1 | writer and the access's delta, and the RS
-//      bits of the read-only accounts (probe-gated); the ticket and write-set log
-//      slots are written here too.  A traced batch keys all four accesses
-//      ((4 i + k) << 1 | writer): the trace records every read's pre-value;
-//   2. CUB radix sort of the 2n (4n) (account, payload) pairs on the account
-//      bits only — the sort is stable, so each account's accesses stay in
-//      input order;
-//   3. CUB inclusive scan-by-account of {delta, last writer}: the delta of an
-//      access is the transaction's net effect on that account (last write wins
-//      when acct0 == acct1), carried by the first slot naming the account;
-//   4. one pass over the sorted accesses: at the end of each account's segment
-//      the final value and version (lk_commit of the last writer's ticket) are
-//      stored and the WS / chunk bits set, at its start the RS bit (bits
-//      warp-aggregated: the stream is sorted).
-//      With a trace armed, a read-only pass first records each access's
-//      pre-value.
+//      the payload (2 i + k) << 1 | writer and the access's delta (the tx's
+//      net effect on the account: last write wins when acct0 == acct1, whose
+//      second slot is then dropped), and the RS bits of the read-only
+//      accounts (probe-gated, per-CTA filter); the ticket and write-set log
+//      slots are written here too;
+//   2. CUB radix sort of the 2n (account, payload) pairs on the account bits
+//      only — the sort is stable, so each account's accesses stay in input
+//      order;
+//   3. one pass over the sorted accesses (sched_commit_red_kernel): per warp
+//      run a segmented shuffle sum of the deltas, added to the cell with one
+//      RED.ADD (commutative: a hot account spread over many runs needs no
+//      order); at each account's segment end the version of its last writer
+//      (lk_commit of its ticket) is stored; RS / WS / ChunkMap bits are set
+//      warp-aggregated (the stream is sorted).
+// A traced batch keys all four accesses ((4 i + k) << 1 | writer), runs a CUB
+// inclusive scan-by-account of {delta, last writer}, records every access's
+// pre-value (sched_trace_kernel) and commits from the scan (sched_commit_kernel).
 // Cost is independent of skew (no locks, no retries): at zipf 0.99 the
 // optimistic PR-STM kernel serializes ~10^5 commits on the hottest account.
 // The result is exactly the deterministic single-worker mode.
