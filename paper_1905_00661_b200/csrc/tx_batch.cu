@@ -249,10 +249,12 @@ static unsigned grid_for(uint64_t n, int threads, int blocks_per_sm, int sms) {
 cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                               DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    static const int ko = [] {
-        const char* e = std::getenv("HETM_KNOCKOUT");  // profiling experiments only
+#ifdef HETM_EXPERIMENTS
+    static const int ko = [] {  // phase knockouts (make EXPERIMENTS=1): profiling only, some incorrect
+        const char* e = std::getenv("HETM_KNOCKOUT");
         return e ? std::atoi(e) : 0;
     }();
+#endif
     static const int bps = [] {  // occupancy experiments only
         const char* e = std::getenv("HETM_TX_BLOCKS_PER_SM");
         return e ? std::atoi(e) : 0;
@@ -264,10 +266,14 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         bank_batch_kernel<KO_TRACE><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
         return cudaGetLastError();
     }
+#ifdef HETM_EXPERIMENTS
     switch (ko) {
         HETM_KO_CASE(4) HETM_KO_CASE(8) HETM_KO_CASE(16) HETM_KO_CASE(64) HETM_KO_CASE(128) HETM_KO_CASE(256) HETM_KO_CASE(512) HETM_KO_CASE(1024) HETM_KO_CASE(1536)
         default: bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
     }
+#else
+    bank_batch_kernel<0><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+#endif
 #undef HETM_KO_CASE
     return cudaGetLastError();
 }

@@ -1,4 +1,5 @@
-"""Per-phase cycle breakdown of the bank batch kernel (run with HETM_KNOCKOUT=128)."""
+"""Per-phase cycle breakdown of the bank batch kernel (run with HETM_KNOCKOUT=128 on the
+experiments build: make -C paper_1905_00661_b200/csrc clean all EXPERIMENTS=1)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

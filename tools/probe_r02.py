@@ -1,4 +1,5 @@
-"""Kernel probes for tuning (not product code).
+"""Kernel probes for tuning (not product code).  HETM_KNOCKOUT variants need the experiments
+build: make -C paper_1905_00661_b200/csrc clean all EXPERIMENTS=1.
 
     python tools/probe_r02.py bank            # bank batch kernel ms (HETM_KNOCKOUT selects variants)
     python tools/probe_r02.py val [log2 n]    # validate+apply ms per chunk (HETM_VAL_WINDOW_LOG2)
