@@ -191,6 +191,7 @@ struct hetm_dev {
     uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
     int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
+    uint32_t auto_scan_left = 0;            // AUTO feedback: host-input bank batches still to run as SCAN
     uint32_t* h_hot = nullptr;              // device-side hot-spot estimate (mapped host word)
     uint32_t* d_hot = nullptr;
     cudaStream_t s_est = nullptr;           // the estimator runs off the batch's critical path
@@ -366,6 +367,9 @@ uint64_t sched_chain() {
 // A count of >= 3 in the sample is required: chance pairs are common under
 // uniform access (8 K sampled accounts over 2^26 meet ~0.5 times).
 bool hot_chain(uint64_t best, uint64_t n, uint64_t S, uint64_t chain) { return best >= 3 && best * n / S >= chain; }
+
+constexpr uint64_t kAutoAbortRatio = 128;  // feedback: aborts per transaction above 1/128 ...
+constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 host-input bank batches as SCAN
 
 bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
     const uint64_t chain = sched_chain();
@@ -948,8 +952,10 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
                               d->s_in));
         CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
     }
-    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
-                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
+    const bool auto_bank = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx;
+    const bool feedback = auto_bank && d->auto_scan_left > 0;
+    if (feedback) --d->auto_scan_left;
+    const bool hot = auto_bank && (feedback || bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx));
     for (uint64_t k = 0; k < P; ++k) {
         const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
         if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
@@ -995,6 +1001,12 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     st.kernel_ms = ms;
     d->last_batch = st;
     if (stats) *stats = st;
+    // AUTO feedback: an optimistic bank batch that aborted more than 1 attempt per
+    // 128 transactions had conflict chains the sample did not predict (the zipf
+    // ~0.5 band: uniform batches abort ~0.2 %, SCAN wins from ~1 %,
+    // profiles/r01g_sched_crossover.txt); the next kAutoScanRun batches run as
+    // SCAN, then the optimistic kernel is tried again.
+    if (auto_bank && !hot && st.aborts * kAutoAbortRatio > n_tx) d->auto_scan_left = kAutoScanRun;
     if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
     if (st.livelocked) return HETM_ERR_LIVELOCK;
     return HETM_OK;
