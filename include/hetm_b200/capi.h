@@ -405,7 +405,8 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
  * host-buffer batches take SCAN when a sample of the inputs predicts a chain
  * of >= 768 conflicting commits on one account (HETM_SCHED_CHAIN), or for the
  * 15 batches after an optimistic batch aborted > 1/128 of its transactions
- * (then the optimistic kernel is tried again); device-
+ * (then the optimistic kernel is tried again; a device-pointer batch's aborts
+ * are judged at the caller's next counters read / verdict); device-
  * pointer batches follow the same estimate of an EARLIER device batch of the
  * handle (a one-CTA kernel samples each batch on a side stream into mapped
  * host memory, read by the next call without a sync), so a steady hot

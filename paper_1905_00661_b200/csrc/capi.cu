@@ -191,7 +191,8 @@ struct hetm_dev {
     uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
     int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
-    uint32_t auto_scan_left = 0;            // AUTO feedback: host-input bank batches still to run as SCAN
+    uint32_t auto_scan_left = 0;            // AUTO feedback: bank batches still to run as SCAN
+    uint64_t dptr_feedback_n = 0;           // last batch: an optimistic AUTO device-pointer bank batch of n tx
     uint32_t* h_hot = nullptr;              // device-side hot-spot estimate (mapped host word)
     uint32_t* d_hot = nullptr;
     cudaStream_t s_est = nullptr;           // the estimator runs off the batch's critical path
@@ -312,8 +313,17 @@ int sync_all(hetm_dev* d) {
     return HETM_OK;
 }
 
+constexpr uint64_t kAutoAbortRatio = 128;  // AUTO feedback: aborts per transaction above 1/128 ...
+constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches as SCAN
+
 int read_counters(hetm_dev* d) {
     CK(d, cudaMemcpy(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
+    // AUTO feedback for device-pointer batches: their stats are only seen when the
+    // caller syncs (round verdict, counters); the last batch's, if it ran optimistic
+    if (d->dptr_feedback_n) {
+        if (d->h_ctr->aborts * kAutoAbortRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
+        d->dptr_feedback_n = 0;
+    }
     return HETM_OK;
 }
 
@@ -367,9 +377,6 @@ uint64_t sched_chain() {
 // A count of >= 3 in the sample is required: chance pairs are common under
 // uniform access (8 K sampled accounts over 2^26 meet ~0.5 times).
 bool hot_chain(uint64_t best, uint64_t n, uint64_t S, uint64_t chain) { return best >= 3 && best * n / S >= chain; }
-
-constexpr uint64_t kAutoAbortRatio = 128;  // feedback: aborts per transaction above 1/128 ...
-constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 host-input bank batches as SCAN
 
 bool bank_batch_hot(const hetm_bank_tx* in, uint64_t n) {
     const uint64_t chain = sched_chain();
@@ -952,6 +959,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
                               d->s_in));
         CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
     }
+    d->dptr_feedback_n = 0;  // this batch's counters are judged below, not by a later read
     const bool auto_bank = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx;
     const bool feedback = auto_bank && d->auto_scan_left > 0;
     if (feedback) --d->auto_scan_left;
@@ -1772,12 +1780,15 @@ int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inp
             CK(d, cudaEventCreateWithFlags(&d->ev_est, cudaEventDisableTiming));
         }
         const uint32_t last = *reinterpret_cast<volatile uint32_t*>(d->h_hot);
-        hot = hot_chain(last, n_tx, bank_hot_estimate_sample(n_tx), sched_chain());
+        const bool feedback = d->auto_scan_left > 0;
+        if (feedback) --d->auto_scan_left;
+        hot = feedback || hot_chain(last, n_tx, bank_hot_estimate_sample(n_tx), sched_chain());
         CK(d, cudaEventRecord(d->ev_est, s));
         CK(d, cudaStreamWaitEvent(d->s_est, d->ev_est, 0));
         cudaError_t e = launch_bank_hot_estimate(static_cast<const hetm_bank_tx*>(d_inputs), n_tx, d->d_hot, d->s_est);
         if (e != cudaSuccess) return fail(d, e, "hot_estimate");
     }
+    d->dptr_feedback_n = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && !hot ? n_tx : 0;
     return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), d_results,
                          s, true, nullptr, hot);
 }
