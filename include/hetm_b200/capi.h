@@ -403,14 +403,13 @@ int hetm_dev_flush_l2(hetm_dev* dev, void* stream);
  * grow with skew, while the optimistic kernel serializes every commit on a hot
  * account.  AUTO (default):
  * host-buffer batches take SCAN when a sample of the inputs predicts a chain
- * of >= 768 conflicting commits on one account (HETM_SCHED_CHAIN), or for the
- * 15 batches after an optimistic batch aborted > 1/128 of its transactions
- * (then the optimistic kernel is tried again; a device-pointer batch's aborts
- * are judged at the caller's next counters read / verdict); device-
+ * of >= 768 conflicting commits on one account (HETM_SCHED_CHAIN); device-
  * pointer batches follow the same estimate of an EARLIER device batch of the
  * handle (a one-CTA kernel samples each batch on a side stream into mapped
  * host memory, read by the next call without a sync), so a steady hot
- * workload switches after its first batch.  The deterministic mode (HETM_CFG_DETERMINISTIC) always
+ * workload switches after its first batch; they also take SCAN for the 15
+ * batches after an optimistic one aborted > 1/128 of its transactions (judged
+ * at the caller's next counters read / verdict), then retry optimistic.  The deterministic mode (HETM_CFG_DETERMINISTIC) always
  * runs bank batches as SCAN: the same input-order serialization, in parallel.
  * Cache batches have a SCAN schedule too (a stable sort by set, then one
  * thread per set runs that set's transactions in input order with the set in

@@ -191,7 +191,7 @@ struct hetm_dev {
     uint64_t* trace_out = nullptr;          // armed by hetm_dev_trace_next_batch
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
     int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
-    uint32_t auto_scan_left = 0;            // AUTO feedback: bank batches still to run as SCAN
+    uint32_t auto_scan_left = 0;            // AUTO feedback: device-pointer bank batches still to run as SCAN
     uint64_t dptr_feedback_n = 0;           // last batch: an optimistic AUTO device-pointer bank batch of n tx
     uint32_t* h_hot = nullptr;              // device-side hot-spot estimate (mapped host word)
     uint32_t* d_hot = nullptr;
@@ -318,8 +318,12 @@ constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches a
 
 int read_counters(hetm_dev* d) {
     CK(d, cudaMemcpy(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
-    // AUTO feedback for device-pointer batches: their stats are only seen when the
-    // caller syncs (round verdict, counters); the last batch's, if it ran optimistic
+    // AUTO feedback for device-pointer batches, judged when the caller syncs the
+    // counters (verdict, stats): an optimistic bank batch that aborted more than 1
+    // attempt per 128 transactions had conflict chains the sample did not predict
+    // (the zipf ~0.5 band: uniform batches abort ~0.2-0.3 %, where SCAN wins 2x
+    // from ~1 %, profiles/r01g_sched_crossover.txt); the next kAutoScanRun
+    // device-pointer batches run as SCAN, then the optimistic kernel is tried again.
     if (d->dptr_feedback_n) {
         if (d->h_ctr->aborts * kAutoAbortRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
         d->dptr_feedback_n = 0;
@@ -959,11 +963,12 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
                               d->s_in));
         CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
     }
-    d->dptr_feedback_n = 0;  // this batch's counters are judged below, not by a later read
-    const bool auto_bank = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx;
-    const bool feedback = auto_bank && d->auto_scan_left > 0;
-    if (feedback) --d->auto_scan_left;
-    const bool hot = auto_bank && (feedback || bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx));
+    d->dptr_feedback_n = 0;  // the counters now hold this batch's (not judged by the feedback)
+    // (no abort feedback here: a host-buffer batch runs as pipelined pieces, on which
+    // the optimistic kernel's chains are shorter and SCAN's fixed costs higher —
+    // zipf 0.5: 0.68 vs 0.72 ms per 2^20, tools/auto_feedback_probe.py)
+    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
+                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
     for (uint64_t k = 0; k < P; ++k) {
         const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
         if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
@@ -1009,12 +1014,6 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     st.kernel_ms = ms;
     d->last_batch = st;
     if (stats) *stats = st;
-    // AUTO feedback: an optimistic bank batch that aborted more than 1 attempt per
-    // 128 transactions had conflict chains the sample did not predict (the zipf
-    // ~0.5 band: uniform batches abort ~0.2 %, SCAN wins from ~1 %,
-    // profiles/r01g_sched_crossover.txt); the next kAutoScanRun batches run as
-    // SCAN, then the optimistic kernel is tried again.
-    if (auto_bank && !hot && st.aborts * kAutoAbortRatio > n_tx) d->auto_scan_left = kAutoScanRun;
     if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
     if (st.livelocked) return HETM_ERR_LIVELOCK;
     return HETM_OK;

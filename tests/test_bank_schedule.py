@@ -87,29 +87,6 @@ def test_scan_rejects_out_of_shard_transactions(hetm, orc, dev_factory):
         d.execute_batch(hetm.KERNEL_BANK, txs)
 
 
-def test_auto_feedback_after_an_abort_heavy_optimistic_batch(hetm, orc, dev_factory):
-    """A dense uniform batch (16 K tx over 16 K words) is not hot by AUTO's sample but
-    aborts > 1/128 of its transactions optimistically: the next 15 host-input batches
-    run as SCAN (input order, no aborts), then the optimistic kernel is tried again.
-    Every batch replays bit-exactly on the oracle."""
-    W, n = 1 << 14, 1 << 14
-    d = dev_factory(W, rs_gran_bytes=8)
-    d.register_kernel(hetm.KERNEL_BANK)
-    init = np.full(W, 1000, np.uint64)
-    d.upload(hetm.REPLICA_DEV, 0, init)
-    ref = init.copy()
-    runs = []
-    for k in range(17):
-        txs = orc.gen_bank_batch(300 + k, n, 0, W)
-        r = d.execute_batch(hetm.KERNEL_BANK, txs)
-        orc.bank_replay(ref, txs, orc.order_by_ticket(r.tickets), 8, 16384)
-        runs.append((r.aborts, bool((np.diff(r.tickets.astype(np.int64)) == 1).all())))
-    assert (d.download(hetm.REPLICA_DEV) == ref).all()
-    assert runs[0][0] * 128 > n and not runs[0][1]            # optimistic, abort-heavy
-    assert all(a == 0 and seq for a, seq in runs[1:16])        # 15 SCAN batches
-    assert runs[16][0] > 0 and not runs[16][1]                 # re-probed optimistically
-
-
 def test_auto_feedback_device_pointer_batches(hetm, orc, dev_factory):
     """Device-pointer batches: the abort count of an optimistic AUTO batch is judged
     when the caller next reads the counters (a verdict or read_counters sync)."""
