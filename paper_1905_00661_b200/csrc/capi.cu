@@ -1782,14 +1782,21 @@ int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inp
         const bool feedback = d->auto_scan_left > 0;
         if (feedback) --d->auto_scan_left;
         hot = feedback || hot_chain(last, n_tx, bank_hot_estimate_sample(n_tx), sched_chain());
+    }
+    d->dptr_feedback_n = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && !hot ? n_tx : 0;
+    if (int rc = enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets),
+                               d_results, s, true, nullptr, hot))
+        return rc;
+    if (d->s_est && kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx) {
+        // the estimate for the next batch starts once this batch's kernels are done:
+        // its CTA (128 KiB of shared memory) must never hold an SM the batch's
+        // persistent CTAs need (it overlaps the validation phase instead)
         CK(d, cudaEventRecord(d->ev_est, s));
         CK(d, cudaStreamWaitEvent(d->s_est, d->ev_est, 0));
         cudaError_t e = launch_bank_hot_estimate(static_cast<const hetm_bank_tx*>(d_inputs), n_tx, d->d_hot, d->s_est);
         if (e != cudaSuccess) return fail(d, e, "hot_estimate");
     }
-    d->dptr_feedback_n = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && !hot ? n_tx : 0;
-    return enqueue_batch(d, kernel_id, d_inputs, n_tx, reinterpret_cast<unsigned long long*>(d_tickets), d_results,
-                         s, true, nullptr, hot);
+    return HETM_OK;
 }
 
 int hetm_dev_set_cache_geometry(hetm_dev* d, uint64_t base_word, uint64_t n_sets) {
