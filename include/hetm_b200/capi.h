@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define HETM_B200_ABI_VERSION 1
+#define HETM_B200_ABI_VERSION 2
 
 /* ---------------------------------------------------------------- status --
  * One code per hetm::HetmError subclass (types.hpp:38-48) plus device codes. */
@@ -272,14 +272,48 @@ int hetm_dev_or_bitmap(hetm_dev* dev, int which, const uint64_t* words, uint64_t
 int hetm_dev_open_intake(hetm_dev* dev);
 int hetm_dev_close_intake(hetm_dev* dev);
 /* streamChunk + validateChunk.  `entries` is a
- * HOST buffer borrowed until the next hetm_dev_round_verdict / hetm_dev_sync
- * (pinned memory gives an asynchronous DMA).  The chunk is appended to the
+ * HOST buffer borrowed until the chunk is delivered (hetm_dev_stream_chunk_ex
+ * handle; at the latest, the next hetm_dev_round_verdict / hetm_dev_sync;
+ * pinned memory gives an asynchronous DMA).  The chunk is appended to the
  * round's device log arena.  APPLY: validate + TS-guarded apply, ordered after
  * the device's in-flight batch.  VALIDATE_ONLY: early validation (SPEC.md:
  * 354-362), runs concurrently with execution; its apply is deferred to
  * hetm_dev_apply_log.  After close_intake -> HETM_ERR_ROUND_CLOSED. */
 int hetm_dev_stream_chunk(hetm_dev* dev, const hetm_log_entry* entries, uint64_t n,
                           int src_thread, uint64_t seq, int mode);
+/* Delivery handle of one streamed chunk (bus.hpp:51-56 `Delivery`, returned by
+ * Bus::streamChunk, bus.hpp:80; "completion observable via the
+ * handle").  `handle` orders every chunk of the device; the chunk is delivered
+ * when its H2D copy into the device log arena has completed, and from then on
+ * its host buffer belongs to the caller again (a producer can recycle a small
+ * pinned staging ring instead of pinning the whole round's log). */
+typedef struct hetm_delivery {
+    uint64_t seq;        /* LogChunk::seq (bus.hpp:47) */
+    uint64_t n_entries;  /* Delivery::nEntries (bus.hpp:53) */
+    uint64_t bytes;      /* wire bytes, 24 per entry (write_log.hpp:25) */
+    uint64_t handle;     /* completion id: hetm_dev_delivery_done / _wait */
+    int32_t src_thread;  /* LogChunk::sourceThread (bus.hpp:46) */
+    int32_t mode;        /* HETM_APPLY / HETM_VALIDATE_ONLY */
+} hetm_delivery;
+/* streamChunk with its delivery handle (out may be NULL).  `entries` is
+ * borrowed until the handle reports delivered.  Chunks of one src_thread are
+ * copied, validated and applied in call order (per-source FIFO). */
+int hetm_dev_stream_chunk_ex(hetm_dev* dev, const hetm_log_entry* entries, uint64_t n,
+                             int src_thread, uint64_t seq, int mode, hetm_delivery* out);
+/* Non-blocking: *done = 1 once the chunk's H2D copy has completed. */
+int hetm_dev_delivery_done(hetm_dev* dev, uint64_t handle, int* done);
+/* Blocks until the chunk's H2D copy has completed. */
+int hetm_dev_delivery_wait(hetm_dev* dev, uint64_t handle);
+/* Per-source accounting of the round's streamed chunks. */
+typedef struct hetm_source_stats {
+    uint64_t chunks, entries;
+    uint64_t last_seq, last_handle;
+} hetm_source_stats;
+int hetm_dev_source_stats(hetm_dev* dev, int src_thread, hetm_source_stats* out);
+/* Early-validation period (default k = 8): VALIDATE_ONLY chunks
+ * are validated in one launch every k chunks; an APPLY chunk, apply_log and the
+ * verdict validate the pending ones first.  k = 1 validates every chunk. */
+int hetm_dev_set_validation_period(hetm_dev* dev, uint32_t k);
 /* Apply every arena entry streamed VALIDATE_ONLY this round (final validation
  * phase re-validates them). */
 int hetm_dev_apply_log(hetm_dev* dev);

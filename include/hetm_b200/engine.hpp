@@ -20,7 +20,8 @@
 // Starvation guard: under FavorHost, after starvation_k
 // consecutive DeviceAborted rounds the next round admits only read-only host
 // transactions (RoundContext::updates_allowed), so the device commits.
-// Chunk buffers are pinned (hetm_host_alloc) and stay valid until the verdict.
+// Chunk buffers come from a pinned staging ring (hetm_host_alloc) and are
+// reused once their chunk is delivered (hetm_dev_stream_chunk_ex handle).
 #pragma once
 
 #include <algorithm>
@@ -51,6 +52,18 @@ struct EngineConfig {
     uint32_t starvation_k = 3;          // PolicyConfig.starvationK (>= 1)
     uint64_t chunk_entries = 1u << 16;  // entries per streamed LogChunk
     bool early_validation = true;       // stream chunks VALIDATE_ONLY during execution
+    uint32_t ev_period = 8;             // early validation every k streamed chunks
+    // hostCutoff: after the execution phase the host keeps
+    // committing while more than cutoff_chunks chunks of its log remain
+    // undelivered to the device; 0 = the basic algorithm (the host stops when
+    // the execution phase ends).  Default 4.
+    uint32_t cutoff_chunks = 4;
+    // Bus real-delay mode (bus.hpp:33-39 BusConfig): each streamed chunk also
+    // sleeps (latency + bytes / bytes_per_unit) * real_delay_us_per_unit us, a
+    // slow-link model for end-to-end experiments (0 = off: the real PCIe only).
+    double bus_latency_units = 2.0;
+    double bus_bytes_per_unit = 8192.0;
+    double bus_real_delay_us_per_unit = 0.0;
     bool optimized_abort = true;        // mergeAbortDevice: shadow + log (true) or chunk copy (false)
     bool keep_round_log = false;        // keep a copy of the last round's host log (checkers)
     bool early_merge = true;            // stage + speculatively apply the delta merge after execution
@@ -75,7 +88,9 @@ struct RoundReport {
     uint64_t chunks = 0;
     uint64_t bytes_merge = 0;       // merge / rollback transfer bytes (D2H + H2D + D2D)
     uint32_t dev_batches = 0;       // device batches executed in the execution phase
+    uint64_t cutoff_chunks = 0;     // chunks streamed while the host ran past the execution phase
     double exec_ms = 0, validate_ms = 0, merge_ms = 0;
+    double host_blocked_ms = 0;     // host admission paused (hostCutoff) until the round ended
     hetm_batch_stats batch{};
 
     /// (name, value, is_string) in the fixed SPEC.md:427 field order; json()
@@ -183,16 +198,23 @@ inline void check_rc(int rc, const char* what) {
     if (rc != HETM_OK) throw std::runtime_error(std::string(what) + ": " + hetm_strerror(rc));
 }
 
-class Engine {
+/// The round controller over a write log: this library's WriteLog or, with the
+/// reference headers, the reference's hetm::WriteLog (log_* in host_tm.hpp).
+template <class Log>
+class BasicEngine {
 public:
-    Engine(hetm_dev* dev, HostStm& stm, WriteLog& log, uint64_t* host_replica, EngineConfig cfg = {})
-        : dev_(dev), stm_(stm), log_(log), host_(host_replica), cfg_(cfg), shipped_(log.threads(), 0) {
+    BasicEngine(hetm_dev* dev, HostStm& stm, Log& log, uint64_t* host_replica, EngineConfig cfg = {})
+        : dev_(dev), stm_(stm), log_(log), host_(host_replica), cfg_(cfg), shipped_(log_threads(log), 0) {
         if (cfg_.starvation_k < 1) throw std::invalid_argument("starvationK >= 1 (SPEC.md:332)");
+        if (cfg_.ev_period < 1) throw std::invalid_argument("early-validation period k >= 1 (SPEC.md:423)");
         if (cfg_.policy == Policy::FavorDevice) snapshot_.resize(stm.sizeWords());
+        check_rc(hetm_dev_set_validation_period(dev_, cfg_.ev_period), "set_validation_period");
     }
-    ~Engine() {
-        for (void* p : pool_) hetm_host_free(p);
+    ~BasicEngine() {
+        for (auto& b : pool_) hetm_host_free(b.ptr);
     }
+    /// Pinned staging buffers allocated so far (chunks recycle them once delivered).
+    std::size_t stagingBuffers() const { return pool_.size(); }
 
     /// Host worker: run transactions until ctx.stop is set or its work ends
     /// (read-only ones when !ctx.updates_allowed); returns how many committed.
@@ -267,8 +289,8 @@ public:
             gpu_done.store(true, std::memory_order_release);
         });
         std::vector<std::thread> hosts;
-        std::vector<uint64_t> commits(log_.threads(), 0);
-        for (int t = 0; t < log_.threads(); ++t)
+        std::vector<uint64_t> commits(log_threads(log_), 0);
+        for (int t = 0; t < log_threads(log_); ++t)
             hosts.emplace_back([&, t] { commits[t] = worker(t, ctx); });
         while (!gpu_done.load(std::memory_order_acquire)) {
             stream_full_chunks(stream_mode, rep);
@@ -282,19 +304,38 @@ public:
             }
             std::this_thread::sleep_for(std::chrono::microseconds(50));
         }
-        stop.store(true, std::memory_order_release);  // host cut-off
-        for (auto& h : hosts) h.join();
         gpu.join();
-        check_rc(gpu_rc, "executeBatch");
-        for (uint64_t c : commits) rep.host_commits += c;
-        // the host is cut off and the device batches are done: the device write
-        // set can travel to the host replica now, under the validation phase
-        // (undone by the abort paths if the round does not commit)
-        if (cfg_.early_merge) check_rc(hetm_dev_merge_prepare(dev_, host_), "merge_prepare");
         const auto t1 = std::chrono::steady_clock::now();
         // ---- VALIDATION: the log tail (APPLY, or validate-only under FavorDevice),
         // early chunks re-validated + applied (FavorDevice: only on success)
         const int tail_mode = favor_device ? HETM_VALIDATE_ONLY : HETM_APPLY;
+        // hostCutoff: the host keeps committing while the log
+        // streams, and pauses once at most cutoff_chunks chunks are undelivered;
+        // 0 stops it as the execution phase ends (the basic algorithm).  Not
+        // after an early conflict: the round is decided, FavorDevice stopped
+        // the host already.
+        // The window also ends once it has shipped as many chunks as were
+        // undelivered when execution ended (what the basic algorithm ships with
+        // the host blocked), so a producer faster than the link cannot extend
+        // the round without bound.
+        if (cfg_.cutoff_chunks > 0 && gpu_rc == HETM_OK && !rep.cut_short && rep.updates_allowed) {
+            const uint64_t backlog0 = backlog_chunks();
+            while (backlog_chunks() > cfg_.cutoff_chunks && rep.cutoff_chunks < backlog0) {
+                const uint64_t before = rep.chunks;
+                stream_all(tail_mode, rep);  // partial chunks too: the backlog drains
+                rep.cutoff_chunks += rep.chunks - before;
+                if (rep.chunks == before) std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+        }
+        stop.store(true, std::memory_order_release);  // host admission paused until the merge completes
+        const auto t_block = std::chrono::steady_clock::now();
+        for (auto& h : hosts) h.join();
+        check_rc(gpu_rc, "executeBatch");
+        for (uint64_t c : commits) rep.host_commits += c;
+        // the host is paused and the device batches are done: the device write
+        // set can travel to the host replica now, under the validation phase
+        // (undone by the abort paths if the round does not commit)
+        if (cfg_.early_merge) check_rc(hetm_dev_merge_prepare(dev_, host_), "merge_prepare");
         stream_full_chunks(tail_mode, rep);
         stream_tail(rep, tail_mode);
         int conflict = 0;
@@ -333,11 +374,11 @@ public:
             check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
         }
         check_rc(hetm_dev_clear_round(dev_, 0), "clear_round");
-        if (cfg_.keep_round_log) last_log_ = log_.allEntries();
-        log_.clearRound();
+        if (cfg_.keep_round_log) last_log_ = log_all(log_);
+        log_clear(log_);
         std::fill(shipped_.begin(), shipped_.end(), 0);
-        used_ = 0;
         const auto t3 = std::chrono::steady_clock::now();
+        rep.host_blocked_ms = std::chrono::duration<double, std::milli>(t3 - t_block).count();
         rep.exec_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         rep.validate_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
         rep.merge_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
@@ -348,13 +389,44 @@ public:
     const std::vector<hetm_log_entry>& lastRoundLog() const { return last_log_; }
 
 private:
-    hetm_log_entry* chunk_buffer() {
-        if (used_ == pool_.size()) {
-            void* p = nullptr;
-            check_rc(hetm_host_alloc(cfg_.chunk_entries * sizeof(hetm_log_entry), &p), "host_alloc");
-            pool_.push_back(p);
+    // Pinned staging ring: a buffer is reused as soon as the chunk it carried is
+    // delivered (hetm_dev_delivery_done), so the pool stays at the chunks in
+    // flight instead of the whole round's log.
+    struct Staging {
+        void* ptr = nullptr;
+        uint64_t handle = 0;
+        bool busy = false;
+    };
+    std::size_t chunk_buffer() {
+        for (std::size_t k = 0; k < pool_.size(); ++k) {
+            const std::size_t idx = (ring_ + k) % pool_.size();
+            Staging& b = pool_[idx];
+            int done = 1;
+            if (b.busy) check_rc(hetm_dev_delivery_done(dev_, b.handle, &done), "delivery_done");
+            if (done) {
+                b.busy = false;
+                ring_ = (idx + 1) % pool_.size();
+                return idx;
+            }
         }
-        return static_cast<hetm_log_entry*>(pool_[used_++]);
+        Staging b;
+        check_rc(hetm_host_alloc(cfg_.chunk_entries * sizeof(hetm_log_entry), &b.ptr), "host_alloc");
+        pool_.push_back(b);
+        return pool_.size() - 1;
+    }
+    // chunks of the host log not yet delivered to the device: shipped but in
+    // flight, plus the unshipped entries of every thread (a partial one counts)
+    uint64_t backlog_chunks() {
+        uint64_t n = 0;
+        for (auto& b : pool_) {
+            int done = 1;
+            if (b.busy) check_rc(hetm_dev_delivery_done(dev_, b.handle, &done), "delivery_done");
+            if (done) b.busy = false;
+            else ++n;
+        }
+        for (int t = 0; t < log_threads(log_); ++t)
+            n += (log_count(log_, t) - shipped_[t] + cfg_.chunk_entries - 1) / cfg_.chunk_entries;
+        return n;
     }
     // Device events of one traced batch, in program order per transaction.
     void trace_batch(int kernel_id, const Batch& b) {
@@ -381,37 +453,49 @@ private:
         }
     }
     void ship(int t, uint64_t n, int mode, RoundReport& rep) {
-        hetm_log_entry* buf = chunk_buffer();
-        const uint64_t got = log_.slice(t, shipped_[t], shipped_[t] + n, buf);
+        Staging& b = pool_[chunk_buffer()];
+        hetm_log_entry* buf = static_cast<hetm_log_entry*>(b.ptr);
+        const uint64_t got = log_copy(log_, t, shipped_[t], n, buf);
         if ((cfg_.fault & ENGINE_FAULT_DROP_CHUNK) && !dropped_ && got) {  // mutation: the chunk never reaches the GPU
             dropped_ = true;
             shipped_[t] += got;
             return;
         }
-        check_rc(hetm_dev_stream_chunk(dev_, buf, got, t, seq_++, mode), "stream_chunk");
+        hetm_delivery dl{};
+        check_rc(hetm_dev_stream_chunk_ex(dev_, buf, got, t, seq_++, mode, &dl), "stream_chunk");
+        b.handle = dl.handle;
+        b.busy = true;
         shipped_[t] += got;
         rep.log_entries += got;
         ++rep.chunks;
+        if (cfg_.bus_real_delay_us_per_unit > 0) {  // BusConfig real-delay mode (bus.hpp:37-39)
+            const double cost = cfg_.bus_latency_units + double(got * sizeof(hetm_log_entry)) / cfg_.bus_bytes_per_unit;
+            std::this_thread::sleep_for(std::chrono::duration<double, std::micro>(cost * cfg_.bus_real_delay_us_per_unit));
+        }
     }
     void stream_full_chunks(int mode, RoundReport& rep) {
-        for (int t = 0; t < log_.threads(); ++t)
-            while (log_.entryCount(t) - shipped_[t] >= cfg_.chunk_entries) ship(t, cfg_.chunk_entries, mode, rep);
+        for (int t = 0; t < log_threads(log_); ++t)
+            while (log_count(log_, t) - shipped_[t] >= cfg_.chunk_entries) ship(t, cfg_.chunk_entries, mode, rep);
     }
     void stream_tail(RoundReport& rep, int mode) {
-        for (int t = 0; t < log_.threads(); ++t) {
-            const uint64_t left = log_.entryCount(t) - shipped_[t];
+        for (int t = 0; t < log_threads(log_); ++t) {
+            const uint64_t left = log_count(log_, t) - shipped_[t];
             if (left) ship(t, left, mode, rep);
         }
+    }
+    void stream_all(int mode, RoundReport& rep) {
+        stream_full_chunks(mode, rep);
+        stream_tail(rep, mode);
     }
 
     hetm_dev* dev_;
     HostStm& stm_;
-    WriteLog& log_;
+    Log& log_;
     uint64_t* host_;
     EngineConfig cfg_;
     std::vector<uint64_t> shipped_;
-    std::vector<void*> pool_;
-    std::size_t used_ = 0;
+    std::vector<Staging> pool_;
+    std::size_t ring_ = 0;
     uint64_t seq_ = 0;
     std::vector<hetm_log_entry> last_log_;
     std::vector<uint64_t> snapshot_;  // FavorDevice round-start host snapshot
@@ -422,5 +506,7 @@ private:
     uint64_t trace_batches_ = 0;
     bool dropped_ = false;             // ENGINE_FAULT_DROP_CHUNK: this round's chunk is gone
 };
+
+using Engine = BasicEngine<WriteLog>;
 
 }  // namespace hetm::b200

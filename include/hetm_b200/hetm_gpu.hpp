@@ -100,10 +100,32 @@ public:
     }
 
     // interconnect sink + engine validation (bus.hpp:78-82)
-    void streamChunk(const LogChunk& c, bool apply = true) {
-        check(hetm_dev_stream_chunk(d_, reinterpret_cast<const hetm_log_entry*>(c.entries.data()), c.entries.size(),
-                                    c.sourceThread, c.seq, apply ? HETM_APPLY : HETM_VALIDATE_ONLY));
+    /// Bus::streamChunk (bus.hpp:80) onto the device: returns the reference's
+    /// Delivery (seq, nEntries, cost = wire bytes / the link, delivered = the H2D
+    /// copy already completed) and, in *handle, the completion id to poll with
+    /// delivered() / waitDelivered().  `c.entries` is borrowed until then.
+    Delivery streamChunk(const LogChunk& c, bool apply = true, std::uint64_t* handle = nullptr) {
+        hetm_delivery dl{};
+        check(hetm_dev_stream_chunk_ex(d_, reinterpret_cast<const hetm_log_entry*>(c.entries.data()),
+                                       c.entries.size(), c.sourceThread, c.seq,
+                                       apply ? HETM_APPLY : HETM_VALIDATE_ONLY, &dl));
+        if (handle) *handle = dl.handle;
+        Delivery out;
+        out.seq = dl.seq;
+        out.nEntries = dl.n_entries;
+        out.cost = static_cast<double>(dl.bytes);
+        out.delivered = delivered(dl.handle);
+        return out;
     }
+    /// The chunk's entries reached the device (its host buffer may be reused).
+    bool delivered(std::uint64_t handle) {
+        int done = 0;
+        check(hetm_dev_delivery_done(d_, handle, &done));
+        return done != 0;
+    }
+    void waitDelivered(std::uint64_t handle) { check(hetm_dev_delivery_wait(d_, handle)); }
+    /// Early-validation period k.
+    void setValidationPeriod(std::uint32_t k) { check(hetm_dev_set_validation_period(d_, k)); }
     void applyLog() { check(hetm_dev_apply_log(d_)); }
     bool roundVerdict() {
         int c = 0;

@@ -19,12 +19,22 @@
 // same words, so per-address ts order = commit order.
 // Writes imply reads (no blind writes).  Aborts throw
 // TxAbort (not a std::exception, types.hpp:51-54); the caller retries.
+//
+// Compiled against the reference headers (-I <reference>/proj/include), the
+// host TM speaks the reference's own types: aborts throw ::hetm::TxAbort
+// (types.hpp:54), out-of-range addresses ::hetm::OutOfBoundsError
+// (types.hpp:39), and commitTo(::hetm::WriteLog&) appends committed write
+// sets to the reference's WriteLog (write_log.hpp:31-101), whose entries are
+// layout-identical to hetm_log_entry.  A reference worker loop written as
+// `catch (hetm::TxAbort&)` therefore catches this TM's aborts.  Without those
+// headers the same names are provided here.
 #pragma once
 
 #include <algorithm>
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <exception>
 #include <functional>
 #include <memory>
@@ -36,24 +46,65 @@
 #include "hetm_b200/capi.h"
 #include "hetm_b200/trace.hpp"
 
+#if !defined(HETM_B200_NO_REFERENCE_TYPES) && __has_include(<hetm/types.hpp>) && __has_include(<hetm/write_log.hpp>)
+#include <hetm/types.hpp>
+#include <hetm/write_log.hpp>
+#define HETM_B200_REFERENCE_TYPES 1
+#endif
+
 namespace hetm::b200 {
 
+#ifdef HETM_B200_REFERENCE_TYPES
+/// The reference's abort signal (types.hpp:51-54) and OutOfBoundsError (types.hpp:39).
+using TxAbort = ::hetm::TxAbort;
+using OutOfBoundsError = ::hetm::OutOfBoundsError;
+static_assert(sizeof(::hetm::WriteLogEntry) == sizeof(hetm_log_entry) &&
+                  offsetof(::hetm::WriteLogEntry, addr) == offsetof(hetm_log_entry, addr) &&
+                  offsetof(::hetm::WriteLogEntry, value) == offsetof(hetm_log_entry, value) &&
+                  offsetof(::hetm::WriteLogEntry, ts) == offsetof(hetm_log_entry, ts),
+              "WriteLogEntry (write_log.hpp:16-21) is the 24-byte wire entry");
+#else
 /// Transaction abort signal (types.hpp:51-54 semantics: not a std::exception).
 struct TxAbort {};
-
-/// OutOfBoundsError counterpart for the host TM (types.hpp:39).
-struct HostOutOfBounds : std::out_of_range {
-    using std::out_of_range::out_of_range;
+/// OutOfBoundsError (types.hpp:36-39 semantics: a runtime_error).
+struct OutOfBoundsError : std::runtime_error {
+    using std::runtime_error::runtime_error;
 };
+#endif
+using HostOutOfBounds = OutOfBoundsError;  // round-1 name
 
 /// Per-thread append-only logs, ts-ordered within a thread (write_log.hpp:27-30).
 /// All threads register before a round starts (write_log.hpp:33-37 race note).
+/// Same operations as the reference WriteLog (registerThread, threadCount,
+/// append, entryCount, totalEntries, slice, allEntries, clearRound) over the
+/// wire entry type.
 class WriteLog {
 public:
-    explicit WriteLog(int threads) : per_(threads) {
+    explicit WriteLog(int threads = 0) : per_(threads) {
         for (auto& p : per_) p = std::make_unique<PerThread>();
     }
-    int threads() const { return static_cast<int>(per_.size()); }
+    /// registerThread (write_log.hpp:33-37): call before the round starts
+    int registerThread() {
+        per_.push_back(std::make_unique<PerThread>());
+        return static_cast<int>(per_.size()) - 1;
+    }
+    int threadCount() const { return static_cast<int>(per_.size()); }
+    int threads() const { return threadCount(); }
+    std::size_t totalEntries() const {
+        std::size_t n = 0;
+        for (int t = 0; t < threadCount(); ++t) n += entryCount(t);
+        return n;
+    }
+    /// slice (write_log.hpp:58-69): copies entries [from, from+max) of one thread
+    std::vector<hetm_log_entry> slice(int thread, std::size_t from, std::size_t max) const {
+        auto& p = *per_.at(thread);
+        std::lock_guard<std::mutex> g(p.mu);
+        std::vector<hetm_log_entry> out;
+        if (from >= p.entries.size()) return out;
+        const std::size_t end = std::min(p.entries.size(), from + max);
+        out.assign(p.entries.begin() + from, p.entries.begin() + end);
+        return out;
+    }
     /// append (write_log.hpp:44-48)
     void append(int thread, std::span<const hetm_log_entry> es) {
         auto& p = *per_.at(thread);
@@ -144,7 +195,7 @@ public:
         }
     }
     uint64_t read(Tx& tx, uint64_t addr) const {
-        if (addr >= words_) throw HostOutOfBounds("host TM read out of bounds");
+        if (addr >= words_) throw OutOfBoundsError("host TM read out of bounds");
         for (auto it = tx.writes.rbegin(); it != tx.writes.rend(); ++it)
             if (it->first == addr) {  // read-your-writes
                 if (trace_) trace_->append(0, HETM_EV_READ, tx.id, addr, it->second);
@@ -160,7 +211,7 @@ public:
         return v;
     }
     void write(Tx& tx, uint64_t addr, uint64_t value) const {
-        if (addr >= words_) throw HostOutOfBounds("host TM write out of bounds");
+        if (addr >= words_) throw OutOfBoundsError("host TM write out of bounds");
         struct Record {  // the WRITE event follows the implicit read in program order
             const HostStm& s;
             Tx& tx;
@@ -283,6 +334,47 @@ private:
     Trace* trace_ = nullptr;
     mutable std::atomic<uint64_t> trace_ids_{0};
 };
+
+/// Commit callback appending each committed write set to a WriteLog
+/// (write_log.hpp:44 append(thread, span)).
+inline HostStm::Callback commitTo(WriteLog& log) {
+    return [&log](int thread, std::span<const hetm_log_entry> es) { log.append(thread, es); };
+}
+#ifdef HETM_B200_REFERENCE_TYPES
+/// The same into the reference's own hetm::WriteLog (entries are layout-identical).
+inline HostStm::Callback commitTo(::hetm::WriteLog& log) {
+    return [&log](int thread, std::span<const hetm_log_entry> es) {
+        log.append(thread, std::span<const ::hetm::WriteLogEntry>(
+                               reinterpret_cast<const ::hetm::WriteLogEntry*>(es.data()), es.size()));
+    };
+}
+#endif
+
+// Log access used by the round controller, for this WriteLog and (with the
+// reference headers) the reference's hetm::WriteLog.
+inline int log_threads(const WriteLog& l) { return l.threadCount(); }
+inline std::size_t log_count(const WriteLog& l, int t) { return l.entryCount(t); }
+inline std::size_t log_copy(const WriteLog& l, int t, std::size_t from, std::size_t n, hetm_log_entry* out) {
+    return l.slice(t, from, from + n, out);
+}
+inline std::vector<hetm_log_entry> log_all(const WriteLog& l) { return l.allEntries(); }
+inline void log_clear(WriteLog& l) { l.clearRound(); }
+#ifdef HETM_B200_REFERENCE_TYPES
+inline int log_threads(const ::hetm::WriteLog& l) { return l.threadCount(); }
+inline std::size_t log_count(const ::hetm::WriteLog& l, int t) { return l.entryCount(t); }
+inline std::size_t log_copy(const ::hetm::WriteLog& l, int t, std::size_t from, std::size_t n, hetm_log_entry* out) {
+    const auto v = l.slice(t, from, n);
+    std::memcpy(out, v.data(), v.size() * sizeof(hetm_log_entry));
+    return v.size();
+}
+inline std::vector<hetm_log_entry> log_all(const ::hetm::WriteLog& l) {
+    const auto v = l.allEntries();
+    std::vector<hetm_log_entry> out(v.size());
+    std::memcpy(out.data(), v.data(), v.size() * sizeof(hetm_log_entry));
+    return out;
+}
+inline void log_clear(::hetm::WriteLog& l) { l.clearRound(); }
+#endif
 
 // ---- the HeTM host API names (north_star: TM_begin / TM_read / TM_write / TM_commit)
 inline void TM_begin(HostStm& stm, HostStm::Tx& tx, int thread) { stm.begin(tx, thread); }

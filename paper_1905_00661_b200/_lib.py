@@ -57,6 +57,22 @@ class DevInfo(C.Structure):
     ]
 
 
+class Delivery(C.Structure):  # hetm_delivery (bus.hpp:51-56 Delivery + completion handle)
+    _fields_ = [
+        ("seq", C.c_uint64),
+        ("n_entries", C.c_uint64),
+        ("bytes", C.c_uint64),
+        ("handle", C.c_uint64),
+        ("src_thread", C.c_int32),
+        ("mode", C.c_int32),
+    ]
+
+
+class SourceStats(C.Structure):  # hetm_source_stats
+    _fields_ = [("chunks", C.c_uint64), ("entries", C.c_uint64), ("last_seq", C.c_uint64),
+                ("last_handle", C.c_uint64)]
+
+
 class BatchStats(C.Structure):
     _fields_ = [
         ("n_tx", C.c_uint64),
@@ -107,6 +123,11 @@ _sigs = {
     "hetm_dev_open_intake": (C.c_int, [_vp]),
     "hetm_dev_close_intake": (C.c_int, [_vp]),
     "hetm_dev_stream_chunk": (C.c_int, [_vp, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_int]),
+    "hetm_dev_stream_chunk_ex": (C.c_int, [_vp, _vp, C.c_uint64, C.c_int, C.c_uint64, C.c_int, C.POINTER(Delivery)]),
+    "hetm_dev_delivery_done": (C.c_int, [_vp, C.c_uint64, C.POINTER(C.c_int)]),
+    "hetm_dev_delivery_wait": (C.c_int, [_vp, C.c_uint64]),
+    "hetm_dev_source_stats": (C.c_int, [_vp, C.c_int, C.POINTER(SourceStats)]),
+    "hetm_dev_set_validation_period": (C.c_int, [_vp, C.c_uint32]),
     "hetm_dev_apply_log": (C.c_int, [_vp]),
     "hetm_dev_poll_conflict": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "hetm_dev_round_verdict": (C.c_int, [_vp, C.POINTER(C.c_int)]),

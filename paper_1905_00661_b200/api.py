@@ -338,6 +338,32 @@ class GpuDevice:
                                             src_thread, seq, mode))
         return entries
 
+    def stream_chunk_ex(self, entries: np.ndarray, src_thread: int = 0, seq: int = 0, mode: int = APPLY):
+        """streamChunk returning its Delivery (bus.hpp:51-56): the buffer is the
+        caller's again once ``delivery_done(d.handle)``."""
+        assert entries.flags.c_contiguous and entries.dtype == LOG_ENTRY, "pass the buffer itself (no copy)"
+        d = _lib.Delivery()
+        self._chk(lib.hetm_dev_stream_chunk_ex(self.h, _ptr(entries) if entries.size else None, entries.size,
+                                               src_thread, seq, mode, C.byref(d)))
+        return d
+
+    def delivery_done(self, handle: int) -> bool:
+        c = C.c_int()
+        self._chk(lib.hetm_dev_delivery_done(self.h, handle, C.byref(c)))
+        return bool(c.value)
+
+    def delivery_wait(self, handle: int):
+        self._chk(lib.hetm_dev_delivery_wait(self.h, handle))
+
+    def source_stats(self, src_thread: int) -> _lib.SourceStats:
+        st = _lib.SourceStats()
+        self._chk(lib.hetm_dev_source_stats(self.h, src_thread, C.byref(st)))
+        return st
+
+    def set_validation_period(self, k: int):
+        """Early validation every k VALIDATE_ONLY chunks (default 8)."""
+        self._chk(lib.hetm_dev_set_validation_period(self.h, k))
+
     def apply_log(self):
         self._chk(lib.hetm_dev_apply_log(self.h))
 

@@ -448,9 +448,9 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
         }
         return cudaGraphLaunch(graph->exec, s);
     }
-    if (n >= (1ull << 29)) return cudaErrorInvalidValue;  // 4n << 1 payloads fit 32 bits
     // keyed slots: the two written accounts, or all four accesses for a trace
     const int S = v.trace ? 4 : 2;
+    if ((uint64_t)S * n * 2 > (1ull << 32)) return cudaErrorInvalidValue;  // (S*i + k) << 1 payloads fit 32 bits
     const uint64_t n4 = (uint64_t)S * n;
     const int end_bit = (int)std::min<uint32_t>(32, bits_for(v.size_words) + 1);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };

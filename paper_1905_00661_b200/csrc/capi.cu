@@ -18,6 +18,7 @@
 // the host except the explicitly synchronous calls (verdict, merge_wait,
 // snapshots, stats) and the pool hand-off of merge_prepare.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -143,7 +144,8 @@ struct hetm_dev {
     DevCounters* h_ctr = nullptr;        // pinned mirror of d_ctr
     uint64_t* h_first = nullptr;         // pinned: first ticket of the current host-buffer batch
     unsigned long long* d_pop = nullptr; // popcount scratch (3)
-    unsigned long long* d_restore = nullptr; // apply-kernel restore queue (kRestoreCap entries)
+    unsigned long long* d_restore = nullptr; // apply-kernel restore queue (restore_cap entries)
+    uint64_t restore_cap = 0;
     CacheGeom cache{};                   // HETM_KERNEL_CACHE region
     hetm_cache_result* d_res = nullptr;  // per-transaction results (host-buffer path)
     uint64_t res_cap = 0;
@@ -166,6 +168,17 @@ struct hetm_dev {
     uint64_t arena_cap = 0, arena_n = 0;
     std::vector<std::pair<uint64_t, uint64_t>> deferred;  // [lo,hi) streamed VALIDATE_ONLY, not applied
     bool deferred_final = false;         // deferred ranges re-validated after execution ended
+    // early-validation cadence: VALIDATE_ONLY chunks are validated
+    // in one launch every ev_period chunks; arena [ev_lo, arena_n) is pending
+    uint32_t ev_period = 8;
+    uint32_t ev_pending = 0;
+    uint64_t ev_lo = 0;
+    // per-chunk delivery handles (bus.hpp:51-56 Delivery): handle h's H2D copy
+    // is complete when dl_ev[h % kDeliveryRing] has fired; handles below
+    // dl_floor are known complete (s_copy is in order)
+    std::vector<cudaEvent_t> dl_ev;
+    uint64_t dl_next = 0, dl_floor = 0;
+    std::map<int, hetm_source_stats> sources;  // per source thread, this round
     void* d_in = nullptr;
     uint64_t in_cap = 0;
     unsigned long long* d_tk = nullptr;
@@ -177,7 +190,9 @@ struct hetm_dev {
     unsigned long long* d_recv_counts = nullptr;
     uint32_t recv_shards = 0;
     uint64_t recv_cap = 0;
-    void** d_peer_ptrs = nullptr;  // device copy of {entries[64], counts[64]} peer pointer tables
+    void** d_peer_ptrs = nullptr;  // device copy of {entries[64], counts[64]} peer pointer tables, per parity
+    std::array<void*, 128> peer_table[2];  // host copies of the uploaded tables
+    bool peer_table_ok[2] = {false, false};
     unsigned long long* d_peer_totals = nullptr;
     void* d_flush = nullptr;
     size_t flush_bytes = 0;
@@ -197,6 +212,7 @@ struct hetm_dev {
     uint32_t* d_hot = nullptr;
     cudaStream_t s_est = nullptr;           // the estimator runs off the batch's critical path
     cudaEvent_t ev_est = nullptr;
+    hetm_bank_tx* d_est_in = nullptr;       // the estimate's copy of the sampled input records
     void* d_sched = nullptr;                // SCAN schedule scratch (bank_sched_temp_bytes)
     size_t sched_bytes = 0;
     SchedGraph sched_graph;                 // its captured launch sequence
@@ -206,7 +222,8 @@ struct hetm_dev {
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
     cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
-                ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_copy_zc = nullptr;
+                ev_d2h = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_copy_zc = nullptr,
+                ev_ext = nullptr;
     bool intake_open = true;
     bool shadow_synced = true;   // devShadow == devReplica as of the round start
     bool round_applied = false;  // some APPLY validation touched devReplica this round
@@ -246,6 +263,7 @@ struct hetm_dev {
         v.chunk_shift = chunk_shift;
         v.wlog = d_wlog;
         v.wlog_slots = wlog_slots;
+        v.wlog_ovf = &d_ctr->wlog_overflow;
         v.serial = (cfg.flags & HETM_CFG_DETERMINISTIC) ? 1u : 0u;
         v.trace = nullptr;
         return v;
@@ -310,8 +328,11 @@ int sync_all(hetm_dev* d) {
     CK(d, cudaStreamSynchronize(d->s_val));
     CK(d, cudaStreamSynchronize(d->s_merge));
     CK(d, cudaStreamSynchronize(d->s_d2h));
+    if (d->s_est) CK(d, cudaStreamSynchronize(d->s_est));
     return HETM_OK;
 }
+
+constexpr uint64_t kDeliveryRing = 4096;  // delivery events in flight per handle
 
 constexpr uint64_t kAutoAbortRatio = 128;  // AUTO feedback: aborts per transaction above 1/128 ...
 constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches as SCAN
@@ -354,8 +375,20 @@ int ensure_wlog(hetm_dev* d, uint64_t n) {
     void* p = nullptr;
     if ((rc = dev_alloc(d, &p, cap * 4))) return rc;
     if (d->d_wlog) {
-        const uint64_t used = std::min<uint64_t>(2 * d->round_tx, d->wlog_slots);
+        // the round's slots in use: 2 per ticket taken since the round's origin
+        // (aborted attempts that took a ticket own slots too, so this can exceed
+        // 2 * round_tx); a span past the old capacity lost slots the kernels
+        // could not store, which the kernels flagged as an overflow already
+        unsigned long long tk[2] = {0, 0};  // {ticket, wlog_base}
+        CK(d, cudaMemcpy(&tk[0], &d->d_ctr->ticket, 8, cudaMemcpyDeviceToHost));
+        CK(d, cudaMemcpy(&tk[1], &d->d_ctr->wlog_base, 8, cudaMemcpyDeviceToHost));
+        const uint64_t span = 2 * (tk[0] - tk[1]);
+        const uint64_t used = std::min<uint64_t>(span, d->wlog_slots);
         if (used) CK(d, cudaMemcpy(p, d->d_wlog, used * 4, cudaMemcpyDeviceToDevice));
+        if (span > d->wlog_slots) {
+            const unsigned long long one = 1;
+            CK(d, cudaMemcpy(&d->d_ctr->wlog_overflow, &one, 8, cudaMemcpyHostToDevice));
+        }
         cudaFree(d->d_wlog);
         d->bytes_alloc -= d->wlog_slots * 4;
     }
@@ -494,6 +527,23 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     return HETM_OK;
 }
 
+// The apply restore queue holds a quarter of the largest apply launch (at
+// least kRestoreCap): at cfg5 sizes (2^26 entries into a 2^31-word shard) ~2^20
+// entries race with an earlier entry of the round, and an overflow costs a
+// full winner pass over the launch.  Growing waits for the launches using it.
+int ensure_restore(hetm_dev* d, uint64_t n) {
+    const uint64_t need = std::max<uint64_t>(kRestoreCap, n / 4);
+    if (need <= d->restore_cap) return HETM_OK;
+    if (int rc = sync_all(d)) return rc;
+    cudaFree(d->d_restore);
+    d->bytes_alloc -= d->restore_cap * 8;
+    d->d_restore = nullptr;
+    d->restore_cap = 0;
+    if (int rc = dev_alloc(d, (void**)&d->d_restore, need * 8)) return rc;
+    d->restore_cap = need;
+    return HETM_OK;
+}
+
 // Validation launch with optional timing brackets.
 cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, int apply, cudaStream_t s) {
     cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -506,7 +556,8 @@ cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, i
     if (d->fault & HETM_FAULT_SKIP_RS) v.rs = d->d_rs_zero;  // mutation: the RS test never fires
     cudaError_t e = (apply && (d->fault & HETM_FAULT_SKIP_TS))
                         ? launch_blind_apply(v, log, n, d->d_ctr, d->geom, s)  // mutation: no TS freshness
-                        : launch_validate(v, log, n, apply, d->d_ctr, d->d_restore, d->geom, s);
+                        : launch_validate(v, log, n, apply, d->d_ctr, RestoreQueue{d->d_restore, d->restore_cap},
+                                          d->geom, s);
     if (d->timing && n) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
@@ -586,16 +637,29 @@ int wait_round_work(hetm_dev* d, cudaStream_t s) {
     return HETM_OK;
 }
 
+// Round work enqueued on a caller's stream (validate_dptr, apply_received,
+// bitmap_or_peers) joins the validation stream at once, so ev_val (recorded on
+// s_val by wait_round_work) and the verdict's s_val sync cover it.
+int join_val(hetm_dev* d, cudaStream_t s) {
+    if (s == d->s_val) return HETM_OK;
+    CK(d, cudaEventRecord(d->ev_ext, s));
+    CK(d, cudaStreamWaitEvent(d->s_val, d->ev_ext, 0));
+    return HETM_OK;
+}
+
 int enqueue_deferred_apply(hetm_dev* d) {
     if (d->deferred.empty()) return HETM_OK;
     CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
     for (auto& r : d->deferred) {
+        if (int rc = ensure_restore(d, r.second - r.first)) return rc;
         cudaError_t e = timed_validate(d, d->d_arena + r.first, r.second - r.first, 1, d->s_val);
         if (e != cudaSuccess) return fail(d, e, "validate(apply deferred)");
     }
     d->deferred.clear();
     d->deferred_final = false;
     d->round_applied = true;
+    d->ev_lo = d->arena_n;  // the apply launches validated the pending early chunks too
+    d->ev_pending = 0;
     return HETM_OK;
 }
 
@@ -695,6 +759,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);
+    d->restore_cap = kRestoreCap;
     d->arena_cap = cfg->log_capacity ? cfg->log_capacity : (1ull << 20);
     if ((rc = dev_alloc(d, (void**)&d->d_arena, d->arena_cap * sizeof(hetm_log_entry)))) return bail(rc);
     if (cudaHostAlloc((void**)&d->h_first, 64, cudaHostAllocPortable) != cudaSuccess)
@@ -713,7 +778,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
 
     for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc, &d->s_in, &d->s_out})
         CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc, &d->ev_stage})
+    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc, &d->ev_stage, &d->ev_ext})
         CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CK(d, cudaEventCreate(&d->ev_t0));
     CK(d, cudaEventCreate(&d->ev_t1));
@@ -754,6 +819,7 @@ int hetm_dev_close(hetm_dev* d) {
         for (cudaEvent_t e : d->piece_ev[b]) cudaEventDestroy(e);
     }
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : d->dl_ev) cudaEventDestroy(e);
     if (d->prep.active) {  // never merged: leave the host replica as it was
         std::lock_guard<std::mutex> g(d->mu);
         cancel_prepare(d);
@@ -770,7 +836,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
-                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched})
+                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     if (d->h_first) cudaFreeHost(d->h_first);
@@ -783,7 +849,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1,
-                          d->ev_copy_zc, d->ev_stage})
+                          d->ev_copy_zc, d->ev_stage, d->ev_ext})
         if (e) cudaEventDestroy(e);
     delete d;
     return HETM_OK;
@@ -1084,7 +1150,7 @@ int hetm_dev_bitmap_or_peers(hetm_dev* d, int which, const void* const* peer_wor
     cudaError_t e = launch_or_peers(p, reinterpret_cast<const unsigned long long* const*>(peer_words), n_peers,
                                     word_lo, word_hi, d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "bitmap_or_peers");
-    return HETM_OK;
+    return join_val(d, s);
 }
 
 int hetm_dev_or_bitmap(hetm_dev* d, int which, const uint64_t* words, uint64_t n_words) {
@@ -1120,38 +1186,150 @@ int hetm_dev_close_intake(hetm_dev* d) {
     return HETM_OK;
 }
 
+// Validate-only launch over the pending early chunks [ev_lo, arena_n).
+int flush_early_validation(hetm_dev* d) {
+    if (d->ev_lo >= d->arena_n) {
+        d->ev_pending = 0;
+        return HETM_OK;
+    }
+    cudaError_t e = timed_validate(d, d->d_arena + d->ev_lo, d->arena_n - d->ev_lo, 0, d->s_val);
+    if (e != cudaSuccess) return fail(d, e, "validate launch");
+    CK(d, cudaMemcpyAsync(&d->h_ctr->conflict, &d->d_ctr->conflict, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                          d->s_val));
+    d->ev_lo = d->arena_n;
+    d->ev_pending = 0;
+    return HETM_OK;
+}
+
 int hetm_dev_stream_chunk(hetm_dev* d, const hetm_log_entry* entries, uint64_t n, int src_thread, uint64_t seq,
                           int mode) {
+    return hetm_dev_stream_chunk_ex(d, entries, n, src_thread, seq, mode, nullptr);
+}
+
+int hetm_dev_stream_chunk_ex(hetm_dev* d, const hetm_log_entry* entries, uint64_t n, int src_thread, uint64_t seq,
+                             int mode, hetm_delivery* out) {
     NvtxRange nvtx_range("hetm.streamChunk");
-    (void)src_thread;
-    (void)seq;
-    if (!d || (!entries && n)) return HETM_ERR_INVALID_ARG;
+    if (!d || (!entries && n) || src_thread < 0) return HETM_ERR_INVALID_ARG;
     if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
+    // One device-wide order for every chunk (the d->mu section): one source
+    // thread's chunks are copied, validated and applied in the order its calls
+    // return, which is the per-source FIFO of SPEC.md:300 (bus.hpp:80 streams
+    // chunks of one thread's log in log order); different sources interleave in
+    // arrival order ("validated in arbitrary order", §4.3).
     std::lock_guard<std::mutex> g(d->mu);
     if (!d->intake_open) return HETM_ERR_ROUND_CLOSED;
     d->record(HETM_H2D, HETM_TAG_LOG, n * sizeof(hetm_log_entry));
-    if (n == 0) return HETM_OK;
-    int rc = ensure_arena(d, d->arena_n + n);
-    if (rc) return rc;
+    // delivery handle: completion of this chunk's H2D copy (the host buffer is
+    // the caller's again once it fires)
+    if (d->dl_ev.empty()) {
+        d->dl_ev.resize(kDeliveryRing, nullptr);
+        for (auto& e : d->dl_ev) CK(d, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const uint64_t h = d->dl_next++;
+    cudaEvent_t ev = d->dl_ev[h % kDeliveryRing];
+    if (h >= kDeliveryRing && d->dl_floor <= h - kDeliveryRing) {  // the slot's previous chunk: long delivered
+        CK(d, cudaEventSynchronize(ev));
+        d->dl_floor = h - kDeliveryRing + 1;
+    }
+    hetm_source_stats& src = d->sources[src_thread];
+    src.chunks += 1;
+    src.entries += n;
+    src.last_seq = seq;
+    src.last_handle = h;
+    if (out) {
+        out->seq = seq;
+        out->n_entries = n;
+        out->bytes = n * sizeof(hetm_log_entry);
+        out->handle = h;
+        out->src_thread = src_thread;
+        out->mode = mode;
+    }
+    int rc;
+    if (n == 0) {  // empty chunk: delivered at once (latency only)
+        CK(d, cudaEventRecord(ev, d->s_copy));
+        return HETM_OK;
+    }
+    if ((rc = ensure_arena(d, d->arena_n + n))) return rc;
     hetm_log_entry* dst = d->d_arena + d->arena_n;
     CK(d, cudaStreamWaitEvent(d->s_copy, d->ev_round, 0));
     CK(d, cudaMemcpyAsync(dst, entries, n * sizeof(hetm_log_entry), cudaMemcpyHostToDevice, d->s_copy));
+    CK(d, cudaEventRecord(ev, d->s_copy));
     CK(d, cudaEventRecord(d->ev_copy, d->s_copy));
     CK(d, cudaStreamWaitEvent(d->s_val, d->ev_copy, 0));
     CK(d, cudaStreamWaitEvent(d->s_val, d->ev_round, 0));
     const bool apply = mode == HETM_APPLY;
-    if (apply) CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));  // apply only after execution
-    cudaError_t e = timed_validate(d, dst, n, apply ? 1 : 0, d->s_val);
-    if (e != cudaSuccess) return fail(d, e, "validate launch");
-    CK(d, cudaMemcpyAsync(&d->h_ctr->conflict, &d->d_ctr->conflict, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                          d->s_val));
     if (apply) {
+        // pending early chunks are validated first (in arrival order)
+        if ((rc = flush_early_validation(d))) return rc;
+        if ((rc = ensure_restore(d, n))) return rc;
+        CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));  // apply only after execution
+        cudaError_t e = timed_validate(d, dst, n, 1, d->s_val);
+        if (e != cudaSuccess) return fail(d, e, "validate launch");
+        CK(d, cudaMemcpyAsync(&d->h_ctr->conflict, &d->d_ctr->conflict, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                              d->s_val));
         d->round_applied = true;
+        d->arena_n += n;
+        d->ev_lo = d->arena_n;
     } else {
-        d->deferred.emplace_back(d->arena_n, d->arena_n + n);
+        if (d->deferred.empty() || d->deferred.back().second != d->arena_n)
+            d->deferred.emplace_back(d->arena_n, d->arena_n + n);
+        else
+            d->deferred.back().second += n;  // contiguous early chunks: one range
         d->deferred_final = false;
+        d->arena_n += n;
+        // early validation every ev_period chunks
+        if (++d->ev_pending >= d->ev_period)
+            if ((rc = flush_early_validation(d))) return rc;
     }
-    d->arena_n += n;
+    return HETM_OK;
+}
+
+int hetm_dev_delivery_done(hetm_dev* d, uint64_t handle, int* done) {
+    if (!d || !done) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (handle >= d->dl_next) return HETM_ERR_INVALID_ARG;
+    if (handle < d->dl_floor) {
+        *done = 1;
+        return HETM_OK;
+    }
+    const cudaError_t e = cudaEventQuery(d->dl_ev[handle % kDeliveryRing]);
+    if (e == cudaErrorNotReady) {
+        *done = 0;
+        return HETM_OK;
+    }
+    if (e != cudaSuccess) return fail(d, e, "delivery query");
+    *done = 1;
+    d->dl_floor = std::max(d->dl_floor, handle + 1);  // s_copy completes in order
+    return HETM_OK;
+}
+
+int hetm_dev_delivery_wait(hetm_dev* d, uint64_t handle) {
+    if (!d) return HETM_ERR_INVALID_ARG;
+    cudaEvent_t ev = nullptr;
+    {
+        std::lock_guard<std::mutex> g(d->mu);
+        if (handle >= d->dl_next) return HETM_ERR_INVALID_ARG;
+        if (handle < d->dl_floor) return HETM_OK;
+        ev = d->dl_ev[handle % kDeliveryRing];
+    }
+    CK(d, cudaEventSynchronize(ev));
+    std::lock_guard<std::mutex> g(d->mu);
+    d->dl_floor = std::max(d->dl_floor, handle + 1);
+    return HETM_OK;
+}
+
+int hetm_dev_source_stats(hetm_dev* d, int src_thread, hetm_source_stats* out) {
+    if (!d || !out || src_thread < 0) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    auto it = d->sources.find(src_thread);
+    *out = it == d->sources.end() ? hetm_source_stats{} : it->second;
+    return HETM_OK;
+}
+
+int hetm_dev_set_validation_period(hetm_dev* d, uint32_t k) {
+    if (!d || k == 0) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->ev_period = k;
     return HETM_OK;
 }
 
@@ -1173,6 +1351,8 @@ int hetm_dev_round_verdict(hetm_dev* d, int* conflict) {
     std::lock_guard<std::mutex> g(d->mu);
     // Chunks validated only early (possibly before the batch finished setting
     // its RS bits) are re-validated once execution has ended.
+    d->ev_lo = d->arena_n;  // the final validation below covers the pending early chunks
+    d->ev_pending = 0;
     if (!d->deferred.empty() && !d->deferred_final) {
         CK(d, cudaStreamWaitEvent(d->s_val, d->ev_exec, 0));
         for (auto& r : d->deferred) {
@@ -1604,7 +1784,9 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
             e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, false,
                                     d->geom, d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "restore(rollback)");
-        e = launch_rollback_reapply(d->view(), d->d_shadow, d->d_arena, d->arena_n, d->d_ctr, d->d_restore, d->geom,
+        if ((rc = ensure_restore(d, d->arena_n))) return rc;
+        e = launch_rollback_reapply(d->view(), d->d_shadow, d->d_arena, d->arena_n, d->d_ctr,
+                                    RestoreQueue{d->d_restore, d->restore_cap}, d->geom,
                                     d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "rollback_reapply");
         d->record(HETM_D2D, HETM_TAG_ROLLBACK, dirty_bytes);
@@ -1720,6 +1902,9 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     CK(d, cudaEventRecord(d->ev_round, s));
     if (!(flags & HETM_CLEAR_ASYNC)) d->h_ctr->conflict = 0;
     d->arena_n = 0;
+    d->ev_lo = 0;
+    d->ev_pending = 0;
+    d->sources.clear();
     d->deferred.clear();
     d->deferred_final = false;
     d->round_applied = false;
@@ -1791,9 +1976,19 @@ int hetm_dev_execute_batch_dptr_ex(hetm_dev* d, int kernel_id, const void* d_inp
         // the estimate for the next batch starts once this batch's kernels are done:
         // its CTA (128 KiB of shared memory) must never hold an SM the batch's
         // persistent CTAs need (it overlaps the validation phase instead)
+        // The sampled records are copied into a handle-owned buffer on the batch's
+        // stream first (S strided records, 48 KiB): the caller may free or reuse
+        // d_inputs once that stream is done, while the estimate still runs on s_est.
+        const uint64_t S = bank_hot_estimate_sample(n_tx), stride = n_tx / S;
+        if (!d->d_est_in) {
+            if (int rc = dev_alloc(d, (void**)&d->d_est_in, bank_hot_estimate_sample(~0ull) * sizeof(hetm_bank_tx)))
+                return rc;
+        }
+        CK(d, cudaMemcpy2DAsync(d->d_est_in, sizeof(hetm_bank_tx), d_inputs, stride * sizeof(hetm_bank_tx),
+                                sizeof(hetm_bank_tx), S, cudaMemcpyDeviceToDevice, s));
         CK(d, cudaEventRecord(d->ev_est, s));
         CK(d, cudaStreamWaitEvent(d->s_est, d->ev_est, 0));
-        cudaError_t e = launch_bank_hot_estimate(static_cast<const hetm_bank_tx*>(d_inputs), n_tx, d->d_hot, d->s_est);
+        cudaError_t e = launch_bank_hot_estimate(d->d_est_in, S, d->d_hot, d->s_est);
         if (e != cudaSuccess) return fail(d, e, "hot_estimate");
     }
     return HETM_OK;
@@ -1818,6 +2013,8 @@ int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_
     if (!d || (n && !d_entries)) return HETM_ERR_INVALID_ARG;
     if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
+    if (mode == HETM_APPLY)
+        if (int rc = ensure_restore(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     if (mode == HETM_APPLY) {
         CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
@@ -1826,8 +2023,7 @@ int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_
     }
     cudaError_t e = timed_validate(d, d_entries, n, mode == HETM_APPLY, s);
     if (e != cudaSuccess) return fail(d, e, "validate_dptr");
-    if (stream) CK(d, cudaEventRecord(d->ev_val, s));
-    return HETM_OK;
+    return join_val(d, s);
 }
 
 int hetm_dev_read_counters(hetm_dev* d, int* conflict, hetm_batch_stats* last) {
@@ -1902,20 +2098,29 @@ int hetm_dev_route_to_peers_dptr(hetm_dev* d, const hetm_log_entry* d_in, uint64
         d->route_cap = need;
     }
     if (!d->d_peer_ptrs) {
-        if ((rc = dev_alloc(d, (void**)&d->d_peer_ptrs, 128 * sizeof(void*)))) return rc;
+        if ((rc = dev_alloc(d, (void**)&d->d_peer_ptrs, 2 * 128 * sizeof(void*)))) return rc;
         if ((rc = dev_alloc(d, (void**)&d->d_peer_totals, 64 * 8))) return rc;
     }
-    void* table[128] = {};
+    const uint32_t par = parity & 1;
+    std::array<void*, 128> table{};
     for (uint32_t s = 0; s < n_shards; ++s) {  // this round's arena / count block of every owner
-        table[s] = static_cast<hetm_log_entry*>(peer_entries[s]) + (uint64_t)(parity & 1) * n_shards * cap;
-        table[64 + s] = static_cast<unsigned long long*>(peer_counts[s]) + (parity & 1) * 64;
+        table[s] = static_cast<hetm_log_entry*>(peer_entries[s]) + (uint64_t)par * n_shards * cap;
+        table[64 + s] = static_cast<unsigned long long*>(peer_counts[s]) + par * 64;
     }
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
-    CK(d, cudaMemcpyAsync(d->d_peer_ptrs, table, sizeof(table), cudaMemcpyHostToDevice, s));
-    CK(d, cudaStreamSynchronize(s));  // `table` is a stack buffer
+    void** dtab = d->d_peer_ptrs + par * 128;
+    // the IPC-opened peer pointers do not change between rounds: each parity's
+    // device table is uploaded once (again only if the peers change), so a
+    // round's routing never waits on the host
+    if (!d->peer_table_ok[par] || d->peer_table[par] != table) {
+        CK(d, cudaStreamSynchronize(s));  // a launch of two rounds ago may still read this parity's table
+        CK(d, cudaMemcpy(dtab, table.data(), sizeof(void*) * 128, cudaMemcpyHostToDevice));
+        d->peer_table[par] = table;
+        d->peer_table_ok[par] = true;
+    }
     cudaError_t e = launch_route_to_peers(d_in, n, n_shards, shard_words, my_shard, cap,
-                                          reinterpret_cast<hetm_log_entry* const*>(d->d_peer_ptrs),
-                                          reinterpret_cast<unsigned long long* const*>(d->d_peer_ptrs + 64),
+                                          reinterpret_cast<hetm_log_entry* const*>(dtab),
+                                          reinterpret_cast<unsigned long long* const*>(dtab + 64),
                                           d->d_peer_totals, d->d_route, d->route_cap, d->geom, s);
     if (e != cudaSuccess) return fail(d, e, "route_to_peers");
     return HETM_OK;
@@ -1929,6 +2134,8 @@ int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_
     const uint64_t p = parity & 1;
     const hetm_log_entry* arena = d->d_recv + p * d->recv_shards * d->recv_cap;
     const unsigned long long* counts = d->d_recv_counts + p * 64;
+    if (mode == HETM_APPLY)
+        if (int rc = ensure_restore(d, d->recv_cap)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     if (mode == HETM_APPLY) {
         CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
@@ -1943,13 +2150,14 @@ int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_
         cudaEventRecord(t0, s);
     }
     const cudaError_t e = launch_validate_regions(d->view(), arena, counts, d->recv_shards, d->recv_cap,
-                                                  mode == HETM_APPLY ? 1 : 0, d->d_ctr, d->d_restore, d->geom, s);
+                                                  mode == HETM_APPLY ? 1 : 0, d->d_ctr,
+                                                  RestoreQueue{d->d_restore, d->restore_cap}, d->geom, s);
     if (d->timing) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
     }
     if (e != cudaSuccess) return fail(d, e, "validate_regions");
-    if (stream) CK(d, cudaEventRecord(d->ev_val, s));
+    if (int rc = join_val(d, s)) return rc;
     if (n_out) {  // optional: the entry count needs a host round trip
         unsigned long long c[64] = {};
         CK(d, cudaMemcpyAsync(c, counts, d->recv_shards * 8, cudaMemcpyDeviceToHost, s));

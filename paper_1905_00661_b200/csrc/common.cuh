@@ -35,8 +35,8 @@ constexpr unsigned long long kTsTag = 1ull << 62;
 // meta of a word whose freshest applied host write has timestamp ts
 __host__ __device__ __forceinline__ unsigned long long ts_meta(uint64_t ts) { return kTsTag | ts; }
 
-// Capacity of the apply kernel's restore queue (entries); overflow falls back
-// to a full winner pass over the launch.
+// Minimum capacity of the apply kernel's restore queue (entries); the handle
+// grows it to a quarter of the largest apply launch (kernels.h RestoreQueue).
 constexpr uint64_t kRestoreCap = 1ull << 20;
 
 // Device-wide counters, one per handle (HBM, 128-B aligned).
@@ -72,6 +72,7 @@ struct ShardView {
     uint32_t chunk_shift;      // chunk = local_word >> chunk_shift
     uint32_t* wlog;            // device write-set log (nullptr: disabled, shard >= 2^32 words)
     uint64_t wlog_slots;       // its capacity in slots
+    unsigned long long* wlog_ovf; // set when a committed write set did not fit (DevCounters::wlog_overflow)
     uint32_t serial;           // deterministic single-worker mode (HETM_CFG_DETERMINISTIC)
     unsigned long long* trace; // checker trace of the batch (nullptr: off): HETM_TRACE_TX_WORDS per tx index
 };
@@ -124,6 +125,7 @@ __device__ __forceinline__ void wlog_put(const ShardView& v, unsigned long long 
                                          uint32_t loc) {
     const unsigned long long s = (t - wbase) * 2ull + (unsigned)j;
     if (s < v.wlog_slots) v.wlog[s] = loc;
+    else if (v.wlog) *v.wlog_ovf = 1;  // the merge and rollback fall back to dirty chunks
 }
 
 __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {

@@ -36,22 +36,29 @@ cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t
                             DevCounters* ctr, uint32_t max_attempts, const LaunchGeom& g, cudaStream_t s);
 
 // engine.validateChunk over n log entries (apply: pass A + pass B).
-// Apply-mode launches of one handle must be stream-ordered (they share d_restore,
-// kRestoreCap entries, and rely on the previous launch's stores being complete).
+// Apply-mode launches of one handle must be stream-ordered (they share the
+// restore queue and rely on the previous launch's stores being complete).
+// Restore queue of the apply kernel: indices of entries whose value store raced
+// with another entry of the round; overflow (> cap) falls back to a full
+// winner pass over the launch.  The handle sizes cap to the launch (n/4).
+struct RestoreQueue {
+    unsigned long long* idx;
+    uint64_t cap;
+};
 cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, DevCounters* ctr,
                                const LaunchGeom& g, cudaStream_t s);  // fault injection only
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
-                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
+                            DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g, cudaStream_t s);
 // Optimized rollback: untag the logged words, re-apply the round log, copy them to shadow.
 cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
-                                    DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g,
+                                    DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g,
                                     cudaStream_t s);
 // Literal TS reset: every TS word becomes an unlocked word.
 cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Validate/apply the received regions of a peer arena (counts on the device; no host sync).
 cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_base, const unsigned long long* d_counts,
                                     uint32_t n_regions, uint64_t cap, int apply, DevCounters* ctr,
-                                    unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s);
+                                    RestoreQueue rq, const LaunchGeom& g, cudaStream_t s);
 // Round boundary: ts_floor = max(ts_floor, round_max_ts) (0 with reset_ts), round_max_ts = 0.
 // Winner store of the round's log: value of the entry whose ts equals the
 // cell's TS goes to dst[addr] (plain array) or, with dst == nullptr, to the

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, LogV
 // store; duplicates (rare under uniform access) cost one more L2 load+store.
 template <int U>
 __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView lv, DevCounters* ctr,
-                                                            unsigned long long* __restrict__ restore) {
+                                                            RestoreQueue restore) {
     __shared__ SegPrefix sp;
     const uint64_t n = view_total(lv, sp);
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView
             v.cells[e[u].addr - v.base].value = e[u].value;
             if ((old[u] & kTsTag) && (old[u] & ~kTsTag) > ts_floor) {  // raced with an entry of this round
                 const unsigned long long k = atomicAdd(&ctr->restore_n, 1ull);
-                if (k < kRestoreCap) restore[k] = i0 + (uint64_t)u * blockDim.x;
+                if (k < restore.cap) restore.idx[k] = i0 + (uint64_t)u * blockDim.x;
             }
         }
     }
@@ -220,7 +220,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 __global__ void __launch_bounds__(kValThreads) apply_tma_kernel(ShardView v, const hetm_log_entry* __restrict__ log,
                                                                 uint64_t n, DevCounters* ctr,
-                                                                unsigned long long* __restrict__ restore) {
+                                                                RestoreQueue restore) {
     extern __shared__ __align__(128) unsigned char apply_smem[];
     auto buf = reinterpret_cast<hetm_log_entry(*)[kTile]>(apply_smem);  // two stages
     __shared__ alignas(8) uint64_t bar[2];
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kValThreads) apply_tma_kernel(ShardView v, con
             v.cells[e[u].addr - v.base].value = e[u].value;
             if ((old[u] & kTsTag) && (old[u] & ~kTsTag) > ts_floor) {
                 const unsigned long long k = atomicAdd(&ctr->restore_n, 1ull);
-                if (k < kRestoreCap) restore[k] = base_i + threadIdx.x + u * kValThreads;
+                if (k < restore.cap) restore.idx[k] = base_i + threadIdx.x + u * kValThreads;
             }
         }
     }
@@ -311,14 +311,14 @@ __global__ void __launch_bounds__(kValThreads) apply_tma_kernel(ShardView v, con
 // is checked (pass B of the classic two-pass scheme).  The last block to
 // finish resets the queue for the next apply launch on this stream.
 __global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, LogView lv, DevCounters* ctr,
-                                                              const unsigned long long* __restrict__ restore) {
+                                                              RestoreQueue restore) {
     __shared__ SegPrefix sp;
     const uint64_t n = view_total(lv, sp);
     const unsigned long long m = ld_relaxed(&ctr->restore_n);
-    const bool full = m > kRestoreCap;
+    const bool full = m > restore.cap;
     const uint64_t cnt = full ? n : m;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x) {
-        const EntryRegs e = view_entry(lv, sp, full ? j : restore[j]);
+        const EntryRegs e = view_entry(lv, sp, full ? j : restore.idx[j]);
         const uint64_t loc = e.addr - v.base;
         if (loc < v.size_words && ld_relaxed(&v.cells[loc].meta) == ts_meta(e.ts)) v.cells[loc].value = e.value;
     }
@@ -469,7 +469,7 @@ cudaError_t launch_clear_round(unsigned long long* rs, unsigned long long* ws, u
 // Core launcher over a LogView; n_hint sizes the grid (the flat count, or the
 // segmented view's capacity when the counts live on the device).
 static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n_hint, int apply, DevCounters* ctr,
-                               unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
+                               RestoreQueue rq, const LaunchGeom& g, cudaStream_t s) {
     if (n_hint == 0) return cudaSuccess;
     const unsigned grid = grid_cap((n_hint + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
     if (!apply) {
@@ -499,14 +499,14 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
         static const cudaError_t attr =
             cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileBytes);
         if (attr != cudaSuccess) return attr;
-        apply_tma_kernel<<<tgrid, kValThreads, 2 * kTileBytes, s>>>(v, lv.base, n_hint, ctr, d_restore);
-        restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+        apply_tma_kernel<<<tgrid, kValThreads, 2 * kTileBytes, s>>>(v, lv.base, n_hint, ctr, rq);
+        restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, rq);
         return cudaGetLastError();
     }
-    if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
-    else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
-    else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
-    restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, d_restore);
+    if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
+    else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
+    else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
+    restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, rq);
     return cudaGetLastError();
 }
 
@@ -536,16 +536,16 @@ cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, 
 }
 
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
-                            DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
-    return launch_view(v, LogView{d_log, n, nullptr, 0, 0}, n, apply, ctr, d_restore, g, s);
+                            DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g, cudaStream_t s) {
+    return launch_view(v, LogView{d_log, n, nullptr, 0, 0}, n, apply, ctr, rq, g, s);
 }
 
 cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_base, const unsigned long long* d_counts,
                                     uint32_t n_regions, uint64_t cap, int apply, DevCounters* ctr,
-                                    unsigned long long* d_restore, const LaunchGeom& g, cudaStream_t s) {
+                                    RestoreQueue rq, const LaunchGeom& g, cudaStream_t s) {
     if (n_regions == 0 || n_regions > 64) return cudaErrorInvalidValue;
     // the grid is sized for one region's worth (the expected share); the kernels grid-stride over the total
-    return launch_view(v, LogView{d_base, 0, d_counts, n_regions, cap}, cap, apply, ctr, d_restore, g, s);
+    return launch_view(v, LogView{d_base, 0, d_counts, n_regions, cap}, cap, apply, ctr, rq, g, s);
 }
 
 // Clean re-apply of the round log onto the device replica whose device write
@@ -553,12 +553,12 @@ cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_
 // ran after an earlier apply may have replaced some), apply the whole log
 // again (apply + restore kernels), copy the logged words to devShadow.
 cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
-                                    DevCounters* ctr, unsigned long long* d_restore, const LaunchGeom& g,
+                                    DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g,
                                     cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const unsigned grid = grid_cap(n, kValThreads, g, 8);
     untag_log_kernel<<<grid, kValThreads, 0, s>>>(v.cells, v.base, v.size_words, d_log, n);
-    cudaError_t e = launch_validate(v, d_log, n, 1, ctr, d_restore, g, s);
+    cudaError_t e = launch_validate(v, d_log, n, 1, ctr, rq, g, s);
     if (e != cudaSuccess) return e;
     if (shadow) log_to_shadow_kernel<<<grid, kValThreads, 0, s>>>(shadow, v.cells, v.base, v.size_words, d_log, n);
     return cudaGetLastError();

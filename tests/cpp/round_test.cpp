@@ -10,7 +10,8 @@
 // plus host replica == device replica and the bank sum.
 //
 //   round_test [rounds] [log2 words] [batch] [host threads] [conflict every k] [host|device] [starvation k]
-//              [batches per round] [early validation 1|0]
+//              [batches per round] [early validation 1|0] [cutoff chunks] [bus delay us/unit]
+//              [host tx per thread per round (0: until the cut-off)] [early-validation period k]
 // policy host (FavorHost, default) or device (FavorDevice: a conflicting round
 // is HostAborted, S' = device batch replay on S, host effects discarded).
 // conflict every k = 1 makes every round conflict (starvation-guard test).
@@ -49,6 +50,10 @@ int main(int argc, char** argv) {
     const uint32_t starvation_k = argc > 7 ? (uint32_t)std::atoi(argv[7]) : 3;
     const uint32_t n_batches = argc > 8 ? (uint32_t)std::atoi(argv[8]) : 1;
     const bool early = argc > 9 ? std::atoi(argv[9]) != 0 : true;
+    const uint32_t cutoff = argc > 10 ? (uint32_t)std::atoi(argv[10]) : 4;
+    const double bus_delay = argc > 11 ? std::atof(argv[11]) : 0.0;
+    const uint64_t per_thread_arg = argc > 12 ? std::strtoull(argv[12], nullptr, 10) : 1500;
+    const uint32_t ev_period = argc > 13 ? (uint32_t)std::atoi(argv[13]) : 8;
     const uint64_t W = 1ull << log2w, half = W / 2;
 
     hetm_dev_config cfg;
@@ -80,7 +85,12 @@ int main(int argc, char** argv) {
     ec.keep_round_log = true;
     ec.policy = favor_device ? Policy::FavorDevice : Policy::FavorHost;
     ec.starvation_k = starvation_k;
+    ec.cutoff_chunks = cutoff;
+    ec.bus_real_delay_us_per_unit = bus_delay;
+    ec.ev_period = ev_period;
     Engine eng(dev, stm, log, host, ec);
+    double blocked_ms = 0;
+    uint64_t cutoff_chunks = 0, log_total = 0;
 
     std::vector<uint64_t> ref(host, host + W), dev_words(W), tickets((uint64_t)B * n_batches), order((uint64_t)B * n_batches);
     std::vector<orc_bank_tx> txs((uint64_t)B * n_batches);
@@ -94,7 +104,7 @@ int main(int argc, char** argv) {
         for (uint32_t k = 0; k < n_batches; ++k)  // device partition [0, W/2)
             orc_gen_bank_batch(1000 + 64 * r + k, B, 0, half, txs.data() + (uint64_t)k * B);
         std::fill(tickets.begin(), tickets.end(), ~0ull);
-        const uint64_t per_thread = 1500;
+        const uint64_t per_thread = per_thread_arg ? per_thread_arg : ~0ull;
         auto worker = [&](int t, const RoundContext& ctx) -> uint64_t {
             uint64_t s = orc_splitmix64(7919u * r + t + 1), done = 0;
             for (uint64_t k = 0; k < per_thread && !ctx.stop.load(std::memory_order_relaxed); ++k) {
@@ -126,6 +136,9 @@ int main(int argc, char** argv) {
             return true;
         }, worker);
         batches_total += rep.dev_batches;
+        blocked_ms += rep.host_blocked_ms;
+        cutoff_chunks += rep.cutoff_chunks;
+        log_total += rep.log_entries;
         if (rep.outcome == Outcome::DeviceAborted) wasted += rep.dev_committed;
         n_conflict += rep.conflict;
         n_cut += rep.cut_short;
@@ -171,11 +184,13 @@ int main(int argc, char** argv) {
     }
     std::printf("{\"rounds\": %d, \"ok\": %d, \"policy\": \"%s\", \"host_commits\": %llu, \"dev_commits\": %llu, "
                 "\"conflict_rounds\": %llu, \"cut_short\": %llu, \"guard_rounds\": %llu, \"max_consecutive_device_aborts\": %u, "
-                "\"host_aborts\": %llu, \"device_batches\": %llu, \"wasted_device_tx\": %llu}\n",
+                "\"host_aborts\": %llu, \"device_batches\": %llu, \"wasted_device_tx\": %llu, "
+                "\"host_blocked_ms\": %.3f, \"cutoff_chunks\": %llu, \"log_entries\": %llu, \"staging_buffers\": %zu}\n",
                 rounds, (int)ok, favor_device ? "FavorDevice" : "FavorHost", (unsigned long long)host_total,
                 (unsigned long long)dev_total, (unsigned long long)n_conflict, (unsigned long long)n_cut,
                 (unsigned long long)n_guard, max_run_aborts, (unsigned long long)stm.aborts(),
-                (unsigned long long)batches_total, (unsigned long long)wasted);
+                (unsigned long long)batches_total, (unsigned long long)wasted, blocked_ms,
+                (unsigned long long)cutoff_chunks, (unsigned long long)log_total, eng.stagingBuffers());
     hetm_host_free(host);
     hetm_dev_close(dev);
     return ok ? 0 : 1;

@@ -15,10 +15,12 @@ def test_binding_compiles_against_reference_headers(hetm, tmp_path):
     lib_dir = os.path.dirname(hetm.LIB_PATH)
     subprocess.check_call(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
                            "-I", REF_INC, os.path.join(ROOT, "tests", "cpp", "binding_smoke.cpp"),
-                           "-L", lib_dir, "-l:libhetm_b200.so", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)])
+                           "-L", lib_dir, "-l:libhetm_b200.so", f"-Wl,-rpath,{lib_dir}", "-pthread", "-o", str(exe)])
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     if hetm.device_count() == 0:
         assert r.returncode == 3 and "no-cuda-device" in r.stdout  # no CPU fallback
+        # the host half ran on the reference types: hetm::TxAbort caught, OutOfBoundsError thrown
+        assert "1 TxAbort retries" in r.stdout and "oob=1" in r.stdout and "sum_ok=1" in r.stdout
     else:
         assert r.returncode == 0, r.stdout + r.stderr
         assert "replicas_match=1" in r.stdout
@@ -33,4 +35,5 @@ def test_prebuilt_binding_runs_a_round_on_the_gpu():
         pytest.skip("build/binding_smoke not built (needs the reference headers at build time)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "replicas_match=1" in r.stdout
+    assert "replicas_match=1" in r.stdout and "oob=1" in r.stdout
+    assert "chunks through a 2-buffer ring" in r.stdout  # staging buffers recycled before the verdict
