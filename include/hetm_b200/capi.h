@@ -71,6 +71,10 @@ enum hetm_bitmap_kind { HETM_BMP_RS = 0, HETM_BMP_WS = 1, HETM_BMP_CHUNK = 2 };
 
 /* validateChunk applyMode. */
 enum hetm_validate_mode { HETM_APPLY = 0, HETM_VALIDATE_ONLY = 1 };
+/* hetm_dev_validate_dptr mode flag: the entries are also copied (D2D) into the
+ * round's log arena, so the incremental shadow refresh and the optimized
+ * rollback cover them (without it the next shadow refresh is a full copy). */
+#define HETM_RETAIN 0x100
 
 /* Built-in transactional kernels (kernels are registered by id). */
 enum hetm_kernel_id {
@@ -465,6 +469,16 @@ int hetm_dev_set_schedule(hetm_dev* dev, int mode);
  * touch host_replica (the host cut-off precedes validation).
  * A no-op without HETM_CFG_MERGE_DELTA or when the write-set log overflowed. */
 int hetm_dev_merge_prepare(hetm_dev* dev, uint64_t* host_replica);
+/* The device half of mergeCommit (HETM_CFG_MERGE_DELTA), fully
+ * asynchronous on the merge stream and without a host round trip: the round's
+ * device write set becomes one {word, value} record per written word in HBM
+ * (claim + emit kernels over the write-set log) and devShadow := devReplica
+ * (the records plus the winners of the round's host log).  The kernels read
+ * the round's verdict themselves: on a conflict (or a write-set log overflow)
+ * they do nothing, so mergeAbortDevice stays exact.  Closes the log intake and
+ * ends the round's execution (later batches: HETM_ERR_STATE).  A following
+ * hetm_dev_merge_commit only ships the staged records to the host replica. */
+int hetm_dev_merge_stage(hetm_dev* dev);
 
 /* ---------------------------------------------------- checker support -- *
  * Traces for the P1 / P2-dagger consistency checker (the

@@ -293,7 +293,7 @@ public:
         for (int t = 0; t < log_threads(log_); ++t)
             hosts.emplace_back([&, t] { commits[t] = worker(t, ctx); });
         while (!gpu_done.load(std::memory_order_acquire)) {
-            stream_full_chunks(stream_mode, rep);
+            stream_full_chunks(stream_mode, rep, &gpu_done);  // the execution phase's end is noticed between chunks
             int c = 0;
             if (cfg_.early_validation && !rep.cut_short && hetm_dev_poll_conflict(dev_, &c) == HETM_OK && c) {
                 // a conflict already decides the round: FavorHost dooms the device's
@@ -473,14 +473,19 @@ private:
             std::this_thread::sleep_for(std::chrono::duration<double, std::micro>(cost * cfg_.bus_real_delay_us_per_unit));
         }
     }
-    void stream_full_chunks(int mode, RoundReport& rep) {
+    void stream_full_chunks(int mode, RoundReport& rep, const std::atomic<bool>* until = nullptr) {
         for (int t = 0; t < log_threads(log_); ++t)
-            while (log_count(log_, t) - shipped_[t] >= cfg_.chunk_entries) ship(t, cfg_.chunk_entries, mode, rep);
+            while (log_count(log_, t) - shipped_[t] >= cfg_.chunk_entries) {
+                if (until && until->load(std::memory_order_acquire)) return;
+                ship(t, cfg_.chunk_entries, mode, rep);
+            }
     }
+    // every unshipped entry, in chunks of at most chunk_entries (host workers
+    // may still be appending during the hostCutoff window)
     void stream_tail(RoundReport& rep, int mode) {
         for (int t = 0; t < log_threads(log_); ++t) {
-            const uint64_t left = log_count(log_, t) - shipped_[t];
-            if (left) ship(t, left, mode, rep);
+            const uint64_t end = log_count(log_, t);
+            while (end > shipped_[t]) ship(t, std::min<uint64_t>(end - shipped_[t], cfg_.chunk_entries), mode, rep);
         }
     }
     void stream_all(int mode, RoundReport& rep) {

@@ -168,6 +168,7 @@ _sigs = {
     "hetm_dev_set_fault": (C.c_int, [_vp, C.c_uint32]),
     "hetm_dev_set_schedule": (C.c_int, [_vp, C.c_int]),
     "hetm_dev_merge_prepare": (C.c_int, [_vp, _vp]),
+    "hetm_dev_merge_stage": (C.c_int, [_vp]),
     "hetm_dev_bitmap_dptr": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "hetm_dev_bitmap_or_peers": (C.c_int, [_vp, C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp]),
     "hetm_dev_timing": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double), u8p]),

@@ -18,6 +18,7 @@ from ._lib import lib
 REPLICA_HOST, REPLICA_DEV, REPLICA_DEV_SHADOW, REPLICA_HOST_SNAPSHOT = 0, 1, 2, 3  # types.hpp:21
 BMP_RS, BMP_WS, BMP_CHUNK = 0, 1, 2
 APPLY, VALIDATE_ONLY = 0, 1
+RETAIN = 0x100  # validate_dptr mode flag: entries join the round arena (capi.h HETM_RETAIN)
 KERNEL_BANK, KERNEL_RW, KERNEL_CACHE = 1, 2, 3
 TRACE_TX_WORDS = 12  # capi.h HETM_TRACE_TX_WORDS
 SCHED_OPTIMISTIC, SCHED_SCAN, SCHED_AUTO = 0, 1, 2  # capi.h HETM_SCHED_* (bank batch schedule)
@@ -471,6 +472,10 @@ class GpuDevice:
         assert out.dtype == np.uint64 and out.flags["C_CONTIGUOUS"]
         self._trace_keep = out
         self._chk(lib.hetm_dev_trace_next_batch(self.h, out.ctypes.data))
+
+    def merge_stage(self):
+        """Device half of mergeCommit, asynchronous (capi.h hetm_dev_merge_stage)."""
+        self._chk(lib.hetm_dev_merge_stage(self.h))
 
     def merge_prepare(self, host_replica: np.ndarray | None = None):
         """Stage the round's delta merge right after the execution phase; with the host

@@ -119,7 +119,8 @@ private:
 struct PreparedMerge {
     bool active = false;
     bool speculative = false;  // the records were swapped into `host` already
-    uint64_t n_slots = 0, k0 = 0, pieces = 0;
+    uint64_t n_slots = 0;      // write-set log slots of the round when staged
+    uint64_t n_rec = 0, k0 = 0, pieces = 0;  // delta records, first DMA'd piece, pieces
     uint64_t round_tx = 0;     // the round's submitted transactions when staged
     uint64_t* host = nullptr;
     int buf = 0;               // delta buffer holding it
@@ -152,9 +153,16 @@ struct hetm_dev {
     uint32_t* d_wlog = nullptr;          // write-set log (2 slots per commit ticket of the round)
     uint64_t wlog_slots = 0;
     uint64_t round_tx = 0;               // transactions submitted this round (ticket upper bound)
-    uint32_t* d_wsorted = nullptr;       // write-set log sorted by word (delta merge)
-    void* d_sort_tmp = nullptr;
-    size_t sort_tmp_bytes = 0;
+    DeltaScratch ds{};                   // delta claim bitmap / unique words / bucket counts (cells.cu)
+    uint64_t* h_nrec = nullptr;          // pinned: record count of the last staged delta
+    cudaEvent_t ev_nrec = nullptr;       // ... landed in h_nrec
+    // hetm_dev_merge_stage: the round's delta staged in HBM + devShadow refreshed
+    // (the device half of mergeCommit), not yet shipped to the host
+    struct {
+        bool active = false;
+        uint64_t round_tx = 0;
+        int buf = 0;
+    } staged;
     // merge delta (device) and its pinned host landing buffer, double-buffered:
     // a round's delta is staged while the worker pool still scatters the
     // previous round's (hetm_dev_merge_prepare)
@@ -179,6 +187,8 @@ struct hetm_dev {
     std::vector<cudaEvent_t> dl_ev;
     uint64_t dl_next = 0, dl_floor = 0;
     std::map<int, hetm_source_stats> sources;  // per source thread, this round
+    uint32_t recv_applied = 0;  // bit p: the peer-arena regions of parity p were applied this round
+    bool merge_staged = false;  // hetm_dev_merge_stage ran this round: no more batches / chunks
     void* d_in = nullptr;
     uint64_t in_cap = 0;
     unsigned long long* d_tk = nullptr;
@@ -476,6 +486,7 @@ extern "C" void cancel_prepare(hetm_dev* d);  // defined with the merge code (C 
 int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, unsigned long long* d_tickets,
                   void* d_results, cudaStream_t s, bool reset_counters = true, unsigned long long* trace = nullptr,
                   bool hot = false) {
+    if (d->merge_staged) return HETM_ERR_STATE;  // the round's merge has started (hetm_dev_merge_stage)
     cancel_prepare(d);  // a new batch of the round: a staged merge would miss it
     if (int rc = ensure_wlog(d, n)) return rc;
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
@@ -580,6 +591,31 @@ int ensure_arena(hetm_dev* d, uint64_t need) {
     return HETM_OK;
 }
 
+// The round's host log on this device: the arena plus the received peer
+// regions applied this round (their counts stay on the device).
+RoundLogs round_logs(hetm_dev* d) {
+    RoundLogs l{};
+    l.flat = d->d_arena;
+    l.n = d->arena_n;
+    for (uint32_t p = 0; p < 2; ++p)
+        if (d->recv_applied & (1u << p))
+            l.region[l.n_regions_sets++] = RoundLogRegions{d->d_recv + (uint64_t)p * d->recv_shards * d->recv_cap,
+                                                           d->d_recv_counts + p * 64, d->recv_shards, d->recv_cap};
+    return l;
+}
+
+// devShadow patch with the winners of the round's host log (the words the
+// validation applied), on s_merge; gate: skipped on the device on a conflict.
+cudaError_t patch_shadow(hetm_dev* d, const DevCounters* gate = nullptr) {
+    const RoundLogs l = round_logs(d);
+    cudaError_t e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, l.flat, l.n, d->geom, d->s_merge,
+                                        gate);
+    for (uint32_t k = 0; k < l.n_regions_sets && e == cudaSuccess; ++k)
+        e = launch_winner_regions(d->d_cells, d->d_shadow, d->base, d->W, l.region[k].base, l.region[k].counts,
+                                  l.region[k].n_regions, l.region[k].cap, d->geom, d->s_merge, gate);
+    return e;
+}
+
 // Dirty chunks of this round as coalesced [offset, bytes) word ranges
 // (adjacent dirty chunks form one transfer descriptor).
 int dirty_ranges(hetm_dev* d, std::vector<std::pair<uint64_t, uint64_t>>& out, uint64_t* n_dirty) {
@@ -614,8 +650,7 @@ int refresh_shadow(hetm_dev* d, bool host_log_applied, uint64_t dirty_bytes) {
                                             true, d->geom, d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "dirty_chunks(shadow)");
         if (host_log_applied) {
-            e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
-                                    d->s_merge);
+            e = patch_shadow(d);
             if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
         }
         d->record(HETM_D2D, HETM_TAG_SHADOW, dirty_bytes);
@@ -812,6 +847,10 @@ int hetm_dev_close(hetm_dev* d) {
     cudaSetDevice(d->device);
     for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
         if (s) cudaStreamSynchronize(s);
+    if (d->prep.active) {  // never merged: leave the host replica as it was
+        std::lock_guard<std::mutex> g(d->mu);
+        cancel_prepare(d);
+    }
     d->pool.reset();
     for (int b = 0; b < 2; ++b) {
         if (d->h_delta[b].loc) cudaFreeHost(d->h_delta[b].loc);
@@ -820,10 +859,6 @@ int hetm_dev_close(hetm_dev* d) {
     }
     for (cudaEvent_t e : d->in_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : d->dl_ev) cudaEventDestroy(e);
-    if (d->prep.active) {  // never merged: leave the host replica as it was
-        std::lock_guard<std::mutex> g(d->mu);
-        cancel_prepare(d);
-    }
     if (d->sched_graph.exec) cudaGraphExecDestroy(d->sched_graph.exec);
     if (d->sched_graph.graph) cudaGraphDestroy(d->sched_graph.graph);
     if (d->sched_graph.cap) cudaStreamDestroy(d->sched_graph.cap);
@@ -834,11 +869,13 @@ int hetm_dev_close(hetm_dev* d) {
         cudaFreeHost(d->h_hot);
     }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->d_wsorted, d->d_sort_tmp, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.n_uniq, (void*)d->ds.bucket_cnt, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
+    if (d->h_nrec) cudaFreeHost(d->h_nrec);
+    if (d->ev_nrec) cudaEventDestroy(d->ev_nrec);
     if (d->h_first) cudaFreeHost(d->h_first);
     for (auto& v : d->tpairs)
         for (auto& pr : v) {
@@ -1388,45 +1425,65 @@ static_assert(kDeltaPiece % 8192 == 0, "host scatter blocks must not straddle pi
 // host replica ends identical to the chunk copy: the words outside the device
 // write set inside a dirty chunk already hold the host's values (the round
 // committed, so no host entry touched a device-read word).
-// Enqueue the delta of the round's device write set: radix sort of the
-// write-set log by word, gather of {word, value} records (refreshing devShadow
-// too when shadow != nullptr), an optional zero-copy head stored by the GPU
-// into the mapped host replica (zc_host), and the DMA of the rest in pieces,
-// each with a completion event.  Returns the first DMA'd piece and the count.
-int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_host, uint64_t* k0_out,
-                uint64_t* pieces_out, uint64_t* bytes_d2h, int* buf_out) {
-    if (n_slots > d->delta_cap) {
-        if (d->pool) d->pool->wait();  // nothing may still read the old buffers
-        CK(d, cudaStreamSynchronize(d->s_merge));
-        CK(d, cudaStreamSynchronize(d->s_d2h));
-        for (int b = 0; b < 2; ++b) {
-            if (d->d_delta[b].loc) { cudaFree(d->d_delta[b].loc); cudaFree(d->d_delta[b].val); d->bytes_alloc -= d->delta_cap * 12; }
-            if (d->h_delta[b].loc) { cudaFreeHost(d->h_delta[b].loc); cudaFreeHost(d->h_delta[b].val); }
-            d->d_delta[b] = DeltaBuf{nullptr, nullptr};
-            d->h_delta[b] = DeltaBuf{nullptr, nullptr};
-        }
-        if (d->d_wsorted) { cudaFree(d->d_wsorted); d->bytes_alloc -= d->delta_cap * 4; d->d_wsorted = nullptr; }
-        if (d->d_sort_tmp) { cudaFree(d->d_sort_tmp); d->bytes_alloc -= d->sort_tmp_bytes; d->d_sort_tmp = nullptr; }
-        const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
-        for (int b = 0; b < 2; ++b) {
-            if (int rc = dev_alloc(d, (void**)&d->d_delta[b].loc, cap * 4)) return rc;
-            if (int rc = dev_alloc(d, (void**)&d->d_delta[b].val, cap * 8)) return rc;
-            if (cudaHostAlloc((void**)&d->h_delta[b].loc, cap * 4, cudaHostAllocPortable) != cudaSuccess ||
-                cudaHostAlloc((void**)&d->h_delta[b].val, cap * 8, cudaHostAllocPortable) != cudaSuccess)
-                return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
-        }
-        if (int rc = dev_alloc(d, (void**)&d->d_wsorted, cap * 4)) return rc;
-        d->sort_tmp_bytes = wlog_sort_temp_bytes(cap, d->W);
-        if (int rc = dev_alloc(d, &d->d_sort_tmp, d->sort_tmp_bytes)) return rc;
-        d->delta_cap = cap;
+// Grow the delta buffers to hold n_slots records (records <= slots), the
+// pinned landing buffers with them, and the claim bitmap (W bits, kept zero
+// between stages by the emit kernel).
+int ensure_delta(hetm_dev* d, uint64_t n_slots) {
+    if (!d->ds.claim) {
+        const uint64_t words = (d->W + 63) / 64;
+        if (int rc = dev_alloc(d, (void**)&d->ds.claim, words * 8)) return rc;
+        CK(d, cudaMemset(d->ds.claim, 0, words * 8));
+        if (int rc = dev_alloc(d, (void**)&d->ds.n_uniq, 8)) return rc;
+        if (int rc = dev_alloc(d, (void**)&d->ds.bucket_cnt, 2 * kDeltaBuckets * sizeof(uint32_t))) return rc;
+        if (cudaHostAlloc((void**)&d->h_nrec, 64, cudaHostAllocPortable) != cudaSuccess)
+            return fail(d, cudaGetLastError(), "cudaHostAlloc(record count)");
+        CK(d, cudaEventCreateWithFlags(&d->ev_nrec, cudaEventDisableTiming));
     }
-    // the other buffer may still feed the worker pool; this one's last job ended
-    // before the pool accepted that one
+    if (n_slots <= d->delta_cap) return HETM_OK;
+    if (d->pool) d->pool->wait();  // nothing may still read the old buffers
+    CK(d, cudaStreamSynchronize(d->s_merge));
+    CK(d, cudaStreamSynchronize(d->s_d2h));
+    for (int b = 0; b < 2; ++b) {
+        if (d->d_delta[b].loc) { cudaFree(d->d_delta[b].loc); cudaFree(d->d_delta[b].val); d->bytes_alloc -= d->delta_cap * 12; }
+        if (d->h_delta[b].loc) { cudaFreeHost(d->h_delta[b].loc); cudaFreeHost(d->h_delta[b].val); }
+        d->d_delta[b] = DeltaBuf{nullptr, nullptr};
+        d->h_delta[b] = DeltaBuf{nullptr, nullptr};
+    }
+    if (d->ds.uniq) { cudaFree(d->ds.uniq); d->bytes_alloc -= d->delta_cap * 4; d->ds.uniq = nullptr; }
+    const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
+    for (int b = 0; b < 2; ++b) {
+        if (int rc = dev_alloc(d, (void**)&d->d_delta[b].loc, cap * 4)) return rc;
+        if (int rc = dev_alloc(d, (void**)&d->d_delta[b].val, cap * 8)) return rc;
+        if (cudaHostAlloc((void**)&d->h_delta[b].loc, cap * 4, cudaHostAllocPortable) != cudaSuccess ||
+            cudaHostAlloc((void**)&d->h_delta[b].val, cap * 8, cudaHostAllocPortable) != cudaSuccess)
+            return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
+    }
+    if (int rc = dev_alloc(d, (void**)&d->ds.uniq, cap * 4)) return rc;
+    d->delta_cap = cap;
+    return HETM_OK;
+}
+
+// Device half of the delta merge, on s_merge: the round's n_slots write-set
+// log slots become one {word, value} record per written word in delta buffer
+// `buf` (claim + emit kernels, no sort), devShadow refreshed with the same
+// values when shadow != nullptr.  The record count lands in h_nrec (ev_nrec).
+int stage_records(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, int buf) {
+    if (int rc = ensure_delta(d, n_slots)) return rc;
+    cudaError_t e = launch_delta_claim(d->d_wlog, n_slots, d->W, d->ds, d->geom, d->s_merge);
+    if (e != cudaSuccess) return fail(d, e, "delta_claim");
+    CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_merge));
+    CK(d, cudaEventRecord(d->ev_nrec, d->s_merge));
+    e = launch_delta_emit(n_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow, d->geom, d->s_merge);
+    if (e != cudaSuccess) return fail(d, e, "delta_emit");
+    CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
+    return HETM_OK;
+}
+
+// The other delta buffer (the one the worker pool is not scattering from) and
+// the host worker pool, created on first use.
+int next_delta_buffer(hetm_dev* d) {
     const int b = d->dbuf;
     d->dbuf ^= 1;
-    const DeltaBuf dd = d->d_delta[b];
-    const DeltaBuf hd = d->h_delta[b];
-    std::vector<cudaEvent_t>& pev = d->piece_ev[b];
     if (!d->pool) {
         // this process's share of the usable cores (torchrun runs one process
         // per GPU: LOCAL_WORLD_SIZE), one core left to the controller thread
@@ -1444,18 +1501,25 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
         const unsigned n = want ? want : std::min(32u, share > 1 ? share - 1 : 1u);
         d->pool.reset(new WorkerPool((int)std::max(1u, n)));
     }
-    cudaError_t e = launch_wlog_sort(d->d_wlog, d->d_wsorted, n_slots, d->W, d->d_sort_tmp, d->sort_tmp_bytes,
-                                     d->s_merge);
-    if (e != cudaSuccess) return fail(d, e, "wlog_sort");
-    e = launch_wlog_gather(dd, shadow, d->d_cells, d->d_wsorted, n_slots, d->W, d->geom, d->s_merge);
-    if (e != cudaSuccess) return fail(d, e, "wlog_gather");
-    CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
+    return b;
+}
+
+// Host half: DMA the staged records of `buf` in pieces (each with a completion
+// event), after their count is known; the first n_zc records optionally go
+// into the mapped host replica as zero-copy stores instead.
+int ship_records(hetm_dev* d, int buf, uint64_t* zc_host, uint64_t* n_rec_out, uint64_t* k0_out,
+                 uint64_t* pieces_out, uint64_t* bytes_d2h) {
+    CK(d, cudaEventSynchronize(d->ev_nrec));  // the claim pass is done (~15 us after the batch)
+    const uint64_t n_rec = *reinterpret_cast<volatile uint64_t*>(d->h_nrec);
+    const DeltaBuf dd = d->d_delta[buf];
+    const DeltaBuf hd = d->h_delta[buf];
+    std::vector<cudaEvent_t>& pev = d->piece_ev[buf];
     CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_stage, 0));
     uint64_t n_zc = 0;
     if (zc_host) {
-        // Split: the first n_zc sorted records are stored into the host replica
-        // by the GPU itself (zero-copy PCIe writes, s_zc) while the copy engine
-        // and the host workers deliver the rest — two independent paths.
+        // Split: the first n_zc records are stored into the host replica by the
+        // GPU itself (zero-copy PCIe writes, s_zc) while the copy engine and the
+        // host workers deliver the rest — two independent paths.
         static const double zc_frac = [] {
             const char* e = std::getenv("HETM_ZC_FRACTION");
             // 0 since the host scatter prefetches: the zero-copy stores then only
@@ -1465,7 +1529,7 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
         cudaPointerAttributes pa{};
         if (zc_frac > 0 && cudaPointerGetAttributes(&pa, zc_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
             pa.devicePointer) {
-            n_zc = std::min<uint64_t>(n_slots, (uint64_t)(zc_frac * (double)n_slots)) / kDeltaPiece * kDeltaPiece;
+            n_zc = std::min<uint64_t>(n_rec, (uint64_t)(zc_frac * (double)n_rec)) / kDeltaPiece * kDeltaPiece;
             if (n_zc) {
                 CK(d, cudaStreamWaitEvent(d->s_zc, d->ev_stage, 0));
                 cudaError_t ez = launch_delta_zc_scatter(static_cast<uint64_t*>(pa.devicePointer), dd, n_zc,
@@ -1477,7 +1541,7 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
             cudaGetLastError();
         }
     }
-    const uint64_t pieces = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
+    const uint64_t pieces = (n_rec + kDeltaPiece - 1) / kDeltaPiece;
     while (pev.size() < pieces) {
         cudaEvent_t ev = nullptr;
         CK(d, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1485,22 +1549,22 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
     }
     const uint64_t k0 = n_zc / kDeltaPiece;  // pieces already delivered by the zero-copy kernel
     for (uint64_t k = k0; k < pieces; ++k) {
-        const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
+        const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_rec - lo);
         CK(d, cudaMemcpyAsync(hd.loc + lo, dd.loc + lo, m * 4, cudaMemcpyDeviceToHost, d->s_d2h));
         CK(d, cudaMemcpyAsync(hd.val + lo, dd.val + lo, m * 8, cudaMemcpyDeviceToHost, d->s_d2h));
         CK(d, cudaEventRecord(pev[k], d->s_d2h));
     }
-    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_slots - n_zc) * 12);
-    *bytes_d2h = n_zc * 8 + (n_slots - n_zc) * 12;
+    d->record(HETM_D2H, HETM_TAG_MERGE_DELTA, (n_rec - n_zc) * 12);
+    *bytes_d2h = n_zc * 8 + (n_rec - n_zc) * 12;
     if (n_zc) {  // the merge is complete when both paths are
         CK(d, cudaEventRecord(d->ev_copy_zc, d->s_zc));
         CK(d, cudaStreamWaitEvent(d->s_d2h, d->ev_copy_zc, 0));
     }
     CK(d, cudaEventRecord(d->ev_d2h, d->s_d2h));
     d->d2h_pending = true;
+    *n_rec_out = n_rec;
     *k0_out = k0;
     *pieces_out = pieces;
-    *buf_out = b;
     return HETM_OK;
 }
 
@@ -1510,7 +1574,7 @@ int stage_delta(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, uint64_t* zc_ho
 // so UNDO can put the replica back (records are unique per word).
 enum ScatterMode { kScatterPlain, kScatterSwap, kScatterUndo };
 
-void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_slots, uint64_t k0, uint64_t pieces,
+void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_rec, uint64_t k0, uint64_t pieces,
                    ScatterMode mode) {
     const DeltaBuf src = d->h_delta[buf];
     const std::vector<cudaEvent_t> evs(d->piece_ev[buf].begin(), d->piece_ev[buf].begin() + pieces);
@@ -1527,14 +1591,14 @@ void start_scatter(hetm_dev* d, int buf, uint64_t* host, uint64_t n_slots, uint6
     auto st = std::make_shared<ScatterState>();
     st->cursor = k0 * kDeltaPiece;
     st->landed = mode == kScatterUndo ? pieces : k0;  // undo runs on records already in place
-    d->pool->start([src, evs, host, n_slots, dev, st, mode](int, int) {
+    d->pool->start([src, evs, host, n_rec, dev, st, mode](int, int) {
         cudaSetDevice(dev);
         constexpr uint64_t kBlock = 8192;   // records per claim (divides kDeltaPiece)
         constexpr uint64_t kPrefetch = 64;  // prefetch-for-write distance, see below
         for (;;) {
             const uint64_t a = st->cursor.fetch_add(kBlock, std::memory_order_relaxed);
-            if (a >= n_slots) return;
-            const uint64_t b = std::min(a + kBlock, n_slots), k = a / kDeltaPiece;
+            if (a >= n_rec) return;
+            const uint64_t b = std::min(a + kBlock, n_rec), k = a / kDeltaPiece;
             while (st->landed.load(std::memory_order_acquire) <= k) {
                 if (st->waiter.try_lock()) {  // the others spin on `landed`, not in the driver
                     // block on the next missing piece: a tight cudaEventQuery loop
@@ -1576,7 +1640,7 @@ void cancel_prepare(hetm_dev* d) {
     if (!d->prep.active) return;
     d->pool->wait();
     if (d->prep.speculative) {
-        start_scatter(d, d->prep.buf, d->prep.host, d->prep.n_slots, d->prep.k0, d->prep.pieces, kScatterUndo);
+        start_scatter(d, d->prep.buf, d->prep.host, d->prep.n_rec, d->prep.k0, d->prep.pieces, kScatterUndo);
         d->pool->wait();
     }
     d->prep = PreparedMerge{};
@@ -1591,8 +1655,9 @@ void cancel_prepare(hetm_dev* d) {
 // values (the round committed, so no host entry touched a device-read word).
 // After hetm_dev_merge_prepare the records are already staged (and, when it
 // got the host replica, already in it): only the shadow is refreshed here.
-int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* bytes_d2h) {
+int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* bytes_d2h, uint64_t* n_rec_out) {
     const bool prepared = d->prep.active && d->prep.round_tx == d->round_tx && d->prep.n_slots == n_slots;
+    const bool staged = !prepared && d->staged.active && d->staged.round_tx == d->round_tx;
     if (!prepared && d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));  // the previous delta
     // shadow: incremental when it held the round-start state, else a full copy
     uint64_t* shadow_inc = (d->d_shadow && d->shadow_synced) ? d->d_shadow : nullptr;
@@ -1607,43 +1672,49 @@ int merge_commit_delta(hetm_dev* d, uint64_t* host, uint64_t n_slots, uint64_t* 
         const PreparedMerge p = d->prep;
         d->prep = PreparedMerge{};
         if (shadow_inc) {
-            cudaError_t e = launch_delta_to_shadow(shadow_inc, d->d_delta[p.buf], n_slots, d->geom, d->s_merge);
-            if (e == cudaSuccess)
-                e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
-                                        d->s_merge);
+            cudaError_t e = launch_delta_to_shadow(shadow_inc, d->d_delta[p.buf], p.n_rec, d->geom, d->s_merge);
+            if (e == cudaSuccess) e = patch_shadow(d);
             if (e != cudaSuccess) return fail(d, e, "shadow(prepared merge)");
-            d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
+            d->record(HETM_D2D, HETM_TAG_SHADOW, p.n_rec * 8);
         }
         CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
         if (!p.speculative || p.host != host) {
             if (p.speculative) {  // prepared for another replica: put that one back first
                 d->pool->wait();
-                start_scatter(d, p.buf, p.host, p.n_slots, p.k0, p.pieces, kScatterUndo);
+                start_scatter(d, p.buf, p.host, p.n_rec, p.k0, p.pieces, kScatterUndo);
                 d->pool->wait();
                 for (uint64_t k = 0; k < p.pieces; ++k) {  // the records hold old values now: restage
-                    const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, n_slots - lo);
+                    const uint64_t lo = k * kDeltaPiece, m = std::min(kDeltaPiece, p.n_rec - lo);
                     CK(d, cudaMemcpyAsync(d->h_delta[p.buf].val + lo, d->d_delta[p.buf].val + lo, m * 8,
                                           cudaMemcpyDeviceToHost, d->s_d2h));
                     CK(d, cudaEventRecord(d->piece_ev[p.buf][k], d->s_d2h));
                 }
             }
-            start_scatter(d, p.buf, host, n_slots, p.k0, p.pieces, kScatterPlain);
+            start_scatter(d, p.buf, host, p.n_rec, p.k0, p.pieces, kScatterPlain);
         }
-        *bytes_d2h = n_slots * 12;
+        *bytes_d2h = p.n_rec * 12;
+        *n_rec_out = p.n_rec;
         return HETM_OK;
     }
     cancel_prepare(d);
-    uint64_t k0 = 0, pieces = 0;
-    int buf = 0;
-    if (int rc = stage_delta(d, n_slots, shadow_inc, host, &k0, &pieces, bytes_d2h, &buf)) return rc;
-    if (shadow_inc) {
-        cudaError_t e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, d->d_arena, d->arena_n, d->geom,
-                                            d->s_merge);
-        if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
-        d->record(HETM_D2D, HETM_TAG_SHADOW, n_slots * 8);
+    int buf;
+    if (staged) {  // hetm_dev_merge_stage did the device half (records + shadow) already
+        buf = d->staged.buf;
+        d->staged.active = false;
+    } else {
+        buf = next_delta_buffer(d);
+        if (int rc = stage_records(d, n_slots, shadow_inc, buf)) return rc;
+        if (shadow_inc) {
+            cudaError_t e = patch_shadow(d);
+            if (e != cudaSuccess) return fail(d, e, "winner_apply(shadow)");
+        }
+        CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
     }
-    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
-    start_scatter(d, buf, host, n_slots, k0, pieces, kScatterPlain);
+    uint64_t n_rec = 0, k0 = 0, pieces = 0;
+    if (int rc = ship_records(d, buf, host, &n_rec, &k0, &pieces, bytes_d2h)) return rc;
+    if (shadow_inc && !staged) d->record(HETM_D2D, HETM_TAG_SHADOW, n_rec * 8);
+    start_scatter(d, buf, host, n_rec, k0, pieces, kScatterPlain);
+    *n_rec_out = n_rec;
     return HETM_OK;
 }
 }  // namespace
@@ -1668,21 +1739,25 @@ int hetm_dev_merge_commit(hetm_dev* d, uint64_t* host, hetm_merge_stats* st) {
     for (auto& r : ranges) dirty_bytes += r.second * 8;
     // delta form when enabled, the write-set log is complete and it moves fewer bytes
     const uint64_t n_slots = 2 * (d->h_ctr->ticket - d->h_ctr->wlog_base);
+    // (a merge prepared for this round has its records in flight or already in
+    // the host replica: it completes as a delta whatever the byte counts)
+    const bool prepared = d->prep.active && d->prep.round_tx == d->round_tx && d->prep.n_slots == n_slots;
     const bool delta = (d->cfg.flags & HETM_CFG_MERGE_DELTA) && d->d_wlog && !d->h_ctr->wlog_overflow &&
-                       n_slots <= d->wlog_slots && n_slots * 12 < dirty_bytes;
+                       n_slots <= d->wlog_slots && (prepared || n_slots * 12 < dirty_bytes);
     if (delta) {
-        uint64_t moved = 0;
-        if ((rc = merge_commit_delta(d, host, n_slots, &moved))) return rc;
+        uint64_t moved = 0, n_rec = 0;
+        if ((rc = merge_commit_delta(d, host, n_slots, &moved, &n_rec))) return rc;
         if (st) {
             std::memset(st, 0, sizeof(*st));
             st->dirty_chunks = nd;
-            st->transfers = (n_slots + kDeltaPiece - 1) / kDeltaPiece;
+            st->transfers = (n_rec + kDeltaPiece - 1) / kDeltaPiece;
             st->bytes_d2h = moved;
-            st->bytes_d2d = d->d_shadow ? n_slots * 8 : 0;
+            st->bytes_d2d = d->d_shadow ? n_rec * 8 : 0;
             st->ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         }
         return HETM_OK;
     }
+    cancel_prepare(d);             // a stale prepared delta (another round) is undone first
     if (d->pool) d->pool->wait();  // a previous delta merge may still be landing in host_replica
     const uint64_t* src = d->d_shadow;
     if (d->d_shadow) {
@@ -1729,19 +1804,60 @@ int hetm_dev_merge_prepare(hetm_dev* d, uint64_t* host) {
     // previous round's; starting this round's job below waits for that one, so
     // host transactions after this call see the previous merge landed
     CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_exec, 0));
-    uint64_t k0 = 0, pieces = 0, moved = 0;
-    int buf = 0;
-    if ((rc = stage_delta(d, n_slots, nullptr, nullptr, &k0, &pieces, &moved, &buf))) return rc;
+    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));  // the previous delta's DMA
+    uint64_t k0 = 0, pieces = 0, moved = 0, n_rec = 0;
+    const int buf = next_delta_buffer(d);
+    d->staged.active = false;
+    if ((rc = stage_records(d, n_slots, nullptr, buf))) return rc;
+    if ((rc = ship_records(d, buf, nullptr, &n_rec, &k0, &pieces, &moved))) return rc;
     d->prep.active = true;
     d->prep.speculative = host != nullptr;
     d->prep.n_slots = n_slots;
+    d->prep.n_rec = n_rec;
     d->prep.k0 = k0;
     d->prep.pieces = pieces;
     d->prep.round_tx = d->round_tx;
     d->prep.host = host;
     d->prep.buf = buf;
-    if (host) start_scatter(d, buf, host, n_slots, k0, pieces, kScatterSwap);
+    if (host) start_scatter(d, buf, host, n_rec, k0, pieces, kScatterSwap);
     else if (d->pool) d->pool->wait();  // still: the previous merge has landed when this returns
+    return HETM_OK;
+}
+
+int hetm_dev_merge_stage(hetm_dev* d) {
+    NvtxRange nvtx_range("hetm.mergeStage");
+    if (!d) return HETM_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(d->mu);
+    if (!(d->cfg.flags & HETM_CFG_MERGE_DELTA) || !d->d_wlog) return HETM_ERR_CONFIG;
+    if (!d->deferred.empty()) return HETM_ERR_STATE;  // every chunk must be applied first
+    cancel_prepare(d);
+    d->intake_open = false;  // the merge has started
+    d->merge_staged = true;
+    int rc = wait_round_work(d, d->s_merge);  // the batches and the validation of the round
+    if (rc) return rc;
+    if (d->d2h_pending) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_d2h, 0));  // the previous delta's DMA
+    uint64_t* shadow_inc = (d->d_shadow && d->shadow_synced) ? d->d_shadow : nullptr;
+    if (d->d_shadow && !d->shadow_synced) {  // gated on the host at merge_commit instead (full copy)
+        d->staged.active = false;
+        return HETM_OK;
+    }
+    const int buf = next_delta_buffer(d);
+    // the slot count and the verdict are read by the kernels themselves: on a
+    // conflict (or a write-set log overflow) they stage nothing and leave
+    // devShadow at the round start, so mergeAbortDevice stays exact
+    if ((rc = ensure_delta(d, d->wlog_slots))) return rc;  // records <= slots in use <= capacity
+    cudaError_t e = launch_delta_claim(d->d_wlog, d->wlog_slots, d->W, d->ds, d->geom, d->s_merge, d->d_ctr);
+    if (e != cudaSuccess) return fail(d, e, "delta_claim(stage)");
+    CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_merge));
+    CK(d, cudaEventRecord(d->ev_nrec, d->s_merge));
+    e = launch_delta_emit(d->wlog_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow_inc, d->geom, d->s_merge);
+    if (e != cudaSuccess) return fail(d, e, "delta_emit(stage)");
+    CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
+    if (shadow_inc && (e = patch_shadow(d, d->d_ctr)) != cudaSuccess) return fail(d, e, "winner_apply(stage)");
+    CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
+    d->staged.active = true;
+    d->staged.round_tx = d->round_tx;
+    d->staged.buf = buf;
     return HETM_OK;
 }
 
@@ -1784,8 +1900,8 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
             e = launch_dirty_chunks(d->d_shadow, d->d_cells, d->W, d->d_chunk, d->chunk_bits, d->chunk_shift, false,
                                     d->geom, d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "restore(rollback)");
-        if ((rc = ensure_restore(d, d->arena_n))) return rc;
-        e = launch_rollback_reapply(d->view(), d->d_shadow, d->d_arena, d->arena_n, d->d_ctr,
+        if ((rc = ensure_restore(d, std::max<uint64_t>(d->arena_n, d->recv_applied ? d->recv_cap : 0)))) return rc;
+        e = launch_rollback_reapply(d->view(), d->d_shadow, round_logs(d), d->d_ctr,
                                     RestoreQueue{d->d_restore, d->restore_cap}, d->geom,
                                     d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "rollback_reapply");
@@ -1905,6 +2021,9 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     d->ev_lo = 0;
     d->ev_pending = 0;
     d->sources.clear();
+    d->recv_applied = 0;
+    d->merge_staged = false;
+    d->staged.active = false;
     d->deferred.clear();
     d->deferred_final = false;
     d->round_applied = false;
@@ -2011,15 +2130,30 @@ uint64_t hetm_cache_set_of(uint64_t key0, uint64_t key1, uint64_t n_sets) {
 
 int hetm_dev_validate_dptr(hetm_dev* d, const hetm_log_entry* d_entries, uint64_t n, int mode, void* stream) {
     if (!d || (n && !d_entries)) return HETM_ERR_INVALID_ARG;
+    const bool retain = (mode & HETM_RETAIN) != 0;
+    mode &= ~HETM_RETAIN;
     if (mode != HETM_APPLY && mode != HETM_VALIDATE_ONLY) return HETM_ERR_INVALID_ARG;
+    if (d->merge_staged) return HETM_ERR_ROUND_CLOSED;  // the merge has started
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->s_val;
     if (mode == HETM_APPLY)
         if (int rc = ensure_restore(d, n)) return rc;
+    if (retain) {  // the entries join the round's arena (D2D), so the shadow patch and the rollback see them
+        std::lock_guard<std::mutex> g(d->mu);
+        if (int rc = ensure_arena(d, d->arena_n + n)) return rc;
+    }
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
+    if (retain && n) {
+        hetm_log_entry* dst = d->d_arena + d->arena_n;
+        CK(d, cudaMemcpyAsync(dst, d_entries, n * sizeof(hetm_log_entry), cudaMemcpyDeviceToDevice, s));
+        d->record(HETM_D2D, HETM_TAG_LOG, n * sizeof(hetm_log_entry));
+        d_entries = dst;
+        d->arena_n += n;
+        d->ev_lo = d->arena_n;
+    }
     if (mode == HETM_APPLY) {
         CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
         d->round_applied = true;
-        d->shadow_synced = false;  // entries are not retained in the arena for the shadow patch
+        if (!retain) d->shadow_synced = false;  // not in the arena: the next shadow refresh is a full copy
     }
     cudaError_t e = timed_validate(d, d_entries, n, mode == HETM_APPLY, s);
     if (e != cudaSuccess) return fail(d, e, "validate_dptr");
@@ -2140,7 +2274,9 @@ int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_
     if (mode == HETM_APPLY) {
         CK(d, cudaStreamWaitEvent(s, d->ev_exec, 0));
         d->round_applied = true;
-        d->shadow_synced = false;  // entries are not retained in the arena for the shadow patch
+        // the regions stay in the receive arena until the next round of this
+        // parity: the shadow patch and the optimized rollback read them there
+        d->recv_applied |= 1u << p;
     }
     // one launch over every received region; the counts stay on the device
     cudaEvent_t t0 = nullptr, t1 = nullptr;

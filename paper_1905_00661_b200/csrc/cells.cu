@@ -4,8 +4,6 @@
 // mergeCommit and the rollback of mergeAbortDevice.
 #include <cstdlib>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -41,23 +39,100 @@ __global__ void dirty_chunks_kernel(uint64_t* __restrict__ plain, Cell* __restri
     }
 }
 
-// mergeCommit delta: out[i] = {word, devReplica value} for every write-set
-// log slot (duplicates carry the same final value; empty slots -> ~0 word),
-// and the same value into devShadow (the incremental shadow refresh).
-__global__ void wlog_gather_kernel(DeltaBuf out, uint64_t* __restrict__ shadow,
-                                   const Cell* __restrict__ cells, const uint32_t* __restrict__ wlog, uint64_t n,
-                                   uint64_t size_words) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t loc = wlog[i];
-        if (loc < size_words && (i == 0 || wlog[i - 1] != loc)) {  // one record per word (the log is sorted)
-            const uint64_t val = cells[loc].value;
-            out.loc[i] = (uint32_t)loc;
-            out.val[i] = val;
-            if (shadow) shadow[loc] = val;
-        } else {
-            out.loc[i] = ~0u;
-            out.val[i] = 0;
+// mergeCommit delta, step 1 of 2 (replaces a radix sort of the log): every
+// write-set log slot claims its word in a W-bit claim bitmap (one returning
+// atomicOr into L2-resident words); the first claimer of a word appends it to
+// the unique-word list (warp-aggregated) and counts it in its address bucket
+// (kDeltaBuckets contiguous word ranges, per-CTA shared histogram).  The
+// write-set log itself is left untouched (the rollback reads it).
+constexpr int kClaimThreads = 256;
+// gate != nullptr (a merge staged before the host has read the verdict): the
+// slot count comes from the device counters and nothing is staged when the
+// round has a conflict or its write-set log overflowed.
+__global__ void __launch_bounds__(kClaimThreads) delta_claim_kernel(const uint32_t* __restrict__ wlog, uint64_t n,
+                                                                    uint64_t size_words, unsigned long long* claim,
+                                                                    uint32_t* __restrict__ uniq,
+                                                                    unsigned long long* n_uniq, uint32_t* bucket_cnt,
+                                                                    uint32_t bshift, const DevCounters* gate) {
+    __shared__ uint32_t hist[kDeltaBuckets];
+    if (gate) {
+        if (gate->conflict || gate->wlog_overflow) return;
+        const uint64_t used = 2 * (gate->ticket - gate->wlog_base);
+        n = used < n ? used : n;
+    }
+    for (int b = threadIdx.x; b < kDeltaBuckets; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const unsigned lane = lane_id();
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = warp * 32; base < n; base += warps * 32) {  // warp-uniform trip count
+        const uint64_t i = base + lane;
+        const uint32_t loc = i < n ? wlog[i] : ~0u;
+        bool first = false;
+        if (loc < size_words) {
+            const unsigned long long m = 1ull << (loc & 63);
+            first = !(atomicOr(&claim[loc >> 6], m) & m);
         }
+        const unsigned ballot = __ballot_sync(0xffffffffu, first);
+        if (!ballot) continue;
+        unsigned long long at = 0;
+        if (lane == (unsigned)(__ffs(ballot) - 1)) at = atomicAdd(n_uniq, (unsigned long long)__popc(ballot));
+        at = __shfl_sync(0xffffffffu, at, __ffs(ballot) - 1);
+        if (first) {
+            uniq[at + __popc(ballot & ((1u << lane) - 1))] = loc;
+            atomicAdd(&hist[loc >> bshift], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kDeltaBuckets; b += blockDim.x)
+        if (hist[b]) atomicAdd(&bucket_cnt[b], hist[b]);
+}
+
+// Step 2: each unique word becomes one {word, value} record at its bucket's
+// next slot (every CTA scans the bucket counts into shared memory), so the
+// delta reaches the host grouped by address range — a host worker's block of
+// records covers one small slice of the replica — and each word appears once
+// (the speculative swap/undo of hetm_dev_merge_prepare needs that).  The same
+// value refreshes devShadow; the claim words are cleared for the next stage.
+__global__ void __launch_bounds__(kClaimThreads) delta_emit_kernel(const uint32_t* __restrict__ uniq,
+                                                                   const unsigned long long* n_uniq,
+                                                                   const uint32_t* __restrict__ bucket_cnt,
+                                                                   uint32_t* cursor, uint32_t bshift,
+                                                                   const Cell* __restrict__ cells, DeltaBuf out,
+                                                                   uint64_t* __restrict__ shadow,
+                                                                   unsigned long long* claim) {
+    __shared__ uint32_t first[kDeltaBuckets];
+    __shared__ uint32_t part[kClaimThreads];
+    constexpr int per = kDeltaBuckets / kClaimThreads;
+    uint32_t run = 0;
+    for (int k = 0; k < per; ++k) run += bucket_cnt[threadIdx.x * per + k];
+    part[threadIdx.x] = run;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // 256 partial sums: serial is fine
+        uint32_t acc = 0;
+        for (int t = 0; t < kClaimThreads; ++t) {
+            const uint32_t x = part[t];
+            part[t] = acc;
+            acc += x;
+        }
+    }
+    __syncthreads();
+    run = part[threadIdx.x];
+    for (int k = 0; k < per; ++k) {
+        first[threadIdx.x * per + k] = run;
+        run += bucket_cnt[threadIdx.x * per + k];
+    }
+    __syncthreads();
+    const uint64_t n = *n_uniq;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t loc = uniq[j];
+        const uint32_t b = loc >> bshift;
+        const uint32_t pos = first[b] + atomicAdd(&cursor[b], 1u);
+        const uint64_t val = cells[loc].value;
+        out.loc[pos] = loc;
+        out.val[pos] = val;
+        if (shadow) shadow[loc] = val;
+        claim[loc >> 6] = 0;
     }
 }
 
@@ -108,41 +183,44 @@ cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_wlog_gather(DeltaBuf out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
-                               uint64_t size_words, const LaunchGeom& g, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    wlog_gather_kernel<<<grid_words(n, g), 256, 0, s>>>(out, shadow, cells, wlog, n, size_words);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_delta_to_shadow(uint64_t* shadow, DeltaBuf d, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     delta_to_shadow_kernel<<<grid_words(n, g), 256, 0, s>>>(shadow, d, n);
     return cudaGetLastError();
 }
 
-// Sort the write-set log by word (CUB onesweep radix sort over the bits a
-// local word index needs): the delta then reaches the host in address order,
-// so each host worker scatters into one contiguous range of the replica.
-// Empty slots (~0u) have all low bits set and sort last (a tie with word
-// 2^bits-1 is harmless: the gather skips empty slots wherever they land).
-static int sort_bits(uint64_t size_words) {
-    int b = 1;
+static uint32_t word_bits(uint64_t size_words) {
+    uint32_t b = 1;
     while (b < 32 && (1ull << b) < size_words) ++b;
     return b;
 }
 
-size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
-                                   sort_bits(size_words));
-    return bytes;
+uint32_t delta_bucket_shift(uint64_t size_words) {
+    const uint32_t b = word_bits(size_words);
+    return b > kDeltaBucketBits ? b - kDeltaBucketBits : 0;
 }
 
-cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
-                             size_t temp_bytes, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int64_t)n, 0, sort_bits(size_words), s);
+cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_words, const DeltaScratch& ds,
+                               const LaunchGeom& g, cudaStream_t s, const DevCounters* gate) {
+    cudaError_t e = cudaMemsetAsync(ds.n_uniq, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ds.bucket_cnt, 0, 2 * kDeltaBuckets * sizeof(uint32_t), s);
+    if (e != cudaSuccess || n == 0) return e;
+    uint64_t want = (n + kClaimThreads - 1) / kClaimThreads;
+    const uint64_t cap = (uint64_t)g.sm_count * 8;
+    delta_claim_kernel<<<(unsigned)(want < cap ? want : cap), kClaimThreads, 0, s>>>(
+        wlog, n, size_words, ds.claim, ds.uniq, ds.n_uniq, ds.bucket_cnt, delta_bucket_shift(size_words), gate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
+                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s) {
+    if (max_records == 0) return cudaSuccess;
+    uint64_t want = (max_records + kClaimThreads - 1) / kClaimThreads;
+    const uint64_t cap = (uint64_t)g.sm_count * 8;
+    delta_emit_kernel<<<(unsigned)(want < cap ? want : cap), kClaimThreads, 0, s>>>(
+        ds.uniq, ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets, delta_bucket_shift(size_words), cells, out,
+        shadow, ds.claim);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,

@@ -49,10 +49,23 @@ cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, 
                                const LaunchGeom& g, cudaStream_t s);  // fault injection only
 cudaError_t launch_validate(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, int apply,
                             DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g, cudaStream_t s);
-// Optimized rollback: untag the logged words, re-apply the round log, copy them to shadow.
-cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
-                                    DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g,
-                                    cudaStream_t s);
+// The round's host log on one device: the arena (flat, in arrival order) and
+// the peer-arena region sets it received this round (multi-GPU exchange).
+struct RoundLogRegions {
+    const hetm_log_entry* base;
+    const unsigned long long* counts;  // device counts of the regions
+    uint32_t n_regions;
+    uint64_t cap;
+};
+struct RoundLogs {
+    const hetm_log_entry* flat;
+    uint64_t n;
+    RoundLogRegions region[2];  // one per round parity applied this round
+    uint32_t n_regions_sets;
+};
+// Optimized rollback: untag the logged words, re-apply the round logs, copy them to shadow.
+cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const RoundLogs& logs, DevCounters* ctr,
+                                    RestoreQueue rq, const LaunchGeom& g, cudaStream_t s);
 // Literal TS reset: every TS word becomes an unlocked word.
 cudaError_t launch_reset_ts(Cell* cells, uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
 // Validate/apply the received regions of a peer arena (counts on the device; no host sync).
@@ -64,7 +77,13 @@ cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_
 // cell's TS goes to dst[addr] (plain array) or, with dst == nullptr, to the
 // cell's value (rollback / shadow patch).
 cudaError_t launch_winner_apply(Cell* cells, uint64_t* dst, uint64_t base, uint64_t size_words,
-                                const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s);
+                                const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s,
+                                const DevCounters* gate = nullptr);
+// The same over received peer-arena regions (counts on the device).
+cudaError_t launch_winner_regions(Cell* cells, uint64_t* dst, uint64_t base, uint64_t size_words,
+                                  const hetm_log_entry* d_base, const unsigned long long* d_counts,
+                                  uint32_t n_regions, uint64_t cap, const LaunchGeom& g, cudaStream_t s,
+                                  const DevCounters* gate = nullptr);
 // Word-cell <-> plain word conversions (cells.cu).
 cudaError_t launch_gather_range(uint64_t* dst, const Cell* cells, uint64_t lo, uint64_t n, const LaunchGeom& g,
                                 cudaStream_t s);
@@ -74,9 +93,24 @@ cudaError_t launch_scatter_range(Cell* cells, const uint64_t* src, uint64_t lo, 
 cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_words, const unsigned long long* bits,
                                 uint64_t n_chunks, uint32_t chunk_shift, bool to_plain, const LaunchGeom& g,
                                 cudaStream_t s);
-// Write-set log -> compact delta (+ devShadow refresh when shadow != nullptr).
-cudaError_t launch_wlog_gather(DeltaBuf out, uint64_t* shadow, const Cell* cells, const uint32_t* wlog, uint64_t n,
-                               uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
+// Write-set log -> compact delta in two hand-written passes (cells.cu): claim
+// (dedup through a W-bit claim bitmap, unique-word list, address-bucket
+// counts), then emit ({word, value} records grouped by bucket, devShadow
+// refreshed when shadow != nullptr, claim words cleared).  The record count
+// is *n_uniq on the device.
+constexpr uint32_t kDeltaBucketBits = 12;
+constexpr int kDeltaBuckets = 1 << kDeltaBucketBits;
+struct DeltaScratch {
+    unsigned long long* claim;      // ceil(W/64) words, all zero between stages
+    uint32_t* uniq;                 // unique words (<= slots)
+    unsigned long long* n_uniq;     // record count
+    uint32_t* bucket_cnt;           // kDeltaBuckets counts, then kDeltaBuckets cursors
+};
+uint32_t delta_bucket_shift(uint64_t size_words);
+cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_words, const DeltaScratch& ds,
+                               const LaunchGeom& g, cudaStream_t s, const DevCounters* gate = nullptr);
+cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
+                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s);
 // Rollback of the device write set: cells[loc].value = shadow[loc] per log slot.
 cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
                                 uint64_t size_words, const LaunchGeom& g, cudaStream_t s);
@@ -133,10 +167,6 @@ cudaError_t launch_or_peers(unsigned long long* dst, const unsigned long long* c
 cudaError_t launch_clear_round(unsigned long long* rs, unsigned long long* ws, uint64_t rs_words,
                                unsigned long long* chunk, uint64_t chunk_words, DevCounters* ctr, int reset_ts,
                                const LaunchGeom& g, cudaStream_t s);
-// Radix sort of n write-set log slots by word (CUB); temp from wlog_sort_temp_bytes.
-size_t wlog_sort_temp_bytes(uint64_t n, uint64_t size_words);
-cudaError_t launch_wlog_sort(const uint32_t* in, uint32_t* out, uint64_t n, uint64_t size_words, void* temp,
-                             size_t temp_bytes, cudaStream_t s);
 // Popcount of n words into *out (device counter, accumulated).
 cudaError_t launch_popcount(const unsigned long long* words, uint64_t n, unsigned long long* out, cudaStream_t s);
 // OR src words into dst words.

@@ -334,10 +334,15 @@ __global__ void __launch_bounds__(kValThreads) restore_kernel(ShardView v, LogVi
 
 // Pass B (dst == nullptr: into the cells' value field) and its variants for
 // the shadow patch / rollback (dst = plain word array): the entry whose ts
-// equals the cell's TS is the freshest one for that word.
+// equals the cell's TS is the freshest one for that word.  Over a flat log or
+// the received regions of a peer arena (LogView); gate != nullptr: nothing is
+// done when the round has a conflict (merge staged before the host knows).
 __global__ void __launch_bounds__(kValThreads) winner_kernel(Cell* cells, uint64_t* dst, uint64_t base,
-                                                             uint64_t size_words, const hetm_log_entry* __restrict__ log,
-                                                             uint64_t n) {
+                                                             uint64_t size_words, LogView lv,
+                                                             const DevCounters* gate) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
+    if (gate && ld_relaxed((const unsigned long long*)&gate->conflict) & 0xffffffffull) return;
     const uint64_t span = (uint64_t)gridDim.x * blockDim.x * kUnroll;
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * kUnroll + threadIdx.x; i0 < n; i0 += span) {
         EntryRegs e[kUnroll];
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(kValThreads) winner_kernel(Cell* cells, uint64
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-            e[u] = i < n ? load_entry(log, i) : EntryRegs{base + size_words, 0, 0};
+            e[u] = i < n ? view_entry(lv, sp, i) : EntryRegs{base + size_words, 0, 0};
         }
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -402,18 +407,21 @@ static unsigned grid_cap(uint64_t items, int threads, const LaunchGeom& g, int p
 // word a TS word reads as (device_tm.cuh), so the batch TM sees no change.
 constexpr unsigned long long kUntagged = 0xffffffffull;
 
-__global__ void untag_log_kernel(Cell* cells, uint64_t base, uint64_t size_words,
-                                 const hetm_log_entry* __restrict__ log, uint64_t n) {
+__global__ void untag_log_kernel(Cell* cells, uint64_t base, uint64_t size_words, LogView lv) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t loc = __ldg(&log[i].addr) - base;
+        const uint64_t loc = view_entry(lv, sp, i).addr - base;
         if (loc < size_words) cells[loc].meta = kUntagged;
     }
 }
 
 __global__ void log_to_shadow_kernel(uint64_t* shadow, const Cell* __restrict__ cells, uint64_t base,
-                                     uint64_t size_words, const hetm_log_entry* __restrict__ log, uint64_t n) {
+                                     uint64_t size_words, LogView lv) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t loc = __ldg(&log[i].addr) - base;
+        const uint64_t loc = view_entry(lv, sp, i).addr - base;
         if (loc < size_words) shadow[loc] = cells[loc].value;
     }
 }
@@ -548,27 +556,52 @@ cudaError_t launch_validate_regions(const ShardView& v, const hetm_log_entry* d_
     return launch_view(v, LogView{d_base, 0, d_counts, n_regions, cap}, cap, apply, ctr, rq, g, s);
 }
 
-// Clean re-apply of the round log onto the device replica whose device write
-// set was restored from devShadow: forget this round's TS words (a batch that
-// ran after an earlier apply may have replaced some), apply the whole log
-// again (apply + restore kernels), copy the logged words to devShadow.
-cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const hetm_log_entry* d_log, uint64_t n,
-                                    DevCounters* ctr, RestoreQueue rq, const LaunchGeom& g,
-                                    cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const unsigned grid = grid_cap(n, kValThreads, g, 8);
-    untag_log_kernel<<<grid, kValThreads, 0, s>>>(v.cells, v.base, v.size_words, d_log, n);
-    cudaError_t e = launch_validate(v, d_log, n, 1, ctr, rq, g, s);
-    if (e != cudaSuccess) return e;
-    if (shadow) log_to_shadow_kernel<<<grid, kValThreads, 0, s>>>(shadow, v.cells, v.base, v.size_words, d_log, n);
+// Clean re-apply of the round's host log (the arena and any received peer
+// regions) onto the device replica whose device write set was restored from
+// devShadow: forget this round's TS words of every logged word first (a batch
+// that ran after an earlier apply may have replaced some), then apply all the
+// logs (apply + restore kernels), then copy the logged words to devShadow.
+cudaError_t launch_rollback_reapply(const ShardView& v, uint64_t* shadow, const RoundLogs& logs, DevCounters* ctr,
+                                    RestoreQueue rq, const LaunchGeom& g, cudaStream_t s) {
+    for (int pass = 0; pass < 3; ++pass) {
+        for (uint32_t k = 0; k <= logs.n_regions_sets; ++k) {
+            const bool flat = k == 0;
+            if (flat && logs.n == 0) continue;
+            const LogView lv = flat ? LogView{logs.flat, logs.n, nullptr, 0, 0}
+                                    : LogView{logs.region[k - 1].base, 0, logs.region[k - 1].counts,
+                                              logs.region[k - 1].n_regions, logs.region[k - 1].cap};
+            const uint64_t hint = flat ? logs.n : lv.cap;
+            const unsigned grid = grid_cap(hint, kValThreads, g, 8);
+            if (pass == 0) {
+                untag_log_kernel<<<grid, kValThreads, 0, s>>>(v.cells, v.base, v.size_words, lv);
+            } else if (pass == 1) {
+                cudaError_t e = launch_view(v, lv, hint, 1, ctr, rq, g, s);
+                if (e != cudaSuccess) return e;
+            } else if (shadow) {
+                log_to_shadow_kernel<<<grid, kValThreads, 0, s>>>(shadow, v.cells, v.base, v.size_words, lv);
+            }
+        }
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_winner_apply(Cell* cells, uint64_t* dst, uint64_t base, uint64_t size_words,
-                                const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s) {
+                                const hetm_log_entry* d_log, uint64_t n, const LaunchGeom& g, cudaStream_t s,
+                                const DevCounters* gate) {
     if (n == 0) return cudaSuccess;
     const unsigned grid = grid_cap((n + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
-    winner_kernel<<<grid, kValThreads, 0, s>>>(cells, dst, base, size_words, d_log, n);
+    winner_kernel<<<grid, kValThreads, 0, s>>>(cells, dst, base, size_words, LogView{d_log, n, nullptr, 0, 0}, gate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_winner_regions(Cell* cells, uint64_t* dst, uint64_t base, uint64_t size_words,
+                                  const hetm_log_entry* d_base, const unsigned long long* d_counts,
+                                  uint32_t n_regions, uint64_t cap, const LaunchGeom& g, cudaStream_t s,
+                                  const DevCounters* gate) {
+    if (n_regions == 0 || n_regions > 64) return cudaErrorInvalidValue;
+    const unsigned grid = grid_cap((cap + kUnroll - 1) / kUnroll, kValThreads, g, g.max_blocks_val);
+    winner_kernel<<<grid, kValThreads, 0, s>>>(cells, dst, base, size_words,
+                                               LogView{d_base, 0, d_counts, n_regions, cap}, gate);
     return cudaGetLastError();
 }
 
