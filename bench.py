@@ -1,27 +1,42 @@
 #!/usr/bin/env python
-"""bench.py — Speculative HeTM GPU-side path on B200 (BASELINE.json metric).
+"""bench.py — Speculative HeTM GPU-side path on B200 (BASELINE.json metric:
+"committed GPU tx/s (synthetic bank) 1 B200; validate+apply GB/s at 1/2/4/8 GPUs").
 
-Workload (BASELINE.json configs[1], per GPU): 1 GiB STMR shard (2^27 words),
-one 2^20-transaction bank batch per round (4 reads / 2 writes, uniform, on the
-GPU half of the shard), and the round's host write log (2^20 entries of
-<addr,value,ts>, uniform over the host halves of ALL shards) validated against
-the GPU read-set bitmap (1 KiB granules) with the TS-guarded apply.
+Headline workload (BASELINE.json configs[1], per GPU): 1 GiB STMR shard (2^27
+words), one 2^20-transaction bank batch per round (4 reads / 2 writes,
+uniform, on the GPU half of the shard), and the round's host write log (2^20
+entries of <addr,value,ts>, uniform over the host halves of ALL shards)
+validated against the GPU read-set bitmap (1 KiB granules) with the
+TS-guarded apply.
 
 One step = one synchronization round of the device side:
-    executeBatch (bank kernel) -> [G>1: route log by owner shard + NCCL
-    all-to-all] -> validateChunk(apply) -> round clear.
+    executeBatch (bank kernel) -> [G>1: fused route to the owner shards over
+    NVLink] -> validateChunk(apply) -> device half of mergeCommit
+    (hetm_dev_merge_stage: write-set records + devShadow refresh) -> round clear.
 `value` = committed GPU tx/s over all ranks, device-timed with CUDA events,
 inputs resident in HBM (rotating per-step buffers; 1 GiB STMR >> L2).
 `e2e` = the same rounds through the C-ABI host-buffer calls: H2D batch input,
-H2D log stream, verdict, D2H tickets, mergeCommit D2H of dirty chunks.
+H2D log stream, verdict, D2H tickets, mergeCommit D2H into the host replica.
+`e2e_live` = Engine::runRound with a LIVE TL2 host producer (build/hetm_live_round).
+`configs` = BASELINE configs[2] (zipf 0.99, conflict + rollback rounds) and
+configs[3] (cache GET/SET 90/10), device-resident, at N = 1.
+`validate_apply` = BASELINE configs[4]: a 64 GiB STMR sharded 64/G GiB per GPU,
+global CPU write logs of 16 MiB .. 4 GiB, each rank ingesting 1/G and routing
+entries to their owner shard over NVLink (fused route kernel, peer stores),
+then validate + TS-guarded apply; aggregate GB/s at every N.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+`torch.distributed.run` with N ranks (one per GPU); fewer visible GPUs than N
+is an error.  --plan prints the configuration line without touching a GPU.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,14 +52,21 @@ METRIC = "committed GPU tx/s (synthetic bank) 1 B200; validate+apply GB/s at 1/2
 UNIT = "tx/s"
 TX_BYTES = 224     # 24 B input + 8 B ticket + 4x32 B STMR sector reads + 2x32 B write-backs
 ENTRY_BYTES = 120  # 24 B log + 32 B TS read + 32 B TS write + 32 B STMR sector write
+LOG_ENTRY_WIRE = 24  # write_log.hpp:25 kLogEntryWireBytes
+NOMINAL_HBM_GBS = 8000.0  # north_star's nominal B200 HBM3e bandwidth (report both fractions)
 
 
-def parse():
+def one_gpu_mode() -> bool:
+    return os.environ.get("HETM_BENCH_ONE_GPU") == "1"
+
+
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--plan", action="store_true", help="print the configuration line only (no GPU work)")
     p.add_argument("--words-log2", type=int, default=27)
     p.add_argument("--batch", type=int, default=1 << 20)
     p.add_argument("--log-entries", type=int, default=1 << 20)
@@ -57,7 +79,21 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=8.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-preroll", action="store_true", help="skip the clock-sampling pre-roll (profiling runs)")
-    return p.parse_args()
+    p.add_argument("--live-rounds", type=int, default=12, help="e2e_live rounds (0: skip)")
+    p.add_argument("--no-configs", action="store_true", help="skip the configs[2]/[3] sub-lines")
+    p.add_argument("--config-rounds", type=int, default=8)
+    p.add_argument("--cfg5-words-log2", type=int, default=None,
+                   help="global STMR of the validate_apply sweep (default 2^33 = 64 GiB; 2^28 in one-GPU mode)")
+    p.add_argument("--cfg5-log-mib", default=None,
+                   help="global log sizes of the sweep, MiB (default 16,256,1024,4096; 1,16 in one-GPU mode)")
+    p.add_argument("--cfg5-reps", type=int, default=3)
+    p.add_argument("--no-cfg5", action="store_true")
+    a = p.parse_args(argv)
+    if a.cfg5_words_log2 is None:
+        a.cfg5_words_log2 = 28 if one_gpu_mode() else 33
+    if a.cfg5_log_mib is None:
+        a.cfg5_log_mib = "1,16" if one_gpu_mode() else "16,256,1024,4096"
+    return a
 
 
 # ---------------------------------------------------------------- clocks
@@ -118,28 +154,24 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# Random 16-B accesses on a 1 GiB footprint, measured on B200 (tools/microbench.cu,
-# profiles/r01_microbench_random_access.txt): L2-missing loads and read-modify-writes per second.
-RANDOM_LOAD_PER_S, RANDOM_RMW_PER_S = 42.6e9, 22.6e9
+# ------------------------------------------------------------- rooflines
+# The bank kernel with every protocol step knocked out (P1 snapshot loads and
+# the P5 stores only: HETM_KNOCKOUT=64 in an EXPERIMENTS=1 build of the same
+# kernel, same 2^20-tx batch on the 2^27-word STMR, 1 CTA/SM), measured on B200:
+# profiles/r01_bank_kernel_knockouts.txt.  The product's protocol (lock CAS,
+# ticket, read-set validation, bitmaps) costs the difference.
+PROTOCOL_FLOOR_MS = 0.1148
 
 
-def access_ceiling(tx_per_s, traffic, kernel_ms, peak):
-    """The bank kernel's access-pattern bound beside the copy roofline: a transfer
-    needs 4 random cell loads (P1) and 2 random RMWs of written cells (lock CAS,
-    then the 128-bit commit store hitting the same line) — no schedule of the
-    protocol issues fewer line fills.  Model time per tx = 4/load rate + 2/RMW rate."""
-    ceil = 1.0 / (4 / RANDOM_LOAD_PER_S + 2 / RANDOM_RMW_PER_S)
-    out = {"model": "4 random loads + 2 random RMWs per tx at the measured random-access rates",
-           "load_per_s": RANDOM_LOAD_PER_S, "rmw_per_s": RANDOM_RMW_PER_S,
-           "source": "profiles/r01_microbench_random_access.txt", "tx_per_s_ceiling": ceil,
-           "kernel_tx_per_s": tx_per_s, "frac": tx_per_s / ceil}
+def protocol_floor(kernel_ms, traffic, peak):
+    out = {"model": "same kernel, every protocol step knocked out (P1 loads + P5 stores only, HETM_KNOCKOUT=64)",
+           "source": "profiles/r01_bank_kernel_knockouts.txt", "floor_kernel_ms": PROTOCOL_FLOOR_MS,
+           "floor_tx_per_s": (1 << 20) / (PROTOCOL_FLOOR_MS * 1e-3),
+           "kernel_over_floor": kernel_ms / PROTOCOL_FLOOR_MS}
     if traffic:
         dram_gbs = traffic / (kernel_ms * 1e-3) / 1e9
         out.update({"dram_gbs": dram_gbs, "dram_frac_of_peak": dram_gbs / peak})
     return out
-
-
-NOMINAL_HBM_GBS = 8000.0  # north_star's nominal B200 HBM3e bandwidth (SURVEY.md §8d: report both fractions)
 
 
 def measured_traffic(kernel):
@@ -160,22 +192,50 @@ def peaks():
 
 
 # ----------------------------------------------------------- distributed
-def dist_setup(args):
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """--gpus N honoured: outside torchrun, N > 1 re-launches this script under
+    torch.distributed.run with N local ranks; inside it, WORLD_SIZE must be N."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus and not (args.gpus == 1 and "--gpus" not in sys.argv):
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
+        return
+    if args.gpus <= 1:
+        return
+    if not args.plan and not one_gpu_mode() and args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, {have} visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dist_setup():
     """One process per GPU over NCCL.  HETM_BENCH_BACKEND=gloo with
     HETM_BENCH_ONE_GPU=1 runs the N-rank protocol with every rank on GPU 0
     (a functional test of the multi-rank path on a single-GPU box)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("HETM_BENCH_ONE_GPU") == "1":
+    if one_gpu_mode():
         local = 0
     pg = None
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         backend = os.environ.get("HETM_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -185,14 +245,25 @@ def dist_setup(args):
 
 def all_reduce(dist, t, op=None):
     """all_reduce that also works for a CPU-only backend (gloo test mode)."""
-    import torch
-
     if os.environ.get("HETM_BENCH_BACKEND", "nccl") == "nccl":
         dist.all_reduce(t, op=op) if op is not None else dist.all_reduce(t)
         return t
     c = t.cpu()
     dist.all_reduce(c, op=op) if op is not None else dist.all_reduce(c)
     return c.to(t.device)
+
+
+def max_over_ranks(dist, values):
+    """Element-wise max of a list of floats over all ranks (CPU tensors work for both backends)."""
+    if not dist:
+        return list(values)
+    import torch
+    if os.environ.get("HETM_BENCH_BACKEND", "nccl") == "nccl":
+        t = torch.tensor(list(values), dtype=torch.float64, device="cuda")
+    else:
+        t = torch.tensor(list(values), dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().tolist()
 
 
 def host_log_slice(hetm, seed, n_entries, world, W, rank, ts_base):
@@ -206,6 +277,22 @@ def host_log_slice(hetm, seed, n_entries, world, W, rank, ts_base):
     return log
 
 
+def cfg5_plan(args, world):
+    """Geometry of the configs[4] sweep and the NVLink bytes it moves per round
+    (DESIGN.md §6): each rank ingests 1/G of the global log; (G-1)/G of its
+    entries belong to another shard and are stored into the owner's arena."""
+    total = 1 << args.cfg5_words_log2
+    out = []
+    for mib in [int(x) for x in args.cfg5_log_mib.split(",")]:
+        n_global = (mib << 20) // LOG_ENTRY_WIRE
+        n_local = n_global // world
+        out.append({"log_mib_global": mib, "entries_global": n_local * world, "entries_ingested_per_rank": n_local,
+                    "nvlink_bytes_out_per_rank": int(n_local * LOG_ENTRY_WIRE * (world - 1) / world),
+                    "nvlink_bytes_total": int(n_local * LOG_ENTRY_WIRE * (world - 1))})
+    return {"stmr_words_global": total, "stmr_gib_global": total * 8 / 2**30, "shard_words": total // world,
+            "shard_gib": total * 8 / 2**30 / world, "sizes": out}
+
+
 # -------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -213,7 +300,7 @@ def run_ours(args):
     import paper_1905_00661_b200 as hetm
     from paper_1905_00661_b200.shard import PeerValidator, ShardedValidator
 
-    world, rank, local, dist = dist_setup(args)
+    world, rank, local, dist = dist_setup()
     torch.cuda.set_device(local)
     W = 1 << args.words_log2
     base = rank * W
@@ -264,16 +351,21 @@ def run_ours(args):
         sv = ShardedValidator(dev, world, W, L, dist, s_val)
         if world > 1:
             exchange = "router -> NCCL all_to_all"
+    # entries validated from device memory join the round arena (HETM_RETAIN), so
+    # the device half of mergeCommit refreshes devShadow incrementally
+    val_mode = hetm.APPLY | (hetm.RETAIN if world == 1 else 0)
+    merge_dev = not args.chunk_merge
 
-
-    def step(j, timed_idx=None):
+    def step(j):
         tb = tx_d[j % n_bufs]
         dev.execute_batch_dptr(hetm.KERNEL_BANK, tb.data_ptr(), B, tickets.data_ptr(), s_exec)
         lg = log_d[j]
         with torch.cuda.stream(vs):  # router, exchange and validation share the validation stream
-            n_local = sv.validate(lg, hetm.APPLY)
+            n_local = sv.validate(lg, val_mode)
         if n_local is None:  # fused peer exchange on NCCL: counts stay on the device; every entry has one owner
             n_local = L
+        if merge_dev:
+            dev.merge_stage()  # device half of mergeCommit: write-set records + devShadow refresh
         dev.clear_round(asynchronous=True)
         return n_local
 
@@ -297,11 +389,12 @@ def run_ours(args):
             if j % 8 == 0:
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
-        dev.timing(0), dev.timing(1)
-        dev.set_timing(True)  # CUDA-event brackets around every batch / validation launch
+        for w in (0, 1, 2):
+            dev.timing(w)
+        dev.set_timing(True)  # CUDA-event brackets around every batch / validation / merge-stage launch
         start.record(ex)
         for i in range(K):
-            n_val += step(WU + i, i)
+            n_val += step(WU + i)
         # join every device stream back into s_exec before the stop event
         for sidx in (1, 2, 3, 4):
             other = torch.cuda.ExternalStream(dev.stream_handle(sidx))
@@ -318,29 +411,32 @@ def run_ours(args):
     assert not conflict
     bt, bc = dev.timing(0)
     vt, vc = dev.timing(1)
+    mt, mc = dev.timing(2)
     dev.set_timing(False)
-    batch_ms, val_ms = bt / max(bc, 1), vt / K  # validation: all launches of a step (G regions with the peer exchange)
+    batch_ms, val_ms, mstage_ms = bt / max(bc, 1), vt / K, mt / K
     if dist:
-        t = torch.tensor([ms_total, batch_ms, val_ms], dtype=torch.float64, device="cuda")
-        t = all_reduce(dist, t, op=dist.ReduceOp.MAX)
-        ms_total, batch_ms, val_ms = t.tolist()
+        ms_total, batch_ms, val_ms, mstage_ms = max_over_ranks(dist, [ms_total, batch_ms, val_ms, mstage_ms])
         nv = torch.tensor([n_val], dtype=torch.int64, device="cuda")
         nv = all_reduce(dist, nv)
         n_val = int(nv.item())
 
-    # correctness spot check after timing: bank sum preserved on the device
+    # correctness spot checks after timing: bank sum preserved; devShadow == devReplica
     dev_words = dev.download(hetm.REPLICA_DEV, base + 0, W // 2)
     bank_sum_ok = int(dev_words.sum(dtype=np.uint64)) == 1000 * (W // 2)
+    shadow_ok = None
+    if merge_dev and world == 1:
+        shadow_ok = bool((dev.download(hetm.REPLICA_DEV_SHADOW) == dev.download(hetm.REPLICA_DEV)).all())
+    del tx_d, log_d, base_log_t
+    torch.cuda.empty_cache()
 
     # ---- end-to-end through the host-buffer C-ABI (pinned host memory)
     e2e = run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist)
-
     ms_step = ms_total / K
-    # our kernels per step (the ncu launch list in profiles/ shows the same set):
-    # bank_batch_kernel (+ the AUTO schedule's side-stream hot_estimate_kernel), apply_kernel +
-    # restore_kernel, clear_round_kernel (async clear: bitmaps zeroed + round counters rolled)
-    launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_kernel": 1, "restore_kernel": 1,
-                       "clear_round_kernel": 1}
+    # our kernels per step (the ncu launch list in profiles/ shows the same set)
+    launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_kernel": 1, "restore_kernel": 1}
+    if merge_dev:
+        launches_detail.update({"delta_claim_kernel": 1, "delta_emit_kernel": 1, "winner_kernel": 1})
+    launches_detail["clear_round_kernel"] = 1
     if world > 1 and isinstance(sv, PeerValidator):
         launches_detail.update({"route_count_kernel": 1, "route_scan_kernel": 1, "route_peer_publish_kernel": 1,
                                 "route_peer_scatter_kernel": 1})
@@ -358,10 +454,12 @@ def run_ours(args):
         "config": {
             "workload": "BASELINE configs[1]: bank, 1 GiB STMR per GPU, 2^20-tx GPU batch per round, 4R/2W "
                         "uniform, RS/WS gran 1 KiB; round host log 2^20 entries on the host halves, "
-                        "validated+applied (routed by owner shard over NCCL when G>1)",
+                        "validated+applied (routed to the owner shard over NVLink when G>1); device half of "
+                        "mergeCommit (write-set records + devShadow refresh) in every step",
             "stmr_words_per_gpu": W, "batch_tx": B, "log_entries_per_gpu": L, "rs_gran_bytes": args.gran,
             "stmr_layout": "16-B word cells {value, lock-or-TS}", "parallelism": f"shard{world}",
             "log_exchange": exchange,
+            "step": "executeBatch -> validateChunk(apply) -> merge_stage -> clearRound",
             "l2": "inputs larger than L2: 1 GiB STMR per GPU, rotating per-step input buffers "
                   f"({n_bufs} tx batches + {n_steps} logs, {(n_bufs * B * 24 + n_steps * L * 24) >> 20} MiB)",
         },
@@ -371,28 +469,37 @@ def run_ours(args):
                      "traffic": measured_traffic("bank_batch_kernel"),
                      "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per launch)",
                      "algorithmic_bytes_per_tx": TX_BYTES, "kernel_ms": batch_ms,
-                     "access_pattern_ceiling": access_ceiling(B / (batch_ms * 1e-3), measured_traffic("bank_batch_kernel"),
-                                                              batch_ms, peak)},
-        "validate_apply": {"kernel": "apply_kernel", "gbs_algorithmic": val_gbs,
-                           "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
-                           "log_gbs_per_gpu": 24 * (n_val / K / world) / (val_ms * 1e-3) / 1e9,
-                           "frac": val_gbs / peak, "frac_nominal": val_gbs / NOMINAL_HBM_GBS,
-                           "algorithmic_bytes_per_entry": ENTRY_BYTES,
-                           "traffic": measured_traffic("validate_apply"),
-                           "kernel_ms": val_ms, "aggregate_gbs": val_gbs * world},
+                     "kernel_share_of_step": batch_ms / ms_step,
+                     "protocol_floor": protocol_floor(batch_ms, measured_traffic("bank_batch_kernel"), peak)},
+        "step_breakdown_ms": {"batch": batch_ms, "validate_apply": val_ms, "merge_stage": mstage_ms,
+                              "step": ms_step},
+        "validate_apply_cfg2": {"kernel": "apply_kernel", "gbs_algorithmic": val_gbs,
+                                "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
+                                "frac": val_gbs / peak, "algorithmic_bytes_per_entry": ENTRY_BYTES,
+                                "traffic": measured_traffic("validate_apply"), "kernel_ms": val_ms},
         "batch": {"committed_last": int(st.committed), "aborts_last": int(st.aborts)},
-        "bank_sum_ok": bank_sum_ok,
+        "bank_sum_ok": bank_sum_ok, "shadow_equals_replica": shadow_ok,
         "e2e": e2e,
         "gpu_launches": K * launches_per_step,
         "gpu_launches_per_step": launches_detail,
         "clocks": clk.summary(),
         "input_gen_s": gen_s,
     }
+    dev.close()
+    host_replica.free()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    if rank == 0 and world == 1 and args.live_rounds > 0:
+        line["e2e_live"] = run_live(args)
+    if world == 1 and not args.no_configs:
+        line["configs"] = run_configs(args, hetm, torch)
+    if not args.no_cfg5:
+        line["validate_apply"] = run_cfg5(args, hetm, torch, world, rank, local, dist, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, seconds=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    dev.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -409,10 +516,12 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
     ts0 = 10_000_000_000
     for j, p in enumerate(logs):  # produced by host txs before the round: not timed
         hetm.gen_host_log(900 + j, L // 2, 2, 8, base + W // 2, W // 2, ts_base=ts0 + j * L, out=p.array)
-    info = dev.info()
     dev.sync()
-    conflict, _ = dev.read_counters()
+    dev.read_counters()
     dev.clear_round()  # synchronous clear: refresh the TS floor after the pipelined rounds
+    # the device-timed loop staged its merges without shipping them: realign the
+    # host replica's device half first (raw read under quiescence)
+    host_replica.array[:W // 2] = dev.download(hetm.REPLICA_DEV, base, W // 2)
     tickets = hetm.PinnedArray((B,), np.uint64)
     import ctypes as C
     lib = hetm._lib.lib
@@ -455,14 +564,15 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
     dev.merge_wait()
     dt = time.perf_counter() - t0
     if dist:
-        import torch
-        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        t = all_reduce(dist, t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
+        dt = max_over_ranks(dist, [dt])[0]
+    # the host replica holds the host's own commits on its half; the device half must match the device
+    dev_half = dev.download(hetm.REPLICA_DEV, base, W // 2)
+    replica_ok = bool((host_replica.array[:W // 2] == dev_half).all())
     for p in txs + logs + [tickets]:
         p.free()
     return {"value": world * B * steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
+            "host_replica_matches_device": replica_ok,
             "merge": ("chunk copy (SPEC.md:363-371)" if args.chunk_merge else
                       "delta (12-B {word,value} per device-written word)" +
                       (", staged + speculatively applied right after the execution phase (hetm_dev_merge_prepare)"
@@ -473,35 +583,257 @@ def run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist):
                       "replica before the next round's host log; the next GPU batch overlaps the merge, PAPER.md:355)"}
 
 
+def run_live(args):
+    """e2e with a LIVE producer (SURVEY.md §8f row 1): Engine::runRound at
+    configs[1] scale, TL2 host workers committing on the host half while the
+    GPU runs the batch; hostCutoff 4, early validation every 8 chunks."""
+    exe = os.path.join(ROOT, "build", "hetm_live_round")
+    if not os.path.exists(exe):
+        return {"error": "build/hetm_live_round not built (run __graft_entry__.build())"}
+    cmd = [exe, str(args.live_rounds), str(args.words_log2), str(args.batch)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    except subprocess.TimeoutExpired:
+        return {"error": "timeout"}
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    if out.returncode != 0 or not lines:
+        return {"error": f"rc {out.returncode}: {(out.stdout + out.stderr)[-400:]}"}
+    r = json.loads(lines[-1])
+    r.update({"value": r["tx_per_s"], "unit": "tx/s (host + device commits)", "driver": "build/hetm_live_round",
+              "timing": "host wall clock over full rounds (first round warm-up); host replica and device batch "
+                        "inputs in pinned host memory, logs streamed through the pinned staging ring"})
+    return r
+
+
+def _device_rounds_time(fn, rounds, torch):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = [fn(r) for r in range(rounds)]
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, res
+
+
+def run_configs(args, hetm, torch):
+    """BASELINE configs[2] and [3] on one GPU, device-resident inputs."""
+    out = {}
+    B = args.batch
+    R = args.config_rounds
+    # ---- configs[2]: zipf 0.99 on both sides over the same 1 GiB STMR -> conflict
+    # every round unless the starvation guard (K = 3, SPEC.md:390-398) makes the
+    # host read-only; FavorHost: DeviceAborted -> optimized mergeAbortDevice.
+    W = 1 << args.words_log2
+    d = hetm.GpuDevice(W, rs_gran_bytes=args.gran, log_capacity=B, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_BANK)
+    d.upload(hetm.REPLICA_DEV, 0, np.full(W, 1000, np.uint64))
+    d.merge_commit(np.full(W, 1000, np.uint64))
+    d.merge_wait()
+    d.clear_round()
+    bats = [torch.from_numpy(hetm.gen_bank_batch(60 + k, B, 0, W, zipf=0.99).view(np.uint8)).cuda() for k in range(2)]
+    logs = []
+    for r in range(R + 1):
+        lg = hetm.gen_host_log(70 + r, B // 2, 2, 8, 0, W, ts_base=(r + 1) << 32, zipf=0.99)
+        logs.append(torch.from_numpy(lg.view(np.uint64).reshape(-1, 3).astype(np.int64)).cuda())
+    tk = torch.empty(B, dtype=torch.int64, device="cuda")
+    K_GUARD = 3
+    state = {"aborts_in_row": 0}
+
+    def zipf_round(r):  # r = -1: warm-up
+        guard = state["aborts_in_row"] >= K_GUARD  # read-only host round: no write log
+        d.execute_batch_dptr(hetm.KERNEL_BANK, bats[r % 2].data_ptr(), B, tk.data_ptr())
+        if not guard:  # logs[r + 1]: ts monotone across the warm-up and the timed rounds
+            lg = logs[r + 1]
+            d.validate_dptr(lg.data_ptr(), lg.shape[0], hetm.APPLY | hetm.RETAIN)
+        conflict = d.round_verdict()
+        _, st = d.read_counters()
+        if conflict:
+            d.merge_abort_device(None, optimized=True)
+            state["aborts_in_row"] += 1
+        else:
+            d.merge_stage()
+            state["aborts_in_row"] = 0
+        d.clear_round()
+        return conflict, int(st.committed), int(st.aborts)
+
+    zipf_round(-1)  # warm-up: a conflicting round (also builds the SCAN graph) ...
+    state["aborts_in_row"] = K_GUARD
+    zipf_round(-1)  # ... and a read-only host round, which commits (sizes the merge buffers)
+    state["aborts_in_row"] = 0
+    dt, res = _device_rounds_time(zipf_round, R, torch)
+    committed = sum(c for conflict, c, _ in res if not conflict)
+    out["cfg3_zipf"] = {
+        "workload": "BASELINE configs[2]: bank 2^20-tx batches, accounts zipf(0.99) over the whole 1 GiB STMR; "
+                    "host log 2^20 entries zipf(0.99) over the same range -> conflict; FavorHost, optimized "
+                    "rollback, starvation guard K=3 (read-only host round after 3 device aborts)",
+        "value": committed / dt, "unit": "committed GPU tx/s", "rounds": R, "ms_per_round": dt / R * 1e3,
+        "device_aborted_rounds": sum(1 for c, _, _ in res if c),
+        "batch_aborted_attempts": sum(a for _, _, a in res),
+        "schedule": "AUTO (hot batch -> SCAN)",
+        "timing": "host wall clock, device-resident inputs; verdict read and rollback synchronous every round"}
+    d.close()
+    del bats, logs
+    torch.cuda.empty_cache()
+
+    # ---- configs[3]: MemcachedGPU-style cache, 2^20 sets x 8 ways, GET/SET 90/10,
+    # keys zipf(0.5) over 4 M keys on the GPU's half (last key bit, PAPER.md:489)
+    n_sets = 1 << 20
+    Wc = n_sets * 64
+    d = hetm.GpuDevice(Wc, rs_gran_bytes=args.gran, merge_delta=True)
+    d.register_kernel(hetm.KERNEL_CACHE)
+    d.merge_commit(np.zeros(Wc, np.uint64))
+    d.merge_wait()
+    d.clear_round()
+    res_t = torch.empty(B * 40, dtype=torch.uint8, device="cuda")
+    warm = torch.from_numpy(hetm.gen_cache_batch(1, B, 1 << 22, 0.5, get_permille=0, part=1).view(np.uint8)).cuda()
+    d.execute_batch_dptr(hetm.KERNEL_CACHE, warm.data_ptr(), B, tk.data_ptr(), 0, res_t.data_ptr())
+    d.merge_stage()
+    d.clear_round()
+    cb = [torch.from_numpy(hetm.gen_cache_batch(10 + k, B, 1 << 22, 0.5, get_permille=900, part=1).view(np.uint8)).cuda()
+          for k in range(4)]
+
+    def cache_round(r):
+        d.execute_batch_dptr(hetm.KERNEL_CACHE, cb[r % 4].data_ptr(), B, tk.data_ptr(), 0, res_t.data_ptr())
+        d.merge_stage()
+        d.clear_round(asynchronous=True)
+        return 0
+
+    cache_round(0)
+    d.sync()
+    d.set_timing(True)
+    d.timing(0)
+    dt, _ = _device_rounds_time(cache_round, R, torch)
+    bt, bc = d.timing(0)
+    d.set_timing(False)
+    _, st = d.read_counters()
+    out["cfg4_cache"] = {
+        "workload": "BASELINE configs[3]: set-associative cache 2^20 sets x 8 ways x 64 B in the STMR (512 MiB), "
+                    "2^20 GET/SET per batch 90/10, keys zipf(0.5) over 4 M keys on the GPU's half",
+        "value": B * R / dt, "unit": "committed GPU tx/s", "rounds": R, "ms_per_round": dt / R * 1e3,
+        "batch_kernel_ms": bt / max(bc, 1), "batch_tx_per_s": B / (bt / max(bc, 1) * 1e-3),
+        "schedule": "AUTO (>= 8192 tx -> SCAN: sort by set, one thread per set segment)",
+        "timing": "host wall clock over pipelined device rounds (batch + merge_stage + async clear), "
+                  "device-resident inputs"}
+    d.close()
+    del cb, warm, res_t, tk
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_cfg5(args, hetm, torch, world, rank, local, dist, peak):
+    """BASELINE configs[4]: validate + apply of global CPU write logs over a
+    sharded STMR (64 GiB over G GPUs).  Each rank ingests 1/G of the global log
+    (uniform over all 2^33 words); at G > 1 the fused route kernel stores every
+    entry into its owner's receive arena over NVLink (PeerValidator), a device
+    barrier, then every owner validates + applies what it received.  Times are
+    CUDA events on the validation stream around route + exchange + apply, max
+    over ranks."""
+    from paper_1905_00661_b200.shard import PeerValidator
+
+    plan = cfg5_plan(args, world)
+    Wg = plan["stmr_words_global"]
+    Ws = plan["shard_words"]
+    base = rank * Ws
+    d = hetm.GpuDevice(Ws, shard_base=base, rs_gran_bytes=1024, device=local, shadow=False, log_capacity=1 << 20)
+    s_val = d.stream_handle(2)
+    vs = torch.cuda.ExternalStream(s_val)
+    # RS bitmap at density 1e-3 of its bits (SURVEY.md §8d cfg5), seeded per shard
+    nbits = Ws * 8 // 1024
+    rng = np.random.default_rng(1234 + rank)
+    bits = rng.integers(0, nbits, max(1, nbits // 1000)).astype(np.uint64)
+    rs = np.zeros((nbits + 63) // 64, np.uint64)
+    np.bitwise_or.at(rs, (bits >> np.uint64(6)).astype(np.int64), np.left_shift(np.uint64(1), bits & np.uint64(63)))
+    n_max = max(s["entries_ingested_per_rank"] for s in plan["sizes"])
+    pv = None
+    exchange = "none (1 shard)"
+    if world > 1:
+        pv = PeerValidator(d, world, rank, Ws, n_max, dist, s_val)
+        exchange = "fused route kernel -> NVLink peer stores into the owner's arena (CUDA IPC); NCCL 4-B device barrier"
+    g = torch.Generator(device="cuda").manual_seed(99 + rank)
+    log = torch.empty((n_max, 3), dtype=torch.int64, device="cuda")
+    ts_next = 1
+    rows = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for sz in plan["sizes"]:
+        n = sz["entries_ingested_per_rank"]
+        lg = log[:n]
+        lg[:, 0] = torch.randint(0, Wg, (n,), device="cuda", generator=g)
+        lg[:, 1] = torch.randint(-(1 << 62), 1 << 62, (n,), device="cuda", generator=g)
+        times = []
+        for r in range(args.cfg5_reps + 1):
+            d.clear_round()  # rolls the TS floor: every rep is a fresh round
+            d.or_bitmap(hetm.BMP_RS, rs)
+            # globally unique, monotone ts: rank-interleaved
+            lg[:, 2] = torch.arange(ts_next, ts_next + n, device="cuda", dtype=torch.int64) * world + rank
+            ts_next += n
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            ev0.record(vs)
+            if pv is not None:
+                with torch.cuda.stream(vs):
+                    pv.validate(lg, hetm.APPLY)
+            else:
+                d.validate_dptr(lg.data_ptr(), n, hetm.APPLY, s_val)
+            ev1.record(vs)
+            torch.cuda.synchronize()
+            if r:
+                times.append(ev0.elapsed_time(ev1))
+        ms = max_over_ranks(dist, [statistics.median(times)])[0]
+        conflict = d.round_verdict()
+        n_glob = sz["entries_global"]
+        gbs = ENTRY_BYTES * n_glob / (ms * 1e-3) / 1e9
+        rows.append({**sz, "ms": ms, "entries_per_s": n_glob / (ms * 1e-3), "gbs_algorithmic": gbs,
+                     "frac": gbs / (world * peak), "frac_nominal": gbs / (world * NOMINAL_HBM_GBS),
+                     "log_gbs": LOG_ENTRY_WIRE * n_glob / (ms * 1e-3) / 1e9, "conflict": bool(conflict)})
+    if pv is not None:
+        pv.close()
+    d.close()
+    del log
+    torch.cuda.empty_cache()
+    head = next((r for r in rows if r["log_mib_global"] == 1024), rows[-1])
+    return {"workload": f"BASELINE configs[4]: {plan['stmr_gib_global']:.0f} GiB STMR sharded {plan['shard_gib']:.0f} "
+                        f"GiB per GPU (no shadow), global CPU write logs uniform over the STMR, RS density 1e-3 at "
+                        "1 KiB granules",
+            "n_gpus": world, "exchange": exchange, "kernel": "apply_kernel (+ route_peer_scatter_kernel at G>1)",
+            "headline_log_mib": head["log_mib_global"], "gbs_algorithmic": head["gbs_algorithmic"],
+            "aggregate_gbs": head["gbs_algorithmic"], "frac": head["frac"], "peak_per_gpu": peak,
+            "algorithmic_bytes_per_entry": ENTRY_BYTES, "entries_per_s": head["entries_per_s"],
+            "sweep": rows, "geometry": {k: v for k, v in plan.items() if k != "sizes"},
+            "timing": "CUDA events on the validation stream around route + NVLink delivery + apply, median of "
+                      f"{args.cfg5_reps} reps, max over ranks"}
+
+
 # ---------------------------------------------------------- CPU baseline
 def cpu_baseline(args, seconds=8.0, rounds=None):
-    """The reference CPU path (oracle port, multi-threaded) on a bounded sample
-    of the same round: one bank batch (guest-stm-batch worker pool)
-    + validate/apply of the round's log on all host threads."""
+    """The reference CPU path (oracle port, multi-threaded) on the SAME round as
+    the GPU step: one 2^20-tx bank batch (guest-stm-batch worker pool,
+    SPEC.md:237) + validate/apply of the round's 2^20-entry log
+     on all host threads, 2^27-word STMR."""
     import oracle as O
 
     threads = os.cpu_count() or 1
     W = 1 << args.words_log2
-    B = args.batch // 4
-    L = args.log_entries // 4
+    B = args.batch
+    L = args.log_entries
     s = np.full(W, 1000, np.uint64)
     ts = np.zeros(W, np.uint64)
     gran = args.gran
-    rs = np.zeros(((W * 8 // gran) + 63) // 64, np.uint64)
-    done_tx, t_tot, r = 0, 0.0, 0
-    while (rounds is None and t_tot < seconds) or (rounds is not None and r < rounds):
+    done_tx, t_tot, t_val, r = 0, 0.0, 0.0, 0
+    while (rounds is None and (t_tot < seconds or r < 2)) or (rounds is not None and r < rounds):
         txs = O.gen_bank_batch(3000 + r, B, 0, W // 2)
         log = O.gen_host_log(4000 + r, L // 2, 2, 8, W // 2, W // 2, ts_base=r * L)
-        rs[:] = 0
         t0 = time.perf_counter()
         c, _, rsb, _, _ = O.mt_bank_batch(s, txs, threads, lock_entries=1 << 24, gran=gran, tickets=False)
+        t1 = time.perf_counter()
         O.mt_validate_apply(log, rsb, gran, ts, s, threads)
-        t_tot += time.perf_counter() - t0
+        t2 = time.perf_counter()
+        t_tot += t2 - t0
+        t_val += t2 - t1
         done_tx += c
         r += 1
     return {"value": done_tx / t_tot, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{r} rounds x ({B} bank tx + {L} log entries) on the 2^{args.words_log2}-word STMR "
-                      f"(1/4 of a GPU round), oracle/hetm_oracle.c pthreads",
+            "sample": f"{r} full rounds x ({B} bank tx + {L} log entries) on the 2^{args.words_log2}-word STMR "
+                      "(the GPU step's configuration), oracle/hetm_oracle.c pthreads",
+            "validate_apply_entries_per_s": r * L / t_val, "rounds": r, "ms_per_round": t_tot / r * 1e3,
             "host": host_info()}
 
 
@@ -531,9 +863,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # warmup rounds untimed, then K timed rounds
     import oracle  # noqa: F401  (builds the checker if needed)
-    cpu_baseline(args, rounds=max(1, args.warmup // 2))
+    cpu_baseline(args, rounds=max(1, min(args.warmup, 3)))  # warm-up rounds, untimed
     t0 = time.perf_counter()
     cb = cpu_baseline(args, rounds=args.steps)
     dt = time.perf_counter() - t0
@@ -541,16 +872,45 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "BASELINE configs[1] (bounded per-step sample, see cpu_baseline.sample)",
-                       "stmr_words": 1 << args.words_log2},
+            "config": {"workload": "BASELINE configs[1]: one full round per step (2^20 bank tx + 2^20 log "
+                                   "entries, 2^27-word STMR), identical to the GPU arm's step",
+                       "stmr_words": 1 << args.words_log2, "batch_tx": args.batch,
+                       "log_entries": args.log_entries},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def run_plan(args):
+    """Configuration line without GPU work: exercises the rank spawn and the
+    process group (gloo on CPU), reports the geometry and NVLink byte counts."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(os.environ.get("HETM_BENCH_BACKEND", "gloo"))
+        import torch
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        assert int(t.item()) == world
+    line = {"metric": METRIC, "plan": True, "n_gpus": world, "rank_count_checked": world,
+            "config": {"stmr_words_per_gpu": 1 << args.words_log2, "batch_tx": args.batch,
+                       "log_entries_per_gpu": args.log_entries, "parallelism": f"shard{world}"},
+            "validate_apply": cfg5_plan(args, world)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    maybe_spawn(args)
+    if args.plan:
+        run_plan(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -422,7 +422,9 @@ int hetm_enable_peer_access(int device, int peer_device);
 /* Streams owned by the handle: 0 = execution, 1 = log copy, 2 = validation, 3 = merge. */
 int hetm_dev_stream_handle(hetm_dev* dev, int which, void** stream);
 /* Per-kernel device timing (CUDA events around every batch / validation
- * launch of this handle).  which: 0 = batch kernels, 1 = validation kernels.
+ * launch of this handle).  which: 0 = batch kernels, 1 = validation kernels,
+ * 2 = the device half of mergeCommit (hetm_dev_merge_stage: claim, emit,
+ * shadow refresh).
  * hetm_dev_timing waits for the recorded launches, returns their summed
  * duration and count, and resets the accumulator. */
 int hetm_dev_set_timing(hetm_dev* dev, int on);

@@ -189,6 +189,9 @@ struct hetm_dev {
     std::map<int, hetm_source_stats> sources;  // per source thread, this round
     uint32_t recv_applied = 0;  // bit p: the peer-arena regions of parity p were applied this round
     bool merge_staged = false;  // hetm_dev_merge_stage ran this round: no more batches / chunks
+    // every batch of the round committed with per-word versions (bank / rw
+    // kernels): the delta merge picks words by version instead of claiming them
+    bool round_versioned = true;
     void* d_in = nullptr;
     uint64_t in_cap = 0;
     unsigned long long* d_tk = nullptr;
@@ -247,7 +250,7 @@ struct hetm_dev {
     uint64_t l2_bytes = 0;
     hetm_batch_stats last_batch{};
     bool timing = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tpairs[2];  // recorded launch brackets
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tpairs[3];  // recorded launch brackets: batch, validation, merge stage
     std::vector<cudaEvent_t> tpool;
 
     cudaEvent_t tev() {
@@ -489,6 +492,7 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     if (d->merge_staged) return HETM_ERR_STATE;  // the round's merge has started (hetm_dev_merge_stage)
     cancel_prepare(d);  // a new batch of the round: a staged merge would miss it
     if (int rc = ensure_wlog(d, n)) return rc;
+    if (kernel_id == HETM_KERNEL_CACHE) d->round_versioned = false;  // set-granular locks: claim the words
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
     if (reset_counters) CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
@@ -869,7 +873,7 @@ int hetm_dev_close(hetm_dev* d) {
         cudaFreeHost(d->h_hot);
     }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.n_uniq, (void*)d->ds.bucket_cnt, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.uniq_val, (void*)d->ds.n_uniq, (void*)d->ds.bucket_cnt, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in})
         if (p) cudaFree(p);
@@ -1433,7 +1437,7 @@ int ensure_delta(hetm_dev* d, uint64_t n_slots) {
         const uint64_t words = (d->W + 63) / 64;
         if (int rc = dev_alloc(d, (void**)&d->ds.claim, words * 8)) return rc;
         CK(d, cudaMemset(d->ds.claim, 0, words * 8));
-        if (int rc = dev_alloc(d, (void**)&d->ds.n_uniq, 8)) return rc;
+        if (int rc = dev_alloc(d, (void**)&d->ds.n_uniq, 16)) return rc;  // records, slots (pick pass)
         if (int rc = dev_alloc(d, (void**)&d->ds.bucket_cnt, 2 * kDeltaBuckets * sizeof(uint32_t))) return rc;
         if (cudaHostAlloc((void**)&d->h_nrec, 64, cudaHostAllocPortable) != cudaSuccess)
             return fail(d, cudaGetLastError(), "cudaHostAlloc(record count)");
@@ -1450,6 +1454,7 @@ int ensure_delta(hetm_dev* d, uint64_t n_slots) {
         d->h_delta[b] = DeltaBuf{nullptr, nullptr};
     }
     if (d->ds.uniq) { cudaFree(d->ds.uniq); d->bytes_alloc -= d->delta_cap * 4; d->ds.uniq = nullptr; }
+    if (d->ds.uniq_val) { cudaFree(d->ds.uniq_val); d->bytes_alloc -= d->delta_cap * 8; d->ds.uniq_val = nullptr; }
     const uint64_t cap = std::max<uint64_t>(n_slots + n_slots / 4, 1ull << 21);  // pinning is slow: grow rarely
     for (int b = 0; b < 2; ++b) {
         if (int rc = dev_alloc(d, (void**)&d->d_delta[b].loc, cap * 4)) return rc;
@@ -1459,6 +1464,7 @@ int ensure_delta(hetm_dev* d, uint64_t n_slots) {
             return fail(d, cudaGetLastError(), "cudaHostAlloc(delta)");
     }
     if (int rc = dev_alloc(d, (void**)&d->ds.uniq, cap * 4)) return rc;
+    if (int rc = dev_alloc(d, (void**)&d->ds.uniq_val, cap * 8)) return rc;
     d->delta_cap = cap;
     return HETM_OK;
 }
@@ -1469,11 +1475,14 @@ int ensure_delta(hetm_dev* d, uint64_t n_slots) {
 // values when shadow != nullptr.  The record count lands in h_nrec (ev_nrec).
 int stage_records(hetm_dev* d, uint64_t n_slots, uint64_t* shadow, int buf) {
     if (int rc = ensure_delta(d, n_slots)) return rc;
-    cudaError_t e = launch_delta_claim(d->d_wlog, n_slots, d->W, d->ds, d->geom, d->s_merge);
+    const bool picked = d->round_versioned;
+    cudaError_t e = picked ? launch_delta_pick(d->d_wlog, n_slots, d->W, d->d_cells, d->ds, d->geom, d->s_merge,
+                                               d->d_ctr, false)
+                           : launch_delta_claim(d->d_wlog, n_slots, d->W, d->ds, d->geom, d->s_merge);
     if (e != cudaSuccess) return fail(d, e, "delta_claim");
     CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_merge));
     CK(d, cudaEventRecord(d->ev_nrec, d->s_merge));
-    e = launch_delta_emit(n_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow, d->geom, d->s_merge);
+    e = launch_delta_emit(n_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow, d->geom, d->s_merge, picked);
     if (e != cudaSuccess) return fail(d, e, "delta_emit");
     CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
     return HETM_OK;
@@ -1846,14 +1855,30 @@ int hetm_dev_merge_stage(hetm_dev* d) {
     // conflict (or a write-set log overflow) they stage nothing and leave
     // devShadow at the round start, so mergeAbortDevice stays exact
     if ((rc = ensure_delta(d, d->wlog_slots))) return rc;  // records <= slots in use <= capacity
-    cudaError_t e = launch_delta_claim(d->d_wlog, d->wlog_slots, d->W, d->ds, d->geom, d->s_merge, d->d_ctr);
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (d->timing) {
+        t0 = d->tev();
+        t1 = d->tev();
+        CK(d, cudaEventRecord(t0, d->s_merge));
+    }
+    const bool picked = d->round_versioned;
+    cudaError_t e = picked ? launch_delta_pick(d->d_wlog, d->wlog_slots, d->W, d->d_cells, d->ds, d->geom,
+                                               d->s_merge, d->d_ctr, true)
+                           : launch_delta_claim(d->d_wlog, d->wlog_slots, d->W, d->ds, d->geom, d->s_merge, d->d_ctr);
     if (e != cudaSuccess) return fail(d, e, "delta_claim(stage)");
     CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_merge));
     CK(d, cudaEventRecord(d->ev_nrec, d->s_merge));
-    e = launch_delta_emit(d->wlog_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow_inc, d->geom, d->s_merge);
+    // (running the emit beside the next round's batch was measured slower: its
+    // random shadow stores and the batch's random accesses share the DRAM)
+    e = launch_delta_emit(d->wlog_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow_inc, d->geom, d->s_merge,
+                          picked);
     if (e != cudaSuccess) return fail(d, e, "delta_emit(stage)");
     CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
     if (shadow_inc && (e = patch_shadow(d, d->d_ctr)) != cudaSuccess) return fail(d, e, "winner_apply(stage)");
+    if (d->timing) {
+        CK(d, cudaEventRecord(t1, d->s_merge));
+        d->tpairs[2].emplace_back(t0, t1);
+    }
     CK(d, cudaEventRecord(d->ev_shadow, d->s_merge));
     d->staged.active = true;
     d->staged.round_tx = d->round_tx;
@@ -2023,6 +2048,7 @@ int hetm_dev_clear_round(hetm_dev* d, uint32_t flags) {
     d->sources.clear();
     d->recv_applied = 0;
     d->merge_staged = false;
+    d->round_versioned = true;
     d->staged.active = false;
     d->deferred.clear();
     d->deferred_final = false;
@@ -2405,7 +2431,7 @@ int hetm_dev_set_timing(hetm_dev* d, int on) {
 }
 
 int hetm_dev_timing(hetm_dev* d, int which, double* total_ms, uint64_t* count) {
-    if (!d || which < 0 || which > 1) return HETM_ERR_INVALID_ARG;
+    if (!d || which < 0 || which > 2) return HETM_ERR_INVALID_ARG;
     double tot = 0;
     uint64_t c = 0;
     for (auto& pr : d->tpairs[which]) {

@@ -88,51 +88,135 @@ __global__ void __launch_bounds__(kClaimThreads) delta_claim_kernel(const uint32
         if (hist[b]) atomicAdd(&bucket_cnt[b], hist[b]);
 }
 
-// Step 2: each unique word becomes one {word, value} record at its bucket's
-// next slot (every CTA scans the bucket counts into shared memory), so the
-// delta reaches the host grouped by address range — a host worker's block of
-// records covers one small slice of the replica — and each word appears once
-// (the speculative swap/undo of hetm_dev_merge_prepare needs that).  The same
-// value refreshes devShadow; the claim words are cleared for the next stage.
-__global__ void __launch_bounds__(kClaimThreads) delta_emit_kernel(const uint32_t* __restrict__ uniq,
-                                                                   const unsigned long long* n_uniq,
-                                                                   const uint32_t* __restrict__ bucket_cnt,
-                                                                   uint32_t* cursor, uint32_t bshift,
-                                                                   const Cell* __restrict__ cells, DeltaBuf out,
-                                                                   uint64_t* __restrict__ shadow,
-                                                                   unsigned long long* claim) {
-    __shared__ uint32_t first[kDeltaBuckets];
-    __shared__ uint32_t part[kClaimThreads];
-    constexpr int per = kDeltaBuckets / kClaimThreads;
-    uint32_t run = 0;
-    for (int k = 0; k < per; ++k) run += bucket_cnt[threadIdx.x * per + k];
-    part[threadIdx.x] = run;
+// Step 1, versioned form (rounds whose batches all commit with per-word
+// versions: bank and rw kernels, both schedules): no claim bitmap.  A word's
+// cell carries the commit version of its LAST writer of the round (ticket + 1,
+// device_tm.cuh lk_commit), and the write-set log slot of ticket t is
+// 2 (t - wlog_base) + j, so exactly one slot per written word sees
+// meta == version(its own ticket) — that slot picks the word and the value it
+// read with the same 16-B load.  (A host-log apply retags a word's meta only
+// in a conflicting round, which is never merged.)  The second slot of a
+// transaction repeating its first word is skipped.  Output is slot-indexed
+// (ploc[s] = the word or ~0u, pval[s] = its value: coalesced stores, no
+// compaction atomics); the record count and slot count go to n_out[0..1].
+__global__ void __launch_bounds__(kClaimThreads) delta_pick_kernel(const uint32_t* __restrict__ wlog, uint64_t n,
+                                                                   uint64_t size_words, const Cell* __restrict__ cells,
+                                                                   uint32_t* __restrict__ ploc,
+                                                                   uint64_t* __restrict__ pval,
+                                                                   unsigned long long* n_out, uint32_t* bucket_cnt,
+                                                                   uint32_t bshift, const DevCounters* ctr, int gated) {
+    __shared__ uint32_t hist[kDeltaBuckets];
+    __shared__ uint32_t picked;
+    if (gated) {
+        if (ctr->conflict || ctr->wlog_overflow) n = 0;  // nothing is staged: emit sees 0 slots
+        const uint64_t used = 2 * (ctr->ticket - ctr->wlog_base);
+        n = used < n ? used : n;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) n_out[1] = n;
+    if (n == 0) return;
+    const unsigned long long wbase = ctr->wlog_base;
+    for (int b = threadIdx.x; b < kDeltaBuckets; b += blockDim.x) hist[b] = 0;
+    if (threadIdx.x == 0) picked = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {  // 256 partial sums: serial is fine
-        uint32_t acc = 0;
-        for (int t = 0; t < kClaimThreads; ++t) {
-            const uint32_t x = part[t];
-            part[t] = acc;
-            acc += x;
+    const unsigned lane = lane_id();
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t mine = 0;
+    for (uint64_t base = warp * 32; base < n; base += warps * 32) {  // warp-uniform trip count; slot pairs in one warp
+        const uint64_t i = base + lane;
+        const uint32_t loc = i < n ? wlog[i] : ~0u;
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, loc, 1);
+        bool pick = false;
+        uint64_t val = 0;
+        if (loc < size_words && !((i & 1) && prev == loc)) {
+            const ulonglong2 c = *reinterpret_cast<const ulonglong2*>(&cells[loc]);  // {value, meta}
+            pick = c.y == ((wbase + (i >> 1) + 1) & 0x7fffffffull);
+            val = c.x;
+        }
+        if (i < n) {
+            ploc[i] = pick ? loc : ~0u;
+            pval[i] = val;
+        }
+        if (pick) {
+            atomicAdd(&hist[loc >> bshift], 1u);
+            ++mine;
         }
     }
+    atomicAdd(&picked, mine);
     __syncthreads();
-    run = part[threadIdx.x];
-    for (int k = 0; k < per; ++k) {
-        first[threadIdx.x * per + k] = run;
-        run += bucket_cnt[threadIdx.x * per + k];
+    for (int b = threadIdx.x; b < kDeltaBuckets; b += blockDim.x)
+        if (hist[b]) atomicAdd(&bucket_cnt[b], hist[b]);
+    if (threadIdx.x == 0 && picked) atomicAdd(&n_out[0], (unsigned long long)picked);
+}
+
+// Step 2: each unique word becomes one {word, value} record in its address
+// bucket's range (kDeltaBuckets contiguous word ranges), so the delta reaches
+// the host grouped by address — a host worker's block of records covers one
+// slice of the replica — and each word appears once (the speculative
+// swap/undo of hetm_dev_merge_prepare needs that).  A CTA partitions a tile
+// of kEmitTile records in shared memory (counting sort by bucket) and
+// reserves one run per (tile, bucket) with a single global atomic, so the
+// record stores land as contiguous runs instead of one scattered store per
+// record.  The same value refreshes devShadow; after a claim pass the claim
+// words are cleared for the next stage.
+constexpr int kEmitPer = 16;                                   // records per thread per tile
+constexpr uint64_t kEmitTile = (uint64_t)kClaimThreads * kEmitPer;
+static_assert(kDeltaBuckets == kClaimThreads, "one bucket per thread in the emit scans");
+__global__ void __launch_bounds__(kClaimThreads) delta_emit_kernel(const uint32_t* __restrict__ uniq,
+                                                                   const unsigned long long* n_in,
+                                                                   const uint32_t* __restrict__ bucket_cnt,
+                                                                   uint32_t* cursor, uint32_t bshift,
+                                                                   const Cell* __restrict__ cells,
+                                                                   const uint64_t* __restrict__ uniq_val, DeltaBuf out,
+                                                                   uint64_t* __restrict__ shadow,
+                                                                   unsigned long long* claim) {
+    __shared__ uint32_t first[kDeltaBuckets];  // global start of each bucket's range
+    __shared__ uint32_t cnt[kDeltaBuckets];    // tile histogram, then the tile's local cursors
+    __shared__ uint32_t run[kDeltaBuckets];    // global start of the tile's run in each bucket
+    __shared__ uint32_t wsum[kClaimThreads / 32];
+    const unsigned t = threadIdx.x, lane = lane_id(), wid = t >> 5;
+    {  // exclusive scan of the bucket counts (one per thread)
+        const uint32_t c = bucket_cnt[t];
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (unsigned)o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        uint32_t off = 0;
+        for (unsigned w = 0; w < wid; ++w) off += wsum[w];
+        first[t] = off + x - c;
     }
-    __syncthreads();
-    const uint64_t n = *n_uniq;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t loc = uniq[j];
-        const uint32_t b = loc >> bshift;
-        const uint32_t pos = first[b] + atomicAdd(&cursor[b], 1u);
-        const uint64_t val = cells[loc].value;
-        out.loc[pos] = loc;
-        out.val[pos] = val;
-        if (shadow) shadow[loc] = val;
-        claim[loc >> 6] = 0;
+    const uint64_t n = *n_in;  // unique words (claim pass) or slots (pick pass: ~0u = not picked)
+    for (uint64_t t0 = (uint64_t)blockIdx.x * kEmitTile; t0 < n; t0 += (uint64_t)gridDim.x * kEmitTile) {
+        cnt[t] = 0;
+        __syncthreads();
+        uint32_t loc[kEmitPer], r[kEmitPer];
+        uint64_t val[kEmitPer];
+#pragma unroll
+        for (int k = 0; k < kEmitPer; ++k) {
+            const uint64_t j = t0 + (uint64_t)k * kClaimThreads + t;
+            loc[k] = j < n ? uniq[j] : ~0u;
+            val[k] = loc[k] != ~0u ? (uniq_val ? uniq_val[j] : cells[loc[k]].value) : 0;  // pick: read already
+        }
+#pragma unroll
+        for (int k = 0; k < kEmitPer; ++k)
+            if (loc[k] != ~0u) r[k] = atomicAdd(&cnt[loc[k] >> bshift], 1u);
+        __syncthreads();
+        if (cnt[t]) run[t] = first[t] + atomicAdd(&cursor[t], cnt[t]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kEmitPer; ++k) {
+            if (loc[k] == ~0u) continue;
+            const uint32_t pos = run[loc[k] >> bshift] + r[k];
+            out.loc[pos] = loc[k];
+            out.val[pos] = val[k];
+            if (shadow) shadow[loc[k]] = val[k];
+            if (!uniq_val) claim[loc[k] >> 6] = 0;
+        }
+        __syncthreads();  // cnt / run are reused by the next tile
     }
 }
 
@@ -212,14 +296,28 @@ cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_w
     return cudaGetLastError();
 }
 
-cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
-                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s) {
-    if (max_records == 0) return cudaSuccess;
-    uint64_t want = (max_records + kClaimThreads - 1) / kClaimThreads;
+cudaError_t launch_delta_pick(const uint32_t* wlog, uint64_t n, uint64_t size_words, const Cell* cells,
+                              const DeltaScratch& ds, const LaunchGeom& g, cudaStream_t s, const DevCounters* ctr,
+                              bool gated) {
+    cudaError_t e = cudaMemsetAsync(ds.n_uniq, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ds.bucket_cnt, 0, 2 * kDeltaBuckets * sizeof(uint32_t), s);
+    if (e != cudaSuccess || n == 0) return e;
+    uint64_t want = (n + kClaimThreads - 1) / kClaimThreads;
     const uint64_t cap = (uint64_t)g.sm_count * 8;
+    delta_pick_kernel<<<(unsigned)(want < cap ? want : cap), kClaimThreads, 0, s>>>(
+        wlog, n, size_words, cells, ds.uniq, ds.uniq_val, ds.n_uniq, ds.bucket_cnt, delta_bucket_shift(size_words),
+        ctr, gated ? 1 : 0);  // n_uniq[0] = records, n_uniq[1] = slots
+    return cudaGetLastError();
+}
+
+cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
+                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s, bool picked) {
+    if (max_records == 0) return cudaSuccess;
+    uint64_t want = (max_records + kEmitTile - 1) / kEmitTile;
+    const uint64_t cap = (uint64_t)g.sm_count * 4;
     delta_emit_kernel<<<(unsigned)(want < cap ? want : cap), kClaimThreads, 0, s>>>(
-        ds.uniq, ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets, delta_bucket_shift(size_words), cells, out,
-        shadow, ds.claim);
+        ds.uniq, picked ? ds.n_uniq + 1 : ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets,
+        delta_bucket_shift(size_words), cells, picked ? ds.uniq_val : nullptr, out, shadow, ds.claim);
     return cudaGetLastError();
 }
 

@@ -98,19 +98,27 @@ cudaError_t launch_dirty_chunks(uint64_t* plain, Cell* cells, uint64_t size_word
 // counts), then emit ({word, value} records grouped by bucket, devShadow
 // refreshed when shadow != nullptr, claim words cleared).  The record count
 // is *n_uniq on the device.
-constexpr uint32_t kDeltaBucketBits = 12;
+constexpr uint32_t kDeltaBucketBits = 8;  // 256 address ranges (4 MiB of a 1 GiB replica each)
 constexpr int kDeltaBuckets = 1 << kDeltaBucketBits;
 struct DeltaScratch {
     unsigned long long* claim;      // ceil(W/64) words, all zero between stages
-    uint32_t* uniq;                 // unique words (<= slots)
-    unsigned long long* n_uniq;     // record count
+    uint32_t* uniq;                 // unique words (claim pass) / per-slot picked word or ~0u (pick pass)
+    uint64_t* uniq_val;             // per-slot values (pick pass only)
+    unsigned long long* n_uniq;     // [0] record count, [1] slot count (pick pass)
     uint32_t* bucket_cnt;           // kDeltaBuckets counts, then kDeltaBuckets cursors
 };
 uint32_t delta_bucket_shift(uint64_t size_words);
 cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_words, const DeltaScratch& ds,
                                const LaunchGeom& g, cudaStream_t s, const DevCounters* gate = nullptr);
+// Versioned replacement of the claim pass (rounds of bank / rw batches only):
+// the slot whose ticket's commit version is still in the word's cell picks
+// the word and its value (no claim bitmap, no atomics on the words).
+cudaError_t launch_delta_pick(const uint32_t* wlog, uint64_t n, uint64_t size_words, const Cell* cells,
+                              const DeltaScratch& ds, const LaunchGeom& g, cudaStream_t s, const DevCounters* ctr,
+                              bool gated);
 cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
-                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s);
+                              DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s,
+                              bool picked = false);
 // Rollback of the device write set: cells[loc].value = shadow[loc] per log slot.
 cudaError_t launch_wlog_restore(Cell* cells, const uint64_t* shadow, const uint32_t* wlog, uint64_t n,
                                 uint64_t size_words, const LaunchGeom& g, cudaStream_t s);

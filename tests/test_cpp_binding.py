@@ -1,6 +1,7 @@
 """The C++ binding (include/hetm_b200/hetm_gpu.hpp) compiles against the
 reference's own headers and maps ABI errors onto the reference exceptions."""
 import os
+import re
 import subprocess
 
 import pytest
@@ -20,7 +21,8 @@ def test_binding_compiles_against_reference_headers(hetm, tmp_path):
     if hetm.device_count() == 0:
         assert r.returncode == 3 and "no-cuda-device" in r.stdout  # no CPU fallback
         # the host half ran on the reference types: hetm::TxAbort caught, OutOfBoundsError thrown
-        assert "1 TxAbort retries" in r.stdout and "oob=1" in r.stdout and "sum_ok=1" in r.stdout
+        m = re.search(r"(\d+) TxAbort retries", r.stdout)  # >= 1: the forced conflict, plus worker retries
+        assert m and int(m.group(1)) >= 1 and "oob=1" in r.stdout and "sum_ok=1" in r.stdout
     else:
         assert r.returncode == 0, r.stdout + r.stderr
         assert "replicas_match=1" in r.stdout
