@@ -12,7 +12,8 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SMALL = ["--e2e-steps", "3", "--cpu-seconds", "0.5", "--live-rounds", "2", "--config-rounds", "2",
+# cfg3 needs > starvationK = 3 rounds: the first three are device-aborted by design
+SMALL = ["--e2e-steps", "3", "--cpu-seconds", "0.5", "--live-rounds", "2", "--config-rounds", "5",
          "--cfg5-words-log2", "30", "--cfg5-log-mib", "16", "--cfg5-reps", "1"]
 
 
