@@ -435,7 +435,8 @@ def run_ours(args):
     # our kernels per step (the ncu launch list in profiles/ shows the same set)
     launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_kernel": 1, "restore_kernel": 1}
     if merge_dev:
-        launches_detail.update({"delta_claim_kernel": 1, "delta_emit_kernel": 1, "winner_kernel": 1})
+        # bank rounds carry per-word commit versions: the versioned pick pass (no claim bitmap)
+        launches_detail.update({"delta_pick_kernel": 1, "delta_emit_kernel": 1, "winner_kernel": 1})
     launches_detail["clear_round_kernel"] = 1
     if world > 1 and isinstance(sv, PeerValidator):
         launches_detail.update({"route_count_kernel": 1, "route_scan_kernel": 1, "route_peer_publish_kernel": 1,

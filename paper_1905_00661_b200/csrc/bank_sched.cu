@@ -10,25 +10,21 @@
 //      second slot is then dropped), and the RS bits of the read-only
 //      accounts (probe-gated, per-CTA filter); the ticket and write-set log
 //      slots are written here too;
-//   2. CUB radix sort of the 2n (account, payload) pairs on the account bits
-//      only — the sort is stable, so each account's accesses stay in input
-//      order;
+//   2. radix sort of the 2n (account, payload) pairs on the account bits
+//      only (sort.cu, hand-written: 3 passes of <= 10-bit digits) — the sort
+//      is stable, so each account's accesses stay in input order;
 //   3. one pass over the sorted accesses (sched_commit_red_kernel): per warp
 //      run a segmented shuffle sum of the deltas, added to the cell with one
 //      RED.ADD (commutative: a hot account spread over many runs needs no
 //      order); at each account's segment end the version of its last writer
 //      (lk_commit of its ticket) is stored; RS / WS / ChunkMap bits are set
 //      warp-aggregated (the stream is sorted).
-// A traced batch keys all four accesses ((4 i + k) << 1 | writer), runs a CUB
-// inclusive scan-by-account of {delta, last writer}, records every access's
+// A traced batch keys all four accesses ((4 i + k) << 1 | writer), runs an
+// inclusive scan-by-account of {delta, last writer} (sort.cu), records every access's
 // pre-value (sched_trace_kernel) and commits from the scan (sched_commit_kernel).
 // Cost is independent of skew (no locks, no retries): at zipf 0.99 the
 // optimistic PR-STM kernel serializes ~10^5 commits on the hottest account.
 // The result is exactly the deterministic single-worker mode.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <thrust/iterator/transform_iterator.h>
-
 #include "common.cuh"
 #include "device_tm.cuh"
 #include "kernels.h"
@@ -51,27 +47,12 @@ constexpr int kKeysU = 2;                                        // keys kernel:
 struct DeltaW {  // scan value: summed delta, last writing transaction (input index) or kNone
     unsigned long long d, w;
 };
-struct DeltaWOp {
-    __host__ __device__ DeltaW operator()(const DeltaW& a, const DeltaW& b) const {
-        return DeltaW{a.d + b.d, b.w != kNone ? b.w : a.w};
-    }
-};
-
 // Sort payload: access index a = S i + k (input order) << 1 | writer, where
 // writer marks the transaction's first slot naming an account it writes and S
 // is the slots keyed per transaction (2: the written accounts; 4: all, traced).
 __device__ __forceinline__ uint32_t acc_of(uint32_t p) { return p >> 1; }
 template <int S>
 __device__ __forceinline__ uint64_t tx_of(uint32_t p) { return p >> (S == 4 ? 3 : 2); }
-
-template <int S>
-struct DeltaOf {  // scan value of a sorted access: its precomputed delta + writer
-    using result_type = DeltaW;
-    const unsigned long long* delta;
-    __device__ DeltaW operator()(uint32_t p) const {
-        return DeltaW{delta[acc_of(p)], (p & 1u) ? tx_of<S>(p) : kNone};
-    }
-};
 
 __device__ __forceinline__ void load_accts(const hetm_bank_tx* in, uint64_t i, uint64_t base, uint64_t (&a)[4],
                                            uint64_t& amount) {
@@ -362,24 +343,20 @@ uint64_t bank_hot_estimate_sample(uint64_t n) { return n < kEstTx ? n : kEstTx; 
 size_t bank_sched_temp_bytes(uint64_t n, uint64_t size_words) {
     const uint64_t n4 = 4 * n;
     const int end_bit = (int)std::min<uint32_t>(32, bits_for(size_words) + 1);  // + the sentinel
-    size_t a = 0, b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n4, 0, end_bit);
-    auto vi = thrust::make_transform_iterator((const uint32_t*)nullptr, DeltaOf<4>{nullptr});
-    cub::DeviceScan::InclusiveScanByKey(nullptr, b, (const uint32_t*)nullptr, vi, (DeltaW*)nullptr, DeltaWOp{},
-                                        (int64_t)n4);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    // [locs in/out | payload in/out | delta | scan | first ticket | cub temp]
-    return 4 * al(n4 * 4) + al(n4 * 8) + al(n4 * sizeof(DeltaW)) + 256 + al(std::max(a, b));
+    // [locs in/out | payload in/out | delta | scan | first ticket | sort / scan temp]
+    return 4 * al(n4 * 4) + al(n4 * 8) + al(n4 * sizeof(DeltaW)) + 256 +
+           al(std::max(radix_sort_temp_bytes(n4, end_bit), seg_scan_temp_bytes(n4)));
 }
 
 cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint64_t n, unsigned long long* d_tickets,
                               DevCounters* ctr, void* temp, size_t temp_bytes, const LaunchGeom& g, cudaStream_t s,
                               SchedGraph* graph) {
     if (n == 0) return cudaSuccess;
+    if (cudaError_t e = radix_sort_init(); e != cudaSuccess) return e;  // before any capture
     if (graph && !v.trace) {
-        // Replay the captured sequence: ~10 dependent launches (4 sort passes, the
-        // scan, CUB's bookkeeping) cost more host time than GPU time when issued
+        // Replay the captured sequence: ~12 dependent launches (3 sort passes of
+        // 3 kernels each) cost more host time than GPU time when issued
         // one by one.  Only the keys kernel's inputs / tickets change per batch.
         const bool same = graph->exec && graph->n == n && graph->temp == temp && graph->wlog == v.wlog &&
                           graph->wlog_slots == v.wlog_slots && graph->cells == v.cells && graph->ctr == ctr;
@@ -463,20 +440,18 @@ cudaError_t launch_bank_sched(const ShardView& v, const hetm_bank_tx* d_in, uint
     auto* incl = reinterpret_cast<DeltaW*>(p + 4 * al(n4 * 4) + al(n4 * 8));
     const size_t off = 4 * al(n4 * 4) + al(n4 * 8) + al(n4 * sizeof(DeltaW));
     auto* first = reinterpret_cast<unsigned long long*>(p + off);
-    void* cub_tmp = p + off + 256;
-    size_t cub_bytes = temp_bytes - (off + 256);
+    void* sort_tmp = p + off + 256;
+    const size_t sort_bytes = temp_bytes - (off + 256);
     const unsigned grid_tx = grid_for(n, kSchedThreads, 8, g.sm_count);
     const unsigned grid_acc = grid_for(n4, kSchedThreads, 8, g.sm_count);
     sched_ticket_kernel<<<1, 1, 0, s>>>(ctr, n, first);
     if (S == 4) sched_keys_kernel<4><<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
     else sched_keys_kernel<2><<<grid_tx, kSchedThreads, 0, s>>>(v, d_in, n, locs, pay, delta, d_tickets, first, ctr);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, locs, locs_s, pay, pay_s, (int64_t)n4, 0,
-                                                    end_bit, s);
+    cudaError_t e = radix_sort_pairs(locs, locs_s, pay, pay_s, n4, end_bit, sort_tmp, sort_bytes, g, s);
     if (e != cudaSuccess) return e;
     if (S == 4) {
-        auto vi = thrust::make_transform_iterator((const uint32_t*)pay_s, DeltaOf<4>{delta});
-        e = cub::DeviceScan::InclusiveScanByKey(cub_tmp, cub_bytes, (const uint32_t*)locs_s, vi, incl, DeltaWOp{},
-                                                 (int64_t)n4, cub::Equality(), s);
+        e = seg_scan_delta_writer(locs_s, pay_s, delta, n4, reinterpret_cast<unsigned long long*>(incl), sort_tmp,
+                                  sort_bytes, s);
         if (e != cudaSuccess) return e;
         sched_trace_kernel<<<grid_acc, kSchedThreads, 0, s>>>(v, d_in, n4, locs_s, pay_s, delta, incl, first);
         sched_commit_kernel<4><<<grid_acc, kSchedThreads, 0, s>>>(v, n4, locs_s, incl, first);

@@ -5,8 +5,8 @@
 // input order is, set by set, the subsequence of that set's transactions:
 //   1. per transaction: sort key = its set (sentinel when the set lies outside
 //      the shard), payload = input index; ticket = first + i;
-//   2. CUB radix sort of the (set, index) pairs on the set bits — stable, so
-//      each set's transactions stay in input order;
+//   2. radix sort of the (set, index) pairs on the set bits (sort.cu,
+//      hand-written) — stable, so each set's transactions stay in input order;
 //   3. one thread per set segment runs them in that order with the whole set
 //      (64 words) in registers, storing the dirty words back at the segment's
 //      end (it is the set's only accessor in this launch): hit / invalid /
@@ -17,10 +17,6 @@
 //      lk_commit(ticket of the set's last update).
 // No lock is taken and nothing retries: hot sets cost one thread a loop over
 // their transactions instead of a chain of lock handoffs.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
-#include <thrust/iterator/counting_iterator.h>
-
 #include <algorithm>
 
 #include "common.cuh"
@@ -260,16 +256,11 @@ __global__ void __launch_bounds__(kCsThreads) cs_run_kernel(ShardView v, CacheGe
 }  // namespace
 
 size_t cache_sched_temp_bytes(uint64_t n, uint64_t n_sets) {
-    size_t a = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, 0,
-                                    (int)std::min<uint32_t>(32, bits_of(n_sets) + 1));
-    size_t b = 0;
-    cub::DeviceSelect::Flagged(nullptr, b, thrust::counting_iterator<uint32_t>(0), (const uint8_t*)nullptr,
-                               (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n);
+    const int end_bit = (int)std::min<uint32_t>(32, bits_of(n_sets) + 1);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    // [sets in/out | payload in/out | starts | records | start flags | first | n_starts | cub temp]
-    return 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + al(n) + 512 + al(std::max(a, b));
+    // [sets in/out | payload in/out | starts | records | start flags | first | n_starts | sort / select temp]
+    return 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + al(n) + 512 +
+           al(std::max(radix_sort_temp_bytes(n, end_bit), select_flagged_temp_bytes(n)));
 }
 
 cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const hetm_cache_tx* d_in, uint64_t n,
@@ -289,17 +280,15 @@ cudaError_t launch_cache_sched(const ShardView& v, const CacheGeom& cg, const he
     const size_t off = 5 * al(n * 4) + al(n * sizeof(hetm_cache_tx)) + al(n);
     auto* first = reinterpret_cast<unsigned long long*>(p + off);
     auto* n_starts = reinterpret_cast<uint32_t*>(p + off + 256);
-    void* cub_tmp = p + off + 512;
-    size_t cub_bytes = temp_bytes - (off + 512);
+    void* sort_tmp = p + off + 512;
+    const size_t sort_bytes = temp_bytes - (off + 512);
     const int end_bit = (int)std::min<uint32_t>(32, bits_of(cg.n_sets) + 1);
     cs_ticket_kernel<<<1, 1, 0, s>>>(ctr, n, first);
     cs_keys_kernel<<<grid_of(n, 256, 8, g.sm_count), 256, 0, s>>>(v, cg, d_in, n, sets, pay, d_tickets, first, ctr);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, sets, sets_s, pay, pay_s, (int64_t)n, 0,
-                                                    end_bit, s);
+    cudaError_t e = radix_sort_pairs(sets, sets_s, pay, pay_s, n, end_bit, sort_tmp, sort_bytes, g, s);
     if (e != cudaSuccess) return e;
     cs_gather_kernel<<<grid_of(n, 256, 8, g.sm_count), 256, 0, s>>>(d_in, n, pay_s, sets_s, recs, start);
-    e = cub::DeviceSelect::Flagged(cub_tmp, cub_bytes, thrust::counting_iterator<uint32_t>(0), start, starts, n_starts,
-                                   (int64_t)n, s);
+    e = select_flagged(start, n, starts, n_starts, sort_tmp, sort_bytes, s);
     if (e != cudaSuccess) return e;
     cs_run_kernel<<<grid_of(n, kCsThreads, 16, g.sm_count), kCsThreads, 0, s>>>(v, cg, recs, n, sets_s, pay_s, starts,
                                                                               n_starts, d_res, first, ctr);

@@ -191,6 +191,24 @@ cudaError_t launch_route_to_peers(const hetm_log_entry* d_in, uint64_t n, uint32
                                   unsigned long long* const* d_peer_counts, unsigned long long* d_totals,
                                   void* d_scratch, size_t scratch_bytes, const LaunchGeom& g, cudaStream_t s);
 
+// Hand-written device primitives of the SCAN schedules (sort.cu).
+// Stable LSD radix sort of (key, value) pairs on key bits [0, end_bit), n < 2^32.
+size_t radix_sort_temp_bytes(uint64_t n, int end_bit);
+cudaError_t radix_sort_init();  // once before any capture of radix_sort_pairs (kernel attributes)
+cudaError_t radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                             uint64_t n, int end_bit, void* temp, size_t temp_bytes, const LaunchGeom& g,
+                             cudaStream_t s);
+// out = the indices i < n with flags[i] != 0, in order; *d_count = their number.
+size_t select_flagged_temp_bytes(uint64_t n);
+cudaError_t select_flagged(const uint8_t* flags, uint64_t n, uint32_t* out, uint32_t* d_count, void* temp,
+                           size_t temp_bytes, cudaStream_t s);
+// Inclusive scan by key of {delta, last writer} over sorted traced-bank accesses
+// (payload (4 i + k) << 1 | writer, delta indexed by 4 i + k): out[2j] = summed
+// delta, out[2j+1] = last writing transaction (~0: none) since the key's start.
+size_t seg_scan_temp_bytes(uint64_t n);
+cudaError_t seg_scan_delta_writer(const uint32_t* keys, const uint32_t* pay, const unsigned long long* delta,
+                                  uint64_t n, unsigned long long* out, void* temp, size_t temp_bytes, cudaStream_t s);
+
 int query_geom(LaunchGeom* g, int device);
 
 }  // namespace hetm_b200

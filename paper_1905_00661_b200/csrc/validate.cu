@@ -141,9 +141,15 @@ __global__ void __launch_bounds__(kValThreads) validate_kernel(ShardView v, LogV
 // atomic order, so every later entry for that word either loses (smaller ts)
 // or is queued itself.  Cost per entry: one random line RMW + one L2-hit
 // store; duplicates (rare under uniform access) cost one more L2 load+store.
+//
+// Address window [win_lo, win_hi) (local words): only entries inside it are
+// processed, so a shard too large for the TLB reach (128 GiB
+// of cells) is applied in a few passes over the log, each confined to a
+// window of cells; out-of-shard entries are flagged by the pass with win_lo = 0.
 template <int U>
 __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView lv, DevCounters* ctr,
-                                                            RestoreQueue restore) {
+                                                            RestoreQueue restore, uint64_t win_lo,
+                                                            uint64_t win_hi) {
     __shared__ SegPrefix sp;
     const uint64_t n = view_total(lv, sp);
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
@@ -163,9 +169,10 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView
             old[u] = ~0ull;
             if (i0 + (uint64_t)u * blockDim.x >= n) continue;
             if (loc >= v.size_words) {
-                f.oob = 1;
+                f.oob |= win_lo == 0;
                 continue;
             }
+            if (loc < win_lo || loc >= win_hi) continue;  // another window's pass
             const uint64_t bit = loc >> v.gran_shift;
             f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
             f.bad |= (e[u].ts <= ts_floor);
@@ -511,9 +518,27 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
         restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, rq);
         return cudaGetLastError();
     }
-    if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
-    else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
-    else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq);
+    // Address windows: random 16-B cells over more than 64 GiB of cells outrun
+    // the TLB reach (5 G entries/s on a 64 GiB shard = 128 GiB of cells vs 13
+    // on 32 GiB; profiles/r02c_bucket_probe.txt), so such shards are applied
+    // in passes over the log, each confined to 2^32 words (64 GiB of cells):
+    // 14.5 G entries/s on the 64 GiB shard (windows of 2^31: 10.1, 2^30: 5.8;
+    // profiles/r02d_window_probe.txt).
+    static const uint32_t win_log2 = [] {  // tuning experiments only: HETM_APPLY_WINDOW_LOG2
+        const char* e = std::getenv("HETM_APPLY_WINDOW_LOG2");
+        return e ? (uint32_t)std::atoi(e) : 32u;
+    }();
+    static const uint64_t win_min_shard = [] {  // shards above this many words are windowed
+        const char* e = std::getenv("HETM_APPLY_WINDOW_ABOVE_LOG2");
+        return 1ull << (e ? std::atoi(e) : 32);
+    }();
+    const uint64_t win = v.size_words > win_min_shard && win_log2 < 40 ? (1ull << win_log2) : v.size_words;
+    for (uint64_t lo = 0; lo < v.size_words; lo += win) {
+        const uint64_t hi = v.size_words - lo > win ? lo + win : v.size_words;
+        if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq, lo, hi);
+        else if (u == 8) apply_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq, lo, hi);
+        else apply_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq, lo, hi);
+    }
     restore_kernel<<<2 * g.sm_count, kValThreads, 0, s>>>(v, lv, ctr, rq);
     return cudaGetLastError();
 }
