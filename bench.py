@@ -155,17 +155,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- rooflines
-# The bank kernel with every protocol step knocked out (P1 snapshot loads and
-# the P5 stores only: HETM_KNOCKOUT=64 in an EXPERIMENTS=1 build of the same
-# kernel, same 2^20-tx batch on the 2^27-word STMR, 1 CTA/SM), measured on B200:
-# profiles/r01_bank_kernel_knockouts.txt.  The product's protocol (lock CAS,
-# ticket, read-set validation, bitmaps) costs the difference.
-PROTOCOL_FLOOR_MS = 0.1148
+# Access floor of the stripe-lock bank kernel: the same 2^20 random transfers
+# doing only what no protocol can avoid — load the two written 16-B cells and
+# store them back (the read-only accounts' values are unused, their locks live
+# in the L2-resident stripe table) — tools/stripe_probe.cu "floor" on B200,
+# 1 CTA/SM: profiles/r02l_stripe_probe.txt.  The protocol (stripe locks,
+# ticket, read-set validation, release fence, bitmaps) costs the difference.
+PROTOCOL_FLOOR_MS = 0.1189
 
 
 def protocol_floor(kernel_ms, traffic, peak):
-    out = {"model": "same kernel, every protocol step knocked out (P1 loads + P5 stores only, HETM_KNOCKOUT=64)",
-           "source": "profiles/r01_bank_kernel_knockouts.txt", "floor_kernel_ms": PROTOCOL_FLOOR_MS,
+    out = {"model": "same transfers, no protocol: 128-bit load + store of the two written cells only",
+           "source": "profiles/r02l_stripe_probe.txt (tools/stripe_probe.cu floor)", "floor_kernel_ms": PROTOCOL_FLOOR_MS,
            "floor_tx_per_s": (1 << 20) / (PROTOCOL_FLOOR_MS * 1e-3),
            "kernel_over_floor": kernel_ms / PROTOCOL_FLOOR_MS}
     if traffic:
@@ -433,7 +434,7 @@ def run_ours(args):
     e2e = run_e2e(args, hetm, dev, host_replica, world, rank, W, base, dist)
     ms_step = ms_total / K
     # our kernels per step (the ncu launch list in profiles/ shows the same set)
-    launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_kernel": 1, "restore_kernel": 1}
+    launches_detail = {"bank_batch_kernel": 1, "hot_estimate_kernel": 1, "apply_xchg_kernel": 1}
     if merge_dev:
         # bank rounds carry per-word commit versions: the versioned pick pass (no claim bitmap)
         launches_detail.update({"delta_pick_kernel": 1, "delta_emit_kernel": 1, "winner_kernel": 1})
@@ -474,7 +475,7 @@ def run_ours(args):
                      "protocol_floor": protocol_floor(batch_ms, measured_traffic("bank_batch_kernel"), peak)},
         "step_breakdown_ms": {"batch": batch_ms, "validate_apply": val_ms, "merge_stage": mstage_ms,
                               "step": ms_step},
-        "validate_apply_cfg2": {"kernel": "apply_kernel", "gbs_algorithmic": val_gbs,
+        "validate_apply_cfg2": {"kernel": "apply_xchg_kernel", "gbs_algorithmic": val_gbs,
                                 "entries_per_s_per_gpu": (n_val / K / world) / (val_ms / 1e3),
                                 "frac": val_gbs / peak, "algorithmic_bytes_per_entry": ENTRY_BYTES,
                                 "traffic": measured_traffic("validate_apply"), "kernel_ms": val_ms},
@@ -794,7 +795,7 @@ def run_cfg5(args, hetm, torch, world, rank, local, dist, peak):
     return {"workload": f"BASELINE configs[4]: {plan['stmr_gib_global']:.0f} GiB STMR sharded {plan['shard_gib']:.0f} "
                         f"GiB per GPU (no shadow), global CPU write logs uniform over the STMR, RS density 1e-3 at "
                         "1 KiB granules",
-            "n_gpus": world, "exchange": exchange, "kernel": "apply_kernel (+ route_peer_scatter_kernel at G>1)",
+            "n_gpus": world, "exchange": exchange, "kernel": "apply_xchg_kernel (+ route_peer_scatter_kernel at G>1)",
             "headline_log_mib": head["log_mib_global"], "gbs_algorithmic": head["gbs_algorithmic"],
             "aggregate_gbs": head["gbs_algorithmic"], "frac": head["frac"], "peak_per_gpu": peak,
             "algorithmic_bytes_per_entry": ENTRY_BYTES, "entries_per_s": head["entries_per_s"],

@@ -232,6 +232,8 @@ struct hetm_dev {
     PreparedMerge prep;                     // hetm_dev_merge_prepare state
     cudaEvent_t ev_stage = nullptr;         // delta records gathered (s_merge)
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
+    unsigned long long* d_stripes = nullptr;  // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES)
+    uint32_t stripe_shift = 64;
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
     cudaEvent_t ev_exec = nullptr, ev_copy = nullptr, ev_val = nullptr, ev_round = nullptr, ev_shadow = nullptr,
@@ -279,6 +281,8 @@ struct hetm_dev {
         v.wlog_ovf = &d_ctr->wlog_overflow;
         v.serial = (cfg.flags & HETM_CFG_DETERMINISTIC) ? 1u : 0u;
         v.trace = nullptr;
+        v.stripes = d_stripes;
+        v.stripe_shift = stripe_shift;
         return v;
     }
     std::mutex xfer_mu;  // record() is reached from the GPU-controller and the log streamer threads
@@ -796,6 +800,17 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_ws, d->rs_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
+    {  // lock-stripe table of the bank kernel: 2^22 words (32 MiB, L2-resident), fewer for small shards
+        static const uint32_t max_bits = [] {  // tuning experiments: HETM_STRIPE_BITS
+            const char* e = std::getenv("HETM_STRIPE_BITS");
+            return e ? (uint32_t)std::atoi(e) : 22u;
+        }();
+        uint32_t bits = 10;
+        while (bits < max_bits && (1ull << bits) < d->W) ++bits;
+        if ((rc = dev_alloc(d, (void**)&d->d_stripes, (8ull << bits)))) return bail(rc);
+        d->stripe_shift = 64 - bits;
+        CK(d, cudaMemset(d->d_stripes, 0, 8ull << bits));  // unlocked, version 0
+    }
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);
     d->restore_cap = kRestoreCap;
@@ -875,7 +890,7 @@ int hetm_dev_close(hetm_dev* d) {
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
     for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.uniq_val, (void*)d->ds.n_uniq, (void*)d->ds.bucket_cnt, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
-                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in})
+                    (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in, (void*)d->d_stripes})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     if (d->h_nrec) cudaFreeHost(d->h_nrec);

@@ -75,6 +75,8 @@ struct ShardView {
     unsigned long long* wlog_ovf; // set when a committed write set did not fit (DevCounters::wlog_overflow)
     uint32_t serial;           // deterministic single-worker mode (HETM_CFG_DETERMINISTIC)
     unsigned long long* trace; // checker trace of the batch (nullptr: off): HETM_TRACE_TX_WORDS per tx index
+    unsigned long long* stripes; // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES; nullptr: cell locks)
+    uint32_t stripe_shift;       // stripe = (loc * 2^64/phi) >> stripe_shift  (64 - log2 stripes)
 };
 
 // Checker trace record of one committed batch transaction (capi.h
@@ -162,6 +164,9 @@ __device__ __forceinline__ void st_pair(Cell* c, uint64_t value, unsigned long l
 
 __device__ __forceinline__ void set_bit(unsigned long long* words, uint64_t bit) {
     atomicOr(&words[bit >> 6], 1ull << (bit & 63));  // REDG.E.OR.64 (result unused)
+}
+__device__ __forceinline__ void red_or_bit(unsigned long long* words, uint64_t bit) {
+    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(&words[bit >> 6]), "l"(1ull << (bit & 63)) : "memory");
 }
 __device__ __forceinline__ bool test_bit(const unsigned long long* words, uint64_t bit) {
     return (words[bit >> 6] >> (bit & 63)) & 1ull;

@@ -29,6 +29,27 @@
 // Duplicate words inside one transaction are handled: each distinct word is
 // locked, validated and stored once (the last write to it wins, as in the
 // oracle's sequential replay).
+//
+// KO_STRIPES (the product bank kernel): the versioned lock words live in an
+// L2-resident STRIPE TABLE (ShardView::stripes, 2^22 words = 32 MiB, word ->
+// stripe by a multiplicative hash) instead of the cells' meta words.  Only the
+// written cells are then touched in DRAM (one 128-bit load, one 128-bit
+// store); every lock/validation access is an L2 hit
+// (tools/stripe_probe.cu: 0.152 vs 0.275 ms for the same access shape,
+// profiles/r02l_stripe_probe.txt).  The phases become
+//   P0  stripe words of all accounts (the P1 cell loads are issued only after
+//       they returned: control dependency, same ordering argument as the ticket
+//       -> validation step of device_tm.cuh)
+//   P1  128-bit {value, meta} of the written cells; bitmap probes
+//   P2  CAS on the distinct written stripes; P3 ticket; P4 reload of the
+//       read-only stripes not held by this transaction
+//   P5  128-bit {value, lk_commit(ticket)} per written cell (the cell keeps
+//       its last writer's version for the merge pick pass), fence.acq_rel.gpu,
+//       release of the held stripes with the same version.
+// Distinct words sharing a stripe are locked / validated once (false sharing
+// only costs an occasional abort).  Kernels that lock the cells' meta words
+// (rw, cache, device_tm.cuh) never run concurrently with a bank batch: batches
+// are serialised on the execution stream.
 #pragma once
 #include "device_tm.cuh"
 
@@ -45,9 +66,17 @@ struct StaticTx {
     uint64_t wval[NW];         // value to write to loc[j]
     uint64_t rv[NR > NW ? NR - NW : 1];  // KO_TRACE only: value of read-only word NW+k seen in P1
     uint32_t first;            // bit k set: loc[k] is the first occurrence of its word
-    uint32_t block_loc;        // abort cause: word held FINAL by another transaction ...
-    unsigned long long block_lk;  // ... with this lock word (0: no such blocker)
+    uint32_t block_loc;        // abort cause: lock word (cell, or stripe under KO_STRIPES) held FINAL ...
+    unsigned long long block_lk;  // ... with this value (0: no such blocker)
+    uint32_t sidx[NR];         // KO_STRIPES: stripe of loc[k]
+    uint32_t sfirst;           // KO_STRIPES: bit k set: sidx[k] is the first occurrence of its stripe
 };
+
+// Stripe of a local word (KO_STRIPES): Fibonacci hash, so neighbouring (hot,
+// zipf-ranked) accounts land on different stripes.
+__device__ __forceinline__ uint32_t stripe_of(uint32_t loc, uint32_t stripe_shift) {
+    return (uint32_t)(((uint64_t)loc * 0x9e3779b97f4a7c15ull) >> stripe_shift);
+}
 
 template <int NR>
 __device__ __forceinline__ uint32_t first_occurrences(const uint32_t (&loc)[NR]) {
@@ -81,8 +110,17 @@ __device__ __forceinline__ unsigned long long warp_ticket(bool ok, unsigned long
 enum : int {
     KO_BITMAPS = 4, KO_NO_PROBE = 8, KO_COUNT_TICKETS = 16, KO_PROTOCOL = 64,
     KO_PHASE_CLOCKS = 128, KO_LOCK_READS = 256, KO_SKIP_VALIDATE = 512, KO_NO_TICKET = 1024,
-    KO_TRACE = 2048  // checker traces: also load the VALUES of the read-only words (tx.rv)
+    KO_TRACE = 2048,  // checker traces: also load the VALUES of the read-only words (tx.rv)
+    KO_STRIPES = 4096,  // lock words in the L2-resident stripe table (product bank kernel)
+    KO_STRIPE_SPIN = 8192  // KO_STRIPES: a stripe found locked in P0 is waited for (bounded) instead of aborting
 };
+
+// The lock word guarding lock index `idx` (a cell index, or a stripe index under KO_STRIPES).
+template <int KO>
+__device__ __forceinline__ unsigned long long* lock_word(const ShardView& v, uint32_t idx) {
+    if constexpr ((KO & KO_STRIPES) != 0) return &v.stripes[idx];
+    else return &v.cells[idx].meta;
+}
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
     const long long now = clock64();
@@ -277,6 +315,182 @@ __device__ __forceinline__ bool phased_attempt(StaticTx<NR, NW>& tx, bool active
         if ((need_bits >> (NR + NW + j)) & 1u) set_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
     }
     if constexpr ((KO & KO_PHASE_CLOCKS) != 0) phase_mark(clocks, 4, tclk);
+    ticket = t;
+    return true;
+}
+
+// KO_STRIPES form of phased_attempt (header comment): same contract, same
+// priority rule and waiting discipline, lock words in the stripe table.
+template <int NR, int NW, int KO, class Compute>
+__device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool active, uint32_t me, const ShardView& v,
+                                                unsigned long long* ticket_ctr, unsigned long long& ticket,
+                                                Compute compute) {
+    static_assert((KO & (KO_PROTOCOL | KO_LOCK_READS | KO_PHASE_CLOCKS)) == 0, "cell-lock experiments only");
+    bool ok = active;
+    if (active) tx.block_lk = 0;
+    unsigned long long sl[NR];  // stripe words seen in P0
+    // ---- P0: stripe words (L2 hits)
+    if (ok) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (tx.sfirst & (1u << k)) sl[k] = ld_relaxed(&v.stripes[tx.sidx[k]]);
+        if constexpr ((KO & KO_STRIPE_SPIN) != 0) {
+            // no lock is held yet, so waiting here cannot close a cycle; a holder
+            // is another warp mid-commit (a warp's own lanes hold nothing in P0)
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                if (!(tx.sfirst & (1u << k))) continue;
+                for (int p = 0; p < 64 && (sl[k] & kLockFinal); ++p) {
+                    __nanosleep(64);
+                    sl[k] = ld_relaxed(&v.stripes[tx.sidx[k]]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            if (!(tx.sfirst & (1u << k))) {
+#pragma unroll
+                for (int q = 0; q < k; ++q)
+                    if (tx.sidx[q] == tx.sidx[k] && (tx.sfirst & (1u << q))) sl[k] = sl[q];
+            }
+            if (sl[k] & kLockFinal) {
+                ok = false;
+                tx.block_loc = tx.sidx[k];
+                tx.block_lk = sl[k];
+            }
+        }
+    }
+    // ---- P1: written cells (issued only once the stripe words returned and
+    // showed no holder: the control dependency orders them after P0) + probes
+    uint32_t need_bits = 0;  // bit k: RS bit of word k clear; bit NR+j: WS, bit NR+NW+j: chunk
+    if (ok) {
+        unsigned long long meta;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], meta);
+            else if constexpr ((KO & KO_TRACE) != 0) ld_pair(&v.cells[tx.loc[k]], tx.rv[k >= NW ? k - NW : 0], meta);
+        }
+        unsigned long long pr[NR + 2 * NW];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
+            pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (!((pr[k] >> ((tx.loc[k] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << k;
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            if (!((pr[NR + j] >> ((tx.loc[j] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << (NR + j);
+            if (!((pr[NR + NW + j] >> ((tx.loc[j] >> v.chunk_shift) & 63)) & 1ull))
+                need_bits |= 1u << (NR + NW + j);
+        }
+    }
+    // ---- P2: lock the distinct written stripes (unlocked version -> FINAL)
+    bool held[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) held[j] = false;
+    if (ok) {
+        unsigned long long prev[NW];
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+            if (tx.sfirst & (1u << j))
+                prev[j] = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], kLockFinal | lk_make(me, lk_ver(sl[j])));
+#pragma unroll
+        for (int j = 0; j < NW; ++j) held[j] = (tx.sfirst & (1u << j)) && prev[j] == sl[j];
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            if (!(tx.sfirst & (1u << j)) || held[j] || !ok) continue;
+            unsigned long long c = prev[j];
+            while (c != sl[j]) {  // lost the race: wait for a LOWER-priority holder, else abort
+                if (lk_ver(c) != lk_ver(sl[j]) || !(c & kLockFinal) || lk_owner(c) < me) {
+                    if ((c & kLockFinal) && lk_ver(c) == lk_ver(sl[j])) {
+                        tx.block_loc = tx.sidx[j];
+                        tx.block_lk = c;
+                    }
+                    ok = false;
+                    break;
+                }
+                c = ld_relaxed(&v.stripes[tx.sidx[j]]);
+                if (c == sl[j]) c = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], kLockFinal | lk_make(me, lk_ver(sl[j])));
+            }
+            held[j] = c == sl[j];
+        }
+        if (!ok) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j)
+                if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], sl[j]);  // nothing written: restore
+        }
+    }
+    // ---- P3: ticket (after every surviving lane's locks are performed)
+    unsigned long long t = ~0ull;
+    if (ok) t = take_ticket(ticket_ctr);
+    // ---- P4: validate the read-only stripes this transaction does not hold
+    if (ok) {
+        unsigned long long cur[NR];
+        bool check[NR];
+#pragma unroll
+        for (int k = NW; k < NR; ++k) {
+            bool mine = false;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) mine |= (tx.sidx[q] == tx.sidx[k]);
+            check[k] = !mine && (tx.sfirst & (1u << k));
+            if (check[k]) cur[k] = ld_relaxed(&v.stripes[tx.sidx[k]]);
+        }
+#pragma unroll
+        for (int k = NW; k < NR; ++k) {
+            if (!check[k]) continue;
+            unsigned long long c = cur[k];
+            while (ok) {
+                if (lk_ver(c) != lk_ver(sl[k])) ok = false;                   // committed since P0
+                else if (!(c & kLockFinal)) break;                            // unclaimed: valid
+                else if (lk_owner(c) < me) {                                  // higher priority holds it
+                    ok = false;
+                    tx.block_loc = tx.sidx[k];
+                    tx.block_lk = c;
+                }
+                else c = ld_relaxed(&v.stripes[tx.sidx[k]]);                  // lower priority: wait
+            }
+        }
+        if (!ok) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j)
+                if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], sl[j]);
+        }
+    }
+    if (!ok) {
+        ticket = t;
+        return false;
+    }
+    // ---- P5: write back the distinct written words, then release the stripes
+    compute(tx);
+    const unsigned long long ver = lk_commit(t);
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        if (!(tx.first & (1u << j))) continue;
+        uint64_t val = tx.wval[j];
+#pragma unroll
+        for (int q = j + 1; q < NW; ++q)
+            if (tx.loc[q] == tx.loc[j]) val = tx.wval[q];  // the last write to a word wins
+        st_pair(&v.cells[tx.loc[j]], val, ver);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // cell stores before the releases
+#pragma unroll
+    for (int j = 0; j < NW; ++j)
+        if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], ver);
+    // bitmap bits after the releases, so the fence waits for the two cell
+    // stores only; fire-and-forget REDs (explicit PTX: after a fence the
+    // compiler emits returning ATOMs for atomicOr)
+#pragma unroll
+    for (int k = 0; k < NR; ++k)
+        if ((need_bits >> k) & 1u) red_or_bit(v.rs, tx.loc[k] >> v.gran_shift);
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+        if ((need_bits >> (NR + j)) & 1u) red_or_bit(v.ws, tx.loc[j] >> v.gran_shift);
+        if ((need_bits >> (NR + NW + j)) & 1u) red_or_bit(v.chunk, tx.loc[j] >> v.chunk_shift);
+    }
     ticket = t;
     return true;
 }

@@ -62,11 +62,30 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
     unsigned long long rng = 0x9e3779b97f4a7c15ull * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1);
     unsigned long long clocks[6] = {0, 0, 0, 0, 0, 0};
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
+    // the next record of this lane is fetched while the current one commits
+    // (its DRAM round trip is off the per-transaction chain)
+    uint64_t nx01 = 0, nx23 = 0, nxamt = 0;
+    uint64_t nx_i = ~0ull;
     while (__any_sync(0xffffffffu, i < n)) {
         if (i < n && !loaded) {
-            const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
-            const uint64_t w01 = __ldg(rec), w23 = __ldg(rec + 1);
-            amount = __ldg(rec + 2);
+            uint64_t w01, w23;
+            if (nx_i == i) {
+                w01 = nx01;
+                w23 = nx23;
+                amount = nxamt;
+            } else {
+                const uint64_t* rec = reinterpret_cast<const uint64_t*>(in + i);
+                w01 = __ldg(rec);
+                w23 = __ldg(rec + 1);
+                amount = __ldg(rec + 2);
+            }
+            if (i + stride < n) {
+                const uint64_t* nrec = reinterpret_cast<const uint64_t*>(in + i + stride);
+                nx01 = __ldg(nrec);
+                nx23 = __ldg(nrec + 1);
+                nxamt = __ldg(nrec + 2);
+                nx_i = i + stride;
+            }
             const uint64_t l0 = (w01 & 0xffffffffu) - v.base, l1 = (w01 >> 32) - v.base;
             const uint64_t l2 = (w23 & 0xffffffffu) - v.base, l3 = (w23 >> 32) - v.base;
             if (l0 >= v.size_words || l1 >= v.size_words || l2 >= v.size_words || l3 >= v.size_words) {
@@ -79,6 +98,11 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                 tx.loc[2] = (uint32_t)l2;
                 tx.loc[3] = (uint32_t)l3;
                 tx.first = first_occurrences(tx.loc);
+                if constexpr ((KO & KO_STRIPES) != 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) tx.sidx[k] = stripe_of(tx.loc[k], v.stripe_shift);
+                    tx.sfirst = first_occurrences(tx.sidx);
+                }
                 loaded = true;
             }
         }
@@ -87,7 +111,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         // so the other lanes of the warp keep committing meanwhile.
         bool blocked = false;
         if (i < n && loaded && tx.block_lk) {
-            blocked = ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk;
+            blocked = ld_relaxed(lock_word<KO>(v, tx.block_loc)) == tx.block_lk;
             if (!blocked) tx.block_lk = 0;
         }
         if (i < n && loaded && backoff) {  // randomized sit-out after repeated version-change aborts
@@ -97,11 +121,15 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         if (__all_sync(0xffffffffu, blocked || !(i < n && loaded))) __nanosleep(256);  // whole warp waits
         const bool active = i < n && loaded && !blocked;
         unsigned long long t = ~0ull;
-        const bool committed =
-            phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, [&](StaticTx<4, 2>& x) {
-                x.wval[0] = x.val[0] - amount;
-                x.wval[1] = x.val[1] + amount;
-            }, clocks);
+        const auto transfer = [&](StaticTx<4, 2>& x) {
+            x.wval[0] = x.val[0] - amount;
+            x.wval[1] = x.val[1] + amount;
+        };
+        bool committed;
+        if constexpr ((KO & KO_STRIPES) != 0)
+            committed = striped_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, transfer);
+        else
+            committed = phased_attempt<4, 2, KO>(tx, active, (uint32_t)(i + 1), v, &ctr->ticket, t, transfer, clocks);
         if (committed) {
             tickets[i] = t;
             if constexpr ((KO & KO_TRACE) != 0) {  // reads acct0..3 in order, then writes acct0, acct1
@@ -125,9 +153,12 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
                 wlog_put(v, wbase, t, 1, ~0u);
             }
             ++aborts;
-            if (tx.block_lk && attempts < 4) {  // mild contention: the holder is mid-commit, wait in place briefly
+            // mild contention: the holder is mid-commit, wait in place briefly (cell
+            // locks; a stripe is mostly held by a transaction on ANOTHER word of
+            // it, so the lane sits out at once)
+            if ((KO & KO_STRIPES) == 0 && tx.block_lk && attempts < 4) {
                 uint32_t ns = 32;
-                for (int p = 0; p < 16 && ld_relaxed(&v.cells[tx.block_loc].meta) == tx.block_lk; ++p) {
+                for (int p = 0; p < 16 && ld_relaxed(lock_word<KO>(v, tx.block_loc)) == tx.block_lk; ++p) {
                     __nanosleep(ns);
                     ns = ns < 512 ? 2 * ns : ns;
                 }
@@ -263,7 +294,22 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
 #define HETM_KO_CASE(K) \
     case K: bank_batch_kernel<K><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
     if (v.trace) {  // checker traces: the KO_TRACE instantiation (the product one is untouched)
-        bank_batch_kernel<KO_TRACE><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        if (v.stripes)
+            bank_batch_kernel<KO_TRACE | KO_STRIPES, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        else
+            bank_batch_kernel<KO_TRACE><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        return cudaGetLastError();
+    }
+    static const int spin = [] {  // tuning experiments: HETM_STRIPE_SPIN=1 waits for P0 holders
+        const char* e = std::getenv("HETM_STRIPE_SPIN");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (v.stripes) {  // product: lock words in the L2-resident stripe table
+        if (spin)
+            bank_batch_kernel<KO_STRIPES | KO_STRIPE_SPIN, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr,
+                                                                                         max_attempts);
+        else
+            bank_batch_kernel<KO_STRIPES, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
         return cudaGetLastError();
     }
 #ifdef HETM_EXPERIMENTS

@@ -192,6 +192,80 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView
     flush_pass_a(f, ctr);
 }
 
+// Exchange form of the apply pass (the product default): the whole cell
+// {value, meta} is swapped with {entry.value, TS(entry.ts)} by ONE returning
+// 128-bit atomic exchange (ATOMG.E.EXCH.128).  If the displaced cell was
+// fresher — meta compares higher: a TS word of a larger ts (any TS word
+// outranks a batch version word, as for atomicMax), or, for equal metas, the
+// larger value — the thread puts it back with another exchange and keeps
+// whatever that one displaced, until the cell holds the freshest of all the
+// entries that touched it.  Each retry strictly increases the (meta, value)
+// held in hand, so it terminates; per word, the cell ends with the maximum
+// over the log of (ts, value) — SPEC.md:348's freshest entry (equal ts on
+// one word needs one transaction writing the word twice, which a host write
+// set never holds; the tie goes to the larger value in any delivery order).
+// Cost per entry under uniform access: one random line RMW and no dependent
+// second access, so no restore pass either (the atomicMax form above needs a
+// dependent value store and a restore queue for same-launch races).
+__device__ __forceinline__ void exch_cell(Cell* c, uint64_t v, unsigned long long m, uint64_t& ov,
+                                          unsigned long long& om) {
+    asm volatile("{\n\t.reg .b128 d, s;\n\tmov.b128 s, {%2, %3};\n\t"
+                 "atom.relaxed.gpu.global.exch.b128 d, [%4], s;\n\tmov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(ov), "=l"(om)
+                 : "l"(v), "l"(m), "l"(c)
+                 : "memory");
+}
+template <int U>
+__global__ void __launch_bounds__(kValThreads) apply_xchg_kernel(ShardView v, LogView lv, DevCounters* ctr,
+                                                                 uint64_t win_lo, uint64_t win_hi) {
+    __shared__ SegPrefix sp;
+    const uint64_t n = view_total(lv, sp);
+    const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
+    PassAFlags f;
+    const uint64_t span = (uint64_t)gridDim.x * blockDim.x * U;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * U + threadIdx.x; i0 < n; i0 += span) {
+        EntryRegs e[U];
+        uint64_t ov[U];
+        unsigned long long om[U];
+        bool live[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+            e[u] = i < n ? view_entry(lv, sp, i) : EntryRegs{v.base + v.size_words, 0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t loc = e[u].addr - v.base;
+            live[u] = false;
+            if (i0 + (uint64_t)u * blockDim.x >= n) continue;
+            if (loc >= v.size_words) {
+                f.oob |= win_lo == 0;
+                continue;
+            }
+            if (loc < win_lo || loc >= win_hi) continue;  // another window's pass
+            const uint64_t bit = loc >> v.gran_shift;
+            f.conflict |= (unsigned)((v.rs[bit >> 6] >> (bit & 63)) & 1ull);  // (a) RS test
+            f.bad |= (e[u].ts <= ts_floor);
+            f.maxts = e[u].ts > f.maxts ? e[u].ts : f.maxts;
+            exch_cell(&v.cells[loc], e[u].value, ts_meta(e[u].ts), ov[u], om[u]);  // (b) swap in
+            live[u] = true;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!live[u]) continue;
+            uint64_t hv = e[u].value;
+            unsigned long long hm = ts_meta(e[u].ts);
+            Cell* c = &v.cells[e[u].addr - v.base];
+            while (om[u] > hm || (om[u] == hm && ov[u] > hv)) {  // displaced a fresher cell: put it back
+                hv = ov[u];
+                hm = om[u];
+                exch_cell(c, hv, hm, ov[u], om[u]);
+            }
+        }
+    }
+    flush_pass_a(f, ctr);
+}
+
 // ---- TMA-staged apply (flat, 16-B aligned logs): one persistent CTA per SM
 // walks tiles of kTile log entries; the tile after next is fetched into
 // shared memory by the bulk-copy engine (cp.async.bulk + mbarrier, SASS
@@ -533,6 +607,19 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
         return 1ull << (e ? std::atoi(e) : 32);
     }();
     const uint64_t win = v.size_words > win_min_shard && win_log2 < 40 ? (1ull << win_log2) : v.size_words;
+    static const bool amax = [] {  // A/B only (HETM_APPLY_AMAX=1): the atomicMax + restore form
+        const char* e = std::getenv("HETM_APPLY_AMAX");
+        return e && std::atoi(e) != 0;
+    }();
+    if (!amax) {
+        for (uint64_t lo = 0; lo < v.size_words; lo += win) {
+            const uint64_t hi = v.size_words - lo > win ? lo + win : v.size_words;
+            if (u == 2) apply_xchg_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, lo, hi);
+            else if (u == 8) apply_xchg_kernel<8><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, lo, hi);
+            else apply_xchg_kernel<4><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, lo, hi);
+        }
+        return cudaGetLastError();
+    }
     for (uint64_t lo = 0; lo < v.size_words; lo += win) {
         const uint64_t hi = v.size_words - lo > win ? lo + win : v.size_words;
         if (u == 2) apply_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, rq, lo, hi);
