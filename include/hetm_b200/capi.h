@@ -365,7 +365,11 @@ int hetm_dev_clear_transfer_log(hetm_dev* dev);
 /* ------------------------------------------------ device-resident entries --
  * The same kernels on DEVICE pointers, enqueued on `stream` (a cudaStream_t;
  * NULL = the handle's execution stream) without synchronising.  Used by the
- * benchmark (inputs resident in HBM) and by the multi-GPU shard router. */
+ * benchmark (inputs resident in HBM) and by the multi-GPU shard router.
+ * Batches of one handle must not run concurrently (executeBatch is
+ * externally single-caller): a caller passing its own streams
+ * orders successive batches itself — the bank kernel locks words through the
+ * handle's stripe table, the rw and cache kernels through the cells. */
 int hetm_dev_execute_batch_dptr(hetm_dev* dev, int kernel_id, const void* d_inputs, uint64_t n_tx,
                                 uint64_t* d_tickets, void* stream);
 /* ... with a device results array (HETM_KERNEL_CACHE). */

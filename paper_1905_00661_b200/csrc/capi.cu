@@ -220,6 +220,9 @@ struct hetm_dev {
     uint32_t fault = 0;                     // HETM_FAULT_* (checker mutation suite)
     int schedule = HETM_SCHED_AUTO;         // bank batch schedule (hetm_dev_set_schedule)
     uint32_t auto_scan_left = 0;            // AUTO feedback: device-pointer bank batches still to run as SCAN
+    uint32_t apply_amax_left = 0;           // apply launches still to run in the atomicMax form (hot logs)
+    uint64_t applied_since_read = 0;        // log entries applied since the counters were last read
+    unsigned long long last_apply_dups = 0; // DevCounters::apply_dups at that read
     uint64_t dptr_feedback_n = 0;           // last batch: an optimistic AUTO device-pointer bank batch of n tx
     uint32_t* h_hot = nullptr;              // device-side hot-spot estimate (mapped host word)
     uint32_t* d_hot = nullptr;
@@ -351,6 +354,8 @@ int sync_all(hetm_dev* d) {
 
 constexpr uint64_t kDeliveryRing = 4096;  // delivery events in flight per handle
 
+constexpr uint64_t kApplyHotRatio = 64;   // apply: put-backs per applied entry above 1/64 ...
+constexpr uint32_t kApplyAmaxRun = 16;     // ... run the next 16 apply launches in the atomicMax form
 constexpr uint64_t kAutoAbortRatio = 128;  // AUTO feedback: aborts per transaction above 1/128 ...
 constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches as SCAN
 
@@ -366,7 +371,25 @@ int read_counters(hetm_dev* d) {
         if (d->h_ctr->aborts * kAutoAbortRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
         d->dptr_feedback_n = 0;
     }
+    // apply form feedback (validate.cu apply_xchg_kernel): the exchange form's
+    // put-backs count the log's repeated words; a hot log (zipf, configs[2])
+    // runs the next kApplyAmaxRun launches in the atomicMax form
+    const unsigned long long dups = d->h_ctr->apply_dups - d->last_apply_dups;
+    d->last_apply_dups = d->h_ctr->apply_dups;
+    if (d->applied_since_read && dups * kApplyHotRatio > d->applied_since_read) d->apply_amax_left = kApplyAmaxRun;
+    d->applied_since_read = 0;
     return HETM_OK;
+}
+
+// Restore queue + apply form of the next apply launch over n entries.
+RestoreQueue apply_queue(hetm_dev* d, uint64_t n) {
+    RestoreQueue rq{d->d_restore, d->restore_cap};
+    if (d->apply_amax_left) {
+        rq.amax = 1;
+        --d->apply_amax_left;
+    }
+    d->applied_since_read += n;
+    return rq;
 }
 
 size_t record_bytes(int kernel_id) {
@@ -575,7 +598,7 @@ cudaError_t timed_validate(hetm_dev* d, const hetm_log_entry* log, uint64_t n, i
     if (d->fault & HETM_FAULT_SKIP_RS) v.rs = d->d_rs_zero;  // mutation: the RS test never fires
     cudaError_t e = (apply && (d->fault & HETM_FAULT_SKIP_TS))
                         ? launch_blind_apply(v, log, n, d->d_ctr, d->geom, s)  // mutation: no TS freshness
-                        : launch_validate(v, log, n, apply, d->d_ctr, RestoreQueue{d->d_restore, d->restore_cap},
+                        : launch_validate(v, log, n, apply, d->d_ctr, apply ? apply_queue(d, n) : RestoreQueue{d->d_restore, d->restore_cap},
                                           d->geom, s);
     if (d->timing && n) {
         cudaEventRecord(t1, s);
@@ -1941,8 +1964,7 @@ int hetm_dev_merge_abort_device(hetm_dev* d, int optimized, const uint64_t* host
                                     d->geom, d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "restore(rollback)");
         if ((rc = ensure_restore(d, std::max<uint64_t>(d->arena_n, d->recv_applied ? d->recv_cap : 0)))) return rc;
-        e = launch_rollback_reapply(d->view(), d->d_shadow, round_logs(d), d->d_ctr,
-                                    RestoreQueue{d->d_restore, d->restore_cap}, d->geom,
+        e = launch_rollback_reapply(d->view(), d->d_shadow, round_logs(d), d->d_ctr, apply_queue(d, d->arena_n), d->geom,
                                     d->s_merge);
         if (e != cudaSuccess) return fail(d, e, "rollback_reapply");
         d->record(HETM_D2D, HETM_TAG_ROLLBACK, dirty_bytes);
@@ -2328,7 +2350,9 @@ int hetm_dev_apply_received(hetm_dev* d, uint32_t parity, int mode, uint64_t* n_
     }
     const cudaError_t e = launch_validate_regions(d->view(), arena, counts, d->recv_shards, d->recv_cap,
                                                   mode == HETM_APPLY ? 1 : 0, d->d_ctr,
-                                                  RestoreQueue{d->d_restore, d->restore_cap}, d->geom, s);
+                                                  mode == HETM_APPLY ? apply_queue(d, (uint64_t)d->recv_shards * d->recv_cap)
+                                                                     : RestoreQueue{d->d_restore, d->restore_cap},
+                                                  d->geom, s);
     if (d->timing) {
         cudaEventRecord(t1, s);
         d->tpairs[1].emplace_back(t0, t1);
@@ -2431,7 +2455,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 20) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 19) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

@@ -44,6 +44,7 @@ cudaError_t launch_rw_batch(const ShardView& v, const hetm_rw_tx* d_in, uint64_t
 struct RestoreQueue {
     unsigned long long* idx;
     uint64_t cap;
+    int amax = 0;  // apply form of the launch: 0 exchange (no restore pass), 1 atomicMax + restore (hot logs)
 };
 cudaError_t launch_blind_apply(const ShardView& v, const hetm_log_entry* d_log, uint64_t n, DevCounters* ctr,
                                const LaunchGeom& g, cudaStream_t s);  // fault injection only

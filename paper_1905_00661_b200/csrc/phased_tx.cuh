@@ -37,12 +37,14 @@
 // store); every lock/validation access is an L2 hit
 // (tools/stripe_probe.cu: 0.152 vs 0.275 ms for the same access shape,
 // profiles/r02l_stripe_probe.txt).  The phases become
-//   P0  stripe words of all accounts (the P1 cell loads are issued only after
-//       they returned: control dependency, same ordering argument as the ticket
-//       -> validation step of device_tm.cuh)
-//   P1  128-bit {value, meta} of the written cells; bitmap probes
-//   P2  CAS on the distinct written stripes; P3 ticket; P4 reload of the
-//       read-only stripes not held by this transaction
+//   P0  stripe words of all accounts + bitmap probes (one L2 round trip)
+//   P2  CAS on the distinct written stripes
+//   P1  128-bit {value, meta} of the written cells, issued once the CAS
+//       returned (control dependency, the ordering argument of the ticket ->
+//       validation step of device_tm.cuh): the cells are read under the
+//       locks, and their DRAM round trip overlaps P3/P4 instead of preceding
+//       the locks
+//   P3  ticket; P4 reload of the read-only stripes not held by this transaction
 //   P5  128-bit {value, lk_commit(ticket)} per written cell (the cell keeps
 //       its last writer's version for the merge pick pass), fence.acq_rel.gpu,
 //       release of the held stripes with the same version.
@@ -112,7 +114,9 @@ enum : int {
     KO_PHASE_CLOCKS = 128, KO_LOCK_READS = 256, KO_SKIP_VALIDATE = 512, KO_NO_TICKET = 1024,
     KO_TRACE = 2048,  // checker traces: also load the VALUES of the read-only words (tx.rv)
     KO_STRIPES = 4096,  // lock words in the L2-resident stripe table (product bank kernel)
-    KO_STRIPE_SPIN = 8192  // KO_STRIPES: a stripe found locked in P0 is waited for (bounded) instead of aborting
+    KO_STRIPE_SPIN = 8192,  // KO_STRIPES: a stripe found locked in P0 is waited for (bounded) instead of aborting
+    KO_NO_FENCE = 16384,    // KO_STRIPES knockout (experiments only, INCORRECT): no release fence
+    KO_STRIPE_2PL = 32768   // KO_STRIPES: lock the read-only stripes too (no validation phase)
 };
 
 // The lock word guarding lock index `idx` (a cell index, or a stripe index under KO_STRIPES).
@@ -329,11 +333,34 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
     bool ok = active;
     if (active) tx.block_lk = 0;
     unsigned long long sl[NR];  // stripe words seen in P0
-    // ---- P0: stripe words (L2 hits)
+    uint32_t need_bits = 0;     // bit k: RS bit of word k clear; bit NR+j: WS, bit NR+NW+j: chunk
+    // ---- P0: stripe words + bitmap probes (L2 hits, one round trip)
     if (ok) {
 #pragma unroll
         for (int k = 0; k < NR; ++k)
             if (tx.sfirst & (1u << k)) sl[k] = ld_relaxed(&v.stripes[tx.sidx[k]]);
+        unsigned long long pr[NR + 2 * NW];  // bitmap probes, in the same round trip
+        if constexpr ((KO & (KO_NO_PROBE | KO_BITMAPS)) != 0) {  // knockouts (experiments only)
+#pragma unroll
+            for (int k = 0; k < NR + 2 * NW; ++k) pr[k] = (KO & KO_BITMAPS) ? ~0ull : 0ull;
+        } else {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+                pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
+                pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (!((pr[k] >> ((tx.loc[k] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << k;
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+            if (!((pr[NR + j] >> ((tx.loc[j] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << (NR + j);
+            if (!((pr[NR + NW + j] >> ((tx.loc[j] >> v.chunk_shift) & 63)) & 1ull))
+                need_bits |= 1u << (NR + NW + j);
+        }
         if constexpr ((KO & KO_STRIPE_SPIN) != 0) {
             // no lock is held yet, so waiting here cannot close a cycle; a holder
             // is another warp mid-commit (a warp's own lanes hold nothing in P0)
@@ -360,48 +387,22 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
             }
         }
     }
-    // ---- P1: written cells (issued only once the stripe words returned and
-    // showed no holder: the control dependency orders them after P0) + probes
-    uint32_t need_bits = 0;  // bit k: RS bit of word k clear; bit NR+j: WS, bit NR+NW+j: chunk
+        // ---- P2: lock the distinct written stripes (unlocked version -> FINAL);
+    // with KO_STRIPE_2PL the read-only ones too
+    constexpr int NL = (KO & KO_STRIPE_2PL) != 0 ? NR : NW;
+    bool held[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) held[j] = false;
     if (ok) {
-        unsigned long long meta;
+        unsigned long long prev[NL];
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], meta);
-            else if constexpr ((KO & KO_TRACE) != 0) ld_pair(&v.cells[tx.loc[k]], tx.rv[k >= NW ? k - NW : 0], meta);
-        }
-        unsigned long long pr[NR + 2 * NW];
-#pragma unroll
-        for (int k = 0; k < NR; ++k) pr[k] = v.rs[(tx.loc[k] >> v.gran_shift) >> 6];
-#pragma unroll
-        for (int j = 0; j < NW; ++j) {
-            pr[NR + j] = v.ws[(tx.loc[j] >> v.gran_shift) >> 6];
-            pr[NR + NW + j] = v.chunk[(tx.loc[j] >> v.chunk_shift) >> 6];
-        }
-#pragma unroll
-        for (int k = 0; k < NR; ++k)
-            if (!((pr[k] >> ((tx.loc[k] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << k;
-#pragma unroll
-        for (int j = 0; j < NW; ++j) {
-            if (!((pr[NR + j] >> ((tx.loc[j] >> v.gran_shift) & 63)) & 1ull)) need_bits |= 1u << (NR + j);
-            if (!((pr[NR + NW + j] >> ((tx.loc[j] >> v.chunk_shift) & 63)) & 1ull))
-                need_bits |= 1u << (NR + NW + j);
-        }
-    }
-    // ---- P2: lock the distinct written stripes (unlocked version -> FINAL)
-    bool held[NW];
-#pragma unroll
-    for (int j = 0; j < NW; ++j) held[j] = false;
-    if (ok) {
-        unsigned long long prev[NW];
-#pragma unroll
-        for (int j = 0; j < NW; ++j)
+        for (int j = 0; j < NL; ++j)
             if (tx.sfirst & (1u << j))
                 prev[j] = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], kLockFinal | lk_make(me, lk_ver(sl[j])));
 #pragma unroll
-        for (int j = 0; j < NW; ++j) held[j] = (tx.sfirst & (1u << j)) && prev[j] == sl[j];
+        for (int j = 0; j < NL; ++j) held[j] = (tx.sfirst & (1u << j)) && prev[j] == sl[j];
 #pragma unroll
-        for (int j = 0; j < NW; ++j) {
+        for (int j = 0; j < NL; ++j) {
             if (!(tx.sfirst & (1u << j)) || held[j] || !ok) continue;
             unsigned long long c = prev[j];
             while (c != sl[j]) {  // lost the race: wait for a LOWER-priority holder, else abort
@@ -420,15 +421,31 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
         }
         if (!ok) {
 #pragma unroll
-            for (int j = 0; j < NW; ++j)
+            for (int j = 0; j < NL; ++j)
                 if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], sl[j]);  // nothing written: restore
+        }
+    }
+    // ---- P1: the written cells, loaded UNDER the stripe locks (issued once the
+    // CAS returned: control dependency), so their DRAM round trip overlaps the
+    // ticket and the validation loads instead of preceding the locks; a held
+    // stripe's last writer released it after a fence, so its value is visible
+    if (ok) {
+        unsigned long long meta;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            if (k < NW) ld_pair(&v.cells[tx.loc[k]], tx.val[k < NW ? k : 0], meta);
+            else if constexpr ((KO & KO_TRACE) != 0) ld_pair(&v.cells[tx.loc[k]], tx.rv[k >= NW ? k - NW : 0], meta);
         }
     }
     // ---- P3: ticket (after every surviving lane's locks are performed)
     unsigned long long t = ~0ull;
-    if (ok) t = take_ticket(ticket_ctr);
+    if constexpr ((KO & KO_NO_TICKET) != 0) {
+        if (ok) t = me;
+    } else {
+        if (ok) t = take_ticket(ticket_ctr);
+    }
     // ---- P4: validate the read-only stripes this transaction does not hold
-    if (ok) {
+    if ((KO & (KO_SKIP_VALIDATE | KO_STRIPE_2PL)) == 0 && ok) {
         unsigned long long cur[NR];
         bool check[NR];
 #pragma unroll
@@ -456,7 +473,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
         }
         if (!ok) {
 #pragma unroll
-            for (int j = 0; j < NW; ++j)
+            for (int j = 0; j < NL; ++j)
                 if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], sl[j]);
         }
     }
@@ -476,10 +493,10 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
             if (tx.loc[q] == tx.loc[j]) val = tx.wval[q];  // the last write to a word wins
         st_pair(&v.cells[tx.loc[j]], val, ver);
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // cell stores before the releases
+    if constexpr ((KO & KO_NO_FENCE) == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // cell stores before the releases
 #pragma unroll
-    for (int j = 0; j < NW; ++j)
-        if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], ver);
+    for (int j = 0; j < NL; ++j)  // written stripes publish the commit version, read-only ones keep theirs
+        if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], j < NW ? ver : sl[j]);
     // bitmap bits after the releases, so the fence waits for the two cell
     // stores only; fire-and-forget REDs (explicit PTX: after a fence the
     // compiler emits returning ATOMs for atomicOr)

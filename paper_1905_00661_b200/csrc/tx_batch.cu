@@ -304,6 +304,32 @@ cudaError_t launch_bank_batch(const ShardView& v, const hetm_bank_tx* d_in, uint
         const char* e = std::getenv("HETM_STRIPE_SPIN");
         return e ? std::atoi(e) : 0;
     }();
+#ifdef HETM_EXPERIMENTS
+    static const int sko = [] {  // stripe-kernel phase knockouts (make EXPERIMENTS=1): profiling only, incorrect
+        const char* e = std::getenv("HETM_STRIPE_KO");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (v.stripes && sko) {
+        constexpr int S = KO_STRIPES;
+        switch (sko) {
+            case KO_BITMAPS: bank_batch_kernel<S | KO_BITMAPS, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+            case KO_NO_TICKET: bank_batch_kernel<S | KO_NO_TICKET, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+            case KO_SKIP_VALIDATE: bank_batch_kernel<S | KO_SKIP_VALIDATE, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+            case KO_NO_FENCE: bank_batch_kernel<S | KO_NO_FENCE, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts); break;
+            default: bank_batch_kernel<S | KO_BITMAPS | KO_NO_TICKET | KO_SKIP_VALIDATE | KO_NO_FENCE, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr, max_attempts);
+        }
+        return cudaGetLastError();
+    }
+#endif
+    static const int two_pl = [] {  // tuning experiments: HETM_STRIPE_2PL=1 locks the read-only stripes too
+        const char* e = std::getenv("HETM_STRIPE_2PL");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (v.stripes && two_pl) {
+        bank_batch_kernel<KO_STRIPES | KO_STRIPE_2PL, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr,
+                                                                                    max_attempts);
+        return cudaGetLastError();
+    }
     if (v.stripes) {  // product: lock words in the L2-resident stripe table
         if (spin)
             bank_batch_kernel<KO_STRIPES | KO_STRIPE_SPIN, 2><<<grid, kTxThreads, 0, s>>>(v, d_in, n, d_tickets, ctr,

@@ -194,16 +194,17 @@ __global__ void __launch_bounds__(kValThreads) apply_kernel(ShardView v, LogView
 
 // Exchange form of the apply pass (the product default): the whole cell
 // {value, meta} is swapped with {entry.value, TS(entry.ts)} by ONE returning
-// 128-bit atomic exchange (ATOMG.E.EXCH.128).  If the displaced cell was
+// 128-bit atomic exchange (ATOMG.E.EXCH.128).  If the displaced cell H was
 // fresher — meta compares higher: a TS word of a larger ts (any TS word
 // outranks a batch version word, as for atomicMax), or, for equal metas, the
-// larger value — the thread puts it back with another exchange and keeps
-// whatever that one displaced, until the cell holds the freshest of all the
-// entries that touched it.  Each retry strictly increases the (meta, value)
-// held in hand, so it terminates; per word, the cell ends with the maximum
-// over the log of (ts, value) — SPEC.md:348's freshest entry (equal ts on
-// one word needs one transaction writing the word twice, which a host write
-// set never holds; the tie goes to the larger value in any delivery order).
+// larger value — the thread puts H back with a 128-bit compare-and-swap
+// (ATOMG.E.CAS.128) that only replaces an older cell, retrying on the value
+// it finds until H is back or the cell holds something at least as fresh.
+// Invariant: the freshest (meta, value) seen so far is always in the cell or
+// in a hand that will put it back, so per word the cell ends with the
+// maximum over the log of (ts, value) — SPEC.md:348's freshest entry (equal ts
+// on one word needs one transaction writing the word twice, which a host
+// write set never holds; the tie goes to the larger value in any order).
 // Cost per entry under uniform access: one random line RMW and no dependent
 // second access, so no restore pass either (the atomicMax form above needs a
 // dependent value store and a restore queue for same-launch races).
@@ -215,6 +216,27 @@ __device__ __forceinline__ void exch_cell(Cell* c, uint64_t v, unsigned long lon
                  : "l"(v), "l"(m), "l"(c)
                  : "memory");
 }
+// 128-bit compare-and-swap of a cell; returns the cell as it was.
+__device__ __forceinline__ void cas_cell(Cell* c, uint64_t ev, unsigned long long em, uint64_t v, unsigned long long m,
+                                         uint64_t& ov, unsigned long long& om) {
+    asm volatile("{\n\t.reg .b128 d, e, s;\n\tmov.b128 e, {%2, %3};\n\tmov.b128 s, {%4, %5};\n\t"
+                 "atom.relaxed.gpu.global.cas.b128 d, [%6], e, s;\n\tmov.b128 {%0, %1}, d;\n\t}"
+                 : "=l"(ov), "=l"(om)
+                 : "l"(ev), "l"(em), "l"(v), "l"(m), "l"(c)
+                 : "memory");
+}
+__device__ __forceinline__ bool fresher(unsigned long long am, uint64_t av, unsigned long long bm, uint64_t bv) {
+    return am > bm || (am == bm && av > bv);
+}
+// Two forms, chosen per launch by the handle (RestoreQueue::amax): a log whose
+// words repeat a lot (zipf host logs, BASELINE configs[2]) makes the exchange
+// form ping-pong on its hot words — 128-bit atomics on one address serialise
+// (cfg3 round 2.1 vs 1.0 ms) — while atomicMax lets every stale duplicate
+// lose in one cheap op.  The kernel counts its put-backs (DevCounters::
+// apply_dups, monotone); when the handle reads the counters and more than
+// 1/64 of the entries applied since the last read needed one, the next
+// launches run the atomicMax form + restore pass (capi.cu read_counters).
+// Both forms leave identical cells.
 template <int U>
 __global__ void __launch_bounds__(kValThreads) apply_xchg_kernel(ShardView v, LogView lv, DevCounters* ctr,
                                                                  uint64_t win_lo, uint64_t win_hi) {
@@ -222,6 +244,7 @@ __global__ void __launch_bounds__(kValThreads) apply_xchg_kernel(ShardView v, Lo
     const uint64_t n = view_total(lv, sp);
     const uint64_t ts_floor = ld_relaxed(&ctr->ts_floor);
     PassAFlags f;
+    unsigned long long putbacks = 0;
     const uint64_t span = (uint64_t)gridDim.x * blockDim.x * U;
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * U + threadIdx.x; i0 < n; i0 += span) {
         EntryRegs e[U];
@@ -253,17 +276,30 @@ __global__ void __launch_bounds__(kValThreads) apply_xchg_kernel(ShardView v, Lo
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (!live[u]) continue;
-            uint64_t hv = e[u].value;
-            unsigned long long hm = ts_meta(e[u].ts);
             Cell* c = &v.cells[e[u].addr - v.base];
-            while (om[u] > hm || (om[u] == hm && ov[u] > hv)) {  // displaced a fresher cell: put it back
-                hv = ov[u];
-                hm = om[u];
-                exch_cell(c, hv, hm, ov[u], om[u]);
+            // displaced a fresher cell H: put it back with a compare-and-swap
+            // that only ever replaces something older than H (our own entry, or
+            // whatever displaced it since)
+            uint64_t cv = e[u].value;  // what we believe the cell holds
+            unsigned long long cm = ts_meta(e[u].ts);
+            if (!fresher(om[u], ov[u], cm, cv)) continue;
+            ++putbacks;
+            const uint64_t hv = ov[u];
+            const unsigned long long hm = om[u];
+            for (;;) {
+                uint64_t pv;
+                unsigned long long pm;
+                cas_cell(c, cv, cm, hv, hm, pv, pm);
+                if (pv == cv && pm == cm) break;      // H is back
+                if (!fresher(hm, hv, pm, pv)) break;  // the cell already holds something at least as fresh
+                cv = pv;
+                cm = pm;
             }
         }
     }
     flush_pass_a(f, ctr);
+    putbacks = warp_sum(putbacks);
+    if (lane_id() == 0 && putbacks) atomicAdd(&ctr->apply_dups, putbacks);
 }
 
 // ---- TMA-staged apply (flat, 16-B aligned logs): one persistent CTA per SM
@@ -607,11 +643,12 @@ static cudaError_t launch_view(const ShardView& v, const LogView& lv, uint64_t n
         return 1ull << (e ? std::atoi(e) : 32);
     }();
     const uint64_t win = v.size_words > win_min_shard && win_log2 < 40 ? (1ull << win_log2) : v.size_words;
-    static const bool amax = [] {  // A/B only (HETM_APPLY_AMAX=1): the atomicMax + restore form
+    static const bool amax = [] {  // A/B only (HETM_APPLY_AMAX=1): always the atomicMax + restore form
+        // (otherwise the handle picks it per launch for hot logs: RestoreQueue::amax)
         const char* e = std::getenv("HETM_APPLY_AMAX");
         return e && std::atoi(e) != 0;
     }();
-    if (!amax) {
+    if (!amax && !rq.amax) {  // the exchange form (apply_xchg_kernel): no restore pass
         for (uint64_t lo = 0; lo < v.size_words; lo += win) {
             const uint64_t hi = v.size_words - lo > win ? lo + win : v.size_words;
             if (u == 2) apply_xchg_kernel<2><<<agrid, kValThreads, 0, s>>>(v, lv, ctr, lo, hi);

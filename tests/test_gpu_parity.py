@@ -249,6 +249,30 @@ def test_validate_hot_words_one_chunk(hetm, orc, dev_factory):
         assert (d.download(hetm.REPLICA_DEV) == want).all(), tsorder
 
 
+def test_validate_adaptive_apply_modes(hetm, orc, dev_factory):
+    """The apply pass switches between its exchange form and its atomicMax form
+    per launch, decided on the device from the duplicates the previous launch
+    met (validate.cu apply_xchg_kernel): chunks alternating uniform and hot
+    words, in both orders, with words repeating ACROSS launches of one round
+    (an older entry arriving after a fresher one was applied), must leave the
+    freshest value in every word after every chunk."""
+    W = 1 << 13
+    rng = np.random.default_rng(2024)
+    d = dev_factory(W, rs_gran_bytes=8, log_capacity=1 << 16)
+    ts, want = np.zeros(W, np.uint64), np.zeros(W, np.uint64)
+    n = 1 << 14
+    all_ts = rng.permutation(12 * n) + 1  # one round: ts unique, chunks arrive out of ts order
+    for k, hot in enumerate([False, True, True, False, False, True, False, True, True, True, False, False]):
+        log = np.zeros(n, dtype=hetm.LOG_ENTRY)
+        log["addr"] = rng.integers(0, 64 if hot else W, n)
+        log["value"] = rng.integers(0, 2**63, n, dtype=np.uint64)
+        log["ts"] = all_ts[k * n:(k + 1) * n]
+        d.stream_chunk(log, seq=k)
+        assert not d.round_verdict()
+        orc.validate_chunk(log, np.zeros(W // 64, np.uint64), 8, ts, want)
+        assert (d.download(hetm.REPLICA_DEV) == want).all(), (k, hot)
+
+
 def test_validate_permuted_delivery_orders(hetm, orc, dev_factory):
     """Acceptance #5 on the device: 10 delivery orders, same max-ts result."""
     W = 256

@@ -1,0 +1,16 @@
+# lean exchange apply + 2PL stripe variant: step sweep, 2PL parity subset, full GPU suite
+mkdir -p gpurun_out
+run() {  # tag, env...
+  tag=$1; shift
+  env "$@" timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --live-rounds 0 --no-cfg5 --e2e-steps 3 > /tmp/b.json 2>/dev/null
+  python -c "
+import json,sys;l=json.loads(open('/tmp/b.json').readline());b=l['step_breakdown_ms'];c=l['configs']
+print('$tag', 'step %.4f batch %.4f va %.4f merge %.4f aborts %d cfg3 %.3f ms cfg4 %.3f ms' % (b['step'],b['batch'],b['validate_apply'],b['merge_stage'],l['batch']['aborts_last'],c['cfg3_zipf']['ms_per_round'],c['cfg4_cache']['ms_per_round']), l['bank_sum_ok'], l['shadow_equals_replica'])" >> gpurun_out/r02v_sweep.txt 2>&1
+}
+run product
+run twopl HETM_STRIPE_2PL=1
+run twopl_b2 HETM_STRIPE_2PL=1 HETM_TX_BLOCKS_PER_SM=2
+run twopl_bits23 HETM_STRIPE_2PL=1 HETM_STRIPE_BITS=23
+run product_again
+HETM_STRIPE_2PL=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_bank_schedule.py tests/test_acceptance.py tests/test_trace_gpu.py -m gpu -q -p no:cacheprovider -x > gpurun_out/r02v_2pl_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r02v_2pl_tests.log
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/r02v_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r02v_tests.log
