@@ -195,6 +195,7 @@ typedef struct hetm_batch_stats {
     uint64_t ticket_first; /* tickets of this batch lie in [ticket_first, ticket_end) */
     uint64_t ticket_end;
     double kernel_ms;      /* device time of the batch kernel (CUDA events) */
+    uint64_t retried;      /* transactions that committed only after >= 2 aborted attempts */
 } hetm_batch_stats;
 
 typedef struct hetm_merge_stats {

@@ -82,6 +82,7 @@ class BatchStats(C.Structure):
         ("ticket_first", C.c_uint64),
         ("ticket_end", C.c_uint64),
         ("kernel_ms", C.c_double),
+        ("retried", C.c_uint64),
     ]
 
 

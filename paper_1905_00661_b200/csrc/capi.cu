@@ -356,16 +356,18 @@ constexpr uint64_t kDeliveryRing = 4096;  // delivery events in flight per handl
 
 constexpr uint64_t kApplyHotRatio = 64;   // apply: put-backs per applied entry above 1/64 ...
 constexpr uint32_t kApplyAmaxRun = 16;     // ... run the next 16 apply launches in the atomicMax form
-constexpr uint64_t kAutoAbortRatio = 128;  // AUTO feedback: aborts per transaction above 1/128 ...
+constexpr uint64_t kAutoAbortRatio = 40;   // AUTO feedback: aborts per transaction above 1/40 (stripe kernel:
+                                           // uniform 1.8 %, zipf 0.5 3.4 %, profiles/r02x_stripe_skew.txt) ...
 constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches as SCAN
 
 int read_counters(hetm_dev* d) {
     CK(d, cudaMemcpy(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
     // AUTO feedback for device-pointer batches, judged when the caller syncs the
     // counters (verdict, stats): an optimistic bank batch that aborted more than 1
-    // attempt per 128 transactions had conflict chains the sample did not predict
-    // (the zipf ~0.5 band: uniform batches abort ~0.2-0.3 %, where SCAN wins 2x
-    // from ~1 %, profiles/r01g_sched_crossover.txt); the next kAutoScanRun
+    // attempt per 40 transactions had conflict chains the sample did not predict
+    // (the zipf ~0.5 band: the stripe kernel aborts 1.8 % of uniform transfers —
+    // stripe false sharing — and 3.4 % at zipf 0.5, where SCAN wins 2.4x: 0.31
+    // vs 0.75 ms, profiles/r02x_stripe_skew.txt); the next kAutoScanRun
     // device-pointer batches run as SCAN, then the optimistic kernel is tried again.
     if (d->dptr_feedback_n) {
         if (d->h_ctr->aborts * kAutoAbortRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
@@ -522,7 +524,10 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     if (kernel_id == HETM_KERNEL_CACHE) d->round_versioned = false;  // set-granular locks: claim the words
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
-    if (reset_counters) CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
+    if (reset_counters) {
+        CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
+        CK(d, cudaMemsetAsync(&d->d_ctr->retried, 0, sizeof(unsigned long long), s));
+    }
     cudaError_t e = cudaSuccess;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (d->timing) {
@@ -823,10 +828,11 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_ws, d->rs_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
-    {  // lock-stripe table of the bank kernel: 2^22 words (32 MiB, L2-resident), fewer for small shards
+    {  // lock-stripe table of the bank kernel: 2^24 words (128 MiB: false-sharing aborts 1.8 % of uniform
+       // transfers vs 6.6 % at 2^22, same batch time, profiles/r02x_stripe_skew.txt), fewer for small shards
         static const uint32_t max_bits = [] {  // tuning experiments: HETM_STRIPE_BITS
             const char* e = std::getenv("HETM_STRIPE_BITS");
-            return e ? (uint32_t)std::atoi(e) : 22u;
+            return e ? (uint32_t)std::atoi(e) : 24u;
         }();
         uint32_t bits = 10;
         while (bits < max_bits && (1ull << bits) < d->W) ++bits;
@@ -1153,6 +1159,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     st.n_tx = n_tx;
     st.committed = d->h_ctr->committed;
     st.aborts = d->h_ctr->aborts;
+    st.retried = d->h_ctr->retried;
     st.livelocked = d->h_ctr->livelocked;
     st.ticket_first = first;
     st.ticket_end = d->h_ctr->ticket;
@@ -2233,6 +2240,7 @@ int hetm_dev_read_counters(hetm_dev* d, int* conflict, hetm_batch_stats* last) {
         std::memset(last, 0, sizeof(*last));
         last->committed = d->h_ctr->committed;
         last->aborts = d->h_ctr->aborts;
+        last->retried = d->h_ctr->retried;
         last->livelocked = d->h_ctr->livelocked;
         last->ticket_end = d->h_ctr->ticket;
     }
@@ -2455,7 +2463,7 @@ int hetm_dev_stream_handle(hetm_dev* d, int which, void** stream) {
 }
 
 int hetm_dev_debug_words(hetm_dev* d, uint64_t* out, uint64_t n) {
-    if (!d || !out || n > 19) return HETM_ERR_INVALID_ARG;
+    if (!d || !out || n > 18) return HETM_ERR_INVALID_ARG;
     int rc = sync_all(d);
     if (rc) return rc;
     if ((rc = read_counters(d))) return rc;

@@ -56,7 +56,8 @@ struct DevCounters {
     unsigned long long wlog_base;    // first commit ticket of the round (write-set log origin)
     unsigned long long wlog_overflow;// a committed write set did not fit the write-set log
     unsigned long long apply_dups;   // apply: exchange put-backs so far (monotone; the host judges deltas)
-    unsigned long long pad[19];      // diagnostics (phase clocks / ticket counts)
+    unsigned long long retried;      // last batch: transactions committed after >= 2 aborted attempts
+    unsigned long long pad[18];      // diagnostics (phase clocks / ticket counts)
 };
 
 static_assert(sizeof(DevCounters) == 256, "two 128-B lines");

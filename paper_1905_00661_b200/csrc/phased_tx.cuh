@@ -31,7 +31,7 @@
 // oracle's sequential replay).
 //
 // KO_STRIPES (the product bank kernel): the versioned lock words live in an
-// L2-resident STRIPE TABLE (ShardView::stripes, 2^22 words = 32 MiB, word ->
+// L2-resident STRIPE TABLE (ShardView::stripes, 2^24 words = 128 MiB, word ->
 // stripe by a multiplicative hash) instead of the cells' meta words.  Only the
 // written cells are then touched in DRAM (one 128-bit load, one 128-bit
 // store); every lock/validation access is an L2 hit

@@ -17,7 +17,10 @@ namespace hetm_b200 {
 constexpr int kTxThreads = 256;
 
 __device__ __forceinline__ void flush_batch_counters(unsigned long long commits, unsigned long long aborts,
-                                                     unsigned long long livelocks, unsigned oob, DevCounters* ctr) {
+                                                     unsigned long long livelocks, unsigned oob, DevCounters* ctr,
+                                                     unsigned long long retried = 0) {
+    retried = warp_sum(retried);
+    if (lane_id() == 0 && retried) atomicAdd(&ctr->retried, retried);
     if (__any_sync(0xffffffffu, oob) && lane_id() == 0) atomicOr(&ctr->oob, 1u);
     commits = warp_sum(commits);
     aborts = warp_sum(aborts);
@@ -49,7 +52,7 @@ template <int KO, int MINB = 4>
 __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView v, const hetm_bank_tx* __restrict__ in,
                                                                    uint64_t n, unsigned long long* __restrict__ tickets,
                                                                    DevCounters* ctr, uint32_t max_attempts) {
-    unsigned long long commits = 0, aborts = 0, livelocks = 0;
+    unsigned long long commits = 0, aborts = 0, livelocks = 0, retried = 0;
     unsigned oob = 0;
     uint64_t i, stride;
     tx_range(v, n, i, stride);
@@ -147,6 +150,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             wlog_put(v, wbase, t, 0, tx.loc[0]);
             wlog_put(v, wbase, t, 1, tx.loc[1]);
             ++commits;
+            retried += attempts >= 2;
         } else if (active) {
             if (t != ~0ull) {  // aborted after taking a ticket: its log slots stay empty
                 wlog_put(v, wbase, t, 0, ~0u);
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             if (lane_id() == 0) atomicAdd(&ctr->pad[p], x);
         }
     }
-    flush_batch_counters(commits, aborts, livelocks, oob, ctr);
+    flush_batch_counters(commits, aborts, livelocks, oob, ctr, retried);
 }
 
 // Generic <=4 reads / <=2 read-modify-writes (hetm_rw_tx) through the

@@ -110,7 +110,7 @@ def test_auto_feedback_device_pointer_batches(hetm, orc, dev_factory):
         orc.bank_replay(ref, txs, orc.order_by_ticket(t), 8, 16384)
         seq.append((int(st.aborts), bool((np.diff(t.astype(np.int64)) == 1).all())))
     assert (d.download(hetm.REPLICA_DEV) == ref).all()
-    assert seq[0][0] * 128 > n and not seq[0][1]          # optimistic, abort-heavy
+    assert seq[0][0] * 40 > n and not seq[0][1]           # optimistic, abort-heavy (capi.cu kAutoAbortRatio)
     assert seq[1] == (0, True) and seq[2] == (0, True)    # then SCAN
 
 
