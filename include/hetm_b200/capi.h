@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define HETM_B200_ABI_VERSION 2
+#define HETM_B200_ABI_VERSION 3  /* 3: hetm_batch_stats.retried */
 
 /* ---------------------------------------------------------------- status --
  * One code per hetm::HetmError subclass (types.hpp:38-48) plus device codes. */

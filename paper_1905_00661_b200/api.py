@@ -202,6 +202,7 @@ class BatchResult:
     ticket_end: int
     kernel_ms: float
     results: np.ndarray | None = None  # CACHE_RESULT per transaction (KERNEL_CACHE)
+    retried: int = 0  # transactions that committed only after >= 2 aborted attempts
 
 
 # ------------------------------------------------------------- device guest
@@ -300,6 +301,7 @@ class GpuDevice:
         r = BatchResult(tickets, st.n_tx, st.committed, st.aborts, st.livelocked, st.ticket_first,
                         st.ticket_end, st.kernel_ms)
         r.results = res
+        r.retried = st.retried
         return r
 
     def set_cache_geometry(self, base_word: int, n_sets: int):

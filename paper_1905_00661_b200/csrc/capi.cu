@@ -356,21 +356,23 @@ constexpr uint64_t kDeliveryRing = 4096;  // delivery events in flight per handl
 
 constexpr uint64_t kApplyHotRatio = 64;   // apply: put-backs per applied entry above 1/64 ...
 constexpr uint32_t kApplyAmaxRun = 16;     // ... run the next 16 apply launches in the atomicMax form
-constexpr uint64_t kAutoAbortRatio = 40;   // AUTO feedback: aborts per transaction above 1/40 (stripe kernel:
-                                           // uniform 1.8 %, zipf 0.5 3.4 %, profiles/r02x_stripe_skew.txt) ...
+constexpr uint64_t kAutoRetryRatio = 1024; // AUTO feedback: transactions needing a 3rd attempt above 1/1024
+                                           // (stripe kernel: uniform 0.035 %, zipf 0.4 0.046 %, zipf 0.5
+                                           // 0.23 %, profiles/r02z_skew.txt) ...
 constexpr uint32_t kAutoScanRun = 15;      // ... run the next 15 bank batches as SCAN
 
 int read_counters(hetm_dev* d) {
     CK(d, cudaMemcpy(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost));
     // AUTO feedback for device-pointer batches, judged when the caller syncs the
-    // counters (verdict, stats): an optimistic bank batch that aborted more than 1
-    // attempt per 40 transactions had conflict chains the sample did not predict
-    // (the zipf ~0.5 band: the stripe kernel aborts 1.8 % of uniform transfers —
-    // stripe false sharing — and 3.4 % at zipf 0.5, where SCAN wins 2.4x: 0.31
-    // vs 0.75 ms, profiles/r02x_stripe_skew.txt); the next kAutoScanRun
-    // device-pointer batches run as SCAN, then the optimistic kernel is tried again.
+    // counters (verdict, stats): an optimistic bank batch in which more than 1
+    // transaction per 1024 needed a third attempt had conflict chains the sample
+    // did not predict (the zipf ~0.5 band, where SCAN wins 2x: 0.31 vs 0.62-0.67
+    // ms).  Repeated aborts of ONE transaction, not the abort count: stripe false
+    // sharing aborts 1.8 % of uniform transfers once but almost never twice
+    // (profiles/r02z_skew.txt).  The next kAutoScanRun device-pointer batches run
+    // as SCAN, then the optimistic kernel is tried again.
     if (d->dptr_feedback_n) {
-        if (d->h_ctr->aborts * kAutoAbortRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
+        if (d->h_ctr->retried * kAutoRetryRatio > d->dptr_feedback_n) d->auto_scan_left = kAutoScanRun;
         d->dptr_feedback_n = 0;
     }
     // apply form feedback (validate.cu apply_xchg_kernel): the exchange form's
@@ -1114,12 +1116,18 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
                               d->s_in));
         CK(d, cudaEventRecord(d->in_ev[k], d->s_in));
     }
-    d->dptr_feedback_n = 0;  // the counters now hold this batch's (not judged by the feedback)
-    // (no abort feedback here: a host-buffer batch runs as pipelined pieces, on which
-    // the optimistic kernel's chains are shorter and SCAN's fixed costs higher —
-    // zipf 0.5: 0.68 vs 0.72 ms per 2^20, tools/auto_feedback_probe.py)
-    const bool hot = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx &&
-                     bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
+    d->dptr_feedback_n = 0;  // the counters now hold this batch's (judged below, synchronously)
+    // AUTO for host-buffer bank batches: the CPU sample, or the retry feedback of
+    // an earlier optimistic batch (judged at the end of this call: the pieces'
+    // counters are read back anyway; zipf 0.5 in 8 pieces: SCAN 0.65 vs
+    // optimistic 0.76 ms median, profiles/r02z_auto_feedback.txt)
+    const bool auto_bank = kernel_id == HETM_KERNEL_BANK && d->schedule == HETM_SCHED_AUTO && n_tx;
+    bool hot = false;
+    if (auto_bank) {
+        const bool feedback = d->auto_scan_left > 0;
+        if (feedback) --d->auto_scan_left;
+        hot = feedback || bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
+    }
     for (uint64_t k = 0; k < P; ++k) {
         const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
         if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
@@ -1166,6 +1174,7 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     st.kernel_ms = ms;
     d->last_batch = st;
     if (stats) *stats = st;
+    if (auto_bank && !hot && !trace && st.retried * kAutoRetryRatio > n_tx) d->auto_scan_left = kAutoScanRun;
     if (d->h_ctr->oob) return HETM_ERR_OUT_OF_BOUNDS;
     if (st.livelocked) return HETM_ERR_LIVELOCK;
     return HETM_OK;

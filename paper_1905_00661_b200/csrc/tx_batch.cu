@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
     uint64_t amount = 0;
     StaticTx<4, 2> tx;
     tx.block_lk = 0;
-    uint32_t backoff = 0;
+    uint32_t backoff = 0, block_polls = 0;
     unsigned long long rng = 0x9e3779b97f4a7c15ull * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1);
     unsigned long long clocks[6] = {0, 0, 0, 0, 0, 0};
     const unsigned long long wbase = ld_relaxed(&ctr->wlog_base);
@@ -115,7 +115,14 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         bool blocked = false;
         if (i < n && loaded && tx.block_lk) {
             blocked = ld_relaxed(lock_word<KO>(v, tx.block_loc)) == tx.block_lk;
-            if (!blocked) tx.block_lk = 0;
+            // bounded: the same lock word can come back (a holder that aborted and
+            // re-locked with the same priority and version), so after 256 polls the
+            // lane simply tries again
+            if (blocked && ++block_polls > 256) blocked = false;
+            if (!blocked) {
+                tx.block_lk = 0;
+                block_polls = 0;
+            }
         }
         if (i < n && loaded && backoff) {  // randomized sit-out after repeated version-change aborts
             --backoff;

@@ -38,7 +38,7 @@ def test_library_is_sm100a_only(hetm):
 
 def test_abi_version_and_strerror(hetm):
     lib = hetm._lib.lib
-    assert lib.hetm_abi_version() == 2
+    assert lib.hetm_abi_version() == 3
     assert lib.hetm_strerror(0) == b"ok"
     assert lib.hetm_strerror(5) == b"livelock-budget-exceeded"
     assert lib.hetm_strerror(102) == b"no-cuda-device"

@@ -19,7 +19,7 @@ d = hetm.GpuDevice(W, rs_gran_bytes=1024)
 d.register_kernel(hetm.KERNEL_BANK)
 d.upload(hetm.REPLICA_DEV, 0, np.full(W, 1000, np.uint64))
 tk = torch.empty(n, dtype=torch.int64, device="cuda")
-print(f"stripe bits (HETM_STRIPE_BITS) {os.environ.get('HETM_STRIPE_BITS', '22')}")
+print(f"stripe bits (HETM_STRIPE_BITS) {os.environ.get('HETM_STRIPE_BITS', '24 (default)')}")
 for alpha in (0.0, 0.3, 0.4, 0.5, 0.6, 0.7):
     bt = [torch.from_numpy(hetm.gen_bank_batch(900 + k, n, 0, W, zipf=alpha).view(np.uint8)).cuda() for k in range(2)]
     row = [f"alpha {alpha:.1f}"]
