@@ -235,7 +235,7 @@ struct hetm_dev {
     PreparedMerge prep;                     // hetm_dev_merge_prepare state
     cudaEvent_t ev_stage = nullptr;         // delta records gathered (s_merge)
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
-    unsigned long long* d_stripes = nullptr;  // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES)
+    unsigned int* d_stripes = nullptr;        // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES)
     uint32_t stripe_shift = 64;
     std::vector<cudaEvent_t> in_ev;       // per-piece input H2D landed
     std::vector<cudaEvent_t> kp_ev;       // per-piece kernel start/end (timing events)
@@ -830,17 +830,18 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     if ((rc = dev_alloc(d, (void**)&d->d_ws, d->rs_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_chunk, d->chunk_words * 8))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_ctr, sizeof(DevCounters)))) return bail(rc);
-    {  // lock-stripe table of the bank kernel: 2^24 words (128 MiB: false-sharing aborts 1.8 % of uniform
-       // transfers vs 6.6 % at 2^22, same batch time, profiles/r02x_stripe_skew.txt), fewer for small shards
+    {  // lock-stripe table of the bank kernel: 2^24 32-bit words (64 MiB: false-sharing aborts 1.8 % of
+       // uniform transfers vs 6.6 % at 2^22, same batch time, profiles/r02x_stripe_skew.txt), fewer for
+       // small shards
         static const uint32_t max_bits = [] {  // tuning experiments: HETM_STRIPE_BITS
             const char* e = std::getenv("HETM_STRIPE_BITS");
             return e ? (uint32_t)std::atoi(e) : 24u;
         }();
         uint32_t bits = 10;
         while (bits < max_bits && (1ull << bits) < d->W) ++bits;
-        if ((rc = dev_alloc(d, (void**)&d->d_stripes, (8ull << bits)))) return bail(rc);
+        if ((rc = dev_alloc(d, (void**)&d->d_stripes, (4ull << bits)))) return bail(rc);
         d->stripe_shift = 64 - bits;
-        CK(d, cudaMemset(d->d_stripes, 0, 8ull << bits));  // unlocked, version 0
+        CK(d, cudaMemset(d->d_stripes, 0, 4ull << bits));  // unlocked, version 0
     }
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);

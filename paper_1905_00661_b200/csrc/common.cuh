@@ -77,7 +77,7 @@ struct ShardView {
     unsigned long long* wlog_ovf; // set when a committed write set did not fit (DevCounters::wlog_overflow)
     uint32_t serial;           // deterministic single-worker mode (HETM_CFG_DETERMINISTIC)
     unsigned long long* trace; // checker trace of the batch (nullptr: off): HETM_TRACE_TX_WORDS per tx index
-    unsigned long long* stripes; // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES; nullptr: cell locks)
+    unsigned int* stripes;     // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES; nullptr: cell locks)
     uint32_t stripe_shift;       // stripe = (loc * 2^64/phi) >> stripe_shift  (64 - log2 stripes)
 };
 
@@ -141,6 +141,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned int* p, unsigned int v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

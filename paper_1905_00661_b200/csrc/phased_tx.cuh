@@ -31,7 +31,7 @@
 // oracle's sequential replay).
 //
 // KO_STRIPES (the product bank kernel): the versioned lock words live in an
-// L2-resident STRIPE TABLE (ShardView::stripes, 2^24 words = 128 MiB, word ->
+// L2-resident STRIPE TABLE (ShardView::stripes, 2^24 32-bit words = 64 MiB, word ->
 // stripe by a multiplicative hash) instead of the cells' meta words.  Only the
 // written cells are then touched in DRAM (one 128-bit load, one 128-bit
 // store); every lock/validation access is an L2 hit
@@ -46,7 +46,7 @@
 //       the locks
 //   P3  ticket; P4 reload of the read-only stripes not held by this transaction
 //   P5  128-bit {value, lk_commit(ticket)} per written cell (the cell keeps
-//       its last writer's version for the merge pick pass), fence.acq_rel.gpu,
+//       its last writer's version for the merge pick pass), fence.release.gpu,
 //       release of the held stripes with the same version.
 // Distinct words sharing a stripe are locked / validated once (false sharing
 // only costs an occasional abort).  Kernels that lock the cells' meta words
@@ -119,11 +119,21 @@ enum : int {
     KO_STRIPE_2PL = 32768   // KO_STRIPES: lock the read-only stripes too (no validation phase)
 };
 
-// The lock word guarding lock index `idx` (a cell index, or a stripe index under KO_STRIPES).
+// Stripe words (KO_STRIPES) are 32 bits: unlocked = the 31-bit commit version
+// of the stripe's last writer (lk_commit), locked = kStripeFinal | owner
+// priority.  A locked stripe hides its version; a waiter compares it after
+// the release, so the priority rule and the abort decisions are unchanged
+// (a holder on a changed version is waited for, then the change aborts).
+constexpr unsigned int kStripeFinal = 0x80000000u;
+__device__ __forceinline__ unsigned int stripe_lock(uint32_t me) { return kStripeFinal | me; }
+__device__ __forceinline__ uint32_t stripe_owner(unsigned int c) { return c & ~kStripeFinal; }
+
+// Current value of the lock word guarding lock index `idx` (a cell index, or a
+// stripe index under KO_STRIPES), widened to 64 bits for the sit-out poll.
 template <int KO>
-__device__ __forceinline__ unsigned long long* lock_word(const ShardView& v, uint32_t idx) {
-    if constexpr ((KO & KO_STRIPES) != 0) return &v.stripes[idx];
-    else return &v.cells[idx].meta;
+__device__ __forceinline__ unsigned long long lock_value(const ShardView& v, uint32_t idx) {
+    if constexpr ((KO & KO_STRIPES) != 0) return ld_relaxed(&v.stripes[idx]);
+    else return ld_relaxed(&v.cells[idx].meta);
 }
 
 __device__ __forceinline__ void phase_mark(unsigned long long* acc, int phase, long long& t) {
@@ -332,7 +342,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
     static_assert((KO & (KO_PROTOCOL | KO_LOCK_READS | KO_PHASE_CLOCKS)) == 0, "cell-lock experiments only");
     bool ok = active;
     if (active) tx.block_lk = 0;
-    unsigned long long sl[NR];  // stripe words seen in P0
+    unsigned int sl[NR];        // stripe words seen in P0
     uint32_t need_bits = 0;     // bit k: RS bit of word k clear; bit NR+j: WS, bit NR+NW+j: chunk
     // ---- P0: stripe words + bitmap probes (L2 hits, one round trip)
     if (ok) {
@@ -367,7 +377,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 if (!(tx.sfirst & (1u << k))) continue;
-                for (int p = 0; p < 64 && (sl[k] & kLockFinal); ++p) {
+                for (int p = 0; p < 64 && (sl[k] & kStripeFinal); ++p) {
                     __nanosleep(64);
                     sl[k] = ld_relaxed(&v.stripes[tx.sidx[k]]);
                 }
@@ -380,7 +390,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
                 for (int q = 0; q < k; ++q)
                     if (tx.sidx[q] == tx.sidx[k] && (tx.sfirst & (1u << q))) sl[k] = sl[q];
             }
-            if (sl[k] & kLockFinal) {
+            if (sl[k] & kStripeFinal) {
                 ok = false;
                 tx.block_loc = tx.sidx[k];
                 tx.block_lk = sl[k];
@@ -394,20 +404,20 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
 #pragma unroll
     for (int j = 0; j < NL; ++j) held[j] = false;
     if (ok) {
-        unsigned long long prev[NL];
+        unsigned int prev[NL];
 #pragma unroll
         for (int j = 0; j < NL; ++j)
             if (tx.sfirst & (1u << j))
-                prev[j] = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], kLockFinal | lk_make(me, lk_ver(sl[j])));
+                prev[j] = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], stripe_lock(me));
 #pragma unroll
         for (int j = 0; j < NL; ++j) held[j] = (tx.sfirst & (1u << j)) && prev[j] == sl[j];
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
             if (!(tx.sfirst & (1u << j)) || held[j] || !ok) continue;
-            unsigned long long c = prev[j];
+            unsigned int c = prev[j];
             while (c != sl[j]) {  // lost the race: wait for a LOWER-priority holder, else abort
-                if (lk_ver(c) != lk_ver(sl[j]) || !(c & kLockFinal) || lk_owner(c) < me) {
-                    if ((c & kLockFinal) && lk_ver(c) == lk_ver(sl[j])) {
+                if (!(c & kStripeFinal) || stripe_owner(c) < me) {  // a new version, or a higher priority holds it
+                    if (c & kStripeFinal) {
                         tx.block_loc = tx.sidx[j];
                         tx.block_lk = c;
                     }
@@ -415,7 +425,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
                     break;
                 }
                 c = ld_relaxed(&v.stripes[tx.sidx[j]]);
-                if (c == sl[j]) c = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], kLockFinal | lk_make(me, lk_ver(sl[j])));
+                if (c == sl[j]) c = atomicCAS(&v.stripes[tx.sidx[j]], sl[j], stripe_lock(me));
             }
             held[j] = c == sl[j];
         }
@@ -446,7 +456,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
     }
     // ---- P4: validate the read-only stripes this transaction does not hold
     if ((KO & (KO_SKIP_VALIDATE | KO_STRIPE_2PL)) == 0 && ok) {
-        unsigned long long cur[NR];
+        unsigned int cur[NR];
         bool check[NR];
 #pragma unroll
         for (int k = NW; k < NR; ++k) {
@@ -459,11 +469,13 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
 #pragma unroll
         for (int k = NW; k < NR; ++k) {
             if (!check[k]) continue;
-            unsigned long long c = cur[k];
+            unsigned int c = cur[k];
             while (ok) {
-                if (lk_ver(c) != lk_ver(sl[k])) ok = false;                   // committed since P0
-                else if (!(c & kLockFinal)) break;                            // unclaimed: valid
-                else if (lk_owner(c) < me) {                                  // higher priority holds it
+                if (!(c & kStripeFinal)) {                                    // unlocked: valid iff unchanged
+                    ok = c == sl[k];
+                    break;
+                }
+                if (stripe_owner(c) < me) {                                   // higher priority holds it
                     ok = false;
                     tx.block_loc = tx.sidx[k];
                     tx.block_lk = c;
@@ -484,6 +496,7 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
     // ---- P5: write back the distinct written words, then release the stripes
     compute(tx);
     const unsigned long long ver = lk_commit(t);
+    const unsigned int sver = (unsigned int)ver;  // 31-bit commit version, bit 31 clear
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
         if (!(tx.first & (1u << j))) continue;
@@ -493,10 +506,12 @@ __device__ __forceinline__ bool striped_attempt(StaticTx<NR, NW>& tx, bool activ
             if (tx.loc[q] == tx.loc[j]) val = tx.wval[q];  // the last write to a word wins
         st_pair(&v.cells[tx.loc[j]], val, ver);
     }
-    if constexpr ((KO & KO_NO_FENCE) == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // cell stores before the releases
+    // release fence (MEMBAR without the L1 invalidate of fence.acq_rel): the cell
+    // stores are performed before the stripe releases
+    if constexpr ((KO & KO_NO_FENCE) == 0) asm volatile("fence.release.gpu;" ::: "memory");
 #pragma unroll
     for (int j = 0; j < NL; ++j)  // written stripes publish the commit version, read-only ones keep theirs
-        if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], j < NW ? ver : sl[j]);
+        if (held[j]) st_relaxed(&v.stripes[tx.sidx[j]], j < NW ? sver : sl[j]);
     // bitmap bits after the releases, so the fence waits for the two cell
     // stores only; fire-and-forget REDs (explicit PTX: after a fence the
     // compiler emits returning ATOMs for atomicOr)

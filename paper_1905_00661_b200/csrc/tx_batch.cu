@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
         // so the other lanes of the warp keep committing meanwhile.
         bool blocked = false;
         if (i < n && loaded && tx.block_lk) {
-            blocked = ld_relaxed(lock_word<KO>(v, tx.block_loc)) == tx.block_lk;
+            blocked = lock_value<KO>(v, tx.block_loc) == tx.block_lk;
             // bounded: the same lock word can come back (a holder that aborted and
             // re-locked with the same priority and version), so after 256 polls the
             // lane simply tries again
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kTxThreads, MINB) bank_batch_kernel(ShardView 
             // it, so the lane sits out at once)
             if ((KO & KO_STRIPES) == 0 && tx.block_lk && attempts < 4) {
                 uint32_t ns = 32;
-                for (int p = 0; p < 16 && ld_relaxed(lock_word<KO>(v, tx.block_loc)) == tx.block_lk; ++p) {
+                for (int p = 0; p < 16 && lock_value<KO>(v, tx.block_loc) == tx.block_lk; ++p) {
                     __nanosleep(ns);
                     ns = ns < 512 ? 2 * ns : ns;
                 }
