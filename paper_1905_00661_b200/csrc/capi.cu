@@ -156,6 +156,7 @@ struct hetm_dev {
     DeltaScratch ds{};                   // delta claim bitmap / unique words / bucket counts (cells.cu)
     uint64_t* h_nrec = nullptr;          // pinned: record count of the last staged delta
     cudaEvent_t ev_nrec = nullptr;       // ... landed in h_nrec
+    cudaEvent_t ev_pick = nullptr;       // merge_stage: the pick/claim pass is done (s_merge)
     // hetm_dev_merge_stage: the round's delta staged in HBM + devShadow refreshed
     // (the device half of mergeCommit), not yet shipped to the host
     struct {
@@ -920,13 +921,14 @@ int hetm_dev_close(hetm_dev* d) {
         cudaFreeHost(d->h_hot);
     }
     for (cudaEvent_t e : d->kp_ev) cudaEventDestroy(e);
-    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.uniq_val, (void*)d->ds.n_uniq, (void*)d->ds.bucket_cnt, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
+    for (void* p : {(void*)d->d_recv, (void*)d->d_recv_counts, (void*)d->d_peer_ptrs, (void*)d->d_peer_totals, (void*)d->d_res, (void*)d->d_wlog, (void*)d->d_delta[0].loc, (void*)d->d_delta[0].val, (void*)d->d_delta[1].loc, (void*)d->d_delta[1].val, (void*)d->ds.claim, (void*)d->ds.uniq, (void*)d->ds.uniq_val, (void*)d->ds.n_uniq, (void*)d->d_cells, (void*)d->d_shadow, (void*)d->d_stage, (void*)d->d_rs, (void*)d->d_ws,
                     (void*)d->d_chunk, (void*)d->d_ctr, (void*)d->d_pop, (void*)d->d_restore, (void*)d->d_arena, d->d_in,
                     (void*)d->d_tk, d->d_route, d->d_flush, (void*)d->d_trace, (void*)d->d_rs_zero, d->d_sched, (void*)d->d_est_in, (void*)d->d_stripes})
         if (p) cudaFree(p);
     if (d->h_ctr) cudaFreeHost(d->h_ctr);
     if (d->h_nrec) cudaFreeHost(d->h_nrec);
     if (d->ev_nrec) cudaEventDestroy(d->ev_nrec);
+    if (d->ev_pick) cudaEventDestroy(d->ev_pick);
     if (d->h_first) cudaFreeHost(d->h_first);
     for (auto& v : d->tpairs)
         for (auto& pr : v) {
@@ -1492,11 +1494,15 @@ int ensure_delta(hetm_dev* d, uint64_t n_slots) {
         const uint64_t words = (d->W + 63) / 64;
         if (int rc = dev_alloc(d, (void**)&d->ds.claim, words * 8)) return rc;
         CK(d, cudaMemset(d->ds.claim, 0, words * 8));
-        if (int rc = dev_alloc(d, (void**)&d->ds.n_uniq, 16)) return rc;  // records, slots (pick pass)
-        if (int rc = dev_alloc(d, (void**)&d->ds.bucket_cnt, 2 * kDeltaBuckets * sizeof(uint32_t))) return rc;
+        // records, slots (pick pass), then the bucket counts/cursors: one allocation, one memset per stage
+        constexpr size_t kCtrPad = 256, kBuckets = 2 * kDeltaBuckets * sizeof(uint32_t);
+        if (int rc = dev_alloc(d, (void**)&d->ds.n_uniq, kCtrPad + kBuckets)) return rc;
+        d->ds.bucket_cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(d->ds.n_uniq) + kCtrPad);
+        d->ds.counters_bytes = kCtrPad + kBuckets;
         if (cudaHostAlloc((void**)&d->h_nrec, 64, cudaHostAllocPortable) != cudaSuccess)
             return fail(d, cudaGetLastError(), "cudaHostAlloc(record count)");
         CK(d, cudaEventCreateWithFlags(&d->ev_nrec, cudaEventDisableTiming));
+        CK(d, cudaEventCreateWithFlags(&d->ev_pick, cudaEventDisableTiming));
     }
     if (n_slots <= d->delta_cap) return HETM_OK;
     if (d->pool) d->pool->wait();  // nothing may still read the old buffers
@@ -1921,8 +1927,12 @@ int hetm_dev_merge_stage(hetm_dev* d) {
                                                d->s_merge, d->d_ctr, true)
                            : launch_delta_claim(d->d_wlog, d->wlog_slots, d->W, d->ds, d->geom, d->s_merge, d->d_ctr);
     if (e != cudaSuccess) return fail(d, e, "delta_claim(stage)");
-    CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_merge));
-    CK(d, cudaEventRecord(d->ev_nrec, d->s_merge));
+    // the record count goes to the host on a side stream, so the copy does not
+    // sit between the pick and the emit on s_merge
+    CK(d, cudaEventRecord(d->ev_pick, d->s_merge));
+    CK(d, cudaStreamWaitEvent(d->s_zc, d->ev_pick, 0));
+    CK(d, cudaMemcpyAsync(d->h_nrec, d->ds.n_uniq, 8, cudaMemcpyDeviceToHost, d->s_zc));
+    CK(d, cudaEventRecord(d->ev_nrec, d->s_zc));
     // (running the emit beside the next round's batch was measured slower: its
     // random shadow stores and the batch's random accesses share the DRAM)
     e = launch_delta_emit(d->wlog_slots, d->W, d->ds, d->d_cells, d->d_delta[buf], shadow_inc, d->geom, d->s_merge,

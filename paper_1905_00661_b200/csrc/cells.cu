@@ -284,10 +284,17 @@ uint32_t delta_bucket_shift(uint64_t size_words) {
     return b > kDeltaBucketBits ? b - kDeltaBucketBits : 0;
 }
 
+// n_uniq[0..1] and the bucket counts/cursors: one memset when contiguous.
+static cudaError_t clear_stage_counters(const DeltaScratch& ds, cudaStream_t s) {
+    if (ds.counters_bytes) return cudaMemsetAsync(ds.n_uniq, 0, ds.counters_bytes, s);
+    cudaError_t e = cudaMemsetAsync(ds.n_uniq, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ds.bucket_cnt, 0, 2 * kDeltaBuckets * sizeof(uint32_t), s);
+    return e;
+}
+
 cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_words, const DeltaScratch& ds,
                                const LaunchGeom& g, cudaStream_t s, const DevCounters* gate) {
-    cudaError_t e = cudaMemsetAsync(ds.n_uniq, 0, sizeof(unsigned long long), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ds.bucket_cnt, 0, 2 * kDeltaBuckets * sizeof(uint32_t), s);
+    cudaError_t e = clear_stage_counters(ds, s);
     if (e != cudaSuccess || n == 0) return e;
     uint64_t want = (n + kClaimThreads - 1) / kClaimThreads;
     const uint64_t cap = (uint64_t)g.sm_count * 8;
@@ -299,8 +306,7 @@ cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_w
 cudaError_t launch_delta_pick(const uint32_t* wlog, uint64_t n, uint64_t size_words, const Cell* cells,
                               const DeltaScratch& ds, const LaunchGeom& g, cudaStream_t s, const DevCounters* ctr,
                               bool gated) {
-    cudaError_t e = cudaMemsetAsync(ds.n_uniq, 0, 2 * sizeof(unsigned long long), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ds.bucket_cnt, 0, 2 * kDeltaBuckets * sizeof(uint32_t), s);
+    cudaError_t e = clear_stage_counters(ds, s);
     if (e != cudaSuccess || n == 0) return e;
     uint64_t want = (n + kClaimThreads - 1) / kClaimThreads;
     const uint64_t cap = (uint64_t)g.sm_count * 8;

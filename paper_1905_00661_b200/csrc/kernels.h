@@ -107,6 +107,9 @@ struct DeltaScratch {
     uint64_t* uniq_val;             // per-slot values (pick pass only)
     unsigned long long* n_uniq;     // [0] record count, [1] slot count (pick pass)
     uint32_t* bucket_cnt;           // kDeltaBuckets counts, then kDeltaBuckets cursors
+    // bytes from n_uniq through the end of bucket_cnt when both live in one
+    // allocation (one memset clears the stage's counters), else 0
+    size_t counters_bytes = 0;
 };
 uint32_t delta_bucket_shift(uint64_t size_words);
 cudaError_t launch_delta_claim(const uint32_t* wlog, uint64_t n, uint64_t size_words, const DeltaScratch& ds,
