@@ -527,10 +527,8 @@ int enqueue_batch(hetm_dev* d, int kernel_id, const void* d_inputs, uint64_t n, 
     if (kernel_id == HETM_KERNEL_CACHE) d->round_versioned = false;  // set-granular locks: claim the words
     CK(d, cudaStreamWaitEvent(s, d->ev_round, 0));
     CK(d, cudaStreamWaitEvent(s, d->ev_shadow, 0));  // shadow refresh reads devReplica
-    if (reset_counters) {
-        CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 3 * sizeof(unsigned long long), s));
-        CK(d, cudaMemsetAsync(&d->d_ctr->retried, 0, sizeof(unsigned long long), s));
-    }
+    if (reset_counters)  // committed, aborts, livelocked, retried: adjacent, one memset
+        CK(d, cudaMemsetAsync(&d->d_ctr->committed, 0, 4 * sizeof(unsigned long long), s));
     cudaError_t e = cudaSuccess;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (d->timing) {

@@ -45,6 +45,7 @@ struct DevCounters {
     unsigned long long committed;   // last batch
     unsigned long long aborts;      // last batch: aborted attempts
     unsigned long long livelocked;  // last batch
+    unsigned long long retried;     // last batch: transactions committed after >= 2 aborted attempts
     unsigned long long round_max_ts;// max log ts seen this round
     unsigned int conflict;          // round conflictFlag
     unsigned int nonmonotone;       // a log ts <= ts_floor was seen
@@ -56,7 +57,6 @@ struct DevCounters {
     unsigned long long wlog_base;    // first commit ticket of the round (write-set log origin)
     unsigned long long wlog_overflow;// a committed write set did not fit the write-set log
     unsigned long long apply_dups;   // apply: exchange put-backs so far (monotone; the host judges deltas)
-    unsigned long long retried;      // last batch: transactions committed after >= 2 aborted attempts
     unsigned long long pad[18];      // diagnostics (phase clocks / ticket counts)
 };
 
