@@ -1129,9 +1129,21 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
         if (feedback) --d->auto_scan_left;
         hot = feedback || bank_batch_hot(static_cast<const hetm_bank_tx*>(inputs), n_tx);
     }
-    for (uint64_t k = 0; k < P; ++k) {
-        const uint64_t lo = n_tx * k / P, m = n_tx * (k + 1) / P - lo;
-        if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[k], 0));
+    // Kernel launches over the pieces: one per piece for the optimistic
+    // kernels; the SCAN schedules pay fixed costs per launch (sort passes,
+    // graph), so their pieces are grouped into two launches — the second half's
+    // H2D still streams under the first half's kernels (zipf-0.5 bank batch:
+    // 8 launches ~0.65 ms of kernel time, one ~0.31; profiles/r02al_*)
+    const bool serial = (d->cfg.flags & HETM_CFG_DETERMINISTIC) != 0;
+    const bool scan_path =
+        (kernel_id == HETM_KERNEL_BANK && (serial || d->schedule == HETM_SCHED_SCAN || (auto_bank && hot))) ||
+        (kernel_id == HETM_KERNEL_CACHE &&
+         (serial || d->schedule == HETM_SCHED_SCAN || (d->schedule == HETM_SCHED_AUTO && n_tx / P >= kCacheScanMin)));
+    const uint64_t G = scan_path ? std::min<uint64_t>(P, 2) : P;
+    for (uint64_t k = 0; k < G; ++k) {
+        const uint64_t p0 = P * k / G, p1 = P * (k + 1) / G;  // pieces [p0, p1) of this launch
+        const uint64_t lo = n_tx * p0 / P, m = n_tx * p1 / P - lo;
+        if (m) CK(d, cudaStreamWaitEvent(s, d->in_ev[p1 - 1], 0));  // s_in lands the pieces in order
         CK(d, cudaEventRecord(d->kp_ev[2 * k], s));
         if ((rc = enqueue_batch(d, kernel_id, in_d + lo * rec_bytes, m, d->d_tk + lo,
                                 results_out ? d->d_res + lo : nullptr, s, k == 0,
@@ -1157,8 +1169,8 @@ int hetm_dev_execute_batch_ex(hetm_dev* d, int kernel_id, const void* inputs, ui
     CK(d, cudaMemcpyAsync(d->h_ctr, d->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(d, cudaStreamSynchronize(s));
     CK(d, cudaStreamSynchronize(d->s_out));
-    float ms = 0.f;  // kernel time only: the sum over pieces
-    for (uint64_t k = 0; k < P; ++k) {
+    float ms = 0.f;  // kernel time only: the sum over the launches
+    for (uint64_t k = 0; k < G; ++k) {
         float mk = 0.f;
         cudaEventElapsedTime(&mk, d->kp_ev[2 * k], d->kp_ev[2 * k + 1]);
         ms += mk;
