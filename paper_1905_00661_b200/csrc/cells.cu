@@ -159,9 +159,11 @@ __global__ void __launch_bounds__(kClaimThreads) delta_pick_kernel(const uint32_
 // record stores land as contiguous runs instead of one scattered store per
 // record.  The same value refreshes devShadow; after a claim pass the claim
 // words are cleared for the next stage.
-constexpr int kEmitPer = 16;                                   // records per thread per tile
-constexpr uint64_t kEmitTile = (uint64_t)kClaimThreads * kEmitPer;
+// records per thread per tile: 8 (2048-record tiles, 1024 CTAs per 2^21
+// slots) beat 16 by ~10 us per cfg2 round (profiles/r02am_emit_sweep.txt)
+constexpr int kEmitPer = 8;
 static_assert(kDeltaBuckets == kClaimThreads, "one bucket per thread in the emit scans");
+template <int PER>
 __global__ void __launch_bounds__(kClaimThreads) delta_emit_kernel(const uint32_t* __restrict__ uniq,
                                                                    const unsigned long long* n_in,
                                                                    const uint32_t* __restrict__ bucket_cnt,
@@ -190,25 +192,25 @@ __global__ void __launch_bounds__(kClaimThreads) delta_emit_kernel(const uint32_
         first[t] = off + x - c;
     }
     const uint64_t n = *n_in;  // unique words (claim pass) or slots (pick pass: ~0u = not picked)
-    for (uint64_t t0 = (uint64_t)blockIdx.x * kEmitTile; t0 < n; t0 += (uint64_t)gridDim.x * kEmitTile) {
+    for (uint64_t t0 = (uint64_t)blockIdx.x * ((uint64_t)kClaimThreads * PER); t0 < n; t0 += (uint64_t)gridDim.x * ((uint64_t)kClaimThreads * PER)) {
         cnt[t] = 0;
         __syncthreads();
-        uint32_t loc[kEmitPer], r[kEmitPer];
-        uint64_t val[kEmitPer];
+        uint32_t loc[PER], r[PER];
+        uint64_t val[PER];
 #pragma unroll
-        for (int k = 0; k < kEmitPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             const uint64_t j = t0 + (uint64_t)k * kClaimThreads + t;
             loc[k] = j < n ? uniq[j] : ~0u;
             val[k] = loc[k] != ~0u ? (uniq_val ? uniq_val[j] : cells[loc[k]].value) : 0;  // pick: read already
         }
 #pragma unroll
-        for (int k = 0; k < kEmitPer; ++k)
+        for (int k = 0; k < PER; ++k)
             if (loc[k] != ~0u) r[k] = atomicAdd(&cnt[loc[k] >> bshift], 1u);
         __syncthreads();
         if (cnt[t]) run[t] = first[t] + atomicAdd(&cursor[t], cnt[t]);
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kEmitPer; ++k) {
+        for (int k = 0; k < PER; ++k) {
             if (loc[k] == ~0u) continue;
             const uint32_t pos = run[loc[k] >> bshift] + r[k];
             out.loc[pos] = loc[k];
@@ -319,11 +321,31 @@ cudaError_t launch_delta_pick(const uint32_t* wlog, uint64_t n, uint64_t size_wo
 cudaError_t launch_delta_emit(uint64_t max_records, uint64_t size_words, const DeltaScratch& ds, const Cell* cells,
                               DeltaBuf out, uint64_t* shadow, const LaunchGeom& g, cudaStream_t s, bool picked) {
     if (max_records == 0) return cudaSuccess;
-    uint64_t want = (max_records + kEmitTile - 1) / kEmitTile;
-    const uint64_t cap = (uint64_t)g.sm_count * 4;
-    delta_emit_kernel<<<(unsigned)(want < cap ? want : cap), kClaimThreads, 0, s>>>(
-        ds.uniq, picked ? ds.n_uniq + 1 : ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets,
-        delta_bucket_shift(size_words), cells, picked ? ds.uniq_val : nullptr, out, shadow, ds.claim);
+    static const int per = [] {  // tuning experiments: HETM_EMIT_PER (4, 8 or 16 records per thread per tile)
+        const char* e = std::getenv("HETM_EMIT_PER");
+        const int v = e ? std::atoi(e) : kEmitPer;
+        return v == 4 || v == 16 ? v : kEmitPer;
+    }();
+    static const uint64_t ctas = [] {  // tuning experiments: HETM_EMIT_CTAS resident CTAs per SM
+        const char* e = std::getenv("HETM_EMIT_CTAS");
+        return e ? (uint64_t)std::atoi(e) : 4ull;
+    }();
+    const uint64_t tile = (uint64_t)kClaimThreads * per;
+    uint64_t want = (max_records + tile - 1) / tile;
+    const uint64_t cap = (uint64_t)g.sm_count * (ctas ? ctas : 4);
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    if (per == 4)
+        delta_emit_kernel<4><<<grid, kClaimThreads, 0, s>>>(
+            ds.uniq, picked ? ds.n_uniq + 1 : ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets,
+            delta_bucket_shift(size_words), cells, picked ? ds.uniq_val : nullptr, out, shadow, ds.claim);
+    else if (per == 16)
+        delta_emit_kernel<16><<<grid, kClaimThreads, 0, s>>>(
+            ds.uniq, picked ? ds.n_uniq + 1 : ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets,
+            delta_bucket_shift(size_words), cells, picked ? ds.uniq_val : nullptr, out, shadow, ds.claim);
+    else
+        delta_emit_kernel<kEmitPer><<<grid, kClaimThreads, 0, s>>>(
+            ds.uniq, picked ? ds.n_uniq + 1 : ds.n_uniq, ds.bucket_cnt, ds.bucket_cnt + kDeltaBuckets,
+            delta_bucket_shift(size_words), cells, picked ? ds.uniq_val : nullptr, out, shadow, ds.claim);
     return cudaGetLastError();
 }
 
