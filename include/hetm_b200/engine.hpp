@@ -68,6 +68,10 @@ struct EngineConfig {
     bool keep_round_log = false;        // keep a copy of the last round's host log (checkers)
     bool early_merge = true;            // stage + speculatively apply the delta merge after execution
                                         // (hetm_dev_merge_prepare; a no-op without HETM_CFG_MERGE_DELTA)
+    bool pipeline_merge = false;        // a committed round returns before its merge has landed in the
+                                        // host replica: the next round's device batches start under it
+                                        // and its host workers wait for it (drain() before
+                                        // reading the host replica outside a round)
     uint32_t fault = 0;                 // ENGINE_FAULT_* (checker mutation suite only)
 };
 
@@ -213,6 +217,15 @@ public:
     ~BasicEngine() {
         for (auto& b : pool_) hetm_host_free(b.ptr);
     }
+    /// pipeline_merge: wait until the last committed round's merge has landed in
+    /// the host replica (before reading it outside a round).
+    void drain() {
+        if (merge_pending_) {
+            check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
+            merge_pending_ = false;
+        }
+    }
+
     /// Pinned staging buffers allocated so far (chunks recycle them once delivered).
     std::size_t stagingBuffers() const { return pool_.size(); }
 
@@ -261,6 +274,11 @@ public:
         const bool favor_device = cfg_.policy == Policy::FavorDevice;
         // starvation guard (FavorHost): a read-only host round after K device aborts
         rep.updates_allowed = favor_device || dev_aborts_ < cfg_.starvation_k;
+        // a pipelined merge of the previous round lands before anything on the host reads the replica
+        // (the FavorDevice snapshot, the host workers); the device batches below do not wait for it
+        const bool merge_pending = merge_pending_;
+        merge_pending_ = false;
+        if (favor_device && merge_pending) check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
         // FavorDevice: explicit host snapshot at round start
         if (favor_device) std::memcpy(snapshot_.data(), host_, snapshot_.size() * sizeof(uint64_t));
         const int stream_mode = (favor_device || cfg_.early_validation) ? HETM_VALIDATE_ONLY : HETM_APPLY;
@@ -290,6 +308,7 @@ public:
         });
         std::vector<std::thread> hosts;
         std::vector<uint64_t> commits(log_threads(log_), 0);
+        if (merge_pending && !favor_device) check_rc(hetm_dev_merge_wait(dev_), "merge_wait");  // GPU already running
         for (int t = 0; t < log_threads(log_); ++t)
             hosts.emplace_back([&, t] { commits[t] = worker(t, ctx); });
         while (!gpu_done.load(std::memory_order_acquire)) {
@@ -357,7 +376,8 @@ public:
             hetm_merge_stats ms{};
             check_rc(hetm_dev_merge_commit(dev_, host_, &ms), "merge_commit");
             rep.bytes_merge = ms.bytes_d2h + ms.bytes_h2d + ms.bytes_d2d;
-            check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
+            if (cfg_.pipeline_merge) merge_pending_ = true;  // lands under the next round's device batches
+            else check_rc(hetm_dev_merge_wait(dev_), "merge_wait");
             dev_aborts_ = 0;
         } else if (!favor_device) {
             rep.outcome = Outcome::DeviceAborted;
@@ -506,6 +526,7 @@ private:
     std::vector<uint64_t> snapshot_;  // FavorDevice round-start host snapshot
     uint64_t round_id_ = 0;
     uint32_t dev_aborts_ = 0;         // consecutiveDeviceAborts
+    bool merge_pending_ = false;      // pipeline_merge: the last committed round's merge has not landed yet
     Trace* trace_ = nullptr;
     std::vector<uint64_t> trace_rec_;  // per-batch device trace records
     uint64_t trace_batches_ = 0;

@@ -14,6 +14,8 @@
 // execution phase).  Partitioned accesses: no conflicts, every round commits.
 //
 //   hetm_live_round [rounds] [log2 words] [batch] [host threads] [cutoff chunks] [ev period] [chunk entries]
+//                   [pipeline merge 1|0: a committed round's merge lands under the next round's device
+//                    batches, EngineConfig::pipeline_merge; default 1]
 //
 // Prints one JSON line: committed host + device transactions per second of
 // wall clock over the timed rounds (the first round is warm-up).
@@ -44,6 +46,7 @@ int main(int argc, char** argv) {
     const uint32_t cutoff = argc > 5 ? (uint32_t)std::atoi(argv[5]) : 4;
     const uint32_t ev_period = argc > 6 ? (uint32_t)std::atoi(argv[6]) : 8;
     const uint64_t chunk = argc > 7 ? std::strtoull(argv[7], nullptr, 10) : (1u << 16);
+    const bool pipeline = argc > 8 ? std::atoi(argv[8]) != 0 : true;  // merge lands under the next batch
     if (T <= 0) {  // every core but the controller's and the GPU-controller thread's
         const int hw = (int)std::thread::hardware_concurrency();
         T = hw > 3 ? hw - 2 : 1;
@@ -85,6 +88,7 @@ int main(int argc, char** argv) {
     EngineConfig ec;
     ec.chunk_entries = chunk;
     ec.cutoff_chunks = cutoff;
+    ec.pipeline_merge = pipeline;
     ec.ev_period = ev_period;
     Engine eng(dev, stm, log, host, ec);
 
@@ -132,6 +136,7 @@ int main(int argc, char** argv) {
         merge_ms += rep.merge_ms;
         blocked_ms += rep.host_blocked_ms;
     }
+    eng.drain();  // the last round's merge lands inside the timed region
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     uint64_t sum = 0;
     for (uint64_t i = 0; i < W; ++i) sum += host[i];
@@ -142,14 +147,14 @@ int main(int argc, char** argv) {
                 "\"host_commits\": %llu, \"dev_commits\": %llu, \"log_entries_per_round\": %.1f, "
                 "\"chunks_per_round\": %.2f, \"chunks_after_exec_per_round\": %.2f, \"exec_ms\": %.4f, "
                 "\"validate_ms\": %.4f, \"merge_ms\": %.4f, \"host_blocked_ms\": %.4f, "
-                "\"staging_buffers\": %zu, \"host_aborts\": %llu, \"bank_sum_ok\": %s}\n",
+                "\"staging_buffers\": %zu, \"host_aborts\": %llu, \"pipeline_merge\": %s, \"bank_sum_ok\": %s}\n",
                 rounds, (unsigned long long)commits, T, (unsigned long long)W, (unsigned long long)B, cutoff,
                 ev_period, (unsigned long long)chunk, wall, (double)(host_commits + dev_commits) / wall,
                 (double)dev_commits / wall, (double)host_commits / wall, (unsigned long long)host_commits,
                 (unsigned long long)dev_commits, (double)log_entries / rounds, (double)chunks / rounds,
                 (double)cut_chunks / rounds, exec_ms / rounds, val_ms / rounds, merge_ms / rounds,
                 blocked_ms / rounds, eng.stagingBuffers(), (unsigned long long)stm.aborts(),
-                sum_ok ? "true" : "false");
+                pipeline ? "true" : "false", sum_ok ? "true" : "false");
     for (auto* p : txs) hetm_host_free(p);
     hetm_host_free(tickets);
     hetm_host_free(host);
