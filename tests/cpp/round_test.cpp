@@ -12,6 +12,7 @@
 //   round_test [rounds] [log2 words] [batch] [host threads] [conflict every k] [host|device] [starvation k]
 //              [batches per round] [early validation 1|0] [cutoff chunks] [bus delay us/unit]
 //              [host tx per thread per round (0: until the cut-off)] [early-validation period k]
+//              [pipelined merge 1|0]
 // policy host (FavorHost, default) or device (FavorDevice: a conflicting round
 // is HostAborted, S' = device batch replay on S, host effects discarded).
 // conflict every k = 1 makes every round conflict (starvation-guard test).
@@ -54,6 +55,7 @@ int main(int argc, char** argv) {
     const double bus_delay = argc > 11 ? std::atof(argv[11]) : 0.0;
     const uint64_t per_thread_arg = argc > 12 ? std::strtoull(argv[12], nullptr, 10) : 1500;
     const uint32_t ev_period = argc > 13 ? (uint32_t)std::atoi(argv[13]) : 8;
+    const bool pipeline = argc > 14 && std::atoi(argv[14]) != 0;  // EngineConfig::pipeline_merge (+ drain() per check)
     const uint64_t W = 1ull << log2w, half = W / 2;
 
     hetm_dev_config cfg;
@@ -88,6 +90,7 @@ int main(int argc, char** argv) {
     ec.cutoff_chunks = cutoff;
     ec.bus_real_delay_us_per_unit = bus_delay;
     ec.ev_period = ev_period;
+    ec.pipeline_merge = pipeline;
     Engine eng(dev, stm, log, host, ec);
     double blocked_ms = 0;
     uint64_t cutoff_chunks = 0, log_total = 0;
@@ -135,6 +138,7 @@ int main(int argc, char** argv) {
             b = Engine::Batch{txs.data() + (uint64_t)k * B, B, tickets.data() + (uint64_t)k * B};
             return true;
         }, worker);
+        eng.drain();  // pipeline_merge: the round's merge lands before the host replica is read below
         batches_total += rep.dev_batches;
         blocked_ms += rep.host_blocked_ms;
         cutoff_chunks += rep.cutoff_chunks;

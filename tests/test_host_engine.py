@@ -35,7 +35,10 @@ def test_round_controller_refuses_without_device(hetm):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("args", [["6", "20", "16384", "4", "3"], ["4", "22", "65536", "8", "2"],
-                                  ["6", "20", "16384", "4", "2", "device"]])
+                                  ["6", "20", "16384", "4", "2", "device"],
+                                  # EngineConfig::pipeline_merge (the merge lands under the next round)
+                                  ["6", "20", "16384", "4", "3", "host", "3", "1", "1", "4", "0", "1500", "8", "1"],
+                                  ["6", "20", "16384", "4", "2", "device", "3", "1", "1", "4", "0", "1500", "8", "1"]])
 def test_live_rounds_match_oracle(args):
     """Host workers commit bank transfers through the host TM while the GPU
     runs a bank batch; the engine streams the log with early validation and
