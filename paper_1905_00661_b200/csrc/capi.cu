@@ -13,6 +13,8 @@
 //   s_in     input pieces H2D of a host-buffer batch, under the kernel on the
 //            previous piece; s_out its tickets / results D2H
 //   s_est    the AUTO schedule's hot-spot estimate of device-pointer batches
+//   s_win    merge_stage's devShadow patch with the host-log winners, beside
+//            the pick/emit on s_merge (joined back before ev_shadow)
 // plus the worker pool that scatters the merge delta into the host replica as
 // its pieces land.  Events carry every cross-stream dependency; nothing blocks
 // the host except the explicitly synchronous calls (verdict, merge_wait,
@@ -235,6 +237,11 @@ struct hetm_dev {
     SchedGraph sched_graph;                 // its captured launch sequence
     PreparedMerge prep;                     // hetm_dev_merge_prepare state
     cudaEvent_t ev_stage = nullptr;         // delta records gathered (s_merge)
+    // merge_stage: the devShadow patch with the host-log winners runs on s_win
+    // beside the pick/emit on s_merge (disjoint words in a committed round)
+    cudaStream_t s_win = nullptr;
+    cudaEvent_t ev_win_fork = nullptr, ev_win = nullptr;
+    bool win_side = true;
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     unsigned int* d_stripes = nullptr;        // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES)
     uint32_t stripe_shift = 64;
@@ -643,13 +650,13 @@ RoundLogs round_logs(hetm_dev* d) {
 
 // devShadow patch with the winners of the round's host log (the words the
 // validation applied), on s_merge; gate: skipped on the device on a conflict.
-cudaError_t patch_shadow(hetm_dev* d, const DevCounters* gate = nullptr) {
+cudaError_t patch_shadow(hetm_dev* d, const DevCounters* gate = nullptr, cudaStream_t s = nullptr) {
     const RoundLogs l = round_logs(d);
-    cudaError_t e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, l.flat, l.n, d->geom, d->s_merge,
-                                        gate);
+    if (!s) s = d->s_merge;
+    cudaError_t e = launch_winner_apply(d->d_cells, d->d_shadow, d->base, d->W, l.flat, l.n, d->geom, s, gate);
     for (uint32_t k = 0; k < l.n_regions_sets && e == cudaSuccess; ++k)
         e = launch_winner_regions(d->d_cells, d->d_shadow, d->base, d->W, l.region[k].base, l.region[k].counts,
-                                  l.region[k].n_regions, l.region[k].cap, d->geom, d->s_merge, gate);
+                                  l.region[k].n_regions, l.region[k].cap, d->geom, s, gate);
     return e;
 }
 
@@ -842,6 +849,13 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
         d->stripe_shift = 64 - bits;
         CK(d, cudaMemset(d->d_stripes, 0, 4ull << bits));  // unlocked, version 0
     }
+    {
+        static const bool win_side = [] {  // A/B experiments: HETM_WIN_SIDE=0 runs the winner patch in line
+            const char* e = std::getenv("HETM_WIN_SIDE");
+            return !e || std::atoi(e) != 0;
+        }();
+        d->win_side = win_side;
+    }
     if ((rc = dev_alloc(d, (void**)&d->d_pop, 4 * sizeof(unsigned long long)))) return bail(rc);
     if ((rc = dev_alloc(d, (void**)&d->d_restore, kRestoreCap * sizeof(unsigned long long)))) return bail(rc);
     d->restore_cap = kRestoreCap;
@@ -861,9 +875,9 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
     CK(d, cudaMemset(d->d_chunk, 0, d->chunk_words * 8));
     CK(d, cudaMemset(d->d_ctr, 0, sizeof(DevCounters)));
 
-    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc, &d->s_in, &d->s_out})
+    for (cudaStream_t* s : {&d->s_exec, &d->s_copy, &d->s_val, &d->s_merge, &d->s_d2h, &d->s_zc, &d->s_in, &d->s_out, &d->s_win})
         CK(d, cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc, &d->ev_stage, &d->ev_ext})
+    for (cudaEvent_t* e : {&d->ev_exec, &d->ev_copy, &d->ev_val, &d->ev_round, &d->ev_shadow, &d->ev_d2h, &d->ev_copy_zc, &d->ev_stage, &d->ev_ext, &d->ev_win_fork, &d->ev_win})
         CK(d, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CK(d, cudaEventCreate(&d->ev_t0));
     CK(d, cudaEventCreate(&d->ev_t1));
@@ -895,7 +909,7 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
 int hetm_dev_close(hetm_dev* d) {
     if (!d) return HETM_ERR_INVALID_ARG;
     cudaSetDevice(d->device);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out, d->s_win})
         if (s) cudaStreamSynchronize(s);
     if (d->prep.active) {  // never merged: leave the host replica as it was
         std::lock_guard<std::mutex> g(d->mu);
@@ -934,10 +948,10 @@ int hetm_dev_close(hetm_dev* d) {
             cudaEventDestroy(pr.second);
         }
     for (cudaEvent_t e : d->tpool) cudaEventDestroy(e);
-    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out})
+    for (cudaStream_t s : {d->s_exec, d->s_copy, d->s_val, d->s_merge, d->s_d2h, d->s_zc, d->s_in, d->s_out, d->s_win})
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : {d->ev_exec, d->ev_copy, d->ev_val, d->ev_round, d->ev_shadow, d->ev_d2h, d->ev_t0, d->ev_t1,
-                          d->ev_copy_zc, d->ev_stage, d->ev_ext})
+                          d->ev_copy_zc, d->ev_stage, d->ev_ext, d->ev_win_fork, d->ev_win})
         if (e) cudaEventDestroy(e);
     delete d;
     return HETM_OK;
@@ -1932,6 +1946,17 @@ int hetm_dev_merge_stage(hetm_dev* d) {
         t1 = d->tev();
         CK(d, cudaEventRecord(t0, d->s_merge));
     }
+    // the winner patch touches only host-log words, the pick/emit only device-
+    // written ones: in a committed round the two sets are disjoint (WS within RS,
+    // no RS/host-write intersection), and both are verdict-gated on the device
+    const bool win_side = shadow_inc && d->win_side;
+    if (win_side) {
+        CK(d, cudaEventRecord(d->ev_win_fork, d->s_merge));
+        CK(d, cudaStreamWaitEvent(d->s_win, d->ev_win_fork, 0));
+        cudaError_t ew = patch_shadow(d, d->d_ctr, d->s_win);
+        if (ew != cudaSuccess) return fail(d, ew, "winner_apply(stage)");
+        CK(d, cudaEventRecord(d->ev_win, d->s_win));
+    }
     const bool picked = d->round_versioned;
     cudaError_t e = picked ? launch_delta_pick(d->d_wlog, d->wlog_slots, d->W, d->d_cells, d->ds, d->geom,
                                                d->s_merge, d->d_ctr, true)
@@ -1949,7 +1974,8 @@ int hetm_dev_merge_stage(hetm_dev* d) {
                           picked);
     if (e != cudaSuccess) return fail(d, e, "delta_emit(stage)");
     CK(d, cudaEventRecord(d->ev_stage, d->s_merge));
-    if (shadow_inc && (e = patch_shadow(d, d->d_ctr)) != cudaSuccess) return fail(d, e, "winner_apply(stage)");
+    if (win_side) CK(d, cudaStreamWaitEvent(d->s_merge, d->ev_win, 0));
+    else if (shadow_inc && (e = patch_shadow(d, d->d_ctr)) != cudaSuccess) return fail(d, e, "winner_apply(stage)");
     if (d->timing) {
         CK(d, cudaEventRecord(t1, d->s_merge));
         d->tpairs[2].emplace_back(t0, t1);
