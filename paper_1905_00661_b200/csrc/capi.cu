@@ -13,8 +13,8 @@
 //   s_in     input pieces H2D of a host-buffer batch, under the kernel on the
 //            previous piece; s_out its tickets / results D2H
 //   s_est    the AUTO schedule's hot-spot estimate of device-pointer batches
-//   s_win    merge_stage's devShadow patch with the host-log winners, beside
-//            the pick/emit on s_merge (joined back before ev_shadow)
+//   s_win    (HETM_WIN_SIDE=1) merge_stage's devShadow patch with the host-log
+//            winners, beside the pick/emit on s_merge (joined before ev_shadow)
 // plus the worker pool that scatters the merge delta into the host replica as
 // its pieces land.  Events carry every cross-stream dependency; nothing blocks
 // the host except the explicitly synchronous calls (verdict, merge_wait,
@@ -241,7 +241,7 @@ struct hetm_dev {
     // beside the pick/emit on s_merge (disjoint words in a committed round)
     cudaStream_t s_win = nullptr;
     cudaEvent_t ev_win_fork = nullptr, ev_win = nullptr;
-    bool win_side = true;
+    bool win_side = false;
     unsigned long long* d_rs_zero = nullptr;  // all-zero RS bitmap (HETM_FAULT_SKIP_RS)
     unsigned int* d_stripes = nullptr;        // bank kernel lock-stripe table (phased_tx.cuh KO_STRIPES)
     uint32_t stripe_shift = 64;
@@ -850,9 +850,13 @@ int hetm_dev_open(const hetm_dev_config* cfg, hetm_dev** out) {
         CK(d, cudaMemset(d->d_stripes, 0, 4ull << bits));  // unlocked, version 0
     }
     {
-        static const bool win_side = [] {  // A/B experiments: HETM_WIN_SIDE=0 runs the winner patch in line
+        // Off by default: on s_win the merge stage drops 0.275 -> 0.258 ms, but the
+        // next bank batch runs ~8 us slower (the emit's dirty lines are the last
+        // ones left in L2 and drain under it), so the step gains only ~1 %
+        // (profiles/r02au_winner_side_stream_ab.txt).  HETM_WIN_SIDE=1 turns it on.
+        static const bool win_side = [] {
             const char* e = std::getenv("HETM_WIN_SIDE");
-            return !e || std::atoi(e) != 0;
+            return e && std::atoi(e) != 0;
         }();
         d->win_side = win_side;
     }
