@@ -6,6 +6,7 @@ identical configuration; --gpus N spawns N ranks.  Small step counts on the
 BASELINE configs[1] shape (GPU); the rank spawn and plan line on CPU."""
 import json
 import os
+import signal
 import subprocess
 import sys
 
@@ -18,13 +19,22 @@ SMALL = ["--e2e-steps", "3", "--cpu-seconds", "0.5", "--live-rounds", "2", "--co
 
 
 def _run(*extra, env=None, timeout=900):
+    """bench.py in its own process group: on a timeout the whole group (the
+    torchrun agent and every rank) is killed, so no rank outlives the test."""
     e = dict(os.environ)
     e.update(env or {})
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3", *extra],
-                         capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=e)
-    assert out.returncode == 0, out.stderr[-3000:]
-    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1, out.stdout[-2000:]
+    p = subprocess.Popen([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3", *extra],
+                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT, env=e,
+                         start_new_session=True)
+    try:
+        stdout, stderr = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        p.communicate()
+        raise
+    assert p.returncode == 0, stderr[-3000:]
+    lines = [ln for ln in stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, stdout[-2000:]
     return json.loads(lines[0])
 
 
