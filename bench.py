@@ -384,11 +384,20 @@ def run_ours(args):
         # pre-roll under the same load so nvidia-smi has samples spanning the timed region
         t_pre = time.time()
         j = 0
-        while not args.no_preroll and time.time() - t_pre < 0.6:
-            step(j % WU if WU else 0)
-            j += 1
-            if j % 8 == 0:
-                torch.cuda.synchronize()
+        # steps carry collectives at N>1 (verdict / delivery barrier), so every
+        # rank must run the same number: the stop decision is taken every 8
+        # steps and agreed over the ranks (a per-rank clock once left one rank
+        # in a step's collective while the other waited in the barrier below)
+        while not args.no_preroll:
+            for _ in range(8):
+                step(j % WU if WU else 0)
+                j += 1
+            torch.cuda.synchronize()
+            done = 1.0 if time.time() - t_pre >= 0.6 else 0.0
+            if dist:
+                done = max_over_ranks(dist, [done])[0]
+            if done > 0:
+                break
         torch.cuda.synchronize()
         for w in (0, 1, 2):
             dev.timing(w)
